@@ -1,0 +1,181 @@
+/*
+ * zolo_b200.h -- C ABI of the B200-native Zolotarev filter path.
+ *
+ * Drop-in boundary for the reference's FilterOperator<S> (ZoloEig,
+ * proj/include/zoloeig/filter_engine.hpp:37-165). The reference has no
+ * runtime plugin seam: its hot path is the concrete class FilterOperator<S>,
+ * constructed by value in subspace_iteration (eigensolver.hpp:172) and
+ * called at eigensolver.hpp:184. Each entry point below replaces one member
+ * or setup step of that class; the header-only C++ adapter
+ * cpp/zolo/gpu_filter_operator.hpp rebuilds the reference's surface
+ * (same names, same exceptions) on top of it.
+ *
+ * Conventions (identical to the reference, dense.hpp:53-115, sparse.hpp:31-36):
+ *   - dense blocks are column-major, leading dimension n;
+ *   - complex scalars are interleaved (re, im) doubles, i.e. std::complex<double>;
+ *   - CSR matrices carry the full (not triangular) pattern with sorted
+ *     column indices; offsets/indices are int64 (the reference's size_t);
+ *   - scalar tag: ZOLO_F64 for real symmetric pencils, ZOLO_C128 for
+ *     complex Hermitian pencils; B == NULL means B = I (SparsePencil::b_mat
+ *     empty, sparse.hpp:133-150).
+ * Every function returns a status (ZOLO_OK, ...). Host pointers are never
+ * retained after a call returns. One context drives one GPU from one host
+ * thread; calls on a context are stream-ordered on its private stream.
+ */
+#ifndef ZOLO_B200_H
+#define ZOLO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the C++ adapter maps them back onto the reference's
+ * exception types (error.hpp:25-43, gmres.hpp:45-52). */
+enum {
+  ZOLO_OK = 0,
+  ZOLO_ERR_DOMAIN = 1,        /* DomainError: bad sizes / arguments */
+  ZOLO_ERR_NUMERICAL = 2,     /* NumericalError */
+  ZOLO_ERR_FACTORIZATION = 3, /* FactorizationError{pivot_index} */
+  ZOLO_ERR_GMRES = 4,         /* GmresError{report} (report is filled) */
+  ZOLO_ERR_CUDA = 5           /* CUDA / device failure (incl. no device) */
+};
+
+enum { ZOLO_F64 = 0, ZOLO_C128 = 1 };
+
+/* Packed FilterDesign (filter_design.hpp:53-69), the boundary input that
+ * build_filter_design (filter_design.hpp:133-169) produces on the host:
+ *   [0..5]   window a, b, a_minus, a_plus, b_minus, b_plus
+ *   [6..9]   mobius gamma, alpha, beta, ell1
+ *   [10..14] m_hat, ell2, zmax, constant_term, delta0
+ *   [15..18] inner.big_m, inner.delta, outer.big_m, outer.delta
+ *   then inner_poles (2r doubles), inner_weights (2r), inner_pf (r),
+ *   outer_pf (r), inner.c (2r-1), outer.c (2r-1).          length 17 + 10 r */
+enum {
+  ZOLO_DESIGN_M_HAT = 10,
+  ZOLO_DESIGN_CONSTANT = 13,
+  ZOLO_DESIGN_DELTA0 = 14,
+  ZOLO_DESIGN_OUTER_M = 17,
+  ZOLO_DESIGN_HEAD = 19
+};
+#define ZOLO_DESIGN_LEN(r) (17 + 10 * (r))
+#define ZOLO_MAX_ORDER 16
+
+/* ShiftedSolveReport (gmres.hpp:31-43) merged over columns exactly as
+ * filter_engine.hpp:127-133 does. column_iterations is caller-owned
+ * (ncols entries) and may be NULL. */
+typedef struct {
+  int64_t iterations;            /* max Krylov dimension over columns */
+  int64_t operator_applications; /* sum over columns */
+  int32_t n_shifts;              /* 2 r */
+  int32_t all_converged;
+  double residuals[2 * ZOLO_MAX_ORDER]; /* per shift, worst column */
+  int32_t converged[2 * ZOLO_MAX_ORDER];
+  int64_t* column_iterations;
+} zolo_report;
+
+/* FactorProfile (band_factor.hpp:31-35) plus the failing pivot. */
+typedef struct {
+  int64_t bandwidth;      /* half bandwidth under the ordering */
+  int64_t stored_entries; /* complex entries stored on the device */
+  double min_pivot_ratio; /* min |pivot| / ||row||_inf */
+  int64_t pivot_index;    /* -1, or first rejected pivot (FactorizationError) */
+} zolo_factor_stats;
+
+typedef struct zolo_ctx zolo_ctx;
+
+/* --- context ---------------------------------------------------------- */
+int zolo_ctx_create(int device, zolo_ctx** out);
+int zolo_ctx_destroy(zolo_ctx* ctx);
+/* Last error message of this context (or of the last failed create when ctx is NULL). */
+const char* zolo_last_error(const zolo_ctx* ctx);
+
+/* --- setup (FilterOperator ctor, filter_engine.hpp:40-45) -------------- */
+/* Upload the Hermitian(-definite) pencil. Replaces SparsePencil<S>. */
+int zolo_pencil_upload(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
+                       const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v);
+
+/* Install the filter design (packed, see above); r = design order. The
+ * effective weights are m_hat * inner_weights (filter_engine.hpp:43-44). */
+int zolo_set_design(zolo_ctx* ctx, const double* design, int r);
+
+/* build_shifted_factors (band_factor.hpp:199-220): one ordering shared by
+ * all shifts -- perm (new -> old, n entries) or NULL for the reference's
+ * RCM ordering of the pattern of A - iB (rcm.hpp:69-115) -- then r numeric
+ * unpivoted factorizations of A - sigma_j B on the device at
+ * sigma = design.inner_poles. stats: r entries or NULL. On a rejected pivot
+ * returns ZOLO_ERR_FACTORIZATION with stats[j].pivot_index set. */
+int zolo_factorize(zolo_ctx* ctx, const int64_t* perm, zolo_factor_stats* stats);
+
+/* FilterOperator(pencil, design): upload + set_design + factorize. */
+int zolo_filter_create(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
+                       const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v,
+                       const double* design, int r, zolo_factor_stats* stats);
+
+/* --- hot path ----------------------------------------------------------- */
+/* FilterOperator::apply_g (filter_engine.hpp:56-82) on an n x ncols host
+ * block (one G application, counted once as the reference does). */
+int zolo_apply_g(zolo_ctx* ctx, const double* v, double* gv, int64_t ncols);
+
+/* FilterOperator::apply_filter (filter_engine.hpp:86-155) on an n x ncols
+ * host block: all 2r outer shifts +-i sqrt(outer.c[2j]) in one multi-shift
+ * GMRES per column (lock-step batched on the device), combined as
+ * 1/2 M_outer sum_j 1/2 a_j (x_2j + x_2j+1) + 1/2 v. Returns ZOLO_ERR_GMRES
+ * with rep filled (y still written) when some shift misses gmres_tol. */
+int zolo_apply_filter(zolo_ctx* ctx, const double* v, double* y, int64_t ncols, double gmres_tol,
+                      int64_t gmres_max, zolo_report* rep);
+
+/* Same with device-resident blocks (original ordering, leading dimension n,
+ * same element layout); no host<->device copies. */
+int zolo_apply_filter_device(zolo_ctx* ctx, const void* d_v, void* d_y, int64_t ncols, double gmres_tol,
+                             int64_t gmres_max, zolo_report* rep);
+
+/* inner_solve_count / g_application_count (filter_engine.hpp:50-51). */
+int zolo_counters(const zolo_ctx* ctx, int64_t* inner_solves, int64_t* g_applications);
+
+/* Rayleigh-Ritz projections (eigensolver.hpp:108-109): Atilde = Y^H A Y,
+ * Btilde = Y^H B Y, k x k column-major, Y an n x k host block. */
+int zolo_rr_project(zolo_ctx* ctx, const double* y, int64_t k, double* a_tilde, double* b_tilde);
+
+/* Device-side GEMM for the subspace update Q = Y * Qsmall (eigensolver.hpp:190):
+ * y n x k, q_small k x kk (host), out n x kk (host). */
+int zolo_block_update(zolo_ctx* ctx, const double* y, int64_t k, const double* q_small, int64_t kk, double* out);
+
+/* --- timing of the last device call (CUDA events on the context stream) - */
+/* ms[0] = last apply_filter device time, ms[1] = last factorize device time,
+ * ms[2] = solve-kernel time summed over the last apply_filter,
+ * ms[3] = number of solve-kernel launches in the last apply_filter. */
+int zolo_last_timings(const zolo_ctx* ctx, double* ms);
+
+/* --- host-only helpers (no GPU needed) ---------------------------------- */
+/* reorder_rcm (rcm.hpp:69-115) of a structurally symmetric pattern;
+ * perm[new] = old. bw/profile (rcm.hpp:118-147) may be NULL. */
+int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int64_t* bw, int64_t* profile);
+
+/* random_gaussian<S> (dense.hpp:181-208, raw mt19937_64 bits + Box-Muller),
+ * optionally followed by mgs_orthonormalize (dense.hpp:212-229). */
+int zolo_random_block(int scalar, int64_t n, int64_t k, uint64_t seed, int orthonormalize, double* out);
+
+/* n uniforms in [0,1) from raw mt19937_64 bits, (x >> 11) * 2^-53 -- the
+ * reference's disorder convention (hamiltonian.hpp:52); used by the
+ * synthetic config generators. */
+int zolo_uniform_stream(uint64_t seed, int64_t n, double* out);
+
+/* build_filter_design (filter_design.hpp:133-169) for the window given by its
+ * four gap endpoints (window_from_gaps, window.hpp:56-68; a_minus may be
+ * -inf, b_plus +inf) at order r; writes ZOLO_DESIGN_LEN(r) doubles. */
+int zolo_build_design(const double* gaps, int r, double* design);
+
+/* eval_g_scalar / eval_filter_scalar (filter_design.hpp:72-82) at npts points;
+ * either output may be NULL. */
+int zolo_eval_filter(const double* gaps, int r, int64_t npts, const double* x, double* g_out, double* filter_out);
+
+/* Library version / build tag. */
+const char* zolo_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ZOLO_B200_H */

@@ -1,0 +1,338 @@
+"""B200-native Zolotarev filter path (ZoloEig, arXiv 1701.08935).
+
+Python mirror of the reference's hot-path API over the C ABI in
+``include/zolo_b200.h`` (``libzolo_b200.so``, sm_100a):
+
+* :class:`FilterOperator` -- ``FilterOperator<S>`` (filter_engine.hpp:37-165):
+  ``apply_g``, ``apply_filter``, ``inner_solve_count``, ``g_application_count``.
+* exceptions with the reference's names and fields (error.hpp:25-43,
+  gmres.hpp:45-52): :class:`DomainError`, :class:`NumericalError`,
+  :class:`FactorizationError` (``pivot_index``), :class:`GmresError` (``report``).
+* :class:`ShiftedSolveReport` (gmres.hpp:31-43).
+* :func:`subspace_iteration` (eigensolver.hpp:154-217) in ``driver.py``.
+
+There is no CPU fallback: constructing an operator without a CUDA device or
+without the built extension raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libzolo_b200.so")
+
+ZOLO_OK, ZOLO_ERR_DOMAIN, ZOLO_ERR_NUMERICAL, ZOLO_ERR_FACTORIZATION, ZOLO_ERR_GMRES, ZOLO_ERR_CUDA = range(6)
+MAX_ORDER = 16
+
+
+class DomainError(ValueError):
+    """Invalid argument or out-of-domain input (error.hpp:25-29)."""
+
+
+class NumericalError(RuntimeError):
+    """Numerical breakdown inside an algorithm (error.hpp:32-35)."""
+
+
+class FactorizationError(NumericalError):
+    """Unpivoted elimination met a pivot below threshold (error.hpp:37-43)."""
+
+    def __init__(self, what: str, pivot_index: int):
+        super().__init__(what)
+        self.pivot_index = pivot_index
+
+
+class GmresError(NumericalError):
+    """Multi-shift GMRES missed the tolerance (gmres.hpp:45-52)."""
+
+    def __init__(self, what: str, report: "ShiftedSolveReport", y=None):
+        super().__init__(what)
+        self.report = report
+        self.y = y
+
+
+class CudaError(RuntimeError):
+    """Device / driver failure (no silent CPU fallback exists)."""
+
+
+@dataclass
+class ShiftedSolveReport:
+    """gmres.hpp:31-43, merged over columns as filter_engine.hpp:127-133."""
+
+    iterations: int = 0
+    residuals: List[float] = field(default_factory=list)
+    converged: List[bool] = field(default_factory=list)
+    column_iterations: List[int] = field(default_factory=list)
+    operator_applications: int = 0
+
+    def all_converged(self) -> bool:
+        return all(self.converged)
+
+
+class _Report(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int64),
+        ("operator_applications", C.c_int64),
+        ("n_shifts", C.c_int32),
+        ("all_converged", C.c_int32),
+        ("residuals", C.c_double * (2 * MAX_ORDER)),
+        ("converged", C.c_int32 * (2 * MAX_ORDER)),
+        ("column_iterations", C.POINTER(C.c_int64)),
+    ]
+
+
+class FactorStats(C.Structure):
+    """FactorProfile (band_factor.hpp:31-35) + the rejected pivot index."""
+
+    _fields_ = [
+        ("bandwidth", C.c_int64),
+        ("stored_entries", C.c_int64),
+        ("min_pivot_ratio", C.c_double),
+        ("pivot_index", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def build() -> None:
+    """Compile libzolo_b200.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    import subprocess
+
+    subprocess.run(["make", "-s", "-C", HERE, "-j8"], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CudaError(f"native extension missing: {LIB_PATH} (run paper_1701_08935_b200.build())")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        I64 = C.c_int64
+        D = C.c_double
+        L.zolo_last_error.restype = C.c_char_p
+        L.zolo_last_error.argtypes = [P]
+        L.zolo_version.restype = C.c_char_p
+        L.zolo_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+        L.zolo_ctx_destroy.argtypes = [P]
+        L.zolo_pencil_upload.argtypes = [P, I64, C.c_int, P, P, P, P, P, P]
+        L.zolo_set_design.argtypes = [P, P, C.c_int]
+        L.zolo_factorize.argtypes = [P, P, P]
+        L.zolo_apply_g.argtypes = [P, P, P, I64]
+        L.zolo_apply_filter.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
+        L.zolo_apply_filter_device.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
+        L.zolo_counters.argtypes = [P, P, P]
+        L.zolo_rr_project.argtypes = [P, P, I64, P, P]
+        L.zolo_block_update.argtypes = [P, P, I64, P, I64, P]
+        L.zolo_last_timings.argtypes = [P, P]
+        L.zolo_rcm.argtypes = [I64, P, P, P, P, P]
+        L.zolo_random_block.argtypes = [C.c_int, I64, I64, C.c_uint64, C.c_int, P]
+        L.zolo_uniform_stream.argtypes = [C.c_uint64, I64, P]
+        L.zolo_build_design.argtypes = [P, C.c_int, P]
+        L.zolo_eval_filter.argtypes = [P, C.c_int, I64, P, P, P]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def design_len(r: int) -> int:
+    return 17 + 10 * r
+
+
+def _check(ctx, st, pivot_index=-1):
+    if st == ZOLO_OK:
+        return
+    msg = lib().zolo_last_error(ctx).decode()
+    if st == ZOLO_ERR_DOMAIN:
+        raise DomainError(msg)
+    if st == ZOLO_ERR_FACTORIZATION:
+        raise FactorizationError(msg, pivot_index)
+    if st == ZOLO_ERR_NUMERICAL:
+        raise NumericalError(msg)
+    if st == ZOLO_ERR_CUDA:
+        raise CudaError(msg)
+    raise NumericalError(msg)
+
+
+def _check_host(st):
+    if st == ZOLO_OK:
+        return
+    msg = lib().zolo_last_error(None).decode()
+    if st == ZOLO_ERR_DOMAIN:
+        raise DomainError(msg)
+    raise NumericalError(msg)
+
+
+def rcm(n, rp, ci):
+    """reorder_rcm (rcm.hpp:69-115): perm[new] = old, plus bandwidth/profile."""
+    rp = np.ascontiguousarray(rp, dtype=np.int64)
+    ci = np.ascontiguousarray(ci, dtype=np.int64)
+    perm = np.zeros(n, dtype=np.int64)
+    bw = np.zeros(1, dtype=np.int64)
+    prof = np.zeros(1, dtype=np.int64)
+    lib().zolo_rcm(n, _ptr(rp), _ptr(ci), _ptr(perm), _ptr(bw), _ptr(prof))
+    return perm, int(bw[0]), int(prof[0])
+
+
+def random_block(n, k, seed, cx=False, orthonormalize=False):
+    """random_gaussian<S> (+ mgs_orthonormalize), dense.hpp:181-229, bit-reproducible."""
+    out = np.zeros((n, k), dtype=np.complex128 if cx else np.float64, order="F")
+    st = lib().zolo_random_block(int(cx), n, k, seed, int(orthonormalize), _ptr(out))
+    if st != ZOLO_OK:
+        raise NumericalError("random block failed to orthonormalize")
+    return out
+
+
+def _csr(m, cx):
+    rp = np.ascontiguousarray(m[0], dtype=np.int64)
+    ci = np.ascontiguousarray(m[1], dtype=np.int64)
+    v = np.ascontiguousarray(m[2], dtype=np.complex128 if cx else np.float64)
+    return rp, ci, v
+
+
+class FilterOperator:
+    """GPU FilterOperator<S> (filter_engine.hpp:37-165).
+
+    ``pencil`` = ``(n, A, B)`` with ``A``/``B`` = ``(rp, ci, vals)`` CSR (full
+    pattern, sorted columns; B ``None`` = identity). ``design`` is the packed
+    FilterDesign of ``include/zolo_b200.h`` (e.g. from
+    :func:`paper_1701_08935_b200.design.build_filter_design`); ``r`` its order.
+    ``is_complex`` selects S = complex128 (Hermitian pencil) vs float64.
+    """
+
+    def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None):
+        L = lib()
+        n, a, b = pencil
+        cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
+        self.n = int(n)
+        self.cx = cx
+        self.r = int(r)
+        self.design = np.ascontiguousarray(design, dtype=np.float64)
+        if self.design.size != design_len(self.r):
+            raise DomainError("design length does not match order r")
+        h = C.c_void_p()
+        st = L.zolo_ctx_create(device, C.byref(h))
+        if st != ZOLO_OK:
+            raise CudaError(L.zolo_last_error(None).decode())
+        self._h = h
+        self._a = _csr(a, cx)
+        self._b = _csr(b, cx) if b is not None else None
+        bp = self._b if self._b is not None else (None, None, None)
+        _check(h, L.zolo_pencil_upload(h, self.n, int(cx), *map(_ptr, self._a), *map(_ptr, bp)))
+        _check(h, L.zolo_set_design(h, _ptr(self.design), self.r))
+        self.stats = (FactorStats * self.r)()
+        perm_arr = None if perm is None else np.ascontiguousarray(perm, dtype=np.int64)
+        st = L.zolo_factorize(h, _ptr(perm_arr), self.stats)
+        if st == ZOLO_ERR_FACTORIZATION:
+            piv = min((s.pivot_index for s in self.stats if s.pivot_index >= 0), default=-1)
+            _check(h, st, piv)
+        _check(h, st)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().zolo_ctx_destroy(h)
+            self._h = None
+
+    # --- reference surface -------------------------------------------------
+    def dim(self) -> int:
+        return self.n
+
+    def inner_solve_count(self) -> int:
+        a = np.zeros(1, dtype=np.int64)
+        b = np.zeros(1, dtype=np.int64)
+        lib().zolo_counters(self._h, _ptr(a), _ptr(b))
+        return int(a[0])
+
+    def g_application_count(self) -> int:
+        a = np.zeros(1, dtype=np.int64)
+        b = np.zeros(1, dtype=np.int64)
+        lib().zolo_counters(self._h, _ptr(a), _ptr(b))
+        return int(b[0])
+
+    def _block(self, v):
+        v = np.asarray(v)
+        if v.ndim == 1:
+            v = v[:, None]
+        if v.shape[0] != self.n:
+            raise DomainError("dimension mismatch")
+        return np.asfortranarray(v, dtype=np.complex128 if self.cx else np.float64)
+
+    def apply_g(self, v):
+        """G v (filter_engine.hpp:56-82)."""
+        v = self._block(v)
+        out = np.zeros_like(v)
+        _check(self._h, lib().zolo_apply_g(self._h, _ptr(v), _ptr(out), v.shape[1]))
+        return out
+
+    def apply_filter(self, v, gmres_tol: float = 1e-12, gmres_max: int = 50):
+        """(R_ab(B^-1 A) V, report) (filter_engine.hpp:86-155). Raises GmresError."""
+        v = self._block(v)
+        k = v.shape[1]
+        y = np.zeros_like(v)
+        cols = np.zeros(k, dtype=np.int64)
+        rep = _Report()
+        rep.column_iterations = cols.ctypes.data_as(C.POINTER(C.c_int64))
+        st = lib().zolo_apply_filter(self._h, _ptr(v), _ptr(y), k, float(gmres_tol), int(gmres_max), C.byref(rep))
+        report = self._report(rep, cols)
+        if st == ZOLO_ERR_GMRES:
+            raise GmresError(lib().zolo_last_error(self._h).decode(), report, y)
+        _check(self._h, st)
+        return y, report
+
+    def apply_filter_device(self, d_v: int, d_y: int, ncols: int, gmres_tol=1e-12, gmres_max=50):
+        """Device-resident variant: raw device pointers (original ordering, ld = n)."""
+        cols = np.zeros(ncols, dtype=np.int64)
+        rep = _Report()
+        rep.column_iterations = cols.ctypes.data_as(C.POINTER(C.c_int64))
+        st = lib().zolo_apply_filter_device(self._h, C.c_void_p(d_v), C.c_void_p(d_y), ncols, float(gmres_tol),
+                                            int(gmres_max), C.byref(rep))
+        report = self._report(rep, cols)
+        if st == ZOLO_ERR_GMRES:
+            raise GmresError(lib().zolo_last_error(self._h).decode(), report)
+        _check(self._h, st)
+        return report
+
+    @staticmethod
+    def _report(rep, cols):
+        q = rep.n_shifts
+        return ShiftedSolveReport(
+            iterations=int(rep.iterations),
+            residuals=[float(rep.residuals[k]) for k in range(q)],
+            converged=[bool(rep.converged[k]) for k in range(q)],
+            column_iterations=[int(c) for c in cols],
+            operator_applications=int(rep.operator_applications),
+        )
+
+    # --- Rayleigh-Ritz helpers (eigensolver.hpp:105-148,190) ---------------
+    def rr_project(self, y):
+        y = self._block(y)
+        k = y.shape[1]
+        at = np.zeros((k, k), dtype=y.dtype, order="F")
+        bt = np.zeros((k, k), dtype=y.dtype, order="F")
+        _check(self._h, lib().zolo_rr_project(self._h, _ptr(y), k, _ptr(at), _ptr(bt)))
+        return at, bt
+
+    def block_update(self, y, q):
+        y = self._block(y)
+        q = np.asfortranarray(q, dtype=y.dtype)
+        out = np.zeros((self.n, q.shape[1]), dtype=y.dtype, order="F")
+        _check(self._h, lib().zolo_block_update(self._h, _ptr(y), y.shape[1], _ptr(q), q.shape[1], _ptr(out)))
+        return out
+
+    def last_timings(self):
+        ms = np.zeros(4)
+        lib().zolo_last_timings(self._h, _ptr(ms))
+        return dict(filter_ms=ms[0], factor_ms=ms[1], trsm_ms=ms[2], trsm_launches=int(ms[3]))
+
+    def factor_profile(self):
+        return [dict(bandwidth=s.bandwidth, stored_entries=s.stored_entries, min_pivot_ratio=s.min_pivot_ratio)
+                for s in self.stats]

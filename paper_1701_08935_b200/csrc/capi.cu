@@ -1,0 +1,986 @@
+// C ABI implementation (include/zolo_b200.h): context, device memory, and the
+// host-side orchestration of FilterOperator<S>::apply_g / apply_filter
+// (filter_engine.hpp:56-155) on the B200.
+//
+// One context = one device + one private stream. The multi-shift GMRES of
+// the reference runs one column at a time (gmres.hpp:98-182, one call per
+// column from filter_engine.hpp:109-111); here all columns of the block run
+// in lock step: each iteration applies G once to the compacted set of still
+// active columns (so g_applications == sum_col m_col, exactly as the
+// reference counts), then CGS2 + the batched shifted least squares decide
+// which columns finish. Everything stays in the factor ordering P v on the
+// device; only the input block is permuted in and the output permuted out.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/zolo_b200.h"
+#include "band.cuh"
+#include "host.hpp"
+#include "krylov.cuh"
+
+namespace zolo {
+void gmres_init(cudaStream_t st, GmresDev g);
+}
+
+using namespace zolo;
+
+namespace {
+
+struct ZoloError : std::runtime_error {
+  int code;
+  ZoloError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw ZoloError(ZOLO_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevMem() = default;
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  ~DevMem() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  // grow-only; returns true when (re)allocated
+  bool ensure(size_t b) {
+    if (b <= bytes && p) return false;
+    release();
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw ZoloError(ZOLO_ERR_CUDA, "cudaMalloc(" + std::to_string(b) + " B): " + cudaGetErrorString(e));
+    }
+    bytes = b;
+    return true;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+template <class T>
+void upload(DevMem& m, const std::vector<T>& v, cudaStream_t st) {
+  m.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
+  if (!v.empty()) CK(cudaMemcpyAsync(m.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+struct zolo_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int num_sms = 148;
+  std::string err;
+
+  // pencil (host copy, original ordering)
+  int64_t n = 0;
+  int cx = 0;
+  bool b_identity = true;
+  std::vector<int64_t> a_rp, a_ci, b_rp, b_ci;
+  std::vector<double> a_v, b_v;
+  bool have_pencil = false;
+
+  // design
+  int r = 0;
+  std::vector<double> design;
+  std::vector<std::complex<double>> eff_w, shifts;
+  std::vector<double> coef;
+  double constant_term = 0.0;
+  bool have_design = false;
+
+  // ordering + device pencil in the factor ordering
+  std::vector<int64_t> perm;
+  bool have_perm = false;
+  BandGeom geom;
+  DevMem perm_d, arp_d, aci_d, av_d, brp_d, bci_d, bv_d;
+
+  // factors
+  bool factored = false;
+  DevMem tiles_mem, rownorm_mem, fstate_mem;
+  std::vector<FactorTiles> tiles;
+  std::vector<cudaStream_t> pole_streams;
+  DevMem weights_d, shifts_d, coef_d;
+
+  // solve workspace
+  int64_t ncap = 0;  // columns the workspace is sized for
+  DevMem vin_orig, vin, vout, w, bbuf, chains_fwd, chains_bwd, flags, counter;
+  std::vector<std::unique_ptr<DevMem>> xbuf;
+  int64_t flags_cap = 0;
+  int epoch = 0;
+
+  // GMRES state
+  int maxit_cap = 0;
+  std::vector<std::unique_ptr<DevMem>> basis;
+  DevMem basis_ptrs, gH, gR, gG, gROT, gY, gZ, gres, gfrozen, gmlen, gbeta, gmcol, ghappy, gdone, gwnorm;
+  DevMem partial, hsave, act_d, rr_partial, rr_tmp, rr_out;
+  int* act_h = nullptr;
+  int* done_h = nullptr;
+
+  int64_t inner_solves = 0, g_apps = 0;
+  double last_ms[4] = {0, 0, 0, 0};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+
+  size_t es() const { return cx ? 16 : 8; }
+  int nchains() const { return cx ? 2 * r : r; }
+};
+
+namespace {
+
+std::string g_create_err;
+
+template <class F>
+int guarded(zolo_ctx* ctx, F&& f) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    f();
+    return ZOLO_OK;
+  } catch (const ZoloError& e) {
+    if (ctx) ctx->err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = "host allocation failed";
+    return ZOLO_ERR_NUMERICAL;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what();
+    return ZOLO_ERR_NUMERICAL;
+  }
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw ZoloError(ZOLO_ERR_DOMAIN, msg);
+}
+
+// Union pattern of A and B (B = I when absent): assemble_shifted (sparse.hpp:153-186).
+struct Union {
+  std::vector<int64_t> rp, ci;
+  std::vector<double> av, bv;  // interleaved when complex
+};
+
+Union union_pattern(const zolo_ctx& c) {
+  Union u;
+  const int64_t n = c.n;
+  const int w = c.cx ? 2 : 1;
+  u.rp.assign(n + 1, 0);
+  u.ci.reserve(c.a_ci.size() + (c.b_identity ? n : c.b_ci.size()));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t ka = c.a_rp[i], kb = c.b_identity ? 0 : c.b_rp[i];
+    const int64_t ea = c.a_rp[i + 1], eb = c.b_identity ? 1 : c.b_rp[i + 1];
+    while (ka < ea || kb < eb) {
+      const int64_t ja = ka < ea ? c.a_ci[ka] : n;
+      const int64_t jb = kb < eb ? (c.b_identity ? i : c.b_ci[kb]) : n;
+      const int64_t j = std::min(ja, jb);
+      u.ci.push_back(j);
+      for (int q = 0; q < w; ++q) {
+        u.av.push_back(ja == j ? c.a_v[ka * w + q] : 0.0);
+        u.bv.push_back(jb == j ? (c.b_identity ? (q == 0 ? 1.0 : 0.0) : c.b_v[kb * w + q]) : 0.0);
+      }
+      if (ja == j) ++ka;
+      if (jb == j) ++kb;
+    }
+    u.rp[i + 1] = static_cast<int64_t>(u.ci.size());
+  }
+  return u;
+}
+
+// P M P^T as int32 CSR with sorted columns.
+void permuted_csr(int64_t n, const std::vector<int64_t>& rp, const std::vector<int64_t>& ci,
+                  const std::vector<double>& v, int w, const std::vector<int64_t>& perm, const std::vector<int>& pos,
+                  std::vector<int>& prp, std::vector<int>& pci, std::vector<double>& pv) {
+  prp.assign(n + 1, 0);
+  pci.clear();
+  pv.clear();
+  std::vector<std::pair<int, int64_t>> row;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t i = perm[t];
+    row.clear();
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) row.emplace_back(pos[ci[k]], k);
+    std::sort(row.begin(), row.end());
+    for (auto& e : row) {
+      pci.push_back(e.first);
+      for (int q = 0; q < w; ++q) pv.push_back(v[e.second * w + q]);
+    }
+    prp[t + 1] = static_cast<int>(pci.size());
+  }
+}
+
+void ensure_perm_csr(zolo_ctx& c) {
+  if (c.have_perm) return;
+  require(c.have_pencil, "no pencil uploaded");
+  c.perm.resize(c.n);
+  for (int64_t i = 0; i < c.n; ++i) c.perm[i] = i;
+  std::vector<int> pos(c.n), prp, pci;
+  for (int64_t i = 0; i < c.n; ++i) pos[i] = static_cast<int>(i);
+  std::vector<double> pv;
+  const int w = c.cx ? 2 : 1;
+  permuted_csr(c.n, c.a_rp, c.a_ci, c.a_v, w, c.perm, pos, prp, pci, pv);
+  upload(c.arp_d, prp, c.st);
+  upload(c.aci_d, pci, c.st);
+  upload(c.av_d, pv, c.st);
+  if (!c.b_identity) {
+    permuted_csr(c.n, c.b_rp, c.b_ci, c.b_v, w, c.perm, pos, prp, pci, pv);
+    upload(c.brp_d, prp, c.st);
+    upload(c.bci_d, pci, c.st);
+    upload(c.bv_d, pv, c.st);
+  }
+  std::vector<int> p32(c.perm.begin(), c.perm.end());
+  upload(c.perm_d, p32, c.st);
+  c.geom.n = c.n;
+  c.geom.nbk = static_cast<int>((c.n + TILE - 1) / TILE);
+  c.geom.npad = static_cast<int64_t>(c.geom.nbk) * TILE;
+  c.have_perm = true;
+}
+
+void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats) {
+  require(c.have_pencil, "zolo_factorize: no pencil uploaded");
+  require(c.have_design, "zolo_factorize: no design installed");
+  const int64_t n = c.n;
+  const int w = c.cx ? 2 : 1;
+  Union u = union_pattern(c);
+  c.perm.resize(n);
+  if (perm_in) {
+    std::vector<char> seen(n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      require(perm_in[i] >= 0 && perm_in[i] < n && !seen[perm_in[i]], "zolo_factorize: invalid permutation");
+      seen[perm_in[i]] = 1;
+      c.perm[i] = perm_in[i];
+    }
+  } else {
+    rcm_order(n, u.rp.data(), u.ci.data(), c.perm.data());  // band_factor.hpp:203-204
+  }
+  std::vector<int> pos(n);
+  for (int64_t k = 0; k < n; ++k) pos[c.perm[k]] = static_cast<int>(k);
+  const int64_t bw = bandwidth_under(n, u.rp.data(), u.ci.data(), c.perm.data());
+
+  BandGeom g;
+  g.n = n;
+  g.nbk = static_cast<int>((n + TILE - 1) / TILE);
+  g.npad = static_cast<int64_t>(g.nbk) * TILE;
+  g.bw = bw;
+  g.J = static_cast<int>((bw + TILE - 1) / TILE);
+  c.geom = g;
+
+  // permuted union entries for the scatter
+  const int64_t nnz = static_cast<int64_t>(u.ci.size());
+  std::vector<int> er(nnz), ec(nnz);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = u.rp[i]; k < u.rp[i + 1]; ++k) {
+      er[k] = pos[i];
+      ec[k] = pos[u.ci[k]];
+    }
+  DevMem er_d, ec_d, ea_d, eb_d;
+  upload(er_d, er, c.st);
+  upload(ec_d, ec, c.st);
+  upload(ea_d, u.av, c.st);
+  upload(eb_d, u.bv, c.st);
+
+  // device pencil in the factor ordering (SpMM with A, B)
+  {
+    std::vector<int> prp, pci;
+    std::vector<double> pv;
+    permuted_csr(n, c.a_rp, c.a_ci, c.a_v, w, c.perm, pos, prp, pci, pv);
+    upload(c.arp_d, prp, c.st);
+    upload(c.aci_d, pci, c.st);
+    upload(c.av_d, pv, c.st);
+    if (!c.b_identity) {
+      permuted_csr(n, c.b_rp, c.b_ci, c.b_v, w, c.perm, pos, prp, pci, pv);
+      upload(c.brp_d, prp, c.st);
+      upload(c.bci_d, pci, c.st);
+      upload(c.bv_d, pv, c.st);
+    }
+    std::vector<int> p32(c.perm.begin(), c.perm.end());
+    upload(c.perm_d, p32, c.st);
+    c.have_perm = true;
+  }
+
+  // tiles for r poles
+  const int r = c.r;
+  const size_t per_array = g.tiles_per_array() * TT;
+  const size_t per_pole = 2 * per_array + 2 * static_cast<size_t>(g.nbk) * TT;  // complex entries
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t need = per_pole * r * sizeof(cd);
+  c.tiles_mem.release();
+  if (need + (size_t(1) << 30) > free_b + c.tiles_mem.bytes)
+    throw ZoloError(ZOLO_ERR_DOMAIN, "zolo_factorize: band factors need " + std::to_string(need >> 20) +
+                                         " MiB, device has " + std::to_string(free_b >> 20) + " MiB free");
+  c.tiles_mem.ensure(need);
+  c.rownorm_mem.ensure(sizeof(double) * g.npad * r);
+  c.fstate_mem.ensure(sizeof(unsigned long long) * 2 * r);
+  c.tiles.assign(r, FactorTiles());
+  cd* base = c.tiles_mem.as<cd>();
+  for (int j = 0; j < r; ++j) {
+    cd* p = base + per_pole * j;
+    c.tiles[j].Lt = p;
+    c.tiles[j].Ut = p + per_array;
+    c.tiles[j].DinvL = p + 2 * per_array;
+    c.tiles[j].DinvU = p + 2 * per_array + static_cast<size_t>(g.nbk) * TT;
+  }
+  // fail index (int, init -1) and min ratio bits (init +inf)
+  std::vector<unsigned long long> fs(2 * r);
+  const double inf = std::numeric_limits<double>::infinity();
+  unsigned long long infbits;
+  std::memcpy(&infbits, &inf, 8);
+  for (int j = 0; j < r; ++j) {
+    fs[2 * j] = 0xffffffffffffffffull;  // int -1 in the low word
+    fs[2 * j + 1] = infbits;
+  }
+  CK(cudaMemcpy(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice));
+
+  while (static_cast<int>(c.pole_streams.size()) < r) {
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    c.pole_streams.push_back(s);
+  }
+  CK(cudaEventRecord(c.ev0, c.st));
+  for (int j = 0; j < r; ++j) CK(cudaStreamWaitEvent(c.pole_streams[j], c.ev0, 0));
+  const double* poles = c.design.data() + ZOLO_DESIGN_HEAD;
+  for (int j = 0; j < r; ++j) {
+    cudaStream_t ps = c.pole_streams[j];
+    double* rn = c.rownorm_mem.as<double>() + g.npad * j;
+    factor_scatter(ps, g, c.tiles[j], nnz, er_d.as<int>(), ec_d.as<int>(), ea_d.as<double>(), eb_d.as<double>(),
+                   c.cx, poles[2 * j], poles[2 * j + 1], rn);
+    FactorDevState ds;
+    ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
+    ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
+    factor_run(ps, g, c.tiles[j], rn, ds);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c.ev2, ps));
+    CK(cudaStreamWaitEvent(c.st, c.ev2, 0));
+  }
+  CK(cudaEventRecord(c.ev1, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  for (int j = 0; j < r; ++j) CK(cudaStreamSynchronize(c.pole_streams[j]));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+  c.last_ms[1] = ms;
+  CK(cudaMemcpy(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost));
+  int fail_any = -1;
+  for (int j = 0; j < r; ++j) {
+    const int fi = static_cast<int>(static_cast<uint32_t>(fs[2 * j] & 0xffffffffull));
+    double mr;
+    std::memcpy(&mr, &fs[2 * j + 1], 8);
+    if (stats) {
+      stats[j].bandwidth = bw;
+      stats[j].stored_entries = static_cast<int64_t>(per_pole);
+      stats[j].min_pivot_ratio = mr;
+      stats[j].pivot_index = fi;
+    }
+    if (fi >= 0 && fail_any < 0) fail_any = fi;
+  }
+  c.factored = fail_any < 0;
+  c.ncap = 0;  // chains must be rebuilt against the new factors
+  if (fail_any >= 0)
+    throw ZoloError(ZOLO_ERR_FACTORIZATION,
+                    "factorize: pivot " + std::to_string(fail_any) + " below threshold");
+}
+
+void ensure_workspace(zolo_ctx& c, int64_t ncols) {
+  const int64_t ld = c.geom.npad;
+  const size_t es = c.es();
+  if (ncols <= c.ncap) return;
+  const int64_t nc = ncols;
+  c.vin_orig.ensure(es * c.n * nc);
+  c.vin.ensure(es * ld * nc);
+  c.vout.ensure(es * ld * nc);
+  c.w.ensure(es * ld * nc);
+  c.bbuf.ensure(sizeof(cd) * ld * nc);
+  const int nch = c.nchains();
+  while (static_cast<int>(c.xbuf.size()) < nch) c.xbuf.emplace_back(new DevMem());
+  for (int i = 0; i < nch; ++i) c.xbuf[i]->ensure(sizeof(cd) * ld * nc);
+  std::vector<Chain> fwd(nch), bwd(nch);
+  for (int p = 0; p < c.r; ++p) {
+    const FactorTiles& t = c.tiles[p];
+    if (c.cx) {
+      cd* x = c.xbuf[2 * p]->as<cd>();
+      cd* xa = c.xbuf[2 * p + 1]->as<cd>();
+      fwd[2 * p] = Chain{t.Lt, t.DinvL, c.bbuf.as<cd>(), x, FWD_L, 0};
+      bwd[2 * p] = Chain{t.Ut, t.DinvU, x, x, BWD_U, 0};
+      fwd[2 * p + 1] = Chain{t.Ut, t.DinvU, c.bbuf.as<cd>(), xa, FWD_UH, 0};
+      bwd[2 * p + 1] = Chain{t.Lt, t.DinvL, xa, xa, BWD_LH, 0};
+    } else {
+      cd* x = c.xbuf[p]->as<cd>();
+      fwd[p] = Chain{t.Lt, t.DinvL, c.bbuf.as<cd>(), x, FWD_L, 0};
+      bwd[p] = Chain{t.Ut, t.DinvU, x, x, BWD_U, 0};
+    }
+  }
+  upload(c.chains_fwd, fwd, c.st);
+  upload(c.chains_bwd, bwd, c.st);
+  const int64_t ngroups = (nc + CG - 1) / CG;
+  const int64_t nflags = static_cast<int64_t>(nch) * ngroups * c.geom.nbk;
+  if (nflags > c.flags_cap) {
+    c.flags.ensure(sizeof(int) * nflags);
+    CK(cudaMemsetAsync(c.flags.p, 0, sizeof(int) * nflags, c.st));
+    c.flags_cap = nflags;
+    c.epoch = 0;
+  }
+  if (c.counter.ensure(sizeof(int) * 4)) CK(cudaMemsetAsync(c.counter.p, 0, sizeof(int) * 4, c.st));
+  c.act_d.ensure(sizeof(int) * nc);
+  if (c.act_h) cudaFreeHost(c.act_h);
+  if (c.done_h) cudaFreeHost(c.done_h);
+  CK(cudaMallocHost(&c.act_h, sizeof(int) * nc));
+  CK(cudaMallocHost(&c.done_h, sizeof(int) * nc));
+  c.ncap = nc;
+  c.maxit_cap = 0;  // GMRES state is sized per (ncap, maxit)
+}
+
+// G applied to the columns act[0..na) of vsrc (ld x ncap, S) -> w[:, act].
+float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
+  const int64_t ld = c.geom.npad, n = c.n;
+  const int* act = c.act_d.as<int>();
+  const int nch = c.nchains();
+  std::vector<cd*> xs(nch);
+  for (int i = 0; i < nch; ++i) xs[i] = c.xbuf[i]->as<cd>();
+  if (c.cx)
+    Krylov<cd>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
+                        c.bv_d.as<cd>(), reinterpret_cast<const cd*>(vsrc), act, na, c.bbuf.as<cd>());
+  else
+    Krylov<double>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
+                            c.bv_d.as<double>(), reinterpret_cast<const double*>(vsrc), act, na, c.bbuf.as<cd>());
+  CK(cudaEventRecord(c.ev2, c.st));
+  trsm_launch(c.st, c.geom, c.chains_fwd.as<Chain>(), nch, na, ld, c.flags.as<int>(), ++c.epoch, c.counter.as<int>(),
+              1, c.num_sms);
+  trsm_launch(c.st, c.geom, c.chains_bwd.as<Chain>(), nch, na, ld, c.flags.as<int>(), ++c.epoch,
+              c.counter.as<int>() + 1, 0, c.num_sms);
+  CK(cudaEventRecord(c.ev3, c.st));
+  CK(cudaGetLastError());
+  if (c.cx)
+    Krylov<cd>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const cd*>(vsrc), act, na, xs.data(),
+                        c.weights_d.as<cd>(), c.r, reinterpret_cast<cd*>(wdst));
+  else
+    Krylov<double>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const double*>(vsrc), act, na, xs.data(),
+                            c.weights_d.as<cd>(), c.r, reinterpret_cast<double*>(wdst));
+  CK(cudaGetLastError());
+  return 0.0f;
+}
+
+template <class S>
+void ensure_gmres(zolo_ctx& c, int maxit) {
+  if (maxit <= c.maxit_cap) return;
+  const int64_t nv = c.ncap;
+  const int q = 2 * c.r;
+  const size_t es = sizeof(S);
+  c.gH.ensure(es * nv * (maxit + 1) * maxit);
+  c.gR.ensure(sizeof(cd) * nv * q * maxit * maxit);
+  c.gG.ensure(sizeof(cd) * nv * q * (maxit + 1));
+  c.gROT.ensure(sizeof(cd) * nv * q * 2 * maxit);
+  c.gY.ensure(sizeof(cd) * nv * q * maxit);
+  c.gZ.ensure(sizeof(cd) * nv * maxit);
+  c.gres.ensure(sizeof(double) * nv * q);
+  c.gfrozen.ensure(sizeof(int) * nv * q);
+  c.gmlen.ensure(sizeof(int) * nv * q);
+  c.gbeta.ensure(sizeof(double) * nv);
+  c.gmcol.ensure(sizeof(int) * nv);
+  c.ghappy.ensure(sizeof(int) * nv);
+  c.gdone.ensure(sizeof(int) * nv);
+  c.gwnorm.ensure(sizeof(double) * nv);
+  const int64_t nchunk = (c.n + CHUNK - 1) / CHUNK;
+  c.partial.ensure(2 * es * nv * nchunk * (maxit + 1) + 64);
+  c.hsave.ensure(es * nv * (maxit + 1));
+  c.basis_ptrs.ensure(sizeof(void*) * (maxit + 1));
+  c.maxit_cap = maxit;
+}
+
+GmresDev gmres_view(zolo_ctx& c, int maxit) {
+  GmresDev g;
+  g.maxit = maxit;
+  g.q = 2 * c.r;
+  g.nv = static_cast<int>(c.ncap);
+  g.H = c.gH.p;
+  g.R = c.gR.as<cd>();
+  g.G = c.gG.as<cd>();
+  g.ROT = c.gROT.as<cd>();
+  g.Y = c.gY.as<cd>();
+  g.Z = c.gZ.as<cd>();
+  g.res = c.gres.as<double>();
+  g.frozen = c.gfrozen.as<int>();
+  g.mlen = c.gmlen.as<int>();
+  g.beta = c.gbeta.as<double>();
+  g.mcol = c.gmcol.as<int>();
+  g.happy = c.ghappy.as<int>();
+  g.done = c.gdone.as<int>();
+  g.wnorm = c.gwnorm.as<double>();
+  g.shifts = c.shifts_d.as<cd>();
+  g.coef = c.coef_d.as<double>();
+  return g;
+}
+
+void* basis_block(zolo_ctx& c, int i) {
+  const size_t bytes = c.es() * c.geom.npad * c.ncap;
+  while (static_cast<int>(c.basis.size()) <= i) c.basis.emplace_back(new DevMem());
+  if (c.basis[i]->ensure(bytes)) {
+    void* p = c.basis[i]->p;
+    CK(cudaMemcpyAsync(c.basis_ptrs.as<void*>() + i, &p, sizeof(void*), cudaMemcpyHostToDevice, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  }
+  return c.basis[i]->p;
+}
+
+template <class S>
+int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
+                      zolo_report* rep) {
+  require(c.factored, "apply_filter: operator not factorized");
+  require(gmres_max >= 1 && gmres_max <= 64, "apply_filter: gmres_max must be in [1, 64]");
+  const int64_t n = c.n, ld = c.geom.npad;
+  const int maxit = static_cast<int>(gmres_max);
+  const int q = 2 * c.r;
+  ensure_workspace(c, ncols);
+  ensure_gmres<S>(c, maxit);
+  // basis pointers may predate a reallocation: refresh all
+  for (int i = 0; i < static_cast<int>(c.basis.size()); ++i) {
+    if (c.basis[i]->bytes < c.es() * ld * c.ncap) c.basis[i]->release();
+  }
+  std::vector<void*> bp;
+  for (int i = 0; i <= maxit; ++i) bp.push_back(i < static_cast<int>(c.basis.size()) ? c.basis[i]->p : nullptr);
+  CK(cudaMemcpyAsync(c.basis_ptrs.p, bp.data(), sizeof(void*) * bp.size(), cudaMemcpyHostToDevice, c.st));
+  CK(cudaStreamSynchronize(c.st));
+
+  CK(cudaEventRecord(c.ev0, c.st));
+  S* vin = c.vin.as<S>();
+  Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(d_v), n, vin, ld, ncols, c.perm_d.as<int>());
+  GmresDev g = gmres_view(c, maxit);
+  g.nv = static_cast<int>(ncols);
+  Krylov<S>::col_norms(c.st, vin, n, ld, ncols, g.beta);
+  S* v0 = reinterpret_cast<S*>(basis_block(c, 0));
+  Krylov<S>::scale_cols(c.st, vin, v0, n, ld, ncols, g.beta);
+  gmres_init(c.st, g);
+  std::vector<double> beta(ncols);
+  CK(cudaMemcpyAsync(beta.data(), g.beta, sizeof(double) * ncols, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  std::vector<int> active;
+  for (int64_t k = 0; k < ncols; ++k)
+    if (beta[k] != 0.0) active.push_back(static_cast<int>(k));
+
+  const int nchunk = static_cast<int>((n + CHUNK - 1) / CHUNK);
+  float trsm_ms = 0.0f;
+  int trsm_launches = 0;
+  for (int it = 0; it < maxit && !active.empty(); ++it) {
+    const int na = static_cast<int>(active.size());
+    std::memcpy(c.act_h, active.data(), sizeof(int) * na);
+    CK(cudaMemcpyAsync(c.act_d.p, c.act_h, sizeof(int) * na, cudaMemcpyHostToDevice, c.st));
+    S* vm = reinterpret_cast<S*>(basis_block(c, it));
+    apply_g_device(c, vm, na, c.w.p);
+    trsm_launches += 2;
+    c.g_apps += na;
+    c.inner_solves += static_cast<int64_t>(c.nchains()) * na;
+    Krylov<S>::arnoldi(c.st, n, ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(), c.act_d.as<int>(), na, g,
+                       c.partial.as<double>(), nchunk, c.hsave.as<S>());
+    Krylov<S>::least_squares(c.st, c.act_d.as<int>(), na, it, g, c.partial.as<double>(), nchunk, tol);
+    if (it + 1 < maxit) {
+      S* vn = reinterpret_cast<S*>(basis_block(c, it + 1));
+      Krylov<S>::next_basis(c.st, n, ld, c.w.as<S>(), vn, c.act_d.as<int>(), na, g);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c.done_h, g.done, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
+    int spin_err[2] = {0, 0};
+    CK(cudaMemcpyAsync(spin_err, c.counter.as<int>() + 2, sizeof(int) * 2, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    if (spin_err[0] || spin_err[1]) throw ZoloError(ZOLO_ERR_CUDA, "triangular solve: dependency wait timed out");
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c.ev2, c.ev3));
+    trsm_ms += ms;
+    std::vector<int> next;
+    for (int col : active)
+      if (!c.done_h[col]) next.push_back(col);
+    active.swap(next);
+  }
+  S* yp = c.vout.as<S>();
+  Krylov<S>::assemble(c.st, n, ld, v0, c.basis_ptrs.as<S*>(), static_cast<int>(ncols), g, vin, yp);
+  Krylov<S>::permute_out(c.st, yp, ld, reinterpret_cast<S*>(d_y), n, ncols, c.perm_d.as<int>());
+  CK(cudaEventRecord(c.ev1, c.st));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c.st));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+  c.last_ms[0] = ms;
+  c.last_ms[2] = trsm_ms;
+  c.last_ms[3] = trsm_launches;
+
+  // report (gmres.hpp:31-43 merged as filter_engine.hpp:127-133)
+  std::vector<double> res(ncols * q);
+  std::vector<int> mcol(ncols), happy(ncols);
+  CK(cudaMemcpy(res.data(), g.res, sizeof(double) * ncols * q, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(mcol.data(), g.mcol, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(happy.data(), g.happy, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
+  bool all_conv = true;
+  if (rep) {
+    rep->iterations = 0;
+    rep->operator_applications = 0;
+    rep->n_shifts = q;
+    for (int k = 0; k < q; ++k) {
+      rep->residuals[k] = 0.0;
+      rep->converged[k] = 1;
+    }
+  }
+  for (int64_t col = 0; col < ncols; ++col) {
+    for (int k = 0; k < q; ++k) {
+      const double rk = res[col * q + k];
+      if (rep) rep->residuals[k] = std::max(rep->residuals[k], rk);
+      if (!(rk <= tol) && !happy[col] && beta[col] != 0.0) {
+        all_conv = false;
+        if (rep) rep->converged[k] = 0;
+      }
+    }
+    if (rep) {
+      rep->iterations = std::max<int64_t>(rep->iterations, mcol[col]);
+      rep->operator_applications += mcol[col];
+      if (rep->column_iterations) rep->column_iterations[col] = mcol[col];
+    }
+  }
+  if (rep) rep->all_converged = all_conv ? 1 : 0;
+  if (!all_conv) {
+    c.err = "multishift_gmres: not converged within " + std::to_string(maxit) + " iterations";
+    return ZOLO_ERR_GMRES;
+  }
+  return ZOLO_OK;
+}
+
+template <class S>
+void apply_g_impl(zolo_ctx& c, const double* v, double* gv, int64_t k) {
+  require(c.factored, "apply_g: operator not factorized");
+  const int64_t n = c.n, ld = c.geom.npad;
+  ensure_workspace(c, k);
+  CK(cudaMemcpyAsync(c.vin_orig.p, v, c.es() * n * k, cudaMemcpyHostToDevice, c.st));
+  Krylov<S>::permute_in(c.st, c.vin_orig.as<S>(), n, c.vin.as<S>(), ld, k, c.perm_d.as<int>());
+  for (int64_t i = 0; i < k; ++i) c.act_h[i] = static_cast<int>(i);
+  CK(cudaMemcpyAsync(c.act_d.p, c.act_h, sizeof(int) * k, cudaMemcpyHostToDevice, c.st));
+  apply_g_device(c, c.vin.p, static_cast<int>(k), c.w.p);
+  Krylov<S>::permute_out(c.st, c.w.as<S>(), ld, c.vin_orig.as<S>(), n, k, c.perm_d.as<int>());
+  CK(cudaMemcpyAsync(gv, c.vin_orig.p, c.es() * n * k, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  // filter_engine.hpp:58,70,79: one application per call, r or 2r solves
+  c.g_apps += 1;
+  c.inner_solves += c.nchains();
+}
+
+template <class S>
+void rr_impl(zolo_ctx& c, const double* y, int64_t k, double* at, double* bt) {
+  ensure_perm_csr(c);
+  const int64_t n = c.n, ld = c.geom.npad;
+  const size_t es = sizeof(S);
+  DevMem yo, yp, ay;
+  yo.ensure(es * n * k);
+  yp.ensure(es * ld * k);
+  ay.ensure(es * ld * k);
+  const int64_t nchunk = (n + CHUNK - 1) / CHUNK;
+  c.rr_partial.ensure(es * nchunk * k * k + 64);
+  c.rr_out.ensure(es * k * k);
+  CK(cudaMemcpyAsync(yo.p, y, es * n * k, cudaMemcpyHostToDevice, c.st));
+  Krylov<S>::permute_in(c.st, yo.as<S>(), n, yp.as<S>(), ld, k, c.perm_d.as<int>());
+  Krylov<S>::spmm(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), yp.as<S>(), k, ay.as<S>());
+  Krylov<S>::gram(c.st, n, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
+  CK(cudaMemcpyAsync(at, c.rr_out.p, es * k * k, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  if (c.b_identity) {
+    Krylov<S>::gram(c.st, n, ld, yp.as<S>(), k, yp.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
+  } else {
+    Krylov<S>::spmm(c.st, n, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), yp.as<S>(), k, ay.as<S>());
+    Krylov<S>::gram(c.st, n, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
+  }
+  CK(cudaMemcpyAsync(bt, c.rr_out.p, es * k * k, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+}
+
+template <class S>
+void block_update_impl(zolo_ctx& c, const double* y, int64_t k, const double* q, int64_t kk, double* out) {
+  const int64_t n = c.n;
+  const size_t es = sizeof(S);
+  DevMem yd, qd, od;
+  yd.ensure(es * n * k);
+  qd.ensure(es * k * kk);
+  od.ensure(es * n * kk);
+  CK(cudaMemcpyAsync(yd.p, y, es * n * k, cudaMemcpyHostToDevice, c.st));
+  CK(cudaMemcpyAsync(qd.p, q, es * k * kk, cudaMemcpyHostToDevice, c.st));
+  Krylov<S>::block_gemm(c.st, n, n, yd.as<S>(), k, qd.as<S>(), kk, od.as<S>());
+  CK(cudaMemcpyAsync(out, od.p, es * n * kk, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* zolo_version(void) { return "zolo-b200 0.1.0 (sm_100a)"; }
+
+int zolo_ctx_create(int device, zolo_ctx** out) {
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    g_create_err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+    return ZOLO_ERR_CUDA;
+  }
+  if (device < 0 || device >= ndev) {
+    g_create_err = "device index out of range";
+    return ZOLO_ERR_DOMAIN;
+  }
+  auto* c = new zolo_ctx();
+  c->device = device;
+  const int st = guarded(c, [&] {
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaEventCreate(&c->ev0));
+    CK(cudaEventCreate(&c->ev1));
+    CK(cudaEventCreate(&c->ev2));
+    CK(cudaEventCreate(&c->ev3));
+  });
+  if (st != ZOLO_OK) {
+    g_create_err = c->err;
+    delete c;
+    return st;
+  }
+  *out = c;
+  return ZOLO_OK;
+}
+
+int zolo_ctx_destroy(zolo_ctx* c) {
+  if (!c) return ZOLO_OK;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  for (auto s : c->pole_streams) cudaStreamDestroy(s);
+  if (c->act_h) cudaFreeHost(c->act_h);
+  if (c->done_h) cudaFreeHost(c->done_h);
+  for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3})
+    if (ev) cudaEventDestroy(ev);
+  cudaStream_t st = c->st;
+  delete c;
+  if (st) cudaStreamDestroy(st);
+  return ZOLO_OK;
+}
+
+const char* zolo_last_error(const zolo_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int zolo_pencil_upload(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
+                       const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v) {
+  return guarded(c, [&] {
+    require(n > 0, "zolo_pencil_upload: n must be positive");
+    require(n < (int64_t(1) << 31) - TILE, "zolo_pencil_upload: n exceeds int32 indexing");
+    require(scalar == ZOLO_F64 || scalar == ZOLO_C128, "zolo_pencil_upload: bad scalar tag");
+    require(a_rp && a_ci && a_v, "zolo_pencil_upload: A missing");
+    c->n = n;
+    c->cx = scalar;
+    const int w = scalar ? 2 : 1;
+    c->a_rp.assign(a_rp, a_rp + n + 1);
+    c->a_ci.assign(a_ci, a_ci + a_rp[n]);
+    c->a_v.assign(a_v, a_v + a_rp[n] * w);
+    c->b_identity = b_rp == nullptr;
+    if (!c->b_identity) {
+      c->b_rp.assign(b_rp, b_rp + n + 1);
+      c->b_ci.assign(b_ci, b_ci + b_rp[n]);
+      c->b_v.assign(b_v, b_v + b_rp[n] * w);
+    } else {
+      c->b_rp.clear();
+      c->b_ci.clear();
+      c->b_v.clear();
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      require(c->a_rp[i] <= c->a_rp[i + 1], "zolo_pencil_upload: A offsets not monotone");
+      for (int64_t k = c->a_rp[i]; k < c->a_rp[i + 1]; ++k)
+        require(c->a_ci[k] >= 0 && c->a_ci[k] < n && (k == c->a_rp[i] || c->a_ci[k] > c->a_ci[k - 1]),
+                "zolo_pencil_upload: A column indices must be in range and sorted");
+      if (!c->b_identity)
+        for (int64_t k = c->b_rp[i]; k < c->b_rp[i + 1]; ++k)
+          require(c->b_ci[k] >= 0 && c->b_ci[k] < n && (k == c->b_rp[i] || c->b_ci[k] > c->b_ci[k - 1]),
+                  "zolo_pencil_upload: B column indices must be in range and sorted");
+    }
+    c->have_pencil = true;
+    c->have_perm = false;
+    c->factored = false;
+    c->ncap = 0;
+  });
+}
+
+int zolo_set_design(zolo_ctx* c, const double* design, int r) {
+  return guarded(c, [&] {
+    require(r >= 1 && r <= ZOLO_MAX_ORDER, "zolo_set_design: order must be in [1,16]");
+    c->design.assign(design, design + ZOLO_DESIGN_LEN(r));
+    c->r = r;
+    const double m_hat = design[ZOLO_DESIGN_M_HAT];
+    const double* wts = design + ZOLO_DESIGN_HEAD + 2 * r;
+    const double* opf = design + ZOLO_DESIGN_HEAD + 5 * r;
+    const double* oc = design + ZOLO_DESIGN_HEAD + 6 * r + (2 * r - 1);
+    const double mo = design[ZOLO_DESIGN_OUTER_M];
+    c->eff_w.clear();
+    c->shifts.clear();
+    c->coef.clear();
+    for (int j = 0; j < r; ++j) {
+      c->eff_w.push_back(m_hat * std::complex<double>(wts[2 * j], wts[2 * j + 1]));  // filter_engine.hpp:43-44
+      const double root = std::sqrt(oc[2 * j]);                                      // filter_engine.hpp:90-96
+      c->shifts.emplace_back(0.0, root);
+      c->shifts.emplace_back(0.0, -root);
+      const double cf = (0.5 * mo) * (0.5 * opf[j]);  // filter_engine.hpp:112-121
+      c->coef.push_back(cf);
+      c->coef.push_back(cf);
+    }
+    for (size_t a = 0; a < c->shifts.size(); ++a)
+      for (size_t b = a + 1; b < c->shifts.size(); ++b)
+        require(c->shifts[a] != c->shifts[b], "multishift_gmres: shifts must be distinct");
+    c->constant_term = design[ZOLO_DESIGN_CONSTANT];
+    std::vector<cd> w(r), s(2 * r);
+    for (int j = 0; j < r; ++j) w[j] = mk(c->eff_w[j].real(), c->eff_w[j].imag());
+    for (int k = 0; k < 2 * r; ++k) s[k] = mk(c->shifts[k].real(), c->shifts[k].imag());
+    upload(c->weights_d, w, c->st);
+    upload(c->shifts_d, s, c->st);
+    upload(c->coef_d, c->coef, c->st);
+    c->have_design = true;
+    c->factored = false;
+  });
+}
+
+int zolo_factorize(zolo_ctx* c, const int64_t* perm, zolo_factor_stats* stats) {
+  return guarded(c, [&] { do_factorize(*c, perm, stats); });
+}
+
+int zolo_filter_create(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
+                       const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v,
+                       const double* design, int r, zolo_factor_stats* stats) {
+  int st = zolo_pencil_upload(c, n, scalar, a_rp, a_ci, a_v, b_rp, b_ci, b_v);
+  if (st) return st;
+  st = zolo_set_design(c, design, r);
+  if (st) return st;
+  return zolo_factorize(c, nullptr, stats);
+}
+
+int zolo_apply_g(zolo_ctx* c, const double* v, double* gv, int64_t ncols) {
+  return guarded(c, [&] {
+    require(ncols >= 1, "apply_g: empty block");
+    if (c->cx)
+      apply_g_impl<cd>(*c, v, gv, ncols);
+    else
+      apply_g_impl<double>(*c, v, gv, ncols);
+  });
+}
+
+int zolo_apply_filter_device(zolo_ctx* c, const void* d_v, void* d_y, int64_t ncols, double gmres_tol,
+                             int64_t gmres_max, zolo_report* rep) {
+  int code = ZOLO_OK;
+  const int st = guarded(c, [&] {
+    require(ncols >= 1, "apply_filter: empty block");
+    code = c->cx ? apply_filter_impl<cd>(*c, d_v, d_y, ncols, gmres_tol, gmres_max, rep)
+                 : apply_filter_impl<double>(*c, d_v, d_y, ncols, gmres_tol, gmres_max, rep);
+  });
+  return st != ZOLO_OK ? st : code;
+}
+
+int zolo_apply_filter(zolo_ctx* c, const double* v, double* y, int64_t ncols, double gmres_tol, int64_t gmres_max,
+                      zolo_report* rep) {
+  int code = ZOLO_OK;
+  const int st = guarded(c, [&] {
+    require(ncols >= 1, "apply_filter: empty block");
+    require(c->factored, "apply_filter: operator not factorized");
+    const size_t bytes = c->es() * c->n * ncols;
+    DevMem dv, dy;
+    dv.ensure(bytes);
+    dy.ensure(bytes);
+    CK(cudaMemcpyAsync(dv.p, v, bytes, cudaMemcpyHostToDevice, c->st));
+    code = c->cx ? apply_filter_impl<cd>(*c, dv.p, dy.p, ncols, gmres_tol, gmres_max, rep)
+                 : apply_filter_impl<double>(*c, dv.p, dy.p, ncols, gmres_tol, gmres_max, rep);
+    CK(cudaMemcpyAsync(y, dy.p, bytes, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  });
+  return st != ZOLO_OK ? st : code;
+}
+
+int zolo_counters(const zolo_ctx* c, int64_t* inner, int64_t* gapps) {
+  if (inner) *inner = c->inner_solves;
+  if (gapps) *gapps = c->g_apps;
+  return ZOLO_OK;
+}
+
+int zolo_rr_project(zolo_ctx* c, const double* y, int64_t k, double* at, double* bt) {
+  return guarded(c, [&] {
+    require(k >= 1, "rr_project: empty block");
+    if (c->cx)
+      rr_impl<cd>(*c, y, k, at, bt);
+    else
+      rr_impl<double>(*c, y, k, at, bt);
+  });
+}
+
+int zolo_block_update(zolo_ctx* c, const double* y, int64_t k, const double* q, int64_t kk, double* out) {
+  return guarded(c, [&] {
+    require(c->have_pencil, "block_update: no pencil");
+    if (kk == 0) return;
+    if (c->cx)
+      block_update_impl<cd>(*c, y, k, q, kk, out);
+    else
+      block_update_impl<double>(*c, y, k, q, kk, out);
+  });
+}
+
+int zolo_last_timings(const zolo_ctx* c, double* ms) {
+  for (int i = 0; i < 4; ++i) ms[i] = c->last_ms[i];
+  return ZOLO_OK;
+}
+
+int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int64_t* bw, int64_t* profile) {
+  try {
+    rcm_order(n, rp, ci, perm);
+    if (bw) *bw = bandwidth_under(n, rp, ci, perm);
+    if (profile) *profile = profile_under(n, rp, ci, perm);
+    return ZOLO_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_NUMERICAL;
+  }
+}
+
+int zolo_build_design(const double* gaps, int r, double* design) {
+  try {
+    build_filter_design(gaps, r, design);
+    return ZOLO_OK;
+  } catch (const DesignError& e) {
+    g_create_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_NUMERICAL;
+  }
+}
+
+int zolo_eval_filter(const double* gaps, int r, int64_t npts, const double* x, double* g_out, double* f_out) {
+  try {
+    eval_filter_scalar(gaps, r, npts, x, g_out, f_out);
+    return ZOLO_OK;
+  } catch (const DesignError& e) {
+    g_create_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_NUMERICAL;
+  }
+}
+
+int zolo_uniform_stream(uint64_t seed, int64_t n, double* out) {
+  uniform_stream(seed, n, out);
+  return ZOLO_OK;
+}
+
+int zolo_random_block(int scalar, int64_t n, int64_t k, uint64_t seed, int orthonormalize, double* out) {
+  return random_block(scalar, n, k, seed, orthonormalize != 0, out) ? ZOLO_OK : ZOLO_ERR_NUMERICAL;
+}
+
+}  // extern "C"

@@ -1,0 +1,552 @@
+// Krylov-side kernels of the filter application.
+//
+// Reference map:
+//   apply_b / spmm          sparse.hpp:113-129 (spmv over a dense block), SparsePencil::apply_b :141-144
+//   combine                 filter_engine.hpp:60-80 (constant term + pole-weight combine)
+//   arnoldi (CGS2)          gmres.hpp:128-141 (MGS with one re-orthogonalisation pass)
+//   least_squares           gmres.hpp:58-88 + :142-161 (shifted Hessenberg LS, freeze, happy breakdown)
+//   assemble                gmres.hpp:163-171 + filter_engine.hpp:112-126 (solutions folded into
+//                           the outer partial-fraction combination)
+//   gram / block_gemm       eigensolver.hpp:108-109,190 (Rayleigh-Ritz projections, Q = Y Q~)
+//
+// All reductions are two-stage with a fixed summation order, so results are
+// bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "krylov.cuh"
+
+namespace zolo {
+
+namespace {
+
+constexpr int RT = 256;          // threads per reduction block
+constexpr int RPT = CHUNK / RT;  // rows per thread in a chunk
+
+template <class S>
+__device__ __forceinline__ S warp_sum(S v);
+template <>
+__device__ __forceinline__ double warp_sum<double>(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <>
+__device__ __forceinline__ cd warp_sum<cd>(cd v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+template <class S>
+__global__ void permute_in_kernel(const S* src, int64_t n, S* dst, int64_t ld, const int* perm) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (t >= ld) return;
+  dst[t + c * ld] = (t < n) ? src[perm[t] + c * n] : szero(S());
+}
+
+template <class S>
+__global__ void permute_out_kernel(const S* src, int64_t ld, S* dst, int64_t n, const int* perm) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (t >= n) return;
+  dst[perm[t] + c * n] = src[t + c * ld];
+}
+
+template <class S>
+__global__ void col_norms_kernel(const S* v, int64_t n, int64_t ld, double* out) {
+  __shared__ double red[32];
+  const int64_t c = blockIdx.x;
+  double s = 0.0;
+  for (int64_t t = threadIdx.x; t < n; t += blockDim.x) s += sabs2(v[t + c * ld]);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+    out[c] = sqrt(tot);
+  }
+}
+
+template <class S>
+__global__ void scale_cols_kernel(const S* v, S* out, int64_t ld, const double* norms) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (t >= ld) return;
+  const double nr = norms[c];
+  out[t + c * ld] = nr != 0.0 ? sscale(v[t + c * ld], 1.0 / nr) : szero(S());
+}
+
+template <class S>
+__global__ void apply_b_kernel(int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
+                               const int* act, cd* out) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int a = blockIdx.y;
+  if (t >= ld) return;
+  const int64_t col = act[a];
+  cd s = mk(0.0, 0.0);
+  if (t < n) {
+    if (rp) {
+      S acc = szero(S());
+      for (int q = rp[t]; q < rp[t + 1]; ++q) acc = sadd(acc, smul(vals[q], v[ci[q] + col * ld]));
+      s = to_cd(acc);
+    } else {
+      s = to_cd(v[t + col * ld]);
+    }
+  }
+  out[t + a * ld] = s;
+}
+
+template <class S>
+__global__ void spmm_kernel(int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v, S* out) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (t >= ld) return;
+  S acc = szero(S());
+  if (t < n)
+    for (int q = rp[t]; q < rp[t + 1]; ++q) acc = sadd(acc, smul(vals[q], v[ci[q] + c * ld]));
+  out[t + c * ld] = acc;
+}
+
+struct XPtrs {
+  cd* p[2 * 16];
+};
+
+// filter_engine.hpp:60-80
+template <class S>
+__global__ void combine_kernel(int64_t ld, double c0, const S* v, const int* act, XPtrs xs, const cd* weights, int r,
+                               S* w) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int a = blockIdx.y;
+  if (t >= ld) return;
+  const int64_t col = act[a];
+  S acc = sscale(v[t + col * ld], c0);
+  const int64_t off = t + a * ld;
+  if constexpr (sizeof(S) == sizeof(double)) {
+    for (int p = 0; p < r; ++p) {
+      const cd x = xs.p[p][off];
+      const cd wp = weights[p];
+      acc += 2.0 * (wp.x * x.x - wp.y * x.y);
+    }
+  } else {
+    for (int p = 0; p < r; ++p) {
+      const cd x = xs.p[2 * p][off], xa = xs.p[2 * p + 1][off];
+      const cd wp = weights[p];
+      acc = cadd(acc, cadd(cmul(wp, x), cmul(cconj(wp), xa)));
+    }
+  }
+  w[t + col * ld] = acc;
+}
+
+// ---- CGS2 Arnoldi -------------------------------------------------------
+// K1: partial dots <V_i, w> over a row chunk.
+template <class S>
+__global__ void __launch_bounds__(RT) dots_kernel(int64_t n, int64_t ld, S* const* basis, int m, const S* w,
+                                                  const int* act, S* partial, int nchunk, int hstride) {
+  __shared__ S red[RT / 32][64];
+  const int a = blockIdx.x, chunk = blockIdx.y;
+  const int64_t col = act[a];
+  const int64_t base = static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
+  S wr[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int64_t t = base + j * RT;
+    wr[j] = (t < n) ? w[t + col * ld] : szero(S());
+  }
+  for (int i = 0; i <= m; ++i) {
+    const S* vi = basis[i] + col * ld;
+    S s = szero(S());
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int64_t t = base + j * RT;
+      if (t < n) s = sadd(s, smul(sconj(vi[t]), wr[j]));
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x <= m) {
+    S tot = szero(S());
+    for (int wq = 0; wq < RT / 32; ++wq) tot = sadd(tot, red[wq][threadIdx.x]);
+    partial[(static_cast<int64_t>(a) * nchunk + chunk) * hstride + threadIdx.x] = tot;
+  }
+}
+
+// K2/K3: h = sum_chunks partial_in; w -= V h; then either dots with the new w
+// (partial_out as S) or the squared norm (norm_out as double).
+template <class S, bool DOTS>
+__global__ void __launch_bounds__(RT) update_kernel(int64_t n, int64_t ld, S* const* basis, int m, S* w,
+                                                    const int* act, const S* partial_in, S* partial_out,
+                                                    double* norm_out, int nchunk, int hstride, S* hsave,
+                                                    void* Hmat, int maxit) {
+  __shared__ S hs[64];
+  __shared__ S red[RT / 32][64];
+  const int a = blockIdx.x, chunk = blockIdx.y;
+  const int64_t col = act[a];
+  if (threadIdx.x <= m) {
+    S tot = szero(S());
+    for (int c = 0; c < nchunk; ++c) tot = sadd(tot, partial_in[(static_cast<int64_t>(a) * nchunk + c) * hstride + threadIdx.x]);
+    hs[threadIdx.x] = tot;
+    if (chunk == 0) {
+      if (DOTS) {
+        hsave[static_cast<int64_t>(a) * hstride + threadIdx.x] = tot;
+      } else {
+        // H(i, m) = h1 + h2  (gmres.hpp:138 accumulates both passes)
+        S* H = reinterpret_cast<S*>(Hmat) + col * static_cast<int64_t>(maxit + 1) * maxit;
+        H[threadIdx.x + static_cast<int64_t>(m) * (maxit + 1)] =
+            sadd(hsave[static_cast<int64_t>(a) * hstride + threadIdx.x], tot);
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t base = static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
+  S wr[RPT];
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int64_t t = base + j * RT;
+    wr[j] = (t < n) ? w[t + col * ld] : szero(S());
+  }
+  for (int i = 0; i <= m; ++i) {
+    const S* vi = basis[i] + col * ld;
+    const S h = hs[i];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int64_t t = base + j * RT;
+      if (t < n) wr[j] = ssub(wr[j], smul(h, vi[t]));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int64_t t = base + j * RT;
+    if (t < n) w[t + col * ld] = wr[j];
+  }
+  if (DOTS) {
+    for (int i = 0; i <= m; ++i) {
+      const S* vi = basis[i] + col * ld;
+      S s = szero(S());
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int64_t t = base + j * RT;
+        if (t < n) s = sadd(s, smul(sconj(vi[t]), wr[j]));
+      }
+      s = warp_sum(s);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][i] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x <= m) {
+      S tot = szero(S());
+      for (int wq = 0; wq < RT / 32; ++wq) tot = sadd(tot, red[wq][threadIdx.x]);
+      partial_out[(static_cast<int64_t>(a) * nchunk + chunk) * hstride + threadIdx.x] = tot;
+    }
+  } else {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) s += sabs2(wr[j]);
+    s = warp_sum(s);
+    __shared__ double nred[RT / 32];
+    if ((threadIdx.x & 31) == 0) nred[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int wq = 0; wq < RT / 32; ++wq) tot += nred[wq];
+      norm_out[static_cast<int64_t>(a) * nchunk + chunk] = tot;
+    }
+  }
+}
+
+__global__ void gmres_init_kernel(GmresDev g) {
+  const int c = blockIdx.x, k = threadIdx.x;
+  if (k < g.q) {
+    const int64_t ck = static_cast<int64_t>(c) * g.q + k;
+    cd* G = g.G + ck * (g.maxit + 1);
+    for (int i = 0; i <= g.maxit; ++i) G[i] = mk(i == 0 ? g.beta[c] : 0.0, 0.0);
+    g.res[ck] = 0.0;
+    g.frozen[ck] = 0;
+    g.mlen[ck] = 0;
+  }
+  if (k == 0) {
+    g.mcol[c] = 0;
+    g.happy[c] = 0;
+    g.done[c] = g.beta[c] == 0.0 ? 1 : 0;
+    g.wnorm[c] = 0.0;
+    for (int i = 0; i < g.maxit; ++i) g.Z[static_cast<int64_t>(c) * g.maxit + i] = mk(0.0, 0.0);
+  }
+}
+
+// y = R^{-1} g for the leading mm x mm block (gmres.hpp:81-86)
+__device__ void back_substitute(const cd* R, const cd* G, cd* y, int mm, int maxit) {
+  for (int i = mm - 1; i >= 0; --i) {
+    cd v = G[i];
+    for (int k = i + 1; k < mm; ++k) v = csub(v, cmul(R[static_cast<int64_t>(k) * maxit + i], y[k]));
+    y[i] = cdiv(v, R[static_cast<int64_t>(i) * maxit + i]);
+  }
+}
+
+// One block per active column, one thread per shift.
+template <class S>
+__global__ void least_squares_kernel(const int* act, int m, GmresDev g, const double* norm_partial, int nchunk,
+                                     double tol) {
+  __shared__ double wn_s;
+  __shared__ int done_s, happy_s;
+  const int a = blockIdx.x, k = threadIdx.x;
+  const int col = act[a];
+  const int maxit = g.maxit;
+  S* H = reinterpret_cast<S*>(g.H) + static_cast<int64_t>(col) * (maxit + 1) * maxit;
+  const double beta = g.beta[col];
+  if (k == 0) {
+    double tot = 0.0;
+    for (int c = 0; c < nchunk; ++c) tot += norm_partial[static_cast<int64_t>(a) * nchunk + c];
+    const double wn = sqrt(tot);
+    wn_s = wn;
+    if constexpr (sizeof(S) == sizeof(double))
+      reinterpret_cast<double*>(H)[(m + 1) + static_cast<int64_t>(m) * (maxit + 1)] = wn;
+    else
+      reinterpret_cast<cd*>(H)[(m + 1) + static_cast<int64_t>(m) * (maxit + 1)] = mk(wn, 0.0);
+    happy_s = (wn > 1e-14 * beta) ? 0 : 1;  // gmres.hpp:145-150
+  }
+  __syncthreads();
+  const int mm = m + 1;
+  if (k < g.q) {
+    const int64_t ck = static_cast<int64_t>(col) * g.q + k;
+    if (!g.frozen[ck]) {
+      cd* R = g.R + ck * maxit * maxit;
+      cd* G = g.G + ck * (maxit + 1);
+      cd* ROT = g.ROT + ck * 2 * maxit;
+      // new column m of H + s I, rotated by the stored Givens (gmres.hpp:62-79)
+      cd* rcol = R + static_cast<int64_t>(m) * maxit;  // rows 0..m
+      for (int i = 0; i <= m; ++i) rcol[i] = to_cd(H[i + static_cast<int64_t>(m) * (maxit + 1)]);
+      rcol[m] = cadd(rcol[m], g.shifts[k]);
+      cd below = to_cd(H[(m + 1) + static_cast<int64_t>(m) * (maxit + 1)]);
+      for (int j = 0; j < m; ++j) {
+        const cd c = ROT[2 * j], sn = ROT[2 * j + 1];
+        const cd t0 = rcol[j], t1 = rcol[j + 1];
+        rcol[j] = cadd(cmul(cconj(c), t0), cmul(cconj(sn), t1));
+        rcol[j + 1] = cadd(cmul(mk(-sn.x, -sn.y), t0), cmul(c, t1));
+      }
+      const cd av = rcol[m], bv = below;
+      const double nr = sqrt(cabs2(av) + cabs2(bv));
+      cd c = mk(1.0, 0.0), sn = mk(0.0, 0.0);
+      if (nr != 0.0) {
+        c = mk(av.x / nr, av.y / nr);
+        sn = mk(bv.x / nr, bv.y / nr);
+        rcol[m] = cadd(cmul(cconj(c), av), cmul(cconj(sn), bv));
+        const cd g0 = G[m], g1 = G[m + 1];
+        G[m] = cadd(cmul(cconj(c), g0), cmul(cconj(sn), g1));
+        G[m + 1] = cadd(cmul(mk(-sn.x, -sn.y), g0), cmul(c, g1));
+      }
+      ROT[2 * m] = c;
+      ROT[2 * m + 1] = sn;
+      const cd gm = G[m + 1];
+      const double res = hypot(gm.x, gm.y) / beta;
+      g.res[ck] = res;
+      if (res <= tol) {  // freeze this shift (gmres.hpp:155-156)
+        g.frozen[ck] = 1;
+        back_substitute(R, G, g.Y + ck * maxit, mm, maxit);
+        g.mlen[ck] = mm;
+      }
+    }
+  }
+  __syncthreads();
+  if (k == 0) {
+    int all = 1;
+    for (int s = 0; s < g.q; ++s) all &= g.frozen[static_cast<int64_t>(col) * g.q + s];
+    const int done = all || happy_s || mm >= maxit;
+    done_s = done;
+    g.wnorm[col] = wn_s;
+    g.happy[col] = happy_s;
+    if (done) {
+      g.done[col] = 1;
+      g.mcol[col] = mm;
+    }
+  }
+  __syncthreads();
+  if (!done_s) return;
+  if (k < g.q) {
+    const int64_t ck = static_cast<int64_t>(col) * g.q + k;
+    if (!g.frozen[ck]) {
+      back_substitute(g.R + ck * maxit * maxit, g.G + ck * (maxit + 1), g.Y + ck * maxit, mm, maxit);
+      g.mlen[ck] = mm;
+    }
+  }
+  __syncthreads();
+  // Z_i = sum_k coef_k y_k[i]  (filter_engine.hpp:112-118 folded through gmres.hpp:163-171)
+  for (int i = threadIdx.x; i < mm; i += blockDim.x) {
+    cd z = mk(0.0, 0.0);
+    for (int s = 0; s < g.q; ++s) {
+      const int64_t ck = static_cast<int64_t>(col) * g.q + s;
+      if (i < g.mlen[ck]) z = cadd(z, cscale(g.Y[ck * maxit + i], g.coef[s]));
+    }
+    g.Z[static_cast<int64_t>(col) * maxit + i] = z;
+  }
+}
+
+template <class S>
+__global__ void next_basis_kernel(int64_t ld, const S* w, S* vnext, const int* act, GmresDev g) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int col = act[blockIdx.y];
+  if (t >= ld || g.done[col]) return;
+  const double wn = g.wnorm[col];
+  vnext[t + col * ld] = sscale(w[t + col * ld], 1.0 / wn);
+}
+
+template <class S>
+__global__ void assemble_kernel(int64_t ld, S* const* basis, GmresDev g, const S* vin, S* out) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t c = blockIdx.y;
+  if (t >= ld) return;
+  const int m = g.mcol[c];
+  cd acc = mk(0.0, 0.0);
+  for (int i = 0; i < m; ++i) {
+    const cd z = g.Z[c * g.maxit + i];
+    const cd v = to_cd(basis[i][t + c * ld]);
+    cfma(acc, z, v);
+  }
+  const cd half_v = cscale(to_cd(vin[t + c * ld]), 0.5);
+  if constexpr (sizeof(S) == sizeof(double))
+    reinterpret_cast<double*>(out)[t + c * ld] = acc.x + half_v.x;
+  else
+    reinterpret_cast<cd*>(out)[t + c * ld] = cadd(acc, half_v);
+}
+
+// ---- tall-skinny GEMMs for Rayleigh-Ritz -------------------------------
+constexpr int GB = 16;
+template <class S>
+__global__ void gram_partial_kernel(int64_t n, int64_t ld, const S* y, int64_t k, const S* z, int64_t kk,
+                                    S* partial) {
+  __shared__ S ys[64][GB + 1];
+  __shared__ S zs[64][GB + 1];
+  const int ti = blockIdx.y * GB, tj = blockIdx.z * GB;
+  const int chunk = blockIdx.x;
+  const int tx = threadIdx.x % GB, ty = threadIdx.x / GB;  // 256 threads: output (tx, ty)
+  S acc = szero(S());
+  const int64_t r0 = static_cast<int64_t>(chunk) * CHUNK;
+  const int64_t rend = (r0 + CHUNK < n) ? r0 + CHUNK : n;
+  for (int64_t rb = r0; rb < rend; rb += 64) {
+    for (int e = threadIdx.x; e < 64 * GB; e += 256) {
+      const int rr = e % 64, cc = e / 64;
+      const int64_t t = rb + rr;
+      ys[rr][cc] = (t < n && ti + cc < k) ? y[t + (ti + cc) * ld] : szero(S());
+      zs[rr][cc] = (t < n && tj + cc < kk) ? z[t + (tj + cc) * ld] : szero(S());
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 64; ++rr) acc = sadd(acc, smul(sconj(ys[rr][tx]), zs[rr][ty]));
+    __syncthreads();
+  }
+  if (ti + tx < k && tj + ty < kk) partial[(static_cast<int64_t>(chunk) * k + ti + tx) * kk + tj + ty] = acc;
+}
+
+template <class S>
+__global__ void gram_reduce_kernel(const S* partial, int nchunk, int64_t k, int64_t kk, S* out) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= k * kk) return;
+  const int64_t i = e % k, j = e / k;
+  S s = szero(S());
+  for (int c = 0; c < nchunk; ++c) s = sadd(s, partial[(static_cast<int64_t>(c) * k + i) * kk + j]);
+  out[i + j * k] = s;
+}
+
+template <class S>
+__global__ void block_gemm_kernel(int64_t ld, const S* y, int64_t k, const S* q, int64_t kk, S* out) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t j = blockIdx.y;
+  if (t >= ld) return;
+  S acc = szero(S());
+  for (int64_t i = 0; i < k; ++i) acc = sadd(acc, smul(y[t + i * ld], q[i + j * k]));
+  out[t + j * ld] = acc;
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+template <class S>
+void Krylov<S>::permute_in(cudaStream_t st, const S* src, int64_t n, S* dst, int64_t ld, int64_t k, const int* perm) {
+  if (k > 0) permute_in_kernel<S><<<dim3(blocks_for(ld, 256), k), 256, 0, st>>>(src, n, dst, ld, perm);
+}
+template <class S>
+void Krylov<S>::permute_out(cudaStream_t st, const S* src, int64_t ld, S* dst, int64_t n, int64_t k, const int* perm) {
+  if (k > 0) permute_out_kernel<S><<<dim3(blocks_for(n, 256), k), 256, 0, st>>>(src, ld, dst, n, perm);
+}
+template <class S>
+void Krylov<S>::col_norms(cudaStream_t st, const S* v, int64_t n, int64_t ld, int64_t k, double* out) {
+  if (k > 0) col_norms_kernel<S><<<k, 512, 0, st>>>(v, n, ld, out);
+}
+template <class S>
+void Krylov<S>::scale_cols(cudaStream_t st, const S* v, S* out, int64_t n, int64_t ld, int64_t k, const double* norms) {
+  if (k > 0) scale_cols_kernel<S><<<dim3(blocks_for(ld, 256), k), 256, 0, st>>>(v, out, ld, norms);
+}
+template <class S>
+void Krylov<S>::apply_b(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals,
+                        const S* v, const int* act, int na, cd* out) {
+  if (na > 0) apply_b_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(n, ld, rp, ci, vals, v, act, out);
+}
+template <class S>
+void Krylov<S>::combine(cudaStream_t st, int64_t n, int64_t ld, double c0, const S* v, const int* act, int na,
+                        cd* const* xs, const cd* weights, int r, S* w) {
+  XPtrs p;
+  const int np = sizeof(S) == sizeof(double) ? r : 2 * r;
+  for (int i = 0; i < np; ++i) p.p[i] = xs[i];
+  if (na > 0) combine_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, c0, v, act, p, weights, r, w);
+}
+template <class S>
+void Krylov<S>::arnoldi(cudaStream_t st, int64_t n, int64_t ld, S* const* d_basis, int m, S* w, const int* act,
+                        int na, GmresDev g, double* partial, int nchunk, S* hsave) {
+  if (na <= 0) return;
+  const int hstride = g.maxit + 1;
+  S* p1 = reinterpret_cast<S*>(partial);
+  S* p2 = p1 + static_cast<int64_t>(na) * nchunk * hstride;
+  double* pn = reinterpret_cast<double*>(p1);  // norm partials reuse p1 after K2
+  const dim3 grid(na, nchunk);
+  dots_kernel<S><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p1, nchunk, hstride);
+  update_kernel<S, true><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p1, p2, nullptr, nchunk, hstride, hsave,
+                                              g.H, g.maxit);
+  update_kernel<S, false><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p2, nullptr, pn, nchunk, hstride, hsave,
+                                               g.H, g.maxit);
+}
+template <class S>
+void Krylov<S>::least_squares(cudaStream_t st, const int* act, int na, int m, GmresDev g, const double* partial,
+                              int nchunk, double tol) {
+  if (na > 0) least_squares_kernel<S><<<na, 32, 0, st>>>(act, m, g, partial, nchunk, tol);
+}
+template <class S>
+void Krylov<S>::next_basis(cudaStream_t st, int64_t n, int64_t ld, const S* w, S* vnext, const int* act, int na,
+                           GmresDev g) {
+  if (na > 0) next_basis_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, w, vnext, act, g);
+}
+template <class S>
+void Krylov<S>::assemble(cudaStream_t st, int64_t n, int64_t ld, const S* v0, S* const* d_basis, int nv, GmresDev g,
+                         const S* vin, S* out) {
+  if (nv > 0) assemble_kernel<S><<<dim3(blocks_for(ld, 256), nv), 256, 0, st>>>(ld, d_basis, g, vin, out);
+}
+template <class S>
+void Krylov<S>::gram(cudaStream_t st, int64_t n, int64_t ld, const S* y, int64_t k, const S* z, int64_t kk, S* out,
+                     double* partial) {
+  const int nchunk = static_cast<int>((n + CHUNK - 1) / CHUNK);
+  S* p = reinterpret_cast<S*>(partial);
+  gram_partial_kernel<S><<<dim3(nchunk, blocks_for(k, GB), blocks_for(kk, GB)), 256, 0, st>>>(n, ld, y, k, z, kk, p);
+  gram_reduce_kernel<S><<<blocks_for(k * kk, 256), 256, 0, st>>>(p, nchunk, k, kk, out);
+}
+template <class S>
+void Krylov<S>::block_gemm(cudaStream_t st, int64_t n, int64_t ld, const S* y, int64_t k, const S* q, int64_t kk,
+                           S* out) {
+  if (kk > 0) block_gemm_kernel<S><<<dim3(blocks_for(ld, 256), kk), 256, 0, st>>>(ld, y, k, q, kk, out);
+}
+template <class S>
+void Krylov<S>::spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
+                     int64_t k, S* out) {
+  if (k > 0) spmm_kernel<S><<<dim3(blocks_for(ld, 256), k), 256, 0, st>>>(n, ld, rp, ci, vals, v, out);
+}
+
+void gmres_init(cudaStream_t st, GmresDev g) { gmres_init_kernel<<<g.nv, 32, 0, st>>>(g); }
+
+template struct Krylov<double>;
+template struct Krylov<cd>;
+
+}  // namespace zolo

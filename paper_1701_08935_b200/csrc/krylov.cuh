@@ -1,0 +1,66 @@
+// Host launchers for the Krylov-side kernels (krylov.cu). Every block of
+// vectors lives on the device in the factor ordering (P v), column-major with
+// leading dimension ld = npad; rows n..npad-1 are kept at zero.
+#pragma once
+
+#include "common.cuh"
+
+namespace zolo {
+
+constexpr int CHUNK = 2048;  // rows per block in the column reductions
+
+struct GmresDev {
+  // per column c (n_v) and shift k (q): see krylov.cu
+  int maxit, q, nv;
+  void* H;        // [nv][(maxit+1) * maxit] S, column-major per column
+  cd* R;          // [nv][q][maxit*maxit]
+  cd* G;          // [nv][q][maxit+1]
+  cd* ROT;        // [nv][q][2*maxit]
+  cd* Y;          // [nv][q][maxit]
+  cd* Z;          // [nv][maxit]  folded outer combination coefficients
+  double* res;    // [nv][q]
+  int* frozen;    // [nv][q]
+  int* mlen;      // [nv][q]  length of y_k
+  double* beta;   // [nv]
+  int* mcol;      // [nv]  Krylov dimension of the column
+  int* happy;     // [nv]
+  int* done;      // [nv]
+  double* wnorm;  // [nv]
+  cd* shifts;     // [q]
+  double* coef;   // [q]  1/2 M_outer * 1/2 a_(k/2)
+};
+
+template <class S>
+struct Krylov {
+  static void permute_in(cudaStream_t st, const S* src, int64_t n, S* dst, int64_t ld, int64_t k, const int* perm);
+  static void permute_out(cudaStream_t st, const S* src, int64_t ld, S* dst, int64_t n, int64_t k, const int* perm);
+  static void col_norms(cudaStream_t st, const S* v, int64_t n, int64_t ld, int64_t k, double* out);
+  static void scale_cols(cudaStream_t st, const S* v, S* out, int64_t n, int64_t ld, int64_t k, const double* norms);
+  // out (complex, ld x na) = B * V[:, act] (or V[:, act] when B = I)
+  static void apply_b(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals,
+                      const S* v, const int* act, int na, cd* out);
+  // w[:, act[a]] = c0 v[:, act[a]] + sum_p (real: 2 Re(w_p X_p) | complex: w_p X_p + conj(w_p) Xa_p)
+  static void combine(cudaStream_t st, int64_t n, int64_t ld, double c0, const S* v, const int* act, int na,
+                      cd* const* xs, const cd* weights, int r, S* w);
+  // CGS2 Arnoldi step against basis V_0..V_m (device pointer array)
+  static void arnoldi(cudaStream_t st, int64_t n, int64_t ld, S* const* d_basis, int m, S* w, const int* act,
+                      int na, GmresDev g, double* partial, int nchunk, S* hsave);
+  // incremental shifted Givens LS + freeze / completion bookkeeping
+  static void least_squares(cudaStream_t st, const int* act, int na, int m, GmresDev g, const double* partial,
+                            int nchunk, double tol);
+  static void next_basis(cudaStream_t st, int64_t n, int64_t ld, const S* w, S* vnext, const int* act, int na,
+                         GmresDev g);
+  static void assemble(cudaStream_t st, int64_t n, int64_t ld, const S* v0, S* const* d_basis, int nv, GmresDev g,
+                       const S* vin, S* out);
+  // C (k x kk) = Y^H Z (column-major, ld rows) -- RR projections
+  static void gram(cudaStream_t st, int64_t n, int64_t ld, const S* y, int64_t k, const S* z, int64_t kk, S* out,
+                   double* partial);
+  // out (ld x kk) = Y (ld x k) * Q (k x kk)
+  static void block_gemm(cudaStream_t st, int64_t n, int64_t ld, const S* y, int64_t k, const S* q, int64_t kk,
+                         S* out);
+  // out (ld x k) = M * V (M permuted CSR with S values)
+  static void spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
+                   int64_t k, S* out);
+};
+
+}  // namespace zolo

@@ -1,0 +1,137 @@
+"""GPU parity: the sm_100a path through the C ABI against the golden vectors
+of the unmodified reference and against the C oracle (oracle/liboracle.so).
+
+Tolerances (BASELINE.json north_star / SURVEY.md §8(d)):
+  * apply_g (direct solves only): relative max error <= 1e-11;
+  * filtered block Y: relative Frobenius error <= 1e-9;
+  * report: per-column Krylov dimensions within +-1 of the reference
+    (lock-step batching reorders roundoff, SURVEY.md §7 "GMRES iteration-count
+    parity"), exact counter identities (test_filter_engine.cpp:174-185).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_pencil, load_golden
+
+pytestmark = pytest.mark.gpu
+
+FILTER_CASES = sorted(os.path.basename(p)[7:-4] for p in glob.glob(os.path.join(GOLDEN, "filter_*.npz")))
+
+
+@pytest.fixture(scope="module")
+def zb():
+    import paper_1701_08935_b200 as zb
+
+    return zb
+
+
+def rel_fro(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("name", FILTER_CASES)
+def test_filter_matches_reference_goldens(zb, name):
+    g = load_golden("filter_" + name)
+    cx, r = bool(g["cx"]), int(g["r"])
+    op = zb.FilterOperator(golden_pencil(g), g["design"], r, is_complex=cx)
+    gv = op.apply_g(g["v"])
+    assert np.abs(gv - g["gv"]).max() <= 1e-11 * max(1.0, np.abs(g["gv"]).max())
+    assert (op.inner_solve_count(), op.g_application_count()) == tuple(int(x) for x in g["g_counters"])
+    tol, gmax = float(g["gmres_tol"]), int(g["gmres_max"])
+    if int(g["status"]) == 4:
+        with pytest.raises(zb.GmresError) as ei:
+            op.apply_filter(g["v"], tol, gmax)
+        assert not ei.value.report.all_converged()
+        assert ei.value.report.iterations == gmax
+        return
+    y, rep = op.apply_filter(g["v"], tol, gmax)
+    assert rel_fro(y, g["y"]) <= 1e-9, rel_fro(y, g["y"])
+    assert rep.all_converged()
+    ci = np.array(rep.column_iterations)
+    assert np.abs(ci - g["column_iterations"]).max() <= 1
+    assert rep.operator_applications == ci.sum()
+    assert rep.iterations == ci.max()
+    # test_filter_engine.cpp:174-185 counter identities
+    inner, gapps = op.inner_solve_count(), op.g_application_count()
+    assert gapps - 1 == rep.operator_applications
+    assert inner == (2 if cx else 1) * r * gapps
+
+
+def test_planted_hybrid_equals_dense_oracle(zb):
+    """criterion 6 / test_filter_engine.cpp:145-159 on the GPU."""
+    for name in ("planted30_real", "planted30_cx"):
+        g = load_golden("filter_" + name)
+        op = zb.FilterOperator(golden_pencil(g), g["design"], int(g["r"]), is_complex=bool(g["cx"]))
+        y, _ = op.apply_filter(g["v"])
+        assert np.linalg.norm(y - g["dense_oracle"]) <= 1e-8 * np.linalg.norm(g["v"])
+
+
+def test_diag_filter_keeps_inside_kills_outside(zb):
+    """test_filter_engine.cpp:114-130."""
+    g = load_golden("filter_diag10")
+    design = g["design"]
+    op = zb.FilterOperator(golden_pencil(g), design, 3)
+    y, rep = op.apply_filter(np.eye(10, order="F"))
+    a, b, delta0 = design[0], design[1], design[14]
+    d = np.arange(1, 11, dtype=float)
+    for k in range(10):
+        expect = np.zeros(10)
+        if a < d[k] < b:
+            expect[k] = 1.0
+        assert np.abs(y[:, k] - expect).max() <= delta0 + 100 * 1e-12
+
+
+def test_zero_pivot_reports_index(zb):
+    """test_sparse.cpp:236-245 via a one-pole design at sigma = 0."""
+    g = load_golden("solve_zeropivot")
+    design = np.zeros(zb.design_len(1))
+    design[19] = 0.0  # inner pole (0, 0)
+    design[20] = 0.0
+    design[21] = 1.0  # weight
+    design[17] = 1.0  # outer M
+    design[24] = 1.0  # outer_pf
+    design[26] = 1.0  # outer.c -> shifts +-i
+    with pytest.raises(zb.FactorizationError) as ei:
+        zb.FilterOperator(golden_pencil(g), design, 1, is_complex=False)
+    assert ei.value.pivot_index == 0
+
+
+def test_zero_column_and_determinism(zb):
+    g = load_golden("filter_zero_column")
+    op = zb.FilterOperator(golden_pencil(g), g["design"], int(g["r"]))
+    y1, rep1 = op.apply_filter(g["v"])
+    y2, rep2 = op.apply_filter(g["v"])
+    assert rep1.column_iterations[1] == 0
+    assert np.abs(y1[:, 1]).max() == 0.0
+    assert (y1 == y2).all()  # bitwise reproducible (fixed-order reductions)
+    assert rel_fro(y1, g["y"]) <= 1e-9
+
+
+def test_cfg1_full_size_against_reference(zb):
+    """BASELINE config 1 at full size (N=4096, n_v=48, r=4) vs the reference
+    itself (oracle/_ref) when it travelled with the repo, else the C oracle."""
+    import oracle
+    from pencils import stencil_2d, to_csr
+
+    s2 = stencil_2d(64)
+    pen = (4096, to_csr(s2, False), None)
+    i = np.arange(1, 65)
+    lam = np.sort((4 * np.sin(i[:, None] * np.pi / 130) ** 2 + 4 * np.sin(i[None, :] * np.pi / 130) ** 2).ravel())
+    gaps = [-np.inf, lam[0], lam[31], lam[32]]
+    v = zb.random_block(4096, 48, 1, cx=False, orthonormalize=True)
+    from paper_1701_08935_b200.design import build_filter_design
+
+    design = build_filter_design(gaps, 4)
+    op = zb.FilterOperator(pen, design, 4)
+    y, rep = op.apply_filter(v)
+    if oracle.Reference.available():
+        ref = oracle.Reference().apply_filter(pen, False, gaps, 4, v, threads=os.cpu_count() or 1)
+        yr, cols = ref["y"], ref["column_iterations"]
+    else:
+        o = oracle.Oracle().operator(pen, False, design, 4).apply_filter(v)
+        yr, cols = o["y"], o["column_iterations"]
+    assert rel_fro(y, yr) <= 1e-9
+    assert np.abs(np.array(rep.column_iterations) - cols).max() <= 1
