@@ -1,0 +1,344 @@
+"""Benchmark of the B200 Zolotarev filter path (BASELINE.json metric:
+filtered vectors/s, all poles applied).
+
+Workload (N=1): BASELINE config 2 -- 3D 7-point Laplacian on 32^3 (N=32768)
++ U[0,1] potential, SPD 7-point mass matrix B, real float64, p=8 poles
+(r=4 factorizations), n_v=96, gmres_tol 1e-12, gmres_max 50, window of 64
+interior eigenvalues near 6 (paper_1701_08935_b200/configs.py).
+
+A step = one FilterOperator::apply_filter (filter_engine.hpp:86-155) of the
+whole n_v-column block: 2r outer shifts by lock-step multi-shift GMRES on
+G, every G application = r shifted band LU solves + B SpMM. The r band
+factorizations are setup (outside the timed region, reported separately).
+
+  value : device-resident block, CUDA events on the library stream, K steps.
+  e2e   : the public host API (zolo_apply_filter) from pinned host memory,
+          H2D of V and D2H of Y inside the timed region.
+Multi-GPU (torchrun): columns are independent (one Krylov basis per column,
+filter_engine.hpp:109-111), so every rank filters its own n_v-column block
+with no data-path collective -- weak scaling; value = N * n_v / max-rank time.
+--impl reference: the reference's own CPU FilterOperator (oracle/_ref,
+compiled from /root/reference) on the host cores, bounded column sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "filtered vectors/s (all poles applied)"
+UNIT = "vectors/s"
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    out = {}
+    try:
+        out.update(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))))
+    except (OSError, ValueError):
+        pass
+    try:
+        fp = json.load(open(os.path.join(REPO, "profiles", "fp64_peak_r01.json")))
+        out["fp64_tflops"] = max(fp["dfma_tflops"], fp["dmma_m8n8k4_tflops"])
+    except (OSError, ValueError, KeyError):
+        pass
+    return out
+
+
+def band_triangle_entries(n, bw):
+    """Entries of a strictly triangular band of half-bandwidth bw: sum_i min(i, bw)."""
+    if bw >= n:
+        return n * (n - 1) // 2
+    return bw * n - bw * (bw + 1) // 2
+
+
+def envelope_entries(pencil):
+    """profile_under(RCM) of the pattern of A - iB (rcm.hpp:133-147)."""
+    import scipy.sparse as sp
+
+    import paper_1701_08935_b200 as zb
+
+    n, a, b = pencil
+    am = sp.csr_matrix((np.ones(len(a[1])), a[1], a[0]), shape=(n, n))
+    bm = sp.identity(n) if b is None else sp.csr_matrix((np.ones(len(b[1])), b[1], b[0]), shape=(n, n))
+    u = (am + bm).tocsr()
+    u.sort_indices()
+    _, _, prof = zb.rcm(n, u.indptr.astype(np.int64), u.indices.astype(np.int64))
+    return prof
+
+
+def workload(name):
+    from paper_1701_08935_b200 import configs
+
+    pen, cx, gaps, r, nv, nl = configs.config(name)
+    return pen, cx, gaps, r, nv, nl
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU path (oracle/_ref)."""
+    if rank != 0:
+        return
+    import oracle
+    import paper_1701_08935_b200 as zb
+
+    pen, cx, gaps, r, nv, nl = workload(args.config)
+    cores = os.cpu_count() or 1
+    if not oracle.Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libzoloref.so not built"}))
+        return
+    ref = oracle.Reference()
+    op = ref.operator(pen, cx, gaps, r, threads=cores)
+    k = min(nv, cores)
+    v = zb.random_block(pen[0], nv, 1, cx=cx, orthonormalize=True)[:, :k]
+    for _ in range(args.warmup):
+        op.apply_filter(v)
+    secs = []
+    for _ in range(args.steps):
+        _, it, s = op.apply_filter(v)
+        secs.append(s)
+    t = sum(secs) / len(secs)
+    value = k / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (reference CPU FilterOperator, {k}-column sample of n_v={nv})",
+                   "N": int(pen[0]), "n_v": nv, "r": r, "gmres_tol": 1e-12},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"apply_filter on {k} of {nv} columns, {cores} threads; factorization "
+                                   f"{op.t_factor:.1f} s excluded"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "t_factor_s": op.t_factor,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(pen, cx, gaps, r, nv):
+    """Reference CPU path on a bounded sample (rank 0, N=1 only)."""
+    import oracle
+    import paper_1701_08935_b200 as zb
+
+    cores = os.cpu_count() or 1
+    if not oracle.Reference.available():
+        return None
+    op = oracle.Reference().operator(pen, cx, gaps, r, threads=cores)
+    k = min(nv, cores)
+    v = zb.random_block(pen[0], nv, 1, cx=cx, orthonormalize=True)[:, :k]
+    _, it, s = op.apply_filter(v)
+    return {"value": k / s, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"reference FilterOperator::apply_filter on {k} of {nv} columns ({cores} threads, "
+                      f"{s:.1f} s); factorization {op.t_factor:.1f} s excluded"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_info()
+
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1701_08935_b200 as zb
+    from paper_1701_08935_b200.design import build_filter_design
+
+    pen, cx, gaps, r, nv, nl = workload(args.config)
+    n = int(pen[0])
+    design = build_filter_design(gaps, r)
+    op = zb.FilterOperator(pen, design, r, is_complex=cx, device=local)
+    t_factor_ms = op.last_timings()["factor_ms"]
+    bw = op.factor_profile()[0]["bandwidth"]
+
+    # each rank: its own n_v-column block (columns are independent units)
+    v = zb.random_block(n, nv, 1 + rank, cx=cx, orthonormalize=True)
+    dt = torch.complex128 if cx else torch.float64
+    dv = torch.from_numpy(np.ascontiguousarray(v.T)).to(device=f"cuda:{local}", dtype=dt)  # (nv, n) = column-major
+    dy = torch.empty_like(dv)
+    torch.cuda.synchronize()
+
+    def step():
+        return op.apply_filter_device(dv.data_ptr(), dy.data_ptr(), nv)
+
+    for _ in range(args.warmup):
+        step()
+    # timed region: inputs (factors 3.4 GB) are larger than L2, no flush needed
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    op.timer_start()
+    trsm_ms = 0.0
+    trsm_launches = 0
+    kernel_launches = 0
+    opapps = 0
+    iters = []
+    for _ in range(args.steps):
+        rep = step()
+        tm = op.last_timings()
+        trsm_ms += tm["trsm_ms"]
+        trsm_launches += tm["trsm_launches"]
+        kernel_launches += tm["kernel_launches"]
+        opapps += tm["operator_applications"]
+        iters.append(rep.iterations)
+    total_ms = op.timer_stop()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if ws > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * nv / (ms_per_step / 1e3)
+
+    # e2e: public host API, pinned host buffers, H2D + D2H inside the timed region
+    dtn = np.complex128 if cx else np.float64
+    hv = torch.from_numpy(np.ascontiguousarray(v.T)).pin_memory()
+    hy = torch.empty_like(hv).pin_memory()
+    vh = hv.numpy().T  # column-major view over pinned memory
+    yh = hy.numpy().T
+    import ctypes as C
+
+    def e2e_step():
+        rep = zb._Report()
+        cols = np.zeros(nv, dtype=np.int64)
+        rep.column_iterations = cols.ctypes.data_as(C.POINTER(C.c_int64))
+        st = zb.lib().zolo_apply_filter(op._h, C.c_void_p(hv.data_ptr()), C.c_void_p(hy.data_ptr()), nv, 1e-12, 50,
+                                        C.byref(rep))
+        zb._check(op._h, st)
+
+    e2e_step()
+    if ws > 1:
+        torch.distributed.barrier()
+    op.timer_start()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_ms = op.timer_stop()
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = ws * nv / (e2e_ms / args.steps / 1e3)
+    esize = 16 if cx else 8
+    assert np.isfinite(yh).all()
+
+    # roofline of the dominant kernel (the wavefront triangular solve)
+    peaks = load_peaks()
+    # factor nnz = the RCM envelope (profile) of the pattern of A - iB: unpivoted
+    # elimination fills exactly the envelope (band_factor.hpp:158-177 skips the rest)
+    nnz_l = envelope_entries(pen)
+    nnz_u = nnz_l + n
+    chains_per_pole = 2 if cx else 1
+    trsm_flops = opapps * r * chains_per_pole * 8.0 * (nnz_l + nnz_u)  # all launches of the K steps
+    achieved = trsm_flops / (trsm_ms * 1e-3) / 1e12 if trsm_ms > 0 else 0.0
+    peak = peaks.get("fp64_tflops")
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(REPO, "profiles", "trsm_traffic.json"))).get("bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128" if cx else "f64", "data": "synthetic (seeded generator, BASELINE config shape)",
+        "config": {"workload": f"{args.config}: 3D 7-point Laplacian 32^3 + U[0,1] potential, SPD mass B, N={n}, "
+                               f"r={r} (p={2 * r} poles), n_v={nv}, gmres_tol=1e-12, 64-eigenvalue window",
+                   "N": n, "n_v": nv, "r": r, "band_half_width": bw, "l2": "factors > L2 (no flush needed)",
+                   "parallelism": f"columns x{ws} (weak)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * nv * esize,
+                "d2h_bytes_per_step": n * nv * esize},
+        "gpu_launches": int(kernel_launches),
+        "roofline": {"bound": "fp64", "kernel": "trsm_kernel (wavefront block-band solve)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if peak else None, "traffic": traffic,
+                     "peak_source": "measured FP64 (tools/fp64_peak.cu, DMMA = DFMA on B200; "
+                                    "MEASURED_PEAKS.json has no FP64 figure)",
+                     "algorithmic": "8 flops per complex MAC x (nnz(L)+nnz(U)) of the band per column per pole "
+                                    "per G application",
+                     "trsm_share_of_step": trsm_ms / total_ms if total_ms else None,
+                     "trsm_launches": trsm_launches},
+        "clocks": clk,
+        "t_factor_ms": t_factor_ms,
+        "gmres_iterations": iters,
+    }
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(pen, cx, gaps, r, nv)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

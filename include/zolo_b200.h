@@ -145,8 +145,15 @@ int zolo_block_update(zolo_ctx* ctx, const double* y, int64_t k, const double* q
 /* --- timing of the last device call (CUDA events on the context stream) - */
 /* ms[0] = last apply_filter device time, ms[1] = last factorize device time,
  * ms[2] = solve-kernel time summed over the last apply_filter,
- * ms[3] = number of solve-kernel launches in the last apply_filter. */
+ * ms[3] = number of solve-kernel launches in the last apply_filter,
+ * ms[4] = kernel launches of the last apply_filter (all kernels),
+ * ms[5] = operator applications (sum of active columns) of the last apply_filter,
+ * ms[6..7] reserved. ms must hold 8 doubles. */
 int zolo_last_timings(const zolo_ctx* ctx, double* ms);
+
+/* Device timer on the context stream: op 0 records the start event, op 1
+ * records the stop event, waits for it and returns the elapsed ms. */
+int zolo_timer(zolo_ctx* ctx, int op, double* ms);
 
 /* --- host-only helpers (no GPU needed) ---------------------------------- */
 /* reorder_rcm (rcm.hpp:69-115) of a structurally symmetric pattern;

@@ -168,6 +168,10 @@ class Reference(_Lib):
                     iterations=int(it[0]), operator_applications=int(ops[0]), inner_solves=int(cnt[0]),
                     g_applications=int(cnt[1]), t_factor=float(sec[0]), t_filter=float(sec[1]))
 
+    def operator(self, pencil, cx, gaps, r, threads=0):
+        """Persistent reference FilterOperator<S> (factorized once)."""
+        return RefOperator(self, pencil, cx, gaps, r, threads)
+
     def rayleigh_ritz(self, pencil, cx, y):
         args, keep = _csr_args(pencil, cx)
         y = _as_f(y, cx)
@@ -213,6 +217,40 @@ class Reference(_Lib):
         self._check(self.lib.zr_dense_filter_oracle(C.c_int(int(cx)), _I64(n), _ptr(a), _ptr(b), _ptr(g),
                                                     C.c_int(r), _I64(v.shape[1]), _ptr(v), _ptr(out), _ptr(lam)))
         return out, lam
+
+
+class RefOperator:
+    """The reference's own FilterOperator<S> (oracle/_ref), for timing."""
+
+    def __init__(self, ref, pencil, cx, gaps, r, threads):
+        self.ref = ref
+        self.cx = bool(cx)
+        self.n = int(pencil[0])
+        args, self._keep = _csr_args(pencil, cx)
+        g = np.asarray(gaps, dtype=np.float64)
+        tf = np.zeros(1)
+        ref.lib.zr_op_create.restype = _P
+        self.h = ref.lib.zr_op_create(C.c_int(int(cx)), _I64(args[0]), *args[1:], _ptr(g), C.c_int(r),
+                                      C.c_int(threads), _ptr(tf))
+        if not self.h:
+            raise RuntimeError("reference: " + ref.lib.zr_last_error().decode())
+        self.t_factor = float(tf[0])
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.zr_op_free(_P(self.h))
+            self.h = None
+
+    def apply_filter(self, v, gmres_tol=1e-12, gmres_max=50):
+        v = _as_f(v, self.cx)
+        y = np.zeros_like(v)
+        it = np.zeros(1, dtype=np.int64)
+        sec = np.zeros(1)
+        st = self.ref.lib.zr_op_apply_filter(_P(self.h), _D(gmres_tol), _I64(gmres_max), _I64(self.n),
+                                             _I64(v.shape[1]), _ptr(v), _ptr(y), _ptr(it), _ptr(sec))
+        if st != 0:
+            raise RuntimeError("reference: " + self.ref.lib.zr_last_error().decode())
+        return y, int(it[0]), float(sec[0])
 
 
 class Oracle(_Lib):

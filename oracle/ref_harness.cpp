@@ -294,6 +294,66 @@ int zr_apply_filter(int cx, int64_t n, const int64_t* arp, const int64_t* aci, c
   });
 }
 
+/// Persistent reference operator (factorize once, apply many times) for the
+/// timed CPU baseline: FilterOperator<S> built with `threads` workers.
+struct ZrOp {
+  int cx;
+  void* op;
+};
+
+void* zr_op_create(int cx, int64_t n, const int64_t* arp, const int64_t* aci, const double* av,
+                   const int64_t* brp, const int64_t* bci, const double* bv, const double* gaps, int r,
+                   int threads, double* t_factor) {
+  ZrOp* h = nullptr;
+  const int st = guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    h = new ZrOp{cx, nullptr};
+    if (cx)
+      h->op = new FilterOperator<Complex>(make_pencil<Complex>(n, arp, aci, av, brp, bci, bv),
+                                          build_filter_design(window_of(gaps), r), threads);
+    else
+      h->op = new FilterOperator<double>(make_pencil<double>(n, arp, aci, av, brp, bci, bv),
+                                         build_filter_design(window_of(gaps), r), threads);
+    if (t_factor)
+      *t_factor = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+  if (st != 0) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+void zr_op_free(void* p) {
+  ZrOp* h = static_cast<ZrOp*>(p);
+  if (!h) return;
+  if (h->cx)
+    delete static_cast<FilterOperator<Complex>*>(h->op);
+  else
+    delete static_cast<FilterOperator<double>*>(h->op);
+  delete h;
+}
+
+/// apply_filter on a persistent operator; seconds = steady_clock wall time.
+int zr_op_apply_filter(void* p, double gmres_tol, int64_t gmres_max, int64_t n, int64_t k, const double* v,
+                       double* y, int64_t* iters, double* seconds) {
+  ZrOp* h = static_cast<ZrOp*>(p);
+  return guarded([&] {
+    const auto run = [&](auto* op, auto tag) {
+      using S = decltype(tag);
+      const auto t0 = std::chrono::steady_clock::now();
+      auto [out, rep] = op->apply_filter(load_block<S>(n, k, v), gmres_tol, static_cast<std::size_t>(gmres_max));
+      *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (y) store_block(out, y);
+      if (iters) *iters = static_cast<int64_t>(rep.iterations);
+    };
+    if (h->cx)
+      run(static_cast<FilterOperator<Complex>*>(h->op), Complex{});
+    else
+      run(static_cast<FilterOperator<double>*>(h->op), double{});
+  });
+}
+
 /// rayleigh_ritz (eigensolver.hpp:105-148). ritz has room for k values, q for
 /// k*k entries; *kept receives the number of Ritz pairs returned.
 int zr_rayleigh_ritz(int cx, int64_t n, const int64_t* arp, const int64_t* aci, const double* av,

@@ -130,6 +130,7 @@ def lib():
         L.zolo_rr_project.argtypes = [P, P, I64, P, P]
         L.zolo_block_update.argtypes = [P, P, I64, P, I64, P]
         L.zolo_last_timings.argtypes = [P, P]
+        L.zolo_timer.argtypes = [P, C.c_int, P]
         L.zolo_rcm.argtypes = [I64, P, P, P, P, P]
         L.zolo_random_block.argtypes = [C.c_int, I64, I64, C.c_uint64, C.c_int, P]
         L.zolo_uniform_stream.argtypes = [C.c_uint64, I64, P]
@@ -329,9 +330,18 @@ class FilterOperator:
         return out
 
     def last_timings(self):
-        ms = np.zeros(4)
+        ms = np.zeros(8)
         lib().zolo_last_timings(self._h, _ptr(ms))
-        return dict(filter_ms=ms[0], factor_ms=ms[1], trsm_ms=ms[2], trsm_launches=int(ms[3]))
+        return dict(filter_ms=ms[0], factor_ms=ms[1], trsm_ms=ms[2], trsm_launches=int(ms[3]),
+                    kernel_launches=int(ms[4]), operator_applications=int(ms[5]))
+
+    def timer_start(self):
+        _check(self._h, lib().zolo_timer(self._h, 0, None))
+
+    def timer_stop(self) -> float:
+        ms = np.zeros(1)
+        _check(self._h, lib().zolo_timer(self._h, 1, _ptr(ms)))
+        return float(ms[0])
 
     def factor_profile(self):
         return [dict(bandwidth=s.bandwidth, stored_entries=s.stored_entries, min_pivot_ratio=s.min_pivot_ratio)

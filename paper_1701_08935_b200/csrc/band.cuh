@@ -11,10 +11,16 @@
 //   Ut[j][d]  = block (j-d, j) of U,  d = 1..J   (slot d = 0 unused)
 //   DinvL[i]  = inverse of the unit lower triangle of the diagonal block
 //   DinvU[i]  = inverse of its upper triangle
+//   MF/MB/MFH/MBH[i] = the next-neighbour couplings premultiplied by the
+//               diagonal inverse (see trsm below), so that the critical chain
+//               of a sweep is one tile product per block row
 //
 // J = ceil(bw / TILE) is the block half-bandwidth; rows beyond n are padded
-// with identity rows so every tile is full. Each tile is TILE*TILE
-// contiguous complex values, column-major.
+// with identity rows so every tile is full. Elimination without pivoting
+// never fills outside the envelope of the (symmetric) pattern, so block row i
+// only holds dl[i] = i - (first nonzero block column of row i) off-diagonal
+// L tiles, and block column i of U the same count: all other tiles are exact
+// zeros and are skipped by the factorization and the solves.
 #pragma once
 
 #include "common.cuh"
@@ -22,11 +28,12 @@
 namespace zolo {
 
 struct BandGeom {
-  int64_t n = 0;     // matrix order
-  int64_t npad = 0;  // nbk * TILE
-  int nbk = 0;       // block rows
-  int J = 0;         // block half-bandwidth
-  int64_t bw = 0;    // scalar half-bandwidth
+  int64_t n = 0;           // matrix order
+  int64_t npad = 0;        // nbk * TILE
+  int nbk = 0;             // block rows
+  int J = 0;               // block half-bandwidth (max over rows of dl)
+  int64_t bw = 0;          // scalar half-bandwidth
+  const int* dl = nullptr; // device: off-diagonal tiles per block row (envelope)
   size_t tiles_per_array() const { return static_cast<size_t>(nbk) * (J + 1); }
 };
 
@@ -35,13 +42,17 @@ struct FactorTiles {
   cd* Ut = nullptr;
   cd* DinvL = nullptr;
   cd* DinvU = nullptr;
+  cd* MF = nullptr;   // DinvL[i] L(i,i-1)          (forward L sweep)
+  cd* MB = nullptr;   // DinvU[i] U(i,i+1)          (backward U sweep)
+  cd* MFH = nullptr;  // U(i-1,i) DinvU[i]  (used as ^H, forward U^H sweep)
+  cd* MBH = nullptr;  // L(i+1,i) DinvL[i]  (used as ^H, backward L^H sweep)
 };
 
 __host__ __device__ inline size_t lt_off(int i, int d, int J) {
   return (static_cast<size_t>(i) * (J + 1) + d) * TT;
 }
 
-// Triangular-solve traversal kinds (see trsm.cu).
+// Triangular-solve traversal kinds (see band.cu).
 enum SweepMode : int {
   FWD_L = 0,   // L y = b           (solve, band_factor.hpp:62-69)
   BWD_U = 1,   // U x = y           (solve, band_factor.hpp:71-80)
@@ -50,15 +61,16 @@ enum SweepMode : int {
 };
 
 struct Chain {
-  const cd* off;    // Lt or Ut array of the pole
-  const cd* dinv;   // DinvL or DinvU of the pole
-  const cd* src;    // right-hand side (ld x ncols), read once per block row
-  cd* dst;          // solution (ld x ncols), written in place
+  const cd* off;   // Lt or Ut array of the pole
+  const cd* dinv;  // DinvL or DinvU of the pole
+  const cd* m;     // MF / MB / MFH / MBH of the pole
+  const cd* src;   // right-hand side (ld x ncols), read once per block row
+  cd* dst;         // solution (ld x ncols), written in place
+  cd* cbuf;        // helper -> owner partial solutions c_i (ld x ncols)
   int mode;
   int pad;
 };
 
-// Host launchers (band.cu)
 struct FactorDevState {
   int* fail_index;                    // first rejected pivot (device, -1 = none)
   unsigned long long* min_ratio_bits; // min |pivot|/||row|| as double bits
@@ -68,10 +80,12 @@ void factor_scatter(cudaStream_t st, const BandGeom& g, const FactorTiles& f, in
                     const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
                     double sig_im, double* row_norm);
 void factor_run(cudaStream_t st, const BandGeom& g, const FactorTiles& f, const double* row_norm,
-                FactorDevState ds);
+                FactorDevState ds, int cx);
 
-// One launch covers nchains x ngroups independent wavefront pipelines.
-void trsm_launch(cudaStream_t st, const BandGeom& g, const Chain* d_chains, int nchains, int ncols, int64_t ld,
-                 int* flags, int epoch, int* task_counter, int fwd, int num_sms);
+// One launch covers nchains x ngroups independent pipelines (owner + helpers).
+// Returns the number of resident CTAs needed (error if owners do not fit).
+int trsm_launch(cudaStream_t st, const BandGeom& g, const Chain* d_chains, int nchains, int ncols, int64_t ld,
+                unsigned long long* prog, int* flags_c, int epoch, int* counter, int fwd, int num_sms,
+                unsigned long long* trace = nullptr);
 
 }  // namespace zolo

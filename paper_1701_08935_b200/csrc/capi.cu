@@ -16,6 +16,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -126,8 +127,11 @@ struct zolo_ctx {
   // solve workspace
   int64_t ncap = 0;  // columns the workspace is sized for
   DevMem vin_orig, vin, vout, w, bbuf, chains_fwd, chains_bwd, flags, counter;
-  std::vector<std::unique_ptr<DevMem>> xbuf;
-  int64_t flags_cap = 0;
+  std::vector<std::unique_ptr<DevMem>> xbuf, cbuf;
+  DevMem dl_d, trace_buf;
+  int64_t env_tiles = 0;
+  bool trace_done = false;
+  int64_t flags_cap = 0, prog_cap = 0;
   int epoch = 0;
 
   // GMRES state
@@ -139,7 +143,8 @@ struct zolo_ctx {
   int* done_h = nullptr;
 
   int64_t inner_solves = 0, g_apps = 0;
-  double last_ms[4] = {0, 0, 0, 0};
+  double last_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaEvent_t tev0 = nullptr, tev1 = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
 
   size_t es() const { return cx ? 16 : 8; }
@@ -278,7 +283,27 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
   g.nbk = static_cast<int>((n + TILE - 1) / TILE);
   g.npad = static_cast<int64_t>(g.nbk) * TILE;
   g.bw = bw;
-  g.J = static_cast<int>((bw + TILE - 1) / TILE);
+  // envelope per block row: dl[i] = i - first nonzero block column (no fill
+  // outside the envelope under unpivoted elimination)
+  {
+    std::vector<int> first(g.npad);
+    for (int64_t t = 0; t < g.npad; ++t) first[t] = static_cast<int>(t);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = u.rp[i]; k < u.rp[i + 1]; ++k) first[pos[i]] = std::min(first[pos[i]], pos[u.ci[k]]);
+    std::vector<int> dl(g.nbk);
+    int jmax = 0;
+    for (int b = 0; b < g.nbk; ++b) {
+      int f = first[static_cast<int64_t>(b) * TILE];
+      for (int q = 1; q < TILE; ++q) f = std::min(f, first[static_cast<int64_t>(b) * TILE + q]);
+      dl[b] = b - f / TILE;
+      jmax = std::max(jmax, dl[b]);
+    }
+    g.J = jmax;
+    upload(c.dl_d, dl, c.st);
+    g.dl = c.dl_d.as<int>();
+    c.env_tiles = 0;
+    for (int b = 0; b < g.nbk; ++b) c.env_tiles += dl[b];
+  }
   c.geom = g;
 
   // permuted union entries for the scatter
@@ -317,7 +342,9 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
   // tiles for r poles
   const int r = c.r;
   const size_t per_array = g.tiles_per_array() * TT;
-  const size_t per_pole = 2 * per_array + 2 * static_cast<size_t>(g.nbk) * TT;  // complex entries
+  const size_t per_diag = static_cast<size_t>(g.nbk) * TT;
+  const int n_m = c.cx ? 4 : 2;                                // coupling tile arrays
+  const size_t per_pole = 2 * per_array + (2 + n_m) * per_diag;  // complex entries
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   const size_t need = per_pole * r * sizeof(cd);
@@ -335,7 +362,13 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     c.tiles[j].Lt = p;
     c.tiles[j].Ut = p + per_array;
     c.tiles[j].DinvL = p + 2 * per_array;
-    c.tiles[j].DinvU = p + 2 * per_array + static_cast<size_t>(g.nbk) * TT;
+    c.tiles[j].DinvU = p + 2 * per_array + per_diag;
+    c.tiles[j].MF = p + 2 * per_array + 2 * per_diag;
+    c.tiles[j].MB = p + 2 * per_array + 3 * per_diag;
+    if (c.cx) {
+      c.tiles[j].MFH = p + 2 * per_array + 4 * per_diag;
+      c.tiles[j].MBH = p + 2 * per_array + 5 * per_diag;
+    }
   }
   // fail index (int, init -1) and min ratio bits (init +inf)
   std::vector<unsigned long long> fs(2 * r);
@@ -364,7 +397,7 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     FactorDevState ds;
     ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
     ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
-    factor_run(ps, g, c.tiles[j], rn, ds);
+    factor_run(ps, g, c.tiles[j], rn, ds, c.cx);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c.ev2, ps));
     CK(cudaStreamWaitEvent(c.st, c.ev2, 0));
@@ -408,21 +441,29 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   c.bbuf.ensure(sizeof(cd) * ld * nc);
   const int nch = c.nchains();
   while (static_cast<int>(c.xbuf.size()) < nch) c.xbuf.emplace_back(new DevMem());
-  for (int i = 0; i < nch; ++i) c.xbuf[i]->ensure(sizeof(cd) * ld * nc);
+  while (static_cast<int>(c.cbuf.size()) < nch) c.cbuf.emplace_back(new DevMem());
+  for (int i = 0; i < nch; ++i) {
+    c.xbuf[i]->ensure(sizeof(cd) * ld * nc);
+    c.cbuf[i]->ensure(sizeof(cd) * ld * nc);
+  }
   std::vector<Chain> fwd(nch), bwd(nch);
   for (int p = 0; p < c.r; ++p) {
     const FactorTiles& t = c.tiles[p];
+    const cd* b = c.bbuf.as<cd>();
     if (c.cx) {
       cd* x = c.xbuf[2 * p]->as<cd>();
       cd* xa = c.xbuf[2 * p + 1]->as<cd>();
-      fwd[2 * p] = Chain{t.Lt, t.DinvL, c.bbuf.as<cd>(), x, FWD_L, 0};
-      bwd[2 * p] = Chain{t.Ut, t.DinvU, x, x, BWD_U, 0};
-      fwd[2 * p + 1] = Chain{t.Ut, t.DinvU, c.bbuf.as<cd>(), xa, FWD_UH, 0};
-      bwd[2 * p + 1] = Chain{t.Lt, t.DinvL, xa, xa, BWD_LH, 0};
+      cd* cb = c.cbuf[2 * p]->as<cd>();
+      cd* cba = c.cbuf[2 * p + 1]->as<cd>();
+      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.MF, b, x, cb, FWD_L, 0};
+      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.MB, x, x, cb, BWD_U, 0};
+      fwd[2 * p + 1] = Chain{t.Ut, t.DinvU, t.MFH, b, xa, cba, FWD_UH, 0};
+      bwd[2 * p + 1] = Chain{t.Lt, t.DinvL, t.MBH, xa, xa, cba, BWD_LH, 0};
     } else {
       cd* x = c.xbuf[p]->as<cd>();
-      fwd[p] = Chain{t.Lt, t.DinvL, c.bbuf.as<cd>(), x, FWD_L, 0};
-      bwd[p] = Chain{t.Ut, t.DinvU, x, x, BWD_U, 0};
+      cd* cb = c.cbuf[p]->as<cd>();
+      fwd[p] = Chain{t.Lt, t.DinvL, t.MF, b, x, cb, FWD_L, 0};
+      bwd[p] = Chain{t.Ut, t.DinvU, t.MB, x, x, cb, BWD_U, 0};
     }
   }
   upload(c.chains_fwd, fwd, c.st);
@@ -430,8 +471,11 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   const int64_t ngroups = (nc + CG - 1) / CG;
   const int64_t nflags = static_cast<int64_t>(nch) * ngroups * c.geom.nbk;
   if (nflags > c.flags_cap) {
-    c.flags.ensure(sizeof(int) * nflags);
-    CK(cudaMemsetAsync(c.flags.p, 0, sizeof(int) * nflags, c.st));
+    // [owner progress: nch x ngroups uint64 | helper flags: nch x ngroups x nbk int]
+    c.prog_cap = static_cast<int64_t>(nch) * ngroups;
+    const size_t bytes = sizeof(unsigned long long) * c.prog_cap + sizeof(int) * nflags;
+    c.flags.ensure(bytes);
+    CK(cudaMemsetAsync(c.flags.p, 0, bytes, c.st));
     c.flags_cap = nflags;
     c.epoch = 0;
   }
@@ -459,10 +503,37 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
     Krylov<double>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
                             c.bv_d.as<double>(), reinterpret_cast<const double*>(vsrc), act, na, c.bbuf.as<cd>());
   CK(cudaEventRecord(c.ev2, c.st));
-  trsm_launch(c.st, c.geom, c.chains_fwd.as<Chain>(), nch, na, ld, c.flags.as<int>(), ++c.epoch, c.counter.as<int>(),
-              1, c.num_sms);
-  trsm_launch(c.st, c.geom, c.chains_bwd.as<Chain>(), nch, na, ld, c.flags.as<int>(), ++c.epoch,
-              c.counter.as<int>() + 1, 0, c.num_sms);
+  unsigned long long* fx = c.flags.as<unsigned long long>();
+  int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
+  // ZOLO_TRACE=<file>: dump per-step timestamps of chain 0 / group 0 of the
+  // first forward sweep (development aid for the pipeline's critical path)
+  static const char* trace_path = std::getenv("ZOLO_TRACE");
+  unsigned long long* tr = nullptr;
+  if (trace_path && !c.trace_done) {
+    c.trace_buf.ensure(sizeof(unsigned long long) * 16 * c.geom.nbk);
+    CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 16 * c.geom.nbk, c.st));
+    tr = c.trace_buf.as<unsigned long long>();
+  }
+  const int g1 = trsm_launch(c.st, c.geom, c.chains_fwd.as<Chain>(), nch, na, ld, fx, fc, ++c.epoch,
+                             c.counter.as<int>(), 1, c.num_sms, tr);
+  if (tr) {
+    std::vector<unsigned long long> h(16 * c.geom.nbk);
+    CK(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    if (FILE* f = std::fopen(trace_path, "w")) {
+      for (int s = 0; s < c.geom.nbk; ++s) {
+        for (int q = 0; q < 16; ++q) std::fprintf(f, "%llu%c", h[16 * s + q], q == 15 ? '\n' : ' ');
+      }
+      std::fclose(f);
+    }
+    c.trace_done = true;
+  }
+  const int g2 = trsm_launch(c.st, c.geom, c.chains_bwd.as<Chain>(), nch, na, ld, fx, fc, ++c.epoch,
+                             c.counter.as<int>() + 1, 0, c.num_sms);
+  if (g1 < 0 || g2 < 0)
+    throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: " + std::to_string(nch) + " chains x " +
+                                         std::to_string((na + CG - 1) / CG) +
+                                         " column groups exceed the resident CTA budget");
   CK(cudaEventRecord(c.ev3, c.st));
   CK(cudaGetLastError());
   if (c.cx)
@@ -575,6 +646,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   const int nchunk = static_cast<int>((n + CHUNK - 1) / CHUNK);
   float trsm_ms = 0.0f;
   int trsm_launches = 0;
+  int64_t launches = 4, opapps = 0;
   for (int it = 0; it < maxit && !active.empty(); ++it) {
     const int na = static_cast<int>(active.size());
     std::memcpy(c.act_h, active.data(), sizeof(int) * na);
@@ -582,6 +654,8 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     S* vm = reinterpret_cast<S*>(basis_block(c, it));
     apply_g_device(c, vm, na, c.w.p);
     trsm_launches += 2;
+    launches += 8 + (it + 1 < maxit ? 1 : 0);
+    opapps += na;
     c.g_apps += na;
     c.inner_solves += static_cast<int64_t>(c.nchains()) * na;
     Krylov<S>::arnoldi(c.st, n, ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(), c.act_d.as<int>(), na, g,
@@ -616,6 +690,8 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   c.last_ms[0] = ms;
   c.last_ms[2] = trsm_ms;
   c.last_ms[3] = trsm_launches;
+  c.last_ms[4] = static_cast<double>(launches + 2);
+  c.last_ms[5] = static_cast<double>(opapps);
 
   // report (gmres.hpp:31-43 merged as filter_engine.hpp:127-133)
   std::vector<double> res(ncols * q);
@@ -763,7 +839,7 @@ int zolo_ctx_destroy(zolo_ctx* c) {
   for (auto s : c->pole_streams) cudaStreamDestroy(s);
   if (c->act_h) cudaFreeHost(c->act_h);
   if (c->done_h) cudaFreeHost(c->done_h);
-  for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3})
+  for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3, c->tev0, c->tev1})
     if (ev) cudaEventDestroy(ev);
   cudaStream_t st = c->st;
   delete c;
@@ -931,8 +1007,26 @@ int zolo_block_update(zolo_ctx* c, const double* y, int64_t k, const double* q, 
   });
 }
 
+int zolo_timer(zolo_ctx* c, int op, double* ms) {
+  return guarded(c, [&] {
+    if (!c->tev0) {
+      CK(cudaEventCreate(&c->tev0));
+      CK(cudaEventCreate(&c->tev1));
+    }
+    if (op == 0) {
+      CK(cudaEventRecord(c->tev0, c->st));
+    } else {
+      CK(cudaEventRecord(c->tev1, c->st));
+      CK(cudaEventSynchronize(c->tev1));
+      float f = 0;
+      CK(cudaEventElapsedTime(&f, c->tev0, c->tev1));
+      if (ms) *ms = f;
+    }
+  });
+}
+
 int zolo_last_timings(const zolo_ctx* c, double* ms) {
-  for (int i = 0; i < 4; ++i) ms[i] = c->last_ms[i];
+  for (int i = 0; i < 8; ++i) ms[i] = c->last_ms[i];
   return ZOLO_OK;
 }
 

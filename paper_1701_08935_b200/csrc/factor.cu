@@ -1,0 +1,331 @@
+// Numeric unpivoted block-band LU of P(A - sigma B)P^T and the multi-RHS
+// pipelined triangular solves on it.
+//
+// Reference: factorize (band_factor.hpp:135-182) eliminates one column at a
+// time with a rank-1 update of the trailing band; ShiftedFactor::solve /
+// adjoint_solve (band_factor.hpp:53-117) sweep the band once per right-hand
+// side column. Here both become dense TILE x TILE complex128 tile products
+// over the envelope of the band (see band.cuh):
+//
+//   factor step k:  diagonal tile LU + pivot monitor + triangular inverses
+//                   -> panel tiles (x DinvU / DinvL) -> trailing updates,
+//                   then one post-pass builds the coupling tiles M.
+//   solve sweep:    x_i = c_i - M_i x_{i-+1},
+//                   c_i = Dinv_i (b_i - sum_{d>=2} T_(i,i-+d) x_(i-+d)).
+//                   HELPER tasks compute every c_i (all the flops, off the
+//                   critical path: they need x up to i-+2); one OWNER task per
+//                   (chain, column group) walks the chain doing only the
+//                   M_i x_{i-+1} product with x_{i-+1} kept on chip. All poles,
+//                   the solve and adjoint chains and all column groups share
+//                   ONE persistent launch per sweep direction; dependencies are
+//                   per-(chain, group, block) epoch flags (release/acquire).
+//                   Owners take the first task indices and helpers are claimed
+//                   in dependency order from an atomic counter, so the launch
+//                   is deadlock free whenever the owners fit on the device.
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include <algorithm>
+
+#include "band.cuh"
+
+namespace zolo {
+
+namespace {
+
+constexpr int FT = 256;  // factorization threads per CTA
+
+__device__ __forceinline__ void load_tile_async(cd* s, const cd* g) {
+  // 1024 complex values, 4 per thread, into the padded [col*TPAD + row] copy
+#pragma unroll
+  for (int q = 0; q < TT / FT; ++q) {
+    const int e = threadIdx.x + q * FT;
+    cp_async16_cg(&s[(e / TILE) * TPAD + (e % TILE)], g + e);
+  }
+}
+
+// out[2x2] = A(rows) * B(cols) over the full tile; thread (tx,ty) owns rows
+// tx, tx+16 and columns ty, ty+16. A, B padded shared tiles.
+__device__ __forceinline__ void tile_mm(const cd* As, const cd* Bs, cd out[4]) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  cd c00 = mk(0, 0), c01 = mk(0, 0), c10 = mk(0, 0), c11 = mk(0, 0);
+#pragma unroll 8
+  for (int k = 0; k < TILE; ++k) {
+    const cd a0 = As[k * TPAD + tx], a1 = As[k * TPAD + tx + 16];
+    const cd b0 = Bs[ty * TPAD + k], b1 = Bs[(ty + 16) * TPAD + k];
+    cfma(c00, a0, b0);
+    cfma(c01, a0, b1);
+    cfma(c10, a1, b0);
+    cfma(c11, a1, b1);
+  }
+  out[0] = c00;
+  out[1] = c01;
+  out[2] = c10;
+  out[3] = c11;
+}
+
+__device__ __forceinline__ void store_tile(cd* c, const cd out[4]) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  c[ty * TILE + tx] = out[0];
+  c[(ty + 16) * TILE + tx] = out[1];
+  c[ty * TILE + tx + 16] = out[2];
+  c[(ty + 16) * TILE + tx + 16] = out[3];
+}
+
+__global__ void scatter_kernel(BandGeom g, cd* Lt, cd* Ut, int64_t nnz, const int* e_row, const int* e_col,
+                               const double* a_val, const double* b_val, int cx, double sr, double si,
+                               unsigned long long* row_norm_bits) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e < nnz) {
+    const int pi = e_row[e], pj = e_col[e];
+    cd a, b;
+    if (cx) {
+      a = mk(a_val[2 * e], a_val[2 * e + 1]);
+      b = mk(b_val[2 * e], b_val[2 * e + 1]);
+    } else {
+      a = mk(a_val[e], 0.0);
+      b = mk(b_val[e], 0.0);
+    }
+    // assemble_shifted (sparse.hpp:153-186): A - sigma B on the union pattern
+    const cd v = csub(a, cmul(mk(sr, si), b));
+    const int bi = pi / TILE, bj = pj / TILE;
+    const int r = pi % TILE, c = pj % TILE;
+    if (bi >= bj)
+      Lt[lt_off(bi, bi - bj, g.J) + c * TILE + r] = v;
+    else
+      Ut[lt_off(bj, bj - bi, g.J) + c * TILE + r] = v;
+    const double av = hypot(v.x, v.y);
+    atomicMax(&row_norm_bits[pi], static_cast<unsigned long long>(__double_as_longlong(av)));
+  } else if (e < nnz + (g.npad - g.n)) {
+    // identity padding rows beyond n
+    const int64_t row = g.n + (e - nnz);
+    const int bi = static_cast<int>(row / TILE), r = static_cast<int>(row % TILE);
+    Lt[lt_off(bi, 0, g.J) + r * TILE + r] = mk(1.0, 0.0);
+    row_norm_bits[row] = static_cast<unsigned long long>(__double_as_longlong(1.0));
+  }
+}
+
+// Diagonal tile: unpivoted LU in shared memory with the reference's pivot
+// monitor (|pivot| > 1e-14 ||row||_inf, band_factor.hpp:160-166), then the
+// inverses of its unit-lower and upper triangles (threads 0..127: L^{-1},
+// 128..255: U^{-1}; 4 threads per column share each dot product).
+__global__ void __launch_bounds__(FT) diag_factor_kernel(BandGeom g, int k, cd* Lt, cd* DinvL, cd* DinvU,
+                                                         const double* row_norm, int* fail_index,
+                                                         unsigned long long* min_ratio_bits) {
+  extern __shared__ __align__(16) unsigned char diag_smem[];
+  cd* D = reinterpret_cast<cd*>(diag_smem);
+  cd* XL = D + TILE * TPAD;
+  cd* XU = XL + TILE * TPAD;
+  cd(*red)[4][TILE] = reinterpret_cast<cd(*)[4][TILE]>(XU + TILE * TPAD);
+  cd* tile = Lt + lt_off(k, 0, g.J);
+  load_tile_async(D, tile);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int t = threadIdx.x;
+  for (int p = 0; p < TILE; ++p) {
+    const cd piv = D[p * TPAD + p];
+    const cd inv = cdiv(mk(1.0, 0.0), piv);
+    if (t == 0) {
+      const int64_t gi = static_cast<int64_t>(k) * TILE + p;
+      if (gi < g.n) {
+        const double rn = row_norm[gi];
+        const double ap = hypot(piv.x, piv.y);
+        const double ratio = ap / fmax(rn, 1e-300);
+        atomicMin(min_ratio_bits, static_cast<unsigned long long>(__double_as_longlong(ratio)));
+        if (!(ap > 1e-14 * rn) && *fail_index < 0) *fail_index = static_cast<int>(gi);
+      }
+    }
+    if (t > p && t < TILE) D[p * TPAD + t] = cmul(D[p * TPAD + t], inv);
+    __syncthreads();
+    const int m = TILE - 1 - p;
+    for (int idx = t; idx < m * m; idx += FT) {
+      const int i = p + 1 + idx % m, j = p + 1 + idx / m;
+      D[j * TPAD + i] = csub(D[j * TPAD + i], cmul(D[p * TPAD + i], D[j * TPAD + p]));
+    }
+    __syncthreads();
+  }
+  for (int q = 0; q < TT / FT; ++q) {
+    const int e = t + q * FT;
+    tile[e] = D[(e / TILE) * TPAD + (e % TILE)];
+  }
+  // triangular inverses, one row of X per step
+  const bool upper = t >= 128;
+  const int tt = t & 127, c = tt & 31, part = tt >> 5;
+  cd* X = upper ? XU : XL;
+  for (int q = tt; q < TT; q += 128) {
+    const int rr = q % TILE, cc = q / TILE;
+    X[cc * TPAD + rr] = mk(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int s = 0; s < TILE; ++s) {
+    // L: row i = s; U: row i = 31 - s
+    const int i = upper ? TILE - 1 - s : s;
+    cd acc = mk(0.0, 0.0);
+    if (!upper) {
+      // X(i,c) = -sum_{k=c}^{i-1} L(i,k) X(k,c), i > c
+      for (int kk = c + part; kk < i; kk += 4) cfma(acc, D[kk * TPAD + i], X[c * TPAD + kk]);
+    } else {
+      // X(i,c) = (delta - sum_{k=i+1}^{c} U(i,k) X(k,c)) / U(i,i), i <= c
+      for (int kk = i + 1 + part; kk <= c; kk += 4) cfma(acc, D[kk * TPAD + i], X[c * TPAD + kk]);
+    }
+    red[upper][part][c] = acc;
+    __syncthreads();
+    if (part == 0) {
+      const cd s4 = cadd(cadd(red[upper][0][c], red[upper][1][c]), cadd(red[upper][2][c], red[upper][3][c]));
+      if (!upper) {
+        if (i == c) X[c * TPAD + i] = mk(1.0, 0.0);
+        else if (i > c) X[c * TPAD + i] = mk(-s4.x, -s4.y);
+      } else if (i <= c) {
+        const cd num = csub(mk(i == c ? 1.0 : 0.0, 0.0), s4);
+        X[c * TPAD + i] = cdiv(num, D[i * TPAD + i]);
+      }
+    }
+    __syncthreads();
+  }
+  cd* outL = DinvL + static_cast<size_t>(k) * TT;
+  cd* outU = DinvU + static_cast<size_t>(k) * TT;
+  for (int q = t; q < TT; q += FT) {
+    const int rr = q % TILE, cc = q / TILE;
+    outL[q] = XL[cc * TPAD + rr];
+    outU[q] = XU[cc * TPAD + rr];
+  }
+}
+
+// Panel: L(k+d,k) = A(k+d,k) U_kk^{-1} (blocks 0..J-1),
+//        U(k,k+d) = L_kk^{-1} A(k,k+d) (blocks J..2J-1); envelope tiles only.
+__global__ void __launch_bounds__(FT) panel_kernel(BandGeom g, int k, cd* Lt, cd* Ut, const cd* DinvL,
+                                                   const cd* DinvU) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int J = g.J;
+  const bool lower = blockIdx.x < J;
+  const int d = lower ? blockIdx.x + 1 : blockIdx.x - J + 1;
+  if (k + d >= g.nbk || d > g.dl[k + d]) return;
+  cd* c;
+  if (lower) {
+    c = Lt + lt_off(k + d, d, J);
+    load_tile_async(As, c);
+    load_tile_async(Bs, DinvU + static_cast<size_t>(k) * TT);
+  } else {
+    c = Ut + lt_off(k + d, d, J);
+    load_tile_async(As, DinvL + static_cast<size_t>(k) * TT);
+    load_tile_async(Bs, c);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  cd out[4];
+  tile_mm(As, Bs, out);
+  store_tile(c, out);
+}
+
+// Trailing update A(k+a, k+b) -= L(k+a, k) U(k, k+b), a, b in 1..J (envelope).
+__global__ void __launch_bounds__(FT) trailing_kernel(BandGeom g, int k, cd* Lt, cd* Ut) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int J = g.J;
+  const int a = blockIdx.x + 1, b = blockIdx.y + 1;
+  if (k + a >= g.nbk || k + b >= g.nbk) return;
+  if (a > g.dl[k + a] || b > g.dl[k + b]) return;
+  load_tile_async(As, Lt + lt_off(k + a, a, J));
+  load_tile_async(Bs, Ut + lt_off(k + b, b, J));
+  cp_async_commit();
+  cd* c = (a >= b) ? Lt + lt_off(k + a, a - b, J) : Ut + lt_off(k + b, b - a, J);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const cd c0 = c[ty * TILE + tx], c1 = c[(ty + 16) * TILE + tx], c2 = c[ty * TILE + tx + 16],
+           c3 = c[(ty + 16) * TILE + tx + 16];
+  cp_async_wait<0>();
+  __syncthreads();
+  cd out[4];
+  tile_mm(As, Bs, out);
+  out[0] = csub(c0, out[0]);
+  out[1] = csub(c1, out[1]);
+  out[2] = csub(c2, out[2]);
+  out[3] = csub(c3, out[3]);
+  store_tile(c, out);
+}
+
+// Coupling tiles of the solve chains (kind: 0 MF, 1 MB, 2 MFH, 3 MBH).
+__global__ void __launch_bounds__(FT) mtiles_kernel(BandGeom g, FactorTiles f) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int i = blockIdx.x, kind = blockIdx.y;
+  const int J = g.J;
+  cd* out = (kind == 0 ? f.MF : kind == 1 ? f.MB : kind == 2 ? f.MFH : f.MBH) + static_cast<size_t>(i) * TT;
+  bool valid;
+  const cd *A, *B;
+  switch (kind) {
+    case 0:  // DinvL[i] L(i, i-1)
+      valid = i >= 1 && J >= 1 && g.dl[i] >= 1;
+      A = f.DinvL + static_cast<size_t>(i) * TT;
+      B = valid ? f.Lt + lt_off(i, 1, J) : nullptr;
+      break;
+    case 1:  // DinvU[i] U(i, i+1)
+      valid = i + 1 < g.nbk && J >= 1 && g.dl[i + 1] >= 1;
+      A = f.DinvU + static_cast<size_t>(i) * TT;
+      B = valid ? f.Ut + lt_off(i + 1, 1, J) : nullptr;
+      break;
+    case 2:  // U(i-1, i) DinvU[i]
+      valid = i >= 1 && J >= 1 && g.dl[i] >= 1;
+      A = valid ? f.Ut + lt_off(i, 1, J) : nullptr;
+      B = f.DinvU + static_cast<size_t>(i) * TT;
+      break;
+    default:  // L(i+1, i) DinvL[i]
+      valid = i + 1 < g.nbk && J >= 1 && g.dl[i + 1] >= 1;
+      A = valid ? f.Lt + lt_off(i + 1, 1, J) : nullptr;
+      B = f.DinvL + static_cast<size_t>(i) * TT;
+      break;
+  }
+  if (!valid) {
+    for (int q = threadIdx.x; q < TT; q += FT) out[q] = mk(0.0, 0.0);
+    return;
+  }
+  load_tile_async(As, A);
+  load_tile_async(Bs, B);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  cd o[4];
+  tile_mm(As, Bs, o);
+  store_tile(out, o);
+}
+
+}  // namespace
+
+void factor_scatter(cudaStream_t st, const BandGeom& g, const FactorTiles& f, int64_t nnz, const int* e_row,
+                    const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
+                    double sig_im, double* row_norm) {
+  const size_t bytes = g.tiles_per_array() * TT * sizeof(cd);
+  cudaMemsetAsync(f.Lt, 0, bytes, st);
+  cudaMemsetAsync(f.Ut, 0, bytes, st);
+  cudaMemsetAsync(row_norm, 0, sizeof(double) * g.npad, st);
+  const int64_t total = nnz + (g.npad - g.n);
+  const int threads = 256;
+  const int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 0)
+    scatter_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(
+        g, f.Lt, f.Ut, nnz, e_row, e_col, a_val, b_val, cx, sig_re, sig_im,
+        reinterpret_cast<unsigned long long*>(row_norm));
+}
+
+void factor_run(cudaStream_t st, const BandGeom& g, const FactorTiles& f, const double* row_norm,
+                FactorDevState ds, int cx) {
+  constexpr int diag_smem = (3 * TILE * TPAD + 2 * 4 * TILE) * sizeof(cd);
+  static bool diag_attr = false;
+  if (!diag_attr) {
+    cudaFuncSetAttribute(diag_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem);
+    diag_attr = true;
+  }
+  for (int k = 0; k < g.nbk; ++k) {
+    diag_factor_kernel<<<1, FT, diag_smem, st>>>(g, k, f.Lt, f.DinvL, f.DinvU, row_norm, ds.fail_index,
+                                                 ds.min_ratio_bits);
+    if (k + 1 < g.nbk && g.J > 0) {
+      panel_kernel<<<2 * g.J, FT, 0, st>>>(g, k, f.Lt, f.Ut, f.DinvL, f.DinvU);
+      trailing_kernel<<<dim3(g.J, g.J), FT, 0, st>>>(g, k, f.Lt, f.Ut);
+    }
+  }
+  mtiles_kernel<<<dim3(g.nbk, cx ? 4 : 2), FT, 0, st>>>(g, f);
+}
+
+}  // namespace zolo

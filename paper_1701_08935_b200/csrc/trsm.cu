@@ -1,0 +1,401 @@
+// Pipelined multi-RHS block-band triangular solves on the FP64 tensor cores.
+//
+// Reference: ShiftedFactor::solve / adjoint_solve (band_factor.hpp:53-117)
+// sweep the band once per right-hand-side column: forward L / backward U for
+// the solve, U^H / L^H for the adjoint. Here every sweep runs over all columns
+// of the block at once, as a recurrence over TILE-row blocks:
+//
+//     x_i = c_i - M_i x_{i-+1},      c_i = Dinv_i (b_i - sum_{d>=2} T_(i,i-+d) x_(i-+d))
+//
+// with M_i = Dinv_i T_(i,i-+1) precomputed by the factorization (factor.cu).
+//   HELPER tasks compute every c_i -- all the flops, off the critical path
+//     (they need x only up to block i-+2) -- through an NS-stage cp.async
+//     pipeline of envelope tiles;
+//   one OWNER task per (chain, column group) walks the chain doing only the
+//     M_i x_{i-+1} product, with x_{i-+1} kept in shared memory.
+// All tile products are mma.sync.m8n8k4.f64 (DMMA): warp w owns an 8x8
+// complex block of the 32 x CG output (4 real MMAs per complex k-step), so no
+// cross-lane reduction is needed. All poles, solve + adjoint chains and all
+// column groups share ONE persistent launch per sweep direction. The owner
+// publishes progress as one monotone (epoch << 32 | steps) counter per chain,
+// helpers publish c_i through per-block epoch flags; tasks are claimed in
+// dependency order (owners first) from an atomic counter, so the launch is
+// deadlock free whenever the owners fit on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "band.cuh"
+
+namespace zolo {
+
+namespace {
+
+constexpr int ST = 256;        // threads per CTA (8 warps)
+constexpr int APAD = TILE + 2; // tile column stride: op N fragment loads conflict free
+constexpr int XPAD = TILE + 4; // x column stride: B fragment loads conflict free
+constexpr int TILE_S = TILE * APAD;
+constexpr int XS = CG * XPAD;
+constexpr int NS = 3;          // helper pipeline stages
+constexpr int SMEM_FIXED = (NS * TILE_S + NS * XS + TILE_S + XS) * static_cast<int>(sizeof(cd));
+static_assert(CG == 16, "warp layout assumes 32 x 16 output blocks");
+
+struct SolveArgs {
+  const Chain* chains;
+  int nchains, ngroups, ncols, nbk, J, epoch, fwd;
+  int64_t ld;
+  const int* dl;
+  unsigned long long* prog;  // per (chain, group): (epoch << 32) | owner steps done
+  int* flags_c;              // per (chain, group, block): epoch when c_i is ready
+  int* counter;              // [0] task counter, [2] wait-timeout error word
+  unsigned long long* trace; // optional: per-step timestamps of chain 0 / group 0
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void dmma(double c[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Per-thread ownership of the 32 x 16 complex output block: warp w holds rows
+// 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1}.
+struct Frag {
+  int row, col;  // first of the two owned (row, col), (row, col+1)
+  int r0, c0;    // warp block origin
+  int lane;
+};
+__device__ __forceinline__ Frag frag() {
+  Frag f;
+  const int w = threadIdx.x >> 5;
+  f.lane = threadIdx.x & 31;
+  f.r0 = 8 * (w & 3);
+  f.c0 = 8 * (w >> 2);
+  f.row = f.r0 + (f.lane >> 2);
+  f.col = f.c0 + 2 * (f.lane & 3);
+  return f;
+}
+
+// acc[2] (complex, the two owned outputs) += op(T)[r0:r0+8, :] X[:, c0:c0+8].
+// T padded [col*APAD + row]; X padded [col*XPAD + k]. op H = conjugate transpose.
+__device__ __forceinline__ void mma_tile(cd acc[2], const cd* ts, const cd* xs, bool opH, const Frag& f) {
+  double re0[2] = {0.0, 0.0}, im0[2] = {0.0, 0.0}, re1[2] = {0.0, 0.0}, im1[2] = {0.0, 0.0};
+  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
+  const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
+#pragma unroll
+  for (int kb = 0; kb < TILE / 4; ++kb) {
+    const int k = 4 * kb + am;
+    const cd a = opH ? cconj(ts[ar * APAD + k]) : ts[k * APAD + ar];
+    const cd b = xs[bc * XPAD + 4 * kb + bm];
+    double* re = (kb & 1) ? re1 : re0;
+    double* im = (kb & 1) ? im1 : im0;
+    dmma(re, a.x, b.x);
+    dmma(re, -a.y, b.y);
+    dmma(im, a.x, b.y);
+    dmma(im, a.y, b.x);
+  }
+  acc[0].x += re0[0] + re1[0];
+  acc[1].x += re0[1] + re1[1];
+  acc[0].y += im0[0] + im1[0];
+  acc[1].y += im0[1] + im1[1];
+}
+
+__device__ __forceinline__ void load_tile(cd* s, const cd* g) {
+#pragma unroll
+  for (int q = 0; q < TT / ST; ++q) {
+    const int e = threadIdx.x + q * ST;
+    cp_async16_cg(&s[(e / TILE) * APAD + (e % TILE)], g + e);
+  }
+}
+
+// 32 rows x CG columns of a column-major block into [col*XPAD + row].
+__device__ __forceinline__ void load_x(cd* xs, const cd* base, int64_t ld, int c0, int nc) {
+  const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < CG / 8; ++q) {
+    const int c = cc + 8 * q;
+    if (c < nc)
+      cp_async16_cg(&xs[c * XPAD + row], base + row + (c0 + c) * ld);
+    else
+      xs[c * XPAD + row] = mk(0.0, 0.0);
+  }
+}
+
+// Coalesced store of a [col*XPAD + row] staging block to the column-major block.
+__device__ __forceinline__ void store_x(cd* base, const cd* xs, int64_t ld, int c0, int nc) {
+  const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < CG / 8; ++q) {
+    const int c = cc + 8 * q;
+    if (c < nc) base[row + (c0 + c) * ld] = xs[c * XPAD + row];
+  }
+}
+
+// thread 0 waits for *f >= epoch (bounded: a lost producer is reported through
+// err, never a hung GPU), then the CTA synchronises.
+__device__ __forceinline__ void wait_flag(const int* f, int epoch, int* err) {
+  if (threadIdx.x == 0) {
+    int spins = 0;
+    while (ld_acquire(f) < epoch) {
+      if (++spins > 256) __nanosleep(32);
+      if (spins > (1 << 25)) {
+        atomicExch(err, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// OWNER: x_i = c_i - op(M_i) x_{i-+1} along the whole chain (one column group).
+__device__ void owner_task(const SolveArgs& A, int ci, int gi, cd* smem) {
+  cd* m_s[2] = {smem, smem + TILE_S};
+  cd* xb[2] = {smem + 2 * TILE_S, smem + 2 * TILE_S + XS};
+  const Chain ch = A.chains[ci];
+  const bool fwd = A.fwd != 0;
+  const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
+  const Frag f = frag();
+  const int c0 = gi * CG, nc = min(CG, A.ncols - c0);
+  const int64_t ld = A.ld;
+  unsigned long long* prog = A.prog + static_cast<size_t>(ci) * A.ngroups + gi;
+  const unsigned long long tag = static_cast<unsigned long long>(A.epoch) << 32;
+  const int* fc = A.flags_c + (static_cast<size_t>(ci) * A.ngroups + gi) * A.nbk;
+  const bool tr = A.trace != nullptr && ci == 0 && gi == 0 && threadIdx.x == 0;
+  for (int s = 0; s < A.nbk; ++s) {
+    const int i = fwd ? s : A.nbk - 1 - s;
+    if (tr) A.trace[s * 16 + 0] = gtimer();
+    if (s + 1 < A.nbk) load_tile(m_s[(s + 1) & 1], ch.m + static_cast<size_t>(fwd ? i + 1 : i - 1) * TT);
+    cp_async_commit();
+    cp_async_wait<1>();  // M_i landed (issued one step earlier)
+    __syncthreads();
+    // the critical product needs only x_{i-+1} (on chip): do it before c_i arrives
+    cd red[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+    if (s > 0) mma_tile(red, m_s[s & 1], xb[(s + 1) & 1], opH, f);
+    if (tr) A.trace[s * 16 + 6] = gtimer() + (red[0].x == 1234.5 ? 1 : 0);
+    wait_flag(fc + i, A.epoch, A.counter + 2);
+    if (tr) A.trace[s * 16 + 1] = gtimer();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = f.col + q;
+      const cd cv = (c < nc) ? __ldcg(ch.cbuf + static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld)
+                             : mk(0.0, 0.0);
+      xb[s & 1][c * XPAD + f.row] = csub(cv, red[q]);
+    }
+    __syncthreads();
+    store_x(ch.dst + static_cast<int64_t>(i) * TILE, xb[s & 1], ld, c0, nc);
+    __syncthreads();
+    if (tr) A.trace[s * 16 + 7] = gtimer();
+    if (threadIdx.x == 0) {
+      st_release64(prog, tag | static_cast<unsigned>(s + 1));  // cumulative release after the barrier
+      if (tr) A.trace[s * 16 + 2] = gtimer();
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// HELPER: c_i = op(Dinv_i) (b_i - sum_{d>=2} op(T_(i,i-+d)) x_(i-+d)).
+__device__ void helper_task(const SolveArgs& A, int s, int ci, int gi, cd* smem, int* dlist) {
+  auto tile_s = [smem](int k) { return smem + k * TILE_S; };
+  auto x_s = [smem](int k) { return smem + NS * TILE_S + k * XS; };
+  cd* dinv_s = smem + NS * TILE_S + NS * XS;
+  cd* acc_s = dinv_s + TILE_S;
+  __shared__ int nlist_s;
+  __shared__ unsigned long long known_s;  // owner progress last acquired by this CTA
+  const Chain ch = A.chains[ci];
+  const bool fwd = A.fwd != 0;
+  const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
+  const Frag f = frag();
+  const int i = fwd ? s : A.nbk - 1 - s;
+  const int c0 = gi * CG, nc = min(CG, A.ncols - c0);
+  const int64_t ld = A.ld;
+  const int J = A.J;
+  const unsigned long long* prog = A.prog + static_cast<size_t>(ci) * A.ngroups + gi;
+  const unsigned long long tag = static_cast<unsigned long long>(A.epoch) << 32;
+  int* fc = A.flags_c + (static_cast<size_t>(ci) * A.ngroups + gi) * A.nbk;
+  const bool tr = A.trace != nullptr && ci == 0 && gi == 0 && threadIdx.x == 0;
+  if (tr) A.trace[s * 16 + 3] = gtimer();
+
+  // envelope tiles d >= 2 of this block row, farthest first
+  if (threadIdx.x == 0) {
+    known_s = ld_acquire64(prog);
+    int n = 0;
+    const int dli = A.dl[i];
+    for (int d = J; d >= 2; --d) {
+      const bool ok = fwd ? (d <= dli) : (i + d < A.nbk && d <= A.dl[i + d]);
+      if (ok) dlist[n++] = d;
+    }
+    nlist_s = n;
+  }
+  load_tile(dinv_s, ch.dinv + static_cast<size_t>(i) * TT);
+  cd bval[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int c = f.col + q;
+    bval[q] = (c < nc) ? ch.src[static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld] : mk(0.0, 0.0);
+  }
+  __syncthreads();
+  const int nl = nlist_s;
+  unsigned long long known = known_s;  // identical in every thread
+  __syncthreads();                     // known_s may be rewritten from here on
+  cd acc[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+
+  auto dep = [&](int d) { return fwd ? i - d : i + d; };
+  auto tile_ptr = [&](int d) -> const cd* { return ch.off + lt_off(fwd ? i : i + d, d, J); };
+  // x of block row j is final once the owner has completed step s_j: the owner
+  // publishes in order, so one cached frontier covers all farther rows and
+  // only a dependency beyond it costs an L2 round trip. The branch is uniform
+  // (every thread holds the same `known`); the slow path re-broadcasts it
+  // between two barriers.
+  auto ensure = [&](int d) {
+    const int j = dep(d);
+    const unsigned long long target = tag | static_cast<unsigned>((fwd ? j : A.nbk - 1 - j) + 1);
+    if (known < target) {
+      if (threadIdx.x == 0) {
+        unsigned long long v;
+        int spins = 0;
+        while ((v = ld_acquire64(prog)) < target) {
+          if (++spins > 256) __nanosleep(32);
+          if (spins > (1 << 25)) {
+            atomicExch(A.counter + 2, 1);
+            break;
+          }
+        }
+        known_s = v;
+      }
+      __syncthreads();
+      known = known_s;
+      __syncthreads();
+    }
+  };
+  // NS-stage cp.async pipeline over the far tiles (d >= NEAR: tile and x
+  // prefetched NS-1 entries ahead); the nearest dependencies (d < NEAR) get
+  // their tile prefetched but x loaded only right before use.
+  constexpr int NEAR = 4;
+  auto issue = [&](int e) {
+    const int d = dlist[e], buf = e % NS;
+    load_tile(tile_s(buf), tile_ptr(d));
+    if (d >= NEAR) {
+      ensure(d);
+      load_x(x_s(buf), ch.dst + static_cast<int64_t>(dep(d)) * TILE, ld, c0, nc);
+    }
+  };
+#pragma unroll
+  for (int e = 0; e < NS - 1; ++e) {
+    if (e < nl) issue(e);
+    cp_async_commit();
+  }
+  if (tr) A.trace[s * 16 + 10] = gtimer();
+  int nfar = 0;
+  for (int q = 0; q < nl; ++q) {
+    const int buf = q % NS, d = dlist[q];
+    if (q + NS - 1 < nl) issue(q + NS - 1);
+    cp_async_commit();
+    if (d >= NEAR) {
+      cp_async_wait<NS - 1>();
+      ++nfar;
+    } else {
+      if (tr && nfar >= 0) {
+        A.trace[s * 16 + 8] = gtimer();
+        A.trace[s * 16 + 9] = nfar;
+        nfar = -1000;
+      }
+      ensure(d);
+      load_x(x_s(buf), ch.dst + static_cast<int64_t>(dep(d)) * TILE, ld, c0, nc);
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    mma_tile(acc, tile_s(buf), x_s(buf), opH, f);
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (tr) A.trace[s * 16 + 4] = gtimer();
+  // c_i = op(Dinv_i) (b_i - acc)
+#pragma unroll
+  for (int q = 0; q < 2; ++q) acc_s[(f.col + q) * XPAD + f.row] = csub(bval[q], acc[q]);
+  __syncthreads();
+  cd out[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+  mma_tile(out, dinv_s, acc_s, opH, f);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) acc_s[(f.col + q) * XPAD + f.row] = out[q];
+  __syncthreads();
+  store_x(ch.cbuf + static_cast<int64_t>(i) * TILE, acc_s, ld, c0, nc);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st_release(fc + i, A.epoch);  // cumulative release after the barrier
+    if (tr) A.trace[s * 16 + 5] = gtimer();
+  }
+}
+
+__global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cd* smem = reinterpret_cast<cd*>(smem_raw);
+  int* dlist = reinterpret_cast<int*>(smem_raw + SMEM_FIXED);
+  __shared__ int task_s;
+  const int owners = A.nchains * A.ngroups;
+  const int ntasks = owners + A.nbk * owners;
+  for (;;) {
+    if (threadIdx.x == 0) task_s = atomicAdd(A.counter, 1);
+    __syncthreads();
+    const int t = task_s;
+    __syncthreads();
+    if (t >= ntasks) break;
+    if (t < owners) {
+      owner_task(A, t / A.ngroups, t % A.ngroups, smem);
+    } else {
+      const int h = t - owners;
+      const int s = h / owners, rem = h % owners;
+      helper_task(A, s, rem / A.ngroups, rem % A.ngroups, smem, dlist);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int trsm_launch(cudaStream_t st, const BandGeom& g, const Chain* d_chains, int nchains, int ncols, int64_t ld,
+                unsigned long long* prog, int* flags_c, int epoch, int* counter, int fwd, int num_sms,
+                unsigned long long* trace) {
+  const int smem = SMEM_FIXED + (g.J + 8) * static_cast<int>(sizeof(int));
+  static int attr_set = 0;
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = smem;
+  }
+  SolveArgs a;
+  a.chains = d_chains;
+  a.nchains = nchains;
+  a.ngroups = (ncols + CG - 1) / CG;
+  a.ncols = ncols;
+  a.nbk = g.nbk;
+  a.J = g.J;
+  a.epoch = epoch;
+  a.fwd = fwd;
+  a.ld = ld;
+  a.dl = g.dl;
+  a.prog = prog;
+  a.flags_c = flags_c;
+  a.counter = counter;
+  a.trace = trace;
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  const int owners = nchains * a.ngroups;
+  const int ntasks = owners + g.nbk * owners;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trsm_kernel, ST, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int resident = num_sms * per_sm;
+  if (owners >= resident) return -1;  // owners must leave room for helpers
+  const int grid = std::min(ntasks, resident);
+  if (grid > 0) trsm_kernel<<<grid, ST, smem, st>>>(a);
+  return grid;
+}
+
+}  // namespace zolo
