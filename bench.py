@@ -319,11 +319,11 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * nv * esize,
                 "d2h_bytes_per_step": n * nv * esize},
         "gpu_launches": int(kernel_launches),
-        "roofline": {"bound": "fp64", "kernel": "trsm_kernel (wavefront block-band solve)",
+        "roofline": {"bound": "tensor", "kernel": "trsm_kernel (pipelined block-band solve, DMMA f64)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if peak else None, "traffic": traffic,
-                     "peak_source": "measured FP64 (tools/fp64_peak.cu, DMMA = DFMA on B200; "
-                                    "MEASURED_PEAKS.json has no FP64 figure)",
+                     "peak_source": "measured FP64 tensor pipe (tools/fp64_peak.cu mma.sync.m8n8k4.f64, "
+                                    "profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no FP64 figure)",
                      "algorithmic": "8 flops per complex MAC x (nnz(L)+nnz(U)) of the band per column per pole "
                                     "per G application",
                      "trsm_share_of_step": trsm_ms / total_ms if total_ms else None,

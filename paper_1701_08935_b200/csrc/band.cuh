@@ -37,15 +37,13 @@ struct BandGeom {
   size_t tiles_per_array() const { return static_cast<size_t>(nbk) * (J + 1); }
 };
 
+// After factor_run the off-diagonal tiles are ROW-SCALED by the diagonal-block
+// inverses: Lt[i][d] = DinvL[i] L(i,i-d), Ut[j][d] = DinvU[j-d] U(j-d,j).
 struct FactorTiles {
   cd* Lt = nullptr;
   cd* Ut = nullptr;
   cd* DinvL = nullptr;
   cd* DinvU = nullptr;
-  cd* MF = nullptr;   // DinvL[i] L(i,i-1)          (forward L sweep)
-  cd* MB = nullptr;   // DinvU[i] U(i,i+1)          (backward U sweep)
-  cd* MFH = nullptr;  // U(i-1,i) DinvU[i]  (used as ^H, forward U^H sweep)
-  cd* MBH = nullptr;  // L(i+1,i) DinvL[i]  (used as ^H, backward L^H sweep)
 };
 
 __host__ __device__ inline size_t lt_off(int i, int d, int J) {
@@ -60,10 +58,13 @@ enum SweepMode : int {
   BWD_LH = 3   // L^H x = y         (adjoint_solve, band_factor.hpp:107-112)
 };
 
+// One triangular sweep over row-scaled tiles T~ (op N, or op H for the
+// adjoint sweeps): u_i = pre(b_i) - sum_d op(T~_(i,i-+d)) u_(i-+d), where
+// pre = op(Dinv_i) or the identity. For the adjoint sweeps u is the
+// diagonally transformed unknown (z = U_ii^H y, w = L_ii^H x, see trsm.cu).
 struct Chain {
-  const cd* off;   // Lt or Ut array of the pole
-  const cd* dinv;  // DinvL or DinvU of the pole
-  const cd* m;     // MF / MB / MFH / MBH of the pole
+  const cd* off;   // row-scaled Lt or Ut array of the pole
+  const cd* pre;   // DinvL / DinvU applied to b_i first, or nullptr (identity)
   const cd* src;   // right-hand side (ld x ncols), read once per block row
   cd* dst;         // solution (ld x ncols), written in place
   cd* cbuf;        // helper -> owner partial solutions c_i (ld x ncols)
@@ -81,6 +82,10 @@ void factor_scatter(cudaStream_t st, const BandGeom& g, const FactorTiles& f, in
                     double sig_im, double* row_norm);
 void factor_run(cudaStream_t st, const BandGeom& g, const FactorTiles& f, const double* row_norm,
                 FactorDevState ds, int cx);
+
+// x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass
+// x_i = DinvL_i^H w_i); x is ld x ncols, D is nbk tiles.
+void blockdiag_apply(cudaStream_t st, const BandGeom& g, const cd* D, bool opH, cd* x, int ncols, int64_t ld);
 
 // One launch covers nchains x ngroups independent pipelines (owner + helpers).
 // Returns the number of resident CTAs needed (error if owners do not fit).

@@ -343,8 +343,7 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
   const int r = c.r;
   const size_t per_array = g.tiles_per_array() * TT;
   const size_t per_diag = static_cast<size_t>(g.nbk) * TT;
-  const int n_m = c.cx ? 4 : 2;                                // coupling tile arrays
-  const size_t per_pole = 2 * per_array + (2 + n_m) * per_diag;  // complex entries
+  const size_t per_pole = 2 * per_array + 2 * per_diag;  // complex entries
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   const size_t need = per_pole * r * sizeof(cd);
@@ -363,12 +362,6 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     c.tiles[j].Ut = p + per_array;
     c.tiles[j].DinvL = p + 2 * per_array;
     c.tiles[j].DinvU = p + 2 * per_array + per_diag;
-    c.tiles[j].MF = p + 2 * per_array + 2 * per_diag;
-    c.tiles[j].MB = p + 2 * per_array + 3 * per_diag;
-    if (c.cx) {
-      c.tiles[j].MFH = p + 2 * per_array + 4 * per_diag;
-      c.tiles[j].MBH = p + 2 * per_array + 5 * per_diag;
-    }
   }
   // fail index (int, init -1) and min ratio bits (init +inf)
   std::vector<unsigned long long> fs(2 * r);
@@ -455,15 +448,18 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
       cd* xa = c.xbuf[2 * p + 1]->as<cd>();
       cd* cb = c.cbuf[2 * p]->as<cd>();
       cd* cba = c.cbuf[2 * p + 1]->as<cd>();
-      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.MF, b, x, cb, FWD_L, 0};
-      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.MB, x, x, cb, BWD_U, 0};
-      fwd[2 * p + 1] = Chain{t.Ut, t.DinvU, t.MFH, b, xa, cba, FWD_UH, 0};
-      bwd[2 * p + 1] = Chain{t.Lt, t.DinvL, t.MBH, xa, xa, cba, BWD_LH, 0};
+      // solve:   y = DinvL b - L~ y ;  x = DinvU y - U~ x
+      // adjoint: z = b - U~^H z (z_i = U_ii^H y_i) ; w = DinvU^H z - L~^H w (w_i = L_ii^H x_i),
+      //          then x_i = DinvL_i^H w_i (blockdiag post-pass)
+      fwd[2 * p] = Chain{t.Lt, t.DinvL, b, x, cb, FWD_L, 0};
+      bwd[2 * p] = Chain{t.Ut, t.DinvU, x, x, cb, BWD_U, 0};
+      fwd[2 * p + 1] = Chain{t.Ut, nullptr, b, xa, cba, FWD_UH, 0};
+      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, xa, xa, cba, BWD_LH, 0};
     } else {
       cd* x = c.xbuf[p]->as<cd>();
       cd* cb = c.cbuf[p]->as<cd>();
-      fwd[p] = Chain{t.Lt, t.DinvL, t.MF, b, x, cb, FWD_L, 0};
-      bwd[p] = Chain{t.Ut, t.DinvU, t.MB, x, x, cb, BWD_U, 0};
+      fwd[p] = Chain{t.Lt, t.DinvL, b, x, cb, FWD_L, 0};
+      bwd[p] = Chain{t.Ut, t.DinvU, x, x, cb, BWD_U, 0};
     }
   }
   upload(c.chains_fwd, fwd, c.st);
@@ -530,6 +526,8 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   }
   const int g2 = trsm_launch(c.st, c.geom, c.chains_bwd.as<Chain>(), nch, na, ld, fx, fc, ++c.epoch,
                              c.counter.as<int>() + 1, 0, c.num_sms);
+  if (c.cx)
+    for (int p = 0; p < c.r; ++p) blockdiag_apply(c.st, c.geom, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
   if (g1 < 0 || g2 < 0)
     throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: " + std::to_string(nch) + " chains x " +
                                          std::to_string((na + CG - 1) / CG) +

@@ -246,49 +246,26 @@ __global__ void __launch_bounds__(FT) trailing_kernel(BandGeom g, int k, cd* Lt,
   store_tile(c, out);
 }
 
-// Coupling tiles of the solve chains (kind: 0 MF, 1 MB, 2 MFH, 3 MBH).
-__global__ void __launch_bounds__(FT) mtiles_kernel(BandGeom g, FactorTiles f) {
+// Row scaling of the off-diagonal factor tiles by the diagonal-block inverses:
+//   L~(i, i-d) = DinvL[i] L(i, i-d),     U~(j-d, j) = DinvU[j-d] U(j-d, j).
+// With these, every triangular sweep (trsm.cu) is a recurrence without any
+// diagonal operation on its critical path. blockIdx = (block row, d - 1, L|U).
+__global__ void __launch_bounds__(FT) scale_tiles_kernel(BandGeom g, FactorTiles f) {
   __shared__ cd As[TILE * TPAD];
   __shared__ cd Bs[TILE * TPAD];
-  const int i = blockIdx.x, kind = blockIdx.y;
-  const int J = g.J;
-  cd* out = (kind == 0 ? f.MF : kind == 1 ? f.MB : kind == 2 ? f.MFH : f.MBH) + static_cast<size_t>(i) * TT;
-  bool valid;
-  const cd *A, *B;
-  switch (kind) {
-    case 0:  // DinvL[i] L(i, i-1)
-      valid = i >= 1 && J >= 1 && g.dl[i] >= 1;
-      A = f.DinvL + static_cast<size_t>(i) * TT;
-      B = valid ? f.Lt + lt_off(i, 1, J) : nullptr;
-      break;
-    case 1:  // DinvU[i] U(i, i+1)
-      valid = i + 1 < g.nbk && J >= 1 && g.dl[i + 1] >= 1;
-      A = f.DinvU + static_cast<size_t>(i) * TT;
-      B = valid ? f.Ut + lt_off(i + 1, 1, J) : nullptr;
-      break;
-    case 2:  // U(i-1, i) DinvU[i]
-      valid = i >= 1 && J >= 1 && g.dl[i] >= 1;
-      A = valid ? f.Ut + lt_off(i, 1, J) : nullptr;
-      B = f.DinvU + static_cast<size_t>(i) * TT;
-      break;
-    default:  // L(i+1, i) DinvL[i]
-      valid = i + 1 < g.nbk && J >= 1 && g.dl[i + 1] >= 1;
-      A = valid ? f.Lt + lt_off(i + 1, 1, J) : nullptr;
-      B = f.DinvL + static_cast<size_t>(i) * TT;
-      break;
-  }
-  if (!valid) {
-    for (int q = threadIdx.x; q < TT; q += FT) out[q] = mk(0.0, 0.0);
-    return;
-  }
-  load_tile_async(As, A);
-  load_tile_async(Bs, B);
+  const int i = blockIdx.x, d = blockIdx.y + 1;
+  const bool lower = blockIdx.z == 0;
+  if (d > g.dl[i]) return;  // outside the envelope: exact zeros
+  cd* t = (lower ? f.Lt : f.Ut) + lt_off(i, d, g.J);
+  const cd* dinv = lower ? f.DinvL + static_cast<size_t>(i) * TT : f.DinvU + static_cast<size_t>(i - d) * TT;
+  load_tile_async(As, dinv);
+  load_tile_async(Bs, t);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   cd o[4];
   tile_mm(As, Bs, o);
-  store_tile(out, o);
+  store_tile(t, o);
 }
 
 }  // namespace
@@ -325,7 +302,7 @@ void factor_run(cudaStream_t st, const BandGeom& g, const FactorTiles& f, const 
       trailing_kernel<<<dim3(g.J, g.J), FT, 0, st>>>(g, k, f.Lt, f.Ut);
     }
   }
-  mtiles_kernel<<<dim3(g.nbk, cx ? 4 : 2), FT, 0, st>>>(g, f);
+  if (g.J > 0) scale_tiles_kernel<<<dim3(g.nbk, g.J, 2), FT, 0, st>>>(g, f);
 }
 
 }  // namespace zolo

@@ -83,26 +83,46 @@ __device__ __forceinline__ Frag frag() {
 
 // acc[2] (complex, the two owned outputs) += op(T)[r0:r0+8, :] X[:, c0:c0+8].
 // T padded [col*APAD + row]; X padded [col*XPAD + k]. op H = conjugate transpose.
-__device__ __forceinline__ void mma_tile(cd acc[2], const cd* ts, const cd* xs, bool opH, const Frag& f) {
-  double re0[2] = {0.0, 0.0}, im0[2] = {0.0, 0.0}, re1[2] = {0.0, 0.0}, im1[2] = {0.0, 0.0};
+template <bool OPH>
+__device__ __forceinline__ void mma_tile_t(cd acc[2], const cd* ts, const cd* xs, const Frag& f) {
   const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
   const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
+  // all 16 fragments first (latency overlapped), then 32 DMMAs on 4 chains
+  cd a[TILE / 4], b[TILE / 4];
 #pragma unroll
   for (int kb = 0; kb < TILE / 4; ++kb) {
     const int k = 4 * kb + am;
-    const cd a = opH ? cconj(ts[ar * APAD + k]) : ts[k * APAD + ar];
-    const cd b = xs[bc * XPAD + 4 * kb + bm];
+    a[kb] = OPH ? ts[ar * APAD + k] : ts[k * APAD + ar];
+    b[kb] = xs[bc * XPAD + 4 * kb + bm];
+  }
+  double re0[2] = {0.0, 0.0}, im0[2] = {0.0, 0.0}, re1[2] = {0.0, 0.0}, im1[2] = {0.0, 0.0};
+#pragma unroll
+  for (int kb = 0; kb < TILE / 4; ++kb) {
     double* re = (kb & 1) ? re1 : re0;
     double* im = (kb & 1) ? im1 : im0;
-    dmma(re, a.x, b.x);
-    dmma(re, -a.y, b.y);
-    dmma(im, a.x, b.y);
-    dmma(im, a.y, b.x);
+    if (OPH) {  // a = conj(t): Re = t.x b.x + t.y b.y, Im = t.x b.y - t.y b.x
+      dmma(re, a[kb].x, b[kb].x);
+      dmma(re, a[kb].y, b[kb].y);
+      dmma(im, a[kb].x, b[kb].y);
+      dmma(im, -a[kb].y, b[kb].x);
+    } else {
+      dmma(re, a[kb].x, b[kb].x);
+      dmma(re, -a[kb].y, b[kb].y);
+      dmma(im, a[kb].x, b[kb].y);
+      dmma(im, a[kb].y, b[kb].x);
+    }
   }
   acc[0].x += re0[0] + re1[0];
   acc[1].x += re0[1] + re1[1];
   acc[0].y += im0[0] + im1[0];
   acc[1].y += im0[1] + im1[1];
+}
+
+__device__ __forceinline__ void mma_tile(cd acc[2], const cd* ts, const cd* xs, bool opH, const Frag& f) {
+  if (opH)
+    mma_tile_t<true>(acc, ts, xs, f);
+  else
+    mma_tile_t<false>(acc, ts, xs, f);
 }
 
 __device__ __forceinline__ void load_tile(cd* s, const cd* g) {
@@ -165,38 +185,84 @@ __device__ void owner_task(const SolveArgs& A, int ci, int gi, cd* smem) {
   unsigned long long* prog = A.prog + static_cast<size_t>(ci) * A.ngroups + gi;
   const unsigned long long tag = static_cast<unsigned long long>(A.epoch) << 32;
   const int* fc = A.flags_c + (static_cast<size_t>(ci) * A.ngroups + gi) * A.nbk;
+  cd* cstage = smem + 2 * TILE_S + 2 * XS;  // per-thread c_i staging (own elements only)
+  int* dl_s = reinterpret_cast<int*>(cstage + 2 * ST);  // envelope table, read once
+  for (int b = threadIdx.x; b < A.nbk; b += ST) dl_s[b] = A.dl[b];
+  // Roles inside the owner: thread 0 publishes (its release fence must not
+  // wait on any cp.async, so warp 0 issues none for the coupling tiles);
+  // thread 32 polls the NEXT step's c flag after the product (no poll sits in
+  // front of a barrier); cready_s is double-buffered by step parity.
+  __shared__ int cready_s[2];
+  if (threadIdx.x == 32) cready_s[0] = ld_acquire(fc + (fwd ? 0 : A.nbk - 1)) >= A.epoch;
+  __syncthreads();
   const bool tr = A.trace != nullptr && ci == 0 && gi == 0 && threadIdx.x == 0;
   for (int s = 0; s < A.nbk; ++s) {
     const int i = fwd ? s : A.nbk - 1 - s;
     if (tr) A.trace[s * 16 + 0] = gtimer();
-    if (s + 1 < A.nbk) load_tile(m_s[(s + 1) & 1], ch.m + static_cast<size_t>(fwd ? i + 1 : i - 1) * TT);
+    // coupling tile of the NEXT step: T~(i', i'-+1) is slot 1 of row i' (fwd) or i'+1 (bwd)
+    if (s + 1 < A.nbk && threadIdx.x >= 32) {
+      const int base = fwd ? i + 1 : i;
+      if (dl_s[base] >= 1) {
+        const cd* g = ch.off + lt_off(base, 1, A.J);
+        cd* sm = m_s[(s + 1) & 1];
+        for (int e = threadIdx.x - 32; e < TT; e += ST - 32)
+          cp_async16_cg(&sm[(e / TILE) * APAD + (e % TILE)], g + e);
+      }
+    }
     cp_async_commit();
     cp_async_wait<1>();  // M_i landed (issued one step earlier)
     __syncthreads();
+    if (tr) A.trace[s * 16 + 11] = gtimer();
+    const bool cready = cready_s[s & 1];
+    cd* crow = ch.cbuf + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
+    if (cready) {  // c_i already published: stream it in under the product
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (f.col + q < nc) cp_async16_cg(&cstage[threadIdx.x * 2 + q], crow + (f.col + q) * ld);
+      cp_async_commit();
+    }
     // the critical product needs only x_{i-+1} (on chip): do it before c_i arrives
     cd red[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
-    if (s > 0) mma_tile(red, m_s[s & 1], xb[(s + 1) & 1], opH, f);
+    if (s > 0 && dl_s[fwd ? i : i + 1] >= 1) mma_tile(red, m_s[s & 1], xb[(s + 1) & 1], opH, f);
+    if (tr) A.trace[s * 16 + 12] = gtimer() + (red[0].x == 1234.5 ? 1 : 0);
+    // publish x_{s-1} now: its global stores were ordered by the barriers of
+    // the previous step and have landed during the product, so the release
+    // fence is cheap and off the chain (helpers need x only 2+ steps later)
+    if (threadIdx.x == 0 && s > 0) {
+      st_release64(prog, tag | static_cast<unsigned>(s));
+      if (A.trace != nullptr && ci == 0 && gi == 0) A.trace[(s - 1) * 16 + 2] = gtimer();
+    }
+    if (threadIdx.x == 32 && s + 1 < A.nbk)
+      cready_s[(s + 1) & 1] = ld_acquire(fc + (fwd ? i + 1 : i - 1)) >= A.epoch;
     if (tr) A.trace[s * 16 + 6] = gtimer() + (red[0].x == 1234.5 ? 1 : 0);
-    wait_flag(fc + i, A.epoch, A.counter + 2);
+    cd cv[2];
+    if (cready) {
+      cp_async_wait<0>();  // this thread's own copies: no barrier needed to read them
+#pragma unroll
+      for (int q = 0; q < 2; ++q) cv[q] = (f.col + q < nc) ? cstage[threadIdx.x * 2 + q] : mk(0.0, 0.0);
+    } else {
+      wait_flag(fc + i, A.epoch, A.counter + 2);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) cv[q] = (f.col + q < nc) ? __ldcg(crow + (f.col + q) * ld) : mk(0.0, 0.0);
+    }
     if (tr) A.trace[s * 16 + 1] = gtimer();
+    cd* xrow = ch.dst + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int c = f.col + q;
-      const cd cv = (c < nc) ? __ldcg(ch.cbuf + static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld)
-                             : mk(0.0, 0.0);
-      xb[s & 1][c * XPAD + f.row] = csub(cv, red[q]);
+      const cd x = csub(cv[q], red[q]);
+      xb[s & 1][c * XPAD + f.row] = x;
+      if (c < nc) xrow[c * ld] = x;
     }
-    __syncthreads();
-    store_x(ch.dst + static_cast<int64_t>(i) * TILE, xb[s & 1], ld, c0, nc);
     __syncthreads();
     if (tr) A.trace[s * 16 + 7] = gtimer();
-    if (threadIdx.x == 0) {
-      st_release64(prog, tag | static_cast<unsigned>(s + 1));  // cumulative release after the barrier
-      if (tr) A.trace[s * 16 + 2] = gtimer();
-    }
   }
   cp_async_wait<0>();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    st_release64(prog, tag | static_cast<unsigned>(A.nbk));  // cumulative release after the barrier
+    if (A.trace != nullptr && ci == 0 && gi == 0) A.trace[(A.nbk - 1) * 16 + 2] = gtimer();
+  }
 }
 
 // HELPER: c_i = op(Dinv_i) (b_i - sum_{d>=2} op(T_(i,i-+d)) x_(i-+d)).
@@ -232,12 +298,22 @@ __device__ void helper_task(const SolveArgs& A, int s, int ci, int gi, cd* smem,
     }
     nlist_s = n;
   }
-  load_tile(dinv_s, ch.dinv + static_cast<size_t>(i) * TT);
+  // b~_i = op(Dinv_i) b_i (or b_i): off the critical path, before any dependency
   cd bval[2];
+  if (ch.pre) {
+    load_tile(dinv_s, ch.pre + static_cast<size_t>(i) * TT);
+    load_x(acc_s, ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    bval[0] = bval[1] = mk(0.0, 0.0);
+    mma_tile(bval, dinv_s, acc_s, opH, f);
+  } else {
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int c = f.col + q;
-    bval[q] = (c < nc) ? ch.src[static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld] : mk(0.0, 0.0);
+    for (int q = 0; q < 2; ++q) {
+      const int c = f.col + q;
+      bval[q] = (c < nc) ? ch.src[static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld] : mk(0.0, 0.0);
+    }
   }
   __syncthreads();
   const int nl = nlist_s;
@@ -294,10 +370,8 @@ __device__ void helper_task(const SolveArgs& A, int s, int ci, int gi, cd* smem,
   int nfar = 0;
   for (int q = 0; q < nl; ++q) {
     const int buf = q % NS, d = dlist[q];
-    if (q + NS - 1 < nl) issue(q + NS - 1);
-    cp_async_commit();
     if (d >= NEAR) {
-      cp_async_wait<NS - 1>();
+      cp_async_wait<NS - 2>();  // entry q landed; entries q+1..q+NS-2 may be in flight
       ++nfar;
     } else {
       if (tr && nfar >= 0) {
@@ -310,24 +384,20 @@ __device__ void helper_task(const SolveArgs& A, int s, int ci, int gi, cd* smem,
       cp_async_commit();
       cp_async_wait<0>();
     }
+    // one barrier per tile: entry q is visible to all warps and every warp has
+    // finished entry q-1, whose stage the next issue refills
     __syncthreads();
+    if (q + NS - 1 < nl) issue(q + NS - 1);
+    cp_async_commit();
     mma_tile(acc, tile_s(buf), x_s(buf), opH, f);
-    __syncthreads();
   }
   cp_async_wait<0>();
-  __syncthreads();
   if (tr) A.trace[s * 16 + 4] = gtimer();
-  // c_i = op(Dinv_i) (b_i - acc)
+  // c_i = b~_i - acc: no diagonal work left on the critical path
+  cd* crow = ch.cbuf + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
 #pragma unroll
-  for (int q = 0; q < 2; ++q) acc_s[(f.col + q) * XPAD + f.row] = csub(bval[q], acc[q]);
-  __syncthreads();
-  cd out[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
-  mma_tile(out, dinv_s, acc_s, opH, f);
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 2; ++q) acc_s[(f.col + q) * XPAD + f.row] = out[q];
-  __syncthreads();
-  store_x(ch.cbuf + static_cast<int64_t>(i) * TILE, acc_s, ld, c0, nc);
+  for (int q = 0; q < 2; ++q)
+    if (f.col + q < nc) crow[(f.col + q) * ld] = csub(bval[q], acc[q]);
   __syncthreads();
   if (threadIdx.x == 0) {
     st_release(fc + i, A.epoch);  // cumulative release after the barrier
@@ -359,7 +429,30 @@ __global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
   }
 }
 
+// x_i <- op(D_i) x_i per (block row, 16-column group): the adjoint post-pass.
+__global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
+  __shared__ __align__(16) cd ds[TILE_S];
+  __shared__ __align__(16) cd xs[XS];
+  const int i = blockIdx.x, c0 = blockIdx.y * CG, nc = min(CG, ncols - c0);
+  const Frag f = frag();
+  load_tile(ds, D + static_cast<size_t>(i) * TT);
+  load_x(xs, x + static_cast<int64_t>(i) * TILE, ld, c0, nc);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  cd out[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+  mma_tile(out, ds, xs, opH, f);
+  cd* row = x + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (f.col + q < nc) row[(f.col + q) * ld] = out[q];
+}
+
 }  // namespace
+
+void blockdiag_apply(cudaStream_t st, const BandGeom& g, const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
+  if (ncols > 0) blockdiag_kernel<<<dim3(g.nbk, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld);
+}
 
 int trsm_launch(cudaStream_t st, const BandGeom& g, const Chain* d_chains, int nchains, int ncols, int64_t ld,
                 unsigned long long* prog, int* flags_c, int epoch, int* counter, int fwd, int num_sms,

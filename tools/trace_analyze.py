@@ -21,3 +21,6 @@ print(f"helper: start->pipeline {med(c(10) - c(3)):.2f} | far tiles {med(c(8) - 
 print(f"far tiles done -> x_(i-3) published (slack, +: waits): {med(c(2)[:-3] - c(8)[3:]):.2f} us")
 print(f"x_(i-2) published -> helper all tiles done {med(c(4)[2:] - c(2)[:-2]):.2f} | -> c published {med(c(5)[2:] - c(2)[:-2]):.2f}")
 print(f"helper c_i published -> owner saw c_i {med(c(1) - c(5)):.2f} us")
+if raw.shape[1] > 12 and (raw[:, 11] > 0).any():
+    print(f"owner detail: start->barrier1 {med(c(11) - c(0)):.2f} | barrier1->product done {med(c(12) - c(11)):.2f} | "
+          f"->after release {med(c(6) - c(12)):.2f}")
