@@ -142,6 +142,35 @@ int zolo_rr_project(zolo_ctx* ctx, const double* y, int64_t k, double* a_tilde, 
  * y n x k, q_small k x kk (host), out n x kk (host). */
 int zolo_block_update(zolo_ctx* ctx, const double* y, int64_t k, const double* q_small, int64_t kk, double* out);
 
+/* --- device-resident block helpers (original ordering, leading dimension n) */
+/* out = A x (which = 0) or B x (which = 1; a copy when B = I), k columns. */
+int zolo_spmm_device(zolo_ctx* ctx, int which, const void* d_x, void* d_out, int64_t k);
+/* out (host, k x kk column-major) = Y^H Z. */
+int zolo_gram_device(zolo_ctx* ctx, const void* d_y, const void* d_z, int64_t k, int64_t kk, double* out);
+/* d_out (n x kk) = Y (n x k) * q (host, k x kk). */
+int zolo_block_gemm_device(zolo_ctx* ctx, const void* d_y, int64_t k, const double* q, int64_t kk, void* d_out);
+/* per column: num = ||ax - lambda bx||^2, den = ||bx||^2 (relative_residual, eigensolver.hpp:77-93). */
+int zolo_residual_norms_device(zolo_ctx* ctx, const void* d_ax, const void* d_bx, int64_t k, const double* lambdas,
+                               double* num, double* den);
+
+/* --- driver: subspace_iteration (eigensolver.hpp:154-217) ---------------- */
+/* Filtered subspace iteration with Rayleigh-Ritz on this context's GPU:
+ * builds the design for window_from_gaps(gaps) at order r (r <= 0 picks
+ * choose_order, filter_design.hpp:219-232), factorizes, iterates. lambdas
+ * has room for n_lambda + oversample values; vectors (optional) for
+ * n x (n_lambda + oversample) entries. stats (12 doubles): n_ss, n_iter,
+ * n_gmres, n_gmres_min, n_solv, t_fact [s], t_iter [s], residual (reference
+ * scaling max(|a|,|b|)), converged, r, residual scaled by |lambda|,
+ * device filter time [ms]. */
+int zolo_subspace_iteration(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
+                            const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v,
+                            const double* gaps, int64_t n_lambda, int64_t oversample, int r, double tol,
+                            int64_t max_iters, double gmres_tol, int64_t gmres_max, uint64_t seed, double* lambdas,
+                            int64_t* n_found, double* vectors, double* stats);
+
+/* Set the context's (or, with NULL, the global) last-error message. */
+void zolo_set_error(zolo_ctx* ctx, const char* msg);
+
 /* --- timing of the last device call (CUDA events on the context stream) - */
 /* ms[0] = last apply_filter device time, ms[1] = last factorize device time,
  * ms[2] = solve-kernel time summed over the last apply_filter,

@@ -138,7 +138,7 @@ struct zolo_ctx {
   int maxit_cap = 0;
   std::vector<std::unique_ptr<DevMem>> basis;
   DevMem basis_ptrs, gH, gR, gG, gROT, gY, gZ, gres, gfrozen, gmlen, gbeta, gmcol, ghappy, gdone, gwnorm;
-  DevMem partial, hsave, act_d, rr_partial, rr_tmp, rr_out;
+  DevMem partial, hsave, act_d, rr_partial, rr_tmp, rr_out, tmp1, tmp2, tmp3;
   int* act_h = nullptr;
   int* done_h = nullptr;
 
@@ -793,11 +793,117 @@ void block_update_impl(zolo_ctx& c, const double* y, int64_t k, const double* q,
   CK(cudaGetLastError());
 }
 
+// ---- device-block helpers for the host driver (original ordering, ld = n) ----
+template <class S>
+void spmm_dev_impl(zolo_ctx& c, int which, const void* x, void* out, int64_t k) {
+  ensure_perm_csr(c);
+  const int64_t n = c.n, ld = c.geom.npad;
+  const size_t es = sizeof(S);
+  if (which == 1 && c.b_identity) {
+    CK(cudaMemcpyAsync(out, x, es * n * k, cudaMemcpyDeviceToDevice, c.st));
+    return;
+  }
+  c.tmp1.ensure(es * ld * k);
+  c.tmp2.ensure(es * ld * k);
+  Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(x), n, c.tmp1.as<S>(), ld, k, c.perm_d.as<int>());
+  if (which == 0)
+    Krylov<S>::spmm(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), c.tmp1.as<S>(), k,
+                    c.tmp2.as<S>());
+  else
+    Krylov<S>::spmm(c.st, n, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), c.tmp1.as<S>(), k,
+                    c.tmp2.as<S>());
+  Krylov<S>::permute_out(c.st, c.tmp2.as<S>(), ld, reinterpret_cast<S*>(out), n, k, c.perm_d.as<int>());
+  CK(cudaGetLastError());
+}
+
+template <class S>
+void gram_dev_impl(zolo_ctx& c, const void* y, const void* z, int64_t k, int64_t kk, double* out) {
+  const int64_t n = c.n;
+  const int64_t nchunk = (n + CHUNK - 1) / CHUNK;
+  c.rr_partial.ensure(sizeof(S) * nchunk * k * kk + 64);
+  c.rr_out.ensure(sizeof(S) * k * kk);
+  Krylov<S>::gram(c.st, n, n, reinterpret_cast<const S*>(y), k, reinterpret_cast<const S*>(z), kk, c.rr_out.as<S>(),
+                  c.rr_partial.as<double>());
+  CK(cudaMemcpyAsync(out, c.rr_out.p, sizeof(S) * k * kk, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+}
+
+template <class S>
+void gemm_dev_impl(zolo_ctx& c, const void* y, int64_t k, const double* q, int64_t kk, void* out) {
+  c.tmp3.ensure(sizeof(S) * k * kk);
+  CK(cudaMemcpyAsync(c.tmp3.p, q, sizeof(S) * k * kk, cudaMemcpyHostToDevice, c.st));
+  Krylov<S>::block_gemm(c.st, c.n, c.n, reinterpret_cast<const S*>(y), k, c.tmp3.as<S>(), kk,
+                        reinterpret_cast<S*>(out));
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+}
+
+template <class S>
+void resid_dev_impl(zolo_ctx& c, const void* ax, const void* bx, int64_t k, const double* lam, double* num,
+                    double* den) {
+  c.tmp3.ensure(sizeof(double) * 3 * k + 64);
+  double* d = c.tmp3.as<double>();
+  CK(cudaMemcpyAsync(d, lam, sizeof(double) * k, cudaMemcpyHostToDevice, c.st));
+  Krylov<S>::residuals(c.st, c.n, reinterpret_cast<const S*>(ax), reinterpret_cast<const S*>(bx), d, k, d + k,
+                       d + 2 * k);
+  CK(cudaMemcpyAsync(num, d + k, sizeof(double) * k, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaMemcpyAsync(den, d + 2 * k, sizeof(double) * k, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* zolo_version(void) { return "zolo-b200 0.1.0 (sm_100a)"; }
+
+int zolo_spmm_device(zolo_ctx* c, int which, const void* d_x, void* d_out, int64_t k) {
+  return guarded(c, [&] {
+    require(c->have_pencil, "spmm: no pencil");
+    require(which == 0 || which == 1, "spmm: which must be 0 (A) or 1 (B)");
+    if (k <= 0) return;
+    if (c->cx)
+      spmm_dev_impl<cd>(*c, which, d_x, d_out, k);
+    else
+      spmm_dev_impl<double>(*c, which, d_x, d_out, k);
+  });
+}
+
+int zolo_gram_device(zolo_ctx* c, const void* d_y, const void* d_z, int64_t k, int64_t kk, double* out) {
+  return guarded(c, [&] {
+    require(c->have_pencil, "gram: no pencil");
+    if (k <= 0 || kk <= 0) return;
+    if (c->cx)
+      gram_dev_impl<cd>(*c, d_y, d_z, k, kk, out);
+    else
+      gram_dev_impl<double>(*c, d_y, d_z, k, kk, out);
+  });
+}
+
+int zolo_block_gemm_device(zolo_ctx* c, const void* d_y, int64_t k, const double* q, int64_t kk, void* d_out) {
+  return guarded(c, [&] {
+    require(c->have_pencil, "block_gemm: no pencil");
+    if (kk <= 0) return;
+    if (c->cx)
+      gemm_dev_impl<cd>(*c, d_y, k, q, kk, d_out);
+    else
+      gemm_dev_impl<double>(*c, d_y, k, q, kk, d_out);
+  });
+}
+
+int zolo_residual_norms_device(zolo_ctx* c, const void* d_ax, const void* d_bx, int64_t k, const double* lambdas,
+                               double* num, double* den) {
+  return guarded(c, [&] {
+    require(c->have_pencil, "residuals: no pencil");
+    if (k <= 0) return;
+    if (c->cx)
+      resid_dev_impl<cd>(*c, d_ax, d_bx, k, lambdas, num, den);
+    else
+      resid_dev_impl<double>(*c, d_ax, d_bx, k, lambdas, num, den);
+  });
+}
 
 int zolo_ctx_create(int device, zolo_ctx** out) {
   *out = nullptr;
@@ -846,6 +952,13 @@ int zolo_ctx_destroy(zolo_ctx* c) {
 }
 
 const char* zolo_last_error(const zolo_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+void zolo_set_error(zolo_ctx* c, const char* msg) {
+  if (c)
+    c->err = msg;
+  else
+    g_create_err = msg;
+}
 
 int zolo_pencil_upload(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
                        const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v) {

@@ -476,6 +476,23 @@ void build_filter_design(const double* gaps, int r, double* o) {
   for (double c : d.outer.c) *o++ = c;
 }
 
+// choose_order (filter_design.hpp:219-232): smallest r in [1,8] whose Gonchar
+// upper bound (goncar_rho / goncar_bracket, filter_design.hpp:180-196) meets eps.
+int choose_order(const double* gaps, double eps) {
+  if (!(eps >= 1e-16) || !(eps < 1.0)) throw DesignError(1, "choose_order: eps outside [1e-16, 1)");
+  const Mobius fit = fit_mobius(window_from_gaps(gaps[0], gaps[1], gaps[2], gaps[3]));
+  const double mu = (1.0 - std::sqrt(fit.ell1)) / (1.0 + std::sqrt(fit.ell1));
+  const double mu_c = std::sqrt((1.0 - mu) * (1.0 + mu));
+  const double rho = std::exp(M_PI * k_complement(mu) / (4.0 * k_complement(mu_c)));
+  for (int r = 1; r <= 8; ++r) {
+    const int deg = 2 * r;
+    const double pw = std::exp(deg * deg * std::log(rho));
+    const double upper = (pw > 1.0) ? 2.0 / (pw - 1.0) : std::numeric_limits<double>::infinity();
+    if (upper <= eps) return r;
+  }
+  return 8;
+}
+
 void eval_filter_scalar(const double* gaps, int r, int64_t npts, const double* x, double* g_out, double* f_out) {
   const Design d = build(gaps, r);
   for (int64_t i = 0; i < npts; ++i) {

@@ -15,5 +15,6 @@ int64_t profile_under(int64_t n, const int64_t* rp, const int64_t* ci, const int
 void uniform_stream(uint64_t seed, int64_t n, double* out);
 bool random_block(int cx, int64_t n, int64_t k, uint64_t seed, bool orthonormalize, double* out);
 void build_filter_design(const double* gaps, int r, double* out);
+int choose_order(const double* gaps, double eps);
 void eval_filter_scalar(const double* gaps, int r, int64_t npts, const double* x, double* g_out, double* f_out);
 }  // namespace zolo

@@ -462,6 +462,37 @@ __global__ void block_gemm_kernel(int64_t ld, const S* y, int64_t k, const S* q,
   out[t + j * ld] = acc;
 }
 
+// Per column c: num = sum_t |ax - lambda_c bx|^2, den = sum_t |bx|^2
+// (relative_residual, eigensolver.hpp:77-93).
+template <class S>
+__global__ void residual_kernel(int64_t n, const S* ax, const S* bx, const double* lam, double* num, double* den) {
+  __shared__ double r1[32], r2[32];
+  const int64_t c = blockIdx.x;
+  const double l = lam[c];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+    const S b = bx[t + c * n];
+    s1 += sabs2(ssub(ax[t + c * n], sscale(b, l)));
+    s2 += sabs2(b);
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if ((threadIdx.x & 31) == 0) {
+    r1[threadIdx.x >> 5] = s1;
+    r2[threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      a += r1[w];
+      b += r2[w];
+    }
+    num[c] = a;
+    den[c] = b;
+  }
+}
+
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 }  // namespace
@@ -542,6 +573,12 @@ template <class S>
 void Krylov<S>::spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
                      int64_t k, S* out) {
   if (k > 0) spmm_kernel<S><<<dim3(blocks_for(ld, 256), k), 256, 0, st>>>(n, ld, rp, ci, vals, v, out);
+}
+
+template <class S>
+void Krylov<S>::residuals(cudaStream_t st, int64_t n, const S* ax, const S* bx, const double* lam, int64_t k,
+                          double* num, double* den) {
+  if (k > 0) residual_kernel<S><<<k, 512, 0, st>>>(n, ax, bx, lam, num, den);
 }
 
 void gmres_init(cudaStream_t st, GmresDev g) { gmres_init_kernel<<<g.nv, 32, 0, st>>>(g); }

@@ -58,6 +58,9 @@ struct Krylov {
   // out (ld x kk) = Y (ld x k) * Q (k x kk)
   static void block_gemm(cudaStream_t st, int64_t n, int64_t ld, const S* y, int64_t k, const S* q, int64_t kk,
                          S* out);
+  // per column: num = ||ax - lam bx||^2, den = ||bx||^2 (n x k, ld = n)
+  static void residuals(cudaStream_t st, int64_t n, const S* ax, const S* bx, const double* lam, int64_t k,
+                        double* num, double* den);
   // out (ld x k) = M * V (M permuted CSR with S values)
   static void spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
                    int64_t k, S* out);

@@ -135,3 +135,35 @@ def test_cfg1_full_size_against_reference(zb):
         yr, cols = o["y"], o["column_iterations"]
     assert rel_fro(y, yr) <= 1e-9
     assert np.abs(np.array(rep.column_iterations) - cols).max() <= 1
+
+
+@pytest.mark.parametrize("name", ["cfg1_k16", "cfg2_k6", "cfg3_k5"])
+def test_subspace_iteration_matches_reference(zb, name):
+    """north_star parity: count in (a,b) exact, eigenvalues within 1e-10 of the
+    reference scale max(|a|,|b|) (test_eigensolver.cpp:179), residuals <= 1e-8
+    in both normalisations, B-orthonormal vectors, and the solve tally bound
+    n_solv <= r * n_ss * n_iter * n_gmres (test_eigensolver.cpp:187-201)."""
+    from paper_1701_08935_b200.driver import SolveConfig, subspace_iteration
+
+    g = load_golden("solve_driver_" + name)
+    cx, r = bool(g["cx"]), int(g["r"])
+    pen = golden_pencil(g)
+    cfg = SolveConfig(n_lambda=int(g["n_lambda"]), oversample_k=int(g["oversample"]), r=r, tol=1e-10, seed=1)
+    res = subspace_iteration(pen, g["gaps"], cfg, is_complex=cx, want_vectors=True)
+    assert res.converged and bool(g["converged"])
+    assert len(res.lambdas) == len(g["lambdas"]) == int(g["n_lambda"])
+    scale = max(abs(g["design"][0]), abs(g["design"][1]))
+    assert np.abs(res.lambdas - g["lambdas"]).max() <= 1e-10 * scale
+    assert np.abs(res.lambdas - g["exact"]).max() <= 1e-10 * scale
+    assert res.residual <= 1e-10 and res.residual_rel_lambda <= 1e-8
+    # B-orthonormality of the returned block
+    from pencils import to_scipy
+
+    n = pen[0]
+    bm = to_scipy(pen[2], n) if pen[2] is not None else None
+    x = res.vectors
+    bx = bm @ x if bm is not None else x
+    gram = x.conj().T @ bx
+    assert np.abs(gram - np.eye(gram.shape[0])).max() <= 1e-8
+    chains = 2 if cx else 1
+    assert res.stats.n_solv <= chains * r * cfg.subspace_size() * res.stats.n_iter * res.stats.n_gmres
