@@ -167,3 +167,23 @@ def test_subspace_iteration_matches_reference(zb, name):
     assert np.abs(gram - np.eye(gram.shape[0])).max() <= 1e-8
     chains = 2 if cx else 1
     assert res.stats.n_solv <= chains * r * cfg.subspace_size() * res.stats.n_iter * res.stats.n_gmres
+
+
+def test_cpp_dropin_adapter_matches_reference_operator():
+    """The C++ drop-in: zolo_b200::GpuFilterOperator<S> next to the reference's
+    zoloeig::FilterOperator<S> in one program (oracle/dropin_test.cpp)."""
+    import json
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_test not built (needs the reference headers at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    lines = [json.loads(s) for s in out.stdout.strip().splitlines()]
+    assert len(lines) == 2
+    for d in lines:
+        assert d["rel_fro_filter"] <= 1e-9 and d["rel_fro_apply_g"] <= 1e-11
+        assert abs(d["ref_iterations"] - d["gpu_iterations"]) <= 1
+        assert d["gpu_inner_solves"] == (2 if "complex" in d["case"] else 1) * d["r"] * d["gpu_g_apps"]
+        assert d["domain_error_ok"]
