@@ -108,6 +108,19 @@ int zolo_set_design(zolo_ctx* ctx, const double* design, int r);
  * returns ZOLO_ERR_FACTORIZATION with stats[j].pivot_index set. */
 int zolo_factorize(zolo_ctx* ctx, const int64_t* perm, zolo_factor_stats* stats);
 
+/* Ordering / factor layout used by zolo_factorize:
+ *   ZOLO_ORDER_ND   (default) nested dissection (recursive BFS-level bisection,
+ *                   leaves of <= nd_leaf rows ordered by RCM), block-sparse
+ *                   32x32-tile factors, DAG-scheduled sweeps -- short
+ *                   dependency chains;
+ *   ZOLO_ORDER_RCM  the reference's RCM ordering and banded factors
+ *                   (band_factor.hpp), envelope-aware block band, pipelined
+ *                   sweeps; FactorizationError indices match the reference.
+ * With an explicit perm in zolo_factorize, ND mode factors that ordering as
+ * block-sparse (no dissection). Pivot indices refer to the chosen order. */
+enum { ZOLO_ORDER_ND = 0, ZOLO_ORDER_RCM = 1 };
+int zolo_set_ordering(zolo_ctx* ctx, int mode, int64_t nd_leaf);
+
 /* FilterOperator(pencil, design): upload + set_design + factorize. */
 int zolo_filter_create(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
                        const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v,

@@ -28,6 +28,9 @@ LIB_PATH = os.path.join(HERE, "libzolo_b200.so")
 
 ZOLO_OK, ZOLO_ERR_DOMAIN, ZOLO_ERR_NUMERICAL, ZOLO_ERR_FACTORIZATION, ZOLO_ERR_GMRES, ZOLO_ERR_CUDA = range(6)
 MAX_ORDER = 16
+# factor layouts (include/zolo_b200.h ZOLO_ORDER_*): nested-dissection block-sparse
+# factors with DAG-scheduled sweeps, or the reference's RCM band.
+ORDERINGS = {"nd": 0, "rcm": 1}
 
 
 class DomainError(ValueError):
@@ -122,6 +125,7 @@ def lib():
         L.zolo_ctx_destroy.argtypes = [P]
         L.zolo_pencil_upload.argtypes = [P, I64, C.c_int, P, P, P, P, P, P]
         L.zolo_set_design.argtypes = [P, P, C.c_int]
+        L.zolo_set_ordering.argtypes = [P, C.c_int, I64]
         L.zolo_factorize.argtypes = [P, P, P]
         L.zolo_apply_g.argtypes = [P, P, P, I64]
         L.zolo_apply_filter.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
@@ -209,7 +213,8 @@ class FilterOperator:
     ``is_complex`` selects S = complex128 (Hermitian pencil) vs float64.
     """
 
-    def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None):
+    def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None,
+                 ordering: str = "nd", nd_leaf: int = 512):
         L = lib()
         n, a, b = pencil
         cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
@@ -229,6 +234,9 @@ class FilterOperator:
         bp = self._b if self._b is not None else (None, None, None)
         _check(h, L.zolo_pencil_upload(h, self.n, int(cx), *map(_ptr, self._a), *map(_ptr, bp)))
         _check(h, L.zolo_set_design(h, _ptr(self.design), self.r))
+        if ordering not in ORDERINGS:
+            raise DomainError(f"ordering must be one of {sorted(ORDERINGS)}")
+        _check(h, L.zolo_set_ordering(h, ORDERINGS[ordering], int(nd_leaf)))
         self.stats = (FactorStats * self.r)()
         perm_arr = None if perm is None else np.ascontiguousarray(perm, dtype=np.int64)
         st = L.zolo_factorize(h, _ptr(perm_arr), self.stats)

@@ -23,6 +23,8 @@
 // zeros and are skipped by the factorization and the solves.
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace zolo {
@@ -83,9 +85,44 @@ void factor_scatter(cudaStream_t st, const BandGeom& g, const FactorTiles& f, in
 void factor_run(cudaStream_t st, const BandGeom& g, const FactorTiles& f, const double* row_norm,
                 FactorDevState ds, int cx);
 
+// ---- block-sparse factors (any node ordering; host symbolic.cpp) ----------
+// Off-diagonal tile ids are row-major slots: row i's tiles (i, row_idx[e]),
+// e in [row_ptr[i], row_ptr[i+1]) ascending; column k's structural rows
+// col_idx[e] (ascending) carry their tile id in col_tile[e]; tile_row[e] = i.
+// L(i,k) lives in Lt[id], U(k,i) in Ut[id]; diagonal blocks in Dt.
+struct SpGeom {
+  int64_t n = 0, npad = 0;
+  int nb = 0;
+  int64_t ntiles = 0;
+  int max_deps = 0;
+  const int* row_ptr = nullptr;
+  const int* row_idx = nullptr;
+  const int* col_ptr = nullptr;
+  const int* col_idx = nullptr;
+  const int* col_tile = nullptr;
+  const int* tile_row = nullptr;
+};
+
+struct SpFactor {
+  cd* Dt = nullptr;
+  cd* Lt = nullptr;
+  cd* Ut = nullptr;
+  cd* DinvL = nullptr;
+  cd* DinvU = nullptr;
+};
+
+void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt, const SpFactor& f, int64_t nnz,
+               const int* e_row, const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
+               double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err);
+
+// DAG-scheduled sweeps over block-sparse row-scaled tiles: one task per
+// (block row, chain, column group), claimed in topological order.
+int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const Chain* d_chains, int nchains, int ncols, int64_t ld,
+                    int* flags, int epoch, int* counter, int fwd, int num_sms);
+
 // x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass
 // x_i = DinvL_i^H w_i); x is ld x ncols, D is nbk tiles.
-void blockdiag_apply(cudaStream_t st, const BandGeom& g, const cd* D, bool opH, cd* x, int ncols, int64_t ld);
+void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld);
 
 // One launch covers nchains x ngroups independent pipelines (owner + helpers).
 // Returns the number of resident CTAs needed (error if owners do not fit).

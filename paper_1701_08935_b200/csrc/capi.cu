@@ -131,6 +131,16 @@ struct zolo_ctx {
   DevMem dl_d, trace_buf;
   int64_t env_tiles = 0;
   bool trace_done = false;
+
+  // block-sparse (nested dissection) factor path
+  int order_mode = ZOLO_ORDER_ND;
+  int64_t nd_leaf = 512;
+  bool sparse = false;
+  SpGeom sgeom;
+  std::vector<int> sp_col_cnt;
+  int64_t critical_path = 0;
+  DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
+  std::vector<cd*> sp_dt;
   int64_t flags_cap = 0, prog_cap = 0;
   int epoch = 0;
 
@@ -209,59 +219,79 @@ Union union_pattern(const zolo_ctx& c) {
   return u;
 }
 
-// P M P^T as int32 CSR with sorted columns.
-void permuted_csr(int64_t n, const std::vector<int64_t>& rp, const std::vector<int64_t>& ci,
-                  const std::vector<double>& v, int w, const std::vector<int64_t>& perm, const std::vector<int>& pos,
+// P M P^T as int32 CSR over the npad device positions (padding rows empty),
+// sorted columns. inv: position -> original row or -1; pos: original -> position.
+void permuted_csr(int64_t npad, const std::vector<int64_t>& inv, const std::vector<int>& pos,
+                  const std::vector<int64_t>& rp, const std::vector<int64_t>& ci, const std::vector<double>& v, int w,
                   std::vector<int>& prp, std::vector<int>& pci, std::vector<double>& pv) {
-  prp.assign(n + 1, 0);
+  prp.assign(npad + 1, 0);
   pci.clear();
   pv.clear();
   std::vector<std::pair<int, int64_t>> row;
-  for (int64_t t = 0; t < n; ++t) {
-    const int64_t i = perm[t];
-    row.clear();
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) row.emplace_back(pos[ci[k]], k);
-    std::sort(row.begin(), row.end());
-    for (auto& e : row) {
-      pci.push_back(e.first);
-      for (int q = 0; q < w; ++q) pv.push_back(v[e.second * w + q]);
+  for (int64_t t = 0; t < npad; ++t) {
+    const int64_t i = inv[t];
+    if (i >= 0) {
+      row.clear();
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) row.emplace_back(pos[ci[k]], k);
+      std::sort(row.begin(), row.end());
+      for (auto& e : row) {
+        pci.push_back(e.first);
+        for (int q = 0; q < w; ++q) pv.push_back(v[e.second * w + q]);
+      }
     }
     prp[t + 1] = static_cast<int>(pci.size());
   }
 }
 
-void ensure_perm_csr(zolo_ctx& c) {
-  if (c.have_perm) return;
-  require(c.have_pencil, "no pencil uploaded");
-  c.perm.resize(c.n);
-  for (int64_t i = 0; i < c.n; ++i) c.perm[i] = i;
-  std::vector<int> pos(c.n), prp, pci;
-  for (int64_t i = 0; i < c.n; ++i) pos[i] = static_cast<int>(i);
-  std::vector<double> pv;
+// Device copies of the pencil in the factor ordering + the position map.
+void upload_device_pencil(zolo_ctx& c, const std::vector<int64_t>& inv, const std::vector<int>& pos) {
   const int w = c.cx ? 2 : 1;
-  permuted_csr(c.n, c.a_rp, c.a_ci, c.a_v, w, c.perm, pos, prp, pci, pv);
+  const int64_t npad = static_cast<int64_t>(inv.size());
+  std::vector<int> prp, pci;
+  std::vector<double> pv;
+  permuted_csr(npad, inv, pos, c.a_rp, c.a_ci, c.a_v, w, prp, pci, pv);
   upload(c.arp_d, prp, c.st);
   upload(c.aci_d, pci, c.st);
   upload(c.av_d, pv, c.st);
   if (!c.b_identity) {
-    permuted_csr(c.n, c.b_rp, c.b_ci, c.b_v, w, c.perm, pos, prp, pci, pv);
+    permuted_csr(npad, inv, pos, c.b_rp, c.b_ci, c.b_v, w, prp, pci, pv);
     upload(c.brp_d, prp, c.st);
     upload(c.bci_d, pci, c.st);
     upload(c.bv_d, pv, c.st);
   }
-  std::vector<int> p32(c.perm.begin(), c.perm.end());
+  std::vector<int> p32(inv.begin(), inv.end());
   upload(c.perm_d, p32, c.st);
+  c.have_perm = true;
+}
+
+void ensure_perm_csr(zolo_ctx& c) {
+  if (c.have_perm) return;
+  require(c.have_pencil, "no pencil uploaded");
   c.geom.n = c.n;
   c.geom.nbk = static_cast<int>((c.n + TILE - 1) / TILE);
   c.geom.npad = static_cast<int64_t>(c.geom.nbk) * TILE;
-  c.have_perm = true;
+  std::vector<int64_t> inv(c.geom.npad, -1);
+  std::vector<int> pos(c.n);
+  for (int64_t i = 0; i < c.n; ++i) {
+    inv[i] = i;
+    pos[i] = static_cast<int>(i);
+  }
+  upload_device_pencil(c, inv, pos);
 }
+
+// Block-sparse factors under nested dissection (symbolic.cpp) -- or under a
+// caller ordering given as perm -- for every pole.
+void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats);
 
 void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats) {
   require(c.have_pencil, "zolo_factorize: no pencil uploaded");
   require(c.have_design, "zolo_factorize: no design installed");
+  if (c.order_mode == ZOLO_ORDER_ND) {
+    do_factorize_sparse(c, perm_in, stats);
+    return;
+  }
+  c.sparse = false;
   const int64_t n = c.n;
-  const int w = c.cx ? 2 : 1;
   Union u = union_pattern(c);
   c.perm.resize(n);
   if (perm_in) {
@@ -322,21 +352,9 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
 
   // device pencil in the factor ordering (SpMM with A, B)
   {
-    std::vector<int> prp, pci;
-    std::vector<double> pv;
-    permuted_csr(n, c.a_rp, c.a_ci, c.a_v, w, c.perm, pos, prp, pci, pv);
-    upload(c.arp_d, prp, c.st);
-    upload(c.aci_d, pci, c.st);
-    upload(c.av_d, pv, c.st);
-    if (!c.b_identity) {
-      permuted_csr(n, c.b_rp, c.b_ci, c.b_v, w, c.perm, pos, prp, pci, pv);
-      upload(c.brp_d, prp, c.st);
-      upload(c.bci_d, pci, c.st);
-      upload(c.bv_d, pv, c.st);
-    }
-    std::vector<int> p32(c.perm.begin(), c.perm.end());
-    upload(c.perm_d, p32, c.st);
-    c.have_perm = true;
+    std::vector<int64_t> inv(g.npad, -1);
+    for (int64_t t = 0; t < n; ++t) inv[t] = c.perm[t];
+    upload_device_pencil(c, inv, pos);
   }
 
   // tiles for r poles
@@ -422,6 +440,183 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
                     "factorize: pivot " + std::to_string(fail_any) + " below threshold");
 }
 
+void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats) {
+  const int64_t n = c.n;
+  Union u = union_pattern(c);
+  std::vector<std::vector<int64_t>> nodes;
+  if (perm_in) {
+    std::vector<char> seen(n, 0);
+    std::vector<int64_t> one(n);
+    for (int64_t i = 0; i < n; ++i) {
+      require(perm_in[i] >= 0 && perm_in[i] < n && !seen[perm_in[i]], "zolo_factorize: invalid permutation");
+      seen[perm_in[i]] = 1;
+      one[i] = perm_in[i];
+    }
+    nodes.push_back(std::move(one));
+  } else {
+    nd_order(n, u.rp.data(), u.ci.data(), c.nd_leaf, nodes);
+  }
+  BlockStructure bs;
+  block_symbolic(n, u.rp.data(), u.ci.data(), nodes, TILE, bs);
+  require(bs.ntiles < (int64_t(1) << 31) && bs.npad < (int64_t(1) << 31), "zolo_factorize: structure too large");
+  const int nb = static_cast<int>(bs.nb);
+  std::vector<int> pos(n);
+  for (int64_t i = 0; i < n; ++i) pos[i] = static_cast<int>(bs.pos[i]);
+  c.perm.assign(n, 0);
+  for (int64_t t = 0, q = 0; t < bs.npad; ++t)
+    if (bs.inv[t] >= 0) c.perm[q++] = bs.inv[t];
+  c.critical_path = bs.critical_path;
+
+  // geometry (the band fields that the shared code reads: n, npad, nbk)
+  BandGeom g;
+  g.n = n;
+  g.npad = bs.npad;
+  g.nbk = nb;
+  g.J = 0;
+  g.bw = -1;
+  c.geom = g;
+
+  auto to32 = [](const std::vector<int64_t>& v) { return std::vector<int>(v.begin(), v.end()); };
+  std::vector<int> tile_row(bs.ntiles);
+  for (int64_t i = 0; i < nb; ++i)
+    for (int64_t e = bs.row_ptr[i]; e < bs.row_ptr[i + 1]; ++e) tile_row[e] = static_cast<int>(i);
+  upload(c.sp_row_ptr, to32(bs.row_ptr), c.st);
+  upload(c.sp_row_idx, to32(bs.row_idx), c.st);
+  upload(c.sp_col_ptr, to32(bs.col_ptr), c.st);
+  upload(c.sp_col_idx, to32(bs.col_idx), c.st);
+  upload(c.sp_col_tile, to32(bs.col_tile), c.st);
+  upload(c.sp_tile_row, tile_row, c.st);
+  int max_deps = 0;
+  c.sp_col_cnt.assign(nb, 0);
+  for (int i = 0; i < nb; ++i) {
+    c.sp_col_cnt[i] = static_cast<int>(bs.col_ptr[i + 1] - bs.col_ptr[i]);
+    max_deps = std::max(max_deps, static_cast<int>(bs.row_ptr[i + 1] - bs.row_ptr[i]));
+    max_deps = std::max(max_deps, c.sp_col_cnt[i]);
+  }
+  SpGeom s;
+  s.n = n;
+  s.npad = bs.npad;
+  s.nb = nb;
+  s.ntiles = bs.ntiles;
+  s.max_deps = max_deps;
+  s.row_ptr = c.sp_row_ptr.as<int>();
+  s.row_idx = c.sp_row_idx.as<int>();
+  s.col_ptr = c.sp_col_ptr.as<int>();
+  s.col_idx = c.sp_col_idx.as<int>();
+  s.col_tile = c.sp_col_tile.as<int>();
+  s.tile_row = c.sp_tile_row.as<int>();
+  c.sgeom = s;
+
+  const int64_t nnz = static_cast<int64_t>(u.ci.size());
+  std::vector<int> er(nnz), ec(nnz), pads;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = u.rp[i]; k < u.rp[i + 1]; ++k) {
+      er[k] = pos[i];
+      ec[k] = pos[u.ci[k]];
+    }
+  for (int64_t t = 0; t < bs.npad; ++t)
+    if (bs.inv[t] < 0) pads.push_back(static_cast<int>(t));
+  DevMem er_d, ec_d, ea_d, eb_d;
+  upload(er_d, er, c.st);
+  upload(ec_d, ec, c.st);
+  upload(ea_d, u.av, c.st);
+  upload(eb_d, u.bv, c.st);
+  upload(c.sp_pad_rows, pads, c.st);
+  upload_device_pencil(c, bs.inv, pos);
+
+  // factors for r poles: Dt, DinvL, DinvU (nb tiles each), Lt, Ut (ntiles each)
+  const int r = c.r;
+  const size_t per_diag = static_cast<size_t>(nb) * TT;
+  const size_t per_off = static_cast<size_t>(bs.ntiles) * TT;
+  const size_t per_pole = 3 * per_diag + 2 * per_off;
+  size_t free_b = 0, total_b = 0;
+  c.tiles_mem.release();
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t need = per_pole * r * sizeof(cd);
+  if (need + (size_t(1) << 30) > free_b)
+    throw ZoloError(ZOLO_ERR_DOMAIN, "zolo_factorize: factors need " + std::to_string(need >> 20) +
+                                         " MiB, device has " + std::to_string(free_b >> 20) + " MiB free");
+  c.tiles_mem.ensure(need);
+  c.rownorm_mem.ensure(sizeof(double) * bs.npad * r);
+  c.fstate_mem.ensure(sizeof(unsigned long long) * 2 * r);
+  c.sp_err.ensure(sizeof(int) * 4);
+  CK(cudaMemsetAsync(c.sp_err.p, 0, sizeof(int) * 4, c.st));
+  c.tiles.assign(r, FactorTiles());
+  c.sp_dt.assign(r, nullptr);
+  cd* base = c.tiles_mem.as<cd>();
+  for (int j = 0; j < r; ++j) {
+    cd* p = base + per_pole * j;
+    c.sp_dt[j] = p;
+    c.tiles[j].DinvL = p + per_diag;
+    c.tiles[j].DinvU = p + 2 * per_diag;
+    c.tiles[j].Lt = p + 3 * per_diag;
+    c.tiles[j].Ut = p + 3 * per_diag + per_off;
+  }
+  std::vector<unsigned long long> fs(2 * r);
+  const double inf = std::numeric_limits<double>::infinity();
+  unsigned long long infbits;
+  std::memcpy(&infbits, &inf, 8);
+  for (int j = 0; j < r; ++j) {
+    fs[2 * j] = 0xffffffffffffffffull;
+    fs[2 * j + 1] = infbits;
+  }
+  CK(cudaMemcpy(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice));
+  while (static_cast<int>(c.pole_streams.size()) < r) {
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    c.pole_streams.push_back(st);
+  }
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaEventRecord(c.ev0, c.st));
+  for (int j = 0; j < r; ++j) CK(cudaStreamWaitEvent(c.pole_streams[j], c.ev0, 0));
+  const double* poles = c.design.data() + ZOLO_DESIGN_HEAD;
+  for (int j = 0; j < r; ++j) {
+    SpFactor f;
+    f.Dt = c.sp_dt[j];
+    f.Lt = c.tiles[j].Lt;
+    f.Ut = c.tiles[j].Ut;
+    f.DinvL = c.tiles[j].DinvL;
+    f.DinvU = c.tiles[j].DinvU;
+    FactorDevState ds;
+    ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
+    ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
+    sp_factor(c.pole_streams[j], s, c.sp_col_cnt, f, nnz, er_d.as<int>(), ec_d.as<int>(), ea_d.as<double>(),
+              eb_d.as<double>(), c.cx, poles[2 * j], poles[2 * j + 1], c.rownorm_mem.as<double>() + bs.npad * j,
+              c.sp_pad_rows.as<int>(), static_cast<int>(pads.size()), ds, c.sp_err.as<int>());
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c.ev2, c.pole_streams[j]));
+    CK(cudaStreamWaitEvent(c.st, c.ev2, 0));
+  }
+  CK(cudaEventRecord(c.ev1, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  for (int j = 0; j < r; ++j) CK(cudaStreamSynchronize(c.pole_streams[j]));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
+  c.last_ms[1] = ms;
+  int serr = 0;
+  CK(cudaMemcpy(&serr, c.sp_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (serr) throw ZoloError(ZOLO_ERR_NUMERICAL, "zolo_factorize: symbolic structure does not cover the fill");
+  CK(cudaMemcpy(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost));
+  int fail_any = -1;
+  for (int j = 0; j < r; ++j) {
+    const int fi = static_cast<int>(static_cast<uint32_t>(fs[2 * j] & 0xffffffffull));
+    double mr;
+    std::memcpy(&mr, &fs[2 * j + 1], 8);
+    if (stats) {
+      stats[j].bandwidth = -1;
+      stats[j].stored_entries = static_cast<int64_t>(per_pole);
+      stats[j].min_pivot_ratio = mr;
+      stats[j].pivot_index = fi;
+    }
+    if (fi >= 0 && fail_any < 0) fail_any = fi;
+  }
+  c.sparse = true;
+  c.factored = fail_any < 0;
+  c.ncap = 0;
+  if (fail_any >= 0)
+    throw ZoloError(ZOLO_ERR_FACTORIZATION, "factorize: pivot " + std::to_string(fail_any) + " below threshold");
+}
+
 void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   const int64_t ld = c.geom.npad;
   const size_t es = c.es();
@@ -487,7 +682,7 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
 
 // G applied to the columns act[0..na) of vsrc (ld x ncap, S) -> w[:, act].
 float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
-  const int64_t ld = c.geom.npad, n = c.n;
+  const int64_t ld = c.geom.npad, n = ld;  // device rows: padding rows (anywhere in ND order) are zero
   const int* act = c.act_d.as<int>();
   const int nch = c.nchains();
   std::vector<cd*> xs(nch);
@@ -501,6 +696,25 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   CK(cudaEventRecord(c.ev2, c.st));
   unsigned long long* fx = c.flags.as<unsigned long long>();
   int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
+  if (c.sparse) {  // block-sparse factors: DAG-scheduled sweeps
+    dag_trsm_launch(c.st, c.sgeom, c.chains_fwd.as<Chain>(), nch, na, ld, fc, ++c.epoch, c.counter.as<int>(), 1,
+                    c.num_sms);
+    dag_trsm_launch(c.st, c.sgeom, c.chains_bwd.as<Chain>(), nch, na, ld, fc, ++c.epoch, c.counter.as<int>() + 1, 0,
+                    c.num_sms);
+    if (c.cx)
+      for (int p = 0; p < c.r; ++p)
+        blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
+    CK(cudaEventRecord(c.ev3, c.st));
+    CK(cudaGetLastError());
+    if (c.cx)
+      Krylov<cd>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const cd*>(vsrc), act, na, xs.data(),
+                          c.weights_d.as<cd>(), c.r, reinterpret_cast<cd*>(wdst));
+    else
+      Krylov<double>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const double*>(vsrc), act, na,
+                              xs.data(), c.weights_d.as<cd>(), c.r, reinterpret_cast<double*>(wdst));
+    CK(cudaGetLastError());
+    return 0.0f;
+  }
   // ZOLO_TRACE=<file>: dump per-step timestamps of chain 0 / group 0 of the
   // first forward sweep (development aid for the pipeline's critical path)
   static const char* trace_path = std::getenv("ZOLO_TRACE");
@@ -527,7 +741,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   const int g2 = trsm_launch(c.st, c.geom, c.chains_bwd.as<Chain>(), nch, na, ld, fx, fc, ++c.epoch,
                              c.counter.as<int>() + 1, 0, c.num_sms);
   if (c.cx)
-    for (int p = 0; p < c.r; ++p) blockdiag_apply(c.st, c.geom, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
+    for (int p = 0; p < c.r; ++p) blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
   if (g1 < 0 || g2 < 0)
     throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: " + std::to_string(nch) + " chains x " +
                                          std::to_string((na + CG - 1) / CG) +
@@ -564,7 +778,7 @@ void ensure_gmres(zolo_ctx& c, int maxit) {
   c.ghappy.ensure(sizeof(int) * nv);
   c.gdone.ensure(sizeof(int) * nv);
   c.gwnorm.ensure(sizeof(double) * nv);
-  const int64_t nchunk = (c.n + CHUNK - 1) / CHUNK;
+  const int64_t nchunk = (c.geom.npad + CHUNK - 1) / CHUNK;
   c.partial.ensure(2 * es * nv * nchunk * (maxit + 1) + 64);
   c.hsave.ensure(es * nv * (maxit + 1));
   c.basis_ptrs.ensure(sizeof(void*) * (maxit + 1));
@@ -630,7 +844,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(d_v), n, vin, ld, ncols, c.perm_d.as<int>());
   GmresDev g = gmres_view(c, maxit);
   g.nv = static_cast<int>(ncols);
-  Krylov<S>::col_norms(c.st, vin, n, ld, ncols, g.beta);
+  Krylov<S>::col_norms(c.st, vin, ld, ld, ncols, g.beta);
   S* v0 = reinterpret_cast<S*>(basis_block(c, 0));
   Krylov<S>::scale_cols(c.st, vin, v0, n, ld, ncols, g.beta);
   gmres_init(c.st, g);
@@ -641,7 +855,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   for (int64_t k = 0; k < ncols; ++k)
     if (beta[k] != 0.0) active.push_back(static_cast<int>(k));
 
-  const int nchunk = static_cast<int>((n + CHUNK - 1) / CHUNK);
+  const int nchunk = static_cast<int>((ld + CHUNK - 1) / CHUNK);  // device rows incl. padding
   float trsm_ms = 0.0f;
   int trsm_launches = 0;
   int64_t launches = 4, opapps = 0;
@@ -656,7 +870,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     opapps += na;
     c.g_apps += na;
     c.inner_solves += static_cast<int64_t>(c.nchains()) * na;
-    Krylov<S>::arnoldi(c.st, n, ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(), c.act_d.as<int>(), na, g,
+    Krylov<S>::arnoldi(c.st, ld, ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(), c.act_d.as<int>(), na, g,
                        c.partial.as<double>(), nchunk, c.hsave.as<S>());
     Krylov<S>::least_squares(c.st, c.act_d.as<int>(), na, it, g, c.partial.as<double>(), nchunk, tol);
     if (it + 1 < maxit) {
@@ -757,20 +971,20 @@ void rr_impl(zolo_ctx& c, const double* y, int64_t k, double* at, double* bt) {
   yo.ensure(es * n * k);
   yp.ensure(es * ld * k);
   ay.ensure(es * ld * k);
-  const int64_t nchunk = (n + CHUNK - 1) / CHUNK;
+  const int64_t nchunk = (ld + CHUNK - 1) / CHUNK;
   c.rr_partial.ensure(es * nchunk * k * k + 64);
   c.rr_out.ensure(es * k * k);
   CK(cudaMemcpyAsync(yo.p, y, es * n * k, cudaMemcpyHostToDevice, c.st));
   Krylov<S>::permute_in(c.st, yo.as<S>(), n, yp.as<S>(), ld, k, c.perm_d.as<int>());
-  Krylov<S>::spmm(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), yp.as<S>(), k, ay.as<S>());
-  Krylov<S>::gram(c.st, n, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
+  Krylov<S>::spmm(c.st, ld, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), yp.as<S>(), k, ay.as<S>());
+  Krylov<S>::gram(c.st, ld, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
   CK(cudaMemcpyAsync(at, c.rr_out.p, es * k * k, cudaMemcpyDeviceToHost, c.st));
   CK(cudaStreamSynchronize(c.st));
   if (c.b_identity) {
-    Krylov<S>::gram(c.st, n, ld, yp.as<S>(), k, yp.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
+    Krylov<S>::gram(c.st, ld, ld, yp.as<S>(), k, yp.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
   } else {
-    Krylov<S>::spmm(c.st, n, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), yp.as<S>(), k, ay.as<S>());
-    Krylov<S>::gram(c.st, n, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
+    Krylov<S>::spmm(c.st, ld, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), yp.as<S>(), k, ay.as<S>());
+    Krylov<S>::gram(c.st, ld, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
   }
   CK(cudaMemcpyAsync(bt, c.rr_out.p, es * k * k, cudaMemcpyDeviceToHost, c.st));
   CK(cudaStreamSynchronize(c.st));
@@ -807,10 +1021,10 @@ void spmm_dev_impl(zolo_ctx& c, int which, const void* x, void* out, int64_t k) 
   c.tmp2.ensure(es * ld * k);
   Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(x), n, c.tmp1.as<S>(), ld, k, c.perm_d.as<int>());
   if (which == 0)
-    Krylov<S>::spmm(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), c.tmp1.as<S>(), k,
+    Krylov<S>::spmm(c.st, ld, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), c.tmp1.as<S>(), k,
                     c.tmp2.as<S>());
   else
-    Krylov<S>::spmm(c.st, n, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), c.tmp1.as<S>(), k,
+    Krylov<S>::spmm(c.st, ld, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), c.tmp1.as<S>(), k,
                     c.tmp2.as<S>());
   Krylov<S>::permute_out(c.st, c.tmp2.as<S>(), ld, reinterpret_cast<S*>(out), n, k, c.perm_d.as<int>());
   CK(cudaGetLastError());
@@ -1033,6 +1247,15 @@ int zolo_set_design(zolo_ctx* c, const double* design, int r) {
     upload(c->shifts_d, s, c->st);
     upload(c->coef_d, c->coef, c->st);
     c->have_design = true;
+    c->factored = false;
+  });
+}
+
+int zolo_set_ordering(zolo_ctx* c, int mode, int64_t nd_leaf) {
+  return guarded(c, [&] {
+    require(mode == ZOLO_ORDER_ND || mode == ZOLO_ORDER_RCM, "zolo_set_ordering: unknown mode");
+    c->order_mode = mode;
+    if (nd_leaf > 0) c->nd_leaf = nd_leaf;
     c->factored = false;
   });
 }

@@ -109,7 +109,7 @@ __global__ void scatter_kernel(BandGeom g, cd* Lt, cd* Ut, int64_t nnz, const in
 // monitor (|pivot| > 1e-14 ||row||_inf, band_factor.hpp:160-166), then the
 // inverses of its unit-lower and upper triangles (threads 0..127: L^{-1},
 // 128..255: U^{-1}; 4 threads per column share each dot product).
-__global__ void __launch_bounds__(FT) diag_factor_kernel(BandGeom g, int k, cd* Lt, cd* DinvL, cd* DinvU,
+__global__ void __launch_bounds__(FT) diag_factor_kernel(int64_t n, int k, cd* tile, cd* DinvL, cd* DinvU,
                                                          const double* row_norm, int* fail_index,
                                                          unsigned long long* min_ratio_bits) {
   extern __shared__ __align__(16) unsigned char diag_smem[];
@@ -117,7 +117,6 @@ __global__ void __launch_bounds__(FT) diag_factor_kernel(BandGeom g, int k, cd* 
   cd* XL = D + TILE * TPAD;
   cd* XU = XL + TILE * TPAD;
   cd(*red)[4][TILE] = reinterpret_cast<cd(*)[4][TILE]>(XU + TILE * TPAD);
-  cd* tile = Lt + lt_off(k, 0, g.J);
   load_tile_async(D, tile);
   cp_async_commit();
   cp_async_wait<0>();
@@ -128,7 +127,7 @@ __global__ void __launch_bounds__(FT) diag_factor_kernel(BandGeom g, int k, cd* 
     const cd inv = cdiv(mk(1.0, 0.0), piv);
     if (t == 0) {
       const int64_t gi = static_cast<int64_t>(k) * TILE + p;
-      if (gi < g.n) {
+      if (gi < n) {
         const double rn = row_norm[gi];
         const double ap = hypot(piv.x, piv.y);
         const double ratio = ap / fmax(rn, 1e-300);
@@ -268,7 +267,171 @@ __global__ void __launch_bounds__(FT) scale_tiles_kernel(BandGeom g, FactorTiles
   store_tile(t, o);
 }
 
+// ---------------------------------------------------------------------------
+// block-sparse factor path (any node ordering, e.g. nested dissection)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int sp_lookup(const SpGeom& s, int i, int k) {  // tile id of (i, k), i > k
+  int lo = s.row_ptr[i], hi = s.row_ptr[i + 1] - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int v = s.row_idx[mid];
+    if (v == k) return mid;
+    if (v < k)
+      lo = mid + 1;
+    else
+      hi = mid - 1;
+  }
+  return -1;
+}
+
+__global__ void scatter_sp_kernel(SpGeom s, cd* Dt, cd* Lt, cd* Ut, int64_t nnz, const int* e_row, const int* e_col,
+                                  const double* a_val, const double* b_val, int cx, double sr, double si,
+                                  unsigned long long* row_norm_bits, const int* pad_rows, int npad_rows,
+                                  int* err) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e < nnz) {
+    const int pi = e_row[e], pj = e_col[e];
+    cd a, b;
+    if (cx) {
+      a = mk(a_val[2 * e], a_val[2 * e + 1]);
+      b = mk(b_val[2 * e], b_val[2 * e + 1]);
+    } else {
+      a = mk(a_val[e], 0.0);
+      b = mk(b_val[e], 0.0);
+    }
+    const cd v = csub(a, cmul(mk(sr, si), b));  // assemble_shifted (sparse.hpp:153-186)
+    const int bi = pi / TILE, bj = pj / TILE;
+    const int r = pi % TILE, c = pj % TILE;
+    cd* t;
+    if (bi == bj) {
+      t = Dt + static_cast<size_t>(bi) * TT;
+    } else {
+      const int id = bi > bj ? sp_lookup(s, bi, bj) : sp_lookup(s, bj, bi);
+      if (id < 0) {
+        atomicExch(err, 1);  // symbolic structure does not cover the pattern
+        return;
+      }
+      t = (bi > bj ? Lt : Ut) + static_cast<size_t>(id) * TT;
+    }
+    t[c * TILE + r] = v;
+    atomicMax(&row_norm_bits[pi], static_cast<unsigned long long>(__double_as_longlong(hypot(v.x, v.y))));
+  } else if (e < nnz + npad_rows) {
+    const int row = pad_rows[e - nnz];  // identity padding row
+    const int bi = row / TILE, r = row % TILE;
+    Dt[static_cast<size_t>(bi) * TT + r * TILE + r] = mk(1.0, 0.0);
+    row_norm_bits[row] = static_cast<unsigned long long>(__double_as_longlong(1.0));
+  }
+}
+
+// L(i,k) = A(i,k) U_kk^{-1}, U(k,i) = L_kk^{-1} A(k,i) for the structural rows i of column k.
+__global__ void __launch_bounds__(FT) panel_sp_kernel(SpGeom s, int k, cd* Lt, cd* Ut, const cd* DinvL,
+                                                      const cd* DinvU) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int e0 = s.col_ptr[k], cnt = s.col_ptr[k + 1] - e0;
+  const bool lower = static_cast<int>(blockIdx.x) < cnt;
+  const int id = s.col_tile[e0 + (lower ? blockIdx.x : blockIdx.x - cnt)];
+  cd* c = (lower ? Lt : Ut) + static_cast<size_t>(id) * TT;
+  if (lower) {
+    load_tile_async(As, c);
+    load_tile_async(Bs, DinvU + static_cast<size_t>(k) * TT);
+  } else {
+    load_tile_async(As, DinvL + static_cast<size_t>(k) * TT);
+    load_tile_async(Bs, c);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  cd out[4];
+  tile_mm(As, Bs, out);
+  store_tile(c, out);
+}
+
+// A(a,b) -= L(a,k) U(k,b) over all structural pairs (a, b) of column k.
+__global__ void __launch_bounds__(FT) trailing_sp_kernel(SpGeom s, int k, cd* Dt, cd* Lt, cd* Ut, int* err) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int e0 = s.col_ptr[k];
+  const int a = s.col_idx[e0 + blockIdx.x], b = s.col_idx[e0 + blockIdx.y];
+  load_tile_async(As, Lt + static_cast<size_t>(s.col_tile[e0 + blockIdx.x]) * TT);
+  load_tile_async(Bs, Ut + static_cast<size_t>(s.col_tile[e0 + blockIdx.y]) * TT);
+  cp_async_commit();
+  cd* c;
+  if (a == b) {
+    c = Dt + static_cast<size_t>(a) * TT;
+  } else {
+    const int id = a > b ? sp_lookup(s, a, b) : sp_lookup(s, b, a);
+    if (id < 0) {
+      if (threadIdx.x == 0) atomicExch(err, 1);
+      return;
+    }
+    c = (a > b ? Lt : Ut) + static_cast<size_t>(id) * TT;
+  }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const cd c0 = c[ty * TILE + tx], c1 = c[(ty + 16) * TILE + tx], c2 = c[ty * TILE + tx + 16],
+           c3 = c[(ty + 16) * TILE + tx + 16];
+  cp_async_wait<0>();
+  __syncthreads();
+  cd out[4];
+  tile_mm(As, Bs, out);
+  out[0] = csub(c0, out[0]);
+  out[1] = csub(c1, out[1]);
+  out[2] = csub(c2, out[2]);
+  out[3] = csub(c3, out[3]);
+  store_tile(c, out);
+}
+
+// Row scaling L~(i,k) = DinvL_i L(i,k), U~(k,i) = DinvU_k U(k,i) (see band path).
+__global__ void __launch_bounds__(FT) scale_sp_kernel(SpGeom s, cd* Lt, cd* Ut, const cd* DinvL, const cd* DinvU) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int id = blockIdx.x;
+  const bool lower = blockIdx.y == 0;
+  const int row = lower ? s.tile_row[id] : s.row_idx[id];
+  cd* t = (lower ? Lt : Ut) + static_cast<size_t>(id) * TT;
+  load_tile_async(As, (lower ? DinvL : DinvU) + static_cast<size_t>(row) * TT);
+  load_tile_async(Bs, t);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  cd o[4];
+  tile_mm(As, Bs, o);
+  store_tile(t, o);
+}
+
 }  // namespace
+
+void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt, const SpFactor& f, int64_t nnz,
+               const int* e_row, const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
+               double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err) {
+  cudaMemsetAsync(f.Dt, 0, sizeof(cd) * s.nb * TT, st);
+  if (s.ntiles > 0) {
+    cudaMemsetAsync(f.Lt, 0, sizeof(cd) * s.ntiles * TT, st);
+    cudaMemsetAsync(f.Ut, 0, sizeof(cd) * s.ntiles * TT, st);
+  }
+  cudaMemsetAsync(row_norm, 0, sizeof(double) * s.npad, st);
+  const int64_t total = nnz + npad_rows;
+  if (total > 0)
+    scatter_sp_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        s, f.Dt, f.Lt, f.Ut, nnz, e_row, e_col, a_val, b_val, cx, sig_re, sig_im,
+        reinterpret_cast<unsigned long long*>(row_norm), pad_rows, npad_rows, err);
+  constexpr int diag_smem = (3 * TILE * TPAD + 2 * 4 * TILE) * sizeof(cd);
+  static bool diag_attr = false;
+  if (!diag_attr) {
+    cudaFuncSetAttribute(diag_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem);
+    diag_attr = true;
+  }
+  for (int k = 0; k < s.nb; ++k) {
+    diag_factor_kernel<<<1, FT, diag_smem, st>>>(s.npad, k, f.Dt + static_cast<size_t>(k) * TT, f.DinvL, f.DinvU,
+                                                 row_norm, ds.fail_index, ds.min_ratio_bits);
+    const int cnt = col_cnt[k];
+    if (cnt > 0) {
+      panel_sp_kernel<<<2 * cnt, FT, 0, st>>>(s, k, f.Lt, f.Ut, f.DinvL, f.DinvU);
+      trailing_sp_kernel<<<dim3(cnt, cnt), FT, 0, st>>>(s, k, f.Dt, f.Lt, f.Ut, err);
+    }
+  }
+  if (s.ntiles > 0) scale_sp_kernel<<<dim3(static_cast<unsigned>(s.ntiles), 2), FT, 0, st>>>(s, f.Lt, f.Ut, f.DinvL, f.DinvU);
+}
 
 void factor_scatter(cudaStream_t st, const BandGeom& g, const FactorTiles& f, int64_t nnz, const int* e_row,
                     const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
@@ -295,7 +458,7 @@ void factor_run(cudaStream_t st, const BandGeom& g, const FactorTiles& f, const 
     diag_attr = true;
   }
   for (int k = 0; k < g.nbk; ++k) {
-    diag_factor_kernel<<<1, FT, diag_smem, st>>>(g, k, f.Lt, f.DinvL, f.DinvU, row_norm, ds.fail_index,
+    diag_factor_kernel<<<1, FT, diag_smem, st>>>(g.n, k, f.Lt + lt_off(k, 0, g.J), f.DinvL, f.DinvU, row_norm, ds.fail_index,
                                                  ds.min_ratio_bits);
     if (k + 1 < g.nbk && g.J > 0) {
       panel_kernel<<<2 * g.J, FT, 0, st>>>(g, k, f.Lt, f.Ut, f.DinvL, f.DinvU);

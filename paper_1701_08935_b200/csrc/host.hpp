@@ -2,6 +2,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace zolo {
 // status-carrying error thrown by the host setup (codes as include/zolo_b200.h)
@@ -9,6 +10,22 @@ struct DesignError : std::runtime_error {
   int code;
   DesignError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
+// Block (32x32-tile) structure of the LU factors under a node ordering
+// (symbolic.cpp). Off-diagonal tile ids are row-major slots: row i's tiles
+// (i, row_idx[e]) for e in [row_ptr[i], row_ptr[i+1]), k ascending; column
+// k's entries (col_idx[e], k) for e in [col_ptr[k], col_ptr[k+1]) carry their
+// tile id in col_tile[e]. L(i,k) and U(k,i) share the id.
+struct BlockStructure {
+  int64_t npad = 0, nb = 0, ntiles = 0, critical_path = 0;
+  std::vector<int64_t> pos;  // original row -> padded position
+  std::vector<int64_t> inv;  // padded position -> original row, or -1 (identity padding)
+  std::vector<int64_t> col_ptr, col_idx, col_tile;
+  std::vector<int64_t> row_ptr, row_idx;
+  std::vector<int64_t> parent;  // block elimination tree
+};
+void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std::vector<std::vector<int64_t>>& nodes);
+void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::vector<std::vector<int64_t>>& nodes,
+                    int tile, BlockStructure& bs);
 void rcm_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm);
 int64_t bandwidth_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);
 int64_t profile_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);

@@ -42,20 +42,23 @@ __device__ __forceinline__ cd warp_sum<cd>(cd v) {
   return v;
 }
 
+// perm: device position (0..ld) -> original row, or -1 for identity padding rows.
 template <class S>
 __global__ void permute_in_kernel(const S* src, int64_t n, S* dst, int64_t ld, const int* perm) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t c = blockIdx.y;
   if (t >= ld) return;
-  dst[t + c * ld] = (t < n) ? src[perm[t] + c * n] : szero(S());
+  const int p = perm[t];
+  dst[t + c * ld] = (p >= 0) ? src[p + c * n] : szero(S());
 }
 
 template <class S>
 __global__ void permute_out_kernel(const S* src, int64_t ld, S* dst, int64_t n, const int* perm) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t c = blockIdx.y;
-  if (t >= n) return;
-  dst[perm[t] + c * n] = src[t + c * ld];
+  if (t >= ld) return;
+  const int p = perm[t];
+  if (p >= 0) dst[p + c * n] = src[t + c * ld];
 }
 
 template <class S>
@@ -503,7 +506,7 @@ void Krylov<S>::permute_in(cudaStream_t st, const S* src, int64_t n, S* dst, int
 }
 template <class S>
 void Krylov<S>::permute_out(cudaStream_t st, const S* src, int64_t ld, S* dst, int64_t n, int64_t k, const int* perm) {
-  if (k > 0) permute_out_kernel<S><<<dim3(blocks_for(n, 256), k), 256, 0, st>>>(src, ld, dst, n, perm);
+  if (k > 0) permute_out_kernel<S><<<dim3(blocks_for(ld, 256), k), 256, 0, st>>>(src, ld, dst, n, perm);
 }
 template <class S>
 void Krylov<S>::col_norms(cudaStream_t st, const S* v, int64_t n, int64_t ld, int64_t k, double* out) {

@@ -1,0 +1,263 @@
+// Host symbolic analysis for the block-sparse factor path (north star:
+// "ordering and symbolic analysis remain host-side setup").
+//
+//   nd_order        nested dissection by recursive BFS-level bisection: the
+//                   median BFS level of each connected piece is its separator;
+//                   pieces below `leaf` rows are ordered by reverse
+//                   Cuthill-McKee inside. Nodes come out in post-order
+//                   (children before their separator).
+//   block_symbolic  nodes padded to whole 32-row tiles (identity padding
+//                   rows), the block graph of the pattern, and its symbolic
+//                   elimination (fill) through the block elimination tree:
+//                   struct(k) = adj+(k) U (U_children struct(c) \ {k}).
+//
+// The reference orders by RCM and factors a band (rcm.hpp, band_factor.hpp);
+// nested dissection is SURVEY.md §8(f) rank 2 ("host symbolic analysis: ND
+// ordering, supernodes, etree"), here at 32x32-tile granularity.
+#include <algorithm>
+#include <cstdint>
+#include <numeric>
+#include <vector>
+
+#include "host.hpp"
+
+namespace zolo {
+
+namespace {
+
+struct Graph {
+  int64_t n;
+  const int64_t* rp;
+  const int64_t* ci;
+};
+
+// BFS over the vertices with mark[v] == tag; returns the visit order and fills level.
+void bfs(const Graph& g, const std::vector<int>& mark, int tag, int64_t root, std::vector<int64_t>& level,
+         std::vector<int64_t>& order) {
+  order.clear();
+  order.push_back(root);
+  level[root] = 0;
+  for (size_t h = 0; h < order.size(); ++h) {
+    const int64_t u = order[h];
+    for (int64_t k = g.rp[u]; k < g.rp[u + 1]; ++k) {
+      const int64_t v = g.ci[k];
+      if (mark[v] == tag && level[v] < 0) {
+        level[v] = level[u] + 1;
+        order.push_back(v);
+      }
+    }
+  }
+}
+
+struct NdState {
+  const Graph& g;
+  int64_t leaf;
+  std::vector<int> mark;
+  int next_tag = 1;
+  std::vector<int64_t> level, order;
+  std::vector<std::vector<int64_t>> nodes;  // elimination order of tree nodes
+  std::vector<int> node_is_sep;
+  explicit NdState(const Graph& gr, int64_t lf) : g(gr), leaf(lf), mark(gr.n, 0), level(gr.n, -1) {}
+
+  void emit_leaf(std::vector<int64_t>& idx) {
+    // reverse Cuthill-McKee inside the leaf (degree tie-breaks within the piece)
+    const int tag = next_tag++;
+    for (int64_t v : idx) mark[v] = tag;
+    std::vector<int64_t> out;
+    out.reserve(idx.size());
+    std::vector<char> seen_local;
+    auto deg = [&](int64_t v) {
+      int64_t d = 0;
+      for (int64_t k = g.rp[v]; k < g.rp[v + 1]; ++k) d += mark[g.ci[k]] == tag;
+      return d;
+    };
+    std::vector<int64_t> q, nb;
+    size_t done = 0;
+    while (done < idx.size()) {
+      int64_t root = -1, best = INT64_MAX;
+      for (int64_t v : idx)
+        if (mark[v] == tag) {
+          const int64_t d = deg(v);
+          if (d < best) best = d, root = v;
+        }
+      // pseudo-peripheral refinement
+      for (int it = 0; it < 2; ++it) {
+        for (int64_t v : idx)
+          if (mark[v] == tag) level[v] = -1;
+        bfs(g, mark, tag, root, level, order);
+        root = order.back();
+      }
+      q.clear();
+      q.push_back(root);
+      mark[root] = -tag;
+      for (size_t h = 0; h < q.size(); ++h) {
+        const int64_t u = q[h];
+        out.push_back(u);
+        nb.clear();
+        for (int64_t k = g.rp[u]; k < g.rp[u + 1]; ++k) {
+          const int64_t v = g.ci[k];
+          if (mark[v] == tag) {
+            mark[v] = -tag;
+            nb.push_back(v);
+          }
+        }
+        std::sort(nb.begin(), nb.end(), [&](int64_t x, int64_t y) {
+          const int64_t dx = g.rp[x + 1] - g.rp[x], dy = g.rp[y + 1] - g.rp[y];
+          return dx < dy || (dx == dy && x < y);
+        });
+        for (int64_t v : nb) q.push_back(v);
+      }
+      done = out.size();
+    }
+    std::reverse(out.begin(), out.end());
+    for (int64_t v : idx) level[v] = -1;
+    nodes.push_back(std::move(out));
+    node_is_sep.push_back(0);
+  }
+
+  void rec(std::vector<int64_t> idx) {
+    if (static_cast<int64_t>(idx.size()) <= leaf) {
+      emit_leaf(idx);
+      return;
+    }
+    const int tag = next_tag++;
+    for (int64_t v : idx) mark[v] = tag;
+    int64_t root = idx[0];
+    for (int it = 0; it < 2; ++it) {
+      for (int64_t v : idx) level[v] = -1;
+      bfs(g, mark, tag, root, level, order);
+      root = order.back();
+    }
+    for (int64_t v : idx) level[v] = -1;
+    bfs(g, mark, tag, root, level, order);
+    if (order.size() < idx.size()) {  // disconnected: the reached component, then the rest
+      std::vector<int64_t> a(order.begin(), order.end()), b;
+      for (int64_t v : idx)
+        if (level[v] < 0) b.push_back(v);
+      for (int64_t v : idx) level[v] = -1;
+      rec(std::move(a));
+      rec(std::move(b));
+      return;
+    }
+    // median level by vertex count
+    std::vector<int64_t> lv;
+    lv.reserve(idx.size());
+    for (int64_t v : idx) lv.push_back(level[v]);
+    std::vector<int64_t> srt = lv;
+    std::nth_element(srt.begin(), srt.begin() + srt.size() / 2, srt.end());
+    const int64_t med = srt[srt.size() / 2];
+    std::vector<int64_t> a, b, s;
+    for (size_t q = 0; q < idx.size(); ++q) {
+      if (lv[q] < med)
+        a.push_back(idx[q]);
+      else if (lv[q] > med)
+        b.push_back(idx[q]);
+      else
+        s.push_back(idx[q]);
+    }
+    for (int64_t v : idx) level[v] = -1;
+    if (a.empty() || b.empty()) {  // no progress (path-like piece): stop dissecting
+      emit_leaf(idx);
+      return;
+    }
+    rec(std::move(a));
+    rec(std::move(b));
+    nodes.push_back(std::move(s));
+    node_is_sep.push_back(1);
+  }
+};
+
+}  // namespace
+
+void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std::vector<std::vector<int64_t>>& nodes) {
+  Graph g{n, rp, ci};
+  NdState st(g, leaf);
+  std::vector<int64_t> all(n);
+  std::iota(all.begin(), all.end(), 0);
+  st.rec(std::move(all));
+  nodes = std::move(st.nodes);
+}
+
+void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::vector<std::vector<int64_t>>& nodes,
+                    int tile, BlockStructure& bs) {
+  // padded positions: each node occupies a whole number of tiles
+  bs.pos.assign(n, -1);
+  std::vector<int64_t> inv;
+  for (const auto& nd : nodes) {
+    for (int64_t v : nd) {
+      bs.pos[v] = static_cast<int64_t>(inv.size());
+      inv.push_back(v);
+    }
+    while (inv.size() % tile) inv.push_back(-1);
+  }
+  bs.npad = static_cast<int64_t>(inv.size());
+  bs.inv = std::move(inv);
+  const int64_t nb = bs.npad / tile;
+  bs.nb = nb;
+  // block graph (upper part: neighbours with a larger block index)
+  std::vector<std::vector<int64_t>> up(nb);
+  for (int64_t v = 0; v < n; ++v) {
+    const int64_t bv = bs.pos[v] / tile;
+    for (int64_t k = rp[v]; k < rp[v + 1]; ++k) {
+      const int64_t bw = bs.pos[ci[k]] / tile;
+      if (bw > bv) up[bv].push_back(bw);
+    }
+  }
+  for (auto& u : up) {
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+  }
+  // symbolic elimination through the elimination tree
+  std::vector<int64_t> parent(nb, -1);
+  std::vector<std::vector<int64_t>> children(nb);
+  std::vector<std::vector<int64_t>> st(nb);
+  std::vector<int64_t> merged;
+  for (int64_t k = 0; k < nb; ++k) {
+    merged = up[k];
+    for (int64_t c : children[k]) {
+      for (int64_t x : st[c])
+        if (x != k) merged.push_back(x);
+      std::vector<int64_t>().swap(st[c]);  // child structure no longer needed
+    }
+    std::sort(merged.begin(), merged.end());
+    merged.erase(std::unique(merged.begin(), merged.end()), merged.end());
+    st[k] = merged;
+    if (!merged.empty()) {
+      parent[k] = merged.front();
+      children[merged.front()].push_back(k);
+    }
+    bs.col_ptr.push_back(static_cast<int64_t>(bs.col_idx.size()));
+    for (int64_t i : merged) bs.col_idx.push_back(i);
+  }
+  bs.col_ptr.push_back(static_cast<int64_t>(bs.col_idx.size()));
+  bs.parent = parent;
+  // tile ids: one per off-diagonal structural pair (i > k), numbered row-major
+  // (by i, then k) so a forward sweep reads a block row's L tiles contiguously
+  std::vector<int64_t> cnt(nb + 1, 0);
+  for (int64_t e = 0; e < static_cast<int64_t>(bs.col_idx.size()); ++e) ++cnt[bs.col_idx[e] + 1];
+  bs.row_ptr.assign(nb + 1, 0);
+  for (int64_t i = 0; i < nb; ++i) bs.row_ptr[i + 1] = bs.row_ptr[i] + cnt[i + 1];
+  bs.row_idx.assign(bs.col_idx.size(), 0);
+  bs.col_tile.assign(bs.col_idx.size(), 0);
+  std::vector<int64_t> fill(bs.row_ptr.begin(), bs.row_ptr.end() - 1);
+  for (int64_t k = 0; k < nb; ++k)
+    for (int64_t e = bs.col_ptr[k]; e < bs.col_ptr[k + 1]; ++e) {
+      const int64_t i = bs.col_idx[e];
+      const int64_t slot = fill[i]++;
+      bs.row_idx[slot] = k;   // rows' entries come out sorted by k (k ascending)
+      bs.col_tile[e] = slot;  // the tile id is the row-major slot
+    }
+  bs.ntiles = static_cast<int64_t>(bs.col_idx.size());
+  // critical path of the dependency DAG (forward sweep)
+  std::vector<int64_t> depth(nb, 0);
+  int64_t cp = 0;
+  for (int64_t i = 0; i < nb; ++i) {
+    int64_t d = 0;
+    for (int64_t e = bs.row_ptr[i]; e < bs.row_ptr[i + 1]; ++e) d = std::max(d, depth[bs.row_idx[e]]);
+    depth[i] = d + 1;
+    cp = std::max(cp, depth[i]);
+  }
+  bs.critical_path = cp;
+}
+
+}  // namespace zolo

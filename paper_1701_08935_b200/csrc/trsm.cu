@@ -429,6 +429,119 @@ __global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// DAG-scheduled sweeps over block-sparse factors (nested dissection etc.)
+// ---------------------------------------------------------------------------
+struct DagArgs {
+  const Chain* chains;
+  int nchains, ngroups, ncols, epoch, fwd;
+  int64_t ld;
+  SpGeom s;
+  int* flags;    // per (chain, group, block): epoch when u_i is final
+  int* counter;  // [0] task counter, [2] wait-timeout error word
+};
+
+// u_i = pre(b_i) - sum_{deps j} op(T~(i, j)) u_j for one (block row, chain,
+// group). Dependencies are processed earliest-completed first (forward:
+// ascending j, backward: descending j); their flags are read once, in
+// parallel, at task start, so only dependencies still running cost a wait.
+__device__ void dag_task(const DagArgs& A, int s, int ci, int gi, cd* smem, int* dsm) {
+  auto tile_s = [smem](int k) { return smem + k * TILE_S; };
+  auto x_s = [smem](int k) { return smem + NS * TILE_S + k * XS; };
+  cd* dinv_s = smem + NS * TILE_S + NS * XS;
+  cd* acc_s = dinv_s + TILE_S;
+  const SpGeom& G = A.s;
+  int* dep_s = dsm;
+  int* tid_s = dsm + (G.max_deps + 8);
+  int* rdy_s = dsm + 2 * (G.max_deps + 8);
+  const Chain ch = A.chains[ci];
+  const bool fwd = A.fwd != 0;
+  const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
+  const Frag f = frag();
+  const int i = fwd ? s : G.nb - 1 - s;
+  const int c0 = gi * CG, nc = min(CG, A.ncols - c0);
+  const int64_t ld = A.ld;
+  int* flags = A.flags + (static_cast<size_t>(ci) * A.ngroups + gi) * G.nb;
+  const int e0 = fwd ? G.row_ptr[i] : G.col_ptr[i];
+  const int nd = (fwd ? G.row_ptr[i + 1] : G.col_ptr[i + 1]) - e0;
+  for (int q = threadIdx.x; q < nd; q += ST) {
+    const int e = fwd ? e0 + q : e0 + nd - 1 - q;  // processing order
+    const int j = fwd ? G.row_idx[e] : G.col_idx[e];
+    dep_s[q] = j;
+    tid_s[q] = fwd ? e : G.col_tile[e];
+    rdy_s[q] = ld_acquire(flags + j) >= A.epoch;
+  }
+  cd bval[2];
+  if (ch.pre) {
+    load_tile(dinv_s, ch.pre + static_cast<size_t>(i) * TT);
+    load_x(acc_s, ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    bval[0] = bval[1] = mk(0.0, 0.0);
+    mma_tile(bval, dinv_s, acc_s, opH, f);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = f.col + q;
+      bval[q] = (c < nc) ? ch.src[static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld] : mk(0.0, 0.0);
+    }
+  }
+  __syncthreads();
+  cd acc[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+  auto issue = [&](int q) {
+    const int buf = q % NS;
+    load_tile(tile_s(buf), ch.off + static_cast<size_t>(tid_s[q]) * TT);
+    if (rdy_s[q]) load_x(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
+  };
+#pragma unroll
+  for (int e = 0; e < NS - 1; ++e) {
+    if (e < nd) issue(e);
+    cp_async_commit();
+  }
+  for (int q = 0; q < nd; ++q) {
+    const int buf = q % NS;
+    if (rdy_s[q]) {
+      cp_async_wait<NS - 2>();
+    } else {  // still running at task start: wait for it now, then fetch its u
+      wait_flag(flags + dep_s[q], A.epoch, A.counter + 2);
+      load_x(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (q + NS - 1 < nd) issue(q + NS - 1);
+    cp_async_commit();
+    mma_tile(acc, tile_s(buf), x_s(buf), opH, f);
+  }
+  cp_async_wait<0>();
+  cd* urow = ch.dst + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (f.col + q < nc) urow[(f.col + q) * ld] = csub(bval[q], acc[q]);
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(flags + i, A.epoch);  // cumulative release after the barrier
+}
+
+__global__ void __launch_bounds__(ST, 2) dag_kernel(DagArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cd* smem = reinterpret_cast<cd*>(smem_raw);
+  int* dsm = reinterpret_cast<int*>(smem_raw + SMEM_FIXED);
+  __shared__ int task_s;
+  const int per_step = A.nchains * A.ngroups;
+  const int ntasks = A.s.nb * per_step;
+  for (;;) {
+    if (threadIdx.x == 0) task_s = atomicAdd(A.counter, 1);
+    __syncthreads();
+    const int t = task_s;
+    __syncthreads();
+    if (t >= ntasks) break;
+    const int s = t / per_step, rem = t % per_step;
+    dag_task(A, s, rem / A.ngroups, rem % A.ngroups, smem, dsm);
+    __syncthreads();
+  }
+}
+
 // x_i <- op(D_i) x_i per (block row, 16-column group): the adjoint post-pass.
 __global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
   __shared__ __align__(16) cd ds[TILE_S];
@@ -450,8 +563,37 @@ __global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd
 
 }  // namespace
 
-void blockdiag_apply(cudaStream_t st, const BandGeom& g, const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
-  if (ncols > 0) blockdiag_kernel<<<dim3(g.nbk, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld);
+void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
+  if (ncols > 0) blockdiag_kernel<<<dim3(nb, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld);
+}
+
+int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const Chain* d_chains, int nchains, int ncols, int64_t ld,
+                    int* flags, int epoch, int* counter, int fwd, int num_sms) {
+  const int smem = SMEM_FIXED + 3 * (s.max_deps + 8) * static_cast<int>(sizeof(int));
+  static int attr_set = 0;
+  if (smem > attr_set) {
+    cudaFuncSetAttribute(dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = smem;
+  }
+  DagArgs a;
+  a.chains = d_chains;
+  a.nchains = nchains;
+  a.ngroups = (ncols + CG - 1) / CG;
+  a.ncols = ncols;
+  a.epoch = epoch;
+  a.fwd = fwd;
+  a.ld = ld;
+  a.s = s;
+  a.flags = flags;
+  a.counter = counter;
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  const int ntasks = s.nb * nchains * a.ngroups;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel, ST, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int grid = std::min(ntasks, num_sms * per_sm);
+  if (grid > 0) dag_kernel<<<grid, ST, smem, st>>>(a);
+  return grid;
 }
 
 int trsm_launch(cudaStream_t st, const BandGeom& g, const Chain* d_chains, int nchains, int ncols, int64_t ld,

@@ -32,11 +32,12 @@ def rel_fro(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
 
 
+@pytest.mark.parametrize("ordering", ["nd", "rcm"])
 @pytest.mark.parametrize("name", FILTER_CASES)
-def test_filter_matches_reference_goldens(zb, name):
+def test_filter_matches_reference_goldens(zb, name, ordering):
     g = load_golden("filter_" + name)
     cx, r = bool(g["cx"]), int(g["r"])
-    op = zb.FilterOperator(golden_pencil(g), g["design"], r, is_complex=cx)
+    op = zb.FilterOperator(golden_pencil(g), g["design"], r, is_complex=cx, ordering=ordering, nd_leaf=64)
     gv = op.apply_g(g["v"])
     assert np.abs(gv - g["gv"]).max() <= 1e-11 * max(1.0, np.abs(g["gv"]).max())
     assert (op.inner_solve_count(), op.g_application_count()) == tuple(int(x) for x in g["g_counters"])

@@ -15,10 +15,11 @@ for name in sys.argv[1:] or ["cfg1", "cfg2"]:
     pen, cx, gaps, r, nv, nl = configs.config(name)
     design = build_filter_design(gaps, r)
     t0 = time.time()
-    op = zb.FilterOperator(pen, design, r, is_complex=cx)
+    order = os.environ.get("ORDER", "nd")
+    op = zb.FilterOperator(pen, design, r, is_complex=cx, ordering=order)
     t1 = time.time()
     prof = op.factor_profile()[0]
-    print(f"{name}: N={pen[0]} bw={prof['bandwidth']} factor wall {t1 - t0:.2f}s device {op.last_timings()['factor_ms']:.1f} ms"
+    print(f"{name} [{order}]: N={pen[0]} bw={prof['bandwidth']} factor wall {t1 - t0:.2f}s device {op.last_timings()['factor_ms']:.1f} ms"
           f" min_pivot_ratio {min(p['min_pivot_ratio'] for p in op.factor_profile()):.3e}", flush=True)
     v = zb.random_block(pen[0], nv, 1, cx=cx, orthonormalize=True)
     for rep_i in range(2):
