@@ -214,7 +214,7 @@ class FilterOperator:
     """
 
     def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None,
-                 ordering: str = "nd", nd_leaf: int = 512):
+                 ordering: str = "nd", nd_leaf: int = 256):
         L = lib()
         n, a, b = pencil
         cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "host.hpp"
 
 namespace zolo {
 
@@ -115,10 +116,19 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt
                const int* e_row, const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
                double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err);
 
-// DAG-scheduled sweeps over block-sparse row-scaled tiles: one task per
-// (block row, chain, column group), claimed in topological order.
-int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const Chain* d_chains, int nchains, int ncols, int64_t ld,
-                    int* flags, int epoch, int* counter, int fwd, int num_sms);
+// DAG-scheduled sweeps over block-sparse row-scaled tiles: the claim-ordered
+// schedule (host.hpp dag_schedule, nsched entries) expanded over (chain,
+// column group). Chunk tasks write partial sums into the chains' cbuf
+// (leading dimension ldp = 32 * nslots) and release cflags[(chain, group, slot)].
+struct DagSched {
+  const DagTask* tasks = nullptr;  // device
+  int ntask = 0;
+  int nslots = 0;
+};
+int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
+                    int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
+                    unsigned long long* trace = nullptr);
+int dag_groups(int ncols);
 
 // x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass
 // x_i = DinvL_i^H w_i); x is ld x ncols, D is nbk tiles.

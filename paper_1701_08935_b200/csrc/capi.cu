@@ -80,6 +80,12 @@ struct DevMem {
   }
 };
 
+// development knobs (schedule tuning); defaults are the shipped configuration
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 template <class T>
 void upload(DevMem& m, const std::vector<T>& v, cudaStream_t st) {
   m.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
@@ -134,14 +140,17 @@ struct zolo_ctx {
 
   // block-sparse (nested dissection) factor path
   int order_mode = ZOLO_ORDER_ND;
-  int64_t nd_leaf = 512;
+  int64_t nd_leaf = 256;
   bool sparse = false;
   SpGeom sgeom;
   std::vector<int> sp_col_cnt;
   int64_t critical_path = 0;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
+  DevMem sp_sched_fwd, sp_sched_bwd;
+  DagSched sched_fwd, sched_bwd;
+  int sp_nslots = 0;
   std::vector<cd*> sp_dt;
-  int64_t flags_cap = 0, prog_cap = 0;
+  int64_t flags_cap = 0, prog_cap = 0, cflags_off = 0;
   int epoch = 0;
 
   // GMRES state
@@ -506,6 +515,18 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
   s.col_tile = c.sp_col_tile.as<int>();
   s.tile_row = c.sp_tile_row.as<int>();
   c.sgeom = s;
+  {  // claim-ordered sweep schedules: wide block rows split into chunk tasks
+    static const int chunk = env_int("ZOLO_DAG_CHUNK", 16), near = env_int("ZOLO_DAG_NEAR", 4),
+                     order = env_int("ZOLO_DAG_ORDER", 2);
+    std::vector<DagTask> tf, tb;
+    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf);
+    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb);
+    upload(c.sp_sched_fwd, tf, c.st);
+    upload(c.sp_sched_bwd, tb, c.st);
+    c.sched_fwd = DagSched{c.sp_sched_fwd.as<DagTask>(), static_cast<int>(tf.size()), sf};
+    c.sched_bwd = DagSched{c.sp_sched_bwd.as<DagTask>(), static_cast<int>(tb.size()), sb};
+    c.sp_nslots = std::max(sf, sb);
+  }
 
   const int64_t nnz = static_cast<int64_t>(u.ci.size());
   std::vector<int> er(nnz), ec(nnz), pads;
@@ -630,9 +651,11 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   const int nch = c.nchains();
   while (static_cast<int>(c.xbuf.size()) < nch) c.xbuf.emplace_back(new DevMem());
   while (static_cast<int>(c.cbuf.size()) < nch) c.cbuf.emplace_back(new DevMem());
+  // cbuf: band helpers' partial solutions (ld rows), or the DAG chunk partials (32 x nslots rows)
+  const int64_t crows = c.sparse ? static_cast<int64_t>(TILE) * std::max(c.sp_nslots, 1) : ld;
   for (int i = 0; i < nch; ++i) {
     c.xbuf[i]->ensure(sizeof(cd) * ld * nc);
-    c.cbuf[i]->ensure(sizeof(cd) * ld * nc);
+    c.cbuf[i]->ensure(sizeof(cd) * crows * nc);
   }
   std::vector<Chain> fwd(nch), bwd(nch);
   for (int p = 0; p < c.r; ++p) {
@@ -660,16 +683,19 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   upload(c.chains_fwd, fwd, c.st);
   upload(c.chains_bwd, bwd, c.st);
   const int64_t ngroups = (nc + CG - 1) / CG;
-  const int64_t nflags = static_cast<int64_t>(nch) * ngroups * c.geom.nbk;
-  if (nflags > c.flags_cap) {
-    // [owner progress: nch x ngroups uint64 | helper flags: nch x ngroups x nbk int]
+  // [owner progress: nch x ngroups uint64 | block flags: nch x ngroups x nbk int |
+  //  DAG chunk flags: nch x dag_groups x nslots int]; all epoch-stamped, zeroed with the epoch
+  const int64_t nbflags = static_cast<int64_t>(nch) * ngroups * c.geom.nbk;
+  const int64_t nflags = nbflags + (c.sparse ? static_cast<int64_t>(nch) * dag_groups(nc) * c.sp_nslots : 0);
+  if (nflags > c.flags_cap || static_cast<int64_t>(nch) * ngroups > c.prog_cap) {
     c.prog_cap = static_cast<int64_t>(nch) * ngroups;
     const size_t bytes = sizeof(unsigned long long) * c.prog_cap + sizeof(int) * nflags;
     c.flags.ensure(bytes);
-    CK(cudaMemsetAsync(c.flags.p, 0, bytes, c.st));
+    CK(cudaMemsetAsync(c.flags.p, 0, c.flags.bytes, c.st));
     c.flags_cap = nflags;
     c.epoch = 0;
   }
+  c.cflags_off = nbflags;
   if (c.counter.ensure(sizeof(int) * 4)) CK(cudaMemsetAsync(c.counter.p, 0, sizeof(int) * 4, c.st));
   c.act_d.ensure(sizeof(int) * nc);
   if (c.act_h) cudaFreeHost(c.act_h);
@@ -697,10 +723,34 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   unsigned long long* fx = c.flags.as<unsigned long long>();
   int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
   if (c.sparse) {  // block-sparse factors: DAG-scheduled sweeps
-    dag_trsm_launch(c.st, c.sgeom, c.chains_fwd.as<Chain>(), nch, na, ld, fc, ++c.epoch, c.counter.as<int>(), 1,
-                    c.num_sms);
-    dag_trsm_launch(c.st, c.sgeom, c.chains_bwd.as<Chain>(), nch, na, ld, fc, ++c.epoch, c.counter.as<int>() + 1, 0,
-                    c.num_sms);
+    // ZOLO_TRACE=<file>: per-task timestamps of the first forward sweep (development aid)
+    static const char* dag_trace = std::getenv("ZOLO_TRACE");
+    unsigned long long* dtr = nullptr;
+    const size_t ntask = static_cast<size_t>(c.sched_fwd.ntask) * nch * dag_groups(na);
+    if (dag_trace && !c.trace_done) {
+      c.trace_buf.ensure(sizeof(unsigned long long) * 4 * ntask);
+      CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 4 * ntask, c.st));
+      dtr = c.trace_buf.as<unsigned long long>();
+    }
+    int* cf = fc + c.cflags_off;
+    dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>(), nch, na, ld, fc, cf, ++c.epoch,
+                    c.counter.as<int>(), 1, c.num_sms, dtr);
+    if (dtr) {
+      std::vector<unsigned long long> h(4 * ntask);
+      CK(cudaMemcpyAsync(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
+      CK(cudaStreamSynchronize(c.st));
+      if (FILE* fh = std::fopen(dag_trace, "w")) {
+        std::fprintf(fh, "# nb %d chains %d groups %d critical_path %lld schedule %d slots %d\n", c.geom.nbk, nch,
+                     dag_groups(na), static_cast<long long>(c.critical_path), c.sched_fwd.ntask,
+                     c.sched_fwd.nslots);
+        for (size_t q = 0; q < ntask; ++q)
+          std::fprintf(fh, "%llu %llu %llu %llu\n", h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+        std::fclose(fh);
+      }
+      c.trace_done = true;
+    }
+    dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>(), nch, na, ld, fc, cf, ++c.epoch,
+                    c.counter.as<int>() + 1, 0, c.num_sms);
     if (c.cx)
       for (int p = 0; p < c.r; ++p)
         blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);

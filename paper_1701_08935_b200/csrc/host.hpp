@@ -26,6 +26,25 @@ struct BlockStructure {
 void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std::vector<std::vector<int64_t>>& nodes);
 void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::vector<std::vector<int64_t>>& nodes,
                     int tile, BlockStructure& bs);
+// One claim-ordered task of a DAG triangular sweep (trsm.cu dag_kernel).
+// Block row i's dependencies, in processing order q (forward: ascending
+// column, backward: descending row), are cut into CHUNK tasks (out >= 0: sum
+// op(T~) u_j over q in [qa, qb) into partial slot `out`) and one ROW task
+// (out = -1: u_i = pre(b_i) - sum over q in [qa, qb) - partial slots
+// [pa, pa + pc)). Every task appears after all tasks it waits on, so
+// persistent CTAs claiming in this order cannot deadlock.
+struct DagTask {
+  int i, qa, qb, pa, pc, out;
+};
+// ptr/idx: forward = (row_ptr, row_idx), backward = (col_ptr, col_idx).
+// Rows with more than near + chunk dependencies keep the `near` latest in
+// the row task; the rest go to chunks of <= chunk dependencies, each claimed
+// right after the row task of its latest dependency. order: 0 = that
+// positional order, 1 = by earliest start time, 2 = by longest path to the
+// sweep's end (both weighted by tile products; both topological). Returns
+// the slot count.
+int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
+                 int near, int order, std::vector<DagTask>& tasks);
 void rcm_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm);
 int64_t bandwidth_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);
 int64_t profile_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);

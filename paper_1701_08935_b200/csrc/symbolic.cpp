@@ -260,4 +260,75 @@ void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::
   bs.critical_path = cp;
 }
 
+int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
+                 int near, int order, std::vector<DagTask>& tasks) {
+  if (chunk < 1 || near < 0) throw std::invalid_argument("dag_schedule: chunk >= 1, near >= 0");
+  // processing position of block row j in the sweep (forward: j, backward: nb-1-j)
+  auto position = [&](int64_t j) { return fwd ? j : nb - 1 - j; };
+  std::vector<std::vector<DagTask>> after(nb);  // chunks claimed right after row task at a position
+  std::vector<DagTask> rows(nb);
+  int slots = 0;
+  for (int64_t s = 0; s < nb; ++s) {
+    const int64_t i = fwd ? s : nb - 1 - s;
+    const int64_t e0 = ptr[i];
+    const int nd = static_cast<int>(ptr[i + 1] - e0);
+    // dependency at processing index q (ascending completion order)
+    auto dep = [&](int q) { return fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q]; };
+    DagTask row{static_cast<int>(i), 0, nd, slots, 0, -1};
+    if (nd > near + chunk) {
+      const int far = nd - near;
+      const int nchunk = (far + chunk - 1) / chunk;
+      for (int c = 0, q0 = 0; c < nchunk; ++c) {
+        const int q1 = static_cast<int>((static_cast<int64_t>(far) * (c + 1)) / nchunk);  // balanced cut
+        const int64_t last = position(dep(q1 - 1));
+        after[last].push_back(DagTask{static_cast<int>(i), q0, q1, 0, 0, slots++});
+        q0 = q1;
+      }
+      row.qa = far;
+      row.pc = nchunk;
+    }
+    rows[s] = row;
+  }
+  std::vector<DagTask> seq;  // positional topological order
+  for (int64_t s = 0; s < nb; ++s) {
+    seq.push_back(rows[s]);
+    for (const DagTask& t : after[s]) seq.push_back(t);
+  }
+  tasks.clear();
+  if (order == 0) {
+    tasks = std::move(seq);
+    return slots;
+  }
+  // list-scheduling priority over the task graph, with cost = tile products
+  // (+1 for the diagonal pre-transform and the store/flag latency)
+  const int64_t nt = static_cast<int64_t>(seq.size());
+  std::vector<int64_t> row_task(nb, -1), slot_task(slots, -1);
+  for (int64_t t = 0; t < nt; ++t) (seq[t].out >= 0 ? slot_task[seq[t].out] : row_task[seq[t].i]) = t;
+  std::vector<double> cost(nt);
+  std::vector<std::vector<int64_t>> deps(nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    const DagTask& k = seq[t];
+    const int64_t e0 = ptr[k.i];
+    const int nd = static_cast<int>(ptr[k.i + 1] - e0);
+    for (int q = k.qa; q < k.qb; ++q) deps[t].push_back(row_task[fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q]]);
+    for (int p = k.pa; p < k.pa + k.pc; ++p) deps[t].push_back(slot_task[p]);
+    cost[t] = (k.qb - k.qa) + 0.25 * k.pc + 2.0;
+  }
+  std::vector<double> key(nt, 0.0);
+  if (order == 1) {  // earliest start time (ascending)
+    for (int64_t t = 0; t < nt; ++t)
+      for (int64_t d : deps[t]) key[t] = std::max(key[t], key[d] + cost[d]);
+  } else {  // longest path to the end of the sweep (descending)
+    std::vector<double> bl(cost);
+    for (int64_t t = nt - 1; t >= 0; --t)
+      for (int64_t d : deps[t]) bl[d] = std::max(bl[d], cost[d] + bl[t]);
+    for (int64_t t = 0; t < nt; ++t) key[t] = -bl[t];
+  }
+  std::vector<int64_t> perm(nt);
+  for (int64_t t = 0; t < nt; ++t) perm[t] = t;
+  std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  for (int64_t t : perm) tasks.push_back(seq[t]);
+  return slots;
+}
+
 }  // namespace zolo

@@ -432,104 +432,240 @@ __global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
 // ---------------------------------------------------------------------------
 // DAG-scheduled sweeps over block-sparse factors (nested dissection etc.)
 // ---------------------------------------------------------------------------
+constexpr int DCG = 32;                  // columns per DAG task
+constexpr int XS2 = DCG * XPAD;          // padded 32 x 32 x block
+constexpr int DNS = 3;                   // pipeline stages
+constexpr int DAG_SMEM_FIXED = DNS * (TILE_S + XS2) * static_cast<int>(sizeof(cd));
+
 struct DagArgs {
   const Chain* chains;
+  const DagTask* tasks;
+  int ntask, nslots;
   int nchains, ngroups, ncols, epoch, fwd;
-  int64_t ld;
+  int64_t ld, ldp;
   SpGeom s;
-  int* flags;    // per (chain, group, block): epoch when u_i is final
+  int* flags;    // per (chain, 32-column group, block): epoch when u_i is final
+  int* cflags;   // per (chain, 32-column group, slot): epoch when the partial sum is written
   int* counter;  // [0] task counter, [2] wait-timeout error word
+  unsigned long long* trace;  // optional: per task (claim, dependencies done, done, smid|chunk|deps)
 };
 
+// Per-thread ownership of a 32 x 32 complex output block: warp w holds rows
+// 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1} (+16 for the
+// second block), i.e. two 8x8 DMMA blocks that share their A fragments.
+// acc[0..1]: first block's two outputs, acc[2..3]: second block's.
+template <bool OPH>
+__device__ __forceinline__ void mma_tile2_t(cd acc[4], const cd* ts, const cd* xs, const Frag& f) {
+  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
+  const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
+  cd a[TILE / 4];
+#pragma unroll
+  for (int kb = 0; kb < TILE / 4; ++kb) {
+    const int k = 4 * kb + am;
+    a[kb] = OPH ? ts[ar * APAD + k] : ts[k * APAD + ar];
+  }
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    cd b[TILE / 4];
+#pragma unroll
+    for (int kb = 0; kb < TILE / 4; ++kb) b[kb] = xs[(bc + 16 * half) * XPAD + 4 * kb + bm];
+    double re0[2] = {0.0, 0.0}, im0[2] = {0.0, 0.0}, re1[2] = {0.0, 0.0}, im1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kb = 0; kb < TILE / 4; ++kb) {
+      double* re = (kb & 1) ? re1 : re0;
+      double* im = (kb & 1) ? im1 : im0;
+      if (OPH) {
+        dmma(re, a[kb].x, b[kb].x);
+        dmma(re, a[kb].y, b[kb].y);
+        dmma(im, a[kb].x, b[kb].y);
+        dmma(im, -a[kb].y, b[kb].x);
+      } else {
+        dmma(re, a[kb].x, b[kb].x);
+        dmma(re, -a[kb].y, b[kb].y);
+        dmma(im, a[kb].x, b[kb].y);
+        dmma(im, a[kb].y, b[kb].x);
+      }
+    }
+    acc[2 * half].x += re0[0] + re1[0];
+    acc[2 * half + 1].x += re0[1] + re1[1];
+    acc[2 * half].y += im0[0] + im1[0];
+    acc[2 * half + 1].y += im0[1] + im1[1];
+  }
+}
+
+__device__ __forceinline__ void mma_tile2(cd acc[4], const cd* ts, const cd* xs, bool opH, const Frag& f) {
+  if (opH)
+    mma_tile2_t<true>(acc, ts, xs, f);
+  else
+    mma_tile2_t<false>(acc, ts, xs, f);
+}
+
+// 32 rows x 32 columns of a column-major block into [col*XPAD + row].
+__device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int c0, int nc) {
+  const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < DCG / 8; ++q) {
+    const int c = cc + 8 * q;
+    if (c < nc)
+      cp_async16_cg(&xs[c * XPAD + row], base + row + (c0 + c) * ld);
+    else
+      xs[c * XPAD + row] = mk(0.0, 0.0);
+  }
+}
+
+// output column of acc[q] within the 32-column group
+__device__ __forceinline__ int ocol(const Frag& f, int q) { return f.col + (q & 1) + 16 * (q >> 1); }
+
 // u_i = pre(b_i) - sum_{deps j} op(T~(i, j)) u_j for one (block row, chain,
-// group). Dependencies are processed earliest-completed first (forward:
-// ascending j, backward: descending j); their flags are read once, in
-// parallel, at task start, so only dependencies still running cost a wait.
-__device__ void dag_task(const DagArgs& A, int s, int ci, int gi, cd* smem, int* dsm) {
-  auto tile_s = [smem](int k) { return smem + k * TILE_S; };
-  auto x_s = [smem](int k) { return smem + NS * TILE_S + k * XS; };
-  cd* dinv_s = smem + NS * TILE_S + NS * XS;
-  cd* acc_s = dinv_s + TILE_S;
+// 32-column group). Dependencies are processed earliest-completed first
+// (forward: ascending j, backward: descending j); their flags are read once,
+// in parallel, at task start, so only dependencies still running cost a wait.
+// every thread spins on a share of cnt flags; the barrier publishes them all
+__device__ __forceinline__ void wait_flags_par(const int* f, int cnt, int epoch, int* err) {
+  for (int p = threadIdx.x; p < cnt; p += ST) {
+    int spins = 0;
+    while (ld_acquire(f + p) < epoch) {
+      if (++spins > 256) __nanosleep(32);
+      if (spins > (1 << 25)) {
+        atomicExch(err, 1);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int* dsm) {
+  auto tile_s = [smem](int k) { return smem + k * (TILE_S + XS2); };
+  auto x_s = [smem](int k) { return smem + k * (TILE_S + XS2) + TILE_S; };
   const SpGeom& G = A.s;
   int* dep_s = dsm;
   int* tid_s = dsm + (G.max_deps + 8);
   int* rdy_s = dsm + 2 * (G.max_deps + 8);
   const Chain ch = A.chains[ci];
+  const DagTask T = A.tasks[t];
   const bool fwd = A.fwd != 0;
   const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
+  const bool chunk = T.out >= 0;
   const Frag f = frag();
-  const int i = fwd ? s : G.nb - 1 - s;
-  const int c0 = gi * CG, nc = min(CG, A.ncols - c0);
+  const int i = T.i;
+  const int c0 = gi * DCG, nc = min(DCG, A.ncols - c0);
   const int64_t ld = A.ld;
-  int* flags = A.flags + (static_cast<size_t>(ci) * A.ngroups + gi) * G.nb;
+  const size_t cg = static_cast<size_t>(ci) * A.ngroups + gi;
+  int* flags = A.flags + cg * G.nb;
+  int* cflags = A.cflags + cg * A.nslots;
+  unsigned long long* trc =
+      A.trace ? A.trace + 4 * ((static_cast<size_t>(t) * A.nchains + ci) * A.ngroups + gi) : nullptr;
+  if (trc && threadIdx.x == 0) trc[0] = gtimer();
   const int e0 = fwd ? G.row_ptr[i] : G.col_ptr[i];
-  const int nd = (fwd ? G.row_ptr[i + 1] : G.col_ptr[i + 1]) - e0;
+  const int ndall = (fwd ? G.row_ptr[i + 1] : G.col_ptr[i + 1]) - e0;
+  const int nd = T.qb - T.qa;
   for (int q = threadIdx.x; q < nd; q += ST) {
-    const int e = fwd ? e0 + q : e0 + nd - 1 - q;  // processing order
+    const int qq = T.qa + q;
+    const int e = fwd ? e0 + qq : e0 + ndall - 1 - qq;  // processing order
     const int j = fwd ? G.row_idx[e] : G.col_idx[e];
     dep_s[q] = j;
     tid_s[q] = fwd ? e : G.col_tile[e];
     rdy_s[q] = ld_acquire(flags + j) >= A.epoch;
   }
-  cd bval[2];
-  if (ch.pre) {
-    load_tile(dinv_s, ch.pre + static_cast<size_t>(i) * TT);
-    load_x(acc_s, ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
+  cd bval[4];
+  if (chunk) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bval[q] = mk(0.0, 0.0);
+  } else if (ch.pre) {  // b~ = op(Dinv_i) b_i, staged through pipeline stage 0 before it is used
+    load_tile(tile_s(0), ch.pre + static_cast<size_t>(i) * TT);
+    load_x32(x_s(0), ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    bval[0] = bval[1] = mk(0.0, 0.0);
-    mma_tile(bval, dinv_s, acc_s, opH, f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bval[q] = mk(0.0, 0.0);
+    mma_tile2(bval, tile_s(0), x_s(0), opH, f);
   } else {
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int c = f.col + q;
+    for (int q = 0; q < 4; ++q) {
+      const int c = ocol(f, q);
       bval[q] = (c < nc) ? ch.src[static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld] : mk(0.0, 0.0);
     }
   }
   __syncthreads();
-  cd acc[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+  cd acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
   auto issue = [&](int q) {
-    const int buf = q % NS;
+    const int buf = q % DNS;
     load_tile(tile_s(buf), ch.off + static_cast<size_t>(tid_s[q]) * TT);
-    if (rdy_s[q]) load_x(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
+    if (rdy_s[q]) load_x32(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
   };
 #pragma unroll
-  for (int e = 0; e < NS - 1; ++e) {
+  for (int e = 0; e < DNS - 1; ++e) {
     if (e < nd) issue(e);
     cp_async_commit();
   }
+  if (T.pc > 0) {  // the chunk partial sums (older dependencies), while the first tiles load
+    wait_flags_par(cflags + T.pa, T.pc, A.epoch, A.counter + 2);
+    const cd* prow = ch.cbuf + static_cast<int64_t>(T.pa) * TILE + f.row + c0 * A.ldp;
+    for (int p = 0; p < T.pc; ++p) {
+      cd v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = ocol(f, q);
+        v[q] = (c < nc) ? __ldcg(prow + static_cast<int64_t>(p) * TILE + c * A.ldp) : mk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = cadd(acc[q], v[q]);
+    }
+  }
   for (int q = 0; q < nd; ++q) {
-    const int buf = q % NS;
+    const int buf = q % DNS;
     if (rdy_s[q]) {
-      cp_async_wait<NS - 2>();
+      cp_async_wait<DNS - 2>();
     } else {  // still running at task start: wait for it now, then fetch its u
       wait_flag(flags + dep_s[q], A.epoch, A.counter + 2);
-      load_x(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
+      load_x32(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
       cp_async_commit();
       cp_async_wait<0>();
     }
+    // one barrier per tile: entry q visible to all warps, entry q-1 finished
     __syncthreads();
-    if (q + NS - 1 < nd) issue(q + NS - 1);
+    if (q + DNS - 1 < nd) issue(q + DNS - 1);
     cp_async_commit();
-    mma_tile(acc, tile_s(buf), x_s(buf), opH, f);
+    mma_tile2(acc, tile_s(buf), x_s(buf), opH, f);
   }
   cp_async_wait<0>();
-  cd* urow = ch.dst + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
+  if (trc && threadIdx.x == 0) trc[1] = gtimer();
+  if (chunk) {
+    cd* prow = ch.cbuf + static_cast<int64_t>(T.out) * TILE + f.row + c0 * A.ldp;
 #pragma unroll
-  for (int q = 0; q < 2; ++q)
-    if (f.col + q < nc) urow[(f.col + q) * ld] = csub(bval[q], acc[q]);
+    for (int q = 0; q < 4; ++q) {
+      const int c = ocol(f, q);
+      if (c < nc) prow[c * A.ldp] = acc[q];
+    }
+  } else {
+    cd* urow = ch.dst + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = ocol(f, q);
+      if (c < nc) urow[c * ld] = csub(bval[q], acc[q]);
+    }
+  }
   __syncthreads();
-  if (threadIdx.x == 0) st_release(flags + i, A.epoch);  // cumulative release after the barrier
+  if (threadIdx.x == 0) {
+    st_release(chunk ? cflags + T.out : flags + i, A.epoch);  // cumulative release after the barrier
+    if (trc) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trc[2] = gtimer();
+      trc[3] = (static_cast<unsigned long long>(smid) << 32) | (chunk ? 0x80000000u : 0u) | static_cast<unsigned>(nd);
+    }
+  }
 }
 
 __global__ void __launch_bounds__(ST, 2) dag_kernel(DagArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cd* smem = reinterpret_cast<cd*>(smem_raw);
-  int* dsm = reinterpret_cast<int*>(smem_raw + SMEM_FIXED);
+  int* dsm = reinterpret_cast<int*>(smem_raw + DAG_SMEM_FIXED);
   __shared__ int task_s;
   const int per_step = A.nchains * A.ngroups;
-  const int ntasks = A.s.nb * per_step;
+  const int ntasks = A.ntask * per_step;
   for (;;) {
     if (threadIdx.x == 0) task_s = atomicAdd(A.counter, 1);
     __syncthreads();
@@ -567,9 +703,12 @@ void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int 
   if (ncols > 0) blockdiag_kernel<<<dim3(nb, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld);
 }
 
-int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const Chain* d_chains, int nchains, int ncols, int64_t ld,
-                    int* flags, int epoch, int* counter, int fwd, int num_sms) {
-  const int smem = SMEM_FIXED + 3 * (s.max_deps + 8) * static_cast<int>(sizeof(int));
+int dag_groups(int ncols) { return (ncols + DCG - 1) / DCG; }
+
+int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
+                    int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
+                    unsigned long long* trace) {
+  const int smem = DAG_SMEM_FIXED + 3 * (s.max_deps + 8) * static_cast<int>(sizeof(int));
   static int attr_set = 0;
   if (smem > attr_set) {
     cudaFuncSetAttribute(dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -578,16 +717,22 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const Chain* d_chains, int
   DagArgs a;
   a.chains = d_chains;
   a.nchains = nchains;
-  a.ngroups = (ncols + CG - 1) / CG;
+  a.ngroups = (ncols + DCG - 1) / DCG;
   a.ncols = ncols;
   a.epoch = epoch;
   a.fwd = fwd;
   a.ld = ld;
+  a.ldp = static_cast<int64_t>(sched.nslots) * TILE;
+  a.tasks = sched.tasks;
+  a.ntask = sched.ntask;
+  a.nslots = sched.nslots;
   a.s = s;
   a.flags = flags;
+  a.cflags = cflags;
   a.counter = counter;
+  a.trace = trace;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
-  const int ntasks = s.nb * nchains * a.ngroups;
+  const int ntasks = sched.ntask * nchains * a.ngroups;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel, ST, smem);
   if (per_sm < 1) per_sm = 1;
