@@ -435,7 +435,8 @@ __global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
 constexpr int DCG = 32;                  // columns per DAG task
 constexpr int XS2 = DCG * XPAD;          // padded 32 x 32 x block
 constexpr int DNS = 3;                   // pipeline stages
-constexpr int DAG_SMEM_FIXED = DNS * (TILE_S + XS2) * static_cast<int>(sizeof(cd));
+constexpr int TSW = TT;                  // swizzled (unpadded) tile
+constexpr int DAG_SMEM_FIXED = DNS * (TSW + XS2) * static_cast<int>(sizeof(cd));
 
 struct DagArgs {
   const Chain* chains;
@@ -450,50 +451,86 @@ struct DagArgs {
   unsigned long long* trace;  // optional: per task (claim, dependencies done, done, smid|chunk|deps)
 };
 
-// Per-thread ownership of a 32 x 32 complex output block: warp w holds rows
-// 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1} (+16 for the
-// second block), i.e. two 8x8 DMMA blocks that share their A fragments.
-// acc[0..1]: first block's two outputs, acc[2..3]: second block's.
-template <bool OPH>
-__device__ __forceinline__ void mma_tile2_t(cd acc[4], const cd* ts, const cd* xs, const Frag& f) {
-  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
-  const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
-  cd a[TILE / 4];
+// Swizzled tile layout: element (row, col) of a 32 x 32 tile at
+// col*32 + (row ^ swz(col)), swz(c) = 4 (c&1) + 2 ((c>>1)&1). Both fragment
+// patterns -- op N reads T(ar, k), op H reads T(k, ar), with ar = lane/4 and
+// k = lane%4 (+ block offsets) -- hit 8 distinct 16-byte bank groups per
+// quarter warp, so the conjugate-transposed chains are conflict free too, and
+// the tile needs no padding.
+__device__ __forceinline__ int swz(int c) { return ((c & 1) << 2) | (c & 2); }
+
+__device__ __forceinline__ void load_tile_sw(cd* s, const cd* g) {
 #pragma unroll
-  for (int kb = 0; kb < TILE / 4; ++kb) {
-    const int k = 4 * kb + am;
-    a[kb] = OPH ? ts[ar * APAD + k] : ts[k * APAD + ar];
-  }
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    cd b[TILE / 4];
-#pragma unroll
-    for (int kb = 0; kb < TILE / 4; ++kb) b[kb] = xs[(bc + 16 * half) * XPAD + 4 * kb + bm];
-    double re0[2] = {0.0, 0.0}, im0[2] = {0.0, 0.0}, re1[2] = {0.0, 0.0}, im1[2] = {0.0, 0.0};
-#pragma unroll
-    for (int kb = 0; kb < TILE / 4; ++kb) {
-      double* re = (kb & 1) ? re1 : re0;
-      double* im = (kb & 1) ? im1 : im0;
-      if (OPH) {
-        dmma(re, a[kb].x, b[kb].x);
-        dmma(re, a[kb].y, b[kb].y);
-        dmma(im, a[kb].x, b[kb].y);
-        dmma(im, -a[kb].y, b[kb].x);
-      } else {
-        dmma(re, a[kb].x, b[kb].x);
-        dmma(re, -a[kb].y, b[kb].y);
-        dmma(im, a[kb].x, b[kb].y);
-        dmma(im, a[kb].y, b[kb].x);
-      }
-    }
-    acc[2 * half].x += re0[0] + re1[0];
-    acc[2 * half + 1].x += re0[1] + re1[1];
-    acc[2 * half].y += im0[0] + im1[0];
-    acc[2 * half + 1].y += im0[1] + im1[1];
+  for (int q = 0; q < TT / ST; ++q) {
+    const int e = threadIdx.x + q * ST;
+    const int col = e / TILE, row = e % TILE;
+    cp_async16_cg(&s[col * TILE + (row ^ swz(col))], g + e);
   }
 }
 
-__device__ __forceinline__ void mma_tile2(cd acc[4], const cd* ts, const cd* xs, bool opH, const Frag& f) {
+// non-volatile DMMA: lets the scheduler interleave independent accumulators
+__device__ __forceinline__ void dmma_nv(double c[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// Per-thread ownership of a 32 x 32 complex output block: warp w holds rows
+// 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1} (+16 for the
+// second block), i.e. two 8x8 DMMA blocks that share their A fragments.
+// DMMA accumulators live across tiles: acc8[h][p][ri][e] (half h, k-step
+// parity p, re/im, element e) = 8 independent chains, folded once per task.
+struct Acc8 {
+  double v[2][2][2][2];
+};
+__device__ __forceinline__ void acc8_zero(Acc8& a) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int ri = 0; ri < 2; ++ri) a.v[h][p][ri][0] = a.v[h][p][ri][1] = 0.0;
+}
+// out[2h + e] = the complex output (row, ocol(2h + e))
+__device__ __forceinline__ void acc8_fold(const Acc8& a, cd out[4]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      out[2 * h + e] = mk(a.v[h][0][0][e] + a.v[h][1][0][e], a.v[h][0][1][e] + a.v[h][1][1][e]);
+}
+
+template <bool OPH>
+__device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* xs, const Frag& f) {
+  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
+  const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
+  const int sa = swz(ar);
+  cd a[TILE / 4], b0[TILE / 4], b1[TILE / 4];
+#pragma unroll
+  for (int kb = 0; kb < TILE / 4; ++kb) {
+    const int k = 4 * kb + am;
+    a[kb] = OPH ? ts[ar * TILE + (k ^ sa)] : ts[k * TILE + (ar ^ swz(k))];
+    b0[kb] = xs[bc * XPAD + k];
+    b1[kb] = xs[(bc + 16) * XPAD + k];
+  }
+#pragma unroll
+  for (int kb = 0; kb < TILE / 4; ++kb) {
+    const int p = kb & 1;
+    // op N: re += ax bx - ay by, im += ax by + ay bx; op H (conj a): re += ax bx + ay by, im += ax by - ay bx
+    const double ny = OPH ? a[kb].y : -a[kb].y;
+    const double py = OPH ? -a[kb].y : a[kb].y;
+    dmma_nv(acc.v[0][p][0], a[kb].x, b0[kb].x);
+    dmma_nv(acc.v[1][p][0], a[kb].x, b1[kb].x);
+    dmma_nv(acc.v[0][p][1], a[kb].x, b0[kb].y);
+    dmma_nv(acc.v[1][p][1], a[kb].x, b1[kb].y);
+    dmma_nv(acc.v[0][p][0], ny, b0[kb].y);
+    dmma_nv(acc.v[1][p][0], ny, b1[kb].y);
+    dmma_nv(acc.v[0][p][1], py, b0[kb].x);
+    dmma_nv(acc.v[1][p][1], py, b1[kb].x);
+  }
+}
+
+__device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs, bool opH, const Frag& f) {
   if (opH)
     mma_tile2_t<true>(acc, ts, xs, f);
   else
@@ -536,8 +573,8 @@ __device__ __forceinline__ void wait_flags_par(const int* f, int cnt, int epoch,
 }
 
 __device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int* dsm) {
-  auto tile_s = [smem](int k) { return smem + k * (TILE_S + XS2); };
-  auto x_s = [smem](int k) { return smem + k * (TILE_S + XS2) + TILE_S; };
+  auto tile_s = [smem](int k) { return smem + k * (TSW + XS2); };
+  auto x_s = [smem](int k) { return smem + k * (TSW + XS2) + TSW; };
   const SpGeom& G = A.s;
   int* dep_s = dsm;
   int* tid_s = dsm + (G.max_deps + 8);
@@ -573,14 +610,15 @@ __device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int*
 #pragma unroll
     for (int q = 0; q < 4; ++q) bval[q] = mk(0.0, 0.0);
   } else if (ch.pre) {  // b~ = op(Dinv_i) b_i, staged through pipeline stage 0 before it is used
-    load_tile(tile_s(0), ch.pre + static_cast<size_t>(i) * TT);
+    load_tile_sw(tile_s(0), ch.pre + static_cast<size_t>(i) * TT);
     load_x32(x_s(0), ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) bval[q] = mk(0.0, 0.0);
-    mma_tile2(bval, tile_s(0), x_s(0), opH, f);
+    Acc8 pre;
+    acc8_zero(pre);
+    mma_tile2(pre, tile_s(0), x_s(0), opH, f);
+    acc8_fold(pre, bval);
   } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -589,10 +627,12 @@ __device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int*
     }
   }
   __syncthreads();
-  cd acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+  Acc8 acc8;
+  acc8_zero(acc8);
+  cd acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};  // chunk partials
   auto issue = [&](int q) {
     const int buf = q % DNS;
-    load_tile(tile_s(buf), ch.off + static_cast<size_t>(tid_s[q]) * TT);
+    load_tile_sw(tile_s(buf), ch.off + static_cast<size_t>(tid_s[q]) * TT);
     if (rdy_s[q]) load_x32(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
   };
 #pragma unroll
@@ -628,9 +668,15 @@ __device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int*
     __syncthreads();
     if (q + DNS - 1 < nd) issue(q + DNS - 1);
     cp_async_commit();
-    mma_tile2(acc, tile_s(buf), x_s(buf), opH, f);
+    mma_tile2(acc8, tile_s(buf), x_s(buf), opH, f);
   }
   cp_async_wait<0>();
+  {
+    cd prod[4];
+    acc8_fold(acc8, prod);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = cadd(acc[q], prod[q]);
+  }
   if (trc && threadIdx.x == 0) trc[1] = gtimer();
   if (chunk) {
     cd* prow = ch.cbuf + static_cast<int64_t>(T.out) * TILE + f.row + c0 * A.ldp;
