@@ -120,8 +120,11 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt
 // schedule (host.hpp dag_schedule, nsched entries) expanded over (chain,
 // column group). Chunk tasks write partial sums into the chains' cbuf
 // (leading dimension ldp = 32 * nslots) and release cflags[(chain, group, slot)].
+// Task record (ints): [i, nd, pa, pc, out, 0, 0, 0, (j, tile id) x nd];
+// nd <= DAG_REC_DEPS (the schedule keeps near + chunk within it).
+constexpr int DAG_REC = 64, DAG_REC_HDR = 8, DAG_REC_DEPS = (DAG_REC - DAG_REC_HDR) / 2;
 struct DagSched {
-  const DagTask* tasks = nullptr;  // device
+  const int* recs = nullptr;  // device, ntask x DAG_REC
   int ntask = 0;
   int nslots = 0;
 };

@@ -516,15 +516,35 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
   s.tile_row = c.sp_tile_row.as<int>();
   c.sgeom = s;
   {  // claim-ordered sweep schedules: wide block rows split into chunk tasks
-    static const int chunk = env_int("ZOLO_DAG_CHUNK", 16), near = env_int("ZOLO_DAG_NEAR", 4),
+    static const int near = std::min(std::max(env_int("ZOLO_DAG_NEAR", 4), 0), DAG_REC_DEPS - 1),
+                     chunk = std::min(std::max(env_int("ZOLO_DAG_CHUNK", 16), 1), DAG_REC_DEPS - near),
                      order = env_int("ZOLO_DAG_ORDER", 2);
+    // self-contained task records: header + the (j, tile id) pairs in processing order
+    auto records = [&](const std::vector<DagTask>& ts, bool fwd) {
+      std::vector<int> rec(ts.size() * DAG_REC, 0);
+      for (size_t t = 0; t < ts.size(); ++t) {
+        const DagTask& k = ts[t];
+        int* r = rec.data() + t * DAG_REC;
+        const int64_t e0 = fwd ? bs.row_ptr[k.i] : bs.col_ptr[k.i];
+        const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
+        const int nd = k.qb - k.qa;
+        require(nd <= DAG_REC_DEPS, "zolo_factorize: DAG task record overflow");
+        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out;
+        for (int q = 0; q < nd; ++q) {
+          const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
+          r[DAG_REC_HDR + 2 * q] = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
+          r[DAG_REC_HDR + 2 * q + 1] = static_cast<int>(fwd ? e : bs.col_tile[e]);
+        }
+      }
+      return rec;
+    };
     std::vector<DagTask> tf, tb;
     const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf);
     const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb);
-    upload(c.sp_sched_fwd, tf, c.st);
-    upload(c.sp_sched_bwd, tb, c.st);
-    c.sched_fwd = DagSched{c.sp_sched_fwd.as<DagTask>(), static_cast<int>(tf.size()), sf};
-    c.sched_bwd = DagSched{c.sp_sched_bwd.as<DagTask>(), static_cast<int>(tb.size()), sb};
+    upload(c.sp_sched_fwd, records(tf, true), c.st);
+    upload(c.sp_sched_bwd, records(tb, false), c.st);
+    c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), static_cast<int>(tf.size()), sf};
+    c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb};
     c.sp_nslots = std::max(sf, sb);
   }
 

@@ -440,7 +440,7 @@ constexpr int DAG_SMEM_FIXED = DNS * (TSW + XS2) * static_cast<int>(sizeof(cd));
 
 struct DagArgs {
   const Chain* chains;
-  const DagTask* tasks;
+  const int* recs;  // ntask x DAG_REC task records (band.cuh)
   int ntask, nslots;
   int nchains, ngroups, ncols, epoch, fwd;
   int64_t ld, ldp;
@@ -500,7 +500,7 @@ __device__ __forceinline__ void acc8_fold(const Acc8& a, cd out[4]) {
       out[2 * h + e] = mk(a.v[h][0][0][e] + a.v[h][1][0][e], a.v[h][0][1][e] + a.v[h][1][1][e]);
 }
 
-template <bool OPH>
+template <bool OPH, bool NEG>
 __device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* xs, const Frag& f) {
   const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
   const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
@@ -510,6 +510,7 @@ __device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* x
   for (int kb = 0; kb < TILE / 4; ++kb) {
     const int k = 4 * kb + am;
     a[kb] = OPH ? ts[ar * TILE + (k ^ sa)] : ts[k * TILE + (ar ^ swz(k))];
+    if (NEG) a[kb] = mk(-a[kb].x, -a[kb].y);
     b0[kb] = xs[bc * XPAD + k];
     b1[kb] = xs[(bc + 16) * XPAD + k];
   }
@@ -530,11 +531,19 @@ __device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* x
   }
 }
 
-__device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs, bool opH, const Frag& f) {
-  if (opH)
-    mma_tile2_t<true>(acc, ts, xs, f);
-  else
-    mma_tile2_t<false>(acc, ts, xs, f);
+// acc += op(T) X, or -= with neg (the pre-transform entry)
+__device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs, bool opH, bool neg, const Frag& f) {
+  if (opH) {
+    if (neg)
+      mma_tile2_t<true, true>(acc, ts, xs, f);
+    else
+      mma_tile2_t<true, false>(acc, ts, xs, f);
+  } else {
+    if (neg)
+      mma_tile2_t<false, true>(acc, ts, xs, f);
+    else
+      mma_tile2_t<false, false>(acc, ts, xs, f);
+  }
 }
 
 // 32 rows x 32 columns of a column-major block into [col*XPAD + row].
@@ -553,10 +562,6 @@ __device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int
 // output column of acc[q] within the 32-column group
 __device__ __forceinline__ int ocol(const Frag& f, int q) { return f.col + (q & 1) + 16 * (q >> 1); }
 
-// u_i = pre(b_i) - sum_{deps j} op(T~(i, j)) u_j for one (block row, chain,
-// 32-column group). Dependencies are processed earliest-completed first
-// (forward: ascending j, backward: descending j); their flags are read once,
-// in parallel, at task start, so only dependencies still running cost a wait.
 // every thread spins on a share of cnt flags; the barrier publishes them all
 __device__ __forceinline__ void wait_flags_par(const int* f, int cnt, int epoch, int* err) {
   for (int p = threadIdx.x; p < cnt; p += ST) {
@@ -572,78 +577,68 @@ __device__ __forceinline__ void wait_flags_par(const int* f, int cnt, int epoch,
   __syncthreads();
 }
 
-__device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int* dsm) {
+// One (task record, chain, 32-column group):
+//   row task:   u_i = pre(b_i) - sum_q op(T~(i, j_q)) u_(j_q) - sum_p partial_p
+//   chunk task: partial_out = sum_q op(T~(i, j_q)) u_(j_q)
+// The pre-transform op(Dinv_i) b_i is pipeline entry 0 with a negated A
+// operand, so the accumulator holds S = sum - pre(b) and u_i = -S: no
+// serialised prologue. Dependencies come in processing order (earliest
+// completed first); their flags are read once, in parallel, at task start,
+// so only dependencies still running cost a wait. `rec` is in shared memory
+// (prefetched by the previous task); `nrec` is where this task prefetches the
+// record of `next` (the CTA's next claimed task) once its first barrier passed.
+__device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* smem, int* rdy_s, int* nrec,
+                         int next_rec, unsigned long long* trc) {
   auto tile_s = [smem](int k) { return smem + k * (TSW + XS2); };
   auto x_s = [smem](int k) { return smem + k * (TSW + XS2) + TSW; };
-  const SpGeom& G = A.s;
-  int* dep_s = dsm;
-  int* tid_s = dsm + (G.max_deps + 8);
-  int* rdy_s = dsm + 2 * (G.max_deps + 8);
   const Chain ch = A.chains[ci];
-  const DagTask T = A.tasks[t];
-  const bool fwd = A.fwd != 0;
+  const int i = rec[0], nd = rec[1], pa = rec[2], pc = rec[3], out = rec[4];
+  const int* dq = rec + DAG_REC_HDR;  // (j, tile id) pairs
+  const bool chunk = out >= 0;
   const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
-  const bool chunk = T.out >= 0;
   const Frag f = frag();
-  const int i = T.i;
   const int c0 = gi * DCG, nc = min(DCG, A.ncols - c0);
   const int64_t ld = A.ld;
-  const size_t cg = static_cast<size_t>(ci) * A.ngroups + gi;
-  int* flags = A.flags + cg * G.nb;
-  int* cflags = A.cflags + cg * A.nslots;
-  unsigned long long* trc =
-      A.trace ? A.trace + 4 * ((static_cast<size_t>(t) * A.nchains + ci) * A.ngroups + gi) : nullptr;
-  if (trc && threadIdx.x == 0) trc[0] = gtimer();
-  const int e0 = fwd ? G.row_ptr[i] : G.col_ptr[i];
-  const int ndall = (fwd ? G.row_ptr[i + 1] : G.col_ptr[i + 1]) - e0;
-  const int nd = T.qb - T.qa;
-  for (int q = threadIdx.x; q < nd; q += ST) {
-    const int qq = T.qa + q;
-    const int e = fwd ? e0 + qq : e0 + ndall - 1 - qq;  // processing order
-    const int j = fwd ? G.row_idx[e] : G.col_idx[e];
-    dep_s[q] = j;
-    tid_s[q] = fwd ? e : G.col_tile[e];
-    rdy_s[q] = ld_acquire(flags + j) >= A.epoch;
-  }
+  const size_t cgi = static_cast<size_t>(ci) * A.ngroups + gi;
+  int* flags = A.flags + cgi * A.s.nb;
+  int* cflags = A.cflags + cgi * A.nslots;
+  const int hp = (!chunk && ch.pre) ? 1 : 0;  // entry 0 = pre-transform
+  const int ne = hp + nd;
+  for (int q = threadIdx.x; q < nd; q += ST) rdy_s[q] = ld_acquire(flags + dq[2 * q]) >= A.epoch;
   cd bval[4];
-  if (chunk) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) bval[q] = mk(0.0, 0.0);
-  } else if (ch.pre) {  // b~ = op(Dinv_i) b_i, staged through pipeline stage 0 before it is used
-    load_tile_sw(tile_s(0), ch.pre + static_cast<size_t>(i) * TT);
-    load_x32(x_s(0), ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    Acc8 pre;
-    acc8_zero(pre);
-    mma_tile2(pre, tile_s(0), x_s(0), opH, f);
-    acc8_fold(pre, bval);
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = ocol(f, q);
-      bval[q] = (c < nc) ? ch.src[static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld] : mk(0.0, 0.0);
-    }
+  for (int q = 0; q < 4; ++q) {
+    const int c = ocol(f, q);
+    bval[q] = (!chunk && !ch.pre && c < nc) ? ch.src[static_cast<int64_t>(i) * TILE + f.row + (c0 + c) * ld]
+                                            : mk(0.0, 0.0);
   }
   __syncthreads();
-  Acc8 acc8;
-  acc8_zero(acc8);
-  cd acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};  // chunk partials
-  auto issue = [&](int q) {
-    const int buf = q % DNS;
-    load_tile_sw(tile_s(buf), ch.off + static_cast<size_t>(tid_s[q]) * TT);
-    if (rdy_s[q]) load_x32(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
+  if (next_rec >= 0 && threadIdx.x < DAG_REC * 4 / 16)  // prefetch the next task's record
+    cp_async16_cg(nrec + 4 * threadIdx.x, A.recs + static_cast<size_t>(next_rec) * DAG_REC + 4 * threadIdx.x);
+  auto ready = [&](int e) { return e < hp || rdy_s[e - hp]; };
+  auto issue = [&](int e) {
+    const int buf = e % DNS;
+    if (e < hp) {
+      load_tile_sw(tile_s(buf), ch.pre + static_cast<size_t>(i) * TT);
+      load_x32(x_s(buf), ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
+    } else {
+      const int q = e - hp;
+      load_tile_sw(tile_s(buf), ch.off + static_cast<size_t>(dq[2 * q + 1]) * TT);
+      if (rdy_s[q]) load_x32(x_s(buf), ch.dst + static_cast<int64_t>(dq[2 * q]) * TILE, ld, c0, nc);
+    }
   };
 #pragma unroll
   for (int e = 0; e < DNS - 1; ++e) {
-    if (e < nd) issue(e);
+    if (e < ne) issue(e);
     cp_async_commit();
   }
-  if (T.pc > 0) {  // the chunk partial sums (older dependencies), while the first tiles load
-    wait_flags_par(cflags + T.pa, T.pc, A.epoch, A.counter + 2);
-    const cd* prow = ch.cbuf + static_cast<int64_t>(T.pa) * TILE + f.row + c0 * A.ldp;
-    for (int p = 0; p < T.pc; ++p) {
+  Acc8 acc8;
+  acc8_zero(acc8);
+  cd acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};  // chunk partials
+  if (pc > 0) {  // partial sums of the older dependencies, while the first tiles load
+    wait_flags_par(cflags + pa, pc, A.epoch, A.counter + 2);
+    const cd* prow = ch.cbuf + static_cast<int64_t>(pa) * TILE + f.row + c0 * A.ldp;
+    for (int p = 0; p < pc; ++p) {
       cd v[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -654,32 +649,33 @@ __device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int*
       for (int q = 0; q < 4; ++q) acc[q] = cadd(acc[q], v[q]);
     }
   }
-  for (int q = 0; q < nd; ++q) {
-    const int buf = q % DNS;
-    if (rdy_s[q]) {
+  for (int e = 0; e < ne; ++e) {
+    const int buf = e % DNS;
+    if (ready(e)) {
       cp_async_wait<DNS - 2>();
     } else {  // still running at task start: wait for it now, then fetch its u
-      wait_flag(flags + dep_s[q], A.epoch, A.counter + 2);
-      load_x32(x_s(buf), ch.dst + static_cast<int64_t>(dep_s[q]) * TILE, ld, c0, nc);
+      const int j = dq[2 * (e - hp)];
+      wait_flag(flags + j, A.epoch, A.counter + 2);
+      load_x32(x_s(buf), ch.dst + static_cast<int64_t>(j) * TILE, ld, c0, nc);
       cp_async_commit();
       cp_async_wait<0>();
     }
-    // one barrier per tile: entry q visible to all warps, entry q-1 finished
+    // one barrier per tile: entry e visible to all warps, entry e-1 finished
     __syncthreads();
-    if (q + DNS - 1 < nd) issue(q + DNS - 1);
+    if (e + DNS - 1 < ne) issue(e + DNS - 1);
     cp_async_commit();
-    mma_tile2(acc8, tile_s(buf), x_s(buf), opH, f);
+    mma_tile2(acc8, tile_s(buf), x_s(buf), opH, e < hp, f);
   }
   cp_async_wait<0>();
+  if (trc && threadIdx.x == 0) trc[1] = gtimer();
   {
     cd prod[4];
     acc8_fold(acc8, prod);
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = cadd(acc[q], prod[q]);
   }
-  if (trc && threadIdx.x == 0) trc[1] = gtimer();
   if (chunk) {
-    cd* prow = ch.cbuf + static_cast<int64_t>(T.out) * TILE + f.row + c0 * A.ldp;
+    cd* prow = ch.cbuf + static_cast<int64_t>(out) * TILE + f.row + c0 * A.ldp;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = ocol(f, q);
@@ -690,12 +686,12 @@ __device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int*
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = ocol(f, q);
-      if (c < nc) urow[c * ld] = csub(bval[q], acc[q]);
+      if (c < nc) urow[c * ld] = csub(bval[q], acc[q]);  // hp: bval = 0, acc = S
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    st_release(chunk ? cflags + T.out : flags + i, A.epoch);  // cumulative release after the barrier
+    st_release(chunk ? cflags + out : flags + i, A.epoch);  // cumulative release after the barrier
     if (trc) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -705,22 +701,37 @@ __device__ void dag_task(const DagArgs& A, int t, int ci, int gi, cd* smem, int*
   }
 }
 
+// Persistent CTAs claim (record, chain, group) tasks in schedule order; each
+// claims its NEXT task when it starts the current one and prefetches that
+// task's record behind the current tile pipeline.
 __global__ void __launch_bounds__(ST, 2) dag_kernel(DagArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cd* smem = reinterpret_cast<cd*>(smem_raw);
-  int* dsm = reinterpret_cast<int*>(smem_raw + DAG_SMEM_FIXED);
-  __shared__ int task_s;
+  int* recb = reinterpret_cast<int*>(smem_raw + DAG_SMEM_FIXED);  // 2 x DAG_REC
+  int* rdy_s = recb + 2 * DAG_REC;
+  __shared__ int cur_s, next_s;
   const int per_step = A.nchains * A.ngroups;
   const int ntasks = A.ntask * per_step;
-  for (;;) {
-    if (threadIdx.x == 0) task_s = atomicAdd(A.counter, 1);
+  if (threadIdx.x == 0) cur_s = atomicAdd(A.counter, 1);
+  __syncthreads();
+  int t = cur_s, b = 0;
+  if (t < ntasks && threadIdx.x < DAG_REC * 4 / 16)
+    cp_async16_cg(recb + 4 * threadIdx.x, A.recs + static_cast<size_t>(t / per_step) * DAG_REC + 4 * threadIdx.x);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  while (t < ntasks) {
+    unsigned long long* trc = A.trace ? A.trace + 4 * static_cast<size_t>(t) : nullptr;
+    if (trc && threadIdx.x == 0) trc[0] = gtimer();
+    if (threadIdx.x == 0) next_s = atomicAdd(A.counter, 1);
     __syncthreads();
-    const int t = task_s;
-    __syncthreads();
-    if (t >= ntasks) break;
-    const int s = t / per_step, rem = t % per_step;
-    dag_task(A, s, rem / A.ngroups, rem % A.ngroups, smem, dsm);
-    __syncthreads();
+    const int tn = next_s;
+    const int rem = t % per_step;
+    dag_task(A, recb + b * DAG_REC, rem / A.ngroups, rem % A.ngroups, smem, rdy_s, recb + (b ^ 1) * DAG_REC,
+             tn < ntasks ? tn / per_step : -1, trc);
+    __syncthreads();  // (dag_task ends with cp.async.wait_all: the next record has landed)
+    t = tn;
+    b ^= 1;
   }
 }
 
@@ -754,7 +765,7 @@ int dag_groups(int ncols) { return (ncols + DCG - 1) / DCG; }
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
                     unsigned long long* trace) {
-  const int smem = DAG_SMEM_FIXED + 3 * (s.max_deps + 8) * static_cast<int>(sizeof(int));
+  const int smem = DAG_SMEM_FIXED + (2 * DAG_REC + DAG_REC_DEPS + 8) * static_cast<int>(sizeof(int));
   static int attr_set = 0;
   if (smem > attr_set) {
     cudaFuncSetAttribute(dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -769,7 +780,7 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   a.fwd = fwd;
   a.ld = ld;
   a.ldp = static_cast<int64_t>(sched.nslots) * TILE;
-  a.tasks = sched.tasks;
+  a.recs = sched.recs;
   a.ntask = sched.ntask;
   a.nslots = sched.nslots;
   a.s = s;
