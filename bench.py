@@ -8,8 +8,9 @@ interior eigenvalues near 6 (paper_1701_08935_b200/configs.py).
 
 A step = one FilterOperator::apply_filter (filter_engine.hpp:86-155) of the
 whole n_v-column block: 2r outer shifts by lock-step multi-shift GMRES on
-G, every G application = r shifted band LU solves + B SpMM. The r band
-factorizations are setup (outside the timed region, reported separately).
+G, every G application = r shifted LU solves (block-sparse nested-dissection
+factors, DAG-scheduled DMMA sweeps) + B SpMM. The r factorizations are setup
+(outside the timed region, reported separately as t_factor_ms).
 
   value : device-resident block, CUDA events on the library stream, K steps.
   e2e   : the public host API (zolo_apply_filter) from pinned host memory,
@@ -101,28 +102,6 @@ def load_peaks():
     except (OSError, ValueError, KeyError):
         pass
     return out
-
-
-def band_triangle_entries(n, bw):
-    """Entries of a strictly triangular band of half-bandwidth bw: sum_i min(i, bw)."""
-    if bw >= n:
-        return n * (n - 1) // 2
-    return bw * n - bw * (bw + 1) // 2
-
-
-def envelope_entries(pencil):
-    """profile_under(RCM) of the pattern of A - iB (rcm.hpp:133-147)."""
-    import scipy.sparse as sp
-
-    import paper_1701_08935_b200 as zb
-
-    n, a, b = pencil
-    am = sp.csr_matrix((np.ones(len(a[1])), a[1], a[0]), shape=(n, n))
-    bm = sp.identity(n) if b is None else sp.csr_matrix((np.ones(len(b[1])), b[1], b[0]), shape=(n, n))
-    u = (am + bm).tocsr()
-    u.sort_indices()
-    _, _, prof = zb.rcm(n, u.indptr.astype(np.int64), u.indices.astype(np.int64))
-    return prof
 
 
 def workload(name):
@@ -218,7 +197,7 @@ def main():
     design = build_filter_design(gaps, r)
     op = zb.FilterOperator(pen, design, r, is_complex=cx, device=local)
     t_factor_ms = op.last_timings()["factor_ms"]
-    bw = op.factor_profile()[0]["bandwidth"]
+    sp = op.sweep_profile()
 
     # each rank: its own n_v-column block (columns are independent units)
     v = zb.random_block(n, nv, 1 + rank, cx=cx, orthonormalize=True)
@@ -293,14 +272,14 @@ def main():
     esize = 16 if cx else 8
     assert np.isfinite(yh).all()
 
-    # roofline of the dominant kernel (the wavefront triangular solve)
+    # roofline of the dominant kernel (the DAG-scheduled block-sparse triangular sweeps)
     peaks = load_peaks()
-    # factor nnz = the RCM envelope (profile) of the pattern of A - iB: unpivoted
-    # elimination fills exactly the envelope (band_factor.hpp:158-177 skips the rest)
-    nnz_l = envelope_entries(pen)
-    nnz_u = nnz_l + n
+    # per G application, per column, per pole and per solve (P = 2 for complex pencils: solve + adjoint):
+    # forward + backward sweep over the off-diagonal tiles plus the diagonal-block inverse
+    # products = 2 (ntiles + nb) complex 32x32 tile-column products of 8 * 1024 flops
     chains_per_pole = 2 if cx else 1
-    trsm_flops = opapps * r * chains_per_pole * 8.0 * (nnz_l + nnz_u)  # all launches of the K steps
+    tile_products = 2 * (sp["offdiag_tiles"] + sp["block_rows"])
+    trsm_flops = opapps * r * chains_per_pole * tile_products * 8.0 * 1024  # all launches of the K steps
     achieved = trsm_flops / (trsm_ms * 1e-3) / 1e12 if trsm_ms > 0 else 0.0
     peak = peaks.get("fp64_tflops")
     traffic = None
@@ -314,18 +293,21 @@ def main():
         "dtype": "c128" if cx else "f64", "data": "synthetic (seeded generator, BASELINE config shape)",
         "config": {"workload": f"{args.config}: 3D 7-point Laplacian 32^3 + U[0,1] potential, SPD mass B, N={n}, "
                                f"r={r} (p={2 * r} poles), n_v={nv}, gmres_tol=1e-12, 64-eigenvalue window",
-                   "N": n, "n_v": nv, "r": r, "band_half_width": bw, "l2": "factors > L2 (no flush needed)",
+                   "N": n, "n_v": nv, "r": r, "ordering": "nested dissection (leaf 256), block-sparse 32x32 tiles",
+                   "factor_tiles_per_pole": sp["offdiag_tiles"] + sp["block_rows"],
+                   "l2": "factors > L2 (no flush needed)",
                    "parallelism": f"columns x{ws} (weak)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * nv * esize,
                 "d2h_bytes_per_step": n * nv * esize},
         "gpu_launches": int(kernel_launches),
-        "roofline": {"bound": "tensor", "kernel": "trsm_kernel (pipelined block-band solve, DMMA f64)",
+        "roofline": {"bound": "tensor", "kernel": "dag_kernel (DAG-scheduled block-sparse sweeps, DMMA f64)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if peak else None, "traffic": traffic,
                      "peak_source": "measured FP64 tensor pipe (tools/fp64_peak.cu mma.sync.m8n8k4.f64, "
                                     "profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no FP64 figure)",
-                     "algorithmic": "8 flops per complex MAC x (nnz(L)+nnz(U)) of the band per column per pole "
-                                    "per G application",
+                     "algorithmic": "8 flops per complex MAC x stored factor entries (off-diagonal L and U "
+                                    "tiles + diagonal-block inverses, 1024 per tile) per column per pole per "
+                                    "solve per G application",
                      "trsm_share_of_step": trsm_ms / total_ms if total_ms else None,
                      "trsm_launches": trsm_launches},
         "clocks": clk,

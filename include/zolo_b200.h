@@ -194,6 +194,14 @@ void zolo_set_error(zolo_ctx* ctx, const char* msg);
  * ms[6..7] reserved. ms must hold 8 doubles. */
 int zolo_last_timings(const zolo_ctx* ctx, double* ms);
 
+/* Structure the triangular sweeps run over (per pole, after zolo_factorize):
+ * out[0] block rows (32-row tiles), out[1] off-diagonal tiles of L (= of U),
+ * out[2] / out[3] forward / backward DAG task records (0 for the band layout),
+ * out[4] chunk partial-sum slots, out[5] critical path in block rows,
+ * out[6] layout: 0 = block-sparse (ND), 1 = block band (RCM), out[7] reserved.
+ * No equivalent in the reference (development / roofline accounting). */
+int zolo_sweep_profile(const zolo_ctx* ctx, int64_t* out);
+
 /* Device timer on the context stream: op 0 records the start event, op 1
  * records the stop event, waits for it and returns the elapsed ms. */
 int zolo_timer(zolo_ctx* ctx, int op, double* ms);

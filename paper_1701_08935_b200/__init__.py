@@ -134,6 +134,7 @@ def lib():
         L.zolo_rr_project.argtypes = [P, P, I64, P, P]
         L.zolo_block_update.argtypes = [P, P, I64, P, I64, P]
         L.zolo_last_timings.argtypes = [P, P]
+        L.zolo_sweep_profile.argtypes = [P, P]
         L.zolo_timer.argtypes = [P, C.c_int, P]
         L.zolo_rcm.argtypes = [I64, P, P, P, P, P]
         L.zolo_random_block.argtypes = [C.c_int, I64, I64, C.c_uint64, C.c_int, P]
@@ -247,7 +248,7 @@ class FilterOperator:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and lib is not None:  # (module globals may be gone at exit)
             lib().zolo_ctx_destroy(h)
             self._h = None
 
@@ -342,6 +343,14 @@ class FilterOperator:
         lib().zolo_last_timings(self._h, _ptr(ms))
         return dict(filter_ms=ms[0], factor_ms=ms[1], trsm_ms=ms[2], trsm_launches=int(ms[3]),
                     kernel_launches=int(ms[4]), operator_applications=int(ms[5]))
+
+    def sweep_profile(self):
+        """Structure the triangular sweeps run over (zolo_sweep_profile)."""
+        out = np.zeros(8, dtype=np.int64)
+        _check(self._h, lib().zolo_sweep_profile(self._h, _ptr(out)))
+        return dict(block_rows=int(out[0]), offdiag_tiles=int(out[1]), fwd_tasks=int(out[2]),
+                    bwd_tasks=int(out[3]), chunk_slots=int(out[4]), critical_path=int(out[5]),
+                    layout="band" if out[6] == 1 else "block-sparse")
 
     def timer_start(self):
         _check(self._h, lib().zolo_timer(self._h, 0, None))

@@ -135,6 +135,7 @@ struct zolo_ctx {
   DevMem vin_orig, vin, vout, w, bbuf, chains_fwd, chains_bwd, flags, counter;
   std::vector<std::unique_ptr<DevMem>> xbuf, cbuf;
   DevMem dl_d, trace_buf;
+  DevMem host_in, host_out;  // staging of the host-buffer entry points
   int64_t env_tiles = 0;
   bool trace_done = false;
 
@@ -1372,13 +1373,12 @@ int zolo_apply_filter(zolo_ctx* c, const double* v, double* y, int64_t ncols, do
     require(ncols >= 1, "apply_filter: empty block");
     require(c->factored, "apply_filter: operator not factorized");
     const size_t bytes = c->es() * c->n * ncols;
-    DevMem dv, dy;
-    dv.ensure(bytes);
-    dy.ensure(bytes);
-    CK(cudaMemcpyAsync(dv.p, v, bytes, cudaMemcpyHostToDevice, c->st));
-    code = c->cx ? apply_filter_impl<cd>(*c, dv.p, dy.p, ncols, gmres_tol, gmres_max, rep)
-                 : apply_filter_impl<double>(*c, dv.p, dy.p, ncols, gmres_tol, gmres_max, rep);
-    CK(cudaMemcpyAsync(y, dy.p, bytes, cudaMemcpyDeviceToHost, c->st));
+    c->host_in.ensure(bytes);  // grow-only staging: no per-call cudaMalloc / cudaFree
+    c->host_out.ensure(bytes);
+    CK(cudaMemcpyAsync(c->host_in.p, v, bytes, cudaMemcpyHostToDevice, c->st));
+    code = c->cx ? apply_filter_impl<cd>(*c, c->host_in.p, c->host_out.p, ncols, gmres_tol, gmres_max, rep)
+                 : apply_filter_impl<double>(*c, c->host_in.p, c->host_out.p, ncols, gmres_tol, gmres_max, rep);
+    CK(cudaMemcpyAsync(y, c->host_out.p, bytes, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
   });
   return st != ZOLO_OK ? st : code;
@@ -1431,6 +1431,25 @@ int zolo_timer(zolo_ctx* c, int op, double* ms) {
 
 int zolo_last_timings(const zolo_ctx* c, double* ms) {
   for (int i = 0; i < 8; ++i) ms[i] = c->last_ms[i];
+  return ZOLO_OK;
+}
+
+int zolo_sweep_profile(const zolo_ctx* c, int64_t* out) {
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  if (!c->factored) return ZOLO_ERR_DOMAIN;
+  out[0] = c->geom.nbk;
+  if (c->sparse) {
+    out[1] = c->sgeom.ntiles;
+    out[2] = c->sched_fwd.ntask;
+    out[3] = c->sched_bwd.ntask;
+    out[4] = c->sp_nslots;
+    out[5] = c->critical_path;
+    out[6] = 0;
+  } else {
+    out[1] = c->env_tiles;
+    out[5] = c->geom.nbk;
+    out[6] = 1;
+  }
   return ZOLO_OK;
 }
 
