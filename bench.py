@@ -15,9 +15,12 @@ factors, DAG-scheduled DMMA sweeps) + B SpMM. The r factorizations are setup
   value : device-resident block, CUDA events on the library stream, K steps.
   e2e   : the public host API (zolo_apply_filter) from pinned host memory,
           H2D of V and D2H of Y inside the timed region.
-Multi-GPU (torchrun): columns are independent (one Krylov basis per column,
-filter_engine.hpp:109-111), so every rank filters its own n_v-column block
-with no data-path collective -- weak scaling; value = N * n_v / max-rank time.
+Multi-GPU (torchrun), --shard columns (default): columns are independent (one
+Krylov basis per column, filter_engine.hpp:109-111), so every rank filters its
+own n_v-column block with no data-path collective -- weak scaling;
+value = N * n_v / max-rank time. --shard poles: rank g factors poles
+g, g + N, ... and every G application is all-reduced over NCCL inside the
+library; all ranks filter the same block -- strong scaling, value = n_v / time.
 --impl reference: the reference's own CPU FilterOperator (oracle/_ref,
 compiled from /root/reference) on the host cores, bounded column sample.
 """
@@ -175,6 +178,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="columns", choices=["columns", "poles"])
     args = ap.parse_args()
     ws, rank, local = dist_info()
 
@@ -195,12 +199,18 @@ def main():
     pen, cx, gaps, r, nv, nl = workload(args.config)
     n = int(pen[0])
     design = build_filter_design(gaps, r)
-    op = zb.FilterOperator(pen, design, r, is_complex=cx, device=local)
+    poles = args.shard == "poles" and ws > 1
+    if poles:
+        from paper_1701_08935_b200.sharding import pole_sharded_operator
+
+        op = pole_sharded_operator(pen, design, r, cx, local)
+    else:
+        op = zb.FilterOperator(pen, design, r, is_complex=cx, device=local)
     t_factor_ms = op.last_timings()["factor_ms"]
     sp = op.sweep_profile()
 
     # each rank: its own n_v-column block (columns are independent units)
-    v = zb.random_block(n, nv, 1 + rank, cx=cx, orthonormalize=True)
+    v = zb.random_block(n, nv, 1 if poles else 1 + rank, cx=cx, orthonormalize=True)
     dt = torch.complex128 if cx else torch.float64
     dv = torch.from_numpy(np.ascontiguousarray(v.T)).to(device=f"cuda:{local}", dtype=dt)  # (nv, n) = column-major
     dy = torch.empty_like(dv)
@@ -239,7 +249,8 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = ws * nv / (ms_per_step / 1e3)
+    units = nv if poles else ws * nv
+    value = units / (ms_per_step / 1e3)
 
     # e2e: public host API, pinned host buffers, H2D + D2H inside the timed region
     dtn = np.complex128 if cx else np.float64
@@ -268,7 +279,7 @@ def main():
         t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = ws * nv / (e2e_ms / args.steps / 1e3)
+    e2e_value = units / (e2e_ms / args.steps / 1e3)
     esize = 16 if cx else 8
     assert np.isfinite(yh).all()
 
@@ -279,7 +290,7 @@ def main():
     # products = 2 (ntiles + nb) complex 32x32 tile-column products of 8 * 1024 flops
     chains_per_pole = 2 if cx else 1
     tile_products = 2 * (sp["offdiag_tiles"] + sp["block_rows"])
-    trsm_flops = opapps * r * chains_per_pole * tile_products * 8.0 * 1024  # all launches of the K steps
+    trsm_flops = opapps * len(op.poles) * chains_per_pole * tile_products * 8.0 * 1024  # this rank, K steps
     achieved = trsm_flops / (trsm_ms * 1e-3) / 1e12 if trsm_ms > 0 else 0.0
     peak = peaks.get("fp64_tflops")
     traffic = None
@@ -289,14 +300,16 @@ def main():
         pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if poles else "weak",
+        "vs_baseline": None,
         "dtype": "c128" if cx else "f64", "data": "synthetic (seeded generator, BASELINE config shape)",
         "config": {"workload": f"{args.config}: 3D 7-point Laplacian 32^3 + U[0,1] potential, SPD mass B, N={n}, "
                                f"r={r} (p={2 * r} poles), n_v={nv}, gmres_tol=1e-12, 64-eigenvalue window",
                    "N": n, "n_v": nv, "r": r, "ordering": "nested dissection (leaf 256), block-sparse 32x32 tiles",
                    "factor_tiles_per_pole": sp["offdiag_tiles"] + sp["block_rows"],
                    "l2": "factors > L2 (no flush needed)",
-                   "parallelism": f"columns x{ws} (weak)"},
+                   "parallelism": f"poles x{ws} (NCCL all-reduce per G application)" if poles
+                   else f"columns x{ws} (weak)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * nv * esize,
                 "d2h_bytes_per_step": n * nv * esize},
         "gpu_launches": int(kernel_launches),

@@ -122,6 +122,21 @@ int zolo_factorize(zolo_ctx* ctx, const int64_t* perm, zolo_factor_stats* stats)
 enum { ZOLO_ORDER_ND = 0, ZOLO_ORDER_RCM = 1 };
 int zolo_set_ordering(zolo_ctx* ctx, int mode, int64_t nd_leaf);
 
+/* Pole sharding over NCCL (no reference equivalent -- the
+ * reference sums all poles in one process, filter_engine.hpp:63-69,73-78).
+ * Rank g of nranks factors the poles j = g, g + nranks, ... (< r; needs
+ * r >= nranks) and every G application ends with one in-place
+ * ncclAllReduce(sum) of the ranks' partial sums, so all ranks hold identical
+ * G v and run an identical (replicated) Krylov iteration; rank 0 adds the
+ * constant term. unique_id: ZOLO_NCCL_ID_BYTES bytes from zolo_nccl_unique_id
+ * on rank 0, broadcast by the caller; all ranks call collectively, before
+ * zolo_factorize. unique_id = NULL with nranks > 1 gives an unreduced context:
+ * zolo_apply_g returns the rank's partial sum, zolo_apply_filter refuses.
+ * NCCL is loaded with dlopen (libnccl.so.2) only when a communicator is built. */
+#define ZOLO_NCCL_ID_BYTES 128
+int zolo_nccl_unique_id(void* out);
+int zolo_set_pole_shard(zolo_ctx* ctx, int rank, int nranks, const void* unique_id);
+
 /* FilterOperator(pencil, design): upload + set_design + factorize. */
 int zolo_filter_create(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
                        const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v,

@@ -126,6 +126,8 @@ def lib():
         L.zolo_pencil_upload.argtypes = [P, I64, C.c_int, P, P, P, P, P, P]
         L.zolo_set_design.argtypes = [P, P, C.c_int]
         L.zolo_set_ordering.argtypes = [P, C.c_int, I64]
+        L.zolo_set_pole_shard.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
+        L.zolo_nccl_unique_id.argtypes = [C.c_char_p]
         L.zolo_factorize.argtypes = [P, P, P]
         L.zolo_apply_g.argtypes = [P, P, P, I64]
         L.zolo_apply_filter.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
@@ -143,6 +145,22 @@ def lib():
         L.zolo_eval_filter.argtypes = [P, C.c_int, I64, P, P, P]
         _lib = L
     return _lib
+
+
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0), to broadcast to the pole-shard ranks."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    if lib().zolo_nccl_unique_id(buf) != ZOLO_OK:
+        raise CudaError(lib().zolo_last_error(None).decode())
+    return buf.raw
+
+
+def shard_poles(r: int, rank: int, nranks: int):
+    """Poles a pole-shard rank factors (zolo_set_pole_shard): j = rank, rank + nranks, ..."""
+    return list(range(rank, r, nranks))
 
 
 def _ptr(a):
@@ -212,10 +230,14 @@ class FilterOperator:
     FilterDesign of ``include/zolo_b200.h`` (e.g. from
     :func:`paper_1701_08935_b200.design.build_filter_design`); ``r`` its order.
     ``is_complex`` selects S = complex128 (Hermitian pencil) vs float64.
+    ``shard=(rank, nranks, unique_id)`` makes this operator one pole shard of a
+    multi-GPU operator (zolo_set_pole_shard): it factors the poles
+    :func:`shard_poles` gives and all-reduces every G application over NCCL;
+    ``unique_id=None`` leaves G unreduced (``apply_g`` returns the partial sum).
     """
 
     def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None,
-                 ordering: str = "nd", nd_leaf: int = 256):
+                 ordering: str = "nd", nd_leaf: int = 256, shard=None):
         L = lib()
         n, a, b = pencil
         cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
@@ -238,6 +260,11 @@ class FilterOperator:
         if ordering not in ORDERINGS:
             raise DomainError(f"ordering must be one of {sorted(ORDERINGS)}")
         _check(h, L.zolo_set_ordering(h, ORDERINGS[ordering], int(nd_leaf)))
+        self.shard = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
+        if shard is not None:
+            uid = shard[2] if len(shard) > 2 else None
+            _check(h, L.zolo_set_pole_shard(h, self.shard[0], self.shard[1], uid))
+        self.poles = shard_poles(self.r, *self.shard)
         self.stats = (FactorStats * self.r)()
         perm_arr = None if perm is None else np.ascontiguousarray(perm, dtype=np.int64)
         st = L.zolo_factorize(h, _ptr(perm_arr), self.stats)
@@ -362,4 +389,4 @@ class FilterOperator:
 
     def factor_profile(self):
         return [dict(bandwidth=s.bandwidth, stored_entries=s.stored_entries, min_pivot_ratio=s.min_pivot_ratio)
-                for s in self.stats]
+                for s in list(self.stats)[:len(self.poles)]]

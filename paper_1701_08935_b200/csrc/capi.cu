@@ -28,6 +28,7 @@
 #include "band.cuh"
 #include "host.hpp"
 #include "krylov.cuh"
+#include "shard.hpp"
 
 namespace zolo {
 void gmres_init(cudaStream_t st, GmresDev g);
@@ -167,8 +168,16 @@ struct zolo_ctx {
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
 
+  // pole sharding: this context factors the poles own[] of the design
+  int shard_rank = 0, shard_size = 1;
+  std::vector<int> own;
+  NcclComm* comm = nullptr;
+  DevMem wc;  // compacted partial G (all-reduced over the ranks)
+
   size_t es() const { return cx ? 16 : 8; }
-  int nchains() const { return cx ? 2 * r : r; }
+  int nloc() const { return static_cast<int>(own.size()); }
+  int nchains() const { return cx ? 2 * nloc() : nloc(); }
+  double local_constant() const { return shard_rank == 0 ? constant_term : 0.0; }
 };
 
 namespace {
@@ -367,8 +376,8 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     upload_device_pencil(c, inv, pos);
   }
 
-  // tiles for r poles
-  const int r = c.r;
+  // tiles for the context's poles
+  const int r = c.nloc();
   const size_t per_array = g.tiles_per_array() * TT;
   const size_t per_diag = static_cast<size_t>(g.nbk) * TT;
   const size_t per_pole = 2 * per_array + 2 * per_diag;  // complex entries
@@ -414,7 +423,7 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     cudaStream_t ps = c.pole_streams[j];
     double* rn = c.rownorm_mem.as<double>() + g.npad * j;
     factor_scatter(ps, g, c.tiles[j], nnz, er_d.as<int>(), ec_d.as<int>(), ea_d.as<double>(), eb_d.as<double>(),
-                   c.cx, poles[2 * j], poles[2 * j + 1], rn);
+                   c.cx, poles[2 * c.own[j]], poles[2 * c.own[j] + 1], rn);
     FactorDevState ds;
     ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
     ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
@@ -566,8 +575,8 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
   upload(c.sp_pad_rows, pads, c.st);
   upload_device_pencil(c, bs.inv, pos);
 
-  // factors for r poles: Dt, DinvL, DinvU (nb tiles each), Lt, Ut (ntiles each)
-  const int r = c.r;
+  // factors for the context's poles: Dt, DinvL, DinvU (nb tiles each), Lt, Ut (ntiles each)
+  const int r = c.nloc();
   const size_t per_diag = static_cast<size_t>(nb) * TT;
   const size_t per_off = static_cast<size_t>(bs.ntiles) * TT;
   const size_t per_pole = 3 * per_diag + 2 * per_off;
@@ -623,7 +632,7 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
     ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
     ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
     sp_factor(c.pole_streams[j], s, c.sp_col_cnt, f, nnz, er_d.as<int>(), ec_d.as<int>(), ea_d.as<double>(),
-              eb_d.as<double>(), c.cx, poles[2 * j], poles[2 * j + 1], c.rownorm_mem.as<double>() + bs.npad * j,
+              eb_d.as<double>(), c.cx, poles[2 * c.own[j]], poles[2 * c.own[j] + 1], c.rownorm_mem.as<double>() + bs.npad * j,
               c.sp_pad_rows.as<int>(), static_cast<int>(pads.size()), ds, c.sp_err.as<int>());
     CK(cudaGetLastError());
     CK(cudaEventRecord(c.ev2, c.pole_streams[j]));
@@ -659,6 +668,17 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
     throw ZoloError(ZOLO_ERR_FACTORIZATION, "factorize: pivot " + std::to_string(fail_any) + " below threshold");
 }
 
+// poles of this context (j = rank, rank + nranks, ... < r) and their weights, local order
+void refresh_own(zolo_ctx& c) {
+  c.own.clear();
+  for (int j = c.shard_rank; j < c.r; j += c.shard_size) c.own.push_back(j);
+  std::vector<cd> w(std::max<size_t>(c.own.size(), 1), mk(0.0, 0.0));
+  for (size_t k = 0; k < c.own.size(); ++k) w[k] = mk(c.eff_w[c.own[k]].real(), c.eff_w[c.own[k]].imag());
+  upload(c.weights_d, w, c.st);
+  c.factored = false;
+  c.ncap = 0;
+}
+
 void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   const int64_t ld = c.geom.npad;
   const size_t es = c.es();
@@ -679,7 +699,7 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
     c.cbuf[i]->ensure(sizeof(cd) * crows * nc);
   }
   std::vector<Chain> fwd(nch), bwd(nch);
-  for (int p = 0; p < c.r; ++p) {
+  for (int p = 0; p < c.nloc(); ++p) {
     const FactorTiles& t = c.tiles[p];
     const cd* b = c.bbuf.as<cd>();
     if (c.cx) {
@@ -725,6 +745,33 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   CK(cudaMallocHost(&c.done_h, sizeof(int) * nc));
   c.ncap = nc;
   c.maxit_cap = 0;  // GMRES state is sized per (ncap, maxit)
+}
+
+// w[:, act] = (rank 0: constant v) + the context's poles' terms; pole-sharded:
+// computed compacted, all-reduced over the ranks (one ncclAllReduce per G
+// application), then scattered -- every rank ends with the
+// same bits, so the replicated Arnoldi stays identical across ranks. Without a
+// communicator (nranks > 1, no unique id) the rank's partial sum is returned.
+void combine_g(zolo_ctx& c, const void* vsrc, const int* act, int na, std::vector<cd*>& xs, void* wdst) {
+  const int64_t ld = c.geom.npad, n = ld;
+  const bool sharded = c.shard_size > 1;
+  void* out = wdst;
+  if (sharded) {
+    c.wc.ensure(c.es() * ld * std::max(na, 1));
+    out = c.wc.p;
+  }
+  if (c.cx)
+    Krylov<cd>::combine(c.st, n, ld, c.local_constant(), reinterpret_cast<const cd*>(vsrc), act, na, xs.data(),
+                        c.weights_d.as<cd>(), c.nloc(), reinterpret_cast<cd*>(out), sharded);
+  else
+    Krylov<double>::combine(c.st, n, ld, c.local_constant(), reinterpret_cast<const double*>(vsrc), act, na,
+                            xs.data(), c.weights_d.as<cd>(), c.nloc(), reinterpret_cast<double*>(out), sharded);
+  if (!sharded) return;
+  if (c.comm) nccl_allreduce_sum(c.comm, c.wc.as<double>(), static_cast<size_t>(ld) * na * (c.es() / 8), c.st);
+  if (c.cx)
+    Krylov<cd>::scatter_cols(c.st, ld, c.wc.as<cd>(), act, na, reinterpret_cast<cd*>(wdst));
+  else
+    Krylov<double>::scatter_cols(c.st, ld, c.wc.as<double>(), act, na, reinterpret_cast<double*>(wdst));
 }
 
 // G applied to the columns act[0..na) of vsrc (ld x ncap, S) -> w[:, act].
@@ -773,16 +820,11 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
     dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>(), nch, na, ld, fc, cf, ++c.epoch,
                     c.counter.as<int>() + 1, 0, c.num_sms);
     if (c.cx)
-      for (int p = 0; p < c.r; ++p)
+      for (int p = 0; p < c.nloc(); ++p)
         blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
     CK(cudaEventRecord(c.ev3, c.st));
     CK(cudaGetLastError());
-    if (c.cx)
-      Krylov<cd>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const cd*>(vsrc), act, na, xs.data(),
-                          c.weights_d.as<cd>(), c.r, reinterpret_cast<cd*>(wdst));
-    else
-      Krylov<double>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const double*>(vsrc), act, na,
-                              xs.data(), c.weights_d.as<cd>(), c.r, reinterpret_cast<double*>(wdst));
+    combine_g(c, vsrc, act, na, xs, wdst);
     CK(cudaGetLastError());
     return 0.0f;
   }
@@ -812,19 +854,14 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   const int g2 = trsm_launch(c.st, c.geom, c.chains_bwd.as<Chain>(), nch, na, ld, fx, fc, ++c.epoch,
                              c.counter.as<int>() + 1, 0, c.num_sms);
   if (c.cx)
-    for (int p = 0; p < c.r; ++p) blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
+    for (int p = 0; p < c.nloc(); ++p) blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
   if (g1 < 0 || g2 < 0)
     throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: " + std::to_string(nch) + " chains x " +
                                          std::to_string((na + CG - 1) / CG) +
                                          " column groups exceed the resident CTA budget");
   CK(cudaEventRecord(c.ev3, c.st));
   CK(cudaGetLastError());
-  if (c.cx)
-    Krylov<cd>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const cd*>(vsrc), act, na, xs.data(),
-                        c.weights_d.as<cd>(), c.r, reinterpret_cast<cd*>(wdst));
-  else
-    Krylov<double>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const double*>(vsrc), act, na, xs.data(),
-                            c.weights_d.as<cd>(), c.r, reinterpret_cast<double*>(wdst));
+  combine_g(c, vsrc, act, na, xs, wdst);
   CK(cudaGetLastError());
   return 0.0f;
 }
@@ -895,6 +932,7 @@ template <class S>
 int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
                       zolo_report* rep) {
   require(c.factored, "apply_filter: operator not factorized");
+  require(c.shard_size == 1 || c.comm, "apply_filter: a pole-sharded context needs its NCCL communicator");
   require(gmres_max >= 1 && gmres_max <= 64, "apply_filter: gmres_max must be in [1, 64]");
   const int64_t n = c.n, ld = c.geom.npad;
   const int maxit = static_cast<int>(gmres_max);
@@ -1226,6 +1264,7 @@ int zolo_ctx_destroy(zolo_ctx* c) {
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   for (auto s : c->pole_streams) cudaStreamDestroy(s);
+  nccl_close(c->comm);
   if (c->act_h) cudaFreeHost(c->act_h);
   if (c->done_h) cudaFreeHost(c->done_h);
   for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3, c->tev0, c->tev1})
@@ -1311,10 +1350,9 @@ int zolo_set_design(zolo_ctx* c, const double* design, int r) {
       for (size_t b = a + 1; b < c->shifts.size(); ++b)
         require(c->shifts[a] != c->shifts[b], "multishift_gmres: shifts must be distinct");
     c->constant_term = design[ZOLO_DESIGN_CONSTANT];
-    std::vector<cd> w(r), s(2 * r);
-    for (int j = 0; j < r; ++j) w[j] = mk(c->eff_w[j].real(), c->eff_w[j].imag());
+    std::vector<cd> s(2 * r);
     for (int k = 0; k < 2 * r; ++k) s[k] = mk(c->shifts[k].real(), c->shifts[k].imag());
-    upload(c->weights_d, w, c->st);
+    refresh_own(*c);
     upload(c->shifts_d, s, c->st);
     upload(c->coef_d, c->coef, c->st);
     c->have_design = true;
@@ -1332,7 +1370,39 @@ int zolo_set_ordering(zolo_ctx* c, int mode, int64_t nd_leaf) {
 }
 
 int zolo_factorize(zolo_ctx* c, const int64_t* perm, zolo_factor_stats* stats) {
-  return guarded(c, [&] { do_factorize(*c, perm, stats); });
+  return guarded(c, [&] {
+    require(c->have_design, "zolo_factorize: no design set");
+    require(c->nloc() >= 1, "zolo_factorize: pole shard owns no pole (need r >= nranks)");
+    do_factorize(*c, perm, stats);
+  });
+}
+
+int zolo_nccl_unique_id(void* out) {
+  try {
+    nccl_unique_id(out);
+    return ZOLO_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_CUDA;
+  }
+}
+
+int zolo_set_pole_shard(zolo_ctx* c, int rank, int nranks, const void* unique_id) {
+  return guarded(c, [&] {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "zolo_set_pole_shard: need 0 <= rank < nranks");
+    nccl_close(c->comm);
+    c->comm = nullptr;
+    c->shard_rank = rank;
+    c->shard_size = nranks;
+    if (nranks > 1 && unique_id) {
+      try {
+        c->comm = nccl_open(unique_id, nranks, rank);
+      } catch (const std::exception& e) {
+        throw ZoloError(ZOLO_ERR_CUDA, e.what());
+      }
+    }
+    if (c->have_design) refresh_own(*c);
+  });
 }
 
 int zolo_filter_create(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,

@@ -124,7 +124,7 @@ struct XPtrs {
 // filter_engine.hpp:60-80
 template <class S>
 __global__ void combine_kernel(int64_t ld, double c0, const S* v, const int* act, XPtrs xs, const cd* weights, int r,
-                               S* w) {
+                               S* w, int compact) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int a = blockIdx.y;
   if (t >= ld) return;
@@ -144,7 +144,15 @@ __global__ void combine_kernel(int64_t ld, double c0, const S* v, const int* act
       acc = cadd(acc, cadd(cmul(wp, x), cmul(cconj(wp), xa)));
     }
   }
-  w[t + col * ld] = acc;
+  w[t + (compact ? a : col) * ld] = acc;
+}
+
+// w[:, act[a]] = wc[:, a] (pole-sharded G: the all-reduced compacted partial sums)
+template <class S>
+__global__ void scatter_cols_kernel(int64_t ld, const S* wc, const int* act, S* w) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int a = blockIdx.y;
+  if (t < ld) w[t + act[a] * ld] = wc[t + a * ld];
 }
 
 // ---- CGS2 Arnoldi -------------------------------------------------------
@@ -523,11 +531,16 @@ void Krylov<S>::apply_b(cudaStream_t st, int64_t n, int64_t ld, const int* rp, c
 }
 template <class S>
 void Krylov<S>::combine(cudaStream_t st, int64_t n, int64_t ld, double c0, const S* v, const int* act, int na,
-                        cd* const* xs, const cd* weights, int r, S* w) {
+                        cd* const* xs, const cd* weights, int r, S* w, bool compact) {
   XPtrs p;
   const int np = sizeof(S) == sizeof(double) ? r : 2 * r;
   for (int i = 0; i < np; ++i) p.p[i] = xs[i];
-  if (na > 0) combine_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, c0, v, act, p, weights, r, w);
+  if (na > 0)
+    combine_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, c0, v, act, p, weights, r, w, compact);
+}
+template <class S>
+void Krylov<S>::scatter_cols(cudaStream_t st, int64_t ld, const S* wc, const int* act, int na, S* w) {
+  if (na > 0) scatter_cols_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, wc, act, w);
 }
 template <class S>
 void Krylov<S>::arnoldi(cudaStream_t st, int64_t n, int64_t ld, S* const* d_basis, int m, S* w, const int* act,

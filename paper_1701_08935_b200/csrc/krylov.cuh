@@ -39,9 +39,12 @@ struct Krylov {
   // out (complex, ld x na) = B * V[:, act] (or V[:, act] when B = I)
   static void apply_b(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals,
                       const S* v, const int* act, int na, cd* out);
-  // w[:, act[a]] = c0 v[:, act[a]] + sum_p (real: 2 Re(w_p X_p) | complex: w_p X_p + conj(w_p) Xa_p)
+  // w[:, act[a]] = c0 v[:, act[a]] + sum_p (real: 2 Re(w_p X_p) | complex: w_p X_p + conj(w_p) Xa_p);
+  // compact: written to w[:, a] instead
   static void combine(cudaStream_t st, int64_t n, int64_t ld, double c0, const S* v, const int* act, int na,
-                      cd* const* xs, const cd* weights, int r, S* w);
+                      cd* const* xs, const cd* weights, int r, S* w, bool compact = false);
+  // w[:, act[a]] = wc[:, a]
+  static void scatter_cols(cudaStream_t st, int64_t ld, const S* wc, const int* act, int na, S* w);
   // CGS2 Arnoldi step against basis V_0..V_m (device pointer array)
   static void arnoldi(cudaStream_t st, int64_t n, int64_t ld, S* const* d_basis, int m, S* w, const int* act,
                       int na, GmresDev g, double* partial, int nchunk, S* hsave);
