@@ -225,6 +225,10 @@ int zolo_timer(zolo_ctx* ctx, int op, double* ms);
 /* reorder_rcm (rcm.hpp:69-115) of a structurally symmetric pattern;
  * perm[new] = old. bw/profile (rcm.hpp:118-147) may be NULL. */
 int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int64_t* bw, int64_t* profile);
+/* The nested-dissection ordering of ZOLO_ORDER_ND (no reference equivalent):
+ * pos[i] = padded device position of row i (tree nodes padded to 32-row
+ * tiles), *npad = padded size. */
+int zolo_nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* pos, int64_t* npad);
 
 /* random_gaussian<S> (dense.hpp:181-208, raw mt19937_64 bits + Box-Muller),
  * optionally followed by mgs_orthonormalize (dense.hpp:212-229). */

@@ -47,6 +47,11 @@ struct FactorTiles {
   cd* Ut = nullptr;
   cd* DinvL = nullptr;
   cd* DinvU = nullptr;
+  // block-sparse path: occupancy masks of each array (tile_masks); nullptr for the band
+  uint2* mLt = nullptr;
+  uint2* mUt = nullptr;
+  uint2* mDL = nullptr;
+  uint2* mDU = nullptr;
 };
 
 __host__ __device__ inline size_t lt_off(int i, int d, int J) {
@@ -68,6 +73,8 @@ enum SweepMode : int {
 struct Chain {
   const cd* off;   // row-scaled Lt or Ut array of the pole
   const cd* pre;   // DinvL / DinvU applied to b_i first, or nullptr (identity)
+  const uint2* offm;  // occupancy masks of off (block-sparse path; nullptr = dense)
+  const uint2* prem;  // occupancy masks of pre
   const cd* src;   // right-hand side (ld x ncols), read once per block row
   cd* dst;         // solution (ld x ncols), written in place
   cd* cbuf;        // helper -> owner partial solutions c_i (ld x ncols)
@@ -115,6 +122,10 @@ struct SpFactor {
 void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt, const SpFactor& f, int64_t nnz,
                const int* e_row, const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
                double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err);
+
+// masks[t] = occupancy of tile t: bit (8 g + kb) of .x for rows 8g.. x cols 4kb..
+// (op N), of .y for the conjugate transpose (factor.cu tile_mask_kernel).
+void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks);
 
 // DAG-scheduled sweeps over block-sparse row-scaled tiles: the claim-ordered
 // schedule (host.hpp dag_schedule, nsched entries) expanded over (chain,

@@ -148,7 +148,7 @@ struct zolo_ctx {
   std::vector<int> sp_col_cnt;
   int64_t critical_path = 0;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
-  DevMem sp_sched_fwd, sp_sched_bwd;
+  DevMem sp_sched_fwd, sp_sched_bwd, sp_masks;
   DagSched sched_fwd, sched_bwd;
   int sp_nslots = 0;
   std::vector<cd*> sp_dt;
@@ -603,6 +603,15 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
     c.tiles[j].Lt = p + 3 * per_diag;
     c.tiles[j].Ut = p + 3 * per_diag + per_off;
   }
+  const size_t mper = 2 * static_cast<size_t>(nb) + 2 * static_cast<size_t>(bs.ntiles);
+  c.sp_masks.ensure(sizeof(uint2) * mper * r);
+  for (int j = 0; j < r; ++j) {
+    uint2* m = c.sp_masks.as<uint2>() + mper * j;
+    c.tiles[j].mDL = m;
+    c.tiles[j].mDU = m + nb;
+    c.tiles[j].mLt = m + 2 * nb;
+    c.tiles[j].mUt = m + 2 * nb + bs.ntiles;
+  }
   std::vector<unsigned long long> fs(2 * r);
   const double inf = std::numeric_limits<double>::infinity();
   unsigned long long infbits;
@@ -634,6 +643,10 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
     sp_factor(c.pole_streams[j], s, c.sp_col_cnt, f, nnz, er_d.as<int>(), ec_d.as<int>(), ea_d.as<double>(),
               eb_d.as<double>(), c.cx, poles[2 * c.own[j]], poles[2 * c.own[j] + 1], c.rownorm_mem.as<double>() + bs.npad * j,
               c.sp_pad_rows.as<int>(), static_cast<int>(pads.size()), ds, c.sp_err.as<int>());
+    tile_masks(c.pole_streams[j], c.tiles[j].DinvL, nb, c.tiles[j].mDL);
+    tile_masks(c.pole_streams[j], c.tiles[j].DinvU, nb, c.tiles[j].mDU);
+    tile_masks(c.pole_streams[j], c.tiles[j].Lt, bs.ntiles, c.tiles[j].mLt);
+    tile_masks(c.pole_streams[j], c.tiles[j].Ut, bs.ntiles, c.tiles[j].mUt);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c.ev2, c.pole_streams[j]));
     CK(cudaStreamWaitEvent(c.st, c.ev2, 0));
@@ -710,15 +723,15 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
       // solve:   y = DinvL b - L~ y ;  x = DinvU y - U~ x
       // adjoint: z = b - U~^H z (z_i = U_ii^H y_i) ; w = DinvU^H z - L~^H w (w_i = L_ii^H x_i),
       //          then x_i = DinvL_i^H w_i (blockdiag post-pass)
-      fwd[2 * p] = Chain{t.Lt, t.DinvL, b, x, cb, FWD_L, 0};
-      bwd[2 * p] = Chain{t.Ut, t.DinvU, x, x, cb, BWD_U, 0};
-      fwd[2 * p + 1] = Chain{t.Ut, nullptr, b, xa, cba, FWD_UH, 0};
-      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, xa, xa, cba, BWD_LH, 0};
+      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
+      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
+      fwd[2 * p + 1] = Chain{t.Ut, nullptr, t.mUt, nullptr, b, xa, cba, FWD_UH, 0};
+      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, t.mLt, t.mDU, xa, xa, cba, BWD_LH, 0};
     } else {
       cd* x = c.xbuf[p]->as<cd>();
       cd* cb = c.cbuf[p]->as<cd>();
-      fwd[p] = Chain{t.Lt, t.DinvL, b, x, cb, FWD_L, 0};
-      bwd[p] = Chain{t.Ut, t.DinvU, x, x, cb, BWD_U, 0};
+      fwd[p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
+      bwd[p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
     }
   }
   upload(c.chains_fwd, fwd, c.st);
@@ -796,15 +809,15 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
     unsigned long long* dtr = nullptr;
     const size_t ntask = static_cast<size_t>(c.sched_fwd.ntask) * nch * dag_groups(na);
     if (dag_trace && !c.trace_done) {
-      c.trace_buf.ensure(sizeof(unsigned long long) * 4 * ntask);
-      CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 4 * ntask, c.st));
+      c.trace_buf.ensure(sizeof(unsigned long long) * 6 * ntask);
+      CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 6 * ntask, c.st));
       dtr = c.trace_buf.as<unsigned long long>();
     }
     int* cf = fc + c.cflags_off;
     dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>(), nch, na, ld, fc, cf, ++c.epoch,
                     c.counter.as<int>(), 1, c.num_sms, dtr);
     if (dtr) {
-      std::vector<unsigned long long> h(4 * ntask);
+      std::vector<unsigned long long> h(6 * ntask);
       CK(cudaMemcpyAsync(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
       CK(cudaStreamSynchronize(c.st));
       if (FILE* fh = std::fopen(dag_trace, "w")) {
@@ -812,7 +825,8 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
                      dag_groups(na), static_cast<long long>(c.critical_path), c.sched_fwd.ntask,
                      c.sched_fwd.nslots);
         for (size_t q = 0; q < ntask; ++q)
-          std::fprintf(fh, "%llu %llu %llu %llu\n", h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+          std::fprintf(fh, "%llu %llu %llu %llu %llu %llu\n", h[6 * q], h[6 * q + 1], h[6 * q + 2], h[6 * q + 3],
+                       h[6 * q + 4], h[6 * q + 5]);
         std::fclose(fh);
       }
       c.trace_done = true;
@@ -1521,6 +1535,21 @@ int zolo_sweep_profile(const zolo_ctx* c, int64_t* out) {
     out[6] = 1;
   }
   return ZOLO_OK;
+}
+
+int zolo_nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* pos, int64_t* npad) {
+  try {
+    std::vector<std::vector<int64_t>> nodes;
+    nd_order(n, rp, ci, leaf, nodes);
+    BlockStructure bs;
+    block_symbolic(n, rp, ci, nodes, TILE, bs);
+    for (int64_t i = 0; i < n; ++i) pos[i] = bs.pos[i];
+    if (npad) *npad = bs.npad;
+    return ZOLO_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_DOMAIN;
+  }
 }
 
 int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int64_t* bw, int64_t* profile) {

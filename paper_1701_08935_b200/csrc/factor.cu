@@ -433,6 +433,35 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt
   if (s.ntiles > 0) scale_sp_kernel<<<dim3(static_cast<unsigned>(s.ntiles), 2), FT, 0, st>>>(s, f.Lt, f.Ut, f.DinvL, f.DinvU);
 }
 
+// Per-tile occupancy masks for the sweeps' DMMA loops: bit (8 g + kb) of
+// .x is set when rows 8g..8g+7 x columns 4kb..4kb+3 of the tile (op N) hold a
+// nonzero, .y the same for the conjugate transpose (rows 4kb.. x columns 8g..).
+// Exact zeros inside a tile are the structural zeros of the elimination.
+__global__ void __launch_bounds__(256) tile_mask_kernel(const cd* tiles, uint2* masks) {
+  __shared__ unsigned mn, mh;
+  const size_t t = blockIdx.x;
+  if (threadIdx.x == 0) mn = mh = 0u;
+  __syncthreads();
+  const cd* T = tiles + t * TT;
+  unsigned bn = 0, bh = 0;
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+    const int col = e / TILE, row = e % TILE;
+    const cd v = T[e];
+    if (v.x != 0.0 || v.y != 0.0) {
+      bn |= 1u << ((row / 8) * 8 + col / 4);
+      bh |= 1u << ((col / 8) * 8 + row / 4);
+    }
+  }
+  if (bn) atomicOr(&mn, bn);
+  if (bh) atomicOr(&mh, bh);
+  __syncthreads();
+  if (threadIdx.x == 0) masks[t] = make_uint2(mn, mh);
+}
+
+void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks) {
+  if (ntiles > 0) tile_mask_kernel<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(tiles, masks);
+}
+
 void factor_scatter(cudaStream_t st, const BandGeom& g, const FactorTiles& f, int64_t nnz, const int* e_row,
                     const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
                     double sig_im, double* row_norm) {

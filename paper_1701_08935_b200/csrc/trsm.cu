@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "band.cuh"
 
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
 constexpr int DCG = 32;                  // columns per DAG task
 constexpr int XS2 = DCG * XPAD;          // padded 32 x 32 x block
 constexpr int DNS = 3;                   // pipeline stages
+constexpr int DAG_TRACE_WORDS = 6;       // start, loop end, done, info, wait ns, first tile ready
 constexpr int TSW = TT;                  // swizzled (unpadded) tile
 constexpr int DAG_SMEM_FIXED = DNS * (TSW + XS2) * static_cast<int>(sizeof(cd));
 
@@ -448,7 +450,8 @@ struct DagArgs {
   int* flags;    // per (chain, 32-column group, block): epoch when u_i is final
   int* cflags;   // per (chain, 32-column group, slot): epoch when the partial sum is written
   int* counter;  // [0] task counter, [2] wait-timeout error word
-  unsigned long long* trace;  // optional: per task (claim, dependencies done, done, smid|chunk|deps)
+  unsigned long long* trace;  // optional: per task (start, dependencies done, done, smid<<48|chunk<<47|i<<16|deps)
+  int hints;                  // L2 eviction-priority hints on (development switch ZOLO_DAG_HINTS)
 };
 
 // Swizzled tile layout: element (row, col) of a 32 x 32 tile at
@@ -459,12 +462,12 @@ struct DagArgs {
 // the tile needs no padding.
 __device__ __forceinline__ int swz(int c) { return ((c & 1) << 2) | (c & 2); }
 
-__device__ __forceinline__ void load_tile_sw(cd* s, const cd* g) {
+__device__ __forceinline__ void load_tile_sw(cd* s, const cd* g, unsigned long long pol) {
 #pragma unroll
   for (int q = 0; q < TT / ST; ++q) {
     const int e = threadIdx.x + q * ST;
     const int col = e / TILE, row = e % TILE;
-    cp_async16_cg(&s[col * TILE + (row ^ swz(col))], g + e);
+    cp_async16_cg_hint(&s[col * TILE + (row ^ swz(col))], g + e, pol);
   }
 }
 
@@ -500,8 +503,11 @@ __device__ __forceinline__ void acc8_fold(const Acc8& a, cd out[4]) {
       out[2 * h + e] = mk(a.v[h][0][0][e] + a.v[h][1][0][e], a.v[h][0][1][e] + a.v[h][1][1][e]);
 }
 
+// km: the k-steps (4-column groups of op(T)) holding nonzeros in this warp's
+// 8 rows (tile_mask_kernel); zero k-steps and all-zero row groups are skipped.
 template <bool OPH, bool NEG>
-__device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* xs, const Frag& f) {
+__device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* xs, const Frag& f, unsigned km) {
+  if (km == 0) return;
   const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
   const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
   const int sa = swz(ar);
@@ -516,6 +522,7 @@ __device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* x
   }
 #pragma unroll
   for (int kb = 0; kb < TILE / 4; ++kb) {
+    if (!((km >> kb) & 1u)) continue;
     const int p = kb & 1;
     // op N: re += ax bx - ay by, im += ax by + ay bx; op H (conj a): re += ax bx + ay by, im += ax by - ay bx
     const double ny = OPH ? a[kb].y : -a[kb].y;
@@ -532,28 +539,29 @@ __device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* x
 }
 
 // acc += op(T) X, or -= with neg (the pre-transform entry)
-__device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs, bool opH, bool neg, const Frag& f) {
+__device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs, bool opH, bool neg, const Frag& f,
+                                          unsigned km) {
   if (opH) {
     if (neg)
-      mma_tile2_t<true, true>(acc, ts, xs, f);
+      mma_tile2_t<true, true>(acc, ts, xs, f, km);
     else
-      mma_tile2_t<true, false>(acc, ts, xs, f);
+      mma_tile2_t<true, false>(acc, ts, xs, f, km);
   } else {
     if (neg)
-      mma_tile2_t<false, true>(acc, ts, xs, f);
+      mma_tile2_t<false, true>(acc, ts, xs, f, km);
     else
-      mma_tile2_t<false, false>(acc, ts, xs, f);
+      mma_tile2_t<false, false>(acc, ts, xs, f, km);
   }
 }
 
 // 32 rows x 32 columns of a column-major block into [col*XPAD + row].
-__device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int c0, int nc) {
+__device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int c0, int nc, unsigned long long pol) {
   const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < DCG / 8; ++q) {
     const int c = cc + 8 * q;
     if (c < nc)
-      cp_async16_cg(&xs[c * XPAD + row], base + row + (c0 + c) * ld);
+      cp_async16_cg_hint(&xs[c * XPAD + row], base + row + (c0 + c) * ld, pol);
     else
       xs[c * XPAD + row] = mk(0.0, 0.0);
   }
@@ -588,7 +596,7 @@ __device__ __forceinline__ void wait_flags_par(const int* f, int cnt, int epoch,
 // (prefetched by the previous task); `nrec` is where this task prefetches the
 // record of `next` (the CTA's next claimed task) once its first barrier passed.
 __device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* smem, int* rdy_s, int* nrec,
-                         int next_rec, unsigned long long* trc) {
+                         int next_rec, unsigned long long* trc, uint2* mask_s) {
   auto tile_s = [smem](int k) { return smem + k * (TSW + XS2); };
   auto x_s = [smem](int k) { return smem + k * (TSW + XS2) + TSW; };
   const Chain ch = A.chains[ci];
@@ -604,6 +612,44 @@ __device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* s
   int* cflags = A.cflags + cgi * A.nslots;
   const int hp = (!chunk && ch.pre) ? 1 : 0;  // entry 0 = pre-transform
   const int ne = hp + nd;
+  // factor tiles and right-hand sides stream through L2 once per column group;
+  // the solution blocks u_j are re-read by every later block row that depends on them
+  const unsigned long long pol_stream = (A.hints & 1) ? l2_evict_first() : l2_evict_normal();
+  const unsigned long long pol_keep = (A.hints & 2) ? l2_evict_last() : l2_evict_normal();
+  // tile + occupancy mask of entry e (and the right-hand side for the pre entry): no producer involved
+  auto issue_tile = [&](int e) {
+    const int buf = e % DNS;
+    const uint2* mk_src;
+    if (e < hp) {
+      load_tile_sw(tile_s(buf), ch.pre + static_cast<size_t>(i) * TT, pol_stream);
+      load_x32(x_s(buf), ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc, pol_stream);
+      mk_src = ch.prem ? ch.prem + i : nullptr;
+    } else {
+      const int q = e - hp;
+      load_tile_sw(tile_s(buf), ch.off + static_cast<size_t>(dq[2 * q + 1]) * TT, pol_stream);
+      mk_src = ch.offm ? ch.offm + dq[2 * q + 1] : nullptr;
+    }
+    if (threadIdx.x == 0) {
+      if (mk_src)
+        cp_async8_ca(mask_s + buf, mk_src);
+      else
+        mask_s[buf] = make_uint2(0xffffffffu, 0xffffffffu);
+    }
+  };
+  // u_j of a dependency entry, when its producer had finished at task start
+  auto issue_x = [&](int e) {
+    if (e < hp) return;
+    const int q = e - hp;
+    if (rdy_s[q]) load_x32(x_s(e % DNS), ch.dst + static_cast<int64_t>(dq[2 * q]) * TILE, ld, c0, nc, pol_keep);
+  };
+  auto issue = [&](int e) {
+    issue_tile(e);
+    issue_x(e);
+  };
+  // prologue: the first tiles load while the dependency flags are read
+#pragma unroll
+  for (int e = 0; e < DNS - 1; ++e)
+    if (e < ne) issue_tile(e);
   for (int q = threadIdx.x; q < nd; q += ST) rdy_s[q] = ld_acquire(flags + dq[2 * q]) >= A.epoch;
   cd bval[4];
 #pragma unroll
@@ -616,27 +662,19 @@ __device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* s
   if (next_rec >= 0 && threadIdx.x < DAG_REC * 4 / 16)  // prefetch the next task's record
     cp_async16_cg(nrec + 4 * threadIdx.x, A.recs + static_cast<size_t>(next_rec) * DAG_REC + 4 * threadIdx.x);
   auto ready = [&](int e) { return e < hp || rdy_s[e - hp]; };
-  auto issue = [&](int e) {
-    const int buf = e % DNS;
-    if (e < hp) {
-      load_tile_sw(tile_s(buf), ch.pre + static_cast<size_t>(i) * TT);
-      load_x32(x_s(buf), ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc);
-    } else {
-      const int q = e - hp;
-      load_tile_sw(tile_s(buf), ch.off + static_cast<size_t>(dq[2 * q + 1]) * TT);
-      if (rdy_s[q]) load_x32(x_s(buf), ch.dst + static_cast<int64_t>(dq[2 * q]) * TILE, ld, c0, nc);
-    }
-  };
 #pragma unroll
   for (int e = 0; e < DNS - 1; ++e) {
-    if (e < ne) issue(e);
+    if (e < ne) issue_x(e);
     cp_async_commit();
   }
   Acc8 acc8;
   acc8_zero(acc8);
   cd acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};  // chunk partials
+  unsigned long long wsum = 0, tw = 0;  // (trace) time spent waiting on producers
   if (pc > 0) {  // partial sums of the older dependencies, while the first tiles load
+    if (trc) tw = gtimer();
     wait_flags_par(cflags + pa, pc, A.epoch, A.counter + 2);
+    if (trc) wsum += gtimer() - tw;
     const cd* prow = ch.cbuf + static_cast<int64_t>(pa) * TILE + f.row + c0 * A.ldp;
     for (int p = 0; p < pc; ++p) {
       cd v[4];
@@ -655,16 +693,20 @@ __device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* s
       cp_async_wait<DNS - 2>();
     } else {  // still running at task start: wait for it now, then fetch its u
       const int j = dq[2 * (e - hp)];
+      if (trc) tw = gtimer();
       wait_flag(flags + j, A.epoch, A.counter + 2);
-      load_x32(x_s(buf), ch.dst + static_cast<int64_t>(j) * TILE, ld, c0, nc);
+      if (trc) wsum += gtimer() - tw;
+      load_x32(x_s(buf), ch.dst + static_cast<int64_t>(j) * TILE, ld, c0, nc, pol_keep);
       cp_async_commit();
       cp_async_wait<0>();
     }
     // one barrier per tile: entry e visible to all warps, entry e-1 finished
     __syncthreads();
+    if (trc && e == 0 && threadIdx.x == 0) trc[5] = gtimer();
     if (e + DNS - 1 < ne) issue(e + DNS - 1);
     cp_async_commit();
-    mma_tile2(acc8, tile_s(buf), x_s(buf), opH, e < hp, f);
+    const uint2 mw = mask_s[buf];
+    mma_tile2(acc8, tile_s(buf), x_s(buf), opH, e < hp, f, ((opH ? mw.y : mw.x) >> f.r0) & 0xffu);
   }
   cp_async_wait<0>();
   if (trc && threadIdx.x == 0) trc[1] = gtimer();
@@ -696,7 +738,9 @@ __device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* s
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       trc[2] = gtimer();
-      trc[3] = (static_cast<unsigned long long>(smid) << 32) | (chunk ? 0x80000000u : 0u) | static_cast<unsigned>(nd);
+      trc[4] = wsum;
+      trc[3] = (static_cast<unsigned long long>(smid) << 48) | (static_cast<unsigned long long>(chunk) << 47) |
+               (static_cast<unsigned long long>(i) << 16) | static_cast<unsigned>(nd);
     }
   }
 }
@@ -710,6 +754,7 @@ __global__ void __launch_bounds__(ST, 2) dag_kernel(DagArgs A) {
   int* recb = reinterpret_cast<int*>(smem_raw + DAG_SMEM_FIXED);  // 2 x DAG_REC
   int* rdy_s = recb + 2 * DAG_REC;
   __shared__ int cur_s, next_s;
+  __shared__ uint2 mask_s[DNS];
   const int per_step = A.nchains * A.ngroups;
   const int ntasks = A.ntask * per_step;
   if (threadIdx.x == 0) cur_s = atomicAdd(A.counter, 1);
@@ -721,14 +766,14 @@ __global__ void __launch_bounds__(ST, 2) dag_kernel(DagArgs A) {
   cp_async_wait<0>();
   __syncthreads();
   while (t < ntasks) {
-    unsigned long long* trc = A.trace ? A.trace + 4 * static_cast<size_t>(t) : nullptr;
+    unsigned long long* trc = A.trace ? A.trace + DAG_TRACE_WORDS * static_cast<size_t>(t) : nullptr;
     if (trc && threadIdx.x == 0) trc[0] = gtimer();
     if (threadIdx.x == 0) next_s = atomicAdd(A.counter, 1);
     __syncthreads();
     const int tn = next_s;
     const int rem = t % per_step;
     dag_task(A, recb + b * DAG_REC, rem / A.ngroups, rem % A.ngroups, smem, rdy_s, recb + (b ^ 1) * DAG_REC,
-             tn < ntasks ? tn / per_step : -1, trc);
+             tn < ntasks ? tn / per_step : -1, trc, mask_s);
     __syncthreads();  // (dag_task ends with cp.async.wait_all: the next record has landed)
     t = tn;
     b ^= 1;
@@ -788,6 +833,11 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   a.cflags = cflags;
   a.counter = counter;
   a.trace = trace;
+  static const int hints = [] {
+    const char* v = std::getenv("ZOLO_DAG_HINTS");
+    return v ? std::atoi(v) : 3;
+  }();
+  a.hints = hints;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int ntasks = sched.ntask * nchains * a.ngroups;
   int per_sm = 0;
