@@ -122,6 +122,18 @@ int zolo_factorize(zolo_ctx* ctx, const int64_t* perm, zolo_factor_stats* stats)
 enum { ZOLO_ORDER_ND = 0, ZOLO_ORDER_RCM = 1 };
 int zolo_set_ordering(zolo_ctx* ctx, int mode, int64_t nd_leaf);
 
+/* Sylvester inertia (the reference takes eigenvalue
+ * counts as inputs): *count = the number of eigenvalues of the
+ * pencil (A, B), B Hermitian positive definite, below the real shift sigma,
+ * from the signs of the pivots of the unpivoted block LU = L D L^H of
+ * A - sigma B under the ND ordering (Sylvester's law of inertia). The count in
+ * (a, b) is count(b) - count(a). A pivot under the monitor threshold
+ * (|piv| <= 1e-14 ||row||, sigma within rounding of an eigenvalue, or an
+ * unpivoted breakdown) returns ZOLO_ERR_FACTORIZATION: retry at a nudged shift.
+ * Uses temporary factor storage; the filter factors are untouched.
+ * min_pivot_ratio may be NULL. */
+int zolo_count_below(zolo_ctx* ctx, double sigma, int64_t* count, double* min_pivot_ratio);
+
 /* Pole sharding over NCCL (no reference equivalent -- the
  * reference sums all poles in one process, filter_engine.hpp:63-69,73-78).
  * Rank g of nranks factors the poles j = g, g + nranks, ... (< r; needs

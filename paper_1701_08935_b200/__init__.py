@@ -128,6 +128,7 @@ def lib():
         L.zolo_set_ordering.argtypes = [P, C.c_int, I64]
         L.zolo_set_pole_shard.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
         L.zolo_nccl_unique_id.argtypes = [C.c_char_p]
+        L.zolo_count_below.argtypes = [P, D, P, P]
         L.zolo_factorize.argtypes = [P, P, P]
         L.zolo_apply_g.argtypes = [P, P, P, I64]
         L.zolo_apply_filter.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
@@ -220,6 +221,53 @@ def _csr(m, cx):
     ci = np.ascontiguousarray(m[1], dtype=np.int64)
     v = np.ascontiguousarray(m[2], dtype=np.complex128 if cx else np.float64)
     return rp, ci, v
+
+
+class InertiaCounter:
+    """Eigenvalue counts of the pencil (A, B) by Sylvester inertia on the GPU
+    (zolo_count_below): the unpivoted block LU of
+    A - sigma B under the ND ordering has as many negative pivots as the pencil
+    has eigenvalues below sigma (B positive definite)."""
+
+    def __init__(self, pencil, is_complex: Optional[bool] = None, device: int = 0, nd_leaf: int = 256):
+        L = lib()
+        n, a, b = pencil
+        cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
+        self.n, self.cx = int(n), cx
+        h = C.c_void_p()
+        if L.zolo_ctx_create(device, C.byref(h)) != ZOLO_OK:
+            raise CudaError(L.zolo_last_error(None).decode())
+        self._h = h
+        self._a = _csr(a, cx)
+        self._b = _csr(b, cx) if b is not None else None
+        bp = self._b if self._b is not None else (None, None, None)
+        _check(h, L.zolo_pencil_upload(h, self.n, int(cx), *map(_ptr, self._a), *map(_ptr, bp)))
+        _check(h, L.zolo_set_ordering(h, ORDERINGS["nd"], int(nd_leaf)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and lib is not None:
+            lib().zolo_ctx_destroy(h)
+            self._h = None
+
+    def count_below(self, sigma: float, nudges: int = 3) -> int:
+        """Eigenvalues < sigma. A shift within rounding of an eigenvalue (rejected
+        pivot) is nudged by 1e-12 relative, up to `nudges` times."""
+        out = np.zeros(1, dtype=np.int64)
+        ratio = np.zeros(1)
+        s = float(sigma)
+        for k in range(nudges + 1):
+            st = lib().zolo_count_below(self._h, C.c_double(s), _ptr(out), _ptr(ratio))
+            if st != ZOLO_ERR_FACTORIZATION:
+                _check(self._h, st)
+                self.last_min_pivot_ratio = float(ratio[0])
+                return int(out[0])
+            s = float(sigma) + (k + 1) * 1e-12 * max(1.0, abs(float(sigma)))
+        _check(self._h, st)
+
+    def count_in(self, a: float, b: float) -> int:
+        """Eigenvalues in (a, b) = count_below(b) - count_below(a)."""
+        return self.count_below(b) - self.count_below(a)
 
 
 class FilterOperator:

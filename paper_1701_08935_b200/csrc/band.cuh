@@ -126,6 +126,8 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt
 // masks[t] = occupancy of tile t: bit (8 g + kb) of .x for rows 8g.. x cols 4kb..
 // (op N), of .y for the conjugate transpose (factor.cu tile_mask_kernel).
 void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks);
+// number of pivots (diagonal of the packed diagonal-tile LUs) with negative real part
+int64_t count_negative_pivots(cudaStream_t st, const cd* dt, int nb);
 
 // DAG-scheduled sweeps over block-sparse row-scaled tiles: the claim-ordered
 // schedule (host.hpp dag_schedule, nsched entries) expanded over (chain,

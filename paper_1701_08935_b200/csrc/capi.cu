@@ -149,6 +149,10 @@ struct zolo_ctx {
   int64_t critical_path = 0;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
   DevMem sp_sched_fwd, sp_sched_bwd, sp_masks;
+  DevMem sp_er, sp_ec, sp_ea, sp_eb;  // scatter lists of the union pattern in the factor ordering
+  int64_t sp_nnz = 0;
+  int sp_npads = 0;
+  bool sym_ready = false;
   DagSched sched_fwd, sched_bwd;
   int sp_nslots = 0;
   std::vector<cd*> sp_dt;
@@ -310,6 +314,7 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     return;
   }
   c.sparse = false;
+  c.sym_ready = false;
   const int64_t n = c.n;
   Union u = union_pattern(c);
   c.perm.resize(n);
@@ -459,7 +464,9 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
                     "factorize: pivot " + std::to_string(fail_any) + " below threshold");
 }
 
-void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats) {
+// Ordering + block symbolic analysis + sweep schedules + the device pencil and
+// scatter lists in the factor ordering: everything shift-independent.
+void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   const int64_t n = c.n;
   Union u = union_pattern(c);
   std::vector<std::vector<int64_t>> nodes;
@@ -567,50 +574,63 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
     }
   for (int64_t t = 0; t < bs.npad; ++t)
     if (bs.inv[t] < 0) pads.push_back(static_cast<int>(t));
-  DevMem er_d, ec_d, ea_d, eb_d;
-  upload(er_d, er, c.st);
-  upload(ec_d, ec, c.st);
-  upload(ea_d, u.av, c.st);
-  upload(eb_d, u.bv, c.st);
+  upload(c.sp_er, er, c.st);
+  upload(c.sp_ec, ec, c.st);
+  upload(c.sp_ea, u.av, c.st);
+  upload(c.sp_eb, u.bv, c.st);
   upload(c.sp_pad_rows, pads, c.st);
+  c.sp_nnz = nnz;
+  c.sp_npads = static_cast<int>(pads.size());
   upload_device_pencil(c, bs.inv, pos);
+  c.sym_ready = true;
+}
 
-  // factors for the context's poles: Dt, DinvL, DinvU (nb tiles each), Lt, Ut (ntiles each)
-  const int r = c.nloc();
+// Numeric block-sparse LU of A - sigma_k B for each shift into `store`
+// (Dt, DinvL, DinvU: nb tiles; Lt, Ut: ntiles), one stream per shift;
+// masks (tile_masks) when `mstore` is given. fail[k] / min_ratio[k] per shift.
+void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, DevMem& store, DevMem* mstore,
+                    std::vector<FactorTiles>& tiles, std::vector<cd*>& dt, std::vector<int>& fail,
+                    std::vector<double>& min_ratio, size_t* per_pole_out) {
+  const int nb = c.sgeom.nb;
+  const int64_t ntiles = c.sgeom.ntiles;
+  const int r = static_cast<int>(sig.size());
   const size_t per_diag = static_cast<size_t>(nb) * TT;
-  const size_t per_off = static_cast<size_t>(bs.ntiles) * TT;
+  const size_t per_off = static_cast<size_t>(ntiles) * TT;
   const size_t per_pole = 3 * per_diag + 2 * per_off;
+  if (per_pole_out) *per_pole_out = per_pole;
   size_t free_b = 0, total_b = 0;
-  c.tiles_mem.release();
+  store.release();
   CK(cudaMemGetInfo(&free_b, &total_b));
   const size_t need = per_pole * r * sizeof(cd);
   if (need + (size_t(1) << 30) > free_b)
     throw ZoloError(ZOLO_ERR_DOMAIN, "zolo_factorize: factors need " + std::to_string(need >> 20) +
                                          " MiB, device has " + std::to_string(free_b >> 20) + " MiB free");
-  c.tiles_mem.ensure(need);
-  c.rownorm_mem.ensure(sizeof(double) * bs.npad * r);
+  store.ensure(need);
+  c.rownorm_mem.ensure(sizeof(double) * c.sgeom.npad * r);
   c.fstate_mem.ensure(sizeof(unsigned long long) * 2 * r);
   c.sp_err.ensure(sizeof(int) * 4);
   CK(cudaMemsetAsync(c.sp_err.p, 0, sizeof(int) * 4, c.st));
-  c.tiles.assign(r, FactorTiles());
-  c.sp_dt.assign(r, nullptr);
-  cd* base = c.tiles_mem.as<cd>();
+  tiles.assign(r, FactorTiles());
+  dt.assign(r, nullptr);
+  cd* base = store.as<cd>();
   for (int j = 0; j < r; ++j) {
     cd* p = base + per_pole * j;
-    c.sp_dt[j] = p;
-    c.tiles[j].DinvL = p + per_diag;
-    c.tiles[j].DinvU = p + 2 * per_diag;
-    c.tiles[j].Lt = p + 3 * per_diag;
-    c.tiles[j].Ut = p + 3 * per_diag + per_off;
+    dt[j] = p;
+    tiles[j].DinvL = p + per_diag;
+    tiles[j].DinvU = p + 2 * per_diag;
+    tiles[j].Lt = p + 3 * per_diag;
+    tiles[j].Ut = p + 3 * per_diag + per_off;
   }
-  const size_t mper = 2 * static_cast<size_t>(nb) + 2 * static_cast<size_t>(bs.ntiles);
-  c.sp_masks.ensure(sizeof(uint2) * mper * r);
-  for (int j = 0; j < r; ++j) {
-    uint2* m = c.sp_masks.as<uint2>() + mper * j;
-    c.tiles[j].mDL = m;
-    c.tiles[j].mDU = m + nb;
-    c.tiles[j].mLt = m + 2 * nb;
-    c.tiles[j].mUt = m + 2 * nb + bs.ntiles;
+  if (mstore) {
+    const size_t mper = 2 * static_cast<size_t>(nb) + 2 * static_cast<size_t>(ntiles);
+    mstore->ensure(sizeof(uint2) * mper * r);
+    for (int j = 0; j < r; ++j) {
+      uint2* m = mstore->as<uint2>() + mper * j;
+      tiles[j].mDL = m;
+      tiles[j].mDU = m + nb;
+      tiles[j].mLt = m + 2 * nb;
+      tiles[j].mUt = m + 2 * nb + ntiles;
+    }
   }
   std::vector<unsigned long long> fs(2 * r);
   const double inf = std::numeric_limits<double>::infinity();
@@ -629,24 +649,26 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
   CK(cudaStreamSynchronize(c.st));
   CK(cudaEventRecord(c.ev0, c.st));
   for (int j = 0; j < r; ++j) CK(cudaStreamWaitEvent(c.pole_streams[j], c.ev0, 0));
-  const double* poles = c.design.data() + ZOLO_DESIGN_HEAD;
   for (int j = 0; j < r; ++j) {
     SpFactor f;
-    f.Dt = c.sp_dt[j];
-    f.Lt = c.tiles[j].Lt;
-    f.Ut = c.tiles[j].Ut;
-    f.DinvL = c.tiles[j].DinvL;
-    f.DinvU = c.tiles[j].DinvU;
+    f.Dt = dt[j];
+    f.Lt = tiles[j].Lt;
+    f.Ut = tiles[j].Ut;
+    f.DinvL = tiles[j].DinvL;
+    f.DinvU = tiles[j].DinvU;
     FactorDevState ds;
     ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
     ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
-    sp_factor(c.pole_streams[j], s, c.sp_col_cnt, f, nnz, er_d.as<int>(), ec_d.as<int>(), ea_d.as<double>(),
-              eb_d.as<double>(), c.cx, poles[2 * c.own[j]], poles[2 * c.own[j] + 1], c.rownorm_mem.as<double>() + bs.npad * j,
-              c.sp_pad_rows.as<int>(), static_cast<int>(pads.size()), ds, c.sp_err.as<int>());
-    tile_masks(c.pole_streams[j], c.tiles[j].DinvL, nb, c.tiles[j].mDL);
-    tile_masks(c.pole_streams[j], c.tiles[j].DinvU, nb, c.tiles[j].mDU);
-    tile_masks(c.pole_streams[j], c.tiles[j].Lt, bs.ntiles, c.tiles[j].mLt);
-    tile_masks(c.pole_streams[j], c.tiles[j].Ut, bs.ntiles, c.tiles[j].mUt);
+    sp_factor(c.pole_streams[j], c.sgeom, c.sp_col_cnt, f, c.sp_nnz, c.sp_er.as<int>(), c.sp_ec.as<int>(),
+              c.sp_ea.as<double>(), c.sp_eb.as<double>(), c.cx, sig[j].real(), sig[j].imag(),
+              c.rownorm_mem.as<double>() + c.sgeom.npad * j, c.sp_pad_rows.as<int>(), c.sp_npads, ds,
+              c.sp_err.as<int>());
+    if (mstore) {
+      tile_masks(c.pole_streams[j], tiles[j].DinvL, nb, tiles[j].mDL);
+      tile_masks(c.pole_streams[j], tiles[j].DinvU, nb, tiles[j].mDU);
+      tile_masks(c.pole_streams[j], tiles[j].Lt, ntiles, tiles[j].mLt);
+      tile_masks(c.pole_streams[j], tiles[j].Ut, ntiles, tiles[j].mUt);
+    }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c.ev2, c.pole_streams[j]));
     CK(cudaStreamWaitEvent(c.st, c.ev2, 0));
@@ -661,18 +683,32 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
   CK(cudaMemcpy(&serr, c.sp_err.p, sizeof(int), cudaMemcpyDeviceToHost));
   if (serr) throw ZoloError(ZOLO_ERR_NUMERICAL, "zolo_factorize: symbolic structure does not cover the fill");
   CK(cudaMemcpy(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost));
-  int fail_any = -1;
+  fail.assign(r, -1);
+  min_ratio.assign(r, 0.0);
   for (int j = 0; j < r; ++j) {
-    const int fi = static_cast<int>(static_cast<uint32_t>(fs[2 * j] & 0xffffffffull));
-    double mr;
-    std::memcpy(&mr, &fs[2 * j + 1], 8);
+    fail[j] = static_cast<int>(static_cast<uint32_t>(fs[2 * j] & 0xffffffffull));
+    std::memcpy(&min_ratio[j], &fs[2 * j + 1], 8);
+  }
+}
+
+void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats) {
+  sparse_symbolic(c, perm_in);
+  const double* poles = c.design.data() + ZOLO_DESIGN_HEAD;
+  std::vector<std::complex<double>> sig;
+  for (int j : c.own) sig.emplace_back(poles[2 * j], poles[2 * j + 1]);
+  std::vector<int> fail;
+  std::vector<double> mr;
+  size_t per_pole = 0;
+  sparse_numeric(c, sig, c.tiles_mem, &c.sp_masks, c.tiles, c.sp_dt, fail, mr, &per_pole);
+  int fail_any = -1;
+  for (size_t j = 0; j < sig.size(); ++j) {
     if (stats) {
       stats[j].bandwidth = -1;
       stats[j].stored_entries = static_cast<int64_t>(per_pole);
-      stats[j].min_pivot_ratio = mr;
-      stats[j].pivot_index = fi;
+      stats[j].min_pivot_ratio = mr[j];
+      stats[j].pivot_index = fail[j];
     }
-    if (fi >= 0 && fail_any < 0) fail_any = fi;
+    if (fail[j] >= 0 && fail_any < 0) fail_any = fail[j];
   }
   c.sparse = true;
   c.factored = fail_any < 0;
@@ -1333,6 +1369,7 @@ int zolo_pencil_upload(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, 
     }
     c->have_pencil = true;
     c->have_perm = false;
+    c->sym_ready = false;
     c->factored = false;
     c->ncap = 0;
   });
@@ -1388,6 +1425,26 @@ int zolo_factorize(zolo_ctx* c, const int64_t* perm, zolo_factor_stats* stats) {
     require(c->have_design, "zolo_factorize: no design set");
     require(c->nloc() >= 1, "zolo_factorize: pole shard owns no pole (need r >= nranks)");
     do_factorize(*c, perm, stats);
+  });
+}
+
+int zolo_count_below(zolo_ctx* c, double sigma, int64_t* count, double* min_pivot_ratio) {
+  return guarded(c, [&] {
+    require(c->have_pencil, "zolo_count_below: no pencil uploaded");
+    require(c->order_mode == ZOLO_ORDER_ND, "zolo_count_below: needs the ND (block-sparse) ordering");
+    require(std::isfinite(sigma), "zolo_count_below: sigma must be finite");
+    if (!c->sym_ready) sparse_symbolic(*c, nullptr);
+    DevMem store;
+    std::vector<FactorTiles> tiles;
+    std::vector<cd*> dt;
+    std::vector<int> fail;
+    std::vector<double> mr;
+    sparse_numeric(*c, {std::complex<double>(sigma, 0.0)}, store, nullptr, tiles, dt, fail, mr, nullptr);
+    if (min_pivot_ratio) *min_pivot_ratio = mr[0];
+    if (fail[0] >= 0)
+      throw ZoloError(ZOLO_ERR_FACTORIZATION, "zolo_count_below: pivot " + std::to_string(fail[0]) +
+                                                  " below threshold (sigma too close to an eigenvalue)");
+    *count = count_negative_pivots(c->st, dt[0], c->sgeom.nb);
   });
 }
 

@@ -458,6 +458,32 @@ __global__ void __launch_bounds__(256) tile_mask_kernel(const cd* tiles, uint2* 
   if (threadIdx.x == 0) masks[t] = make_uint2(mn, mh);
 }
 
+// Sylvester inertia: negative real parts among the pivots (diagonal of the
+// packed U_ii of every diagonal tile; identity padding rows have pivot 1).
+__global__ void neg_pivots_kernel(const cd* dt, int nb, unsigned long long* out) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int neg = 0;
+  if (t < static_cast<int64_t>(nb) * TILE) {
+    const int64_t b = t / TILE, k = t % TILE;
+    neg = dt[b * TT + k * TILE + k].x < 0.0;
+  }
+  neg = __reduce_add_sync(0xffffffffu, neg);
+  if ((threadIdx.x & 31) == 0 && neg) atomicAdd(out, static_cast<unsigned long long>(neg));
+}
+
+int64_t count_negative_pivots(cudaStream_t st, const cd* dt, int nb) {
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return -1;
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), st);
+  const int64_t n = static_cast<int64_t>(nb) * TILE;
+  neg_pivots_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(dt, nb, d);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  cudaFree(d);
+  return static_cast<int64_t>(h);
+}
+
 void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks) {
   if (ntiles > 0) tile_mask_kernel<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(tiles, masks);
 }
