@@ -117,6 +117,10 @@ WINDOWS = {
     # eigsh k=140 sigma=6.0 on stencil3d_pencil(32, seed=2): 64 eigenvalues near 6,
     # relative eigengap 2.44e-2 (SURVEY.md §8(d) probe: 2.4e-2, m = 21-22)
     "cfg2": {"gaps": [5.988587801896479, 5.989530607165887, 6.0273252122304335, 6.0282488360560285], "count": 64},
+    # tools/find_window_gpu.py cfg3 0.0 128 (Sylvester-inertia bisection on the B200, rtol 1e-12):
+    # the 128 eigenvalues of tight_binding_pencil(48, seed=3, disorder=1.5) around 0
+    "cfg3": {"gaps": [-0.004303539789179923, -0.004240734865379634, 0.004296055916711339, 0.004322829099328374],
+             "count": 128},
 }
 
 

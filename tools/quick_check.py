@@ -21,6 +21,8 @@ for name in sys.argv[1:] or ["cfg1", "cfg2"]:
     prof = op.factor_profile()[0]
     print(f"{name} [{order}]: N={pen[0]} bw={prof['bandwidth']} factor wall {t1 - t0:.2f}s device {op.last_timings()['factor_ms']:.1f} ms"
           f" min_pivot_ratio {min(p['min_pivot_ratio'] for p in op.factor_profile()):.3e}", flush=True)
+    sp = op.sweep_profile()
+    print(f"  sweep profile: {sp}", flush=True)
     v = zb.random_block(pen[0], nv, 1, cx=cx, orthonormalize=True)
     for rep_i in range(2):
         t0 = time.time()
@@ -30,6 +32,8 @@ for name in sys.argv[1:] or ["cfg1", "cfg2"]:
         print(f"  apply_filter wall {t1 - t0:.3f}s device {tm['filter_ms']:.1f} ms trsm {tm['trsm_ms']:.1f} ms"
               f" ({tm['trsm_launches']} launches) iters {rep.iterations} min_col {min(rep.column_iterations)}"
               f" -> {nv / (tm['filter_ms'] / 1e3):.1f} vec/s", flush=True)
+        flops = tm["operator_applications"] * r * (2 if cx else 1) * 2 * (sp["offdiag_tiles"] + sp["block_rows"]) * 8192.0
+        print(f"  solve: {flops / (tm['trsm_ms'] * 1e-3) / 1e12:.1f} TF/s over stored tiles", flush=True)
     if name == "cfg1" or os.environ.get("CHECK_ORACLE"):
         import oracle
         if oracle.Reference.available():
