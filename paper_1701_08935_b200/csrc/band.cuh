@@ -119,9 +119,22 @@ struct SpFactor {
   cd* DinvU = nullptr;
 };
 
+// device copy of a FactorPlan (host.hpp): level ranges stay on the host
+struct FactorPlanDev {
+  const std::vector<int>* lvl_ptr = nullptr;
+  const std::vector<int>* pan_ptr = nullptr;
+  const std::vector<int>* tgt_ptr = nullptr;
+  const int* cols = nullptr;
+  const int* pan = nullptr;
+  const int* tgt = nullptr;
+  const int* con = nullptr;
+  int simt = 0;  // (debug) SIMT trailing updates
+};
+// plan == nullptr: the column-serial right-looking loop (3 launches per block column)
 void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt, const SpFactor& f, int64_t nnz,
                const int* e_row, const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
-               double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err);
+               double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err,
+               const FactorPlanDev* plan = nullptr);
 
 // masks[t] = occupancy of tile t: bit (8 g + kb) of .x for rows 8g.. x cols 4kb..
 // (op N), of .y for the conjugate transpose (factor.cu tile_mask_kernel).

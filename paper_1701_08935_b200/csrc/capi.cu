@@ -153,6 +153,8 @@ struct zolo_ctx {
   int64_t sp_nnz = 0;
   int sp_npads = 0;
   bool sym_ready = false;
+  FactorPlan fplan;                         // level-scheduled factorization (host level ranges)
+  DevMem fp_cols, fp_pan, fp_tgt, fp_con;   // its device arrays
   DagSched sched_fwd, sched_bwd;
   int sp_nslots = 0;
   std::vector<cd*> sp_dt;
@@ -582,6 +584,11 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   c.sp_nnz = nnz;
   c.sp_npads = static_cast<int>(pads.size());
   upload_device_pencil(c, bs.inv, pos);
+  factor_plan(bs, c.fplan);
+  upload(c.fp_cols, c.fplan.cols, c.st);
+  upload(c.fp_pan, c.fplan.pan, c.st);
+  upload(c.fp_tgt, c.fplan.tgt, c.st);
+  upload(c.fp_con, c.fplan.con, c.st);
   c.sym_ready = true;
 }
 
@@ -646,6 +653,16 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     c.pole_streams.push_back(st);
   }
+  static const int levels = env_int("ZOLO_FACTOR_LEVELS", 1);
+  FactorPlanDev pd;
+  pd.lvl_ptr = &c.fplan.lvl_ptr;
+  pd.pan_ptr = &c.fplan.pan_ptr;
+  pd.tgt_ptr = &c.fplan.tgt_ptr;
+  pd.cols = c.fp_cols.as<int>();
+  pd.pan = c.fp_pan.as<int>();
+  pd.tgt = c.fp_tgt.as<int>();
+  pd.con = c.fp_con.as<int>();
+  pd.simt = levels == 2;
   CK(cudaStreamSynchronize(c.st));
   CK(cudaEventRecord(c.ev0, c.st));
   for (int j = 0; j < r; ++j) CK(cudaStreamWaitEvent(c.pole_streams[j], c.ev0, 0));
@@ -662,7 +679,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     sp_factor(c.pole_streams[j], c.sgeom, c.sp_col_cnt, f, c.sp_nnz, c.sp_er.as<int>(), c.sp_ec.as<int>(),
               c.sp_ea.as<double>(), c.sp_eb.as<double>(), c.cx, sig[j].real(), sig[j].imag(),
               c.rownorm_mem.as<double>() + c.sgeom.npad * j, c.sp_pad_rows.as<int>(), c.sp_npads, ds,
-              c.sp_err.as<int>());
+              c.sp_err.as<int>(), levels ? &pd : nullptr);
     if (mstore) {
       tile_masks(c.pole_streams[j], tiles[j].DinvL, nb, tiles[j].mDL);
       tile_masks(c.pole_streams[j], tiles[j].DinvU, nb, tiles[j].mDU);

@@ -28,6 +28,7 @@
 #include <algorithm>
 
 #include "band.cuh"
+#include "mma.cuh"
 
 namespace zolo {
 
@@ -109,9 +110,9 @@ __global__ void scatter_kernel(BandGeom g, cd* Lt, cd* Ut, int64_t nnz, const in
 // monitor (|pivot| > 1e-14 ||row||_inf, band_factor.hpp:160-166), then the
 // inverses of its unit-lower and upper triangles (threads 0..127: L^{-1},
 // 128..255: U^{-1}; 4 threads per column share each dot product).
-__global__ void __launch_bounds__(FT) diag_factor_kernel(int64_t n, int k, cd* tile, cd* DinvL, cd* DinvU,
-                                                         const double* row_norm, int* fail_index,
-                                                         unsigned long long* min_ratio_bits) {
+__device__ __forceinline__ void diag_factor_body(int64_t n, int k, cd* tile, cd* DinvL, cd* DinvU,
+                                                 const double* row_norm, int* fail_index,
+                                                 unsigned long long* min_ratio_bits) {
   extern __shared__ __align__(16) unsigned char diag_smem[];
   cd* D = reinterpret_cast<cd*>(diag_smem);
   cd* XL = D + TILE * TPAD;
@@ -189,6 +190,12 @@ __global__ void __launch_bounds__(FT) diag_factor_kernel(int64_t n, int k, cd* t
     outL[q] = XL[cc * TPAD + rr];
     outU[q] = XU[cc * TPAD + rr];
   }
+}
+
+__global__ void __launch_bounds__(FT) diag_factor_kernel(int64_t n, int k, cd* tile, cd* DinvL, cd* DinvU,
+                                                         const double* row_norm, int* fail_index,
+                                                         unsigned long long* min_ratio_bits) {
+  diag_factor_body(n, k, tile, DinvL, DinvU, row_norm, fail_index, min_ratio_bits);
 }
 
 // Panel: L(k+d,k) = A(k+d,k) U_kk^{-1} (blocks 0..J-1),
@@ -381,6 +388,100 @@ __global__ void __launch_bounds__(FT) trailing_sp_kernel(SpGeom s, int k, cd* Dt
   store_tile(c, out);
 }
 
+// ---- level-scheduled block LU (host factor_plan) --------------------------
+// all block columns of one level of the block elimination tree at once
+__global__ void __launch_bounds__(FT) diag_level_kernel(const int* cols, int c0, int64_t n, cd* Dt, cd* DinvL,
+                                                        cd* DinvU, const double* row_norm, int* fail_index,
+                                                        unsigned long long* min_ratio_bits) {
+  const int k = cols[c0 + blockIdx.x];
+  diag_factor_body(n, k, Dt + static_cast<size_t>(k) * TT, DinvL, DinvU, row_norm, fail_index, min_ratio_bits);
+}
+
+// panel items (k, 2 id + upper): L(a,k) = A(a,k) U_kk^{-1} | U(k,a) = L_kk^{-1} A(k,a)
+__global__ void __launch_bounds__(FT) panel_level_kernel(const int* pan, int p0, cd* Lt, cd* Ut, const cd* DinvL,
+                                                         const cd* DinvU) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int k = pan[2 * (p0 + blockIdx.x)], code = pan[2 * (p0 + blockIdx.x) + 1];
+  const bool lower = (code & 1) == 0;
+  const int id = code >> 1;
+  cd* c = (lower ? Lt : Ut) + static_cast<size_t>(id) * TT;
+  if (lower) {
+    load_tile_async(As, c);
+    load_tile_async(Bs, DinvU + static_cast<size_t>(k) * TT);
+  } else {
+    load_tile_async(As, DinvL + static_cast<size_t>(k) * TT);
+    load_tile_async(Bs, c);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  cd out[4];
+  tile_mm(As, Bs, out);
+  store_tile(c, out);
+}
+
+// One trailing-update target per CTA: C -= sum_k L(a,k) U(k,b) over its
+// contributions (fixed ascending-k order), on DMMA. (A double-buffered variant
+// of this loop raised "illegal instruction" on the B200 -- tools/dev/trail_unit.cu
+// reproduces it -- so the stages are single-buffered; the factorization is setup.)
+constexpr int TRAIL_SMEM = (TT + XS2) * static_cast<int>(sizeof(cd));
+__global__ void __launch_bounds__(ST, 2) trailing_level_kernel(const int* tgt, const int* con, int t0, cd* Dt,
+                                                               cd* Lt, cd* Ut) {
+  extern __shared__ __align__(16) unsigned char trail_smem[];
+  cd* sm = reinterpret_cast<cd*>(trail_smem);
+  const int* T = tgt + 4 * (t0 + blockIdx.x);
+  const int kind = T[0], id = T[1], cb = T[2], ce = T[3];
+  const unsigned long long pol = l2_evict_normal();
+  const Frag f = frag();
+  Acc8 acc;
+  acc8_zero(acc);
+  for (int q = cb; q < ce; ++q) {
+    load_tile_sw(sm, Lt + static_cast<size_t>(con[2 * q]) * TT, pol);
+    load_x32(sm + TT, Ut + static_cast<size_t>(con[2 * q + 1]) * TT, TILE, 0, TILE, pol);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    mma_tile2(acc, sm, sm + TT, false, false, f, 0xffu);
+    __syncthreads();
+  }
+  cd prod[4];
+  acc8_fold(acc, prod);
+  cd* c = (kind == 0 ? Dt : (kind == 1 ? Lt : Ut)) + static_cast<size_t>(id) * TT;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = ocol(f, q) * TILE + f.row;
+    c[e] = csub(c[e], prod[q]);
+  }
+}
+
+// (debug) SIMT variant of trailing_level_kernel
+__global__ void __launch_bounds__(FT) trailing_level_simt_kernel(const int* tgt, const int* con, int t0, cd* Dt,
+                                                                 cd* Lt, cd* Ut) {
+  __shared__ cd As[TILE * TPAD];
+  __shared__ cd Bs[TILE * TPAD];
+  const int* T = tgt + 4 * (t0 + blockIdx.x);
+  const int kind = T[0], id = T[1], cb = T[2], ce = T[3];
+  cd acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+  for (int q = cb; q < ce; ++q) {
+    load_tile_async(As, Lt + static_cast<size_t>(con[2 * q]) * TT);
+    load_tile_async(Bs, Ut + static_cast<size_t>(con[2 * q + 1]) * TT);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    cd out[4];
+    tile_mm(As, Bs, out);
+    for (int u = 0; u < 4; ++u) acc[u] = cadd(acc[u], out[u]);
+    __syncthreads();
+  }
+  cd* c = (kind == 0 ? Dt : (kind == 1 ? Lt : Ut)) + static_cast<size_t>(id) * TT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  c[ty * TILE + tx] = csub(c[ty * TILE + tx], acc[0]);
+  c[(ty + 16) * TILE + tx] = csub(c[(ty + 16) * TILE + tx], acc[1]);
+  c[ty * TILE + tx + 16] = csub(c[ty * TILE + tx + 16], acc[2]);
+  c[(ty + 16) * TILE + tx + 16] = csub(c[(ty + 16) * TILE + tx + 16], acc[3]);
+}
+
 // Row scaling L~(i,k) = DinvL_i L(i,k), U~(k,i) = DinvU_k U(k,i) (see band path).
 __global__ void __launch_bounds__(FT) scale_sp_kernel(SpGeom s, cd* Lt, cd* Ut, const cd* DinvL, const cd* DinvU) {
   __shared__ cd As[TILE * TPAD];
@@ -403,7 +504,8 @@ __global__ void __launch_bounds__(FT) scale_sp_kernel(SpGeom s, cd* Lt, cd* Ut, 
 
 void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt, const SpFactor& f, int64_t nnz,
                const int* e_row, const int* e_col, const double* a_val, const double* b_val, int cx, double sig_re,
-               double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err) {
+               double sig_im, double* row_norm, const int* pad_rows, int npad_rows, FactorDevState ds, int* err,
+               const FactorPlanDev* plan) {
   cudaMemsetAsync(f.Dt, 0, sizeof(cd) * s.nb * TT, st);
   if (s.ntiles > 0) {
     cudaMemsetAsync(f.Lt, 0, sizeof(cd) * s.ntiles * TT, st);
@@ -421,13 +523,41 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt
     cudaFuncSetAttribute(diag_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem);
     diag_attr = true;
   }
-  for (int k = 0; k < s.nb; ++k) {
-    diag_factor_kernel<<<1, FT, diag_smem, st>>>(s.npad, k, f.Dt + static_cast<size_t>(k) * TT, f.DinvL, f.DinvU,
-                                                 row_norm, ds.fail_index, ds.min_ratio_bits);
-    const int cnt = col_cnt[k];
-    if (cnt > 0) {
-      panel_sp_kernel<<<2 * cnt, FT, 0, st>>>(s, k, f.Lt, f.Ut, f.DinvL, f.DinvU);
-      trailing_sp_kernel<<<dim3(cnt, cnt), FT, 0, st>>>(s, k, f.Dt, f.Lt, f.Ut, err);
+  if (plan) {  // level-scheduled: 3 launches per level of the block elimination tree
+    static bool trail_attr = false;
+    if (!trail_attr) {
+      cudaFuncSetAttribute(diag_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem);
+      cudaFuncSetAttribute(trailing_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRAIL_SMEM);
+      trail_attr = true;
+    }
+    const std::vector<int>& lv = *plan->lvl_ptr;
+    const std::vector<int>& pp = *plan->pan_ptr;
+    const std::vector<int>& tp = *plan->tgt_ptr;
+    for (size_t l = 0; l + 1 < lv.size(); ++l) {
+      if (lv[l + 1] > lv[l])
+        diag_level_kernel<<<lv[l + 1] - lv[l], FT, diag_smem, st>>>(plan->cols, lv[l], s.npad, f.Dt, f.DinvL,
+                                                                     f.DinvU, row_norm, ds.fail_index,
+                                                                     ds.min_ratio_bits);
+      if (pp[l + 1] > pp[l])
+        panel_level_kernel<<<pp[l + 1] - pp[l], FT, 0, st>>>(plan->pan, pp[l], f.Lt, f.Ut, f.DinvL, f.DinvU);
+      if (tp[l + 1] > tp[l]) {
+        if (plan->simt)
+          trailing_level_simt_kernel<<<tp[l + 1] - tp[l], FT, 0, st>>>(plan->tgt, plan->con, tp[l], f.Dt, f.Lt,
+                                                                        f.Ut);
+        else
+          trailing_level_kernel<<<tp[l + 1] - tp[l], ST, TRAIL_SMEM, st>>>(plan->tgt, plan->con, tp[l], f.Dt, f.Lt,
+                                                                            f.Ut);
+      }
+    }
+  } else {
+    for (int k = 0; k < s.nb; ++k) {
+      diag_factor_kernel<<<1, FT, diag_smem, st>>>(s.npad, k, f.Dt + static_cast<size_t>(k) * TT, f.DinvL, f.DinvU,
+                                                   row_norm, ds.fail_index, ds.min_ratio_bits);
+      const int cnt = col_cnt[k];
+      if (cnt > 0) {
+        panel_sp_kernel<<<2 * cnt, FT, 0, st>>>(s, k, f.Lt, f.Ut, f.DinvL, f.DinvU);
+        trailing_sp_kernel<<<dim3(cnt, cnt), FT, 0, st>>>(s, k, f.Dt, f.Lt, f.Ut, err);
+      }
     }
   }
   if (s.ntiles > 0) scale_sp_kernel<<<dim3(static_cast<unsigned>(s.ntiles), 2), FT, 0, st>>>(s, f.Lt, f.Ut, f.DinvL, f.DinvU);

@@ -26,6 +26,20 @@ struct BlockStructure {
 void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std::vector<std::vector<int64_t>>& nodes);
 void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::vector<std::vector<int64_t>>& nodes,
                     int tile, BlockStructure& bs);
+// Level-scheduled block LU (factor.cu sp_factor): block columns grouped by
+// their height in the block elimination tree (columns of one level are
+// independent); per level the panel tiles and the trailing-update targets,
+// each target with its contributions (L(a,k), U(k,b)) in ascending k so the
+// accumulation order is fixed (deterministic factors).
+//   pan: 2 ints per item (k, 2 * tile id + upper)
+//   tgt: 4 ints per target (kind 0 = Dt / 1 = Lt / 2 = Ut, tile id, first, end contribution)
+//   con: 2 ints per contribution (L tile id, U tile id)
+struct FactorPlan {
+  std::vector<int> lvl_ptr, cols, pan_ptr, pan, tgt_ptr, tgt, con;
+  int64_t contributions = 0;
+};
+void factor_plan(const BlockStructure& bs, FactorPlan& plan);
+
 // One claim-ordered task of a DAG triangular sweep (trsm.cu dag_kernel).
 // Block row i's dependencies, in processing order q (forward: ascending
 // column, backward: descending row), are cut into CHUNK tasks (out >= 0: sum

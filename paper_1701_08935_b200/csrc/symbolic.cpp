@@ -260,6 +260,98 @@ void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::
   bs.critical_path = cp;
 }
 
+void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
+  const int64_t nb = bs.nb;
+  // level = height in the block elimination tree (parent = first structural row below)
+  std::vector<int> level(nb, 0);
+  int nlev = 0;
+  for (int64_t k = 0; k < nb; ++k) {
+    const int64_t p = bs.col_ptr[k + 1] > bs.col_ptr[k] ? bs.col_idx[bs.col_ptr[k]] : -1;
+    if (p >= 0) level[p] = std::max(level[p], level[k] + 1);
+    nlev = std::max(nlev, level[k] + 1);
+  }
+  std::vector<std::vector<int>> by(nlev);
+  for (int64_t k = 0; k < nb; ++k) by[level[k]].push_back(static_cast<int>(k));
+  auto lookup = [&](int64_t i, int64_t k) {  // tile id of (i, k), i > k
+    const auto b = bs.row_idx.begin() + bs.row_ptr[i], e = bs.row_idx.begin() + bs.row_ptr[i + 1];
+    const auto it = std::lower_bound(b, e, k);
+    if (it == e || *it != k) throw std::runtime_error("factor_plan: update target outside the structure");
+    return static_cast<int>(it - bs.row_idx.begin());
+  };
+  plan = FactorPlan();
+  plan.lvl_ptr.push_back(0);
+  plan.pan_ptr.push_back(0);
+  plan.tgt_ptr.push_back(0);
+  const int64_t nkey = nb + 2 * bs.ntiles;  // Dt | Lt | Ut
+  std::vector<int> slot(nkey, -1), cnt;
+  std::vector<int64_t> touched;
+  for (int l = 0; l < nlev; ++l) {
+    for (int k : by[l]) {
+      plan.cols.push_back(k);
+      for (int64_t e = bs.col_ptr[k]; e < bs.col_ptr[k + 1]; ++e) {
+        const int id = static_cast<int>(bs.col_tile[e]);
+        plan.pan.push_back(k);
+        plan.pan.push_back(2 * id);
+        plan.pan.push_back(k);
+        plan.pan.push_back(2 * id + 1);
+      }
+    }
+    // targets of this level: count, then fill contributions in ascending k
+    touched.clear();
+    cnt.clear();
+    std::vector<int64_t> keys;
+    auto key_of = [&](int64_t a, int64_t b) -> int64_t {
+      if (a == b) return a;
+      return a > b ? nb + lookup(a, b) : nb + bs.ntiles + lookup(b, a);
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int k : by[l]) {
+        const int64_t e0 = bs.col_ptr[k], e1 = bs.col_ptr[k + 1];
+        for (int64_t ea = e0; ea < e1; ++ea)
+          for (int64_t eb = e0; eb < e1; ++eb) {
+            const int64_t key = key_of(bs.col_idx[ea], bs.col_idx[eb]);
+            if (pass == 0) {
+              if (slot[key] < 0) {
+                slot[key] = static_cast<int>(keys.size());
+                keys.push_back(key);
+                cnt.push_back(0);
+              }
+              ++cnt[slot[key]];
+            } else {
+              const int t = slot[key];
+              const int at = plan.tgt[4 * t + 3]++;
+              plan.con[2 * at] = static_cast<int>(bs.col_tile[ea]);
+              plan.con[2 * at + 1] = static_cast<int>(bs.col_tile[eb]);
+            }
+          }
+      }
+      if (pass == 0) {
+        // targets of this level are appended after the previous levels' ones
+        const int tbase = static_cast<int>(plan.tgt.size() / 4);
+        int64_t c0 = static_cast<int64_t>(plan.con.size() / 2);
+        for (size_t t = 0; t < keys.size(); ++t) {
+          const int64_t key = keys[t];
+          const int kind = key < nb ? 0 : (key < nb + bs.ntiles ? 1 : 2);
+          const int id = static_cast<int>(kind == 0 ? key : (kind == 1 ? key - nb : key - nb - bs.ntiles));
+          plan.tgt.push_back(kind);
+          plan.tgt.push_back(id);
+          plan.tgt.push_back(static_cast<int>(c0));
+          plan.tgt.push_back(static_cast<int>(c0));  // fill cursor -> end
+          c0 += cnt[t];
+          slot[key] = tbase + static_cast<int>(t);
+        }
+        if (c0 >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
+        plan.con.resize(2 * c0);
+      }
+    }
+    for (int64_t key : keys) slot[key] = -1;
+    plan.lvl_ptr.push_back(static_cast<int>(plan.cols.size()));
+    plan.pan_ptr.push_back(static_cast<int>(plan.pan.size() / 2));
+    plan.tgt_ptr.push_back(static_cast<int>(plan.tgt.size() / 4));
+  }
+  plan.contributions = static_cast<int64_t>(plan.con.size() / 2);
+}
+
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
                  int near, int order, std::vector<DagTask>& tasks) {
   if (chunk < 1 || near < 0) throw std::invalid_argument("dag_schedule: chunk >= 1, near >= 0");

@@ -27,14 +27,13 @@
 #include <cstdlib>
 
 #include "band.cuh"
+#include "mma.cuh"
 
 namespace zolo {
 
 namespace {
 
-constexpr int ST = 256;        // threads per CTA (8 warps)
 constexpr int APAD = TILE + 2; // tile column stride: op N fragment loads conflict free
-constexpr int XPAD = TILE + 4; // x column stride: B fragment loads conflict free
 constexpr int TILE_S = TILE * APAD;
 constexpr int XS = CG * XPAD;
 constexpr int NS = 3;          // helper pipeline stages
@@ -62,24 +61,6 @@ __device__ __forceinline__ void dmma(double c[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
-}
-
-// Per-thread ownership of the 32 x 16 complex output block: warp w holds rows
-// 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1}.
-struct Frag {
-  int row, col;  // first of the two owned (row, col), (row, col+1)
-  int r0, c0;    // warp block origin
-  int lane;
-};
-__device__ __forceinline__ Frag frag() {
-  Frag f;
-  const int w = threadIdx.x >> 5;
-  f.lane = threadIdx.x & 31;
-  f.r0 = 8 * (w & 3);
-  f.c0 = 8 * (w >> 2);
-  f.row = f.r0 + (f.lane >> 2);
-  f.col = f.c0 + 2 * (f.lane & 3);
-  return f;
 }
 
 // acc[2] (complex, the two owned outputs) += op(T)[r0:r0+8, :] X[:, c0:c0+8].
@@ -433,8 +414,6 @@ __global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
 // ---------------------------------------------------------------------------
 // DAG-scheduled sweeps over block-sparse factors (nested dissection etc.)
 // ---------------------------------------------------------------------------
-constexpr int DCG = 32;                  // columns per DAG task
-constexpr int XS2 = DCG * XPAD;          // padded 32 x 32 x block
 constexpr int DNS = 3;                   // pipeline stages
 constexpr int DAG_TRACE_WORDS = 6;       // start, loop end, done, info, wait ns, first tile ready
 constexpr int TSW = TT;                  // swizzled (unpadded) tile
@@ -453,122 +432,6 @@ struct DagArgs {
   unsigned long long* trace;  // optional: per task (start, dependencies done, done, smid<<48|chunk<<47|i<<16|deps)
   int hints;                  // L2 eviction-priority hints on (development switch ZOLO_DAG_HINTS)
 };
-
-// Swizzled tile layout: element (row, col) of a 32 x 32 tile at
-// col*32 + (row ^ swz(col)), swz(c) = 4 (c&1) + 2 ((c>>1)&1). Both fragment
-// patterns -- op N reads T(ar, k), op H reads T(k, ar), with ar = lane/4 and
-// k = lane%4 (+ block offsets) -- hit 8 distinct 16-byte bank groups per
-// quarter warp, so the conjugate-transposed chains are conflict free too, and
-// the tile needs no padding.
-__device__ __forceinline__ int swz(int c) { return ((c & 1) << 2) | (c & 2); }
-
-__device__ __forceinline__ void load_tile_sw(cd* s, const cd* g, unsigned long long pol) {
-#pragma unroll
-  for (int q = 0; q < TT / ST; ++q) {
-    const int e = threadIdx.x + q * ST;
-    const int col = e / TILE, row = e % TILE;
-    cp_async16_cg_hint(&s[col * TILE + (row ^ swz(col))], g + e, pol);
-  }
-}
-
-// non-volatile DMMA: lets the scheduler interleave independent accumulators
-__device__ __forceinline__ void dmma_nv(double c[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c[0]), "+d"(c[1])
-      : "d"(a), "d"(b));
-}
-
-// Per-thread ownership of a 32 x 32 complex output block: warp w holds rows
-// 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1} (+16 for the
-// second block), i.e. two 8x8 DMMA blocks that share their A fragments.
-// DMMA accumulators live across tiles: acc8[h][p][ri][e] (half h, k-step
-// parity p, re/im, element e) = 8 independent chains, folded once per task.
-struct Acc8 {
-  double v[2][2][2][2];
-};
-__device__ __forceinline__ void acc8_zero(Acc8& a) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int p = 0; p < 2; ++p)
-#pragma unroll
-      for (int ri = 0; ri < 2; ++ri) a.v[h][p][ri][0] = a.v[h][p][ri][1] = 0.0;
-}
-// out[2h + e] = the complex output (row, ocol(2h + e))
-__device__ __forceinline__ void acc8_fold(const Acc8& a, cd out[4]) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      out[2 * h + e] = mk(a.v[h][0][0][e] + a.v[h][1][0][e], a.v[h][0][1][e] + a.v[h][1][1][e]);
-}
-
-// km: the k-steps (4-column groups of op(T)) holding nonzeros in this warp's
-// 8 rows (tile_mask_kernel); zero k-steps and all-zero row groups are skipped.
-template <bool OPH, bool NEG>
-__device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* xs, const Frag& f, unsigned km) {
-  if (km == 0) return;
-  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
-  const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
-  const int sa = swz(ar);
-  cd a[TILE / 4], b0[TILE / 4], b1[TILE / 4];
-#pragma unroll
-  for (int kb = 0; kb < TILE / 4; ++kb) {
-    const int k = 4 * kb + am;
-    a[kb] = OPH ? ts[ar * TILE + (k ^ sa)] : ts[k * TILE + (ar ^ swz(k))];
-    if (NEG) a[kb] = mk(-a[kb].x, -a[kb].y);
-    b0[kb] = xs[bc * XPAD + k];
-    b1[kb] = xs[(bc + 16) * XPAD + k];
-  }
-#pragma unroll
-  for (int kb = 0; kb < TILE / 4; ++kb) {
-    if (!((km >> kb) & 1u)) continue;
-    const int p = kb & 1;
-    // op N: re += ax bx - ay by, im += ax by + ay bx; op H (conj a): re += ax bx + ay by, im += ax by - ay bx
-    const double ny = OPH ? a[kb].y : -a[kb].y;
-    const double py = OPH ? -a[kb].y : a[kb].y;
-    dmma_nv(acc.v[0][p][0], a[kb].x, b0[kb].x);
-    dmma_nv(acc.v[1][p][0], a[kb].x, b1[kb].x);
-    dmma_nv(acc.v[0][p][1], a[kb].x, b0[kb].y);
-    dmma_nv(acc.v[1][p][1], a[kb].x, b1[kb].y);
-    dmma_nv(acc.v[0][p][0], ny, b0[kb].y);
-    dmma_nv(acc.v[1][p][0], ny, b1[kb].y);
-    dmma_nv(acc.v[0][p][1], py, b0[kb].x);
-    dmma_nv(acc.v[1][p][1], py, b1[kb].x);
-  }
-}
-
-// acc += op(T) X, or -= with neg (the pre-transform entry)
-__device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs, bool opH, bool neg, const Frag& f,
-                                          unsigned km) {
-  if (opH) {
-    if (neg)
-      mma_tile2_t<true, true>(acc, ts, xs, f, km);
-    else
-      mma_tile2_t<true, false>(acc, ts, xs, f, km);
-  } else {
-    if (neg)
-      mma_tile2_t<false, true>(acc, ts, xs, f, km);
-    else
-      mma_tile2_t<false, false>(acc, ts, xs, f, km);
-  }
-}
-
-// 32 rows x 32 columns of a column-major block into [col*XPAD + row].
-__device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int c0, int nc, unsigned long long pol) {
-  const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < DCG / 8; ++q) {
-    const int c = cc + 8 * q;
-    if (c < nc)
-      cp_async16_cg_hint(&xs[c * XPAD + row], base + row + (c0 + c) * ld, pol);
-    else
-      xs[c * XPAD + row] = mk(0.0, 0.0);
-  }
-}
-
-// output column of acc[q] within the 32-column group
-__device__ __forceinline__ int ocol(const Frag& f, int q) { return f.col + (q & 1) + 16 * (q >> 1); }
 
 // every thread spins on a share of cnt flags; the barrier publishes them all
 __device__ __forceinline__ void wait_flags_par(const int* f, int cnt, int epoch, int* err) {

@@ -1,6 +1,5 @@
 #!/bin/bash
-# Development sweep over DAG knobs on cfg2 (GPU box).
-for h in 0 1 2 3; do
-  echo "== hints $h"
-  ZOLO_DAG_HINTS=$h timeout 120 python tools/quick_check.py cfg2 2>&1 | tail -1
+for lv in 2 1; do
+  echo "== levels $lv"
+  ZOLO_FACTOR_LEVELS=$lv timeout 300 python tools/quick_check.py cfg2 cfg1 2>&1 | grep -E "factor wall|apply_filter|vs reference" | head -6
 done
