@@ -327,6 +327,18 @@ def main():
         "t_factor_ms": t_factor_ms,
         "gmres_iterations": iters,
     }
+    if ws == 1 and rank == 0:
+        # BASELINE metric 2 on the same config: the whole eigensolver (factorization +
+        # subspace iterations to tol 1e-10, eigensolver.hpp:154-217) through zolo_subspace_iteration
+        from paper_1701_08935_b200.driver import SolveConfig, subspace_iteration
+
+        res = subspace_iteration(pen, gaps, SolveConfig(n_lambda=nl, oversample_k=nv - nl, r=r, tol=1e-10, seed=1),
+                                 is_complex=cx, device=local)
+        line["time_to_all_eigenpairs"] = {
+            "value": res.time_to_all_eigenpairs, "unit": "s", "t_factor_s": res.stats.factorization_time,
+            "t_iter_s": res.stats.iteration_time, "found": int(len(res.lambdas)), "n_lambda": nl,
+            "converged": bool(res.converged), "residual": res.residual, "n_iter": res.stats.n_iter,
+            "n_gmres": res.stats.n_gmres}
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(pen, cx, gaps, r, nv)
     if rank == 0:
