@@ -24,7 +24,7 @@ from typing import List, Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libzolo_b200.so")
+LIB_PATH = os.environ.get("ZOLO_LIB_PATH") or os.path.join(HERE, "libzolo_b200.so")  # (override: development builds)
 
 ZOLO_OK, ZOLO_ERR_DOMAIN, ZOLO_ERR_NUMERICAL, ZOLO_ERR_FACTORIZATION, ZOLO_ERR_GMRES, ZOLO_ERR_CUDA = range(6)
 MAX_ORDER = 16

@@ -414,7 +414,13 @@ __global__ void __launch_bounds__(ST, 2) trsm_kernel(SolveArgs A) {
 // ---------------------------------------------------------------------------
 // DAG-scheduled sweeps over block-sparse factors (nested dissection etc.)
 // ---------------------------------------------------------------------------
-constexpr int DNS = 3;                   // pipeline stages
+#ifndef ZOLO_DNS
+#define ZOLO_DNS 3
+#endif
+#ifndef ZOLO_DAG_MINB
+#define ZOLO_DAG_MINB 2
+#endif
+constexpr int DNS = ZOLO_DNS;            // pipeline stages
 constexpr int DAG_TRACE_WORDS = 6;       // start, loop end, done, info, wait ns, first tile ready
 constexpr int TSW = TT;                  // swizzled (unpadded) tile
 constexpr int DAG_SMEM_FIXED = DNS * (TSW + XS2) * static_cast<int>(sizeof(cd));
@@ -611,7 +617,7 @@ __device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* s
 // Persistent CTAs claim (record, chain, group) tasks in schedule order; each
 // claims its NEXT task when it starts the current one and prefetches that
 // task's record behind the current tile pipeline.
-__global__ void __launch_bounds__(ST, 2) dag_kernel(DagArgs A) {
+__global__ void __launch_bounds__(ST, ZOLO_DAG_MINB) dag_kernel(DagArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cd* smem = reinterpret_cast<cd*>(smem_raw);
   int* recb = reinterpret_cast<int*>(smem_raw + DAG_SMEM_FIXED);  // 2 x DAG_REC

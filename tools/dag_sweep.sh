@@ -1,5 +1,5 @@
 #!/bin/bash
-for lv in 2 1; do
-  echo "== levels $lv"
-  ZOLO_FACTOR_LEVELS=$lv timeout 300 python tools/quick_check.py cfg2 cfg1 2>&1 | grep -E "factor wall|apply_filter|vs reference" | head -6
+for lib in "" tools/dev/lib_dns2_b3.so; do
+  echo "== lib ${lib:-default}"
+  ZOLO_LIB_PATH=$lib timeout 300 python tools/quick_check.py cfg2 cfg3 2>&1 | grep -E "apply_filter|solve:" | sed -n '3,4p;7,8p'
 done
