@@ -122,6 +122,19 @@ int zolo_factorize(zolo_ctx* ctx, const int64_t* perm, zolo_factor_stats* stats)
 enum { ZOLO_ORDER_ND = 0, ZOLO_ORDER_RCM = 1 };
 int zolo_set_ordering(zolo_ctx* ctx, int mode, int64_t nd_leaf);
 
+/* Solve mode of the shifted systems (BASELINE config 2 "hybrid solve";
+ * the reference factors every pole):
+ *   ZOLO_SOLVE_DIRECT  (default) every pole factored, as the reference;
+ *   ZOLO_SOLVE_HYBRID  only `pole` is factored; for the others
+ *     (A - s_j B)^{-1} B v = (I - (s_j - s_p) K_p^{-1} B)^{-1} K_p^{-1} B v
+ *     by one shift-invariant multi-shift GMRES on K_p^{-1} B per G application
+ *     (one Krylov basis serving every other pole), to relative residual
+ *     inner_tol within inner_max iterations (else ZOLO_ERR_NUMERICAL).
+ * ND ordering, no pole sharding; call after zolo_set_design, before
+ * zolo_factorize. The inner-solve counter then counts K_p applications. */
+enum { ZOLO_SOLVE_DIRECT = 0, ZOLO_SOLVE_HYBRID = 1 };
+int zolo_set_solve_mode(zolo_ctx* ctx, int mode, int pole, double inner_tol, int inner_max);
+
 /* Sylvester inertia (the reference takes eigenvalue
  * counts as inputs): *count = the number of eigenvalues of the
  * pencil (A, B), B Hermitian positive definite, below the real shift sigma,
@@ -218,7 +231,8 @@ void zolo_set_error(zolo_ctx* ctx, const char* msg);
  * ms[3] = number of solve-kernel launches in the last apply_filter,
  * ms[4] = kernel launches of the last apply_filter (all kernels),
  * ms[5] = operator applications (sum of active columns) of the last apply_filter,
- * ms[6..7] reserved. ms must hold 8 doubles. */
+ * ms[6] = hybrid solve: inner K_p applications (column-steps) of the last apply_filter,
+ * ms[7] reserved. ms must hold 8 doubles. */
 int zolo_last_timings(const zolo_ctx* ctx, double* ms);
 
 /* Structure the triangular sweeps run over (per pole, after zolo_factorize):

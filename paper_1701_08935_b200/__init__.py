@@ -129,6 +129,7 @@ def lib():
         L.zolo_set_pole_shard.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
         L.zolo_nccl_unique_id.argtypes = [C.c_char_p]
         L.zolo_count_below.argtypes = [P, D, P, P]
+        L.zolo_set_solve_mode.argtypes = [P, C.c_int, C.c_int, D, C.c_int]
         L.zolo_factorize.argtypes = [P, P, P]
         L.zolo_apply_g.argtypes = [P, P, P, I64]
         L.zolo_apply_filter.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
@@ -282,10 +283,14 @@ class FilterOperator:
     multi-GPU operator (zolo_set_pole_shard): it factors the poles
     :func:`shard_poles` gives and all-reduces every G application over NCCL;
     ``unique_id=None`` leaves G unreduced (``apply_g`` returns the partial sum).
+    ``solve="hybrid"`` factors only pole ``hybrid_pole`` and solves the other
+    shifted systems by shift-invariant GMRES on K_p^{-1} B (zolo_set_solve_mode;
+    BASELINE config 2) to ``inner_tol`` within ``inner_max`` iterations.
     """
 
     def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None,
-                 ordering: str = "nd", nd_leaf: int = 256, shard=None):
+                 ordering: str = "nd", nd_leaf: int = 256, shard=None, solve: str = "direct", hybrid_pole: int = 0,
+                 inner_tol: float = 1e-14, inner_max: int = 256):
         L = lib()
         n, a, b = pencil
         cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
@@ -313,6 +318,12 @@ class FilterOperator:
             uid = shard[2] if len(shard) > 2 else None
             _check(h, L.zolo_set_pole_shard(h, self.shard[0], self.shard[1], uid))
         self.poles = shard_poles(self.r, *self.shard)
+        if solve not in ("direct", "hybrid"):
+            raise DomainError("solve must be 'direct' or 'hybrid'")
+        self.solve = solve
+        if solve == "hybrid":
+            _check(h, L.zolo_set_solve_mode(h, 1, int(hybrid_pole), float(inner_tol), int(inner_max)))
+            self.poles = [int(hybrid_pole)]
         self.stats = (FactorStats * self.r)()
         perm_arr = None if perm is None else np.ascontiguousarray(perm, dtype=np.int64)
         st = L.zolo_factorize(h, _ptr(perm_arr), self.stats)
@@ -417,7 +428,7 @@ class FilterOperator:
         ms = np.zeros(8)
         lib().zolo_last_timings(self._h, _ptr(ms))
         return dict(filter_ms=ms[0], factor_ms=ms[1], trsm_ms=ms[2], trsm_launches=int(ms[3]),
-                    kernel_launches=int(ms[4]), operator_applications=int(ms[5]))
+                    kernel_launches=int(ms[4]), operator_applications=int(ms[5]), inner_steps=int(ms[6]))
 
     def sweep_profile(self):
         """Structure the triangular sweeps run over (zolo_sweep_profile)."""

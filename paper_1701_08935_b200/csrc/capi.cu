@@ -122,7 +122,7 @@ struct zolo_ctx {
   std::vector<int64_t> perm;
   bool have_perm = false;
   BandGeom geom;
-  DevMem perm_d, arp_d, aci_d, av_d, brp_d, bci_d, bv_d;
+  DevMem perm_d, arp_d, aci_d, av_d, brp_d, bci_d, bv_d, bvc_d;
 
   // factors
   bool factored = false;
@@ -173,6 +173,19 @@ struct zolo_ctx {
   double last_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+
+  // hybrid inner solve (BASELINE config 2): one factored pole,
+  // shift-invariant GMRES on K_p^{-1} B for the others
+  int hybrid = 0, hy_pole = 0, hy_max = 256;
+  double hy_tol = 1e-14;
+  int64_t hy_inner_its = 0;  // inner Arnoldi steps (summed over columns) of the last apply_filter
+  DevMem hy_x0[2], hy_y[2], hy_w, hy_weights, hy_shifts[2], hy_ccoef[2], act_in_d;
+  DevMem iH, iR, iG, iROT, iY, iZ, ires, ifrozen, imlen, ibeta, imcol, ihappy, idone, iwnorm, ipartial, ihsave,
+      ibasis_ptrs;
+  std::vector<std::unique_ptr<DevMem>> ibasis;
+  int imaxit_cap = 0;
+  int64_t incap = 0;
+  int* act_in_h = nullptr;
 
   // pole sharding: this context factors the poles own[] of the design
   int shard_rank = 0, shard_size = 1;
@@ -283,6 +296,11 @@ void upload_device_pencil(zolo_ctx& c, const std::vector<int64_t>& inv, const st
     upload(c.brp_d, prp, c.st);
     upload(c.bci_d, pci, c.st);
     upload(c.bv_d, pv, c.st);
+    if (!c.cx) {  // complex copy for the hybrid solve's inner Krylov space (complex even for real pencils)
+      std::vector<double> pvc(2 * pv.size(), 0.0);
+      for (size_t q = 0; q < pv.size(); ++q) pvc[2 * q] = pv[q];
+      upload(c.bvc_d, pvc, c.st);
+    }
   }
   std::vector<int> p32(inv.begin(), inv.end());
   upload(c.perm_d, p32, c.st);
@@ -737,7 +755,10 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
 // poles of this context (j = rank, rank + nranks, ... < r) and their weights, local order
 void refresh_own(zolo_ctx& c) {
   c.own.clear();
-  for (int j = c.shard_rank; j < c.r; j += c.shard_size) c.own.push_back(j);
+  if (c.hybrid)
+    c.own.push_back(c.hy_pole);
+  else
+    for (int j = c.shard_rank; j < c.r; j += c.shard_size) c.own.push_back(j);
   std::vector<cd> w(std::max<size_t>(c.own.size(), 1), mk(0.0, 0.0));
   for (size_t k = 0; k < c.own.size(); ++k) w[k] = mk(c.eff_w[c.own[k]].real(), c.eff_w[c.own[k]].imag());
   upload(c.weights_d, w, c.st);
@@ -840,8 +861,27 @@ void combine_g(zolo_ctx& c, const void* vsrc, const int* act, int na, std::vecto
     Krylov<double>::scatter_cols(c.st, ld, c.wc.as<double>(), act, na, reinterpret_cast<double*>(wdst));
 }
 
+// DAG sweeps (forward, backward, and the adjoint post-pass) of the chains
+// [first, first + nsub) on bbuf's first na (compacted) columns -> their xbuf.
+void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* trace = nullptr) {
+  const int64_t ld = c.geom.npad;
+  unsigned long long* fx = c.flags.as<unsigned long long>();
+  int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
+  int* cf = fc + c.cflags_off;
+  dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
+                  c.counter.as<int>(), 1, c.num_sms, trace);
+  dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
+                  c.counter.as<int>() + 1, 0, c.num_sms);
+  if (c.cx)
+    for (int ci = first; ci < first + nsub; ++ci)
+      if (ci & 1) blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true, c.xbuf[ci]->as<cd>(), na, ld);
+}
+
+float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst);
+
 // G applied to the columns act[0..na) of vsrc (ld x ncap, S) -> w[:, act].
 float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
+  if (c.hybrid) return apply_g_hybrid(c, vsrc, na, wdst);
   const int64_t ld = c.geom.npad, n = ld;  // device rows: padding rows (anywhere in ND order) are zero
   const int* act = c.act_d.as<int>();
   const int nch = c.nchains();
@@ -866,9 +906,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
       CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 6 * ntask, c.st));
       dtr = c.trace_buf.as<unsigned long long>();
     }
-    int* cf = fc + c.cflags_off;
-    dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>(), nch, na, ld, fc, cf, ++c.epoch,
-                    c.counter.as<int>(), 1, c.num_sms, dtr);
+    sweep_sparse(c, 0, nch, na, dtr);
     if (dtr) {
       std::vector<unsigned long long> h(6 * ntask);
       CK(cudaMemcpyAsync(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
@@ -884,11 +922,6 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
       }
       c.trace_done = true;
     }
-    dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>(), nch, na, ld, fc, cf, ++c.epoch,
-                    c.counter.as<int>() + 1, 0, c.num_sms);
-    if (c.cx)
-      for (int p = 0; p < c.nloc(); ++p)
-        blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
     CK(cudaEventRecord(c.ev3, c.st));
     CK(cudaGetLastError());
     combine_g(c, vsrc, act, na, xs, wdst);
@@ -995,6 +1028,212 @@ void* basis_block(zolo_ctx& c, int i) {
   return c.basis[i]->p;
 }
 
+// ---- hybrid inner solve (BASELINE config 2) --------
+// Only pole p is factored. With M = K_p^{-1} B and delta_j = s_j - s_p,
+//   K_j^{-1} B v = (I - delta_j M)^{-1} K_p^{-1} B v = -(1/delta_j) (M - I/delta_j)^{-1} x0,
+// x0 = K_p^{-1} B v, so one Krylov space K_m(M, x0) per column serves every
+// other pole (shift-invariance): the batched multi-shift GMRES of the outer
+// loop (krylov.cu) runs on M with shifts -1/delta_j and folds the weighted
+// solutions sum_j w_j (-1/delta_j) y_j into one block (complex coefficients).
+// Complex pencils repeat it for the adjoint solves with M' = K_p^{-H} B and the
+// conjugated shifts / weights.
+void ensure_inner(zolo_ctx& c, int64_t nv, int q, int maxit) {
+  const int64_t ld = c.geom.npad;
+  if (nv > c.incap) {
+    for (int k = 0; k < 2; ++k) {
+      c.hy_x0[k].ensure(sizeof(cd) * ld * nv);
+      c.hy_y[k].ensure(sizeof(cd) * ld * nv);
+    }
+    c.hy_w.ensure(sizeof(cd) * ld * nv);
+    c.act_in_d.ensure(sizeof(int) * nv);
+    if (c.act_in_h) cudaFreeHost(c.act_in_h);
+    CK(cudaMallocHost(&c.act_in_h, sizeof(int) * nv));
+    c.imaxit_cap = 0;
+    for (auto& b : c.ibasis) b->release();
+    c.incap = nv;
+  }
+  if (maxit > c.imaxit_cap) {
+    nv = c.incap;
+    const size_t es = sizeof(cd);
+    c.iH.ensure(es * nv * (maxit + 1) * maxit);
+    c.iR.ensure(sizeof(cd) * nv * q * maxit * maxit);
+    c.iG.ensure(sizeof(cd) * nv * q * (maxit + 1));
+    c.iROT.ensure(sizeof(cd) * nv * q * 2 * maxit);
+    c.iY.ensure(sizeof(cd) * nv * q * maxit);
+    c.iZ.ensure(sizeof(cd) * nv * maxit);
+    c.ires.ensure(sizeof(double) * nv * q);
+    c.ifrozen.ensure(sizeof(int) * nv * q);
+    c.imlen.ensure(sizeof(int) * nv * q);
+    c.ibeta.ensure(sizeof(double) * nv);
+    c.imcol.ensure(sizeof(int) * nv);
+    c.ihappy.ensure(sizeof(int) * nv);
+    c.idone.ensure(sizeof(int) * nv);
+    c.iwnorm.ensure(sizeof(double) * nv);
+    const int64_t nchunk = (ld + CHUNK - 1) / CHUNK;
+    c.ipartial.ensure(2 * es * nv * nchunk * (maxit + 1) + 64);
+    c.ihsave.ensure(es * nv * (maxit + 1));
+    c.ibasis_ptrs.ensure(sizeof(void*) * (maxit + 1));
+    while (static_cast<int>(c.ibasis.size()) <= maxit) c.ibasis.emplace_back(new DevMem());
+    std::vector<void*> bp(maxit + 1);
+    for (int i = 0; i <= maxit; ++i) {
+      c.ibasis[i]->ensure(sizeof(cd) * ld * c.incap);
+      bp[i] = c.ibasis[i]->p;
+    }
+    CK(cudaMemcpyAsync(c.ibasis_ptrs.p, bp.data(), sizeof(void*) * bp.size(), cudaMemcpyHostToDevice, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    c.imaxit_cap = maxit;
+  }
+}
+
+// inner shifts / folded coefficients of problem k (0: solve, 1: adjoint)
+void hybrid_setup(zolo_ctx& c) {
+  const double* poles = c.design.data() + ZOLO_DESIGN_HEAD;
+  const std::complex<double> sp(poles[2 * c.hy_pole], poles[2 * c.hy_pole + 1]);
+  for (int k = 0; k < 2; ++k) {
+    std::vector<cd> sh, cf;
+    for (int j = 0; j < c.r; ++j) {
+      if (j == c.hy_pole) continue;
+      std::complex<double> d = std::complex<double>(poles[2 * j], poles[2 * j + 1]) - sp;
+      std::complex<double> w = c.eff_w[j];
+      if (k == 1) {
+        d = std::conj(d);
+        w = std::conj(w);
+      }
+      const std::complex<double> s = -1.0 / d, co = w * (-1.0 / d);
+      sh.push_back(mk(s.real(), s.imag()));
+      cf.push_back(mk(co.real(), co.imag()));
+    }
+    if (sh.empty()) sh.push_back(mk(0.0, 0.0)), cf.push_back(mk(0.0, 0.0));
+    upload(c.hy_shifts[k], sh, c.st);
+    upload(c.hy_ccoef[k], cf, c.st);
+  }
+  const std::complex<double> w0 = c.eff_w[c.hy_pole];
+  upload(c.hy_weights, std::vector<cd>{mk(w0.real(), w0.imag()), mk(1.0, 0.0)}, c.st);
+}
+
+GmresDev inner_view(zolo_ctx& c, int k, int nv, int q, int maxit) {
+  GmresDev g;
+  g.maxit = maxit;
+  g.q = q;
+  g.nv = nv;
+  g.H = c.iH.p;
+  g.R = c.iR.as<cd>();
+  g.G = c.iG.as<cd>();
+  g.ROT = c.iROT.as<cd>();
+  g.Y = c.iY.as<cd>();
+  g.Z = c.iZ.as<cd>();
+  g.res = c.ires.as<double>();
+  g.frozen = c.ifrozen.as<int>();
+  g.mlen = c.imlen.as<int>();
+  g.beta = c.ibeta.as<double>();
+  g.mcol = c.imcol.as<int>();
+  g.happy = c.ihappy.as<int>();
+  g.done = c.idone.as<int>();
+  g.wnorm = c.iwnorm.as<double>();
+  g.shifts = c.hy_shifts[k].as<cd>();
+  g.coef = nullptr;
+  g.ccoef = c.hy_ccoef[k].as<cd>();
+  return g;
+}
+
+// y[:, 0:na] = sum_j ccoef_j (M_k + s_j I)^{-1} x0[:, 0:na] (compacted columns), M_0 = K_p^{-1} B,
+// M_1 = K_p^{-H} B; the operator is applied through chain k of the factored pole.
+void inner_gmres(zolo_ctx& c, int k, int na) {
+  const int64_t ld = c.geom.npad, n = ld;
+  const int q = c.r - 1, maxit = c.hy_max;
+  GmresDev g = inner_view(c, k, na, q, maxit);
+  const cd* x0 = c.hy_x0[k].as<cd>();
+  cd* const* basis = c.ibasis_ptrs.as<cd*>();
+  Krylov<cd>::col_norms(c.st, x0, ld, ld, na, g.beta);
+  Krylov<cd>::scale_cols(c.st, x0, c.ibasis[0]->as<cd>(), n, ld, na, g.beta);
+  gmres_init(c.st, g);
+  std::vector<double> beta(na);
+  CK(cudaMemcpyAsync(beta.data(), g.beta, sizeof(double) * na, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  std::vector<int> active, done(na);
+  for (int a = 0; a < na; ++a)
+    if (beta[a] != 0.0) active.push_back(a);
+  const int nchunk = static_cast<int>((ld + CHUNK - 1) / CHUNK);
+  for (int it = 0; it < maxit && !active.empty(); ++it) {
+    const int nai = static_cast<int>(active.size());
+    std::memcpy(c.act_in_h, active.data(), sizeof(int) * nai);
+    CK(cudaMemcpyAsync(c.act_in_d.p, c.act_in_h, sizeof(int) * nai, cudaMemcpyHostToDevice, c.st));
+    const int* act = c.act_in_d.as<int>();
+    // w = M V_it: B, then the sweeps of chain k, scattered back to the columns
+    Krylov<cd>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
+                        c.cx ? c.bv_d.as<cd>() : c.bvc_d.as<cd>(), c.ibasis[it]->as<cd>(), act, nai,
+                        c.bbuf.as<cd>());
+    sweep_sparse(c, k, 1, nai);
+    Krylov<cd>::scatter_cols(c.st, ld, c.xbuf[k]->as<cd>(), act, nai, c.hy_w.as<cd>());
+    c.inner_solves += nai;
+    c.hy_inner_its += nai;
+    Krylov<cd>::arnoldi(c.st, ld, ld, basis, it, c.hy_w.as<cd>(), act, nai, g, c.ipartial.as<double>(), nchunk,
+                        c.ihsave.as<cd>());
+    Krylov<cd>::least_squares(c.st, act, nai, it, g, c.ipartial.as<double>(), nchunk, c.hy_tol);
+    if (it + 1 < maxit) Krylov<cd>::next_basis(c.st, n, ld, c.hy_w.as<cd>(), c.ibasis[it + 1]->as<cd>(), act, nai, g);
+    CK(cudaGetLastError());
+    int spin_err[2] = {0, 0};
+    CK(cudaMemcpyAsync(done.data(), g.done, sizeof(int) * na, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaMemcpyAsync(spin_err, c.counter.as<int>() + 2, sizeof(int) * 2, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    if (spin_err[0] || spin_err[1]) throw ZoloError(ZOLO_ERR_CUDA, "triangular solve: dependency wait timed out");
+    std::vector<int> next;
+    for (int a : active)
+      if (!done[a]) next.push_back(a);
+    active.swap(next);
+  }
+  Krylov<cd>::assemble(c.st, n, ld, nullptr, basis, na, g, nullptr, c.hy_y[k].as<cd>());
+  // every shift must have reached the inner tolerance (or a happy breakdown)
+  std::vector<double> res(static_cast<size_t>(na) * q);
+  std::vector<int> happy(na);
+  CK(cudaMemcpyAsync(res.data(), g.res, sizeof(double) * res.size(), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaMemcpyAsync(happy.data(), g.happy, sizeof(int) * na, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  double worst = 0.0;
+  for (int a = 0; a < na; ++a)
+    if (!happy[a] && beta[a] != 0.0)
+      for (int j = 0; j < q; ++j) worst = std::max(worst, res[static_cast<size_t>(a) * q + j]);
+  if (worst > 1e3 * c.hy_tol)
+    throw ZoloError(ZOLO_ERR_NUMERICAL, "hybrid inner GMRES: relative residual " + std::to_string(worst) +
+                                            " after " + std::to_string(maxit) + " iterations");
+}
+
+float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
+  const int64_t ld = c.geom.npad, n = ld;
+  const int* act = c.act_d.as<int>();
+  require(c.sparse, "hybrid solve: needs the ND (block-sparse) factors");
+  ensure_inner(c, c.ncap, std::max(c.r - 1, 1), c.hy_max);
+  if (c.cx)
+    Krylov<cd>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
+                        c.bv_d.as<cd>(), reinterpret_cast<const cd*>(vsrc), act, na, c.bbuf.as<cd>());
+  else
+    Krylov<double>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
+                            c.bv_d.as<double>(), reinterpret_cast<const double*>(vsrc), act, na, c.bbuf.as<cd>());
+  CK(cudaEventRecord(c.ev2, c.st));
+  const int nch = c.nchains();  // 1 (solve) or 2 (solve + adjoint)
+  sweep_sparse(c, 0, nch, na);
+  for (int k = 0; k < nch; ++k)
+    CK(cudaMemcpyAsync(c.hy_x0[k].p, c.xbuf[k]->p, sizeof(cd) * ld * na, cudaMemcpyDeviceToDevice, c.st));
+  if (c.r > 1)
+    for (int k = 0; k < nch; ++k) inner_gmres(c, k, na);
+  else
+    for (int k = 0; k < nch; ++k) CK(cudaMemsetAsync(c.hy_y[k].p, 0, sizeof(cd) * ld * na, c.st));
+  CK(cudaEventRecord(c.ev3, c.st));
+  std::vector<cd*> xs;
+  xs.push_back(c.hy_x0[0].as<cd>());
+  if (c.cx) xs.push_back(c.hy_x0[1].as<cd>());
+  xs.push_back(c.hy_y[0].as<cd>());
+  if (c.cx) xs.push_back(c.hy_y[1].as<cd>());
+  if (c.cx)
+    Krylov<cd>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const cd*>(vsrc), act, na, xs.data(),
+                        c.hy_weights.as<cd>(), 2, reinterpret_cast<cd*>(wdst));
+  else
+    Krylov<double>::combine(c.st, n, ld, c.constant_term, reinterpret_cast<const double*>(vsrc), act, na,
+                            xs.data(), c.hy_weights.as<cd>(), 2, reinterpret_cast<double*>(wdst));
+  CK(cudaGetLastError());
+  return 0.0f;
+}
+
 template <class S>
 int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
                       zolo_report* rep) {
@@ -1015,6 +1254,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   CK(cudaMemcpyAsync(c.basis_ptrs.p, bp.data(), sizeof(void*) * bp.size(), cudaMemcpyHostToDevice, c.st));
   CK(cudaStreamSynchronize(c.st));
 
+  c.hy_inner_its = 0;
   CK(cudaEventRecord(c.ev0, c.st));
   S* vin = c.vin.as<S>();
   Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(d_v), n, vin, ld, ncols, c.perm_d.as<int>());
@@ -1080,6 +1320,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   c.last_ms[3] = trsm_launches;
   c.last_ms[4] = static_cast<double>(launches + 2);
   c.last_ms[5] = static_cast<double>(opapps);
+  c.last_ms[6] = static_cast<double>(c.hy_inner_its);  // hybrid: inner K_p applications (column-steps)
 
   // report (gmres.hpp:31-43 merged as filter_engine.hpp:127-133)
   std::vector<double> res(ncols * q);
@@ -1333,6 +1574,7 @@ int zolo_ctx_destroy(zolo_ctx* c) {
   for (auto s : c->pole_streams) cudaStreamDestroy(s);
   nccl_close(c->comm);
   if (c->act_h) cudaFreeHost(c->act_h);
+  if (c->act_in_h) cudaFreeHost(c->act_in_h);
   if (c->done_h) cudaFreeHost(c->done_h);
   for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3, c->tev0, c->tev1})
     if (ev) cudaEventDestroy(ev);
@@ -1465,6 +1707,25 @@ int zolo_count_below(zolo_ctx* c, double sigma, int64_t* count, double* min_pivo
   });
 }
 
+int zolo_set_solve_mode(zolo_ctx* c, int mode, int pole, double inner_tol, int inner_max) {
+  return guarded(c, [&] {
+    require(mode == ZOLO_SOLVE_DIRECT || mode == ZOLO_SOLVE_HYBRID, "zolo_set_solve_mode: unknown mode");
+    require(c->have_design, "zolo_set_solve_mode: set the design first");
+    if (mode == ZOLO_SOLVE_HYBRID) {
+      require(pole >= 0 && pole < c->r, "zolo_set_solve_mode: factored pole out of range");
+      require(c->order_mode == ZOLO_ORDER_ND, "zolo_set_solve_mode: the hybrid solve needs the ND ordering");
+      require(c->shard_size == 1, "zolo_set_solve_mode: hybrid solve and pole sharding are exclusive");
+      require(inner_tol > 0.0 && inner_max >= 1 && inner_max <= 256, "zolo_set_solve_mode: bad inner limits");
+      c->hy_pole = pole;
+      c->hy_tol = inner_tol;
+      c->hy_max = inner_max;
+    }
+    c->hybrid = mode == ZOLO_SOLVE_HYBRID;
+    refresh_own(*c);
+    if (c->hybrid) hybrid_setup(*c);
+  });
+}
+
 int zolo_nccl_unique_id(void* out) {
   try {
     nccl_unique_id(out);
@@ -1478,6 +1739,7 @@ int zolo_nccl_unique_id(void* out) {
 int zolo_set_pole_shard(zolo_ctx* c, int rank, int nranks, const void* unique_id) {
   return guarded(c, [&] {
     require(nranks >= 1 && rank >= 0 && rank < nranks, "zolo_set_pole_shard: need 0 <= rank < nranks");
+    require(!c->hybrid || nranks == 1, "zolo_set_pole_shard: hybrid solve and pole sharding are exclusive");
     nccl_close(c->comm);
     c->comm = nullptr;
     c->shard_rank = rank;

@@ -23,6 +23,7 @@ namespace {
 
 constexpr int RT = 256;          // threads per reduction block
 constexpr int RPT = CHUNK / RT;  // rows per thread in a chunk
+constexpr int KMAX = 256;         // largest Krylov dimension (outer GMRES <= 64, hybrid inner <= 256)
 
 template <class S>
 __device__ __forceinline__ S warp_sum(S v);
@@ -160,7 +161,7 @@ __global__ void scatter_cols_kernel(int64_t ld, const S* wc, const int* act, S* 
 template <class S>
 __global__ void __launch_bounds__(RT) dots_kernel(int64_t n, int64_t ld, S* const* basis, int m, const S* w,
                                                   const int* act, S* partial, int nchunk, int hstride) {
-  __shared__ S red[RT / 32][64];
+  __shared__ S red[RT / 32][KMAX];
   const int a = blockIdx.x, chunk = blockIdx.y;
   const int64_t col = act[a];
   const int64_t base = static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
@@ -196,8 +197,8 @@ __global__ void __launch_bounds__(RT) update_kernel(int64_t n, int64_t ld, S* co
                                                     const int* act, const S* partial_in, S* partial_out,
                                                     double* norm_out, int nchunk, int hstride, S* hsave,
                                                     void* Hmat, int maxit) {
-  __shared__ S hs[64];
-  __shared__ S red[RT / 32][64];
+  __shared__ S hs[KMAX];
+  __shared__ S red[RT / 32][KMAX];
   const int a = blockIdx.x, chunk = blockIdx.y;
   const int64_t col = act[a];
   if (threadIdx.x <= m) {
@@ -391,7 +392,7 @@ __global__ void least_squares_kernel(const int* act, int m, GmresDev g, const do
     cd z = mk(0.0, 0.0);
     for (int s = 0; s < g.q; ++s) {
       const int64_t ck = static_cast<int64_t>(col) * g.q + s;
-      if (i < g.mlen[ck]) z = cadd(z, cscale(g.Y[ck * maxit + i], g.coef[s]));
+      if (i < g.mlen[ck]) z = cadd(z, g.ccoef ? cmul(g.Y[ck * maxit + i], g.ccoef[s]) : cscale(g.Y[ck * maxit + i], g.coef[s]));
     }
     g.Z[static_cast<int64_t>(col) * maxit + i] = z;
   }
@@ -418,7 +419,7 @@ __global__ void assemble_kernel(int64_t ld, S* const* basis, GmresDev g, const S
     const cd v = to_cd(basis[i][t + c * ld]);
     cfma(acc, z, v);
   }
-  const cd half_v = cscale(to_cd(vin[t + c * ld]), 0.5);
+  const cd half_v = vin ? cscale(to_cd(vin[t + c * ld]), 0.5) : mk(0.0, 0.0);
   if constexpr (sizeof(S) == sizeof(double))
     reinterpret_cast<double*>(out)[t + c * ld] = acc.x + half_v.x;
   else

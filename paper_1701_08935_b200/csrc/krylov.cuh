@@ -28,6 +28,7 @@ struct GmresDev {
   double* wnorm;  // [nv]
   cd* shifts;     // [q]
   double* coef;   // [q]  1/2 M_outer * 1/2 a_(k/2)
+  cd* ccoef = nullptr;  // [q] complex combination coefficients (hybrid inner solve), overrides coef
 };
 
 template <class S>
@@ -53,6 +54,7 @@ struct Krylov {
                             int nchunk, double tol);
   static void next_basis(cudaStream_t st, int64_t n, int64_t ld, const S* w, S* vnext, const int* act, int na,
                          GmresDev g);
+  // out[:, c] = sum_i Z_i V_i (+ vin / 2 when vin != nullptr: the outer filter's 1/2 v)
   static void assemble(cudaStream_t st, int64_t n, int64_t ld, const S* v0, S* const* d_basis, int nv, GmresDev g,
                        const S* vin, S* out);
   // C (k x kk) = Y^H Z (column-major, ld rows) -- RR projections
