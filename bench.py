@@ -334,11 +334,16 @@ def main():
 
         res = subspace_iteration(pen, gaps, SolveConfig(n_lambda=nl, oversample_k=nv - nl, r=r, tol=1e-10, seed=1),
                                  is_complex=cx, device=local)
+        # the window's eigenvalue count by Sylvester inertia (BASELINE config 2: "counted by the oracle via
+        # Sylvester inertia"), on the GPU
+        ctr = zb.InertiaCounter(pen, is_complex=cx, device=local)
+        inertia = ctr.count_in(0.5 * (gaps[0] + gaps[1]), 0.5 * (gaps[2] + gaps[3]))
+        del ctr
         line["time_to_all_eigenpairs"] = {
             "value": res.time_to_all_eigenpairs, "unit": "s", "t_factor_s": res.stats.factorization_time,
             "t_iter_s": res.stats.iteration_time, "found": int(len(res.lambdas)), "n_lambda": nl,
             "converged": bool(res.converged), "residual": res.residual, "n_iter": res.stats.n_iter,
-            "n_gmres": res.stats.n_gmres}
+            "n_gmres": res.stats.n_gmres, "inertia_count": inertia}
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(pen, cx, gaps, r, nv)
     if rank == 0:
