@@ -649,6 +649,252 @@ __global__ void __launch_bounds__(ST, ZOLO_DAG_MINB) dag_kernel(DagArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised DAG sweep (v2): one persistent CTA per SM = 8 consumer warps
+// (DMMA) + 1 producer warp. The producer claims tasks, waits on their producers'
+// flags and streams (tile, u_j) / add-block entries into an NST2-deep ring of
+// shared-memory stages with cp.async + mbarriers, running ahead across task
+// boundaries; consumers never touch global memory except for the task's output,
+// and no CTA-wide barrier sits on the per-tile path.
+// ---------------------------------------------------------------------------
+#ifndef ZOLO_NST2
+#define ZOLO_NST2 3
+#endif
+#ifndef ZOLO_V2_MINB
+#define ZOLO_V2_MINB 2
+#endif
+constexpr int NST2 = ZOLO_NST2;
+constexpr int P2T = ST + 32;  // threads: 8 consumer warps + the producer warp
+struct Meta2 {
+  int kind;  // 0 MMA(tile, x, neg = sign), 1 ADD(x block * sign), 2 END
+  int sign;
+  unsigned mx, my;  // occupancy mask (op N / op H)
+  int last, i, ci, gi, out, nc, pad0, pad1;
+};
+constexpr int DAG2_CHAINS = 32;
+constexpr int DAG2_SMEM = NST2 * (TSW + XS2) * static_cast<int>(sizeof(cd)) + NST2 * static_cast<int>(sizeof(Meta2)) +
+                          2 * NST2 * 8 + DAG2_CHAINS * static_cast<int>(sizeof(Chain)) + DAG_REC * 4;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
+  const unsigned a = smem_u32(b);
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cpasync(unsigned long long* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(ST) : "memory"); }
+
+// lane 0 spins on *f >= epoch (bounded), then the warp reconverges
+__device__ __forceinline__ void warp_wait_flag(const int* f, int epoch, int* err) {
+  if ((threadIdx.x & 31) == 0) {
+    int spins = 0;
+    while (ld_acquire(f) < epoch) {
+      if (++spins > 64) __nanosleep(64);
+      if (spins > (1 << 24)) {
+        atomicExch(err, 1);
+        break;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
+  extern __shared__ __align__(16) unsigned char sm2[];
+  cd* ring = reinterpret_cast<cd*>(sm2);
+  Meta2* meta = reinterpret_cast<Meta2*>(sm2 + NST2 * (TSW + XS2) * sizeof(cd));
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(meta + NST2);
+  unsigned long long* empty = full + NST2;
+  Chain* chs = reinterpret_cast<Chain*>(empty + NST2);
+  int* recp = reinterpret_cast<int*>(chs + DAG2_CHAINS);
+  auto tile_s = [ring](int s) { return ring + s * (TSW + XS2); };
+  auto x_s = [ring](int s) { return ring + s * (TSW + XS2) + TSW; };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = threadIdx.x; q < A.nchains; q += blockDim.x) chs[q] = A.chains[q];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST2; ++s) {
+      mbar_init(full + s, 33);   // 32 producer lanes' copies + the producer's metadata arrive
+      mbar_init(empty + s, ST / 32);
+    }
+  }
+  __syncthreads();
+  const int per_step = A.nchains * A.ngroups;
+  const int ntasks = A.ntask * per_step;
+  if (warp == ST / 32) {
+    // ------------------------------ producer ------------------------------
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    int g = 0;
+    // one ring entry: tile (optional) + a 32 x 32 block with column stride `stride`
+    auto produce = [&](int kind, int sign, const cd* tile, const uint2* mask, const cd* blk, int64_t stride, int c0,
+                       int nc, unsigned long long pol, int last, int i, int ci, int gi, int out) {
+      const int s = g % NST2, round = g / NST2;
+      mbar_wait(empty + s, (round & 1) ^ 1);
+      if (tile) {
+        cd* ts = tile_s(s);
+#pragma unroll 4
+        for (int k = 0; k < TILE; ++k) {  // element (row = lane, col = k)
+          cp_async16_cg_hint(&ts[k * TILE + (lane ^ swz(k))], tile + k * TILE + lane, pol_stream);
+        }
+      }
+      cd* xs = x_s(s);
+#pragma unroll 4
+      for (int c = 0; c < DCG; ++c) {
+        if (c < nc)
+          cp_async16_cg_hint(&xs[c * XPAD + lane], blk + lane + (c0 + c) * stride, pol);
+        else
+          xs[c * XPAD + lane] = mk(0.0, 0.0);
+      }
+      uint2 mw = make_uint2(0xffffffffu, 0xffffffffu);
+      if (mask && lane == 0) mw = *mask;
+      __syncwarp();
+      mbar_arrive_cpasync(full + s);
+      if (lane == 0) {
+        Meta2 m;
+        m.kind = kind;
+        m.sign = sign;
+        m.mx = mw.x;
+        m.my = mw.y;
+        m.last = last;
+        m.i = i;
+        m.ci = ci;
+        m.gi = gi;
+        m.out = out;
+        m.nc = nc;
+        meta[s] = m;
+        mbar_arrive(full + s);
+      }
+      ++g;
+    };
+    // claims run one task ahead: the atomic for task T+1 is issued when T starts
+    int t = 0;
+    if (lane == 0) t = atomicAdd(A.counter, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    for (;;) {
+      if (t >= ntasks) {
+        produce(2, 0, nullptr, nullptr, A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
+        break;
+      }
+      int tn = 0;
+      if (lane == 0) tn = atomicAdd(A.counter, 1);
+      const int r = t / per_step, rem = t % per_step, ci = rem / A.ngroups, gi = rem % A.ngroups;
+      const int* rg = A.recs + static_cast<size_t>(r) * DAG_REC;
+      recp[lane] = rg[lane];
+      recp[lane + 32] = rg[lane + 32];
+      __syncwarp();
+      const int i = recp[0], nd = recp[1], pa = recp[2], pc = recp[3], out = recp[4];
+      const bool chunk = out >= 0;
+      const Chain& ch = chs[ci];
+      const int c0 = gi * DCG, nc = min(DCG, A.ncols - c0);
+      const size_t cgi = static_cast<size_t>(ci) * A.ngroups + gi;
+      const int* flags = A.flags + cgi * A.s.nb;
+      const int* cflags = A.cflags + cgi * A.nslots;
+      // readiness of every dependency and partial, read in parallel (one round trip)
+      const unsigned dep_ready =
+          __ballot_sync(0xffffffffu, lane >= nd || ld_acquire(flags + recp[DAG_REC_HDR + 2 * lane]) >= A.epoch);
+      const int nent = (chunk ? 0 : 1) + pc + nd;
+      int e = 0;
+      if (!chunk) {
+        ++e;
+        if (ch.pre)
+          produce(0, 1, ch.pre + static_cast<size_t>(i) * TT, ch.prem ? ch.prem + i : nullptr,
+                  ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0, nc, pol_stream, e == nent, i, ci, gi, out);
+        else
+          produce(1, -1, nullptr, nullptr, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0, nc, pol_stream,
+                  e == nent, i, ci, gi, out);
+      }
+      for (int p0 = 0; p0 < pc; p0 += 32) {
+        const unsigned prdy =
+            __ballot_sync(0xffffffffu, p0 + lane >= pc || ld_acquire(cflags + pa + p0 + lane) >= A.epoch);
+        for (int p = p0; p < pc && p < p0 + 32; ++p) {
+          if (!((prdy >> (p - p0)) & 1u)) warp_wait_flag(cflags + pa + p, A.epoch, A.counter + 2);
+          ++e;
+          produce(1, 1, nullptr, nullptr, ch.cbuf + static_cast<int64_t>(pa + p) * TILE, A.ldp, c0, nc, pol_stream,
+                  e == nent, i, ci, gi, out);
+        }
+      }
+      for (int q = 0; q < nd; ++q) {
+        const int j = recp[DAG_REC_HDR + 2 * q], tid = recp[DAG_REC_HDR + 2 * q + 1];
+        if (!((dep_ready >> q) & 1u)) warp_wait_flag(flags + j, A.epoch, A.counter + 2);
+        ++e;
+        produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, ch.offm ? ch.offm + tid : nullptr,
+                ch.dst + static_cast<int64_t>(j) * TILE, A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
+      }
+      __syncwarp();
+      t = __shfl_sync(0xffffffffu, tn, 0);
+    }
+    return;
+  }
+  // ------------------------------ consumers ------------------------------
+  const Frag f = frag();
+  Acc8 acc;
+  acc8_zero(acc);
+  for (int g = 0;; ++g) {
+    const int s = g % NST2, round = g / NST2;
+    mbar_wait(full + s, round & 1);
+    const Meta2 m = meta[s];
+    if (m.kind == 2) break;
+    const Chain& ch = chs[m.ci];
+    const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
+    if (m.kind == 0) {
+      mma_tile2(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
+    } else {
+      const cd* xs = x_s(s);
+      const double sg = static_cast<double>(m.sign);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const cd v = xs[ocol(f, 2 * h + e2) * XPAD + f.row];
+          acc.v[h][0][0][e2] += sg * v.x;
+          acc.v[h][0][1][e2] += sg * v.y;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+    if (m.last) {
+      cd o[4];
+      acc8_fold(acc, o);
+      acc8_zero(acc);
+      const bool chunk = m.out >= 0;
+      const int c0 = m.gi * DCG;
+      if (chunk) {
+        cd* prow = ch.cbuf + static_cast<int64_t>(m.out) * TILE + f.row + c0 * A.ldp;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = ocol(f, q);
+          if (c < m.nc) prow[c * A.ldp] = o[q];
+        }
+      } else {
+        cd* urow = ch.dst + static_cast<int64_t>(m.i) * TILE + f.row + c0 * A.ld;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = ocol(f, q);
+          if (c < m.nc) urow[c * A.ld] = mk(-o[q].x, -o[q].y);
+        }
+      }
+      consumers_sync();
+      if (threadIdx.x == 0) {
+        const size_t cgi = static_cast<size_t>(m.ci) * A.ngroups + m.gi;
+        st_release(chunk ? A.cflags + cgi * A.nslots + m.out : A.flags + cgi * A.s.nb + m.i, A.epoch);
+      }
+    }
+  }
+}
+
 // x_i <- op(D_i) x_i per (block row, 16-column group): the adjoint post-pass.
 __global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
   __shared__ __align__(16) cd ds[TILE_S];
@@ -709,6 +955,20 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   a.hints = hints;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int ntasks = sched.ntask * nchains * a.ngroups;
+  static const int v2 = [] {
+    const char* v = std::getenv("ZOLO_DAG_V2");
+    return v ? std::atoi(v) : 1;
+  }();
+  if (v2 && nchains <= DAG2_CHAINS && !trace) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(dag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DAG2_SMEM);
+      attr2 = true;
+    }
+    const int grid = std::min(ntasks, num_sms * ZOLO_V2_MINB);
+    if (grid > 0) dag2_kernel<<<grid, P2T, DAG2_SMEM, st>>>(a);
+    return grid;
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel, ST, smem);
   if (per_sm < 1) per_sm = 1;
