@@ -313,7 +313,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * nv * esize,
                 "d2h_bytes_per_step": n * nv * esize},
         "gpu_launches": int(kernel_launches),
-        "roofline": {"bound": "tensor", "kernel": "dag_kernel (DAG-scheduled block-sparse sweeps, DMMA f64)",
+        "roofline": {"bound": "tensor", "kernel": "dag2_kernel (warp-specialised DAG-scheduled block-sparse sweeps, DMMA f64)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if peak else None, "traffic": traffic,
                      "peak_source": "measured FP64 tensor pipe (tools/fp64_peak.cu mma.sync.m8n8k4.f64, "
