@@ -23,7 +23,8 @@ namespace {
 
 constexpr int RT = 256;          // threads per reduction block
 constexpr int RPT = CHUNK / RT;  // rows per thread in a chunk
-constexpr int KMAX = 256;         // largest Krylov dimension (outer GMRES <= 64, hybrid inner <= 256)
+constexpr int KMAX = 256;
+constexpr int SPC = 8;            // SpMM columns per thread         // largest Krylov dimension (outer GMRES <= 64, hybrid inner <= 256)
 
 template <class S>
 __device__ __forceinline__ S warp_sum(S v);
@@ -89,33 +90,56 @@ __global__ void scale_cols_kernel(const S* v, S* out, int64_t ld, const double* 
 
 template <class S>
 __global__ void apply_b_kernel(int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
-                               const int* act, cd* out) {
+                               const int* act, int na, cd* out) {
+  // one row x SPC columns per thread: the row's indices and values are loaded once
+  // and reused across the columns (the SpMM is index-load bound otherwise)
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int a = blockIdx.y;
+  const int a0 = blockIdx.y * SPC;
   if (t >= ld) return;
-  const int64_t col = act[a];
-  cd s = mk(0.0, 0.0);
+  int64_t col[SPC];
+#pragma unroll
+  for (int c = 0; c < SPC; ++c) col[c] = (a0 + c < na) ? act[a0 + c] : act[a0];
+  S acc[SPC];
+#pragma unroll
+  for (int c = 0; c < SPC; ++c) acc[c] = szero(S());
   if (t < n) {
     if (rp) {
-      S acc = szero(S());
-      for (int q = rp[t]; q < rp[t + 1]; ++q) acc = sadd(acc, smul(vals[q], v[ci[q] + col * ld]));
-      s = to_cd(acc);
+      for (int q = rp[t]; q < rp[t + 1]; ++q) {
+        const S b = vals[q];
+        const int64_t j = ci[q];
+#pragma unroll
+        for (int c = 0; c < SPC; ++c) acc[c] = sadd(acc[c], smul(b, v[j + col[c] * ld]));
+      }
     } else {
-      s = to_cd(v[t + col * ld]);
+#pragma unroll
+      for (int c = 0; c < SPC; ++c) acc[c] = v[t + col[c] * ld];
     }
   }
-  out[t + a * ld] = s;
+#pragma unroll
+  for (int c = 0; c < SPC; ++c)
+    if (a0 + c < na) out[t + (a0 + c) * ld] = to_cd(acc[c]);
 }
 
 template <class S>
-__global__ void spmm_kernel(int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v, S* out) {
+__global__ void spmm_kernel(int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v, int64_t k,
+                            S* out) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t c = blockIdx.y;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.y) * SPC;
   if (t >= ld) return;
-  S acc = szero(S());
+  S acc[SPC];
+#pragma unroll
+  for (int c = 0; c < SPC; ++c) acc[c] = szero(S());
   if (t < n)
-    for (int q = rp[t]; q < rp[t + 1]; ++q) acc = sadd(acc, smul(vals[q], v[ci[q] + c * ld]));
-  out[t + c * ld] = acc;
+    for (int q = rp[t]; q < rp[t + 1]; ++q) {
+      const S b = vals[q];
+      const int64_t j = ci[q];
+#pragma unroll
+      for (int c = 0; c < SPC; ++c)
+        if (c0 + c < k) acc[c] = sadd(acc[c], smul(b, v[j + (c0 + c) * ld]));
+    }
+#pragma unroll
+  for (int c = 0; c < SPC; ++c)
+    if (c0 + c < k) out[t + (c0 + c) * ld] = acc[c];
 }
 
 struct XPtrs {
@@ -528,7 +552,9 @@ void Krylov<S>::scale_cols(cudaStream_t st, const S* v, S* out, int64_t n, int64
 template <class S>
 void Krylov<S>::apply_b(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals,
                         const S* v, const int* act, int na, cd* out) {
-  if (na > 0) apply_b_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(n, ld, rp, ci, vals, v, act, out);
+  if (na > 0)
+    apply_b_kernel<S><<<dim3(blocks_for(ld, 256), (na + SPC - 1) / SPC), 256, 0, st>>>(n, ld, rp, ci, vals, v, act, na,
+                                                                                      out);
 }
 template <class S>
 void Krylov<S>::combine(cudaStream_t st, int64_t n, int64_t ld, double c0, const S* v, const int* act, int na,
@@ -589,7 +615,9 @@ void Krylov<S>::block_gemm(cudaStream_t st, int64_t n, int64_t ld, const S* y, i
 template <class S>
 void Krylov<S>::spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
                      int64_t k, S* out) {
-  if (k > 0) spmm_kernel<S><<<dim3(blocks_for(ld, 256), k), 256, 0, st>>>(n, ld, rp, ci, vals, v, out);
+  if (k > 0)
+    spmm_kernel<S><<<dim3(blocks_for(ld, 256), static_cast<unsigned>((k + SPC - 1) / SPC)), 256, 0, st>>>(n, ld, rp, ci,
+                                                                                                       vals, v, k, out);
 }
 
 template <class S>
