@@ -156,7 +156,7 @@ struct DagSched {
 };
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
-                    unsigned long long* trace = nullptr);
+                    unsigned long long* trace = nullptr, const int* tmap = nullptr);
 int dag_groups(int ncols);
 
 // x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass

@@ -148,7 +148,8 @@ struct zolo_ctx {
   std::vector<int> sp_col_cnt;
   int64_t critical_path = 0;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
-  DevMem sp_sched_fwd, sp_sched_bwd, sp_masks;
+  DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
+  int tmap_nch = -1;  // chain count the staggered claim maps were built for
   DevMem sp_er, sp_ec, sp_ea, sp_eb;  // scatter lists of the union pattern in the factor ordering
   int64_t sp_nnz = 0;
   int sp_npads = 0;
@@ -581,6 +582,9 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     upload(c.sp_sched_fwd, records(tf, true), c.st);
     upload(c.sp_sched_bwd, records(tb, false), c.st);
     c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), static_cast<int>(tf.size()), sf};
+    c.tmap_nch = -1;
+    c.sp_tmap_fwd.release();
+    c.sp_tmap_bwd.release();
     c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb};
     c.sp_nslots = std::max(sf, sb);
   }
@@ -863,15 +867,41 @@ void combine_g(zolo_ctx& c, const void* vsrc, const int* act, int na, std::vecto
 
 // DAG sweeps (forward, backward, and the adjoint post-pass) of the chains
 // [first, first + nsub) on bbuf's first na (compacted) columns -> their xbuf.
+// Claim order with the chains staggered by `stagger` x (records / chains)
+// positions: each chain keeps its topological order, and at any time only a
+// few chains are in their narrow (top-separator) phase.
+void build_tmap(zolo_ctx& c, int nch) {
+  static const double stagger = [] {
+    const char* v = std::getenv("ZOLO_DAG_STAGGER");
+    return v ? std::atof(v) : 0.0;
+  }();
+  c.tmap_nch = nch;
+  if (stagger <= 0.0 || nch < 2) return;
+  for (int dir = 0; dir < 2; ++dir) {
+    const int nt = dir == 0 ? c.sched_fwd.ntask : c.sched_bwd.ntask;
+    const double delta = stagger * nt / nch;
+    std::vector<std::pair<double, int>> key;
+    key.reserve(static_cast<size_t>(nt) * nch);
+    for (int ci = 0; ci < nch; ++ci)
+      for (int p = 0; p < nt; ++p) key.emplace_back(p + ci * delta, p * nch + ci);
+    std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<int> map(key.size());
+    for (size_t k = 0; k < key.size(); ++k) map[k] = key[k].second;
+    upload(dir == 0 ? c.sp_tmap_fwd : c.sp_tmap_bwd, map, c.st);
+  }
+}
+
 void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* trace = nullptr) {
   const int64_t ld = c.geom.npad;
   unsigned long long* fx = c.flags.as<unsigned long long>();
   int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
   int* cf = fc + c.cflags_off;
+  if (c.tmap_nch != c.nchains()) build_tmap(c, c.nchains());
+  const bool full = first == 0 && nsub == c.nchains() && c.sp_tmap_fwd.p && c.tmap_nch == nsub;
   dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
-                  c.counter.as<int>(), 1, c.num_sms, trace);
+                  c.counter.as<int>(), 1, c.num_sms, trace, full ? c.sp_tmap_fwd.as<int>() : nullptr);
   dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
-                  c.counter.as<int>() + 1, 0, c.num_sms);
+                  c.counter.as<int>() + 1, 0, c.num_sms, nullptr, full ? c.sp_tmap_bwd.as<int>() : nullptr);
   if (c.cx)
     for (int ci = first; ci < first + nsub; ++ci)
       if (ci & 1) blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true, c.xbuf[ci]->as<cd>(), na, ld);

@@ -437,6 +437,7 @@ struct DagArgs {
   int* counter;  // [0] task counter, [2] wait-timeout error word
   unsigned long long* trace;  // optional: per task (start, dependencies done, done, smid<<48|chunk<<47|i<<16|deps)
   int hints;                  // L2 eviction-priority hints on (development switch ZOLO_DAG_HINTS)
+  const int* tmap;            // v2, optional: claim slot k -> record * nchains + chain (groups consecutive)
 };
 
 // every thread spins on a share of cnt flags; the barrier publishes them all
@@ -790,7 +791,18 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
       int tn = 0;
       if (lane == 0) tn = atomicAdd(A.counter, 1);
-      const int r = t / per_step, rem = t % per_step, ci = rem / A.ngroups, gi = rem % A.ngroups;
+      int r, ci, gi;
+      if (A.tmap) {  // chains staggered in the claim order (each chain keeps its topological order)
+        const int rc = A.tmap[t / A.ngroups];
+        r = rc / A.nchains;
+        ci = rc % A.nchains;
+        gi = t % A.ngroups;
+      } else {
+        r = t / per_step;
+        const int rem = t % per_step;
+        ci = rem / A.ngroups;
+        gi = rem % A.ngroups;
+      }
       const int* rg = A.recs + static_cast<size_t>(r) * DAG_REC;
       recp[lane] = rg[lane];
       recp[lane + 32] = rg[lane + 32];
@@ -924,7 +936,7 @@ int dag_groups(int ncols) { return (ncols + DCG - 1) / DCG; }
 
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
-                    unsigned long long* trace) {
+                    unsigned long long* trace, const int* tmap) {
   const int smem = DAG_SMEM_FIXED + (2 * DAG_REC + DAG_REC_DEPS + 8) * static_cast<int>(sizeof(int));
   static int attr_set = 0;
   if (smem > attr_set) {
@@ -953,6 +965,7 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
     return v ? std::atoi(v) : 3;
   }();
   a.hints = hints;
+  a.tmap = tmap;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int ntasks = sched.ntask * nchains * a.ngroups;
   static const int v2 = [] {
