@@ -72,6 +72,11 @@ struct DevMem {
       p = nullptr;
       throw ZoloError(ZOLO_ERR_CUDA, "cudaMalloc(" + std::to_string(b) + " B): " + cudaGetErrorString(e));
     }
+    static const bool zero = std::getenv("ZOLO_ZERO_ALLOC") != nullptr;  // (debug) zero-fill allocations
+    if (zero) {
+      cudaMemset(p, 0, b);
+      cudaDeviceSynchronize();
+    }
     bytes = b;
     return true;
   }
@@ -435,7 +440,8 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     fs[2 * j] = 0xffffffffffffffffull;  // int -1 in the low word
     fs[2 * j + 1] = infbits;
   }
-  CK(cudaMemcpy(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice, c.st));
+  CK(cudaStreamSynchronize(c.st));
 
   while (static_cast<int>(c.pole_streams.size()) < r) {
     cudaStream_t s;
@@ -464,7 +470,8 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
   c.last_ms[1] = ms;
-  CK(cudaMemcpy(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
   int fail_any = -1;
   for (int j = 0; j < r; ++j) {
     const int fi = static_cast<int>(static_cast<uint32_t>(fs[2 * j] & 0xffffffffull));
@@ -669,7 +676,8 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     fs[2 * j] = 0xffffffffffffffffull;
     fs[2 * j + 1] = infbits;
   }
-  CK(cudaMemcpy(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice, c.st));
+  CK(cudaStreamSynchronize(c.st));
   while (static_cast<int>(c.pole_streams.size()) < r) {
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -719,9 +727,11 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
   c.last_ms[1] = ms;
   int serr = 0;
-  CK(cudaMemcpy(&serr, c.sp_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(&serr, c.sp_err.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
   if (serr) throw ZoloError(ZOLO_ERR_NUMERICAL, "zolo_factorize: symbolic structure does not cover the fill");
-  CK(cudaMemcpy(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
   fail.assign(r, -1);
   min_ratio.assign(r, 0.0);
   for (int j = 0; j < r; ++j) {
@@ -1355,9 +1365,11 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   // report (gmres.hpp:31-43 merged as filter_engine.hpp:127-133)
   std::vector<double> res(ncols * q);
   std::vector<int> mcol(ncols), happy(ncols);
-  CK(cudaMemcpy(res.data(), g.res, sizeof(double) * ncols * q, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(mcol.data(), g.mcol, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(happy.data(), g.happy, sizeof(int) * ncols, cudaMemcpyDeviceToHost));
+  // (on the context stream: the legacy default stream does not order with it)
+  CK(cudaMemcpyAsync(res.data(), g.res, sizeof(double) * ncols * q, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaMemcpyAsync(mcol.data(), g.mcol, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaMemcpyAsync(happy.data(), g.happy, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
   bool all_conv = true;
   if (rep) {
     rep->iterations = 0;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -105,17 +106,24 @@ void herm_eig(int n, std::vector<S> a, std::vector<double>& w, std::vector<S>& z
     if (mag > 0.0) phi = phi * (sub[i] / mag);
     for (int r = 0; r < n; ++r) Z(r, i + 1) *= phi;
   }
-  // implicit-shift QL on (d, e), rotations applied to the columns of Z
+  // implicit-shift QL on (d, e), rotations applied to the columns of Z. Deflation:
+  // relative to the neighbouring diagonal, or absolute at eps^2 ||T|| -- a filtered
+  // block's projected B spans ~28 orders of magnitude and its bottom cluster would
+  // otherwise iterate at the underflow level (those eigenvalues are dropped by the
+  // 1e-13 mu_max cut of rayleigh_ritz anyway)
+  const double eps = std::numeric_limits<double>::epsilon();
+  double tnorm = 0.0;
+  for (int i = 0; i < n; ++i) tnorm = std::max(tnorm, std::abs(d[i]) + std::abs(e[i]) + (i ? std::abs(e[i - 1]) : 0.0));
   for (int l = 0; l < n; ++l) {
     int iter = 0;
     for (;;) {
       int m = l;
       for (; m < n - 1; ++m) {
         const double dd = std::abs(d[m]) + std::abs(d[m + 1]);
-        if (std::abs(e[m]) <= std::numeric_limits<double>::epsilon() * dd) break;
+        if (std::abs(e[m]) <= eps * dd || std::abs(e[m]) <= eps * eps * tnorm) break;
       }
       if (m == l) break;
-      if (++iter > 60) throw Fail(ZOLO_ERR_NUMERICAL, "dense_hermitian_eig: QL did not converge");
+      if (++iter > 100) throw Fail(ZOLO_ERR_NUMERICAL, "dense_hermitian_eig: QL did not converge");
       double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
       double r = std::hypot(g, 1.0);
       g = d[m] - d[l] + e[l] / (g + (g >= 0 ? r : -r));
@@ -209,7 +217,13 @@ void cuda_ck(cudaError_t e) {
 
 struct DevBuf {
   void* p = nullptr;
-  explicit DevBuf(size_t bytes) { cuda_ck(cudaMalloc(&p, bytes ? bytes : 16)); }
+  explicit DevBuf(size_t bytes) {
+    cuda_ck(cudaMalloc(&p, bytes ? bytes : 16));
+    if (std::getenv("ZOLO_ZERO_ALLOC")) {
+      cuda_ck(cudaMemset(p, 0, bytes ? bytes : 16));
+      cuda_ck(cudaDeviceSynchronize());
+    }
+  }
   ~DevBuf() { cudaFree(p); }
 };
 
@@ -241,6 +255,8 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
     std::vector<S> h(static_cast<size_t>(n) * n_ss);
     zolo::random_block(scalar, n, n_ss, seed, false, reinterpret_cast<double*>(h.data()));
     cuda_ck(cudaMemcpy(q.p, h.data(), es * n * n_ss, cudaMemcpyHostToDevice));
+    // the context's stream is non-blocking: make the legacy-stream copy complete first
+    cuda_ck(cudaDeviceSynchronize());
     for (int pass = 0; pass < 2; ++pass) {
       std::vector<S> g(static_cast<size_t>(n_ss) * n_ss), rinv;
       ck(ctx, zolo_gram_device(ctx, q.p, q.p, n_ss, n_ss, reinterpret_cast<double*>(g.data())));
@@ -337,6 +353,9 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
     for (int64_t c = 0; c < ni; ++c)  // gather the inside columns (contiguous since ritz ascends)
       cuda_ck(cudaMemcpy(static_cast<char*>(u.p) + es * n * c, static_cast<char*>(q.p) + es * n * inside[c], es * n,
                          cudaMemcpyDeviceToDevice));
+    // device-to-device cudaMemcpy returns before the copy ends and runs on the legacy
+    // stream, which the context's non-blocking stream does not wait for
+    cuda_ck(cudaDeviceSynchronize());
     ck(ctx, zolo_spmm_device(ctx, 0, u.p, t.p, ni));
     ck(ctx, zolo_spmm_device(ctx, 1, u.p, y.p, ni));
     std::vector<double> num(ni), den(ni);
