@@ -52,6 +52,7 @@ struct FactorTiles {
   uint2* mUt = nullptr;
   uint2* mDL = nullptr;
   uint2* mDU = nullptr;
+  bool swz = false;  // Lt, Ut, DinvL, DinvU stored in the swizzled sweep layout (swizzle_tiles)
 };
 
 __host__ __device__ inline size_t lt_off(int i, int d, int J) {
@@ -139,6 +140,8 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt
 // masks[t] = occupancy of tile t: bit (8 g + kb) of .x for rows 8g.. x cols 4kb..
 // (op N), of .y for the conjugate transpose (factor.cu tile_mask_kernel).
 void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks);
+// tiles permuted in place into the sweep layout: element (row, col) at col*32 + (row ^ swz(col))
+void swizzle_tiles(cudaStream_t st, cd* tiles, int64_t ntiles);
 // number of pivots (diagonal of the packed diagonal-tile LUs) with negative real part
 int64_t count_negative_pivots(cudaStream_t st, const cd* dt, int nb);
 
@@ -154,14 +157,16 @@ struct DagSched {
   int ntask = 0;
   int nslots = 0;
 };
+// presw: the chains' tiles are stored swizzled (swizzle_tiles); required by the v2 kernel
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
-                    unsigned long long* trace = nullptr, const int* tmap = nullptr);
+                    unsigned long long* trace = nullptr, const int* tmap = nullptr, bool presw = false);
 int dag_groups(int ncols);
 
 // x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass
 // x_i = DinvL_i^H w_i); x is ld x ncols, D is nbk tiles.
-void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld);
+void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld,
+                     bool swizzled = false);
 
 // One launch covers nchains x ngroups independent pipelines (owner + helpers).
 // Returns the number of resident CTAs needed (error if owners do not fit).

@@ -710,11 +710,16 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
               c.sp_ea.as<double>(), c.sp_eb.as<double>(), c.cx, sig[j].real(), sig[j].imag(),
               c.rownorm_mem.as<double>() + c.sgeom.npad * j, c.sp_pad_rows.as<int>(), c.sp_npads, ds,
               c.sp_err.as<int>(), levels ? &pd : nullptr);
-    if (mstore) {
+    if (mstore) {  // sweep factors: occupancy masks, then the swizzled sweep layout
       tile_masks(c.pole_streams[j], tiles[j].DinvL, nb, tiles[j].mDL);
       tile_masks(c.pole_streams[j], tiles[j].DinvU, nb, tiles[j].mDU);
       tile_masks(c.pole_streams[j], tiles[j].Lt, ntiles, tiles[j].mLt);
       tile_masks(c.pole_streams[j], tiles[j].Ut, ntiles, tiles[j].mUt);
+      swizzle_tiles(c.pole_streams[j], tiles[j].DinvL, nb);
+      swizzle_tiles(c.pole_streams[j], tiles[j].DinvU, nb);
+      swizzle_tiles(c.pole_streams[j], tiles[j].Lt, ntiles);
+      swizzle_tiles(c.pole_streams[j], tiles[j].Ut, ntiles);
+      tiles[j].swz = true;
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c.ev2, c.pole_streams[j]));
@@ -908,13 +913,16 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
   int* cf = fc + c.cflags_off;
   if (c.tmap_nch != c.nchains()) build_tmap(c, c.nchains());
   const bool full = first == 0 && nsub == c.nchains() && c.sp_tmap_fwd.p && c.tmap_nch == nsub;
+  const bool presw = c.tiles[0].swz;
   dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
-                  c.counter.as<int>(), 1, c.num_sms, trace, full ? c.sp_tmap_fwd.as<int>() : nullptr);
+                  c.counter.as<int>(), 1, c.num_sms, trace, full ? c.sp_tmap_fwd.as<int>() : nullptr, presw);
   dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
-                  c.counter.as<int>() + 1, 0, c.num_sms, nullptr, full ? c.sp_tmap_bwd.as<int>() : nullptr);
+                  c.counter.as<int>() + 1, 0, c.num_sms, nullptr, full ? c.sp_tmap_bwd.as<int>() : nullptr, presw);
   if (c.cx)
     for (int ci = first; ci < first + nsub; ++ci)
-      if (ci & 1) blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true, c.xbuf[ci]->as<cd>(), na, ld);
+      if (ci & 1)
+        blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true, c.xbuf[ci]->as<cd>(), na, ld,
+                        c.tiles[ci / 2].swz);
 }
 
 float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst);

@@ -614,6 +614,24 @@ int64_t count_negative_pivots(cudaStream_t st, const cd* dt, int nb) {
   return static_cast<int64_t>(h);
 }
 
+// In-place permutation of each 32 x 32 tile into the sweeps' shared-memory
+// layout, element (row, col) at col*32 + (row ^ swz(col)) (mma.cuh), so that a
+// whole tile moves with one bulk copy (cp.async.bulk) and lands conflict-free.
+__global__ void __launch_bounds__(256) swizzle_tile_kernel(cd* tiles) {
+  __shared__ cd buf[TT];
+  cd* T = tiles + static_cast<size_t>(blockIdx.x) * TT;
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) buf[e] = T[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+    const int col = e / TILE, row = e % TILE;
+    T[col * TILE + (row ^ swz(col))] = buf[e];
+  }
+}
+
+void swizzle_tiles(cudaStream_t st, cd* tiles, int64_t ntiles) {
+  if (ntiles > 0) swizzle_tile_kernel<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(tiles);
+}
+
 void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks) {
   if (ntiles > 0) tile_mask_kernel<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(tiles, masks);
 }

@@ -438,7 +438,22 @@ struct DagArgs {
   unsigned long long* trace;  // optional: per task (start, dependencies done, done, smid<<48|chunk<<47|i<<16|deps)
   int hints;                  // L2 eviction-priority hints on (development switch ZOLO_DAG_HINTS)
   const int* tmap;            // v2, optional: claim slot k -> record * nchains + chain (groups consecutive)
+  int presw;                  // tiles stored pre-swizzled (swizzle_tiles): linear / bulk copies
 };
+
+// a tile into the swizzled shared layout: permuted on the way (column-major global
+// tile) or copied linearly (tile stored pre-swizzled)
+__device__ __forceinline__ void load_tile_any(cd* s, const cd* g, unsigned long long pol, int presw) {
+  if (!presw) {
+    load_tile_sw(s, g, pol);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < TT / ST; ++q) {
+    const int e = threadIdx.x + q * ST;
+    cp_async16_cg_hint(&s[e], g + e, pol);
+  }
+}
 
 // every thread spins on a share of cnt flags; the barrier publishes them all
 __device__ __forceinline__ void wait_flags_par(const int* f, int cnt, int epoch, int* err) {
@@ -491,12 +506,12 @@ __device__ void dag_task(const DagArgs& A, const int* rec, int ci, int gi, cd* s
     const int buf = e % DNS;
     const uint2* mk_src;
     if (e < hp) {
-      load_tile_sw(tile_s(buf), ch.pre + static_cast<size_t>(i) * TT, pol_stream);
+      load_tile_any(tile_s(buf), ch.pre + static_cast<size_t>(i) * TT, pol_stream, A.presw);
       load_x32(x_s(buf), ch.src + static_cast<int64_t>(i) * TILE, ld, c0, nc, pol_stream);
       mk_src = ch.prem ? ch.prem + i : nullptr;
     } else {
       const int q = e - hp;
-      load_tile_sw(tile_s(buf), ch.off + static_cast<size_t>(dq[2 * q + 1]) * TT, pol_stream);
+      load_tile_any(tile_s(buf), ch.off + static_cast<size_t>(dq[2 * q + 1]) * TT, pol_stream, A.presw);
       mk_src = ch.offm ? ch.offm + dq[2 * q + 1] : nullptr;
     }
     if (threadIdx.x == 0) {
@@ -697,6 +712,18 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
 __device__ __forceinline__ void mbar_arrive_cpasync(unsigned long long* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// bulk (TMA-engine) global -> shared copy completing `bytes` on the mbarrier's transaction count
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                          unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(ST) : "memory"); }
 
 // lane 0 spins on *f >= epoch (bounded), then the warp reconverges
@@ -728,7 +755,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
   for (int q = threadIdx.x; q < A.nchains; q += blockDim.x) chs[q] = A.chains[q];
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST2; ++s) {
-      mbar_init(full + s, 33);   // 32 producer lanes' copies + the producer's metadata arrive
+      mbar_init(full + s, 1);    // the producer's arrive (+ the stage's bulk-copy bytes)
       mbar_init(empty + s, ST / 32);
     }
   }
@@ -744,25 +771,20 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
                        int nc, unsigned long long pol, int last, int i, int ci, int gi, int out) {
       const int s = g % NST2, round = g / NST2;
       mbar_wait(empty + s, (round & 1) ^ 1);
-      if (tile) {
-        cd* ts = tile_s(s);
-#pragma unroll 4
-        for (int k = 0; k < TILE; ++k) {  // element (row = lane, col = k)
-          cp_async16_cg_hint(&ts[k * TILE + (lane ^ swz(k))], tile + k * TILE + lane, pol_stream);
-        }
-      }
+      // bulk copies: the (pre-swizzled) tile in one, the block's columns one per lane
+      const unsigned bytes = (tile ? static_cast<unsigned>(TT * sizeof(cd)) : 0u) +
+                             static_cast<unsigned>(nc) * TILE * static_cast<unsigned>(sizeof(cd));
+      if (lane == 0) mbar_expect_tx(full + s, bytes);
+      __syncwarp();
+      if (tile && lane == 0) bulk_copy(tile_s(s), tile, TT * sizeof(cd), full + s, pol_stream);
       cd* xs = x_s(s);
-#pragma unroll 4
-      for (int c = 0; c < DCG; ++c) {
-        if (c < nc)
-          cp_async16_cg_hint(&xs[c * XPAD + lane], blk + lane + (c0 + c) * stride, pol);
-        else
-          xs[c * XPAD + lane] = mk(0.0, 0.0);
-      }
+      if (lane < nc)
+        bulk_copy(xs + lane * XPAD, blk + (c0 + lane) * stride, TILE * sizeof(cd), full + s, pol);
+      else
+        for (int r = 0; r < TILE; ++r) xs[lane * XPAD + r] = mk(0.0, 0.0);
       uint2 mw = make_uint2(0xffffffffu, 0xffffffffu);
       if (mask && lane == 0) mw = *mask;
       __syncwarp();
-      mbar_arrive_cpasync(full + s);
       if (lane == 0) {
         Meta2 m;
         m.kind = kind;
@@ -908,12 +930,22 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
 }
 
 // x_i <- op(D_i) x_i per (block row, 16-column group): the adjoint post-pass.
-__global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
+__global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd* x, int ncols, int64_t ld,
+                                                      int swizzled) {
   __shared__ __align__(16) cd ds[TILE_S];
   __shared__ __align__(16) cd xs[XS];
   const int i = blockIdx.x, c0 = blockIdx.y * CG, nc = min(CG, ncols - c0);
   const Frag f = frag();
-  load_tile(ds, D + static_cast<size_t>(i) * TT);
+  if (swizzled) {  // undo the sweep layout into the padded column-major copy
+    const cd* g = D + static_cast<size_t>(i) * TT;
+#pragma unroll
+    for (int q = 0; q < TT / ST; ++q) {
+      const int e = threadIdx.x + q * ST, col = e / TILE, row = e % TILE;
+      cp_async16_cg(&ds[col * APAD + row], g + col * TILE + (row ^ swz(col)));
+    }
+  } else {
+    load_tile(ds, D + static_cast<size_t>(i) * TT);
+  }
   load_x(xs, x + static_cast<int64_t>(i) * TILE, ld, c0, nc);
   cp_async_commit();
   cp_async_wait<0>();
@@ -928,15 +960,16 @@ __global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd
 
 }  // namespace
 
-void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
-  if (ncols > 0) blockdiag_kernel<<<dim3(nb, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld);
+void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld, bool swizzled) {
+  if (ncols > 0)
+    blockdiag_kernel<<<dim3(nb, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld, swizzled ? 1 : 0);
 }
 
 int dag_groups(int ncols) { return (ncols + DCG - 1) / DCG; }
 
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
-                    unsigned long long* trace, const int* tmap) {
+                    unsigned long long* trace, const int* tmap, bool presw) {
   const int smem = DAG_SMEM_FIXED + (2 * DAG_REC + DAG_REC_DEPS + 8) * static_cast<int>(sizeof(int));
   static int attr_set = 0;
   if (smem > attr_set) {
@@ -966,13 +999,14 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   }();
   a.hints = hints;
   a.tmap = tmap;
+  a.presw = presw ? 1 : 0;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int ntasks = sched.ntask * nchains * a.ngroups;
   static const int v2 = [] {
     const char* v = std::getenv("ZOLO_DAG_V2");
     return v ? std::atoi(v) : 1;
   }();
-  if (v2 && nchains <= DAG2_CHAINS && !trace) {
+  if (v2 && presw && nchains <= DAG2_CHAINS && !trace) {
     static bool attr2 = false;
     if (!attr2) {
       cudaFuncSetAttribute(dag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DAG2_SMEM);
