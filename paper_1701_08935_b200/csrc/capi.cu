@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -494,9 +495,23 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
 
 // Ordering + block symbolic analysis + sweep schedules + the device pencil and
 // scatter lists in the factor ordering: everything shift-independent.
+// (development) ZOLO_SETUP_TIMES=1 prints the host setup phases
+struct SetupClock {
+  bool on = std::getenv("ZOLO_SETUP_TIMES") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-22s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
+  SetupClock clk;
   const int64_t n = c.n;
   Union u = union_pattern(c);
+  clk.mark("union pattern");
   std::vector<std::vector<int64_t>> nodes;
   if (perm_in) {
     std::vector<char> seen(n, 0);
@@ -510,8 +525,10 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   } else {
     nd_order(n, u.rp.data(), u.ci.data(), c.nd_leaf, nodes);
   }
+  clk.mark("nested dissection");
   BlockStructure bs;
   block_symbolic(n, u.rp.data(), u.ci.data(), nodes, TILE, bs);
+  clk.mark("block symbolic");
   require(bs.ntiles < (int64_t(1) << 31) && bs.npad < (int64_t(1) << 31), "zolo_factorize: structure too large");
   const int nb = static_cast<int>(bs.nb);
   std::vector<int> pos(n);
@@ -595,6 +612,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb};
     c.sp_nslots = std::max(sf, sb);
   }
+  clk.mark("sweep schedules");
 
   const int64_t nnz = static_cast<int64_t>(u.ci.size());
   std::vector<int> er(nnz), ec(nnz), pads;
@@ -613,11 +631,14 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   c.sp_nnz = nnz;
   c.sp_npads = static_cast<int>(pads.size());
   upload_device_pencil(c, bs.inv, pos);
+  clk.mark("device pencil");
   factor_plan(bs, c.fplan);
+  clk.mark("factor plan");
   upload(c.fp_cols, c.fplan.cols, c.st);
   upload(c.fp_pan, c.fplan.pan, c.st);
   upload(c.fp_tgt, c.fplan.tgt, c.st);
   upload(c.fp_con, c.fplan.con, c.st);
+  clk.mark("plan upload");
   c.sym_ready = true;
 }
 
