@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cstdlib>
 #include <cmath>
 #include <complex>
@@ -242,6 +243,16 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
   if (r <= 0) r = zolo::choose_order(gaps, std::max(tol * 1e-2, 1e-16));
 
   const auto t0 = clock::now();
+  // the seeded start block (random_gaussian, dense.hpp:193-208) does not depend on the
+  // factorization: generate it on a host thread while the factors are built
+  std::vector<S> h0(static_cast<size_t>(n) * n_ss);
+  std::thread rng([&] { zolo::random_block(scalar, n, n_ss, seed, false, reinterpret_cast<double*>(h0.data())); });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{rng};
   std::vector<double> design(ZOLO_DESIGN_LEN(r));
   zolo::build_filter_design(gaps, r, design.data());
   ck(ctx, zolo_filter_create(ctx, n, scalar, a_rp, a_ci, a_v, b_rp, b_ci, b_v, design.data(), r, nullptr));
@@ -252,9 +263,8 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
   const size_t es = sizeof(S);
   DevBuf q(es * n * n_ss), y(es * n * n_ss), t(es * n * n_ss), u(es * n * n_ss);
   {  // Q0: seeded Gaussian block, orthonormalised (CholQR2 == MGS's Q up to rounding)
-    std::vector<S> h(static_cast<size_t>(n) * n_ss);
-    zolo::random_block(scalar, n, n_ss, seed, false, reinterpret_cast<double*>(h.data()));
-    cuda_ck(cudaMemcpy(q.p, h.data(), es * n * n_ss, cudaMemcpyHostToDevice));
+    rng.join();
+    cuda_ck(cudaMemcpy(q.p, h0.data(), es * n * n_ss, cudaMemcpyHostToDevice));
     // the context's stream is non-blocking: make the legacy-stream copy complete first
     cuda_ck(cudaDeviceSynchronize());
     for (int pass = 0; pass < 2; ++pass) {
