@@ -767,6 +767,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
     int g = 0;
     // one ring entry: tile (optional) + a 32 x 32 block with column stride `stride`
+    int cur_t = 0;  // claim index of the task being produced (trace)
     auto produce = [&](int kind, int sign, const cd* tile, const uint2* mask, const cd* blk, int64_t stride, int c0,
                        int nc, unsigned long long pol, int last, int i, int ci, int gi, int out) {
       const int s = g % NST2, round = g / NST2;
@@ -797,6 +798,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         m.gi = gi;
         m.out = out;
         m.nc = nc;
+        m.pad0 = cur_t;
         meta[s] = m;
         mbar_arrive(full + s);
       }
@@ -813,6 +815,10 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
       int tn = 0;
       if (lane == 0) tn = atomicAdd(A.counter, 1);
+      cur_t = t;
+      unsigned long long* trp = A.trace ? A.trace + DAG_TRACE_WORDS * static_cast<size_t>(t) : nullptr;
+      unsigned long long wsum = 0;
+      if (trp && lane == 0) trp[0] = gtimer();
       int r, ci, gi;
       if (A.tmap) {  // chains staggered in the claim order (each chain keeps its topological order)
         const int rc = A.tmap[t / A.ngroups];
@@ -854,7 +860,11 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         const unsigned prdy =
             __ballot_sync(0xffffffffu, p0 + lane >= pc || ld_acquire(cflags + pa + p0 + lane) >= A.epoch);
         for (int p = p0; p < pc && p < p0 + 32; ++p) {
-          if (!((prdy >> (p - p0)) & 1u)) warp_wait_flag(cflags + pa + p, A.epoch, A.counter + 2);
+          if (!((prdy >> (p - p0)) & 1u)) {
+            const unsigned long long tw = trp ? gtimer() : 0;
+            warp_wait_flag(cflags + pa + p, A.epoch, A.counter + 2);
+            if (trp) wsum += gtimer() - tw;
+          }
           ++e;
           produce(1, 1, nullptr, nullptr, ch.cbuf + static_cast<int64_t>(pa + p) * TILE, A.ldp, c0, nc, pol_stream,
                   e == nent, i, ci, gi, out);
@@ -862,12 +872,20 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
       for (int q = 0; q < nd; ++q) {
         const int j = recp[DAG_REC_HDR + 2 * q], tid = recp[DAG_REC_HDR + 2 * q + 1];
-        if (!((dep_ready >> q) & 1u)) warp_wait_flag(flags + j, A.epoch, A.counter + 2);
+        if (!((dep_ready >> q) & 1u)) {
+          const unsigned long long tw = trp ? gtimer() : 0;
+          warp_wait_flag(flags + j, A.epoch, A.counter + 2);
+          if (trp) wsum += gtimer() - tw;
+        }
         ++e;
         produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, ch.offm ? ch.offm + tid : nullptr,
                 ch.dst + static_cast<int64_t>(j) * TILE, A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
       }
       __syncwarp();
+      if (trp && lane == 0) {
+        trp[4] = wsum;
+        trp[5] = gtimer();
+      }
       t = __shfl_sync(0xffffffffu, tn, 0);
     }
     return;
@@ -876,6 +894,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
   const Frag f = frag();
   Acc8 acc;
   acc8_zero(acc);
+  int ntiles_task = 0;  // (trace) tile products of the current task
   for (int g = 0;; ++g) {
     const int s = g % NST2, round = g / NST2;
     mbar_wait(full + s, round & 1);
@@ -883,6 +902,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     if (m.kind == 2) break;
     const Chain& ch = chs[m.ci];
     const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
+    ntiles_task += m.kind == 0;
     if (m.kind == 0) {
       mma_tile2(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
     } else {
@@ -924,7 +944,16 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       if (threadIdx.x == 0) {
         const size_t cgi = static_cast<size_t>(m.ci) * A.ngroups + m.gi;
         st_release(chunk ? A.cflags + cgi * A.nslots + m.out : A.flags + cgi * A.s.nb + m.i, A.epoch);
+        if (A.trace) {
+          unsigned long long* trc = A.trace + DAG_TRACE_WORDS * static_cast<size_t>(m.pad0);
+          unsigned smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          trc[2] = gtimer();
+          trc[3] = (static_cast<unsigned long long>(smid) << 48) | (static_cast<unsigned long long>(chunk) << 47) |
+                   (static_cast<unsigned long long>(m.i) << 16) | static_cast<unsigned>(ntiles_task);
+        }
       }
+      ntiles_task = 0;
     }
   }
 }
@@ -1006,7 +1035,7 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
     const char* v = std::getenv("ZOLO_DAG_V2");
     return v ? std::atoi(v) : 1;
   }();
-  if (v2 && presw && nchains <= DAG2_CHAINS && !trace) {
+  if (v2 && presw && nchains <= DAG2_CHAINS) {
     static bool attr2 = false;
     if (!attr2) {
       cudaFuncSetAttribute(dag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DAG2_SMEM);
