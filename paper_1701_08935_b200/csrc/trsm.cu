@@ -439,6 +439,7 @@ struct DagArgs {
   int hints;                  // L2 eviction-priority hints on (development switch ZOLO_DAG_HINTS)
   const int* tmap;            // v2, optional: claim slot k -> record * nchains + chain (groups consecutive)
   int presw;                  // tiles stored pre-swizzled (swizzle_tiles): linear / bulk copies
+  int l2pf;                   // v2: L2 prefetch of the next task's tiles / blocks (ZOLO_DAG_L2PF)
 };
 
 // a tile into the swizzled shared layout: permuted on the way (column-major global
@@ -724,6 +725,9 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(ST) : "memory"); }
 
 // lane 0 spins on *f >= epoch (bounded), then the warp reconverges
@@ -815,6 +819,37 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
       int tn = 0;
       if (lane == 0) tn = atomicAdd(A.counter, 1);
+      tn = __shfl_sync(0xffffffffu, tn, 0);
+      if (A.l2pf && tn < ntasks) {
+        // warm L2 with the next task's tiles and solution blocks while this one streams
+        int rn, cin, gin;
+        if (A.tmap) {
+          const int rc = A.tmap[tn / A.ngroups];
+          rn = rc / A.nchains;
+          cin = rc % A.nchains;
+          gin = tn % A.ngroups;
+        } else {
+          rn = tn / per_step;
+          cin = (tn % per_step) / A.ngroups;
+          gin = (tn % per_step) % A.ngroups;
+        }
+        const int* rgn = A.recs + static_cast<size_t>(rn) * DAG_REC;
+        const int in = rgn[0], ndn = rgn[1], outn = rgn[4];
+        const Chain& chn = chs[cin];
+        const int c0n = gin * DCG, ncn = min(DCG, A.ncols - c0n);
+        const cd* tsrc = nullptr;
+        const cd* xsrc = nullptr;
+        if (lane < ndn) {
+          tsrc = chn.off + static_cast<size_t>(rgn[DAG_REC_HDR + 2 * lane + 1]) * TT;
+          xsrc = chn.dst + static_cast<int64_t>(rgn[DAG_REC_HDR + 2 * lane]) * TILE;
+        } else if (lane == ndn && outn < 0) {
+          tsrc = chn.pre ? chn.pre + static_cast<size_t>(in) * TT : nullptr;
+          xsrc = chn.src + static_cast<int64_t>(in) * TILE;
+        }
+        if (tsrc) l2_prefetch(tsrc, TT * sizeof(cd));
+        if (xsrc)
+          for (int c = 0; c < ncn; ++c) l2_prefetch(xsrc + (c0n + c) * A.ld, TILE * sizeof(cd));
+      }
       cur_t = t;
       unsigned long long* trp = A.trace ? A.trace + DAG_TRACE_WORDS * static_cast<size_t>(t) : nullptr;
       unsigned long long wsum = 0;
@@ -886,7 +921,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         trp[4] = wsum;
         trp[5] = gtimer();
       }
-      t = __shfl_sync(0xffffffffu, tn, 0);
+      t = tn;
     }
     return;
   }
@@ -1029,6 +1064,11 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   a.hints = hints;
   a.tmap = tmap;
   a.presw = presw ? 1 : 0;
+  static const int l2pf = [] {
+    const char* v = std::getenv("ZOLO_DAG_L2PF");  // off: measured slower (the producer is on the path)
+    return v ? std::atoi(v) : 0;
+  }();
+  a.l2pf = l2pf;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int ntasks = sched.ntask * nchains * a.ngroups;
   static const int v2 = [] {
