@@ -817,9 +817,9 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         produce(2, 0, nullptr, nullptr, A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
         break;
       }
-      int tn = 0;
-      if (lane == 0) tn = atomicAdd(A.counter, 1);
-      tn = __shfl_sync(0xffffffffu, tn, 0);
+      int tn_raw = 0;
+      if (lane == 0) tn_raw = atomicAdd(A.counter, 1);  // consumed late unless the L2 prefetch needs it
+      const int tn = A.l2pf ? __shfl_sync(0xffffffffu, tn_raw, 0) : 0;
       if (A.l2pf && tn < ntasks) {
         // warm L2 with the next task's tiles and solution blocks while this one streams
         int rn, cin, gin;
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         trp[4] = wsum;
         trp[5] = gtimer();
       }
-      t = tn;
+      t = A.l2pf ? tn : __shfl_sync(0xffffffffu, tn_raw, 0);
     }
     return;
   }
