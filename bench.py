@@ -305,7 +305,7 @@ def main():
         "dtype": "c128" if cx else "f64", "data": "synthetic (seeded generator, BASELINE config shape)",
         "config": {"workload": f"{args.config}: 3D 7-point Laplacian 32^3 + U[0,1] potential, SPD mass B, N={n}, "
                                f"r={r} (p={2 * r} poles), n_v={nv}, gmres_tol=1e-12, 64-eigenvalue window",
-                   "N": n, "n_v": nv, "r": r, "ordering": "nested dissection (leaf 256), block-sparse 32x32 tiles",
+                   "N": n, "n_v": nv, "r": r, "ordering": "nested dissection (leaf 192), block-sparse 32x32 tiles",
                    "factor_tiles_per_pole": sp["offdiag_tiles"] + sp["block_rows"],
                    "l2": "factors > L2 (no flush needed)",
                    "parallelism": f"poles x{ws} (NCCL all-reduce per G application)" if poles

@@ -110,7 +110,7 @@ int zolo_factorize(zolo_ctx* ctx, const int64_t* perm, zolo_factor_stats* stats)
 
 /* Ordering / factor layout used by zolo_factorize:
  *   ZOLO_ORDER_ND   (default) nested dissection (recursive BFS-level bisection,
- *                   leaves of <= nd_leaf rows ordered by RCM; default 256,
+ *                   leaves of <= nd_leaf rows ordered by RCM; default 192,
  *                   nd_leaf <= 0 keeps the current value), block-sparse
  *                   32x32-tile factors, DAG-scheduled sweeps -- short
  *                   dependency chains;

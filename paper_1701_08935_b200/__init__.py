@@ -230,7 +230,7 @@ class InertiaCounter:
     A - sigma B under the ND ordering has as many negative pivots as the pencil
     has eigenvalues below sigma (B positive definite)."""
 
-    def __init__(self, pencil, is_complex: Optional[bool] = None, device: int = 0, nd_leaf: int = 256):
+    def __init__(self, pencil, is_complex: Optional[bool] = None, device: int = 0, nd_leaf: int = 192):
         L = lib()
         n, a, b = pencil
         cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
@@ -289,7 +289,7 @@ class FilterOperator:
     """
 
     def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None,
-                 ordering: str = "nd", nd_leaf: int = 256, shard=None, solve: str = "direct", hybrid_pole: int = 0,
+                 ordering: str = "nd", nd_leaf: int = 192, shard=None, solve: str = "direct", hybrid_pole: int = 0,
                  inner_tol: float = 1e-14, inner_max: int = 256):
         L = lib()
         n, a, b = pencil

@@ -148,7 +148,7 @@ struct zolo_ctx {
 
   // block-sparse (nested dissection) factor path
   int order_mode = ZOLO_ORDER_ND;
-  int64_t nd_leaf = 256;
+  int64_t nd_leaf = 192;
   bool sparse = false;
   SpGeom sgeom;
   std::vector<int> sp_col_cnt;
