@@ -580,7 +580,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   {  // claim-ordered sweep schedules: wide block rows split into chunk tasks
     static const int near = std::min(std::max(env_int("ZOLO_DAG_NEAR", 4), 0), DAG_REC_DEPS - 1),
                      chunk = std::min(std::max(env_int("ZOLO_DAG_CHUNK", 16), 1), DAG_REC_DEPS - near),
-                     order = env_int("ZOLO_DAG_ORDER", 1);
+                     order = env_int("ZOLO_DAG_ORDER", 3);
     // self-contained task records: header + the (j, tile id) pairs in processing order
     auto records = [&](const std::vector<DagTask>& ts, bool fwd) {
       std::vector<int> rec(ts.size() * DAG_REC, 0);

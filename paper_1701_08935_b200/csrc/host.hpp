@@ -54,9 +54,9 @@ struct DagTask {
 // Rows with more than near + chunk dependencies keep the `near` latest in
 // the row task; the rest go to chunks of <= chunk dependencies, each claimed
 // right after the row task of its latest dependency. order: 0 = that
-// positional order, 1 = by earliest start time, 2 = by longest path to the
-// sweep's end (both weighted by tile products; both topological). Returns
-// the slot count.
+// positional order, 1 = by earliest start time (EST), 2 = by longest path to
+// the sweep's end (BL), >= 3: EST - (order - 2)/8 * BL (all weighted by tile
+// products; all topological). Returns the slot count.
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
                  int near, int order, std::vector<DagTask>& tasks);
 void rcm_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm);

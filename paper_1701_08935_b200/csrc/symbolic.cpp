@@ -407,15 +407,16 @@ int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<
     cost[t] = (k.qb - k.qa) + 0.25 * k.pc + 2.0;
   }
   std::vector<double> key(nt, 0.0);
-  if (order == 1) {  // earliest start time (ascending)
-    for (int64_t t = 0; t < nt; ++t)
-      for (int64_t d : deps[t]) key[t] = std::max(key[t], key[d] + cost[d]);
-  } else {  // longest path to the end of the sweep (descending)
-    std::vector<double> bl(cost);
-    for (int64_t t = nt - 1; t >= 0; --t)
-      for (int64_t d : deps[t]) bl[d] = std::max(bl[d], cost[d] + bl[t]);
-    for (int64_t t = 0; t < nt; ++t) key[t] = -bl[t];
-  }
+  // earliest start time (EST) and longest path to the end (bottom level, BL); key = EST - lambda * BL
+  // is topological for every lambda >= 0: lambda = 0 pure EST (order 1), order 2 pure BL,
+  // order >= 3 a blend with lambda = (order - 2) / 8
+  std::vector<double> est(nt, 0.0), bl(cost);
+  for (int64_t t = 0; t < nt; ++t)
+    for (int64_t d : deps[t]) est[t] = std::max(est[t], est[d] + cost[d]);
+  for (int64_t t = nt - 1; t >= 0; --t)
+    for (int64_t d : deps[t]) bl[d] = std::max(bl[d], cost[d] + bl[t]);
+  const double lambda = order >= 3 ? (order - 2) / 8.0 : 0.0;
+  for (int64_t t = 0; t < nt; ++t) key[t] = order == 2 ? -bl[t] : est[t] - lambda * bl[t];
   std::vector<int64_t> perm(nt);
   for (int64_t t = 0; t < nt; ++t) perm[t] = t;
   std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
