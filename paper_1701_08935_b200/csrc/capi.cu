@@ -581,6 +581,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     static const int near = std::min(std::max(env_int("ZOLO_DAG_NEAR", 4), 0), DAG_REC_DEPS - 1),
                      chunk = std::min(std::max(env_int("ZOLO_DAG_CHUNK", 16), 1), DAG_REC_DEPS - near),
                      order = env_int("ZOLO_DAG_ORDER", 3);
+    static const bool chain = env_int("ZOLO_DAG_CHAIN", 0) != 0;  // chained partials: measured slower
     // self-contained task records: header + the (j, tile id) pairs in processing order
     auto records = [&](const std::vector<DagTask>& ts, bool fwd) {
       std::vector<int> rec(ts.size() * DAG_REC, 0);
@@ -601,8 +602,8 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
       return rec;
     };
     std::vector<DagTask> tf, tb;
-    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf);
-    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb);
+    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf, chain);
+    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb, chain);
     upload(c.sp_sched_fwd, records(tf, true), c.st);
     upload(c.sp_sched_bwd, records(tb, false), c.st);
     c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), static_cast<int>(tf.size()), sf};

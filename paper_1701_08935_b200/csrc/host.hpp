@@ -57,8 +57,10 @@ struct DagTask {
 // positional order, 1 = by earliest start time (EST), 2 = by longest path to
 // the sweep's end (BL), >= 3: EST - (order - 2)/8 * BL (all weighted by tile
 // products; all topological). Returns the slot count.
+// chain_partials: chunk c adds chunk c-1's partial (pa = its slot, pc = 1) and the row task
+// adds only the last one -- one add-block on the row's critical path instead of one per chunk.
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
-                 int near, int order, std::vector<DagTask>& tasks);
+                 int near, int order, std::vector<DagTask>& tasks, bool chain_partials = false);
 void rcm_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm);
 int64_t bandwidth_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);
 int64_t profile_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);

@@ -353,7 +353,7 @@ void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
 }
 
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
-                 int near, int order, std::vector<DagTask>& tasks) {
+                 int near, int order, std::vector<DagTask>& tasks, bool chain_partials) {
   if (chunk < 1 || near < 0) throw std::invalid_argument("dag_schedule: chunk >= 1, near >= 0");
   // processing position of block row j in the sweep (forward: j, backward: nb-1-j)
   auto position = [&](int64_t j) { return fwd ? j : nb - 1 - j; };
@@ -370,14 +370,23 @@ int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<
     if (nd > near + chunk) {
       const int far = nd - near;
       const int nchunk = (far + chunk - 1) / chunk;
+      const int first_slot = slots;
       for (int c = 0, q0 = 0; c < nchunk; ++c) {
         const int q1 = static_cast<int>((static_cast<int64_t>(far) * (c + 1)) / nchunk);  // balanced cut
         const int64_t last = position(dep(q1 - 1));
-        after[last].push_back(DagTask{static_cast<int>(i), q0, q1, 0, 0, slots++});
+        // chained partials: chunk c also adds chunk c-1's partial, so the row task adds one block
+        const int pa = chain_partials && c > 0 ? first_slot + c - 1 : 0;
+        const int pc = chain_partials && c > 0 ? 1 : 0;
+        after[last].push_back(DagTask{static_cast<int>(i), q0, q1, pa, pc, slots++});
         q0 = q1;
       }
       row.qa = far;
-      row.pc = nchunk;
+      if (chain_partials) {
+        row.pa = first_slot + nchunk - 1;
+        row.pc = 1;
+      } else {
+        row.pc = nchunk;
+      }
     }
     rows[s] = row;
   }
