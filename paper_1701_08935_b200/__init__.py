@@ -266,6 +266,12 @@ class InertiaCounter:
             s = float(sigma) + (k + 1) * 1e-12 * max(1.0, abs(float(sigma)))
         _check(self._h, st)
 
+    def structure(self):
+        """Block structure of the ND factors (zolo_sweep_profile; after a count)."""
+        out = np.zeros(8, dtype=np.int64)
+        _check(self._h, lib().zolo_sweep_profile(self._h, _ptr(out)))
+        return dict(block_rows=int(out[0]), offdiag_tiles=int(out[1]), critical_path=int(out[5]))
+
     def count_in(self, a: float, b: float) -> int:
         """Eigenvalues in (a, b) = count_below(b) - count_below(a)."""
         return self.count_below(b) - self.count_below(a)

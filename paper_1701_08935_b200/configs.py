@@ -101,6 +101,85 @@ def tight_binding_pencil(k: int, seed: int = 3, disorder: float = 1.5, overlap: 
     return (n, to_csr(a, True), b)
 
 
+def _gaussian(seed: int, n: int) -> np.ndarray:
+    """n standard normal deviates by Box-Muller over the seeded uniform stream."""
+    u = uniform(seed, 2 * ((n + 1) // 2))
+    u1 = np.maximum(u[0::2], 2.0 ** -53)
+    r = np.sqrt(-2.0 * np.log(u1))
+    z = np.concatenate([r * np.cos(2 * np.pi * u[1::2]), r * np.sin(2 * np.pi * u[1::2])])
+    return z[:n]
+
+
+def chemistry_pencil(k: int = 20, seed: int = 4, block: int = 13, cutoff: float = 2.5, jitter: float = 0.15,
+                     overlap: float = 0.1):
+    """Config 4: a chemistry-shaped block-sparse Hermitian pencil (BSR, `block` x `block`
+    dense blocks per atom). k^3 atoms on a cubic lattice jittered by U[-jitter, jitter]
+    spacings; atoms closer than `cutoff` spacings are coupled. A: off-diagonal blocks
+    complex Gaussian x exp(-distance), Hermitian-symmetrised, diagonal blocks Hermitian
+    Gaussian. B: the same pattern, off-diagonal blocks overlap x exp(-distance) x complex
+    Gaussian (Hermitian), plus a diagonal making every row strictly diagonally dominant
+    (so B is Hermitian positive definite). Returns the full-pattern CSR pencil
+    (io.bsr_to_csr) of order k^3 * block."""
+    from . import io as zio
+
+    na = k ** 3
+    g = np.stack(np.meshgrid(np.arange(k), np.arange(k), np.arange(k), indexing="ij"), -1).reshape(-1, 3)
+    pos = g + jitter * (2.0 * uniform(seed, 3 * na).reshape(na, 3) - 1.0)
+    # neighbour pairs within the cutoff (cell list over the lattice: |di| <= ceil(cutoff) + 1)
+    reach = int(np.ceil(cutoff)) + 1
+    pairs_i, pairs_j, dist = [], [], []
+    for dx in range(-reach, reach + 1):
+        for dy in range(-reach, reach + 1):
+            for dz in range(0, reach + 1):
+                if dz == 0 and (dy < 0 or (dy == 0 and dx <= 0)):
+                    continue  # each unordered pair once
+                sh = g + np.array([dx, dy, dz])
+                ok = np.all((sh >= 0) & (sh < k), axis=1)
+                i = np.nonzero(ok)[0]
+                j = (sh[ok, 0] * k + sh[ok, 1]) * k + sh[ok, 2]
+                d = np.linalg.norm(pos[j] - pos[i], axis=1)
+                m = d < cutoff
+                pairs_i.append(i[m])
+                pairs_j.append(j[m])
+                dist.append(d[m])
+    pi, pj, pd = (np.concatenate(x) for x in (pairs_i, pairs_j, dist))
+    npairs, bs2 = len(pi), block * block
+    z = _gaussian(seed + 1, 2 * bs2 * (npairs + na) + 2 * bs2 * npairs)
+    za = (z[0:2 * bs2 * npairs:2] + 1j * z[1:2 * bs2 * npairs:2]).reshape(npairs, block, block)
+    zd = z[2 * bs2 * npairs:2 * bs2 * (npairs + na)]
+    zd = (zd[0::2] + 1j * zd[1::2]).reshape(na, block, block)
+    zb = z[2 * bs2 * (npairs + na):]
+    zb = (zb[0::2] + 1j * zb[1::2]).reshape(npairs, block, block)
+    off_a = za * np.exp(-pd)[:, None, None]
+    off_b = overlap * zb * np.exp(-pd)[:, None, None]
+    diag_a = 0.5 * (zd + np.conj(np.transpose(zd, (0, 2, 1))))
+    # block rows: (i, j) and (j, i) = conjugate transpose, plus the diagonal blocks
+    rows = np.concatenate([pi, pj, np.arange(na)])
+    cols = np.concatenate([pj, pi, np.arange(na)])
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    ba = np.concatenate([off_a, np.conj(np.transpose(off_a, (0, 2, 1))), diag_a])[order]
+    bb_off = np.concatenate([off_b, np.conj(np.transpose(off_b, (0, 2, 1))), np.zeros((na, block, block))])
+    # strict diagonal dominance of B: diagonal = 1 + sum_j |B_ij| over the row
+    rowsum = np.zeros((na, block))
+    np.add.at(rowsum, np.concatenate([pi, pj]), np.abs(np.concatenate([off_b, np.conj(np.transpose(off_b, (0, 2, 1)))])).sum(axis=2))
+    dd = np.zeros((na, block, block), dtype=np.complex128)
+    dd[:, np.arange(block), np.arange(block)] = 1.0 + rowsum
+    bb_off[2 * npairs:] = dd
+    bb = bb_off[order]
+    indptr = np.zeros(na + 1, dtype=np.int64)
+    np.add.at(indptr, rows + 1, 1)
+    indptr = np.cumsum(indptr)
+    a_csr = zio.bsr_to_csr(na, block, indptr, cols, ba, True)
+    b_csr = zio.bsr_to_csr(na, block, indptr, cols, bb, True)
+    return (na * block, a_csr, b_csr)
+
+
+def multi_gpu_pencil(k: int = 64, seed: int = 5):
+    """Config 5: tight binding as config 3 on a k^3 periodic grid, disorder U[-2, 2], B = I."""
+    return tight_binding_pencil(k, seed=seed, disorder=2.0, with_b=False)
+
+
 def window_by_dense_eigs(pencil, lo: int, count: int):
     """Gap endpoints isolating eigenvalues lo..lo+count-1 (dense; small pencils)."""
     from scipy.linalg import eigh
@@ -121,6 +200,12 @@ WINDOWS = {
     # the 128 eigenvalues of tight_binding_pencil(48, seed=3, disorder=1.5) around 0
     "cfg3": {"gaps": [-0.004303539789179923, -0.004240734865379634, 0.004296055916711339, 0.004322829099328374],
              "count": 128},
+    # tools/find_window_gpu.py cfg4 0.0 200: chemistry_pencil(20, seed=4), 200 eigenvalues around 0
+    "cfg4": {"gaps": [-0.0014473551429546204, -0.0014319087193143789, 0.0014380021788383598, 0.0014440721712162489],
+             "count": 200},
+    # tools/find_window_gpu.py cfg5 0.0 256: multi_gpu_pencil(64, seed=5), 256 eigenvalues around 0
+    "cfg5": {"gaps": [-0.004444281498217607, -0.004424367355750291, 0.004403209645170138, 0.004455014820632642],
+             "count": 256},
 }
 
 
@@ -135,4 +220,10 @@ def config(name: str):
     if name == "cfg3":
         w = WINDOWS["cfg3"]
         return tight_binding_pencil(48, seed=3, disorder=1.5), True, w["gaps"], 8, 192, w["count"]
+    if name == "cfg4":  # ~35 GB of factors per pole: all 8 poles need pole sharding (8 GPUs) or the hybrid solve
+        w = WINDOWS["cfg4"]
+        return chemistry_pencil(20, seed=4), True, w["gaps"], 8, 256, w["count"]
+    if name == "cfg5":
+        w = WINDOWS["cfg5"]
+        return multi_gpu_pencil(64, seed=5), True, w["gaps"], 8, 320, w["count"]
     raise KeyError(name)

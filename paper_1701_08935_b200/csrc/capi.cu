@@ -1847,13 +1847,107 @@ int zolo_apply_g(zolo_ctx* c, const double* v, double* gv, int64_t ncols) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Device bytes of the per-column workspace (vectors, Krylov basis, GMRES state) of one column.
+double bytes_per_column(zolo_ctx& c, int maxit) {
+  const double ld = static_cast<double>(c.geom.npad), es = static_cast<double>(c.es());
+  const int nch = c.nchains(), q = 2 * c.r;
+  const double crows = c.sparse ? static_cast<double>(TILE) * std::max(c.sp_nslots, 1) : ld;
+  const double nchunk = std::ceil(ld / CHUNK);
+  double b = c.n * es + ld * (3 * es + 16 + 16.0 * nch + es * (maxit + 2)) + 16.0 * nch * crows;
+  b += es * (maxit + 1) * maxit + 16.0 * q * (maxit * maxit + 4.0 * maxit + 1) + 2 * es * nchunk * (maxit + 1);
+  if (c.hybrid) b += 16.0 * ld * (c.hy_max + 4) + 16.0 * (c.r - 1) * c.hy_max * c.hy_max;
+  return b;
+}
+
+void release_workspace(zolo_ctx& c) {
+  for (DevMem* m : {&c.vin_orig, &c.vin, &c.vout, &c.w, &c.bbuf, &c.gH, &c.gR, &c.gG, &c.gROT, &c.gY, &c.gZ,
+                    &c.partial, &c.hsave, &c.wc, &c.hy_w, &c.iH, &c.iR, &c.iG, &c.iROT, &c.iY, &c.iZ, &c.ipartial,
+                    &c.ihsave})
+    m->release();
+  for (auto& m : c.xbuf) m->release();
+  for (auto& m : c.cbuf) m->release();
+  for (auto& m : c.basis) m->release();
+  for (auto& m : c.ibasis) m->release();
+  for (int k = 0; k < 2; ++k) {
+    c.hy_x0[k].release();
+    c.hy_y[k].release();
+  }
+  c.ncap = 0;
+  c.maxit_cap = 0;
+  c.incap = 0;
+  c.imaxit_cap = 0;
+}
+
+// Columns are independent (one Krylov basis per column, filter_engine.hpp:109-111): when the
+// workspace of all columns does not fit beside the factors, filter them in column batches.
+int apply_filter_batched(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
+                         zolo_report* rep) {
+  auto run = [&](const void* v, void* y, int64_t k, zolo_report* r) {
+    return c.cx ? apply_filter_impl<cd>(c, v, y, k, tol, gmres_max, r)
+                : apply_filter_impl<double>(c, v, y, k, tol, gmres_max, r);
+  };
+  const double per_col = bytes_per_column(c, static_cast<int>(gmres_max));
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  static const int64_t forced = env_int("ZOLO_FILTER_BATCH", 0);  // (testing) force a column batch size
+  int64_t batch = forced > 0 ? forced : ncols;
+  if (forced <= 0) {
+    if (ncols <= c.ncap || ncols * per_col < 0.85 * free_b) return run(d_v, d_y, ncols, rep);
+    release_workspace(c);
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    batch = std::max<int64_t>(1, static_cast<int64_t>(0.85 * free_b / per_col));
+  }
+  if (batch >= ncols) return run(d_v, d_y, ncols, rep);
+  const size_t colb = c.es() * c.n;
+  int code = ZOLO_OK;
+  double ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (rep) {
+    rep->iterations = 0;
+    rep->operator_applications = 0;
+    rep->n_shifts = 2 * c.r;
+    rep->all_converged = 1;
+    for (int k = 0; k < 2 * c.r; ++k) rep->residuals[k] = 0.0, rep->converged[k] = 1;
+  }
+  std::string err;
+  for (int64_t c0 = 0; c0 < ncols; c0 += batch) {
+    const int64_t k = std::min(batch, ncols - c0);
+    zolo_report rb;
+    rb.column_iterations = rep && rep->column_iterations ? rep->column_iterations + c0 : nullptr;
+    const int st = run(static_cast<const char*>(d_v) + colb * c0, static_cast<char*>(d_y) + colb * c0, k, &rb);
+    if (st != ZOLO_OK && code == ZOLO_OK) {
+      code = st;  // the reference finishes every column before rethrowing (filter_engine.hpp:134-137)
+      err = c.err;
+    }
+    for (int i : {0, 2, 3, 4, 5, 6}) ms[i] += c.last_ms[i];
+    if (rep) {
+      rep->iterations = std::max(rep->iterations, rb.iterations);
+      rep->operator_applications += rb.operator_applications;
+      rep->all_converged &= rb.all_converged;
+      for (int q = 0; q < rb.n_shifts; ++q) {
+        rep->residuals[q] = std::max(rep->residuals[q], rb.residuals[q]);
+        rep->converged[q] &= rb.converged[q];
+      }
+    }
+  }
+  for (int i : {0, 2, 3, 4, 5, 6}) c.last_ms[i] = ms[i];
+  if (code != ZOLO_OK) c.err = err;
+  return code;
+}
+
+}  // namespace
+
+extern "C" {
+
 int zolo_apply_filter_device(zolo_ctx* c, const void* d_v, void* d_y, int64_t ncols, double gmres_tol,
                              int64_t gmres_max, zolo_report* rep) {
   int code = ZOLO_OK;
   const int st = guarded(c, [&] {
     require(ncols >= 1, "apply_filter: empty block");
-    code = c->cx ? apply_filter_impl<cd>(*c, d_v, d_y, ncols, gmres_tol, gmres_max, rep)
-                 : apply_filter_impl<double>(*c, d_v, d_y, ncols, gmres_tol, gmres_max, rep);
+    code = apply_filter_batched(*c, d_v, d_y, ncols, gmres_tol, gmres_max, rep);
   });
   return st != ZOLO_OK ? st : code;
 }
@@ -1868,8 +1962,7 @@ int zolo_apply_filter(zolo_ctx* c, const double* v, double* y, int64_t ncols, do
     c->host_in.ensure(bytes);  // grow-only staging: no per-call cudaMalloc / cudaFree
     c->host_out.ensure(bytes);
     CK(cudaMemcpyAsync(c->host_in.p, v, bytes, cudaMemcpyHostToDevice, c->st));
-    code = c->cx ? apply_filter_impl<cd>(*c, c->host_in.p, c->host_out.p, ncols, gmres_tol, gmres_max, rep)
-                 : apply_filter_impl<double>(*c, c->host_in.p, c->host_out.p, ncols, gmres_tol, gmres_max, rep);
+    code = apply_filter_batched(*c, c->host_in.p, c->host_out.p, ncols, gmres_tol, gmres_max, rep);
     CK(cudaMemcpyAsync(y, c->host_out.p, bytes, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
   });
@@ -1928,9 +2021,9 @@ int zolo_last_timings(const zolo_ctx* c, double* ms) {
 
 int zolo_sweep_profile(const zolo_ctx* c, int64_t* out) {
   for (int i = 0; i < 8; ++i) out[i] = 0;
-  if (!c->factored) return ZOLO_ERR_DOMAIN;
+  if (!c->factored && !c->sym_ready) return ZOLO_ERR_DOMAIN;
   out[0] = c->geom.nbk;
-  if (c->sparse) {
+  if (c->sparse || (!c->factored && c->sym_ready)) {
     out[1] = c->sgeom.ntiles;
     out[2] = c->sched_fwd.ntask;
     out[3] = c->sched_bwd.ntask;

@@ -221,3 +221,35 @@ def test_driver_full_size_configs(zb, name):
     x = res.vectors
     bx = bm @ x if bm is not None else x
     assert np.abs(x.conj().T @ bx - np.eye(x.shape[1])).max() <= 1e-8
+
+
+def test_column_batching_is_bitwise_transparent(zb):
+    """apply_filter filters columns in batches when the workspace does not fit (columns are
+    independent, filter_engine.hpp:109-111): a forced small batch must give the same bits and
+    the same merged report (ZOLO_FILTER_BATCH, read once per process -> subprocess)."""
+    import subprocess
+    import sys
+
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from conftest import load_golden, golden_pencil
+import paper_1701_08935_b200 as zb
+g = load_golden("filter_cfg3_k5")
+op = zb.FilterOperator(golden_pencil(g), g["design"], int(g["r"]), is_complex=True, nd_leaf=64)
+y, rep = op.apply_filter(g["v"])
+np.savez(sys.argv[1], y=y, it=rep.iterations, ops=rep.operator_applications, cols=np.array(rep.column_iterations))
+'''
+    import os
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for batch in ("0", "2"):
+        f = tempfile.mktemp(suffix=".npz")
+        env = dict(os.environ, ZOLO_FILTER_BATCH=batch)
+        subprocess.run([sys.executable, "-c", code, f], check=True, cwd=root, env=env, timeout=300)
+        outs.append(np.load(f))
+    a, b = outs
+    assert (a["y"] == b["y"]).all()
+    assert int(a["it"]) == int(b["it"]) and int(a["ops"]) == int(b["ops"]) and (a["cols"] == b["cols"]).all()

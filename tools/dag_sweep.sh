@@ -1,5 +1,5 @@
 #!/bin/bash
-for leaf in 192 256; do
-  echo "== leaf $leaf"
-  ND_LEAF=$leaf timeout 300 python tools/quick_check.py cfg3 cfg1 2>&1 | grep -E "apply_filter" | sed -n '2p;4p'
+for ch in 0 1; do
+  echo "== chain $ch"
+  ZOLO_DAG_CHAIN=$ch timeout 300 python tools/quick_check.py cfg2 cfg3 cfg1 2>&1 | grep -E "apply_filter" | sed -n '2p;4p;6p'
 done
