@@ -1816,7 +1816,9 @@ int zolo_set_pole_shard(zolo_ctx* c, int rank, int nranks, const void* unique_id
     c->comm = nullptr;
     c->shard_rank = rank;
     c->shard_size = nranks;
-    if (nranks > 1 && unique_id) {
+    // a 1-rank communicator is legal: its all-reduce is the identity, which lets one GPU run the
+    // in-library NCCL path end to end
+    if (unique_id) {
       try {
         c->comm = nccl_open(unique_id, nranks, rank);
       } catch (const std::exception& e) {

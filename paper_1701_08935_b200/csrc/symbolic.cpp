@@ -15,6 +15,7 @@
 // nested dissection is SURVEY.md §8(f) rank 2 ("host symbolic analysis: ND
 // ordering, supernodes, etree"), here at 32x32-tile granularity.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <numeric>
 #include <vector>
@@ -167,6 +168,54 @@ struct NdState {
   }
 };
 
+// Separator rows ordered by the descendants they couple to. A separator's
+// factor rows below a descendant subtree D are the separator vertices adjacent
+// to D, so sorting them by the (already final) position of their earliest
+// descendant neighbour makes each subtree's coupling rows contiguous: fewer,
+// denser 32x32 tiles in L(separator, D) and U(D, separator). Nodes are in
+// post-order, so every earlier neighbour of a separator vertex is a descendant.
+// mode 1: earliest neighbour; 2: latest; 3: mean.
+void order_separators(const Graph& g, const std::vector<int>& is_sep, std::vector<std::vector<int64_t>>& nodes,
+                      int mode) {
+  std::vector<int64_t> ord(g.n, -1);
+  int64_t next = 0;
+  std::vector<std::pair<double, int64_t>> keyed;
+  for (size_t t = 0; t < nodes.size(); ++t) {
+    auto& nd = nodes[t];
+    if (is_sep[t] && nd.size() > 1) {
+      keyed.clear();
+      for (size_t q = 0; q < nd.size(); ++q) {
+        const int64_t v = nd[q];
+        double key = 0.0;
+        int64_t cnt = 0, lo = INT64_MAX, hi = -1;
+        for (int64_t k = g.rp[v]; k < g.rp[v + 1]; ++k) {
+          const int64_t o = ord[g.ci[k]];
+          if (o < 0) continue;
+          lo = std::min(lo, o);
+          hi = std::max(hi, o);
+          key += static_cast<double>(o);
+          ++cnt;
+        }
+        if (!cnt)
+          key = 1e300;
+        else if (mode == 1)
+          key = static_cast<double>(lo);
+        else if (mode == 2)
+          key = static_cast<double>(hi);
+        else
+          key /= static_cast<double>(cnt);
+        keyed.emplace_back(key, static_cast<int64_t>(q));
+      }
+      std::stable_sort(keyed.begin(), keyed.end(),
+                       [](const auto& x, const auto& y) { return x.first < y.first; });
+      std::vector<int64_t> out(nd.size());
+      for (size_t q = 0; q < nd.size(); ++q) out[q] = nd[keyed[q].second];
+      nd.swap(out);
+    }
+    for (int64_t v : nd) ord[v] = next++;
+  }
+}
+
 }  // namespace
 
 void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std::vector<std::vector<int64_t>>& nodes) {
@@ -176,6 +225,30 @@ void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std
   std::iota(all.begin(), all.end(), 0);
   st.rec(std::move(all));
   nodes = std::move(st.nodes);
+  static const int sep_mode = [] {
+    const char* v = std::getenv("ZOLO_SEP_ORDER");
+    return v ? std::atoi(v) : 1;
+  }();
+  if (sep_mode) order_separators(g, st.node_is_sep, nodes, sep_mode);
+  // The node just before a separator (in post-order) is the root of its last child subtree,
+  // whose factor structure lies inside separator + struct(separator): the two can share a
+  // tile without adding fill, so only nodes followed by a non-separator start a new tile.
+  static const bool merge = [] {
+    const char* v = std::getenv("ZOLO_ND_MERGE");
+    return v ? std::atoi(v) != 0 : true;
+  }();
+  if (merge && nodes.size() > 1) {
+    std::vector<std::vector<int64_t>> out;
+    std::vector<int64_t> cur;
+    for (size_t t = 0; t < nodes.size(); ++t) {
+      cur.insert(cur.end(), nodes[t].begin(), nodes[t].end());
+      if (t + 1 == nodes.size() || !st.node_is_sep[t + 1]) {
+        out.push_back(std::move(cur));
+        cur.clear();
+      }
+    }
+    nodes.swap(out);
+  }
 }
 
 void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::vector<std::vector<int64_t>>& nodes,

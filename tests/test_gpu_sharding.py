@@ -2,8 +2,9 @@
 (zolo_set_pole_shard without a communicator) return each rank's partial G;
 their sum must equal the unsharded G (filter_engine.hpp:63-69, 73-78), the
 inner-solve counters must add up, and a 1-rank shard is the plain operator.
-The NCCL all-reduce itself needs two GPUs (NCCL rejects two ranks on one
-device); its host logic is covered by tests/test_sharding_cpu.py (gloo).
+A 1-rank NCCL communicator runs the in-library all-reduce path on one GPU;
+the multi-rank exchange needs two GPUs (NCCL rejects two ranks on one device)
+and its host logic is covered by tests/test_sharding_cpu.py (gloo).
 """
 import numpy as np
 import pytest
@@ -54,3 +55,20 @@ def test_single_rank_shard_is_plain_operator(zb):
     ya, _ = a.apply_filter(g["v"])
     yb, _ = b.apply_filter(g["v"])
     assert (ya == yb).all()
+
+
+def test_one_rank_nccl_communicator(zb):
+    """The in-library NCCL path on one GPU: a 1-rank communicator (ncclCommInitRank with nranks=1)
+    all-reduces every G application in place; the sum over one rank is the identity, so the filtered
+    block, report and counters must equal the plain operator's bit for bit."""
+    g = load_golden("filter_planted30_cx")
+    cx, r = bool(g["cx"]), int(g["r"])
+    pen = golden_pencil(g)
+    a = zb.FilterOperator(pen, g["design"], r, is_complex=cx, nd_leaf=64)
+    b = zb.FilterOperator(pen, g["design"], r, is_complex=cx, nd_leaf=64, shard=(0, 1, zb.nccl_unique_id()))
+    ya, ra = a.apply_filter(g["v"])
+    yb, rb = b.apply_filter(g["v"])
+    assert (ya == yb).all()
+    assert ra.iterations == rb.iterations and ra.column_iterations == rb.column_iterations
+    assert a.inner_solve_count() == b.inner_solve_count() and a.g_application_count() == b.g_application_count()
+    assert (a.apply_g(g["v"]) == b.apply_g(g["v"])).all()
