@@ -107,6 +107,15 @@ def load_peaks():
     return out
 
 
+DESCR = {
+    "cfg1": "2D 5-point Laplacian 64^2 (Dirichlet), B=I",
+    "cfg2": "3D 7-point Laplacian 32^3 + U[0,1] potential, SPD mass B",
+    "cfg3": "complex Hermitian 3D tight-binding 48^3 (Peierls phases, Anderson disorder 1.5), B=I+0.05 S",
+    "cfg4": "chemistry-shaped block-sparse Hermitian pencil, 8000 atoms x 13x13 blocks, SPD overlap B",
+    "cfg5": "complex Hermitian 3D tight-binding 64^3 (disorder 2), B=I",
+}
+
+
 def workload(name):
     from paper_1701_08935_b200 import configs
 
@@ -303,8 +312,8 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if poles else "weak",
         "vs_baseline": None,
         "dtype": "c128" if cx else "f64", "data": "synthetic (seeded generator, BASELINE config shape)",
-        "config": {"workload": f"{args.config}: 3D 7-point Laplacian 32^3 + U[0,1] potential, SPD mass B, N={n}, "
-                               f"r={r} (p={2 * r} poles), n_v={nv}, gmres_tol=1e-12, 64-eigenvalue window",
+        "config": {"workload": f"{args.config}: {DESCR.get(args.config, args.config)}, N={n}, "
+                               f"r={r} (p={2 * r} poles), n_v={nv}, gmres_tol=1e-12, {nl}-eigenvalue window",
                    "N": n, "n_v": nv, "r": r, "ordering": "nested dissection (leaf 192), block-sparse 32x32 tiles",
                    "factor_tiles_per_pole": sp["offdiag_tiles"] + sp["block_rows"],
                    "l2": "factors > L2 (no flush needed)",

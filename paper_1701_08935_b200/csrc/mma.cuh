@@ -17,7 +17,7 @@ constexpr int DCG = 32;         // columns per DAG task / output block
 constexpr int XS2 = DCG * XPAD; // padded 32 x 32 x block
 
 // Per-thread ownership of the 32 x 16 complex output block: warp w holds rows
-// 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1}.
+// 8 ((w%4) ^ 2 (w/4)) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1}.
 struct Frag {
   int row, col;  // first of the two owned (row, col), (row, col+1)
   int r0, c0;    // warp block origin
@@ -27,8 +27,10 @@ __device__ __forceinline__ Frag frag() {
   Frag f;
   const int w = threadIdx.x >> 5;
   f.lane = threadIdx.x & 31;
-  f.r0 = 8 * (w & 3);
-  f.c0 = 8 * (w >> 2);
+  // warps w and w + 4 share an SM sub-partition (DMMA pipe): give them row groups g and g ^ 2, so
+  // a tile whose nonzeros sit in some row groups (occupancy masks) still spreads over all pipes
+  f.r0 = 8 * ((w & 3) ^ ((w >> 1) & 2));
+  f.c0 = 8 * ((w >> 2) & 1);
   f.row = f.r0 + (f.lane >> 2);
   f.col = f.c0 + 2 * (f.lane & 3);
   return f;

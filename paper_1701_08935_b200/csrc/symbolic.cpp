@@ -146,7 +146,27 @@ struct NdState {
     for (int64_t v : idx) lv.push_back(level[v]);
     std::vector<int64_t> srt = lv;
     std::nth_element(srt.begin(), srt.begin() + srt.size() / 2, srt.end());
-    const int64_t med = srt[srt.size() / 2];
+    int64_t med = srt[srt.size() / 2];
+    static const double win = [] {
+      const char* v = std::getenv("ZOLO_ND_WINDOW");
+      return v ? std::atof(v) : 0.0;
+    }();
+    if (win > 0.0) {
+      // smallest level set whose two sides both hold at least (0.5 - win) of the piece
+      std::vector<int64_t> cnt;
+      for (int64_t l : lv) {
+        if (l >= static_cast<int64_t>(cnt.size())) cnt.resize(l + 1, 0);
+        ++cnt[l];
+      }
+      const double tot = static_cast<double>(idx.size());
+      int64_t below = 0, best = -1;
+      for (int64_t l = 0; l < static_cast<int64_t>(cnt.size()); ++l) {
+        const double fa = below / tot, fb = (tot - below - cnt[l]) / tot;
+        if (fa >= 0.5 - win && fb >= 0.5 - win && (best < 0 || cnt[l] < cnt[best])) best = l;
+        below += cnt[l];
+      }
+      if (best >= 0) med = best;
+    }
     std::vector<int64_t> a, b, s;
     for (size_t q = 0; q < idx.size(); ++q) {
       if (lv[q] < med)

@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     int g = 0;
     // one ring entry: tile (optional) + a 32 x 32 block with column stride `stride`
     int cur_t = 0;  // claim index of the task being produced (trace)
-    auto produce = [&](int kind, int sign, const cd* tile, const uint2* mask, const cd* blk, int64_t stride, int c0,
+    auto produce = [&](int kind, int sign, const cd* tile, uint2 mw, const cd* blk, int64_t stride, int c0,
                        int nc, unsigned long long pol, int last, int i, int ci, int gi, int out) {
       const int s = g % NST2, round = g / NST2;
       mbar_wait(empty + s, (round & 1) ^ 1);
@@ -787,8 +787,6 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         bulk_copy(xs + lane * XPAD, blk + (c0 + lane) * stride, TILE * sizeof(cd), full + s, pol);
       else
         for (int r = 0; r < TILE; ++r) xs[lane * XPAD + r] = mk(0.0, 0.0);
-      uint2 mw = make_uint2(0xffffffffu, 0xffffffffu);
-      if (mask && lane == 0) mw = *mask;
       __syncwarp();
       if (lane == 0) {
         Meta2 m;
@@ -808,18 +806,47 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
       ++g;
     };
-    // claims run one task ahead: the atomic for task T+1 is issued when T starts
+    auto decode = [&](int tt, int& r, int& ci, int& gi) {
+      if (A.tmap) {  // chains staggered in the claim order (each chain keeps its topological order)
+        const int rc = A.tmap[tt / A.ngroups];
+        r = rc / A.nchains;
+        ci = rc % A.nchains;
+        gi = tt % A.ngroups;
+      } else {
+        r = tt / per_step;
+        const int rem = tt % per_step;
+        ci = rem / A.ngroups;
+        gi = rem % A.ngroups;
+      }
+    };
+    // Claims run two tasks ahead: when task T starts, T+1's id has arrived (its record load is
+    // issued now and lands while T streams) and the atomic for T+2 goes out.
     int t = 0;
     if (lane == 0) t = atomicAdd(A.counter, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
+    int rec_lo = 0, rec_hi = 0;  // this lane's two words of the current task's record
+    if (t < ntasks) {
+      int r0, c0_, g0_;
+      decode(t, r0, c0_, g0_);
+      rec_lo = A.recs[static_cast<size_t>(r0) * DAG_REC + lane];
+      rec_hi = A.recs[static_cast<size_t>(r0) * DAG_REC + lane + 32];
+    }
+    int tn_raw = 0;
+    if (lane == 0) tn_raw = atomicAdd(A.counter, 1);
     for (;;) {
       if (t >= ntasks) {
-        produce(2, 0, nullptr, nullptr, A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
+        produce(2, 0, nullptr, make_uint2(0u, 0u), A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
         break;
       }
-      int tn_raw = 0;
-      if (lane == 0) tn_raw = atomicAdd(A.counter, 1);  // consumed late unless the L2 prefetch needs it
-      const int tn = A.l2pf ? __shfl_sync(0xffffffffu, tn_raw, 0) : 0;
+      const int tn = __shfl_sync(0xffffffffu, tn_raw, 0);
+      int nrec_lo = 0, nrec_hi = 0;
+      if (tn < ntasks) {
+        int rn_, cn_, gn_;
+        decode(tn, rn_, cn_, gn_);
+        nrec_lo = A.recs[static_cast<size_t>(rn_) * DAG_REC + lane];
+        nrec_hi = A.recs[static_cast<size_t>(rn_) * DAG_REC + lane + 32];
+      }
+      if (lane == 0) tn_raw = atomicAdd(A.counter, 1);
       if (A.l2pf && tn < ntasks) {
         // warm L2 with the next task's tiles and solution blocks while this one streams
         int rn, cin, gin;
@@ -855,20 +882,9 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       unsigned long long wsum = 0;
       if (trp && lane == 0) trp[0] = gtimer();
       int r, ci, gi;
-      if (A.tmap) {  // chains staggered in the claim order (each chain keeps its topological order)
-        const int rc = A.tmap[t / A.ngroups];
-        r = rc / A.nchains;
-        ci = rc % A.nchains;
-        gi = t % A.ngroups;
-      } else {
-        r = t / per_step;
-        const int rem = t % per_step;
-        ci = rem / A.ngroups;
-        gi = rem % A.ngroups;
-      }
-      const int* rg = A.recs + static_cast<size_t>(r) * DAG_REC;
-      recp[lane] = rg[lane];
-      recp[lane + 32] = rg[lane + 32];
+      decode(t, r, ci, gi);
+      recp[lane] = rec_lo;
+      recp[lane + 32] = rec_hi;
       __syncwarp();
       const int i = recp[0], nd = recp[1], pa = recp[2], pc = recp[3], out = recp[4];
       const bool chunk = out >= 0;
@@ -877,19 +893,30 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       const size_t cgi = static_cast<size_t>(ci) * A.ngroups + gi;
       const int* flags = A.flags + cgi * A.s.nb;
       const int* cflags = A.cflags + cgi * A.nslots;
-      // readiness of every dependency and partial, read in parallel (one round trip)
+      // occupancy masks of all the task's tiles (lane q: dependency q, lane 31: the pre-transform)
+      // and readiness of every dependency, each read in parallel (one round trip)
+      uint2 my_mask = make_uint2(0xffffffffu, 0xffffffffu);
+      if (lane < nd) {
+        if (ch.offm) my_mask = ch.offm[recp[DAG_REC_HDR + 2 * lane + 1]];
+      } else if (lane == 31 && !chunk && ch.pre && ch.prem) {
+        my_mask = ch.prem[i];
+      }
       const unsigned dep_ready =
           __ballot_sync(0xffffffffu, lane >= nd || ld_acquire(flags + recp[DAG_REC_HDR + 2 * lane]) >= A.epoch);
+      auto mask_of = [&](int q) {
+        return make_uint2(__shfl_sync(0xffffffffu, my_mask.x, q), __shfl_sync(0xffffffffu, my_mask.y, q));
+      };
       const int nent = (chunk ? 0 : 1) + pc + nd;
       int e = 0;
       if (!chunk) {
         ++e;
+        const uint2 pm = mask_of(31);
         if (ch.pre)
-          produce(0, 1, ch.pre + static_cast<size_t>(i) * TT, ch.prem ? ch.prem + i : nullptr,
-                  ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0, nc, pol_stream, e == nent, i, ci, gi, out);
+          produce(0, 1, ch.pre + static_cast<size_t>(i) * TT, pm, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0,
+                  nc, pol_stream, e == nent, i, ci, gi, out);
         else
-          produce(1, -1, nullptr, nullptr, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0, nc, pol_stream,
-                  e == nent, i, ci, gi, out);
+          produce(1, -1, nullptr, pm, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0, nc, pol_stream, e == nent,
+                  i, ci, gi, out);
       }
       for (int p0 = 0; p0 < pc; p0 += 32) {
         const unsigned prdy =
@@ -901,8 +928,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
             if (trp) wsum += gtimer() - tw;
           }
           ++e;
-          produce(1, 1, nullptr, nullptr, ch.cbuf + static_cast<int64_t>(pa + p) * TILE, A.ldp, c0, nc, pol_stream,
-                  e == nent, i, ci, gi, out);
+          produce(1, 1, nullptr, make_uint2(0xffffffffu, 0xffffffffu), ch.cbuf + static_cast<int64_t>(pa + p) * TILE,
+                  A.ldp, c0, nc, pol_stream, e == nent, i, ci, gi, out);
         }
       }
       for (int q = 0; q < nd; ++q) {
@@ -913,15 +940,17 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
           if (trp) wsum += gtimer() - tw;
         }
         ++e;
-        produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, ch.offm ? ch.offm + tid : nullptr,
-                ch.dst + static_cast<int64_t>(j) * TILE, A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
+        produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, mask_of(q), ch.dst + static_cast<int64_t>(j) * TILE,
+                A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
       }
       __syncwarp();
       if (trp && lane == 0) {
         trp[4] = wsum;
         trp[5] = gtimer();
       }
-      t = A.l2pf ? tn : __shfl_sync(0xffffffffu, tn_raw, 0);
+      t = tn;
+      rec_lo = nrec_lo;
+      rec_hi = nrec_hi;
     }
     return;
   }
