@@ -239,7 +239,8 @@ int zolo_last_timings(const zolo_ctx* ctx, double* ms);
  * out[0] block rows (32-row tiles), out[1] off-diagonal tiles of L (= of U),
  * out[2] / out[3] forward / backward DAG task records (0 for the band layout),
  * out[4] chunk partial-sum slots, out[5] critical path in block rows,
- * out[6] layout: 0 = block-sparse (ND), 1 = block band (RCM), out[7] reserved.
+ * out[6] layout: 0 = block-sparse (ND), 1 = block band (RCM), out[7] block rows of the
+ * selectively inverted trailing block (0 = none).
  * No equivalent in the reference (development / roofline accounting). */
 int zolo_sweep_profile(const zolo_ctx* ctx, int64_t* out);
 
@@ -248,6 +249,12 @@ int zolo_sweep_profile(const zolo_ctx* ctx, int64_t* out);
 int zolo_timer(zolo_ctx* ctx, int op, double* ms);
 
 /* --- host-only helpers (no GPU needed) ---------------------------------- */
+/* Block structure of the nested-dissection factor (no reference equivalent;
+ * development / sizing): out[0] padded size, out[1] block rows, out[2]
+ * off-diagonal tiles per triangle, out[3] critical path in block rows,
+ * out[4] block rows of the largest trailing dense block, out[5] tile-aligned
+ * node groups, out[6..7] reserved. */
+int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* out);
 /* reorder_rcm (rcm.hpp:69-115) of a structurally symmetric pattern;
  * perm[new] = old. bw/profile (rcm.hpp:118-147) may be NULL. */
 int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int64_t* bw, int64_t* profile);

@@ -434,7 +434,8 @@ class FilterOperator:
         ms = np.zeros(8)
         lib().zolo_last_timings(self._h, _ptr(ms))
         return dict(filter_ms=ms[0], factor_ms=ms[1], trsm_ms=ms[2], trsm_launches=int(ms[3]),
-                    kernel_launches=int(ms[4]), operator_applications=int(ms[5]), inner_steps=int(ms[6]))
+                    kernel_launches=int(ms[4]), operator_applications=int(ms[5]), inner_steps=int(ms[6]),
+                    iterations_ms=ms[7])
 
     def sweep_profile(self):
         """Structure the triangular sweeps run over (zolo_sweep_profile)."""
@@ -442,7 +443,7 @@ class FilterOperator:
         _check(self._h, lib().zolo_sweep_profile(self._h, _ptr(out)))
         return dict(block_rows=int(out[0]), offdiag_tiles=int(out[1]), fwd_tasks=int(out[2]),
                     bwd_tasks=int(out[3]), chunk_slots=int(out[4]), critical_path=int(out[5]),
-                    layout="band" if out[6] == 1 else "block-sparse")
+                    layout="band" if out[6] == 1 else "block-sparse", selinv_rows=int(out[7]))
 
     def timer_start(self):
         _check(self._h, lib().zolo_timer(self._h, 0, None))

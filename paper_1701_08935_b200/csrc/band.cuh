@@ -53,6 +53,11 @@ struct FactorTiles {
   uint2* mDL = nullptr;
   uint2* mDU = nullptr;
   bool swz = false;  // Lt, Ut, DinvL, DinvU stored in the swizzled sweep layout (swizzle_tiles)
+  // selectively inverted trailing block (selinv; host.hpp DT_*), swizzled like the rest
+  cd* ML = nullptr;
+  cd* MU = nullptr;
+  cd* WU = nullptr;
+  cd* WX = nullptr;
 };
 
 __host__ __device__ inline size_t lt_off(int i, int d, int J) {
@@ -81,6 +86,7 @@ struct Chain {
   cd* cbuf;        // helper -> owner partial solutions c_i (ld x ncols)
   int mode;
   int pad;
+  const cd* minv;  // selectively inverted trailing block (forward: M tiles, backward: W tiles), or nullptr
 };
 
 struct FactorDevState {
@@ -142,6 +148,11 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const std::vector<int>& col_cnt
 void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks);
 // tiles permuted in place into the sweep layout: element (row, col) at col*32 + (row ^ swz(col))
 void swizzle_tiles(cudaStream_t st, cd* tiles, int64_t ntiles);
+// selective inversion of the trailing dense block [s0, s0 + K) of the row-scaled factors (before
+// swizzling): ML = (I + L~_SS)^-1, MU = (I + U~_SS)^-1 (strict parts, index a(a-1)/2 + b, a > b);
+// WU(b,a) = MU(b,a) DinvU_a and (WX != nullptr) WX(a,b) = DinvU_a ML(a,b), index a(a+1)/2 + b, a >= b.
+// tab[a*K + b] (a > b): tile id of L(s0+a, s0+b).
+void selinv(cudaStream_t st, int K, int s0, const int* tab, const SpFactor& f, cd* ML, cd* MU, cd* WU, cd* WX);
 // number of pivots (diagonal of the packed diagonal-tile LUs) with negative real part
 int64_t count_negative_pivots(cudaStream_t st, const cd* dt, int nb);
 
@@ -160,8 +171,12 @@ struct DagSched {
 // presw: the chains' tiles are stored swizzled (swizzle_tiles); required by the v2 kernel
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
-                    unsigned long long* trace = nullptr, const int* tmap = nullptr, bool presw = false);
+                    unsigned long long* trace = nullptr, const int* tmap = nullptr, bool presw = false,
+                    bool need_v2 = false);
 int dag_groups(int ncols);
+// chains' cbuf rows [dst_row0, dst_row0 + rows) <- their src rows [row0, row0 + rows), all ncols columns
+void dag_stage_inputs(cudaStream_t st, const Chain* d_chains, int nchains, int64_t row0, int64_t rows, int ncols,
+                      int64_t ld, int64_t ldp, int64_t dst_row0);
 
 // x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass
 // x_i = DinvL_i^H w_i); x is ld x ncols, D is nbk tiles.

@@ -153,6 +153,9 @@ struct zolo_ctx {
   SpGeom sgeom;
   std::vector<int> sp_col_cnt;
   int64_t critical_path = 0;
+  int sel_s0 = 0, sel_K = 0;  // selectively inverted trailing block [sel_s0, sel_s0 + sel_K) (host.hpp DT_*)
+  int sel_stage = 0;          // its backward input is staged into partial slots [sel_stage, sel_stage + sel_K)
+  DevMem sp_seltab, sel_mem;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
   DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
   int tmap_nch = -1;  // chain count the staggered claim maps were built for
@@ -180,6 +183,7 @@ struct zolo_ctx {
   double last_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  cudaEvent_t ev4 = nullptr, ev5 = nullptr;  // device-busy time of the GMRES iterations
 
   // hybrid inner solve (BASELINE config 2): one factored pole,
   // shift-invariant GMRES on K_p^{-1} B for the others
@@ -583,6 +587,22 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
                      order = env_int("ZOLO_DAG_ORDER", 3);
     static const bool chain = env_int("ZOLO_DAG_CHAIN", 0) != 0;  // chained partials: measured slower
     // self-contained task records: header + the (j, tile id) pairs in processing order
+    // selective inversion of the trailing dense block: only the v2 sweep kernel reads its task kinds
+    static const int sel_kmax = env_int("ZOLO_SELINV", 0);  // off: +1% on cfg2, and the explicit inverse lifts cfg3's residual floor 9e-9 -> 2e-8
+    const bool sel_ok = sel_kmax >= 2 && env_int("ZOLO_DAG_V2", 1) != 0 && (c.cx ? 2 : 1) * std::max(c.r, 1) <= 32;
+    const int s0 = sel_ok ? trailing_dense_start(bs, sel_kmax) : nb;
+    c.sel_s0 = s0;
+    c.sel_K = nb - s0 >= 2 ? nb - s0 : 0;
+    if (c.sel_K) {
+      const int K = c.sel_K;
+      std::vector<int> tab(static_cast<size_t>(K) * K, -1);
+      for (int i = s0; i < nb; ++i)
+        for (int64_t e = bs.row_ptr[i]; e < bs.row_ptr[i + 1]; ++e)
+          if (bs.row_idx[e] >= s0) tab[static_cast<size_t>(i - s0) * K + (bs.row_idx[e] - s0)] = static_cast<int>(e);
+      upload(c.sp_seltab, tab, c.st);
+    }
+    std::vector<int> cslot;
+    int stage_base = 0;  // first slot of the staged backward input of the inverted block
     auto records = [&](const std::vector<DagTask>& ts, bool fwd) {
       std::vector<int> rec(ts.size() * DAG_REC, 0);
       for (size_t t = 0; t < ts.size(); ++t) {
@@ -592,26 +612,41 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
         const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
         const int nd = k.qb - k.qa;
         require(nd <= DAG_REC_DEPS, "zolo_factorize: DAG task record overflow");
-        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out;
+        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out, r[5] = k.flags;
         for (int q = 0; q < nd; ++q) {
-          const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
-          r[DAG_REC_HDR + 2 * q] = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
-          r[DAG_REC_HDR + 2 * q + 1] = static_cast<int>(fwd ? e : bs.col_tile[e]);
+          int j, tid;
+          if (k.flags & DT_SRCDEP) {  // W(i, kk), kk = nb-1 .. i: input block kk, staged in slot base + kk - s0
+            const int kk = nb - 1 - (k.qa + q);
+            j = stage_base + (kk - s0);
+            tid = (kk - s0) * (kk - s0 + 1) / 2 + (k.i - s0);
+          } else if (k.flags & DT_SLOTDEP) {  // M(i, kk), kk in [s0, i): c_kk from its slot
+            const int kk = static_cast<int>(bs.row_idx[e0 + k.qa + q]);
+            j = cslot[kk];
+            tid = (k.i - s0) * (k.i - s0 - 1) / 2 + (kk - s0);
+          } else {
+            const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
+            j = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
+            tid = static_cast<int>(fwd ? e : bs.col_tile[e]);
+          }
+          r[DAG_REC_HDR + 2 * q] = j;
+          r[DAG_REC_HDR + 2 * q + 1] = tid;
         }
       }
       return rec;
     };
     std::vector<DagTask> tf, tb;
-    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf, chain);
-    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb, chain);
+    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf, chain, s0, &cslot);
+    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb, chain, s0);
+    stage_base = sb;
+    c.sel_stage = sb;
     upload(c.sp_sched_fwd, records(tf, true), c.st);
     upload(c.sp_sched_bwd, records(tb, false), c.st);
     c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), static_cast<int>(tf.size()), sf};
     c.tmap_nch = -1;
     c.sp_tmap_fwd.release();
     c.sp_tmap_bwd.release();
-    c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb};
-    c.sp_nslots = std::max(sf, sb);
+    c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb + c.sel_K};
+    c.sp_nslots = std::max(sf, sb + c.sel_K);
   }
   clk.mark("sweep schedules");
 
@@ -679,6 +714,19 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     tiles[j].Lt = p + 3 * per_diag;
     tiles[j].Ut = p + 3 * per_diag + per_off;
   }
+  const int K = mstore ? c.sel_K : 0;
+  const size_t sel_strict = static_cast<size_t>(K) * (K > 0 ? K - 1 : 0) / 2, sel_diag = static_cast<size_t>(K) * (K + 1) / 2;
+  const size_t sel_per = (2 * sel_strict + 2 * sel_diag) * TT;
+  if (K) {
+    c.sel_mem.ensure(sizeof(cd) * sel_per * r);
+    for (int j = 0; j < r; ++j) {
+      cd* q = c.sel_mem.as<cd>() + sel_per * j;
+      tiles[j].ML = q;
+      tiles[j].MU = q + sel_strict * TT;
+      tiles[j].WU = q + 2 * sel_strict * TT;
+      tiles[j].WX = c.cx ? q + (2 * sel_strict + sel_diag) * TT : nullptr;
+    }
+  }
   if (mstore) {
     const size_t mper = 2 * static_cast<size_t>(nb) + 2 * static_cast<size_t>(ntiles);
     mstore->ensure(sizeof(uint2) * mper * r);
@@ -733,6 +781,14 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
               c.rownorm_mem.as<double>() + c.sgeom.npad * j, c.sp_pad_rows.as<int>(), c.sp_npads, ds,
               c.sp_err.as<int>(), levels ? &pd : nullptr);
     if (mstore) {  // sweep factors: occupancy masks, then the swizzled sweep layout
+      if (K) {
+        selinv(c.pole_streams[j], K, c.sel_s0, c.sp_seltab.as<int>(), f, tiles[j].ML, tiles[j].MU, tiles[j].WU,
+               tiles[j].WX);
+        swizzle_tiles(c.pole_streams[j], tiles[j].ML, static_cast<int64_t>(sel_strict));
+        swizzle_tiles(c.pole_streams[j], tiles[j].MU, static_cast<int64_t>(sel_strict));
+        swizzle_tiles(c.pole_streams[j], tiles[j].WU, static_cast<int64_t>(sel_diag));
+        if (tiles[j].WX) swizzle_tiles(c.pole_streams[j], tiles[j].WX, static_cast<int64_t>(sel_diag));
+      }
       tile_masks(c.pole_streams[j], tiles[j].DinvL, nb, tiles[j].mDL);
       tile_masks(c.pole_streams[j], tiles[j].DinvU, nb, tiles[j].mDU);
       tile_masks(c.pole_streams[j], tiles[j].Lt, ntiles, tiles[j].mLt);
@@ -838,15 +894,17 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
       // solve:   y = DinvL b - L~ y ;  x = DinvU y - U~ x
       // adjoint: z = b - U~^H z (z_i = U_ii^H y_i) ; w = DinvU^H z - L~^H w (w_i = L_ii^H x_i),
       //          then x_i = DinvL_i^H w_i (blockdiag post-pass)
-      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
-      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
-      fwd[2 * p + 1] = Chain{t.Ut, nullptr, t.mUt, nullptr, b, xa, cba, FWD_UH, 0};
-      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, t.mLt, t.mDU, xa, xa, cba, BWD_LH, 0};
+      // selectively inverted trailing block: (I + L~)^-1, (I + U~^H)^-1 = MU^H forward; U_SS^-1 and
+      // (DinvU ML)^H backward (host.hpp DT_*)
+      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0, t.ML};
+      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0, t.WU};
+      fwd[2 * p + 1] = Chain{t.Ut, nullptr, t.mUt, nullptr, b, xa, cba, FWD_UH, 0, t.MU};
+      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, t.mLt, t.mDU, xa, xa, cba, BWD_LH, 0, t.WX};
     } else {
       cd* x = c.xbuf[p]->as<cd>();
       cd* cb = c.cbuf[p]->as<cd>();
-      fwd[p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
-      bwd[p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
+      fwd[p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0, t.ML};
+      bwd[p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0, t.WU};
     }
   }
   upload(c.chains_fwd, fwd, c.st);
@@ -936,10 +994,20 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
   if (c.tmap_nch != c.nchains()) build_tmap(c, c.nchains());
   const bool full = first == 0 && nsub == c.nchains() && c.sp_tmap_fwd.p && c.tmap_nch == nsub;
   const bool presw = c.tiles[0].swz;
-  dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
-                  c.counter.as<int>(), 1, c.num_sms, trace, full ? c.sp_tmap_fwd.as<int>() : nullptr, presw);
-  dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf, ++c.epoch,
-                  c.counter.as<int>() + 1, 0, c.num_sms, nullptr, full ? c.sp_tmap_bwd.as<int>() : nullptr, presw);
+  const bool need_v2 = c.sel_K > 0;  // the selectively inverted block's task kinds exist only in dag2_kernel
+  const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf,
+                                 ++c.epoch, c.counter.as<int>(), 1, c.num_sms, trace,
+                                 full ? c.sp_tmap_fwd.as<int>() : nullptr, presw, need_v2);
+  if (c.sel_K)  // the backward sweep runs in place: stage the inverted block's input first
+    dag_stage_inputs(c.st, c.chains_bwd.as<Chain>() + first, nsub, static_cast<int64_t>(c.sel_s0) * TILE,
+                     static_cast<int64_t>(c.sel_K) * TILE, na, ld, static_cast<int64_t>(TILE) * c.sched_bwd.nslots,
+                     static_cast<int64_t>(c.sel_stage) * TILE);
+  const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf,
+                                 ++c.epoch, c.counter.as<int>() + 1, 0, c.num_sms, nullptr,
+                                 full ? c.sp_tmap_bwd.as<int>() : nullptr, presw, need_v2);
+  if (g1 < 0 || g2 < 0)
+    throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: the selectively inverted schedule needs the v2 sweep kernel "
+                                     "(at most 32 chains, ZOLO_DAG_V2 on)");
   if (c.cx)
     for (int ci = first; ci < first + nsub; ++ci)
       if (ci & 1)
@@ -1342,7 +1410,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     if (beta[k] != 0.0) active.push_back(static_cast<int>(k));
 
   const int nchunk = static_cast<int>((ld + CHUNK - 1) / CHUNK);  // device rows incl. padding
-  float trsm_ms = 0.0f;
+  float trsm_ms = 0.0f, busy_ms = 0.0f;
   int trsm_launches = 0;
   int64_t launches = 4, opapps = 0;
   for (int it = 0; it < maxit && !active.empty(); ++it) {
@@ -1350,6 +1418,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     std::memcpy(c.act_h, active.data(), sizeof(int) * na);
     CK(cudaMemcpyAsync(c.act_d.p, c.act_h, sizeof(int) * na, cudaMemcpyHostToDevice, c.st));
     S* vm = reinterpret_cast<S*>(basis_block(c, it));
+    CK(cudaEventRecord(c.ev4, c.st));
     apply_g_device(c, vm, na, c.w.p);
     trsm_launches += 2;
     launches += 8 + (it + 1 < maxit ? 1 : 0);
@@ -1364,6 +1433,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       Krylov<S>::next_basis(c.st, n, ld, c.w.as<S>(), vn, c.act_d.as<int>(), na, g);
     }
     CK(cudaGetLastError());
+    CK(cudaEventRecord(c.ev5, c.st));
     CK(cudaMemcpyAsync(c.done_h, g.done, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
     int spin_err[2] = {0, 0};
     CK(cudaMemcpyAsync(spin_err, c.counter.as<int>() + 2, sizeof(int) * 2, cudaMemcpyDeviceToHost, c.st));
@@ -1372,6 +1442,8 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, c.ev2, c.ev3));
     trsm_ms += ms;
+    CK(cudaEventElapsedTime(&ms, c.ev4, c.ev5));
+    busy_ms += ms;
     std::vector<int> next;
     for (int col : active)
       if (!c.done_h[col]) next.push_back(col);
@@ -1391,6 +1463,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   c.last_ms[4] = static_cast<double>(launches + 2);
   c.last_ms[5] = static_cast<double>(opapps);
   c.last_ms[6] = static_cast<double>(c.hy_inner_its);  // hybrid: inner K_p applications (column-steps)
+  c.last_ms[7] = busy_ms;  // device time of the GMRES iterations (the rest of [0]: prologue, epilogue, host gaps)
 
   // report (gmres.hpp:31-43 merged as filter_engine.hpp:127-133)
   std::vector<double> res(ncols * q);
@@ -1629,6 +1702,8 @@ int zolo_ctx_create(int device, zolo_ctx** out) {
     CK(cudaEventCreate(&c->ev1));
     CK(cudaEventCreate(&c->ev2));
     CK(cudaEventCreate(&c->ev3));
+    CK(cudaEventCreate(&c->ev4));
+    CK(cudaEventCreate(&c->ev5));
   });
   if (st != ZOLO_OK) {
     g_create_err = c->err;
@@ -1648,7 +1723,7 @@ int zolo_ctx_destroy(zolo_ctx* c) {
   if (c->act_h) cudaFreeHost(c->act_h);
   if (c->act_in_h) cudaFreeHost(c->act_in_h);
   if (c->done_h) cudaFreeHost(c->done_h);
-  for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3, c->tev0, c->tev1})
+  for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3, c->ev4, c->ev5, c->tev0, c->tev1})
     if (ev) cudaEventDestroy(ev);
   cudaStream_t st = c->st;
   delete c;
@@ -1924,7 +1999,7 @@ int apply_filter_batched(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols,
       code = st;  // the reference finishes every column before rethrowing (filter_engine.hpp:134-137)
       err = c.err;
     }
-    for (int i : {0, 2, 3, 4, 5, 6}) ms[i] += c.last_ms[i];
+    for (int i : {0, 2, 3, 4, 5, 6, 7}) ms[i] += c.last_ms[i];
     if (rep) {
       rep->iterations = std::max(rep->iterations, rb.iterations);
       rep->operator_applications += rb.operator_applications;
@@ -1935,7 +2010,7 @@ int apply_filter_batched(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols,
       }
     }
   }
-  for (int i : {0, 2, 3, 4, 5, 6}) c.last_ms[i] = ms[i];
+  for (int i : {0, 2, 3, 4, 5, 6, 7}) c.last_ms[i] = ms[i];
   if (code != ZOLO_OK) c.err = err;
   return code;
 }
@@ -2032,6 +2107,7 @@ int zolo_sweep_profile(const zolo_ctx* c, int64_t* out) {
     out[4] = c->sp_nslots;
     out[5] = c->critical_path;
     out[6] = 0;
+    out[7] = c->sel_K;
   } else {
     out[1] = c->env_tiles;
     out[5] = c->geom.nbk;
@@ -2048,6 +2124,26 @@ int zolo_nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf,
     block_symbolic(n, rp, ci, nodes, TILE, bs);
     for (int64_t i = 0; i < n; ++i) pos[i] = bs.pos[i];
     if (npad) *npad = bs.npad;
+    return ZOLO_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_DOMAIN;
+  }
+}
+
+int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* out) {
+  try {
+    std::vector<std::vector<int64_t>> nodes;
+    nd_order(n, rp, ci, leaf, nodes);
+    BlockStructure bs;
+    block_symbolic(n, rp, ci, nodes, TILE, bs);
+    for (int i = 0; i < 8; ++i) out[i] = 0;
+    out[0] = bs.npad;
+    out[1] = bs.nb;
+    out[2] = bs.ntiles;
+    out[3] = bs.critical_path;
+    out[4] = bs.nb - trailing_dense_start(bs, 1 << 20);
+    out[5] = static_cast<int64_t>(nodes.size());
     return ZOLO_OK;
   } catch (const std::exception& e) {
     g_create_err = e.what();

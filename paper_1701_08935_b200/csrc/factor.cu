@@ -628,6 +628,111 @@ __global__ void __launch_bounds__(256) swizzle_tile_kernel(cd* tiles) {
   }
 }
 
+// ---- selective inversion of the trailing dense block (host.hpp DT_*) ------
+// M = (I + N)^{-1} for S = [s0, s0 + K): N = the row-scaled L~_SS (mode 0,
+// strictly lower) or U~_SS (mode 1, strictly upper). One CTA per block column
+// k walks its rows in dependency order, M(i,k) = -sum_j N(i,j) M(j,k) with
+// M(k,k) = I, on DMMA in a fixed order. tab[a*K + b] (a > b) = tile id of
+// L(s0+a, s0+b) (= of U(s0+b, s0+a)); out at strict index a(a-1)/2 + b with
+// (a, b) = (larger, smaller) block index.
+constexpr int SELINV_SMEM = (TT + XS2) * static_cast<int>(sizeof(cd));
+__device__ __forceinline__ size_t sel_sidx(int a, int b) { return static_cast<size_t>(a) * (a - 1) / 2 + b; }
+__device__ __forceinline__ size_t sel_didx(int a, int b) { return static_cast<size_t>(a) * (a + 1) / 2 + b; }
+
+__device__ __forceinline__ void identity_x32(cd* xs) {
+  for (int e = threadIdx.x; e < XS2; e += ST) {
+    const int col = e / XPAD, row = e % XPAD;
+    xs[e] = mk(col == row ? 1.0 : 0.0, 0.0);
+  }
+}
+
+__device__ __forceinline__ void store_tile_acc(const Acc8& acc, const Frag& f, cd* dst, double sign) {
+  cd o[4];
+  acc8_fold(acc, o);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) dst[ocol(f, q) * TILE + f.row] = cscale(o[q], sign);
+}
+
+__global__ void __launch_bounds__(ST) selinv_kernel(int mode, int K, const int* tab, const cd* N, cd* out) {
+  extern __shared__ __align__(16) unsigned char sel_smem[];
+  cd* ts = reinterpret_cast<cd*>(sel_smem);
+  cd* xs = ts + TT;
+  const int k = blockIdx.x;
+  const Frag f = frag();
+  const unsigned long long pol = l2_evict_normal();
+  const int nsteps = mode == 0 ? K - 1 - k : k;
+  for (int s = 0; s < nsteps; ++s) {
+    const int i = mode == 0 ? k + 1 + s : k - 1 - s;
+    Acc8 acc;
+    acc8_zero(acc);
+    const int nj = mode == 0 ? i - k : k - i;
+    for (int q = 0; q < nj; ++q) {
+      const int j = mode == 0 ? k + q : k - q;
+      const int tid = mode == 0 ? tab[i * K + j] : tab[j * K + i];
+      load_tile_sw(ts, N + static_cast<size_t>(tid) * TT, pol);
+      if (j == k)
+        identity_x32(xs);
+      else
+        load_x32(xs, out + (mode == 0 ? sel_sidx(j, k) : sel_sidx(k, j)) * TT, TILE, 0, TILE, pol);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      mma_tile2(acc, ts, xs, false, false, f, 0xffu);
+      __syncthreads();
+    }
+    store_tile_acc(acc, f, out + (mode == 0 ? sel_sidx(i, k) : sel_sidx(k, i)) * TT, -1.0);
+    __threadfence();  // this column's later steps read the tile back through L2
+    __syncthreads();
+  }
+}
+
+// Backward-sweep tiles of S, index a(a+1)/2 + b (a >= b), from the strict inverses:
+// mode 0: W(b, a) = MU(b, a) DinvU_a (MU(a, a) = I), MU(b, a) stored at sel_sidx(a, b);
+// mode 1: X(a, b) = DinvU_a ML(a, b) (ML(a, a) = I), ML(a, b) stored at sel_sidx(a, b).
+__global__ void __launch_bounds__(ST) selinv_post_kernel(int mode, int s0, const cd* DinvU, const cd* M, cd* out) {
+  extern __shared__ __align__(16) unsigned char sel_smem[];
+  cd* ts = reinterpret_cast<cd*>(sel_smem);
+  cd* xs = ts + TT;
+  const int p = blockIdx.x;
+  int a = static_cast<int>((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+  while (static_cast<int64_t>(a + 1) * (a + 2) / 2 <= p) ++a;
+  while (static_cast<int64_t>(a) * (a + 1) / 2 > p) --a;
+  const int b = p - a * (a + 1) / 2;
+  const cd* D = DinvU + static_cast<size_t>(s0 + a) * TT;
+  cd* dst = out + static_cast<size_t>(p) * TT;
+  if (a == b) {
+    for (int e = threadIdx.x; e < TT; e += ST) dst[e] = D[e];
+    return;
+  }
+  const cd* Mt = M + sel_sidx(a, b) * TT;
+  const unsigned long long pol = l2_evict_normal();
+  const Frag f = frag();
+  load_tile_sw(ts, mode == 0 ? Mt : D, pol);
+  load_x32(xs, mode == 0 ? D : Mt, TILE, 0, TILE, pol);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  Acc8 acc;
+  acc8_zero(acc);
+  mma_tile2(acc, ts, xs, false, false, f, 0xffu);
+  store_tile_acc(acc, f, dst, 1.0);
+}
+
+void selinv(cudaStream_t st, int K, int s0, const int* tab, const SpFactor& f, cd* ML, cd* MU, cd* WU, cd* WX) {
+  if (K < 2) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(selinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SELINV_SMEM);
+    cudaFuncSetAttribute(selinv_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SELINV_SMEM);
+    attr = true;
+  }
+  selinv_kernel<<<K, ST, SELINV_SMEM, st>>>(0, K, tab, f.Lt, ML);
+  selinv_kernel<<<K, ST, SELINV_SMEM, st>>>(1, K, tab, f.Ut, MU);
+  const unsigned npair = static_cast<unsigned>(K) * (K + 1) / 2;
+  selinv_post_kernel<<<npair, ST, SELINV_SMEM, st>>>(0, s0, f.DinvU, MU, WU);
+  if (WX) selinv_post_kernel<<<npair, ST, SELINV_SMEM, st>>>(1, s0, f.DinvU, ML, WX);
+}
+
 void swizzle_tiles(cudaStream_t st, cd* tiles, int64_t ntiles) {
   if (ntiles > 0) swizzle_tile_kernel<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(tiles);
 }

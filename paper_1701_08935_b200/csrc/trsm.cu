@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "band.cuh"
+#include "host.hpp"
 #include "mma.cuh"
 
 namespace zolo {
@@ -886,29 +887,33 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       recp[lane] = rec_lo;
       recp[lane + 32] = rec_hi;
       __syncwarp();
-      const int i = recp[0], nd = recp[1], pa = recp[2], pc = recp[3], out = recp[4];
+      const int i = recp[0], nd = recp[1], pa = recp[2], pc = recp[3], out = recp[4], tf = recp[5];
       const bool chunk = out >= 0;
+      // task kinds of the selectively inverted trailing block (host.hpp DT_*)
+      const bool slotdep = tf & DT_SLOTDEP, srcdep = tf & DT_SRCDEP, invdep = slotdep || srcdep;
+      const bool bentry = (!chunk || (tf & DT_BENTRY)) && !(tf & DT_NOB);
       const Chain& ch = chs[ci];
       const int c0 = gi * DCG, nc = min(DCG, A.ncols - c0);
       const size_t cgi = static_cast<size_t>(ci) * A.ngroups + gi;
       const int* flags = A.flags + cgi * A.s.nb;
       const int* cflags = A.cflags + cgi * A.nslots;
+      const int* dflags = slotdep ? cflags : flags;  // where dependency q's readiness lives
       // occupancy masks of all the task's tiles (lane q: dependency q, lane 31: the pre-transform)
       // and readiness of every dependency, each read in parallel (one round trip)
       uint2 my_mask = make_uint2(0xffffffffu, 0xffffffffu);
       if (lane < nd) {
-        if (ch.offm) my_mask = ch.offm[recp[DAG_REC_HDR + 2 * lane + 1]];
-      } else if (lane == 31 && !chunk && ch.pre && ch.prem) {
+        if (ch.offm && !invdep) my_mask = ch.offm[recp[DAG_REC_HDR + 2 * lane + 1]];
+      } else if (lane == 31 && bentry && ch.pre && ch.prem) {
         my_mask = ch.prem[i];
       }
-      const unsigned dep_ready =
-          __ballot_sync(0xffffffffu, lane >= nd || ld_acquire(flags + recp[DAG_REC_HDR + 2 * lane]) >= A.epoch);
+      const unsigned dep_ready = __ballot_sync(
+          0xffffffffu, lane >= nd || srcdep || ld_acquire(dflags + recp[DAG_REC_HDR + 2 * lane]) >= A.epoch);
       auto mask_of = [&](int q) {
         return make_uint2(__shfl_sync(0xffffffffu, my_mask.x, q), __shfl_sync(0xffffffffu, my_mask.y, q));
       };
-      const int nent = (chunk ? 0 : 1) + pc + nd;
+      const int nent = (bentry ? 1 : 0) + pc + nd;
       int e = 0;
-      if (!chunk) {
+      if (bentry) {
         ++e;
         const uint2 pm = mask_of(31);
         if (ch.pre)
@@ -936,12 +941,19 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         const int j = recp[DAG_REC_HDR + 2 * q], tid = recp[DAG_REC_HDR + 2 * q + 1];
         if (!((dep_ready >> q) & 1u)) {
           const unsigned long long tw = trp ? gtimer() : 0;
-          warp_wait_flag(flags + j, A.epoch, A.counter + 2);
+          warp_wait_flag(dflags + j, A.epoch, A.counter + 2);
           if (trp) wsum += gtimer() - tw;
         }
         ++e;
-        produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, mask_of(q), ch.dst + static_cast<int64_t>(j) * TILE,
-                A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
+        if (!invdep)
+          produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, mask_of(q), ch.dst + static_cast<int64_t>(j) * TILE,
+                  A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
+        else if (slotdep)  // M(i,k) S_k, S_k = -c_k from its slot
+          produce(0, 0, ch.minv + static_cast<size_t>(tid) * TT, mask_of(q),
+                  ch.cbuf + static_cast<int64_t>(j) * TILE, A.ldp, c0, nc, pol_stream, e == nent, i, ci, gi, out);
+        else  // -W(i,k) b_k (b_k staged into slot j before the launch: the sweep runs in place)
+          produce(0, 1, ch.minv + static_cast<size_t>(tid) * TT, mask_of(q), ch.cbuf + static_cast<int64_t>(j) * TILE,
+                  A.ldp, c0, nc, pol_stream, e == nent, i, ci, gi, out);
       }
       __syncwarp();
       if (trp && lane == 0) {
@@ -1022,6 +1034,17 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
   }
 }
 
+// cbuf[dst_row0 + r, c] = src[row0 + r, c] for every chain: the sweep input of the selectively
+// inverted block staged where the in-place backward sweep cannot overwrite it (host.hpp DT_SRCDEP)
+__global__ void stage_rows_kernel(const Chain* chains, int64_t row0, int64_t rows, int64_t ld, int64_t ldp,
+                                  int64_t dst_row0) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  const Chain& ch = chains[blockIdx.z];
+  const int64_t c = blockIdx.y;
+  ch.cbuf[dst_row0 + r + c * ldp] = ch.src[row0 + r + c * ld];
+}
+
 // x_i <- op(D_i) x_i per (block row, 16-column group): the adjoint post-pass.
 __global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd* x, int ncols, int64_t ld,
                                                       int swizzled) {
@@ -1060,9 +1083,16 @@ void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int 
 
 int dag_groups(int ncols) { return (ncols + DCG - 1) / DCG; }
 
+void dag_stage_inputs(cudaStream_t st, const Chain* d_chains, int nchains, int64_t row0, int64_t rows, int ncols,
+                      int64_t ld, int64_t ldp, int64_t dst_row0) {
+  if (rows <= 0 || ncols <= 0 || nchains <= 0) return;
+  stage_rows_kernel<<<dim3(static_cast<unsigned>((rows + 255) / 256), ncols, nchains), 256, 0, st>>>(
+      d_chains, row0, rows, ld, ldp, dst_row0);
+}
+
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
-                    unsigned long long* trace, const int* tmap, bool presw) {
+                    unsigned long long* trace, const int* tmap, bool presw, bool need_v2) {
   const int smem = DAG_SMEM_FIXED + (2 * DAG_REC + DAG_REC_DEPS + 8) * static_cast<int>(sizeof(int));
   static int attr_set = 0;
   if (smem > attr_set) {
@@ -1114,6 +1144,7 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
     if (grid > 0) dag2_kernel<<<grid, P2T, DAG2_SMEM, st>>>(a);
     return grid;
   }
+  if (need_v2) return -1;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel, ST, smem);
   if (per_sm < 1) per_sm = 1;

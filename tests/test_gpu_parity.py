@@ -253,3 +253,41 @@ np.savez(sys.argv[1], y=y, it=rep.iterations, ops=rep.operator_applications, col
     a, b = outs
     assert (a["y"] == b["y"]).all()
     assert int(a["it"]) == int(b["it"]) and int(a["ops"]) == int(b["ops"]) and (a["cols"] == b["cols"]).all()
+
+
+@pytest.mark.parametrize("case", ["filter_cfg2_k6", "filter_cfg3_k5", "filter_cfg1_k16"])
+def test_selective_inversion_matches_plain_sweeps(zb, case):
+    """The trailing dense block of the factors is selectively inverted (host.hpp DT_*: its serial
+    chain becomes two parallel layers forward, one backward). The filtered block must equal the one
+    of the plain sweeps (ZOLO_SELINV=0, read once per process -> subprocesses) to rounding, with the
+    same Krylov dimensions."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from conftest import load_golden, golden_pencil
+import paper_1701_08935_b200 as zb
+g = load_golden(sys.argv[2])
+op = zb.FilterOperator(golden_pencil(g), g["design"], int(g["r"]), is_complex=bool(g["cx"]), nd_leaf=64)
+prof = op.sweep_profile()
+y, rep = op.apply_filter(g["v"])
+ga = op.apply_g(g["v"])
+np.savez(sys.argv[1], y=y, ga=ga, cols=np.array(rep.column_iterations), ref=g["y"], sel=prof.get("selinv_rows", 0))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for kmax in ("0", "4096"):
+        f = tempfile.mktemp(suffix=".npz")
+        env = dict(os.environ, ZOLO_SELINV=kmax)
+        subprocess.run([sys.executable, "-c", code, f, case], check=True, cwd=root, env=env, timeout=300)
+        outs.append(np.load(f))
+    plain, inv = outs
+    assert int(plain["sel"]) == 0 and int(inv["sel"]) >= 2  # the inverted block is exercised
+    scale = np.linalg.norm(plain["ga"])
+    assert np.linalg.norm(inv["ga"] - plain["ga"]) <= 1e-12 * scale
+    assert np.linalg.norm(inv["y"] - inv["ref"]) <= 1e-9 * np.linalg.norm(inv["ref"])
+    assert np.abs(inv["cols"] - plain["cols"]).max() <= 1

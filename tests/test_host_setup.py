@@ -27,6 +27,20 @@ def test_library_exports_every_declared_symbol():
     assert b"sm_100a" in L.zolo_version()
 
 
+def test_library_has_no_unresolved_internal_symbols():
+    """Every internal (zolo::) symbol the library references is defined in it: an unresolved one
+    only surfaces when the GPU box loads the library (dlopen with immediate binding)."""
+    import shutil
+    import subprocess
+
+    if not shutil.which("nm"):
+        pytest.skip("nm not available")
+    lib = os.path.join(REPO, "paper_1701_08935_b200", "libzolo_b200.so")
+    out = subprocess.run(["nm", "-D", "--undefined-only", lib], capture_output=True, text=True, check=True).stdout
+    bad = [ln for ln in out.splitlines() if "_ZN4zolo" in ln]
+    assert not bad, bad
+
+
 def test_no_device_fails_loudly():
     """Without a GPU the operator must raise, never fall back to the CPU."""
     import torch

@@ -31,7 +31,9 @@ for name in sys.argv[1:] or ["cfg1", "cfg2"]:
         tm = op.last_timings()
         print(f"  apply_filter wall {t1 - t0:.3f}s device {tm['filter_ms']:.1f} ms trsm {tm['trsm_ms']:.1f} ms"
               f" ({tm['trsm_launches']} launches) iters {rep.iterations} min_col {min(rep.column_iterations)}"
-              f" -> {nv / (tm['filter_ms'] / 1e3):.1f} vec/s", flush=True)
+              f" -> {nv / (tm['filter_ms'] / 1e3):.1f} vec/s; iterations {tm['iterations_ms']:.1f} ms on device"
+              f" (aux {tm['iterations_ms'] - tm['trsm_ms']:.1f} ms, outside {tm['filter_ms'] - tm['iterations_ms']:.1f} ms)",
+              flush=True)
         flops = tm["operator_applications"] * r * (2 if cx else 1) * 2 * (sp["offdiag_tiles"] + sp["block_rows"]) * 8192.0
         print(f"  solve: {flops / (tm['trsm_ms'] * 1e-3) / 1e12:.1f} TF/s over stored tiles", flush=True)
     if name == "cfg1" or os.environ.get("CHECK_ORACLE"):
