@@ -1519,6 +1519,11 @@ void apply_g_impl(zolo_ctx& c, const double* v, double* gv, int64_t k) {
   Krylov<S>::permute_out(c.st, c.w.as<S>(), ld, c.vin_orig.as<S>(), n, k, c.perm_d.as<int>());
   CK(cudaMemcpyAsync(gv, c.vin_orig.p, c.es() * n * k, cudaMemcpyDeviceToHost, c.st));
   CK(cudaStreamSynchronize(c.st));
+  if (!c.hybrid) {  // sweep time of this application (last_timings trsm_ms)
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c.ev2, c.ev3));
+    c.last_ms[2] = ms;
+  }
   // filter_engine.hpp:58,70,79: one application per call, r or 2r solves
   c.g_apps += 1;
   c.inner_solves += c.nchains();

@@ -784,10 +784,14 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       __syncwarp();
       if (tile && lane == 0) bulk_copy(tile_s(s), tile, TT * sizeof(cd), full + s, pol_stream);
       cd* xs = x_s(s);
+#ifdef ZOLO_XPROBE  // (development timing probe, wrong results) one contiguous copy per block
+      if (lane == 0) bulk_copy(xs, blk + c0 * stride, nc * TILE * sizeof(cd), full + s, pol);
+#else
       if (lane < nc)
         bulk_copy(xs + lane * XPAD, blk + (c0 + lane) * stride, TILE * sizeof(cd), full + s, pol);
       else
         for (int r = 0; r < TILE; ++r) xs[lane * XPAD + r] = mk(0.0, 0.0);
+#endif
       __syncwarp();
       if (lane == 0) {
         Meta2 m;

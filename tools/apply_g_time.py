@@ -14,6 +14,9 @@ op = zb.FilterOperator(pen, build_filter_design(gaps, r), r, is_complex=cx)
 v = zb.random_block(pen[0], nv, 1, cx=cx)
 op.apply_g(v)
 t0 = time.time()
+sw = []
 for _ in range(5):
     op.apply_g(v)
-print(f"{name} {os.environ.get('ZOLO_LIB_PATH', 'default')}: apply_g {1e3 * (time.time() - t0) / 5:.2f} ms", flush=True)
+    sw.append(op.last_timings()["trsm_ms"])
+print(f"{name} {os.environ.get('ZOLO_LIB_PATH', 'default')}: apply_g {1e3 * (time.time() - t0) / 5:.2f} ms, "
+      f"sweeps {min(sw):.3f} ms (min of 5)", flush=True)
