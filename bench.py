@@ -341,15 +341,23 @@ def main():
         # subspace iterations to tol 1e-10, eigensolver.hpp:154-217) through zolo_subspace_iteration
         from paper_1701_08935_b200.driver import SolveConfig, subspace_iteration
 
-        res = subspace_iteration(pen, gaps, SolveConfig(n_lambda=nl, oversample_k=nv - nl, r=r, tol=1e-10, seed=1),
-                                 is_complex=cx, device=local)
+        # three independent solves (each builds its own context: ordering, symbolic analysis, factors); the
+        # median is reported with all three (the first solve of a process pays one-time host/driver costs)
+        runs = []
+        for _ in range(3):
+            res = subspace_iteration(pen, gaps, SolveConfig(n_lambda=nl, oversample_k=nv - nl, r=r, tol=1e-10,
+                                                            seed=1), is_complex=cx, device=local)
+            runs.append((res.time_to_all_eigenpairs, res))
+        runs.sort(key=lambda x: x[0])
+        res = runs[1][1]
         # the window's eigenvalue count by Sylvester inertia (BASELINE config 2: "counted by the oracle via
         # Sylvester inertia"), on the GPU
         ctr = zb.InertiaCounter(pen, is_complex=cx, device=local)
         inertia = ctr.count_in(0.5 * (gaps[0] + gaps[1]), 0.5 * (gaps[2] + gaps[3]))
         del ctr
         line["time_to_all_eigenpairs"] = {
-            "value": res.time_to_all_eigenpairs, "unit": "s", "t_factor_s": res.stats.factorization_time,
+            "value": res.time_to_all_eigenpairs, "unit": "s", "runs_s": [round(t, 4) for t, _ in runs],
+            "statistic": "median of 3 solves", "t_factor_s": res.stats.factorization_time,
             "t_iter_s": res.stats.iteration_time, "found": int(len(res.lambdas)), "n_lambda": nl,
             "converged": bool(res.converged), "residual": res.residual, "n_iter": res.stats.n_iter,
             "n_gmres": res.stats.n_gmres, "inertia_count": inertia}
