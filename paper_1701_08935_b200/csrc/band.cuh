@@ -174,6 +174,11 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
                     unsigned long long* trace = nullptr, const int* tmap = nullptr, bool presw = false,
                     bool need_v2 = false);
 int dag_groups(int ncols);
+// forward + backward sweeps in one launch (v2 kernel); tmap: fused claim map (bit 30 = backward), or
+// nullptr for forward-then-backward order. Returns the grid, or -1 when the v2 kernel cannot run it.
+int dag_fused_launch(cudaStream_t st, const SpGeom& s, const DagSched& sf, const DagSched& sb, const Chain* d_fwd,
+                     const Chain* d_bwd, int nchains, int ncols, int64_t ld, int* flags, int* cflags, int epoch,
+                     int* counter, int num_sms, const int* tmap);
 // chains' cbuf rows [dst_row0, dst_row0 + rows) <- their src rows [row0, row0 + rows), all ncols columns
 void dag_stage_inputs(cudaStream_t st, const Chain* d_chains, int nchains, int64_t row0, int64_t rows, int ncols,
                       int64_t ld, int64_t ldp, int64_t dst_row0);

@@ -158,6 +158,8 @@ struct zolo_ctx {
   DevMem sp_seltab, sel_mem;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
   DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
+  DevMem sp_tmap_fused;  // claim map of the fused forward + backward launch (dag_fused_launch)
+  int tmap_fused_nch = -1;
   int tmap_nch = -1;  // chain count the staggered claim maps were built for
   DevMem sp_er, sp_ec, sp_ea, sp_eb;  // scatter lists of the union pattern in the factor ordering
   int64_t sp_nnz = 0;
@@ -613,6 +615,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
         const int nd = k.qb - k.qa;
         require(nd <= DAG_REC_DEPS, "zolo_factorize: DAG task record overflow");
         r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out, r[5] = k.flags;
+        if (!fwd && k.out < 0 && ndall == 0 && !(k.flags & (DT_SRCDEP | DT_SLOTDEP))) r[5] |= DT_FWDWAIT;
         for (int q = 0; q < nd; ++q) {
           int j, tid;
           if (k.flags & DT_SRCDEP) {  // W(i, kk), kk = nb-1 .. i: input block kk, staged in slot base + kk - s0
@@ -643,6 +646,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     upload(c.sp_sched_bwd, records(tb, false), c.st);
     c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), static_cast<int>(tf.size()), sf};
     c.tmap_nch = -1;
+    c.tmap_fused_nch = -1;
     c.sp_tmap_fwd.release();
     c.sp_tmap_bwd.release();
     c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb + c.sel_K};
@@ -986,6 +990,30 @@ void build_tmap(zolo_ctx& c, int nch) {
   }
 }
 
+// Claim map of the fused launch: every (direction, record, chain) keyed by its sweep progress
+// (forward in [0, 1), backward in [1, 2)) plus a per-chain stagger (ZOLO_FUSE_STAGGER, odd chains
+// shifted), stable-sorted; topological within each chain, chains are independent.
+void build_fused_tmap(zolo_ctx& c, int nch) {
+  static const double stagger = [] {
+    const char* v = std::getenv("ZOLO_FUSE_STAGGER");
+    return v ? std::atof(v) : 0.0;
+  }();
+  const int ntf = c.sched_fwd.ntask, ntb = c.sched_bwd.ntask;
+  std::vector<std::pair<double, int>> key;
+  key.reserve(static_cast<size_t>(ntf + ntb) * nch);
+  for (int dir = 0; dir < 2; ++dir) {
+    const int nt = dir ? ntb : ntf;
+    for (int p = 0; p < nt; ++p)
+      for (int ci = 0; ci < nch; ++ci)
+        key.emplace_back(dir + static_cast<double>(p) / nt + stagger * (ci & 1), (dir << 30) | (p * nch + ci));
+  }
+  std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::vector<int> map(key.size());
+  for (size_t k = 0; k < key.size(); ++k) map[k] = key[k].second;
+  upload(c.sp_tmap_fused, map, c.st);
+  c.tmap_fused_nch = nch;
+}
+
 void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* trace = nullptr) {
   const int64_t ld = c.geom.npad;
   unsigned long long* fx = c.flags.as<unsigned long long>();
@@ -994,6 +1022,22 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
   if (c.tmap_nch != c.nchains()) build_tmap(c, c.nchains());
   const bool full = first == 0 && nsub == c.nchains() && c.sp_tmap_fwd.p && c.tmap_nch == nsub;
   const bool presw = c.tiles[0].swz;
+  static const bool fuse = env_int("ZOLO_DAG_FUSED", 0) != 0 && env_int("ZOLO_DAG_V2", 1) != 0;  // measured equal to two launches; staggered chains slower
+  if (fuse && !trace && c.sel_K == 0 && presw && nsub <= 32) {
+    // one launch for both sweep directions (dag_fused_launch)
+    if (c.tmap_fused_nch != nsub) build_fused_tmap(c, nsub);
+    const int g = dag_fused_launch(c.st, c.sgeom, c.sched_fwd, c.sched_bwd, c.chains_fwd.as<Chain>() + first,
+                                   c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf, c.epoch + 1,
+                                   c.counter.as<int>(), c.num_sms, c.sp_tmap_fused.as<int>());
+    c.epoch += 2;
+    if (g < 0) throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: fused sweep launch failed");
+    if (c.cx)
+      for (int ci = first; ci < first + nsub; ++ci)
+        if (ci & 1)
+          blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true, c.xbuf[ci]->as<cd>(), na, ld,
+                          c.tiles[ci / 2].swz);
+    return;
+  }
   const bool need_v2 = c.sel_K > 0;  // the selectively inverted block's task kinds exist only in dag2_kernel
   const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf,
                                  ++c.epoch, c.counter.as<int>(), 1, c.num_sms, trace,

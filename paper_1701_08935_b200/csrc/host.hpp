@@ -60,6 +60,8 @@ constexpr int DT_BENTRY = 1;   // chunk-kind task (out >= 0) that also takes the
 constexpr int DT_SLOTDEP = 2;  // dependencies are (slot of c_k, inverse tile id)
 constexpr int DT_SRCDEP = 4;   // dependencies are (block row k of the sweep input, inverse tile id)
 constexpr int DT_NOB = 8;      // row task without the b_i entry
+constexpr int DT_FWDWAIT = 16; // backward root (no backward dependencies; informational: in a fused
+                               // launch every backward row task waits for its forward u_i)
 struct DagTask {
   int i, qa, qb, pa, pc, out;
   int flags = 0;

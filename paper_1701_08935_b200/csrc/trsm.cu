@@ -441,6 +441,14 @@ struct DagArgs {
   const int* tmap;            // v2, optional: claim slot k -> record * nchains + chain (groups consecutive)
   int presw;                  // tiles stored pre-swizzled (swizzle_tiles): linear / bulk copies
   int l2pf;                   // v2: L2 prefetch of the next task's tiles / blocks (ZOLO_DAG_L2PF)
+  // v2 fused forward + backward launch (dag_fused_launch): the backward sweep's schedule and
+  // chains; backward tasks run at epoch + 1 and the tmap entries carry bit 30 for them
+  int fused = 0;
+  const int* recs_b = nullptr;
+  const Chain* chains_b = nullptr;
+  int ntask_b = 0, nslots_b = 0;
+  int64_t ldp_b = 0;
+  int cfs = 0;  // chunk-flag stride per (chain, group): one for both directions, so they never alias
 };
 
 // a tile into the swizzled shared layout: permuted on the way (column-major global
@@ -691,7 +699,7 @@ struct Meta2 {
 };
 constexpr int DAG2_CHAINS = 32;
 constexpr int DAG2_SMEM = NST2 * (TSW + XS2) * static_cast<int>(sizeof(cd)) + NST2 * static_cast<int>(sizeof(Meta2)) +
-                          2 * NST2 * 8 + DAG2_CHAINS * static_cast<int>(sizeof(Chain)) + DAG_REC * 4;
+                          2 * NST2 * 8 + 2 * DAG2_CHAINS * static_cast<int>(sizeof(Chain)) + DAG_REC * 4;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
@@ -753,11 +761,14 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
   unsigned long long* full = reinterpret_cast<unsigned long long*>(meta + NST2);
   unsigned long long* empty = full + NST2;
   Chain* chs = reinterpret_cast<Chain*>(empty + NST2);
-  int* recp = reinterpret_cast<int*>(chs + DAG2_CHAINS);
+  int* recp = reinterpret_cast<int*>(chs + 2 * DAG2_CHAINS);
   auto tile_s = [ring](int s) { return ring + s * (TSW + XS2); };
   auto x_s = [ring](int s) { return ring + s * (TSW + XS2) + TSW; };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int q = threadIdx.x; q < A.nchains; q += blockDim.x) chs[q] = A.chains[q];
+  for (int q = threadIdx.x; q < A.nchains; q += blockDim.x) {
+    chs[q] = A.chains[q];
+    if (A.fused) chs[DAG2_CHAINS + q] = A.chains_b[q];
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST2; ++s) {
       mbar_init(full + s, 1);    // the producer's arrive (+ the stage's bulk-copy bytes)
@@ -766,13 +777,15 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
   }
   __syncthreads();
   const int per_step = A.nchains * A.ngroups;
-  const int ntasks = A.ntask * per_step;
+  const int ntasks_f = A.ntask * per_step;
+  const int ntasks = ntasks_f + (A.fused ? A.ntask_b * per_step : 0);
   if (warp == ST / 32) {
     // ------------------------------ producer ------------------------------
     const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
     int g = 0;
     // one ring entry: tile (optional) + a 32 x 32 block with column stride `stride`
     int cur_t = 0;  // claim index of the task being produced (trace)
+    int cur_dir = 0;  // fused launch: 1 while producing a backward task
     auto produce = [&](int kind, int sign, const cd* tile, uint2 mw, const cd* blk, int64_t stride, int c0,
                        int nc, unsigned long long pol, int last, int i, int ci, int gi, int out) {
       const int s = g % NST2, round = g / NST2;
@@ -806,24 +819,30 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         m.out = out;
         m.nc = nc;
         m.pad0 = cur_t;
+        m.pad1 = cur_dir;
         meta[s] = m;
         mbar_arrive(full + s);
       }
       ++g;
     };
-    auto decode = [&](int tt, int& r, int& ci, int& gi) {
+    auto decode = [&](int tt, int& r, int& ci, int& gi, int& dir) {
       if (A.tmap) {  // chains staggered in the claim order (each chain keeps its topological order)
-        const int rc = A.tmap[tt / A.ngroups];
+        int rc = A.tmap[tt / A.ngroups];
+        dir = (rc >> 30) & 1;
+        rc &= (1 << 30) - 1;
         r = rc / A.nchains;
         ci = rc % A.nchains;
         gi = tt % A.ngroups;
       } else {
+        dir = tt >= ntasks_f;
+        if (dir) tt -= ntasks_f;
         r = tt / per_step;
         const int rem = tt % per_step;
         ci = rem / A.ngroups;
         gi = rem % A.ngroups;
       }
     };
+    auto recs_of = [&](int dir) { return dir ? A.recs_b : A.recs; };
     // Claims run two tasks ahead: when task T starts, T+1's id has arrived (its record load is
     // issued now and lands while T streams) and the atomic for T+2 goes out.
     int t = 0;
@@ -831,10 +850,10 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     t = __shfl_sync(0xffffffffu, t, 0);
     int rec_lo = 0, rec_hi = 0;  // this lane's two words of the current task's record
     if (t < ntasks) {
-      int r0, c0_, g0_;
-      decode(t, r0, c0_, g0_);
-      rec_lo = A.recs[static_cast<size_t>(r0) * DAG_REC + lane];
-      rec_hi = A.recs[static_cast<size_t>(r0) * DAG_REC + lane + 32];
+      int r0, c0_, g0_, d0_;
+      decode(t, r0, c0_, g0_, d0_);
+      rec_lo = recs_of(d0_)[static_cast<size_t>(r0) * DAG_REC + lane];
+      rec_hi = recs_of(d0_)[static_cast<size_t>(r0) * DAG_REC + lane + 32];
     }
     int tn_raw = 0;
     if (lane == 0) tn_raw = atomicAdd(A.counter, 1);
@@ -846,10 +865,10 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       const int tn = __shfl_sync(0xffffffffu, tn_raw, 0);
       int nrec_lo = 0, nrec_hi = 0;
       if (tn < ntasks) {
-        int rn_, cn_, gn_;
-        decode(tn, rn_, cn_, gn_);
-        nrec_lo = A.recs[static_cast<size_t>(rn_) * DAG_REC + lane];
-        nrec_hi = A.recs[static_cast<size_t>(rn_) * DAG_REC + lane + 32];
+        int rn_, cn_, gn_, dn_;
+        decode(tn, rn_, cn_, gn_, dn_);
+        nrec_lo = recs_of(dn_)[static_cast<size_t>(rn_) * DAG_REC + lane];
+        nrec_hi = recs_of(dn_)[static_cast<size_t>(rn_) * DAG_REC + lane + 32];
       }
       if (lane == 0) tn_raw = atomicAdd(A.counter, 1);
       if (A.l2pf && tn < ntasks) {
@@ -886,8 +905,11 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       unsigned long long* trp = A.trace ? A.trace + DAG_TRACE_WORDS * static_cast<size_t>(t) : nullptr;
       unsigned long long wsum = 0;
       if (trp && lane == 0) trp[0] = gtimer();
-      int r, ci, gi;
-      decode(t, r, ci, gi);
+      int r, ci, gi, dir;
+      decode(t, r, ci, gi, dir);
+      cur_dir = dir;
+      const int epoch = A.epoch + dir;
+      const int64_t ldp = dir ? A.ldp_b : A.ldp;
       recp[lane] = rec_lo;
       recp[lane + 32] = rec_hi;
       __syncwarp();
@@ -896,11 +918,11 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       // task kinds of the selectively inverted trailing block (host.hpp DT_*)
       const bool slotdep = tf & DT_SLOTDEP, srcdep = tf & DT_SRCDEP, invdep = slotdep || srcdep;
       const bool bentry = (!chunk || (tf & DT_BENTRY)) && !(tf & DT_NOB);
-      const Chain& ch = chs[ci];
+      const Chain& ch = chs[ci + dir * DAG2_CHAINS];
       const int c0 = gi * DCG, nc = min(DCG, A.ncols - c0);
       const size_t cgi = static_cast<size_t>(ci) * A.ngroups + gi;
       const int* flags = A.flags + cgi * A.s.nb;
-      const int* cflags = A.cflags + cgi * A.nslots;
+      const int* cflags = A.cflags + cgi * A.cfs;
       const int* dflags = slotdep ? cflags : flags;  // where dependency q's readiness lives
       // occupancy masks of all the task's tiles (lane q: dependency q, lane 31: the pre-transform)
       // and readiness of every dependency, each read in parallel (one round trip)
@@ -911,53 +933,61 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         my_mask = ch.prem[i];
       }
       const unsigned dep_ready = __ballot_sync(
-          0xffffffffu, lane >= nd || srcdep || ld_acquire(dflags + recp[DAG_REC_HDR + 2 * lane]) >= A.epoch);
+          0xffffffffu, lane >= nd || srcdep || ld_acquire(dflags + recp[DAG_REC_HDR + 2 * lane]) >= epoch);
       auto mask_of = [&](int q) {
         return make_uint2(__shfl_sync(0xffffffffu, my_mask.x, q), __shfl_sync(0xffffffffu, my_mask.y, q));
       };
       const int nent = (bentry ? 1 : 0) + pc + nd;
       int e = 0;
+      // fused launch: a backward task's b_i is the forward sweep's u_i of the same chain, which may
+      // still be in flight when the task is claimed (claims are topological, completions are not)
+      if (A.fused && dir && bentry && ld_acquire(flags + i) < A.epoch) {
+        const unsigned long long tw = trp ? gtimer() : 0;
+        warp_wait_flag(flags + i, A.epoch, A.counter + 2);
+        if (trp) wsum += gtimer() - tw;
+      }
       if (bentry) {
         ++e;
         const uint2 pm = mask_of(31);
         if (ch.pre)
           produce(0, 1, ch.pre + static_cast<size_t>(i) * TT, pm, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0,
-                  nc, pol_stream, e == nent, i, ci, gi, out);
+                  nc, pol_stream, e == nent, i, ci + dir * DAG2_CHAINS, gi, out);
         else
           produce(1, -1, nullptr, pm, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0, nc, pol_stream, e == nent,
-                  i, ci, gi, out);
+                  i, ci + dir * DAG2_CHAINS, gi, out);
       }
       for (int p0 = 0; p0 < pc; p0 += 32) {
         const unsigned prdy =
-            __ballot_sync(0xffffffffu, p0 + lane >= pc || ld_acquire(cflags + pa + p0 + lane) >= A.epoch);
+            __ballot_sync(0xffffffffu, p0 + lane >= pc || ld_acquire(cflags + pa + p0 + lane) >= epoch);
         for (int p = p0; p < pc && p < p0 + 32; ++p) {
           if (!((prdy >> (p - p0)) & 1u)) {
             const unsigned long long tw = trp ? gtimer() : 0;
-            warp_wait_flag(cflags + pa + p, A.epoch, A.counter + 2);
+            warp_wait_flag(cflags + pa + p, epoch, A.counter + 2);
             if (trp) wsum += gtimer() - tw;
           }
           ++e;
           produce(1, 1, nullptr, make_uint2(0xffffffffu, 0xffffffffu), ch.cbuf + static_cast<int64_t>(pa + p) * TILE,
-                  A.ldp, c0, nc, pol_stream, e == nent, i, ci, gi, out);
+                  ldp, c0, nc, pol_stream, e == nent, i, ci + dir * DAG2_CHAINS, gi, out);
         }
       }
       for (int q = 0; q < nd; ++q) {
         const int j = recp[DAG_REC_HDR + 2 * q], tid = recp[DAG_REC_HDR + 2 * q + 1];
         if (!((dep_ready >> q) & 1u)) {
           const unsigned long long tw = trp ? gtimer() : 0;
-          warp_wait_flag(dflags + j, A.epoch, A.counter + 2);
+          warp_wait_flag(dflags + j, epoch, A.counter + 2);
           if (trp) wsum += gtimer() - tw;
         }
         ++e;
+        const int cix = ci + dir * DAG2_CHAINS;
         if (!invdep)
           produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, mask_of(q), ch.dst + static_cast<int64_t>(j) * TILE,
-                  A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
+                  A.ld, c0, nc, pol_keep, e == nent, i, cix, gi, out);
         else if (slotdep)  // M(i,k) S_k, S_k = -c_k from its slot
           produce(0, 0, ch.minv + static_cast<size_t>(tid) * TT, mask_of(q),
-                  ch.cbuf + static_cast<int64_t>(j) * TILE, A.ldp, c0, nc, pol_stream, e == nent, i, ci, gi, out);
+                  ch.cbuf + static_cast<int64_t>(j) * TILE, ldp, c0, nc, pol_stream, e == nent, i, cix, gi, out);
         else  // -W(i,k) b_k (b_k staged into slot j before the launch: the sweep runs in place)
           produce(0, 1, ch.minv + static_cast<size_t>(tid) * TT, mask_of(q), ch.cbuf + static_cast<int64_t>(j) * TILE,
-                  A.ldp, c0, nc, pol_stream, e == nent, i, ci, gi, out);
+                  ldp, c0, nc, pol_stream, e == nent, i, cix, gi, out);
       }
       __syncwarp();
       if (trp && lane == 0) {
@@ -982,6 +1012,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     if (m.kind == 2) break;
     const Chain& ch = chs[m.ci];
     const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
+    const int mdir = m.pad1;
     ntiles_task += m.kind == 0;
     if (m.kind == 0) {
       mma_tile2(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
@@ -1006,11 +1037,12 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       const bool chunk = m.out >= 0;
       const int c0 = m.gi * DCG;
       if (chunk) {
-        cd* prow = ch.cbuf + static_cast<int64_t>(m.out) * TILE + f.row + c0 * A.ldp;
+        const int64_t ldp = mdir ? A.ldp_b : A.ldp;
+        cd* prow = ch.cbuf + static_cast<int64_t>(m.out) * TILE + f.row + c0 * ldp;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int c = ocol(f, q);
-          if (c < m.nc) prow[c * A.ldp] = o[q];
+          if (c < m.nc) prow[c * ldp] = o[q];
         }
       } else {
         cd* urow = ch.dst + static_cast<int64_t>(m.i) * TILE + f.row + c0 * A.ld;
@@ -1022,8 +1054,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
       consumers_sync();
       if (threadIdx.x == 0) {
-        const size_t cgi = static_cast<size_t>(m.ci) * A.ngroups + m.gi;
-        st_release(chunk ? A.cflags + cgi * A.nslots + m.out : A.flags + cgi * A.s.nb + m.i, A.epoch);
+        const size_t cgi = static_cast<size_t>(m.ci - mdir * DAG2_CHAINS) * A.ngroups + m.gi;
+        st_release(chunk ? A.cflags + cgi * A.cfs + m.out : A.flags + cgi * A.s.nb + m.i, A.epoch + mdir);
         if (A.trace) {
           unsigned long long* trc = A.trace + DAG_TRACE_WORDS * static_cast<size_t>(m.pad0);
           unsigned smid;
@@ -1094,6 +1126,55 @@ void dag_stage_inputs(cudaStream_t st, const Chain* d_chains, int nchains, int64
       d_chains, row0, rows, ld, ldp, dst_row0);
 }
 
+// Forward and backward sweeps of all chains in ONE persistent launch (v2 kernel): backward tasks
+// (epoch + 1) are claimed after the forward tasks of their chain (tmap bit 30), and a backward
+// root waits on the forward flag of its own row (DT_FWDWAIT) -- every other backward row depends
+// on it transitively, as does every forward row of its chain. Lets one chain's narrow top-level
+// phase overlap another chain's wide phase instead of every chain draining at a kernel boundary.
+int dag_fused_launch(cudaStream_t st, const SpGeom& s, const DagSched& sf, const DagSched& sb, const Chain* d_fwd,
+                     const Chain* d_bwd, int nchains, int ncols, int64_t ld, int* flags, int* cflags, int epoch,
+                     int* counter, int num_sms, const int* tmap) {
+  if (nchains > DAG2_CHAINS) return -1;
+  DagArgs a;
+  a.chains = d_fwd;
+  a.nchains = nchains;
+  a.ngroups = (ncols + DCG - 1) / DCG;
+  a.ncols = ncols;
+  a.epoch = epoch;
+  a.fwd = 1;
+  a.ld = ld;
+  a.ldp = static_cast<int64_t>(sf.nslots) * TILE;
+  a.recs = sf.recs;
+  a.ntask = sf.ntask;
+  a.nslots = sf.nslots;
+  a.s = s;
+  a.flags = flags;
+  a.cflags = cflags;
+  a.counter = counter;
+  a.trace = nullptr;
+  a.hints = 3;
+  a.tmap = tmap;
+  a.presw = 1;
+  a.l2pf = 0;
+  a.fused = 1;
+  a.recs_b = sb.recs;
+  a.chains_b = d_bwd;
+  a.ntask_b = sb.ntask;
+  a.nslots_b = sb.nslots;
+  a.ldp_b = static_cast<int64_t>(sb.nslots) * TILE;
+  a.cfs = std::max(sf.nslots, sb.nslots);
+  static bool attr2 = false;
+  if (!attr2) {
+    cudaFuncSetAttribute(dag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DAG2_SMEM);
+    attr2 = true;
+  }
+  cudaMemsetAsync(counter, 0, sizeof(int), st);
+  const int ntasks = (sf.ntask + sb.ntask) * nchains * a.ngroups;
+  const int grid = std::min(ntasks, num_sms * ZOLO_V2_MINB);
+  if (grid > 0) dag2_kernel<<<grid, P2T, DAG2_SMEM, st>>>(a);
+  return grid;
+}
+
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
                     unsigned long long* trace, const int* tmap, bool presw, bool need_v2) {
@@ -1115,6 +1196,7 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   a.recs = sched.recs;
   a.ntask = sched.ntask;
   a.nslots = sched.nslots;
+  a.cfs = sched.nslots;
   a.s = s;
   a.flags = flags;
   a.cflags = cflags;

@@ -291,3 +291,32 @@ np.savez(sys.argv[1], y=y, ga=ga, cols=np.array(rep.column_iterations), ref=g["y
     assert np.linalg.norm(inv["ga"] - plain["ga"]) <= 1e-12 * scale
     assert np.linalg.norm(inv["y"] - inv["ref"]) <= 1e-9 * np.linalg.norm(inv["ref"])
     assert np.abs(inv["cols"] - plain["cols"]).max() <= 1
+
+
+@pytest.mark.parametrize("case", ["filter_cfg2_k6", "filter_cfg3_k5"])
+def test_fused_sweep_launch_is_bitwise_identical(zb, case):
+    """Forward and backward sweeps in one persistent launch (ZOLO_DAG_FUSED=1, dag_fused_launch)
+    accumulate every tile product in the same order as two launches: identical bits."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from conftest import load_golden, golden_pencil
+import paper_1701_08935_b200 as zb
+g = load_golden(sys.argv[2])
+op = zb.FilterOperator(golden_pencil(g), g["design"], int(g["r"]), is_complex=bool(g["cx"]), nd_leaf=64)
+y, rep = op.apply_filter(g["v"])
+np.savez(sys.argv[1], y=y, ga=op.apply_g(g["v"]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for fused in ("0", "1"):
+        f = tempfile.mktemp(suffix=".npz")
+        env = dict(os.environ, ZOLO_DAG_FUSED=fused)
+        subprocess.run([sys.executable, "-c", code, f, case], check=True, cwd=root, env=env, timeout=300)
+        outs.append(np.load(f))
+    assert (outs[0]["y"] == outs[1]["y"]).all() and (outs[0]["ga"] == outs[1]["ga"]).all()
