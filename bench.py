@@ -277,13 +277,19 @@ def main():
                                         C.byref(rep))
         zb._check(op._h, st)
 
-    e2e_step()
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
     if ws > 1:
         torch.distributed.barrier()
     op.timer_start()
+    e2e_wall = []
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         e2e_step()
+        e2e_wall.append((time.perf_counter() - t0) * 1e3)
     e2e_ms = op.timer_stop()
+    print(f"[bench] e2e steps (wall ms): {[round(x, 2) for x in e2e_wall]}, device-timed {e2e_ms / args.steps:.2f} ms",
+          file=sys.stderr, flush=True)
     if ws > 1:
         t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
