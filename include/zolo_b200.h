@@ -108,6 +108,19 @@ int zolo_set_design(zolo_ctx* ctx, const double* design, int r);
  * returns ZOLO_ERR_FACTORIZATION with stats[j].pivot_index set. */
 int zolo_factorize(zolo_ctx* ctx, const int64_t* perm, zolo_factor_stats* stats);
 
+/* Block (BSR) structure of the pencil (BASELINE config 4: dense b x b blocks
+ * per atom; no reference equivalent -- the reference reads CSR only): rows
+ * [k b, (k + 1) b) form atom k. The nested dissection then runs on the atom
+ * graph and keeps every atom's rows contiguous, and the B products of the
+ * filter and the A / B products of the Rayleigh-Ritz projection use a BSR
+ * SpMM (dense blocks, one column index per block). Call before
+ * zolo_factorize; block = 1 (default) is plain CSR. n must be a multiple of
+ * block. */
+int zolo_set_block_size(zolo_ctx* ctx, int64_t block);
+/* out[0] = the block size, out[1] = atoms of the device BSR copies (0 when the
+ * SpMMs run on CSR: block 1, or an ordering that splits atoms). */
+int zolo_bsr_info(const zolo_ctx* ctx, int64_t* out);
+
 /* Ordering / factor layout used by zolo_factorize:
  *   ZOLO_ORDER_ND   (default) nested dissection (recursive BFS-level bisection,
  *                   leaves of <= nd_leaf rows ordered by RCM; default 192,

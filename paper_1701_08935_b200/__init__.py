@@ -127,6 +127,7 @@ def lib():
         L.zolo_set_design.argtypes = [P, P, C.c_int]
         L.zolo_set_ordering.argtypes = [P, C.c_int, I64]
         L.zolo_set_pole_shard.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
+        L.zolo_set_block_size.argtypes = [P, I64]
         L.zolo_nccl_unique_id.argtypes = [C.c_char_p]
         L.zolo_count_below.argtypes = [P, D, P, P]
         L.zolo_set_solve_mode.argtypes = [P, C.c_int, C.c_int, D, C.c_int]
@@ -289,6 +290,8 @@ class FilterOperator:
     multi-GPU operator (zolo_set_pole_shard): it factors the poles
     :func:`shard_poles` gives and all-reduces every G application over NCCL;
     ``unique_id=None`` leaves G unreduced (``apply_g`` returns the partial sum).
+    ``block_size=b`` declares a BSR pencil (atoms of b rows, BASELINE config 4;
+    zolo_set_block_size): the ordering keeps atoms whole and the SpMMs use BSR.
     ``solve="hybrid"`` factors only pole ``hybrid_pole`` and solves the other
     shifted systems by shift-invariant GMRES on K_p^{-1} B (zolo_set_solve_mode;
     BASELINE config 2) to ``inner_tol`` within ``inner_max`` iterations.
@@ -296,7 +299,7 @@ class FilterOperator:
 
     def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None,
                  ordering: str = "nd", nd_leaf: int = 192, shard=None, solve: str = "direct", hybrid_pole: int = 0,
-                 inner_tol: float = 1e-14, inner_max: int = 256):
+                 inner_tol: float = 1e-14, inner_max: int = 256, block_size: int = 1):
         L = lib()
         n, a, b = pencil
         cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
@@ -319,6 +322,8 @@ class FilterOperator:
         if ordering not in ORDERINGS:
             raise DomainError(f"ordering must be one of {sorted(ORDERINGS)}")
         _check(h, L.zolo_set_ordering(h, ORDERINGS[ordering], int(nd_leaf)))
+        if block_size != 1:  # BSR pencil: atoms of block_size rows (zolo_set_block_size)
+            _check(h, L.zolo_set_block_size(h, int(block_size)))
         self.shard = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
         if shard is not None:
             uid = shard[2] if len(shard) > 2 else None
@@ -436,6 +441,12 @@ class FilterOperator:
         return dict(filter_ms=ms[0], factor_ms=ms[1], trsm_ms=ms[2], trsm_launches=int(ms[3]),
                     kernel_launches=int(ms[4]), operator_applications=int(ms[5]), inner_steps=int(ms[6]),
                     iterations_ms=ms[7])
+
+    def bsr_info(self):
+        """(block size, atoms of the device BSR copies or 0) -- zolo_bsr_info."""
+        out = np.zeros(2, dtype=np.int64)
+        lib().zolo_bsr_info(self._h, _ptr(out))
+        return int(out[0]), int(out[1])
 
     def sweep_profile(self):
         """Structure the triangular sweeps run over (zolo_sweep_profile)."""

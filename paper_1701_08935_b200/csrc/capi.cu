@@ -129,6 +129,10 @@ struct zolo_ctx {
   bool have_perm = false;
   BandGeom geom;
   DevMem perm_d, arp_d, aci_d, av_d, brp_d, bci_d, bv_d, bvc_d;
+  // BSR copies of A and B in the device ordering (zolo_set_block_size): atoms of `bsr` rows
+  int64_t bsr = 1, bsr_na = 0;
+  bool bsr_dev = false;  // the device ordering keeps every atom's rows contiguous: SpMMs use BSR
+  DevMem abrp_d, abci_d, abv_d, bbrp_d, bbci_d, bbv_d, brow0_d;
 
   // factors
   bool factored = false;
@@ -295,7 +299,80 @@ void permuted_csr(int64_t npad, const std::vector<int64_t>& inv, const std::vect
 }
 
 // Device copies of the pencil in the factor ordering + the position map.
+// M (CSR, original ordering) as BSR over atoms of b rows, atoms in device order (rank), dense
+// row-major blocks, block columns ascending by rank; row0[rank] = device row of the atom's first row.
+void bsr_from_csr(int64_t na, int b, const std::vector<int64_t>& rank_of, const std::vector<int64_t>& atom_of_rank,
+                  const std::vector<int64_t>& rp, const std::vector<int64_t>& ci, const std::vector<double>& v, int w,
+                  std::vector<int>& brp, std::vector<int>& bci, std::vector<double>& bval) {
+  brp.assign(na + 1, 0);
+  bci.clear();
+  bval.clear();
+  std::vector<int64_t> slot(na, -1), cols;
+  for (int64_t I = 0; I < na; ++I) {
+    const int64_t atom = atom_of_rank[I];
+    cols.clear();
+    for (int r = 0; r < b; ++r)
+      for (int64_t q = rp[atom * b + r]; q < rp[atom * b + r + 1]; ++q) {
+        const int64_t J = rank_of[ci[q] / b];
+        if (slot[J] < 0) {
+          slot[J] = 0;
+          cols.push_back(J);
+        }
+      }
+    std::sort(cols.begin(), cols.end());
+    const size_t base = bci.size();
+    for (size_t k = 0; k < cols.size(); ++k) {
+      slot[cols[k]] = static_cast<int64_t>(base + k);
+      bci.push_back(static_cast<int>(cols[k]));
+    }
+    bval.resize(bci.size() * b * b * w, 0.0);
+    for (int r = 0; r < b; ++r)
+      for (int64_t q = rp[atom * b + r]; q < rp[atom * b + r + 1]; ++q) {
+        const int64_t J = rank_of[ci[q] / b], kk = ci[q] % b;
+        const size_t e = ((static_cast<size_t>(slot[J]) * b + r) * b + kk) * w;
+        for (int z = 0; z < w; ++z) bval[e + z] = v[q * w + z];
+      }
+    for (int64_t J : cols) slot[J] = -1;
+    brp[I + 1] = static_cast<int>(bci.size());
+  }
+}
+
+void upload_device_bsr(zolo_ctx& c, const std::vector<int>& pos) {
+  c.bsr_dev = false;
+  const int64_t b = c.bsr, n = c.n;
+  if (b <= 1 || n % b) return;
+  const int64_t na = n / b;
+  for (int64_t a = 0; a < na; ++a)
+    for (int64_t r = 1; r < b; ++r)
+      if (pos[a * b + r] != pos[a * b] + r) return;  // an atom split by the ordering: CSR SpMMs
+  std::vector<int64_t> atom_of_rank(na), rank_of(na);
+  for (int64_t a = 0; a < na; ++a) atom_of_rank[a] = a;
+  std::sort(atom_of_rank.begin(), atom_of_rank.end(), [&](int64_t x, int64_t y) { return pos[x * b] < pos[y * b]; });
+  std::vector<int> row0(na);
+  for (int64_t I = 0; I < na; ++I) {
+    rank_of[atom_of_rank[I]] = I;
+    row0[I] = pos[atom_of_rank[I] * b];
+  }
+  const int w = c.cx ? 2 : 1;
+  std::vector<int> brp, bci;
+  std::vector<double> bval;
+  bsr_from_csr(na, static_cast<int>(b), rank_of, atom_of_rank, c.a_rp, c.a_ci, c.a_v, w, brp, bci, bval);
+  upload(c.abrp_d, brp, c.st);
+  upload(c.abci_d, bci, c.st);
+  upload(c.abv_d, bval, c.st);
+  if (!c.b_identity) {
+    bsr_from_csr(na, static_cast<int>(b), rank_of, atom_of_rank, c.b_rp, c.b_ci, c.b_v, w, brp, bci, bval);
+    upload(c.bbrp_d, brp, c.st);
+    upload(c.bbci_d, bci, c.st);
+    upload(c.bbv_d, bval, c.st);
+  }
+  upload(c.brow0_d, row0, c.st);
+  c.bsr_na = na;
+  c.bsr_dev = true;
+}
+
 void upload_device_pencil(zolo_ctx& c, const std::vector<int64_t>& inv, const std::vector<int>& pos) {
+  upload_device_bsr(c, pos);
   const int w = c.cx ? 2 : 1;
   const int64_t npad = static_cast<int64_t>(inv.size());
   std::vector<int> prp, pci;
@@ -528,6 +605,32 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
       one[i] = perm_in[i];
     }
     nodes.push_back(std::move(one));
+  } else if (c.bsr > 1 && n % c.bsr == 0) {
+    // atoms of bsr rows (BSR pencils): dissect the block graph, then expand every atom into its
+    // rows in order, so atoms stay contiguous in the device ordering (BSR SpMMs)
+    const int64_t b = c.bsr, na = n / b;
+    std::vector<int64_t> brp(na + 1, 0), bci, mark(na, -1);
+    for (int64_t I = 0; I < na; ++I) {
+      for (int64_t i = I * b; i < (I + 1) * b; ++i)
+        for (int64_t q = u.rp[i]; q < u.rp[i + 1]; ++q) {
+          const int64_t J = u.ci[q] / b;
+          if (mark[J] != I) {
+            mark[J] = I;
+            bci.push_back(J);
+          }
+        }
+      std::sort(bci.begin() + brp[I], bci.end());
+      brp[I + 1] = static_cast<int64_t>(bci.size());
+    }
+    std::vector<std::vector<int64_t>> anodes;
+    nd_order(na, brp.data(), bci.data(), std::max<int64_t>(1, c.nd_leaf / b), anodes);
+    for (const auto& an : anodes) {
+      std::vector<int64_t> rows;
+      rows.reserve(an.size() * b);
+      for (int64_t a : an)
+        for (int64_t r = 0; r < b; ++r) rows.push_back(a * b + r);
+      nodes.push_back(std::move(rows));
+    }
   } else {
     nd_order(n, u.rp.data(), u.ci.data(), c.nd_leaf, nodes);
   }
@@ -1059,6 +1162,46 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
                         c.tiles[ci / 2].swz);
 }
 
+// out[:, a] = B v[:, act[a]] (complex, the sweeps' input) over the device rows: BSR kernel when
+// the pencil has atoms (zolo_set_block_size) kept contiguous by the ordering, CSR otherwise.
+void device_apply_b(zolo_ctx& c, const void* v, const int* act, int na, cd* out) {
+  const int64_t ld = c.geom.npad, n = ld;
+  if (c.bsr_dev && !c.b_identity) {
+    if (c.cx)
+      Krylov<cd>::bsr_spmm(c.st, c.bsr_na, static_cast<int>(c.bsr), c.bbrp_d.as<int>(), c.bbci_d.as<int>(),
+                           c.bbv_d.as<cd>(), c.brow0_d.as<int>(), reinterpret_cast<const cd*>(v), ld, act, na, nullptr,
+                           out);
+    else
+      Krylov<double>::bsr_spmm(c.st, c.bsr_na, static_cast<int>(c.bsr), c.bbrp_d.as<int>(), c.bbci_d.as<int>(),
+                               c.bbv_d.as<double>(), c.brow0_d.as<int>(), reinterpret_cast<const double*>(v), ld, act,
+                               na, nullptr, out);
+    zero_rows(c.st, c.sp_pad_rows.as<int>(), c.sparse ? c.sp_npads : 0, out, ld, na);
+    return;
+  }
+  if (c.cx)
+    Krylov<cd>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<cd>(),
+                        reinterpret_cast<const cd*>(v), act, na, out);
+  else
+    Krylov<double>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
+                            c.bv_d.as<double>(), reinterpret_cast<const double*>(v), act, na, out);
+}
+
+// out (ld x k, device rows) = M x, M = A (which 0) or B (which 1); BSR when available
+template <class S>
+void device_spmm(zolo_ctx& c, int which, const S* x, int64_t k, S* out) {
+  const int64_t ld = c.geom.npad;
+  if (c.bsr_dev) {
+    Krylov<S>::bsr_spmm(c.st, c.bsr_na, static_cast<int>(c.bsr), (which ? c.bbrp_d : c.abrp_d).template as<int>(),
+                        (which ? c.bbci_d : c.abci_d).template as<int>(), (which ? c.bbv_d : c.abv_d).template as<S>(),
+                        c.brow0_d.as<int>(), x, ld, nullptr, k, out, nullptr);
+    return;
+  }
+  if (which == 0)
+    Krylov<S>::spmm(c.st, ld, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), x, k, out);
+  else
+    Krylov<S>::spmm(c.st, ld, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), x, k, out);
+}
+
 float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst);
 
 // G applied to the columns act[0..na) of vsrc (ld x ncap, S) -> w[:, act].
@@ -1069,12 +1212,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   const int nch = c.nchains();
   std::vector<cd*> xs(nch);
   for (int i = 0; i < nch; ++i) xs[i] = c.xbuf[i]->as<cd>();
-  if (c.cx)
-    Krylov<cd>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
-                        c.bv_d.as<cd>(), reinterpret_cast<const cd*>(vsrc), act, na, c.bbuf.as<cd>());
-  else
-    Krylov<double>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
-                            c.bv_d.as<double>(), reinterpret_cast<const double*>(vsrc), act, na, c.bbuf.as<cd>());
+  device_apply_b(c, vsrc, act, na, c.bbuf.as<cd>());
   CK(cudaEventRecord(c.ev2, c.st));
   unsigned long long* fx = c.flags.as<unsigned long long>();
   int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
@@ -1587,14 +1725,14 @@ void rr_impl(zolo_ctx& c, const double* y, int64_t k, double* at, double* bt) {
   c.rr_out.ensure(es * k * k);
   CK(cudaMemcpyAsync(yo.p, y, es * n * k, cudaMemcpyHostToDevice, c.st));
   Krylov<S>::permute_in(c.st, yo.as<S>(), n, yp.as<S>(), ld, k, c.perm_d.as<int>());
-  Krylov<S>::spmm(c.st, ld, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), yp.as<S>(), k, ay.as<S>());
+  device_spmm<S>(c, 0, yp.as<S>(), k, ay.as<S>());
   Krylov<S>::gram(c.st, ld, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
   CK(cudaMemcpyAsync(at, c.rr_out.p, es * k * k, cudaMemcpyDeviceToHost, c.st));
   CK(cudaStreamSynchronize(c.st));
   if (c.b_identity) {
     Krylov<S>::gram(c.st, ld, ld, yp.as<S>(), k, yp.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
   } else {
-    Krylov<S>::spmm(c.st, ld, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), yp.as<S>(), k, ay.as<S>());
+    device_spmm<S>(c, 1, yp.as<S>(), k, ay.as<S>());
     Krylov<S>::gram(c.st, ld, ld, yp.as<S>(), k, ay.as<S>(), k, c.rr_out.as<S>(), c.rr_partial.as<double>());
   }
   CK(cudaMemcpyAsync(bt, c.rr_out.p, es * k * k, cudaMemcpyDeviceToHost, c.st));
@@ -1631,12 +1769,7 @@ void spmm_dev_impl(zolo_ctx& c, int which, const void* x, void* out, int64_t k) 
   c.tmp1.ensure(es * ld * k);
   c.tmp2.ensure(es * ld * k);
   Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(x), n, c.tmp1.as<S>(), ld, k, c.perm_d.as<int>());
-  if (which == 0)
-    Krylov<S>::spmm(c.st, ld, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<S>(), c.tmp1.as<S>(), k,
-                    c.tmp2.as<S>());
-  else
-    Krylov<S>::spmm(c.st, ld, ld, c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<S>(), c.tmp1.as<S>(), k,
-                    c.tmp2.as<S>());
+  device_spmm<S>(c, which, c.tmp1.as<S>(), k, c.tmp2.as<S>());
   Krylov<S>::permute_out(c.st, c.tmp2.as<S>(), ld, reinterpret_cast<S*>(out), n, k, c.perm_d.as<int>());
   CK(cudaGetLastError());
 }
@@ -1864,6 +1997,23 @@ int zolo_set_design(zolo_ctx* c, const double* design, int r) {
     c->have_design = true;
     c->factored = false;
   });
+}
+
+int zolo_set_block_size(zolo_ctx* c, int64_t block) {
+  return guarded(c, [&] {
+    require(block >= 1 && block <= 64, "zolo_set_block_size: block must be in [1, 64]");
+    require(!c->have_pencil || c->n % block == 0, "zolo_set_block_size: the order is not a multiple of the block");
+    c->bsr = block;
+    c->have_perm = false;
+    c->sym_ready = false;
+    c->factored = false;
+  });
+}
+
+int zolo_bsr_info(const zolo_ctx* c, int64_t* out) {
+  out[0] = c->bsr;
+  out[1] = c->bsr_dev ? c->bsr_na : 0;
+  return ZOLO_OK;
 }
 
 int zolo_set_ordering(zolo_ctx* c, int mode, int64_t nd_leaf) {

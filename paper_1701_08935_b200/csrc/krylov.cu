@@ -142,6 +142,55 @@ __global__ void spmm_kernel(int64_t n, int64_t ld, const int* rp, const int* ci,
     if (c0 + c < k) out[t + (c0 + c) * ld] = acc[c];
 }
 
+// BSR SpMM (pencils with dense b x b blocks per atom, BASELINE config 4): atoms I in device
+// order, block row I holds blocks (I, bci[q]) with dense row-major values bval[q][r][k]; atom I
+// occupies device rows row0[I] .. row0[I] + b - 1. One thread per scalar row x SPC columns:
+// each block entry is loaded once for the SPC columns, no per-entry column index.
+// act != nullptr: columns act[a] of v, output column a of outc (complex, the sweeps' input);
+// otherwise columns 0..k-1 of v into out (S).
+template <class S>
+__global__ void bsr_spmm_kernel(int64_t na, int b, const int* brp, const int* bci, const S* bval, const int* row0,
+                                const S* v, int64_t ld, const int* act, int64_t k, S* out, cd* outc) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= na * b) return;
+  const int64_t I = t / b;
+  const int r = static_cast<int>(t - I * b);
+  const int64_t a0 = static_cast<int64_t>(blockIdx.y) * SPC;
+  int64_t col[SPC];
+#pragma unroll
+  for (int c = 0; c < SPC; ++c) {
+    const int64_t a = a0 + c < k ? a0 + c : a0;
+    col[c] = act ? act[a] : a;
+  }
+  S acc[SPC];
+#pragma unroll
+  for (int c = 0; c < SPC; ++c) acc[c] = szero(S());
+  for (int q = brp[I]; q < brp[I + 1]; ++q) {
+    const S* bv = bval + (static_cast<int64_t>(q) * b + r) * b;
+    const int64_t x0 = row0[bci[q]];
+    for (int kk = 0; kk < b; ++kk) {
+      const S m = bv[kk];
+#pragma unroll
+      for (int c = 0; c < SPC; ++c) acc[c] = sadd(acc[c], smul(m, v[x0 + kk + col[c] * ld]));
+    }
+  }
+  const int64_t row = row0[I] + r;
+#pragma unroll
+  for (int c = 0; c < SPC; ++c)
+    if (a0 + c < k) {
+      if (outc)
+        outc[row + (a0 + c) * ld] = to_cd(acc[c]);
+      else
+        out[row + (a0 + c) * ld] = acc[c];
+    }
+}
+
+// rows[0..nrows) of columns 0..k-1 set to zero (the identity padding rows of the BSR SpMM output)
+__global__ void zero_rows_kernel(const int* rows, int nrows, cd* out, int64_t ld) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nrows) out[rows[q] + blockIdx.y * ld] = mk(0.0, 0.0);
+}
+
 struct XPtrs {
   cd* p[2 * 16];
 };
@@ -618,6 +667,20 @@ void Krylov<S>::spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, cons
   if (k > 0)
     spmm_kernel<S><<<dim3(blocks_for(ld, 256), static_cast<unsigned>((k + SPC - 1) / SPC)), 256, 0, st>>>(n, ld, rp, ci,
                                                                                                        vals, v, k, out);
+}
+
+template <class S>
+void Krylov<S>::bsr_spmm(cudaStream_t st, int64_t na, int b, const int* brp, const int* bci, const S* bval,
+                         const int* row0, const S* v, int64_t ld, const int* act, int64_t k, S* out, cd* outc) {
+  if (k > 0 && na > 0)
+    bsr_spmm_kernel<S><<<dim3(blocks_for(na * b, 256), static_cast<unsigned>((k + SPC - 1) / SPC)), 256, 0, st>>>(
+        na, b, brp, bci, bval, row0, v, ld, act, k, out, outc);
+}
+
+void zero_rows(cudaStream_t st, const int* rows, int nrows, cd* out, int64_t ld, int64_t k) {
+  if (nrows > 0 && k > 0)
+    zero_rows_kernel<<<dim3(static_cast<unsigned>((nrows + 255) / 256), static_cast<unsigned>(k)), 256, 0, st>>>(
+        rows, nrows, out, ld);
 }
 
 template <class S>

@@ -66,9 +66,16 @@ struct Krylov {
   // per column: num = ||ax - lam bx||^2, den = ||bx||^2 (n x k, ld = n)
   static void residuals(cudaStream_t st, int64_t n, const S* ax, const S* bx, const double* lam, int64_t k,
                         double* num, double* den);
+  // BSR (atoms of b rows, device rows row0[I]..): act != nullptr: outc[:, a] = M V[:, act[a]] (complex),
+  // else out[:, 0:k] = M V[:, 0:k]; padding rows are not written
+  static void bsr_spmm(cudaStream_t st, int64_t na, int b, const int* brp, const int* bci, const S* bval,
+                       const int* row0, const S* v, int64_t ld, const int* act, int64_t k, S* out, cd* outc);
   // out (ld x k) = M * V (M permuted CSR with S values)
   static void spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
                    int64_t k, S* out);
 };
+
+// out[rows[q], c] = 0 for q < nrows, c < k (ld rows per column)
+void zero_rows(cudaStream_t st, const int* rows, int nrows, cd* out, int64_t ld, int64_t k);
 
 }  // namespace zolo
