@@ -15,9 +15,12 @@
 // nested dissection is SURVEY.md §8(f) rank 2 ("host symbolic analysis: ND
 // ordering, supernodes, etree"), here at 32x32-tile granularity.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstdint>
 #include <numeric>
+#include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "host.hpp"
@@ -365,79 +368,104 @@ void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
   }
   std::vector<std::vector<int>> by(nlev);
   for (int64_t k = 0; k < nb; ++k) by[level[k]].push_back(static_cast<int>(k));
-  auto lookup = [&](int64_t i, int64_t k) {  // tile id of (i, k), i > k
-    const auto b = bs.row_idx.begin() + bs.row_ptr[i], e = bs.row_idx.begin() + bs.row_ptr[i + 1];
-    const auto it = std::lower_bound(b, e, k);
-    if (it == e || *it != k) throw std::runtime_error("factor_plan: update target outside the structure");
-    return static_cast<int>(it - bs.row_idx.begin());
+  const int64_t nkey = nb + 2 * bs.ntiles;  // Dt | Lt | Ut
+  // Levels are independent: each thread builds whole levels with its own scratch, then the
+  // per-level lists are concatenated in level order (targets' contribution offsets rebased).
+  struct Level {
+    std::vector<int> pan, tgt, con;
   };
+  std::vector<Level> lv(nlev);
+  std::atomic<int> next{0};
+  auto worker = [&] {
+    std::vector<int> slot(nkey, -1), cnt, mark(nb, -1), epos(nb, 0);
+    std::vector<int64_t> keys;
+    for (int l = next++; l < nlev; l = next++) {
+      Level& L = lv[l];
+      keys.clear();
+      cnt.clear();
+      // every (a, b) with a, b in col(k): a == b -> Dt(a); a > b -> Lt(a, b); a < b -> Ut(b, a). The
+      // tile id of (x, y), x > y both in col(k), is found by walking col(y), which holds col(k)'s
+      // rows below y (fill): no searches. visit(key, L(a,k) id, U(k,b) id) in a fixed order.
+      auto enumerate = [&](int k, auto&& visit) {
+        const int64_t e0 = bs.col_ptr[k], e1 = bs.col_ptr[k + 1];
+        for (int64_t e = e0; e < e1; ++e) {
+          mark[bs.col_idx[e]] = k;
+          epos[bs.col_idx[e]] = static_cast<int>(e);
+        }
+        for (int64_t ey = e0; ey < e1; ++ey) {
+          const int64_t y = bs.col_idx[ey];
+          const int ty = static_cast<int>(bs.col_tile[ey]);
+          visit(y, ty, ty);
+          for (int64_t e = bs.col_ptr[y]; e < bs.col_ptr[y + 1]; ++e) {
+            const int64_t x = bs.col_idx[e];
+            if (mark[x] != k) continue;
+            const int64_t t = bs.col_tile[e];
+            const int tx = static_cast<int>(bs.col_tile[epos[x]]);
+            visit(nb + t, tx, ty);              // L(x, y) -= L(x, k) U(k, y)
+            visit(nb + bs.ntiles + t, ty, tx);  // U(y, x) -= L(y, k) U(k, x)
+          }
+        }
+      };
+      for (int k : by[l])
+        for (int64_t e = bs.col_ptr[k]; e < bs.col_ptr[k + 1]; ++e) {
+          const int id = static_cast<int>(bs.col_tile[e]);
+          L.pan.insert(L.pan.end(), {k, 2 * id, k, 2 * id + 1});
+        }
+      for (int k : by[l])
+        enumerate(k, [&](int64_t key, int, int) {
+          if (slot[key] < 0) {
+            slot[key] = static_cast<int>(keys.size());
+            keys.push_back(key);
+            cnt.push_back(0);
+          }
+          ++cnt[slot[key]];
+        });
+      int64_t c0 = 0;
+      L.tgt.resize(4 * keys.size());
+      for (size_t t = 0; t < keys.size(); ++t) {
+        const int64_t key = keys[t];
+        const int kind = key < nb ? 0 : (key < nb + bs.ntiles ? 1 : 2);
+        L.tgt[4 * t] = kind;
+        L.tgt[4 * t + 1] = static_cast<int>(kind == 0 ? key : (kind == 1 ? key - nb : key - nb - bs.ntiles));
+        L.tgt[4 * t + 2] = static_cast<int>(c0);
+        L.tgt[4 * t + 3] = static_cast<int>(c0);  // fill cursor -> end
+        c0 += cnt[t];
+      }
+      L.con.resize(2 * c0);
+      for (int k : by[l])  // contributions of each target in ascending k (fixed summation order)
+        enumerate(k, [&](int64_t key, int la, int ub) {
+          const int at = L.tgt[4 * slot[key] + 3]++;
+          L.con[2 * at] = la;
+          L.con[2 * at + 1] = ub;
+        });
+      for (int64_t key : keys) slot[key] = -1;
+    }
+  };
+  const int nthr = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  std::vector<std::thread> pool;
+  for (int q = 1; q < nthr; ++q) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
   plan = FactorPlan();
+  int64_t ncon = 0, ntgt = 0, npan = 0;
+  for (const Level& L : lv) ncon += L.con.size() / 2, ntgt += L.tgt.size() / 4, npan += L.pan.size() / 2;
+  if (ncon >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
+  plan.cols.reserve(nb);
+  plan.pan.reserve(2 * npan);
+  plan.tgt.reserve(4 * ntgt);
+  plan.con.reserve(2 * ncon);
   plan.lvl_ptr.push_back(0);
   plan.pan_ptr.push_back(0);
   plan.tgt_ptr.push_back(0);
-  const int64_t nkey = nb + 2 * bs.ntiles;  // Dt | Lt | Ut
-  std::vector<int> slot(nkey, -1), cnt;
-  std::vector<int64_t> touched;
   for (int l = 0; l < nlev; ++l) {
-    for (int k : by[l]) {
-      plan.cols.push_back(k);
-      for (int64_t e = bs.col_ptr[k]; e < bs.col_ptr[k + 1]; ++e) {
-        const int id = static_cast<int>(bs.col_tile[e]);
-        plan.pan.push_back(k);
-        plan.pan.push_back(2 * id);
-        plan.pan.push_back(k);
-        plan.pan.push_back(2 * id + 1);
-      }
+    const int base = static_cast<int>(plan.con.size() / 2);
+    for (int k : by[l]) plan.cols.push_back(k);
+    plan.pan.insert(plan.pan.end(), lv[l].pan.begin(), lv[l].pan.end());
+    for (size_t t = 0; t < lv[l].tgt.size(); t += 4) {
+      plan.tgt.insert(plan.tgt.end(), {lv[l].tgt[t], lv[l].tgt[t + 1], lv[l].tgt[t + 2] + base, lv[l].tgt[t + 3] + base});
     }
-    // targets of this level: count, then fill contributions in ascending k
-    touched.clear();
-    cnt.clear();
-    std::vector<int64_t> keys;
-    auto key_of = [&](int64_t a, int64_t b) -> int64_t {
-      if (a == b) return a;
-      return a > b ? nb + lookup(a, b) : nb + bs.ntiles + lookup(b, a);
-    };
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int k : by[l]) {
-        const int64_t e0 = bs.col_ptr[k], e1 = bs.col_ptr[k + 1];
-        for (int64_t ea = e0; ea < e1; ++ea)
-          for (int64_t eb = e0; eb < e1; ++eb) {
-            const int64_t key = key_of(bs.col_idx[ea], bs.col_idx[eb]);
-            if (pass == 0) {
-              if (slot[key] < 0) {
-                slot[key] = static_cast<int>(keys.size());
-                keys.push_back(key);
-                cnt.push_back(0);
-              }
-              ++cnt[slot[key]];
-            } else {
-              const int t = slot[key];
-              const int at = plan.tgt[4 * t + 3]++;
-              plan.con[2 * at] = static_cast<int>(bs.col_tile[ea]);
-              plan.con[2 * at + 1] = static_cast<int>(bs.col_tile[eb]);
-            }
-          }
-      }
-      if (pass == 0) {
-        // targets of this level are appended after the previous levels' ones
-        const int tbase = static_cast<int>(plan.tgt.size() / 4);
-        int64_t c0 = static_cast<int64_t>(plan.con.size() / 2);
-        for (size_t t = 0; t < keys.size(); ++t) {
-          const int64_t key = keys[t];
-          const int kind = key < nb ? 0 : (key < nb + bs.ntiles ? 1 : 2);
-          const int id = static_cast<int>(kind == 0 ? key : (kind == 1 ? key - nb : key - nb - bs.ntiles));
-          plan.tgt.push_back(kind);
-          plan.tgt.push_back(id);
-          plan.tgt.push_back(static_cast<int>(c0));
-          plan.tgt.push_back(static_cast<int>(c0));  // fill cursor -> end
-          c0 += cnt[t];
-          slot[key] = tbase + static_cast<int>(t);
-        }
-        if (c0 >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
-        plan.con.resize(2 * c0);
-      }
-    }
-    for (int64_t key : keys) slot[key] = -1;
+    plan.con.insert(plan.con.end(), lv[l].con.begin(), lv[l].con.end());
+    std::vector<int>().swap(lv[l].con);
     plan.lvl_ptr.push_back(static_cast<int>(plan.cols.size()));
     plan.pan_ptr.push_back(static_cast<int>(plan.pan.size() / 2));
     plan.tgt_ptr.push_back(static_cast<int>(plan.tgt.size() / 4));
