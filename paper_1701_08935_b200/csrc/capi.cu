@@ -198,6 +198,7 @@ struct zolo_ctx {
   int64_t critical_path = 0;
   int sel_s0 = 0, sel_K = 0;  // selectively inverted trailing block [sel_s0, sel_s0 + sel_K) (host.hpp DT_*)
   int sel_stage = 0;          // its backward input is staged into partial slots [sel_stage, sel_stage + sel_K)
+  int iters_seen = 0;         // largest Krylov dimension an apply_filter on this context has needed
   DevMem sp_seltab, sel_mem;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
   DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
@@ -1634,7 +1635,9 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   float trsm_ms = 0.0f, busy_ms = 0.0f;
   int trsm_launches = 0;
   int64_t launches = 4, opapps = 0;
+  int its = 0;
   for (int it = 0; it < maxit && !active.empty(); ++it) {
+    its = it + 1;
     const int na = static_cast<int>(active.size());
     std::memcpy(c.act_h, active.data(), sizeof(int) * na);
     CK(cudaMemcpyAsync(c.act_d.p, c.act_h, sizeof(int) * na, cudaMemcpyHostToDevice, c.st));
@@ -1670,6 +1673,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       if (!c.done_h[col]) next.push_back(col);
     active.swap(next);
   }
+  c.iters_seen = std::max(c.iters_seen, its);
   S* yp = c.vout.as<S>();
   Krylov<S>::assemble(c.st, n, ld, v0, c.basis_ptrs.as<S*>(), static_cast<int>(ncols), g, vin, yp);
   Krylov<S>::permute_out(c.st, yp, ld, reinterpret_cast<S*>(d_y), n, ncols, c.perm_d.as<int>());
@@ -2199,13 +2203,15 @@ void release_workspace(zolo_ctx& c) {
 
 // Columns are independent (one Krylov basis per column, filter_engine.hpp:109-111): when the
 // workspace of all columns does not fit beside the factors, filter them in column batches.
-int apply_filter_batched(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
-                         zolo_report* rep) {
+// Columns are filtered in batches when their workspace does not fit beside the factors. The
+// Krylov basis is allocated on demand, so the budget counts `budget_its` basis vectors per column.
+int apply_filter_batched_at(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
+                            zolo_report* rep, int budget_its) {
   auto run = [&](const void* v, void* y, int64_t k, zolo_report* r) {
     return c.cx ? apply_filter_impl<cd>(c, v, y, k, tol, gmres_max, r)
                 : apply_filter_impl<double>(c, v, y, k, tol, gmres_max, r);
   };
-  const double per_col = bytes_per_column(c, static_cast<int>(gmres_max));
+  const double per_col = bytes_per_column(c, budget_its);
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
   static const int64_t forced = env_int("ZOLO_FILTER_BATCH", 0);  // (testing) force a column batch size
@@ -2215,6 +2221,12 @@ int apply_filter_batched(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols,
     release_workspace(c);
     CK(cudaMemGetInfo(&free_b, &total_b));
     batch = std::max<int64_t>(1, static_cast<int64_t>(0.85 * free_b / per_col));
+    constexpr int64_t G = 32;  // columns per sweep task group (mma.cuh DCG)
+    if (batch >= G) {          // whole column groups, spread evenly over the batches
+      const int64_t groups = (ncols + G - 1) / G, per = batch / G;
+      const int64_t nbat = (groups + per - 1) / per;
+      batch = ((groups + nbat - 1) / nbat) * G;
+    }
   }
   if (batch >= ncols) return run(d_v, d_y, ncols, rep);
   const size_t colb = c.es() * c.n;
@@ -2251,6 +2263,30 @@ int apply_filter_batched(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols,
   for (int i : {0, 2, 3, 4, 5, 6, 7}) c.last_ms[i] = ms[i];
   if (code != ZOLO_OK) c.err = err;
   return code;
+}
+
+// The first application on a context budgets the full gmres_max basis; later ones budget the
+// Krylov dimension seen so far (+4), which keeps the whole block in one batch when the factors
+// leave room for it. Should an application need more, the basis allocation fails and it is
+// re-run under the full budget (columns are independent and deterministic: same bits).
+int apply_filter_batched(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
+                         zolo_report* rep) {
+  const int full = static_cast<int>(gmres_max);
+  const int seen = c.iters_seen > 0 ? std::min(full, c.iters_seen + 4) : full;
+  if (seen >= full || c.hybrid) return apply_filter_batched_at(c, d_v, d_y, ncols, tol, gmres_max, rep, full);
+  const int64_t g0 = c.g_apps, s0 = c.inner_solves;
+  int64_t* cols = rep ? rep->column_iterations : nullptr;
+  try {
+    return apply_filter_batched_at(c, d_v, d_y, ncols, tol, gmres_max, rep, seen);
+  } catch (const ZoloError& e) {
+    if (e.code != ZOLO_ERR_CUDA || std::string(e.what()).find("cudaMalloc") == std::string::npos) throw;
+    cudaGetLastError();  // clear the allocation failure
+    c.g_apps = g0;
+    c.inner_solves = s0;
+    if (rep) rep->column_iterations = cols;
+    release_workspace(c);
+    return apply_filter_batched_at(c, d_v, d_y, ncols, tol, gmres_max, rep, full);
+  }
 }
 
 }  // namespace
