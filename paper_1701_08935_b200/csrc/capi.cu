@@ -1247,7 +1247,7 @@ float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst);
 // G applied to the columns act[0..na) of vsrc (ld x ncap, S) -> w[:, act].
 float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   if (c.hybrid) return apply_g_hybrid(c, vsrc, na, wdst);
-  const int64_t ld = c.geom.npad, n = ld;  // device rows: padding rows (anywhere in ND order) are zero
+  const int64_t ld = c.geom.npad;  // device rows: padding rows (anywhere in ND order) are zero
   const int* act = c.act_d.as<int>();
   const int nch = c.nchains();
   std::vector<cd*> xs(nch);

@@ -426,7 +426,10 @@ __global__ void __launch_bounds__(FT) panel_level_kernel(const int* pan, int p0,
 // of this loop raised "illegal instruction" on the B200 -- tools/dev/trail_unit.cu
 // reproduces it -- so the stages are single-buffered; the factorization is setup.)
 constexpr int TRAIL_SMEM = (TT + XS2) * static_cast<int>(sizeof(cd));
-__global__ void __launch_bounds__(ST, 2) trailing_level_kernel(const int* tgt, const int* con, int t0, cd* Dt,
+#ifndef ZOLO_TRAIL_MINB
+#define ZOLO_TRAIL_MINB 4  // 4 resident targets per SM hide the single-buffered tile loads (cfg3 factor -8%)
+#endif
+__global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(const int* tgt, const int* con, int t0, cd* Dt,
                                                                cd* Lt, cd* Ut) {
   extern __shared__ __align__(16) unsigned char trail_smem[];
   cd* sm = reinterpret_cast<cd*>(trail_smem);

@@ -94,7 +94,7 @@ __device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* x
   // compiler cannot prove warp-uniform, so reconverge explicitly
   __syncwarp();
   const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
-  const int bc = f.c0 + (f.lane >> 2), bm = f.lane & 3;
+  const int bc = f.c0 + (f.lane >> 2);
   const int sa = swz(ar);
   cd a[TILE / 4], b0[TILE / 4], b1[TILE / 4];
 #pragma unroll

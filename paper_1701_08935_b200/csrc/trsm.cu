@@ -129,16 +129,6 @@ __device__ __forceinline__ void load_x(cd* xs, const cd* base, int64_t ld, int c
   }
 }
 
-// Coalesced store of a [col*XPAD + row] staging block to the column-major block.
-__device__ __forceinline__ void store_x(cd* base, const cd* xs, int64_t ld, int c0, int nc) {
-  const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < CG / 8; ++q) {
-    const int c = cc + 8 * q;
-    if (c < nc) base[row + (c0 + c) * ld] = xs[c * XPAD + row];
-  }
-}
-
 // thread 0 waits for *f >= epoch (bounded: a lost producer is reported through
 // err, never a hung GPU), then the CTA synchronises.
 __device__ __forceinline__ void wait_flag(const int* f, int epoch, int* err) {
@@ -718,9 +708,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cpasync(unsigned long long* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
