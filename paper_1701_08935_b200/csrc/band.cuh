@@ -167,12 +167,25 @@ struct DagSched {
   const int* recs = nullptr;  // device, ntask x DAG_REC
   int ntask = 0;
   int nslots = 0;
+  // ready-queue scheduling (ZOLO_DAG_QUEUE): per record its dependency count, its dependents
+  // (CSR) and the records ready at the start (claim order)
+  const int* q_cnt0 = nullptr;
+  const int* q_dptr = nullptr;
+  const int* q_didx = nullptr;
+  const int* q_init = nullptr;
+  int q_ninit = 0;
+};
+// device scratch of a ready-queue launch: cnt (ntask x chains x groups), q (same), ctr[2]
+struct DagQueueWork {
+  int* cnt = nullptr;
+  int* q = nullptr;
+  int* ctr = nullptr;
 };
 // presw: the chains' tiles are stored swizzled (swizzle_tiles); required by the v2 kernel
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
                     unsigned long long* trace = nullptr, const int* tmap = nullptr, bool presw = false,
-                    bool need_v2 = false);
+                    bool need_v2 = false, const DagQueueWork* qw = nullptr);
 int dag_groups(int ncols);
 // forward + backward sweeps in one launch (v2 kernel); tmap: fused claim map (bit 30 = backward), or
 // nullptr for forward-then-backward order. Returns the grid, or -1 when the v2 kernel cannot run it.

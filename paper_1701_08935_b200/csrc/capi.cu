@@ -203,6 +203,8 @@ struct zolo_ctx {
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
   DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
   DevMem sp_tmap_fused;  // claim map of the fused forward + backward launch (dag_fused_launch)
+  DevMem q_fwd[4], q_bwd[4];  // ready-queue structures per direction: cnt0, dptr, didx, init
+  DevMem q_work;              // ready-queue scratch (cnt | q | ctr)
   int tmap_fused_nch = -1;
   int tmap_nch = -1;  // chain count the staggered claim maps were built for
   DevMem sp_er, sp_ec, sp_ea, sp_eb;  // scatter lists of the union pattern in the factor ordering
@@ -793,6 +795,47 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     c.sp_tmap_fwd.release();
     c.sp_tmap_bwd.release();
     c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb + c.sel_K};
+    // ready-queue structures (ZOLO_DAG_QUEUE): a record's dependencies are the row tasks of its
+    // dependency rows and the chunk tasks of its partial slots (exactly what the static schedule
+    // waits on); the selectively inverted block's task kinds are not covered
+    auto build_queue = [&](const std::vector<DagTask>& ts, bool fwd, DevMem* q, DagSched& sc) {
+      if (c.sel_K) return;
+      const int nt = static_cast<int>(ts.size());
+      std::vector<int> row_task(nb, -1), slot_task(std::max(sf, sb) + 1, -1), cnt0(nt, 0), dptr(nt + 1, 0),
+          didx, init;
+      for (int t = 0; t < nt; ++t) (ts[t].out >= 0 ? slot_task[ts[t].out] : row_task[ts[t].i]) = t;
+      std::vector<std::vector<int>> deps(nt);
+      for (int t = 0; t < nt; ++t) {
+        const DagTask& k = ts[t];
+        const int64_t e0 = fwd ? bs.row_ptr[k.i] : bs.col_ptr[k.i];
+        const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
+        for (int qd = k.qa; qd < k.qb; ++qd) {
+          const int64_t e = fwd ? e0 + qd : e0 + ndall - 1 - qd;
+          deps[t].push_back(row_task[fwd ? bs.row_idx[e] : bs.col_idx[e]]);
+        }
+        for (int p = k.pa; p < k.pa + k.pc; ++p) deps[t].push_back(slot_task[p]);
+        cnt0[t] = static_cast<int>(deps[t].size());
+        if (!cnt0[t]) init.push_back(t);
+      }
+      std::vector<std::vector<int>> users(nt);
+      for (int t = 0; t < nt; ++t)
+        for (int d : deps[t]) users[d].push_back(t);
+      for (int t = 0; t < nt; ++t) {
+        didx.insert(didx.end(), users[t].begin(), users[t].end());
+        dptr[t + 1] = static_cast<int>(didx.size());
+      }
+      upload(q[0], cnt0, c.st);
+      upload(q[1], dptr, c.st);
+      upload(q[2], didx, c.st);
+      upload(q[3], init, c.st);
+      sc.q_cnt0 = q[0].as<int>();
+      sc.q_dptr = q[1].as<int>();
+      sc.q_didx = q[2].as<int>();
+      sc.q_init = q[3].as<int>();
+      sc.q_ninit = static_cast<int>(init.size());
+    };
+    build_queue(tf, true, c.q_fwd, c.sched_fwd);
+    build_queue(tb, false, c.q_bwd, c.sched_bwd);
     c.sp_nslots = std::max(sf, sb + c.sel_K);
   }
   clk.mark("sweep schedules");
@@ -1182,16 +1225,27 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
     return;
   }
   const bool need_v2 = c.sel_K > 0;  // the selectively inverted block's task kinds exist only in dag2_kernel
+  static const bool queue = env_int("ZOLO_DAG_QUEUE", 0) != 0;
+  DagQueueWork qw;
+  const DagQueueWork* qwp = nullptr;
+  if (queue && c.sched_fwd.q_cnt0 && c.sched_bwd.q_cnt0 && !full) {
+    const int64_t nt = static_cast<int64_t>(std::max(c.sched_fwd.ntask, c.sched_bwd.ntask)) * nsub * dag_groups(na);
+    c.q_work.ensure(sizeof(int) * (2 * nt + 2));
+    qw.cnt = c.q_work.as<int>();
+    qw.q = qw.cnt + nt;
+    qw.ctr = qw.q + nt;
+    qwp = &qw;
+  }
   const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf,
                                  ++c.epoch, c.counter.as<int>(), 1, c.num_sms, trace,
-                                 full ? c.sp_tmap_fwd.as<int>() : nullptr, presw, need_v2);
+                                 full ? c.sp_tmap_fwd.as<int>() : nullptr, presw, need_v2, qwp);
   if (c.sel_K)  // the backward sweep runs in place: stage the inverted block's input first
     dag_stage_inputs(c.st, c.chains_bwd.as<Chain>() + first, nsub, static_cast<int64_t>(c.sel_s0) * TILE,
                      static_cast<int64_t>(c.sel_K) * TILE, na, ld, static_cast<int64_t>(TILE) * c.sched_bwd.nslots,
                      static_cast<int64_t>(c.sel_stage) * TILE);
   const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf,
                                  ++c.epoch, c.counter.as<int>() + 1, 0, c.num_sms, nullptr,
-                                 full ? c.sp_tmap_bwd.as<int>() : nullptr, presw, need_v2);
+                                 full ? c.sp_tmap_bwd.as<int>() : nullptr, presw, need_v2, qwp);
   if (g1 < 0 || g2 < 0)
     throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: the selectively inverted schedule needs the v2 sweep kernel "
                                      "(at most 32 chains, ZOLO_DAG_V2 on)");

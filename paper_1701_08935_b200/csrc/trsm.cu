@@ -439,7 +439,24 @@ struct DagArgs {
   int ntask_b = 0, nslots_b = 0;
   int64_t ldp_b = 0;
   int cfs = 0;  // chunk-flag stride per (chain, group): one for both directions, so they never alias
+  // ready-queue scheduling: tasks are popped when all their dependencies are done (no claimed
+  // task ever waits); the first q_ninit x per_step pops are the initially ready records
+  int queue = 0;
+  const int* q_cnt0 = nullptr;
+  const int* q_dptr = nullptr;
+  const int* q_didx = nullptr;
+  const int* q_init = nullptr;
+  int q_ninit = 0;
+  int* q_cnt = nullptr;  // per task: dependencies completed
+  int* q_arr = nullptr;  // pushed task ids + 1
+  int* q_ctr = nullptr;  // [0] pops, [1] pushes
 };
+
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 
 // a tile into the swizzled shared layout: permuted on the way (column-major global
 // tile) or copied linearly (tile stored pre-swizzled)
@@ -830,11 +847,34 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
     };
     auto recs_of = [&](int dir) { return dir ? A.recs_b : A.recs; };
+    // ready queue: pop position -> task id (the initial records directly, later ones once pushed)
+    const int q_base = A.q_ninit * per_step;
+    auto resolve = [&](int pos) {
+      int id = ntasks;
+      if (lane == 0 && pos < ntasks) {
+        if (pos < q_base) {
+          id = A.q_init[pos / per_step] * per_step + pos % per_step;
+        } else {
+          int spins = 0;
+          while ((id = ld_acquire(A.q_arr + (pos - q_base))) == 0) {
+            if (++spins > 64) __nanosleep(64);
+            if (spins > (1 << 26)) {
+              atomicExch(A.counter + 2, 1);
+              break;
+            }
+          }
+          id = id > 0 ? id - 1 : ntasks;
+        }
+      }
+      return __shfl_sync(0xffffffffu, id, 0);
+    };
     // Claims run two tasks ahead: when task T starts, T+1's id has arrived (its record load is
-    // issued now and lands while T streams) and the atomic for T+2 goes out.
+    // issued now and lands while T streams) and the atomic for T+2 goes out. (Ready-queue mode:
+    // one task at a time, popped when the previous one has been issued.)
     int t = 0;
-    if (lane == 0) t = atomicAdd(A.counter, 1);
+    if (lane == 0) t = atomicAdd(A.queue ? A.q_ctr : A.counter, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
+    if (A.queue) t = resolve(t);
     int rec_lo = 0, rec_hi = 0;  // this lane's two words of the current task's record
     if (t < ntasks) {
       int r0, c0_, g0_, d0_;
@@ -843,13 +883,13 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       rec_hi = recs_of(d0_)[static_cast<size_t>(r0) * DAG_REC + lane + 32];
     }
     int tn_raw = 0;
-    if (lane == 0) tn_raw = atomicAdd(A.counter, 1);
+    if (lane == 0 && !A.queue) tn_raw = atomicAdd(A.counter, 1);
     for (;;) {
       if (t >= ntasks) {
         produce(2, 0, nullptr, make_uint2(0u, 0u), A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
         break;
       }
-      const int tn = __shfl_sync(0xffffffffu, tn_raw, 0);
+      const int tn = A.queue ? ntasks : __shfl_sync(0xffffffffu, tn_raw, 0);
       int nrec_lo = 0, nrec_hi = 0;
       if (tn < ntasks) {
         int rn_, cn_, gn_, dn_;
@@ -857,7 +897,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         nrec_lo = recs_of(dn_)[static_cast<size_t>(rn_) * DAG_REC + lane];
         nrec_hi = recs_of(dn_)[static_cast<size_t>(rn_) * DAG_REC + lane + 32];
       }
-      if (lane == 0) tn_raw = atomicAdd(A.counter, 1);
+      if (lane == 0 && !A.queue) tn_raw = atomicAdd(A.counter, 1);
       if (A.l2pf && tn < ntasks) {
         // warm L2 with the next task's tiles and solution blocks while this one streams
         int rn, cin, gin;
@@ -920,7 +960,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         my_mask = ch.prem[i];
       }
       const unsigned dep_ready = __ballot_sync(
-          0xffffffffu, lane >= nd || srcdep || ld_acquire(dflags + recp[DAG_REC_HDR + 2 * lane]) >= epoch);
+          0xffffffffu,
+          lane >= nd || srcdep || A.queue || ld_acquire(dflags + recp[DAG_REC_HDR + 2 * lane]) >= epoch);
       auto mask_of = [&](int q) {
         return make_uint2(__shfl_sync(0xffffffffu, my_mask.x, q), __shfl_sync(0xffffffffu, my_mask.y, q));
       };
@@ -944,8 +985,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
                   i, ci + dir * DAG2_CHAINS, gi, out);
       }
       for (int p0 = 0; p0 < pc; p0 += 32) {
-        const unsigned prdy =
-            __ballot_sync(0xffffffffu, p0 + lane >= pc || ld_acquire(cflags + pa + p0 + lane) >= epoch);
+        const unsigned prdy = __ballot_sync(
+            0xffffffffu, p0 + lane >= pc || A.queue || ld_acquire(cflags + pa + p0 + lane) >= epoch);
         for (int p = p0; p < pc && p < p0 + 32; ++p) {
           if (!((prdy >> (p - p0)) & 1u)) {
             const unsigned long long tw = trp ? gtimer() : 0;
@@ -981,9 +1022,21 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
         trp[4] = wsum;
         trp[5] = gtimer();
       }
-      t = tn;
-      rec_lo = nrec_lo;
-      rec_hi = nrec_hi;
+      if (A.queue) {  // pop the next ready task and load its record
+        int pos = 0;
+        if (lane == 0) pos = atomicAdd(A.q_ctr, 1);
+        t = resolve(__shfl_sync(0xffffffffu, pos, 0));
+        if (t < ntasks) {
+          int rq, cq, gq, dq;
+          decode(t, rq, cq, gq, dq);
+          rec_lo = recs_of(dq)[static_cast<size_t>(rq) * DAG_REC + lane];
+          rec_hi = recs_of(dq)[static_cast<size_t>(rq) * DAG_REC + lane + 32];
+        }
+      } else {
+        t = tn;
+        rec_lo = nrec_lo;
+        rec_hi = nrec_hi;
+      }
     }
     return;
   }
@@ -1043,6 +1096,21 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       if (threadIdx.x == 0) {
         const size_t cgi = static_cast<size_t>(m.ci - mdir * DAG2_CHAINS) * A.ngroups + m.gi;
         st_release(chunk ? A.cflags + cgi * A.cfs + m.out : A.flags + cgi * A.s.nb + m.i, A.epoch + mdir);
+      }
+      if (A.queue) {  // this task is done: count it in its dependents and push the ones now ready
+        consumers_sync();
+        __threadfence();
+        const int r = m.pad0 / (A.nchains * A.ngroups), rem = m.pad0 % (A.nchains * A.ngroups);
+        for (int q = A.q_dptr[r] + static_cast<int>(threadIdx.x); q < A.q_dptr[r + 1]; q += ST) {
+          const int d = A.q_didx[q];
+          const int idd = d * A.nchains * A.ngroups + rem;
+          if (atom_add_acq_rel(A.q_cnt + idd, 1) + 1 == A.q_cnt0[d]) {
+            const int pos = atomicAdd(A.q_ctr + 1, 1);
+            st_release(A.q_arr + pos, idd + 1);
+          }
+        }
+      }
+      if (threadIdx.x == 0) {
         if (A.trace) {
           unsigned long long* trc = A.trace + DAG_TRACE_WORDS * static_cast<size_t>(m.pad0);
           unsigned smid;
@@ -1164,7 +1232,8 @@ int dag_fused_launch(cudaStream_t st, const SpGeom& s, const DagSched& sf, const
 
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
-                    unsigned long long* trace, const int* tmap, bool presw, bool need_v2) {
+                    unsigned long long* trace, const int* tmap, bool presw, bool need_v2,
+                    const DagQueueWork* qw) {
   const int smem = DAG_SMEM_FIXED + (2 * DAG_REC + DAG_REC_DEPS + 8) * static_cast<int>(sizeof(int));
   static int attr_set = 0;
   if (smem > attr_set) {
@@ -1203,6 +1272,20 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   a.l2pf = l2pf;
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int ntasks = sched.ntask * nchains * a.ngroups;
+  if (qw && sched.q_cnt0 && !tmap) {  // ready-queue scheduling
+    a.queue = 1;
+    a.q_cnt0 = sched.q_cnt0;
+    a.q_dptr = sched.q_dptr;
+    a.q_didx = sched.q_didx;
+    a.q_init = sched.q_init;
+    a.q_ninit = sched.q_ninit;
+    a.q_cnt = qw->cnt;
+    a.q_arr = qw->q;
+    a.q_ctr = qw->ctr;
+    cudaMemsetAsync(qw->cnt, 0, sizeof(int) * ntasks, st);
+    cudaMemsetAsync(qw->q, 0, sizeof(int) * ntasks, st);
+    cudaMemsetAsync(qw->ctr, 0, sizeof(int) * 2, st);
+  }
   static const int v2 = [] {
     const char* v = std::getenv("ZOLO_DAG_V2");
     return v ? std::atoi(v) : 1;

@@ -320,3 +320,32 @@ np.savez(sys.argv[1], y=y, ga=op.apply_g(g["v"]))
         subprocess.run([sys.executable, "-c", code, f, case], check=True, cwd=root, env=env, timeout=300)
         outs.append(np.load(f))
     assert (outs[0]["y"] == outs[1]["y"]).all() and (outs[0]["ga"] == outs[1]["ga"]).all()
+
+
+@pytest.mark.parametrize("case", ["filter_cfg2_k6", "filter_cfg3_k5", "filter_cfg1_k16"])
+def test_ready_queue_schedule_is_bitwise_identical(zb, case):
+    """Ready-queue task scheduling (ZOLO_DAG_QUEUE=1: a task is popped once all its dependencies
+    are done) changes only when tasks run, not what they sum or in which order: identical bits."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from conftest import load_golden, golden_pencil
+import paper_1701_08935_b200 as zb
+g = load_golden(sys.argv[2])
+op = zb.FilterOperator(golden_pencil(g), g["design"], int(g["r"]), is_complex=bool(g["cx"]), nd_leaf=64)
+y, rep = op.apply_filter(g["v"])
+np.savez(sys.argv[1], y=y, ga=op.apply_g(g["v"]))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for queue in ("0", "1"):
+        f = tempfile.mktemp(suffix=".npz")
+        env = dict(os.environ, ZOLO_DAG_QUEUE=queue)
+        subprocess.run([sys.executable, "-c", code, f, case], check=True, cwd=root, env=env, timeout=300)
+        outs.append(np.load(f))
+    assert (outs[0]["y"] == outs[1]["y"]).all() and (outs[0]["ga"] == outs[1]["ga"]).all()
