@@ -63,8 +63,8 @@ __device__ __forceinline__ void dmma_nv(double c[2], double a, double b) {
 // Per-thread ownership of a 32 x 32 complex output block: warp w holds rows
 // 8 (w%4) + lane/4 and columns 8 (w/4) + 2 (lane%4) + {0,1} (+16 for the
 // second block), i.e. two 8x8 DMMA blocks that share their A fragments.
-// DMMA accumulators live across tiles: acc8[h][p][ri][e] (half h, k-step
-// parity p, re/im, element e) = 8 independent chains, folded once per task.
+// DMMA accumulators live across tiles: acc8[h][p][ri][e] (half h, product part
+// p: a.x or a.y products, re/im, element e) = 8 independent chains, folded once per task.
 struct Acc8 {
   double v[2][2][2][2];
 };
@@ -108,18 +108,19 @@ __device__ __forceinline__ void mma_tile2_t(Acc8& acc, const cd* ts, const cd* x
 #pragma unroll
   for (int kb = 0; kb < TILE / 4; ++kb) {
     if (!((km >> kb) & 1u)) continue;
-    const int p = kb & 1;
-    // op N: re += ax bx - ay by, im += ax by + ay bx; op H (conj a): re += ax bx + ay by, im += ax by - ay bx
+    // op N: re += ax bx - ay by, im += ax by + ay bx; op H (conj a): re += ax bx + ay by, im += ax by - ay bx.
+    // The a.x products and the a.y products accumulate in separate chains (second index), so the
+    // eight DMMAs of a k-step are independent: no DMMA waits on the one before it.
     const double ny = OPH ? a[kb].y : -a[kb].y;
     const double py = OPH ? -a[kb].y : a[kb].y;
-    dmma_nv(acc.v[0][p][0], a[kb].x, b0[kb].x);
-    dmma_nv(acc.v[1][p][0], a[kb].x, b1[kb].x);
-    dmma_nv(acc.v[0][p][1], a[kb].x, b0[kb].y);
-    dmma_nv(acc.v[1][p][1], a[kb].x, b1[kb].y);
-    dmma_nv(acc.v[0][p][0], ny, b0[kb].y);
-    dmma_nv(acc.v[1][p][0], ny, b1[kb].y);
-    dmma_nv(acc.v[0][p][1], py, b0[kb].x);
-    dmma_nv(acc.v[1][p][1], py, b1[kb].x);
+    dmma_nv(acc.v[0][0][0], a[kb].x, b0[kb].x);
+    dmma_nv(acc.v[1][0][0], a[kb].x, b1[kb].x);
+    dmma_nv(acc.v[0][0][1], a[kb].x, b0[kb].y);
+    dmma_nv(acc.v[1][0][1], a[kb].x, b1[kb].y);
+    dmma_nv(acc.v[0][1][0], ny, b0[kb].y);
+    dmma_nv(acc.v[1][1][0], ny, b1[kb].y);
+    dmma_nv(acc.v[0][1][1], py, b0[kb].x);
+    dmma_nv(acc.v[1][1][1], py, b1[kb].x);
   }
 }
 

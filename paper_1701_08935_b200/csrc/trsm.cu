@@ -1056,6 +1056,9 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     ntiles_task += m.kind == 0;
     if (m.kind == 0) {
       mma_tile2(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
+#ifdef ZOLO_DMMA2X  // (development timing probe, wrong results) twice the tensor work per stage
+      mma_tile2(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
+#endif
     } else {
       const cd* xs = x_s(s);
       const double sg = static_cast<double>(m.sign);
