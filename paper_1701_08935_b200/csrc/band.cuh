@@ -185,7 +185,8 @@ struct DagQueueWork {
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
                     unsigned long long* trace = nullptr, const int* tmap = nullptr, bool presw = false,
-                    bool need_v2 = false, const DagQueueWork* qw = nullptr);
+                    bool need_v2 = false, const DagQueueWork* qw = nullptr, const int* gact = nullptr,
+                    const int* gdone = nullptr);
 int dag_groups(int ncols);
 // forward + backward sweeps in one launch (v2 kernel); tmap: fused claim map (bit 30 = backward), or
 // nullptr for forward-then-backward order. Returns the grid, or -1 when the v2 kernel cannot run it.

@@ -199,6 +199,9 @@ struct zolo_ctx {
   int sel_s0 = 0, sel_K = 0;  // selectively inverted trailing block [sel_s0, sel_s0 + sel_K) (host.hpp DT_*)
   int sel_stage = 0;          // its backward input is staged into partial slots [sel_stage, sel_stage + sel_K)
   int iters_seen = 0;         // largest Krylov dimension an apply_filter on this context has needed
+  const int* lag_done = nullptr;  // lagged GMRES control: per-column done flags the sweeps may skip on
+  int* act_h2 = nullptr;          // second pinned active list / done buffer (lagged control)
+  int* done_h2 = nullptr;
   DevMem sp_seltab, sel_mem;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
   DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
@@ -232,6 +235,8 @@ struct zolo_ctx {
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   cudaEvent_t ev4 = nullptr, ev5 = nullptr;  // device-busy time of the GMRES iterations
+  cudaEvent_t lag_ev[10] = {};                // lagged GMRES loop: done-copy, sweep and busy events x 2
+  cudaEvent_t ev2_use = nullptr, ev3_use = nullptr;  // apply_g_device's sweep events when set
 
   // hybrid inner solve (BASELINE config 2): one factored pole,
   // shift-invariant GMRES on K_p^{-1} B for the others
@@ -1115,10 +1120,10 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   c.cflags_off = nbflags;
   if (c.counter.ensure(sizeof(int) * 4)) CK(cudaMemsetAsync(c.counter.p, 0, sizeof(int) * 4, c.st));
   c.act_d.ensure(sizeof(int) * nc);
-  if (c.act_h) cudaFreeHost(c.act_h);
-  if (c.done_h) cudaFreeHost(c.done_h);
-  CK(cudaMallocHost(&c.act_h, sizeof(int) * nc));
-  CK(cudaMallocHost(&c.done_h, sizeof(int) * nc));
+  for (int** hp : {&c.act_h, &c.done_h, &c.act_h2, &c.done_h2}) {
+    if (*hp) cudaFreeHost(*hp);
+    CK(cudaMallocHost(hp, sizeof(int) * nc));
+  }
   c.ncap = nc;
   c.maxit_cap = 0;  // GMRES state is sized per (ncap, maxit)
 }
@@ -1238,14 +1243,16 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
   }
   const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf,
                                  ++c.epoch, c.counter.as<int>(), 1, c.num_sms, trace,
-                                 full ? c.sp_tmap_fwd.as<int>() : nullptr, presw, need_v2, qwp);
+                                 full ? c.sp_tmap_fwd.as<int>() : nullptr, presw, need_v2, qwp, c.act_d.as<int>(),
+                                 c.lag_done);
   if (c.sel_K)  // the backward sweep runs in place: stage the inverted block's input first
     dag_stage_inputs(c.st, c.chains_bwd.as<Chain>() + first, nsub, static_cast<int64_t>(c.sel_s0) * TILE,
                      static_cast<int64_t>(c.sel_K) * TILE, na, ld, static_cast<int64_t>(TILE) * c.sched_bwd.nslots,
                      static_cast<int64_t>(c.sel_stage) * TILE);
   const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf,
                                  ++c.epoch, c.counter.as<int>() + 1, 0, c.num_sms, nullptr,
-                                 full ? c.sp_tmap_bwd.as<int>() : nullptr, presw, need_v2, qwp);
+                                 full ? c.sp_tmap_bwd.as<int>() : nullptr, presw, need_v2, qwp, c.act_d.as<int>(),
+                                 c.lag_done);
   if (g1 < 0 || g2 < 0)
     throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: the selectively inverted schedule needs the v2 sweep kernel "
                                      "(at most 32 chains, ZOLO_DAG_V2 on)");
@@ -1307,7 +1314,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   std::vector<cd*> xs(nch);
   for (int i = 0; i < nch; ++i) xs[i] = c.xbuf[i]->as<cd>();
   device_apply_b(c, vsrc, act, na, c.bbuf.as<cd>());
-  CK(cudaEventRecord(c.ev2, c.st));
+  CK(cudaEventRecord(c.ev2_use ? c.ev2_use : c.ev2, c.st));
   unsigned long long* fx = c.flags.as<unsigned long long>();
   int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
   if (c.sparse) {  // block-sparse factors: DAG-scheduled sweeps
@@ -1336,7 +1343,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
       }
       c.trace_done = true;
     }
-    CK(cudaEventRecord(c.ev3, c.st));
+    CK(cudaEventRecord(c.ev3_use ? c.ev3_use : c.ev3, c.st));
     CK(cudaGetLastError());
     combine_g(c, vsrc, act, na, xs, wdst);
     CK(cudaGetLastError());
@@ -1373,7 +1380,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
     throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: " + std::to_string(nch) + " chains x " +
                                          std::to_string((na + CG - 1) / CG) +
                                          " column groups exceed the resident CTA budget");
-  CK(cudaEventRecord(c.ev3, c.st));
+  CK(cudaEventRecord(c.ev3_use ? c.ev3_use : c.ev3, c.st));
   CK(cudaGetLastError());
   combine_g(c, vsrc, act, na, xs, wdst);
   CK(cudaGetLastError());
@@ -1623,7 +1630,7 @@ float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   else
     Krylov<double>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
                             c.bv_d.as<double>(), reinterpret_cast<const double*>(vsrc), act, na, c.bbuf.as<cd>());
-  CK(cudaEventRecord(c.ev2, c.st));
+  CK(cudaEventRecord(c.ev2_use ? c.ev2_use : c.ev2, c.st));
   const int nch = c.nchains();  // 1 (solve) or 2 (solve + adjoint)
   sweep_sparse(c, 0, nch, na);
   for (int k = 0; k < nch; ++k)
@@ -1632,7 +1639,7 @@ float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
     for (int k = 0; k < nch; ++k) inner_gmres(c, k, na);
   else
     for (int k = 0; k < nch; ++k) CK(cudaMemsetAsync(c.hy_y[k].p, 0, sizeof(cd) * ld * na, c.st));
-  CK(cudaEventRecord(c.ev3, c.st));
+  CK(cudaEventRecord(c.ev3_use ? c.ev3_use : c.ev3, c.st));
   std::vector<cd*> xs;
   xs.push_back(c.hy_x0[0].as<cd>());
   if (c.cx) xs.push_back(c.hy_x0[1].as<cd>());
@@ -1688,21 +1695,63 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   const int nchunk = static_cast<int>((ld + CHUNK - 1) / CHUNK);  // device rows incl. padding
   float trsm_ms = 0.0f, busy_ms = 0.0f;
   int trsm_launches = 0;
-  int64_t launches = 4, opapps = 0;
+  int64_t launches = 4;
   int its = 0;
+  // Lagged control: iteration it+1 is enqueued before iteration it's convergence flags reach the
+  // host, with the active list known from iteration it-1. Columns that converged in between are
+  // skipped on the device (done flags: the Arnoldi / least-squares kernels return, the sweeps skip
+  // fully converged column groups), so the GPU never waits for a host round trip. The hybrid solve
+  // keeps the synchronous loop (its inner GMRES must not see finished columns).
+  static const bool lag_env = env_int("ZOLO_GMRES_LAG", 1) != 0;
+  const bool lag = lag_env && !c.hybrid;
+  struct LagGuard {
+    zolo_ctx& c;
+    ~LagGuard() {
+      c.lag_done = nullptr;
+      c.ev2_use = c.ev3_use = nullptr;
+    }
+  } lag_guard{c};
+  c.lag_done = lag ? g.done : nullptr;
+  int* act_buf[2] = {c.act_h, c.act_h2};
+  int* done_buf[2] = {c.done_h, c.done_h2};
+  cudaEvent_t ev_done[2], ev_t[2][2], ev_b[2][2];
+  for (int p = 0; p < 2; ++p) {
+    ev_done[p] = c.lag_ev[p];
+    for (int q = 0; q < 2; ++q) ev_t[p][q] = c.lag_ev[2 + 2 * p + q], ev_b[p][q] = c.lag_ev[6 + 2 * p + q];
+  }
+  auto collect = [&](int p) {  // timings of a finished iteration of parity p
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev_t[p][0], ev_t[p][1]));
+    trsm_ms += ms;
+    CK(cudaEventElapsedTime(&ms, ev_b[p][0], ev_b[p][1]));
+    busy_ms += ms;
+  };
+  auto check_spin = [&] {
+    int spin_err[2] = {0, 0};
+    CK(cudaMemcpyAsync(spin_err, c.counter.as<int>() + 2, sizeof(int) * 2, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    if (spin_err[0] || spin_err[1]) throw ZoloError(ZOLO_ERR_CUDA, "triangular solve: dependency wait timed out");
+  };
+  auto filter_active = [&](const int* dn) {
+    std::vector<int> next;
+    for (int col : active)
+      if (!dn[col]) next.push_back(col);
+    active.swap(next);
+  };
+  int pending = -1;  // parity of the last enqueued iteration whose flags are not yet read
   for (int it = 0; it < maxit && !active.empty(); ++it) {
     its = it + 1;
+    const int p = it & 1;
     const int na = static_cast<int>(active.size());
-    std::memcpy(c.act_h, active.data(), sizeof(int) * na);
-    CK(cudaMemcpyAsync(c.act_d.p, c.act_h, sizeof(int) * na, cudaMemcpyHostToDevice, c.st));
+    std::memcpy(act_buf[p], active.data(), sizeof(int) * na);
+    CK(cudaMemcpyAsync(c.act_d.p, act_buf[p], sizeof(int) * na, cudaMemcpyHostToDevice, c.st));
     S* vm = reinterpret_cast<S*>(basis_block(c, it));
-    CK(cudaEventRecord(c.ev4, c.st));
+    CK(cudaEventRecord(ev_b[p][0], c.st));
+    c.ev2_use = ev_t[p][0];
+    c.ev3_use = ev_t[p][1];
     apply_g_device(c, vm, na, c.w.p);
     trsm_launches += 2;
     launches += 8 + (it + 1 < maxit ? 1 : 0);
-    opapps += na;
-    c.g_apps += na;
-    c.inner_solves += static_cast<int64_t>(c.nchains()) * na;
     Krylov<S>::arnoldi(c.st, ld, ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(), c.act_d.as<int>(), na, g,
                        c.partial.as<double>(), nchunk, c.hsave.as<S>());
     Krylov<S>::least_squares(c.st, c.act_d.as<int>(), na, it, g, c.partial.as<double>(), nchunk, tol);
@@ -1711,22 +1760,30 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       Krylov<S>::next_basis(c.st, n, ld, c.w.as<S>(), vn, c.act_d.as<int>(), na, g);
     }
     CK(cudaGetLastError());
-    CK(cudaEventRecord(c.ev5, c.st));
-    CK(cudaMemcpyAsync(c.done_h, g.done, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
-    int spin_err[2] = {0, 0};
-    CK(cudaMemcpyAsync(spin_err, c.counter.as<int>() + 2, sizeof(int) * 2, cudaMemcpyDeviceToHost, c.st));
-    CK(cudaStreamSynchronize(c.st));
-    if (spin_err[0] || spin_err[1]) throw ZoloError(ZOLO_ERR_CUDA, "triangular solve: dependency wait timed out");
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, c.ev2, c.ev3));
-    trsm_ms += ms;
-    CK(cudaEventElapsedTime(&ms, c.ev4, c.ev5));
-    busy_ms += ms;
-    std::vector<int> next;
-    for (int col : active)
-      if (!c.done_h[col]) next.push_back(col);
-    active.swap(next);
+    CK(cudaEventRecord(ev_b[p][1], c.st));
+    CK(cudaMemcpyAsync(done_buf[p], g.done, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaEventRecord(ev_done[p], c.st));
+    if (!lag) {
+      CK(cudaEventSynchronize(ev_done[p]));
+      check_spin();
+      collect(p);
+      filter_active(done_buf[p]);
+      continue;
+    }
+    if (pending >= 0) {  // the previous iteration's flags: the active list of the next one
+      CK(cudaEventSynchronize(ev_done[pending]));
+      collect(pending);
+      filter_active(done_buf[pending]);
+    }
+    pending = p;
   }
+  if (pending >= 0) {
+    CK(cudaEventSynchronize(ev_done[pending]));
+    collect(pending);
+  }
+  check_spin();
+  c.ev2_use = nullptr;
+  c.ev3_use = nullptr;
   c.iters_seen = std::max(c.iters_seen, its);
   S* yp = c.vout.as<S>();
   Krylov<S>::assemble(c.st, n, ld, v0, c.basis_ptrs.as<S*>(), static_cast<int>(ncols), g, vin, yp);
@@ -1740,7 +1797,6 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   c.last_ms[2] = trsm_ms;
   c.last_ms[3] = trsm_launches;
   c.last_ms[4] = static_cast<double>(launches + 2);
-  c.last_ms[5] = static_cast<double>(opapps);
   c.last_ms[6] = static_cast<double>(c.hy_inner_its);  // hybrid: inner K_p applications (column-steps)
   c.last_ms[7] = busy_ms;  // device time of the GMRES iterations (the rest of [0]: prologue, epilogue, host gaps)
 
@@ -1762,6 +1818,11 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       rep->converged[k] = 1;
     }
   }
+  int64_t opapps = 0;  // G applications = sum of the columns' Krylov dimensions (gmres.hpp:31-43)
+  for (int64_t col = 0; col < ncols; ++col) opapps += mcol[col];
+  c.g_apps += opapps;
+  c.inner_solves += static_cast<int64_t>(c.nchains()) * opapps;
+  c.last_ms[5] = static_cast<double>(opapps);
   for (int64_t col = 0; col < ncols; ++col) {
     for (int k = 0; k < q; ++k) {
       const double rk = res[col * q + k];
@@ -1983,6 +2044,7 @@ int zolo_ctx_create(int device, zolo_ctx** out) {
     CK(cudaEventCreate(&c->ev3));
     CK(cudaEventCreate(&c->ev4));
     CK(cudaEventCreate(&c->ev5));
+    for (auto& e : c->lag_ev) CK(cudaEventCreate(&e));
   });
   if (st != ZOLO_OK) {
     g_create_err = c->err;
@@ -2000,9 +2062,13 @@ int zolo_ctx_destroy(zolo_ctx* c) {
   for (auto s : c->pole_streams) cudaStreamDestroy(s);
   nccl_close(c->comm);
   if (c->act_h) cudaFreeHost(c->act_h);
+  if (c->act_h2) cudaFreeHost(c->act_h2);
+  if (c->done_h2) cudaFreeHost(c->done_h2);
   if (c->act_in_h) cudaFreeHost(c->act_in_h);
   if (c->done_h) cudaFreeHost(c->done_h);
   for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3, c->ev4, c->ev5, c->tev0, c->tev1})
+    if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : c->lag_ev)
     if (ev) cudaEventDestroy(ev);
   cudaStream_t st = c->st;
   delete c;

@@ -233,10 +233,12 @@ __global__ void scatter_cols_kernel(int64_t ld, const S* wc, const int* act, S* 
 // K1: partial dots <V_i, w> over a row chunk.
 template <class S>
 __global__ void __launch_bounds__(RT) dots_kernel(int64_t n, int64_t ld, S* const* basis, int m, const S* w,
-                                                  const int* act, S* partial, int nchunk, int hstride) {
+                                                  const int* act, S* partial, int nchunk, int hstride,
+                                                  const int* done) {
   __shared__ S red[RT / 32][KMAX];
   const int a = blockIdx.x, chunk = blockIdx.y;
   const int64_t col = act[a];
+  if (done[col]) return;  // converged in an earlier iteration (lagged active list)
   const int64_t base = static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
   S wr[RPT];
 #pragma unroll
@@ -269,11 +271,12 @@ template <class S, bool DOTS>
 __global__ void __launch_bounds__(RT) update_kernel(int64_t n, int64_t ld, S* const* basis, int m, S* w,
                                                     const int* act, const S* partial_in, S* partial_out,
                                                     double* norm_out, int nchunk, int hstride, S* hsave,
-                                                    void* Hmat, int maxit) {
+                                                    void* Hmat, int maxit, const int* done) {
   __shared__ S hs[KMAX];
   __shared__ S red[RT / 32][KMAX];
   const int a = blockIdx.x, chunk = blockIdx.y;
   const int64_t col = act[a];
+  if (done[col]) return;
   if (threadIdx.x <= m) {
     S tot = szero(S());
     for (int c = 0; c < nchunk; ++c) tot = sadd(tot, partial_in[(static_cast<int64_t>(a) * nchunk + c) * hstride + threadIdx.x]);
@@ -381,6 +384,7 @@ __global__ void least_squares_kernel(const int* act, int m, GmresDev g, const do
   __shared__ int done_s, happy_s;
   const int a = blockIdx.x, k = threadIdx.x;
   const int col = act[a];
+  if (g.done[col]) return;  // converged in an earlier iteration (lagged active list): state frozen
   const int maxit = g.maxit;
   S* H = reinterpret_cast<S*>(g.H) + static_cast<int64_t>(col) * (maxit + 1) * maxit;
   const double beta = g.beta[col];
@@ -627,11 +631,11 @@ void Krylov<S>::arnoldi(cudaStream_t st, int64_t n, int64_t ld, S* const* d_basi
   S* p2 = p1 + static_cast<int64_t>(na) * nchunk * hstride;
   double* pn = reinterpret_cast<double*>(p1);  // norm partials reuse p1 after K2
   const dim3 grid(na, nchunk);
-  dots_kernel<S><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p1, nchunk, hstride);
+  dots_kernel<S><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p1, nchunk, hstride, g.done);
   update_kernel<S, true><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p1, p2, nullptr, nchunk, hstride, hsave,
-                                              g.H, g.maxit);
+                                              g.H, g.maxit, g.done);
   update_kernel<S, false><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p2, nullptr, pn, nchunk, hstride, hsave,
-                                               g.H, g.maxit);
+                                               g.H, g.maxit, g.done);
 }
 template <class S>
 void Krylov<S>::least_squares(cudaStream_t st, const int* act, int na, int m, GmresDev g, const double* partial,

@@ -450,6 +450,10 @@ struct DagArgs {
   int* q_cnt = nullptr;  // per task: dependencies completed
   int* q_arr = nullptr;  // pushed task ids + 1
   int* q_ctr = nullptr;  // [0] pops, [1] pushes
+  // lagged GMRES control (capi apply_filter_impl): the launch covers a superset of the columns
+  // still running; a task whose column group has converged entirely is skipped
+  const int* gact = nullptr;
+  const int* gdone = nullptr;
 };
 
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
@@ -847,6 +851,18 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
     };
     auto recs_of = [&](int dir) { return dir ? A.recs_b : A.recs; };
+    // lagged GMRES control: the column groups whose columns have all converged (read once)
+    unsigned gmask = 0;
+    if (A.gdone && A.ngroups <= 32) {
+      for (int gg = 0; gg < A.ngroups; ++gg) {
+        const int cg0 = gg * DCG, ncg = min(DCG, A.ncols - cg0);
+        if (__all_sync(0xffffffffu, lane >= ncg || A.gdone[A.gact[cg0 + lane]] != 0)) gmask |= 1u << gg;
+      }
+      if (gmask == (A.ngroups == 32 ? ~0u : (1u << A.ngroups) - 1u)) {  // nothing left: leave at once
+        produce(2, 0, nullptr, make_uint2(0u, 0u), A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
+        return;
+      }
+    }
     // ready queue: pop position -> task id (the initial records directly, later ones once pushed)
     const int q_base = A.q_ninit * per_step;
     auto resolve = [&](int pos) {
@@ -951,6 +967,9 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       const int* flags = A.flags + cgi * A.s.nb;
       const int* cflags = A.cflags + cgi * A.cfs;
       const int* dflags = slotdep ? cflags : flags;  // where dependency q's readiness lives
+      // every task of a fully converged column group skips (its dependents are in the same group)
+      const bool skip = (gmask >> gi) & 1u;
+      if (!skip) {
       // occupancy masks of all the task's tiles (lane q: dependency q, lane 31: the pre-transform)
       // and readiness of every dependency, each read in parallel (one round trip)
       uint2 my_mask = make_uint2(0xffffffffu, 0xffffffffu);
@@ -1017,6 +1036,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
           produce(0, 1, ch.minv + static_cast<size_t>(tid) * TT, mask_of(q), ch.cbuf + static_cast<int64_t>(j) * TILE,
                   ldp, c0, nc, pol_stream, e == nent, i, cix, gi, out);
       }
+      }  // !skip
       __syncwarp();
       if (trp && lane == 0) {
         trp[4] = wsum;
@@ -1236,7 +1256,7 @@ int dag_fused_launch(cudaStream_t st, const SpGeom& s, const DagSched& sf, const
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
                     int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int fwd, int num_sms,
                     unsigned long long* trace, const int* tmap, bool presw, bool need_v2,
-                    const DagQueueWork* qw) {
+                    const DagQueueWork* qw, const int* gact, const int* gdone) {
   const int smem = DAG_SMEM_FIXED + (2 * DAG_REC + DAG_REC_DEPS + 8) * static_cast<int>(sizeof(int));
   static int attr_set = 0;
   if (smem > attr_set) {
@@ -1288,6 +1308,10 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
     cudaMemsetAsync(qw->cnt, 0, sizeof(int) * ntasks, st);
     cudaMemsetAsync(qw->q, 0, sizeof(int) * ntasks, st);
     cudaMemsetAsync(qw->ctr, 0, sizeof(int) * 2, st);
+  }
+  if (!a.queue && gdone) {  // lagged GMRES control: converged column groups skip their tasks
+    a.gact = gact;
+    a.gdone = gdone;
   }
   static const int v2 = [] {
     const char* v = std::getenv("ZOLO_DAG_V2");
