@@ -112,6 +112,7 @@ DESCR = {
     "cfg2": "3D 7-point Laplacian 32^3 + U[0,1] potential, SPD mass B",
     "cfg3": "complex Hermitian 3D tight-binding 48^3 (Peierls phases, Anderson disorder 1.5), B=I+0.05 S",
     "cfg4": "chemistry-shaped block-sparse Hermitian pencil, 8000 atoms x 13x13 blocks, SPD overlap B",
+    "cfg4s": "config 4's chemistry-shaped BSR pencil at 1000 atoms x 13x13 blocks (one-GPU size), SPD overlap B",
     "cfg5": "complex Hermitian 3D tight-binding 64^3 (disorder 2), B=I",
 }
 
@@ -203,6 +204,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1701_08935_b200 as zb
+    from paper_1701_08935_b200 import configs
     from paper_1701_08935_b200.design import build_filter_design
 
     pen, cx, gaps, r, nv, nl = workload(args.config)
@@ -214,7 +216,8 @@ def main():
 
         op = pole_sharded_operator(pen, design, r, cx, local)
     else:
-        op = zb.FilterOperator(pen, design, r, is_complex=cx, device=local)
+        op = zb.FilterOperator(pen, design, r, is_complex=cx, device=local,
+                               block_size=configs.BLOCK_SIZE.get(args.config, 1))
     t_factor_ms = op.last_timings()["factor_ms"]
     sp = op.sweep_profile()
 

@@ -203,10 +203,17 @@ WINDOWS = {
     # tools/find_window_gpu.py cfg4 0.0 200: chemistry_pencil(20, seed=4), 200 eigenvalues around 0
     "cfg4": {"gaps": [-0.0014473551429546204, -0.0014319087193143789, 0.0014380021788383598, 0.0014440721712162489],
              "count": 200},
+    # tools/find_window_gpu.py cfg4s 0.0 32: chemistry_pencil(10, seed=4), 32 eigenvalues around 0
+    "cfg4s": {"gaps": [-0.002050713632706902, -0.00195394425863924, 0.0019219309968320887, 0.002050941998095368],
+              "count": 32},
     # tools/find_window_gpu.py cfg5 0.0 256: multi_gpu_pencil(64, seed=5), 256 eigenvalues around 0
     "cfg5": {"gaps": [-0.004444281498217607, -0.004424367355750291, 0.004403209645170138, 0.004455014820632642],
              "count": 256},
 }
+
+
+# BSR block size of a config's pencil (atoms of 13 rows for the chemistry-shaped configs)
+BLOCK_SIZE = {"cfg4": 13, "cfg4s": 13}
 
 
 def config(name: str):
@@ -223,6 +230,9 @@ def config(name: str):
     if name == "cfg4":  # ~35 GB of factors per pole: all 8 poles need pole sharding (8 GPUs) or the hybrid solve
         w = WINDOWS["cfg4"]
         return chemistry_pencil(20, seed=4), True, w["gaps"], 8, 256, w["count"]
+    if name == "cfg4s":  # config 4's generator at 10^3 atoms (N = 13000): fits one GPU with all 8 poles
+        w = WINDOWS["cfg4s"]
+        return chemistry_pencil(10, seed=4), True, w["gaps"], 8, 64, w["count"]
     if name == "cfg5":
         w = WINDOWS["cfg5"]
         return multi_gpu_pencil(64, seed=5), True, w["gaps"], 8, 320, w["count"]

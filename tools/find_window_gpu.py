@@ -1,7 +1,7 @@
 """Locate a BASELINE window on the GPU by Sylvester-inertia bisection
 (paper_1701_08935_b200/slicing.py) and print its gap endpoints for configs.py.
 
-usage: python tools/find_window_gpu.py cfg3|cfg4|cfg5 [center] [count]
+usage: python tools/find_window_gpu.py cfg3|cfg4|cfg4s|cfg5 [center] [count]
 """
 import sys
 import time
@@ -15,6 +15,7 @@ center = float(sys.argv[2]) if len(sys.argv) > 2 else 0.0
 count = int(sys.argv[3]) if len(sys.argv) > 3 else 128
 gen = {"cfg3": lambda: configs.tight_binding_pencil(48, seed=3, disorder=1.5),
        "cfg4": lambda: configs.chemistry_pencil(20, seed=4),
+       "cfg4s": lambda: configs.chemistry_pencil(10, seed=4),
        "cfg5": lambda: configs.multi_gpu_pencil(64, seed=5)}[name]
 t0 = time.time()
 pen = gen()

@@ -16,7 +16,8 @@ for name in sys.argv[1:] or ["cfg1", "cfg2"]:
     design = build_filter_design(gaps, r)
     t0 = time.time()
     order = os.environ.get("ORDER", "nd")
-    op = zb.FilterOperator(pen, design, r, is_complex=cx, ordering=order, nd_leaf=int(os.environ.get("ND_LEAF", "192")))
+    op = zb.FilterOperator(pen, design, r, is_complex=cx, ordering=order, nd_leaf=int(os.environ.get("ND_LEAF", "192")),
+                           block_size=configs.BLOCK_SIZE.get(name, 1))
     t1 = time.time()
     prof = op.factor_profile()[0]
     print(f"{name} [{order}]: N={pen[0]} bw={prof['bandwidth']} factor wall {t1 - t0:.2f}s device {op.last_timings()['factor_ms']:.1f} ms"
