@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include "krylov.cuh"
+#include "mma.cuh"
 
 namespace zolo {
 
@@ -652,18 +653,110 @@ void Krylov<S>::assemble(cudaStream_t st, int64_t n, int64_t ld, const S* v0, S*
                          const S* vin, S* out) {
   if (nv > 0) assemble_kernel<S><<<dim3(blocks_for(ld, 256), nv), 256, 0, st>>>(ld, d_basis, g, vin, out);
 }
+// ---- Rayleigh-Ritz block algebra on the FP64 tensor cores (complex pencils) ----------
+// (Y^H A Y, Y^H B Y, the CholQR Gram matrices and Q = Y Q~ are
+// tall-skinny GEMMs). A 32 x 32 block of a column-major matrix into the swizzled tile layout
+// (rows >= nr or columns >= nc are zero).
+__device__ __forceinline__ void load_block_sw(cd* s, const cd* g, int64_t ld, int64_t nr, int64_t nc) {
+  for (int e = threadIdx.x; e < TT; e += ST) {
+    const int col = e / TILE, row = e % TILE;
+    cd* dst = &s[col * TILE + (row ^ swz(col))];
+    if (row < nr && col < nc)
+      cp_async16_cg(dst, g + row + col * ld);
+    else
+      *dst = mk(0.0, 0.0);
+  }
+}
+// a 32 x 32 block as the right operand [col * XPAD + row]
+__device__ __forceinline__ void load_block_x(cd* xs, const cd* g, int64_t ld, int64_t nr, int64_t nc) {
+  for (int e = threadIdx.x; e < TILE * TILE; e += ST) {
+    const int col = e / TILE, row = e % TILE;
+    cd* dst = &xs[col * XPAD + row];
+    if (row < nr && col < nc)
+      cp_async16_cg(dst, g + row + col * ld);
+    else
+      *dst = mk(0.0, 0.0);
+  }
+}
+
+// partial[chunk] (k x kk, row-major like gram_partial_kernel) = Y[rows of chunk]^H Z[rows of chunk]:
+// one 32 x 32 output tile per CTA, 32-row blocks of the chunk as DMMA tile products (op H)
+__global__ void __launch_bounds__(ST) gram_dmma_kernel(int64_t n, int64_t ld, const cd* y, int64_t k, const cd* z,
+                                                       int64_t kk, cd* partial) {
+  __shared__ __align__(16) cd ts[TT];
+  __shared__ __align__(16) cd xs[XS2];
+  const int64_t ti = static_cast<int64_t>(blockIdx.y) * TILE, tj = static_cast<int64_t>(blockIdx.z) * TILE;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * CHUNK;
+  const int64_t rend = r0 + CHUNK < n ? r0 + CHUNK : n;
+  const Frag f = frag();
+  Acc8 acc;
+  acc8_zero(acc);
+  for (int64_t rb = r0; rb < rend; rb += TILE) {
+    load_block_sw(ts, y + rb + ti * ld, ld, rend - rb, k - ti);
+    load_block_x(xs, z + rb + tj * ld, ld, rend - rb, kk - tj);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    mma_tile2(acc, ts, xs, true, false, f, 0xffu);
+    __syncthreads();
+  }
+  cd o[4];
+  acc8_fold(acc, o);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t i = ti + f.row, j = tj + ocol(f, q);
+    if (i < k && j < kk) partial[(static_cast<int64_t>(blockIdx.x) * k + i) * kk + j] = o[q];
+  }
+}
+
+// out (ld x kk) = Y (ld x k) Q (k x kk): one 32-row x 32-column output tile per CTA
+__global__ void __launch_bounds__(ST) block_gemm_dmma_kernel(int64_t ld, const cd* y, int64_t k, const cd* q,
+                                                             int64_t kk, cd* out) {
+  __shared__ __align__(16) cd ts[TT];
+  __shared__ __align__(16) cd xs[XS2];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * TILE, tj = static_cast<int64_t>(blockIdx.y) * TILE;
+  const Frag f = frag();
+  Acc8 acc;
+  acc8_zero(acc);
+  for (int64_t kb = 0; kb < k; kb += TILE) {
+    load_block_sw(ts, y + r0 + kb * ld, ld, ld - r0, k - kb);
+    load_block_x(xs, q + kb + tj * k, k, k - kb, kk - tj);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    mma_tile2(acc, ts, xs, false, false, f, 0xffu);
+    __syncthreads();
+  }
+  cd o[4];
+  acc8_fold(acc, o);
+#pragma unroll
+  for (int qq = 0; qq < 4; ++qq) {
+    const int64_t r = r0 + f.row, j = tj + ocol(f, qq);
+    if (r < ld && j < kk) out[r + j * ld] = o[qq];
+  }
+}
+
 template <class S>
 void Krylov<S>::gram(cudaStream_t st, int64_t n, int64_t ld, const S* y, int64_t k, const S* z, int64_t kk, S* out,
                      double* partial) {
   const int nchunk = static_cast<int>((n + CHUNK - 1) / CHUNK);
   S* p = reinterpret_cast<S*>(partial);
-  gram_partial_kernel<S><<<dim3(nchunk, blocks_for(k, GB), blocks_for(kk, GB)), 256, 0, st>>>(n, ld, y, k, z, kk, p);
+  if constexpr (sizeof(S) == sizeof(cd))  // complex: DMMA tile products
+    gram_dmma_kernel<<<dim3(nchunk, blocks_for(k, TILE), blocks_for(kk, TILE)), ST, 0, st>>>(
+        n, ld, reinterpret_cast<const cd*>(y), k, reinterpret_cast<const cd*>(z), kk, reinterpret_cast<cd*>(p));
+  else
+    gram_partial_kernel<S><<<dim3(nchunk, blocks_for(k, GB), blocks_for(kk, GB)), 256, 0, st>>>(n, ld, y, k, z, kk, p);
   gram_reduce_kernel<S><<<blocks_for(k * kk, 256), 256, 0, st>>>(p, nchunk, k, kk, out);
 }
 template <class S>
 void Krylov<S>::block_gemm(cudaStream_t st, int64_t n, int64_t ld, const S* y, int64_t k, const S* q, int64_t kk,
                            S* out) {
-  if (kk > 0) block_gemm_kernel<S><<<dim3(blocks_for(ld, 256), kk), 256, 0, st>>>(ld, y, k, q, kk, out);
+  if (kk <= 0) return;
+  if constexpr (sizeof(S) == sizeof(cd))
+    block_gemm_dmma_kernel<<<dim3(blocks_for(ld, TILE), blocks_for(kk, TILE)), ST, 0, st>>>(
+        ld, reinterpret_cast<const cd*>(y), k, reinterpret_cast<const cd*>(q), kk, reinterpret_cast<cd*>(out));
+  else
+    block_gemm_kernel<S><<<dim3(blocks_for(ld, 256), kk), 256, 0, st>>>(ld, y, k, q, kk, out);
 }
 template <class S>
 void Krylov<S>::spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,

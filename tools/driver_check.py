@@ -1,7 +1,7 @@
 """End-to-end eigensolver (subspace_iteration on the GPU filter) on a BASELINE
 config: time-to-all-eigenpairs (BASELINE metric 2) and the solve statistics.
 
-usage: python tools/driver_check.py cfg2 [oversample]
+usage: python tools/driver_check.py cfg2 [tol]
 """
 import sys
 import time
@@ -14,7 +14,8 @@ from paper_1701_08935_b200.driver import SolveConfig, subspace_iteration  # noqa
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 pen, cx, gaps, r, nv, nl = configs.config(name)
-cfg = SolveConfig(n_lambda=nl, oversample_k=nv - nl, r=r, tol=1e-10, seed=1)
+tol = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-10
+cfg = SolveConfig(n_lambda=nl, oversample_k=nv - nl, r=r, tol=tol, seed=1)
 for rep in range(2):
     t0 = time.time()
     res = subspace_iteration(pen, gaps, cfg, is_complex=cx)
