@@ -10,7 +10,7 @@ import torch
 res = {}
 if not os.path.exists("tools/fp64_peak"):  # probe binary (not versioned): build it for sm_100a
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", "tools/fp64_peak",
-                    "tools/fp64_peak.cu", "-lcublas"], check=True)
+                    "tools/fp64_peak.cu"], check=True)
 out = subprocess.run(["./tools/fp64_peak"], capture_output=True, text=True).stdout.strip()
 res.update(json.loads(out))
 for name, dt, mult in (("dgemm", torch.float64, 2), ("zgemm", torch.complex128, 8)):
