@@ -209,6 +209,23 @@ bool chol_inverse(int k, const std::vector<S>& g, std::vector<S>& rinv) {
   return true;
 }
 
+// fn(c) for c in [0, n) on the host cores (the n_v x n_v products of the Rayleigh-Ritz step);
+// each c is computed by one thread in the serial order, so the result does not depend on threading
+template <class F>
+void par_for(int n, F&& fn) {
+  const int nt = static_cast<int>(std::min<unsigned>(16u, std::max(1u, std::thread::hardware_concurrency())));
+  if (n < 64 || nt < 2) {
+    for (int c = 0; c < n; ++c) fn(c);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int q = 0; q < nt; ++q)
+    pool.emplace_back([&, q] {
+      for (int c = q; c < n; c += nt) fn(c);
+    });
+  for (auto& t : pool) t.join();
+}
+
 void ck(zolo_ctx* ctx, int st) {
   if (st != ZOLO_OK) throw Fail(st, zolo_last_error(ctx));
 }
@@ -323,27 +340,30 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
       for (int i = 0; i < k; ++i) w[static_cast<size_t>(c) * k + i] = vb[static_cast<size_t>(kept[c]) * k + i] * sc;
     }
     std::vector<S> aw(static_cast<size_t>(k) * kk, S(0)), ar(static_cast<size_t>(kk) * kk, S(0));
-    for (int c = 0; c < kk; ++c)
+    par_for(kk, [&](int c) {
       for (int p = 0; p < k; ++p) {
         const S wpc = w[static_cast<size_t>(c) * k + p];
         for (int i = 0; i < k; ++i) aw[static_cast<size_t>(c) * k + i] += at[static_cast<size_t>(p) * k + i] * wpc;
       }
-    for (int c = 0; c < kk; ++c)
+    });
+    par_for(kk, [&](int c) {
       for (int i = 0; i < kk; ++i) {
         S s(0);
         for (int p = 0; p < k; ++p) s += conj_s(w[static_cast<size_t>(i) * k + p]) * aw[static_cast<size_t>(c) * k + p];
         ar[static_cast<size_t>(c) * kk + i] = s;
       }
+    });
     hermitianize(kk, ar);
     std::vector<double> ritz;
     std::vector<S> qa;
     herm_eig(kk, ar, ritz, qa);
     std::vector<S> small(static_cast<size_t>(k) * kk, S(0));
-    for (int c = 0; c < kk; ++c)
+    par_for(kk, [&](int c) {
       for (int p = 0; p < kk; ++p) {
         const S v = qa[static_cast<size_t>(c) * kk + p];
         for (int i = 0; i < k; ++i) small[static_cast<size_t>(c) * k + i] += w[static_cast<size_t>(p) * k + i] * v;
       }
+    });
     ck(ctx, zolo_block_gemm_device(ctx, y.p, kq, reinterpret_cast<const double*>(small.data()), kk, q.p));
     kq = kk;
 
