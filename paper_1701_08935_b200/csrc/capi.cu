@@ -200,8 +200,8 @@ struct zolo_ctx {
   int sel_stage = 0;          // its backward input is staged into partial slots [sel_stage, sel_stage + sel_K)
   int iters_seen = 0;         // largest Krylov dimension an apply_filter on this context has needed
   const int* lag_done = nullptr;  // lagged GMRES control: per-column done flags the sweeps may skip on
-  int* act_h2 = nullptr;          // second pinned active list / done buffer (lagged control)
-  int* done_h2 = nullptr;
+  int* act_hq[4] = {};   // pinned active lists / done flags, one per lagged-loop slot
+  int* done_hq[4] = {};
   DevMem sp_seltab, sel_mem;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
   DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
@@ -235,7 +235,7 @@ struct zolo_ctx {
   cudaEvent_t tev0 = nullptr, tev1 = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   cudaEvent_t ev4 = nullptr, ev5 = nullptr;  // device-busy time of the GMRES iterations
-  cudaEvent_t lag_ev[10] = {};                // lagged GMRES loop: done-copy, sweep and busy events x 2
+  cudaEvent_t lag_ev[20] = {};                // lagged GMRES loop: done-copy, sweep and busy events x 4 slots
   cudaEvent_t ev2_use = nullptr, ev3_use = nullptr;  // apply_g_device's sweep events when set
 
   // hybrid inner solve (BASELINE config 2): one factored pole,
@@ -1120,7 +1120,8 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   c.cflags_off = nbflags;
   if (c.counter.ensure(sizeof(int) * 4)) CK(cudaMemsetAsync(c.counter.p, 0, sizeof(int) * 4, c.st));
   c.act_d.ensure(sizeof(int) * nc);
-  for (int** hp : {&c.act_h, &c.done_h, &c.act_h2, &c.done_h2}) {
+  for (int** hp : {&c.act_h, &c.done_h, &c.act_hq[0], &c.act_hq[1], &c.act_hq[2], &c.act_hq[3], &c.done_hq[0],
+                    &c.done_hq[1], &c.done_hq[2], &c.done_hq[3]}) {
     if (*hp) cudaFreeHost(*hp);
     CK(cudaMallocHost(hp, sizeof(int) * nc));
   }
@@ -1697,13 +1698,16 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   int trsm_launches = 0;
   int64_t launches = 4;
   int its = 0;
-  // Lagged control: iteration it+1 is enqueued before iteration it's convergence flags reach the
-  // host, with the active list known from iteration it-1. Columns that converged in between are
-  // skipped on the device (done flags: the Arnoldi / least-squares kernels return, the sweeps skip
-  // fully converged column groups), so the GPU never waits for a host round trip. The hybrid solve
-  // keeps the synchronous loop (its inner GMRES must not see finished columns).
-  static const bool lag_env = env_int("ZOLO_GMRES_LAG", 1) != 0;
-  const bool lag = lag_env && !c.hybrid;
+  // Lagged control: iterations are enqueued up to `lag` ahead of the convergence flags the host
+  // has read -- the active list of iteration it+1 is the one known from iteration it-lag+... i.e.
+  // filtered by the flags of iteration it+1-lag-1. Columns that converged in between are skipped
+  // on the device (done flags: the Arnoldi / least-squares kernels return, the sweeps skip fully
+  // converged column groups, an all-converged sweep exits at once), so the GPU does not wait for
+  // host round trips and a short host stall is absorbed by the queued iterations. The hybrid
+  // solve keeps the synchronous loop (its inner GMRES must not see finished columns).
+  static const int lag_env = std::min(std::max(env_int("ZOLO_GMRES_LAG", 2), 0), 3);
+  const int lag = c.hybrid ? 0 : lag_env;
+  const int nslot = lag + 1;
   struct LagGuard {
     zolo_ctx& c;
     ~LagGuard() {
@@ -1712,14 +1716,12 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     }
   } lag_guard{c};
   c.lag_done = lag ? g.done : nullptr;
-  int* act_buf[2] = {c.act_h, c.act_h2};
-  int* done_buf[2] = {c.done_h, c.done_h2};
-  cudaEvent_t ev_done[2], ev_t[2][2], ev_b[2][2];
-  for (int p = 0; p < 2; ++p) {
+  cudaEvent_t ev_done[4], ev_t[4][2], ev_b[4][2];
+  for (int p = 0; p < 4; ++p) {
     ev_done[p] = c.lag_ev[p];
-    for (int q = 0; q < 2; ++q) ev_t[p][q] = c.lag_ev[2 + 2 * p + q], ev_b[p][q] = c.lag_ev[6 + 2 * p + q];
+    for (int q = 0; q < 2; ++q) ev_t[p][q] = c.lag_ev[4 + 2 * p + q], ev_b[p][q] = c.lag_ev[12 + 2 * p + q];
   }
-  auto collect = [&](int p) {  // timings of a finished iteration of parity p
+  auto collect = [&](int p) {  // timings of a finished iteration in slot p
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, ev_t[p][0], ev_t[p][1]));
     trsm_ms += ms;
@@ -1738,13 +1740,13 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       if (!dn[col]) next.push_back(col);
     active.swap(next);
   };
-  int pending = -1;  // parity of the last enqueued iteration whose flags are not yet read
+  int pend[4], npend = 0;  // slots enqueued whose flags are not yet read, oldest first
   for (int it = 0; it < maxit && !active.empty(); ++it) {
     its = it + 1;
-    const int p = it & 1;
+    const int p = it % nslot;  // its previous user (iteration it - nslot) has been read
     const int na = static_cast<int>(active.size());
-    std::memcpy(act_buf[p], active.data(), sizeof(int) * na);
-    CK(cudaMemcpyAsync(c.act_d.p, act_buf[p], sizeof(int) * na, cudaMemcpyHostToDevice, c.st));
+    std::memcpy(c.act_hq[p], active.data(), sizeof(int) * na);
+    CK(cudaMemcpyAsync(c.act_d.p, c.act_hq[p], sizeof(int) * na, cudaMemcpyHostToDevice, c.st));
     S* vm = reinterpret_cast<S*>(basis_block(c, it));
     CK(cudaEventRecord(ev_b[p][0], c.st));
     c.ev2_use = ev_t[p][0];
@@ -1761,25 +1763,22 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev_b[p][1], c.st));
-    CK(cudaMemcpyAsync(done_buf[p], g.done, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaMemcpyAsync(c.done_hq[p], g.done, sizeof(int) * ncols, cudaMemcpyDeviceToHost, c.st));
     CK(cudaEventRecord(ev_done[p], c.st));
-    if (!lag) {
-      CK(cudaEventSynchronize(ev_done[p]));
-      check_spin();
-      collect(p);
-      filter_active(done_buf[p]);
-      continue;
+    pend[npend++] = p;
+    if (npend > lag) {  // the oldest pending iteration's flags: filter the next active list
+      const int q = pend[0];
+      for (int k = 1; k < npend; ++k) pend[k - 1] = pend[k];
+      --npend;
+      CK(cudaEventSynchronize(ev_done[q]));
+      if (!lag) check_spin();
+      collect(q);
+      filter_active(c.done_hq[q]);
     }
-    if (pending >= 0) {  // the previous iteration's flags: the active list of the next one
-      CK(cudaEventSynchronize(ev_done[pending]));
-      collect(pending);
-      filter_active(done_buf[pending]);
-    }
-    pending = p;
   }
-  if (pending >= 0) {
-    CK(cudaEventSynchronize(ev_done[pending]));
-    collect(pending);
+  for (int k = 0; k < npend; ++k) {
+    CK(cudaEventSynchronize(ev_done[pend[k]]));
+    collect(pend[k]);
   }
   check_spin();
   c.ev2_use = nullptr;
@@ -2044,7 +2043,7 @@ int zolo_ctx_create(int device, zolo_ctx** out) {
     CK(cudaEventCreate(&c->ev3));
     CK(cudaEventCreate(&c->ev4));
     CK(cudaEventCreate(&c->ev5));
-    for (auto& e : c->lag_ev) CK(cudaEventCreate(&e));
+    for (auto& e : c->lag_ev) CK(cudaEventCreate(&e));  // 4 slots x (done copy, sweep pair, busy pair)
   });
   if (st != ZOLO_OK) {
     g_create_err = c->err;
@@ -2062,8 +2061,10 @@ int zolo_ctx_destroy(zolo_ctx* c) {
   for (auto s : c->pole_streams) cudaStreamDestroy(s);
   nccl_close(c->comm);
   if (c->act_h) cudaFreeHost(c->act_h);
-  if (c->act_h2) cudaFreeHost(c->act_h2);
-  if (c->done_h2) cudaFreeHost(c->done_h2);
+  for (int q = 0; q < 4; ++q) {
+    if (c->act_hq[q]) cudaFreeHost(c->act_hq[q]);
+    if (c->done_hq[q]) cudaFreeHost(c->done_hq[q]);
+  }
   if (c->act_in_h) cudaFreeHost(c->act_in_h);
   if (c->done_h) cudaFreeHost(c->done_h);
   for (cudaEvent_t ev : {c->ev0, c->ev1, c->ev2, c->ev3, c->ev4, c->ev5, c->tev0, c->tev1})
