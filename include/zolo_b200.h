@@ -268,6 +268,12 @@ int zolo_timer(zolo_ctx* ctx, int op, double* ms);
  * out[4] block rows of the largest trailing dense block, out[5] tile-aligned
  * node groups, out[6..7] reserved. */
 int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* out);
+/* Builds the DAG sweep schedules (both directions) of the ND factor of a pattern and checks them
+ * on the host (no reference equivalent; test support): out[0] = violations (0 when every block
+ * row has one row task, every dependency is summed exactly once, every partial slot is written
+ * once and the claim order is topological), out[1] tasks, out[2] partial slots, out[3] block rows. */
+int zolo_dag_schedule_check(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int near, int chunk,
+                            int order, int64_t* out);
 /* reorder_rcm (rcm.hpp:69-115) of a structurally symmetric pattern;
  * perm[new] = old. bw/profile (rcm.hpp:118-147) may be NULL. */
 int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int64_t* bw, int64_t* profile);

@@ -2546,6 +2546,62 @@ int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t l
   }
 }
 
+int zolo_dag_schedule_check(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int near, int chunk,
+                            int order, int64_t* out) {
+  try {
+    std::vector<std::vector<int64_t>> nodes;
+    nd_order(n, rp, ci, leaf, nodes);
+    BlockStructure bs;
+    block_symbolic(n, rp, ci, nodes, TILE, bs);
+    const int64_t nb = bs.nb;
+    int64_t bad = 0, ntask = 0, nslot_all = 0;
+    for (int dir = 0; dir < 2; ++dir) {
+      const bool fwd = dir == 0;
+      const auto& ptr = fwd ? bs.row_ptr : bs.col_ptr;
+      const auto& idx = fwd ? bs.row_idx : bs.col_idx;
+      std::vector<DagTask> ts;
+      const int nslots = dag_schedule(nb, ptr, idx, fwd, chunk, near, order, ts);
+      // every row has one row task; every dependency of every row is summed exactly once; every
+      // slot is written once; a task appears after the tasks it waits on (claim order topological)
+      std::vector<int64_t> row_at(nb, -1), slot_at(nslots, -1), covered(nb, 0);
+      for (size_t t = 0; t < ts.size(); ++t) {
+        const DagTask& k = ts[t];
+        if (k.out >= 0) {
+          if (slot_at[k.out] >= 0) ++bad;
+          slot_at[k.out] = static_cast<int64_t>(t);
+        } else {
+          if (row_at[k.i] >= 0) ++bad;
+          row_at[k.i] = static_cast<int64_t>(t);
+        }
+        covered[k.i] += k.qb - k.qa;
+      }
+      for (size_t t = 0; t < ts.size(); ++t) {
+        const DagTask& k = ts[t];
+        const int64_t e0 = ptr[k.i];
+        const int nd = static_cast<int>(ptr[k.i + 1] - e0);
+        for (int q = k.qa; q < k.qb; ++q) {
+          const int64_t j = fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q];
+          if (row_at[j] < 0 || row_at[j] >= static_cast<int64_t>(t)) ++bad;
+        }
+        for (int pq = k.pa; pq < k.pa + k.pc; ++pq)
+          if (pq >= nslots || slot_at[pq] < 0 || slot_at[pq] >= static_cast<int64_t>(t)) ++bad;
+      }
+      for (int64_t i = 0; i < nb; ++i)
+        if (row_at[i] < 0 || covered[i] != ptr[i + 1] - ptr[i]) ++bad;
+      ntask += static_cast<int64_t>(ts.size());
+      nslot_all += nslots;
+    }
+    out[0] = bad;
+    out[1] = ntask;
+    out[2] = nslot_all;
+    out[3] = nb;
+    return ZOLO_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_DOMAIN;
+  }
+}
+
 int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int64_t* bw, int64_t* profile) {
   try {
     rcm_order(n, rp, ci, perm);

@@ -118,3 +118,44 @@ def test_random_block_is_bit_identical_to_reference():
     g = load_golden("solve_driver_cfg3_k5")
     q0 = zb.random_block(125, 16, 1, cx=True, orthonormalize=True)
     assert np.abs(q0 - g["q0"]).max() == 0.0
+
+
+@pytest.mark.parametrize("name,near,chunk,order", [("grid2d", 4, 16, 3), ("grid3d", 4, 16, 3), ("grid3d", 2, 8, 1),
+                                                   ("grid3d", 3, 12, 0), ("random", 4, 16, 2)])
+def test_dag_schedules_are_complete_and_topological(name, near, chunk, order):
+    """The claim-ordered sweep schedules (symbolic.cpp dag_schedule) of the ND factor: one row task
+    per block row, every dependency summed exactly once (near in the row task, the rest in chunk
+    tasks), every partial slot written once, and every task after the tasks it waits on -- the
+    property that lets persistent CTAs claim in order without deadlock (checked in C++ on the host)."""
+    import ctypes as C
+
+    import scipy.sparse as sp
+
+    import paper_1701_08935_b200 as zb
+
+    if name == "grid2d":
+        k = 40
+        t = sp.diags([1.0, 1.0, 1.0], [-1, 0, 1], shape=(k, k))
+        m = sp.kron(t, sp.identity(k)) + sp.kron(sp.identity(k), t)
+    elif name == "grid3d":
+        k = 14
+        t = sp.diags([1.0, 1.0, 1.0], [-1, 0, 1], shape=(k, k))
+        i = sp.identity(k)
+        m = sp.kron(sp.kron(t, i), i) + sp.kron(sp.kron(i, t), i) + sp.kron(sp.kron(i, i), t)
+    else:
+        rng = np.random.default_rng(7)
+        n = 1500
+        r = sp.random(n, n, density=0.004, random_state=rng)
+        m = r + r.T + sp.identity(n)
+    m = sp.csr_matrix(m)
+    m.sort_indices()
+    rp, ci = m.indptr.astype(np.int64), m.indices.astype(np.int64)
+    out = np.zeros(4, dtype=np.int64)
+    L = zb.lib()
+    L.zolo_dag_schedule_check.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                          C.c_void_p]
+    st = L.zolo_dag_schedule_check(m.shape[0], rp.ctypes.data, ci.ctypes.data, 64, near, chunk, order,
+                                   out.ctypes.data)
+    assert st == 0
+    assert out[0] == 0, f"{out[0]} schedule violations"
+    assert out[1] >= 2 * out[3]  # at least one row task per block row and direction
