@@ -35,6 +35,9 @@
 
 namespace zolo {
 void gmres_init(cudaStream_t st, GmresDev g);
+// the caching device allocator below, for the other translation units (driver.cu)
+void* device_alloc(size_t bytes, size_t* got);
+void device_free(void* p, size_t bytes);
 }
 
 using namespace zolo;
@@ -53,6 +56,70 @@ struct ZoloError : std::runtime_error {
       throw ZoloError(ZOLO_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));         \
   } while (0)
 
+// Process-wide caching device allocator: freed blocks stay mapped and are handed to later
+// requests of up to 2x smaller size on the same device, so repeated contexts (every eigensolver
+// call builds one: factors, workspaces, Krylov basis) skip cudaMalloc / cudaFree, driver round
+// trips that cost milliseconds each on a busy host. A release synchronizes the device first, as
+// cudaFree did, so a cached block is never reused while a kernel may still touch it.
+struct DevPool {
+  std::mutex mu;
+  std::map<int, std::multimap<size_t, void*>> cache;
+  std::map<int, size_t> cached;
+};
+DevPool& dev_pool() {
+  static DevPool* pool = new DevPool;  // never destroyed: blocks live until process exit
+  return *pool;
+}
+size_t pool_cached_bytes() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  return P.cached[dev];
+}
+void pool_trim(int dev) {
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  for (auto& kv : P.cache[dev]) cudaFree(kv.second);
+  P.cache[dev].clear();
+  P.cached[dev] = 0;
+}
+// returns the block and its size (>= b), or nullptr
+void* pool_alloc(size_t b, size_t* got) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevPool& P = dev_pool();
+  {
+    std::lock_guard<std::mutex> lock(P.mu);
+    auto& m = P.cache[dev];
+    auto it = m.lower_bound(b);
+    if (it != m.end() && it->first <= 2 * b + (size_t(1) << 20)) {
+      void* p = it->second;
+      *got = it->first;
+      P.cached[dev] -= it->first;
+      m.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, b) != cudaSuccess) {
+    cudaGetLastError();
+    pool_trim(dev);  // give the cached blocks back and retry once
+    if (cudaMalloc(&p, b) != cudaSuccess) return nullptr;
+  }
+  *got = b;
+  return p;
+}
+void pool_free(void* p, size_t b) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceSynchronize();
+  DevPool& P = dev_pool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  P.cache[dev].emplace(b, p);
+  P.cached[dev] += b;
+}
+
 struct DevMem {
   void* p = nullptr;
   size_t bytes = 0;
@@ -61,7 +128,7 @@ struct DevMem {
   DevMem& operator=(const DevMem&) = delete;
   ~DevMem() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p, bytes);
     p = nullptr;
     bytes = 0;
   }
@@ -70,11 +137,13 @@ struct DevMem {
     if (b <= bytes && p) return false;
     release();
     if (b == 0) b = 16;
-    cudaError_t e = cudaMalloc(&p, b);
-    if (e != cudaSuccess) {
-      p = nullptr;
+    size_t got = 0;
+    p = pool_alloc(b, &got);
+    if (!p) {
+      cudaError_t e = cudaGetLastError();
       throw ZoloError(ZOLO_ERR_CUDA, "cudaMalloc(" + std::to_string(b) + " B): " + cudaGetErrorString(e));
     }
+    b = got;
     static const bool zero = std::getenv("ZOLO_ZERO_ALLOC") != nullptr;  // (debug) zero-fill allocations
     if (zero) {
       cudaMemset(p, 0, b);
@@ -140,6 +209,11 @@ void upload(DevMem& m, const std::vector<T>& v, cudaStream_t st) {
 }
 
 }  // namespace
+
+namespace zolo {
+void* device_alloc(size_t bytes, size_t* got) { return pool_alloc(bytes, got); }
+void device_free(void* p, size_t bytes) { pool_free(p, bytes); }
+}  // namespace zolo
 
 struct zolo_ctx {
   int device = 0;
@@ -547,7 +621,8 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
   CK(cudaMemGetInfo(&free_b, &total_b));
   const size_t need = per_pole * r * sizeof(cd);
   c.tiles_mem.release();
-  if (need + (size_t(1) << 30) > free_b + c.tiles_mem.bytes)
+  free_b += pool_cached_bytes();  // cached blocks are reusable
+  if (need + (size_t(1) << 30) > free_b)
     throw ZoloError(ZOLO_ERR_DOMAIN, "zolo_factorize: band factors need " + std::to_string(need >> 20) +
                                          " MiB, device has " + std::to_string(free_b >> 20) + " MiB free");
   c.tiles_mem.ensure(need);
@@ -889,6 +964,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   size_t free_b = 0, total_b = 0;
   store.release();
   CK(cudaMemGetInfo(&free_b, &total_b));
+  free_b += pool_cached_bytes();  // cached blocks are reusable
   const size_t need = per_pole * r * sizeof(cd);
   if (need + (size_t(1) << 30) > free_b)
     throw ZoloError(ZOLO_ERR_DOMAIN, "zolo_factorize: factors need " + std::to_string(need >> 20) +
@@ -2333,14 +2409,19 @@ int apply_filter_batched_at(zolo_ctx& c, const void* d_v, void* d_y, int64_t nco
                 : apply_filter_impl<double>(c, v, y, k, tol, gmres_max, r);
   };
   const double per_col = bytes_per_column(c, budget_its);
+  static const int64_t forced = env_int("ZOLO_FILTER_BATCH", 0);  // (testing) force a column batch size
+  // the workspace of an earlier application fits: no device-memory query (cudaMemGetInfo is a
+  // driver round trip that can take milliseconds on a busy host)
+  if (forced <= 0 && ncols <= c.ncap) return run(d_v, d_y, ncols, rep);
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
-  static const int64_t forced = env_int("ZOLO_FILTER_BATCH", 0);  // (testing) force a column batch size
+  free_b += pool_cached_bytes();
   int64_t batch = forced > 0 ? forced : ncols;
   if (forced <= 0) {
-    if (ncols <= c.ncap || ncols * per_col < 0.85 * free_b) return run(d_v, d_y, ncols, rep);
+    if (ncols * per_col < 0.85 * free_b) return run(d_v, d_y, ncols, rep);
     release_workspace(c);
     CK(cudaMemGetInfo(&free_b, &total_b));
+    free_b += pool_cached_bytes();
     batch = std::max<int64_t>(1, static_cast<int64_t>(0.85 * free_b / per_col));
     constexpr int64_t G = 32;  // columns per sweep task group (mma.cuh DCG)
     if (batch >= G) {          // whole column groups, spread evenly over the batches

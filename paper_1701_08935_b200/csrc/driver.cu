@@ -33,6 +33,11 @@
 #include "../../include/zolo_b200.h"
 #include "host.hpp"
 
+namespace zolo {
+void* device_alloc(size_t bytes, size_t* got);
+void device_free(void* p, size_t bytes);
+}
+
 namespace {
 
 using cplx = std::complex<double>;
@@ -235,14 +240,18 @@ void cuda_ck(cudaError_t e) {
 
 struct DevBuf {
   void* p = nullptr;
+  size_t got = 0;
   explicit DevBuf(size_t bytes) {
-    cuda_ck(cudaMalloc(&p, bytes ? bytes : 16));
+    p = zolo::device_alloc(bytes ? bytes : 16, &got);  // capi.cu's caching allocator
+    if (!p) throw Fail(ZOLO_ERR_CUDA, "cudaMalloc: out of device memory");
     if (std::getenv("ZOLO_ZERO_ALLOC")) {
       cuda_ck(cudaMemset(p, 0, bytes ? bytes : 16));
       cuda_ck(cudaDeviceSynchronize());
     }
   }
-  ~DevBuf() { cudaFree(p); }
+  ~DevBuf() {
+    if (p) zolo::device_free(p, got);
+  }
 };
 
 template <class S>
@@ -292,6 +301,7 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
         throw Fail(ZOLO_ERR_NUMERICAL, "subspace_iteration: random block failed to orthonormalize");
       ck(ctx, zolo_block_gemm_device(ctx, q.p, n_ss, reinterpret_cast<const double*>(rinv.data()), n_ss, t.p));
       std::swap(q.p, t.p);
+      std::swap(q.got, t.got);  // block sizes travel with the blocks (caching allocator)
     }
   }
 
