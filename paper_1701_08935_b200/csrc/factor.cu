@@ -114,25 +114,30 @@ __device__ __forceinline__ void diag_factor_body(int64_t n, int k, cd* tile, cd*
                                                  const double* row_norm, int* fail_index,
                                                  unsigned long long* min_ratio_bits) {
   extern __shared__ __align__(16) unsigned char diag_smem[];
+  __shared__ double rn_s[TILE];
   cd* D = reinterpret_cast<cd*>(diag_smem);
   cd* XL = D + TILE * TPAD;
   cd* XU = XL + TILE * TPAD;
   cd(*red)[4][TILE] = reinterpret_cast<cd(*)[4][TILE]>(XU + TILE * TPAD);
   load_tile_async(D, tile);
   cp_async_commit();
+  const int t = threadIdx.x;
+  if (t < TILE) {  // the pivot monitor's 32 row norms, read once instead of one round trip per pivot
+    const int64_t gi = static_cast<int64_t>(k) * TILE + t;
+    rn_s[t] = gi < n ? row_norm[gi] : 0.0;
+  }
   cp_async_wait<0>();
   __syncthreads();
-  const int t = threadIdx.x;
+  double min_ratio = INFINITY;  // thread 0: the smallest |pivot| / ||row|| of the tile
   for (int p = 0; p < TILE; ++p) {
     const cd piv = D[p * TPAD + p];
     const cd inv = cdiv(mk(1.0, 0.0), piv);
     if (t == 0) {
       const int64_t gi = static_cast<int64_t>(k) * TILE + p;
       if (gi < n) {
-        const double rn = row_norm[gi];
+        const double rn = rn_s[p];
         const double ap = hypot(piv.x, piv.y);
-        const double ratio = ap / fmax(rn, 1e-300);
-        atomicMin(min_ratio_bits, static_cast<unsigned long long>(__double_as_longlong(ratio)));
+        min_ratio = fmin(min_ratio, ap / fmax(rn, 1e-300));
         if (!(ap > 1e-14 * rn) && *fail_index < 0) *fail_index = static_cast<int>(gi);
       }
     }
@@ -145,6 +150,8 @@ __device__ __forceinline__ void diag_factor_body(int64_t n, int k, cd* tile, cd*
     }
     __syncthreads();
   }
+  if (t == 0 && min_ratio < INFINITY)
+    atomicMin(min_ratio_bits, static_cast<unsigned long long>(__double_as_longlong(min_ratio)));
   for (int q = 0; q < TT / FT; ++q) {
     const int e = t + q * FT;
     tile[e] = D[(e / TILE) * TPAD + (e % TILE)];
