@@ -24,8 +24,8 @@ namespace {
 
 constexpr int RT = 256;          // threads per reduction block
 constexpr int RPT = CHUNK / RT;  // rows per thread in a chunk
-constexpr int KMAX = 256;
-constexpr int SPC = 8;            // SpMM columns per thread         // largest Krylov dimension (outer GMRES <= 64, hybrid inner <= 256)
+constexpr int KMAX = 256;        // largest Krylov dimension (outer GMRES <= 64, hybrid inner <= 256)
+constexpr int SPC = 8;           // SpMM columns per thread (4 and 16 measured the same)
 
 template <class S>
 __device__ __forceinline__ S warp_sum(S v);
