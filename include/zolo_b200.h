@@ -121,17 +121,18 @@ int zolo_set_block_size(zolo_ctx* ctx, int64_t block);
  * SpMMs run on CSR: block 1, or an ordering that splits atoms). */
 int zolo_bsr_info(const zolo_ctx* ctx, int64_t* out);
 
-/* Ordering / factor layout used by zolo_factorize:
+/* Ordering used by zolo_factorize (both factor into 32 x 32-tile block-sparse
+ * LU factors with DAG-scheduled sweeps):
  *   ZOLO_ORDER_ND   (default) nested dissection (recursive BFS-level bisection,
  *                   leaves of <= nd_leaf rows ordered by RCM; default 192,
- *                   nd_leaf <= 0 keeps the current value), block-sparse
- *                   32x32-tile factors, DAG-scheduled sweeps -- short
- *                   dependency chains;
- *   ZOLO_ORDER_RCM  the reference's RCM ordering and banded factors
- *                   (band_factor.hpp), envelope-aware block band, pipelined
- *                   sweeps; FactorizationError indices match the reference.
- * With an explicit perm in zolo_factorize, ND mode factors that ordering as
- * block-sparse (no dissection). Pivot indices refer to the chosen order. */
+ *                   nd_leaf <= 0 keeps the current value) -- short dependency
+ *                   chains;
+ *   ZOLO_ORDER_RCM  the reference's RCM ordering of the pattern of A - iB
+ *                   (band_factor.hpp:203-204, rcm.hpp:69-115): the factor is the
+ *                   reference's band envelope, and FactorizationError pivot
+ *                   indices are the reference's (positions in RCM order).
+ * With an explicit perm in zolo_factorize, that ordering is factored as is.
+ * Pivot indices refer to positions in the chosen order. */
 enum { ZOLO_ORDER_ND = 0, ZOLO_ORDER_RCM = 1 };
 int zolo_set_ordering(zolo_ctx* ctx, int mode, int64_t nd_leaf);
 
@@ -189,7 +190,10 @@ int zolo_apply_g(zolo_ctx* ctx, const double* v, double* gv, int64_t ncols);
  * host block: all 2r outer shifts +-i sqrt(outer.c[2j]) in one multi-shift
  * GMRES per column (lock-step batched on the device), combined as
  * 1/2 M_outer sum_j 1/2 a_j (x_2j + x_2j+1) + 1/2 v. Returns ZOLO_ERR_GMRES
- * with rep filled (y still written) when some shift misses gmres_tol. */
+ * with rep filled (y still written) when some shift misses gmres_tol.
+ * gmres_max <= ZOLO_KRYLOV_MAX (the reference has no cap, gmres.hpp:98-101;
+ * the device keeps at most that many basis vectors per column). */
+#define ZOLO_KRYLOV_MAX 256
 int zolo_apply_filter(zolo_ctx* ctx, const double* v, double* y, int64_t ncols, double gmres_tol,
                       int64_t gmres_max, zolo_report* rep);
 
@@ -221,19 +225,37 @@ int zolo_residual_norms_device(zolo_ctx* ctx, const void* d_ax, const void* d_bx
                                double* num, double* den);
 
 /* --- driver: subspace_iteration (eigensolver.hpp:154-217) ---------------- */
-/* Filtered subspace iteration with Rayleigh-Ritz on this context's GPU:
- * builds the design for window_from_gaps(gaps) at order r (r <= 0 picks
- * choose_order, filter_design.hpp:219-232), factorizes, iterates. lambdas
- * has room for n_lambda + oversample values; vectors (optional) for
- * n x (n_lambda + oversample) entries. stats (12 doubles): n_ss, n_iter,
- * n_gmres, n_gmres_min, n_solv, t_fact [s], t_iter [s], residual (reference
- * scaling max(|a|,|b|)), converged, r, residual scaled by |lambda|,
- * device filter time [ms]. */
+/* Filtered subspace iteration with Rayleigh-Ritz on this context's GPU for the
+ * packed filter design `design` of order r (built on the host, e.g. by the
+ * reference's build_filter_design; the window (a, b) is design[0..1]):
+ * factorizes, iterates. lambdas has room for n_lambda + oversample values;
+ * vectors (optional) for n x (n_lambda + oversample) entries. stats (14 doubles):
+ * n_ss, n_iter, n_gmres, n_gmres_min, n_solv, t_fact [s], t_iter [s], residual
+ * (reference scaling max(|a|,|b|)), converged, r, residual scaled by |lambda|,
+ * device filter time [ms], first refined iteration (0 = none), residual of the
+ * first iteration.
+ * refine: residual-correction refinement of the shifted solves (see
+ * zolo_set_refinement): 0 never, 1 always, -1 automatic (once an iteration has
+ * brought the residual below 1e-5 without meeting tol: the remaining gap is the
+ * solves' rounding floor, eps / min pivot ratio of the unpivoted LU). */
 int zolo_subspace_iteration(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
                             const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v,
-                            const double* gaps, int64_t n_lambda, int64_t oversample, int r, double tol,
-                            int64_t max_iters, double gmres_tol, int64_t gmres_max, uint64_t seed, double* lambdas,
-                            int64_t* n_found, double* vectors, double* stats);
+                            const double* design, int r, int64_t n_lambda, int64_t oversample, double tol,
+                            int64_t max_iters, double gmres_tol, int64_t gmres_max, uint64_t seed, int refine,
+                            double* lambdas, int64_t* n_found, double* vectors, double* stats);
+
+/* Residual-correction (iterative) refinement of every shifted solve:
+ * x = K^-1 b, then `steps` times x += K^-1 (b - K x) with K = A - sigma_j B
+ * (K^H for the adjoint solves), the residual formed from the pencil's CSR
+ * in FP64. The unpivoted LU's rounding (eps / min pivot ratio, band_factor.hpp
+ * has no pivoting) then drops to the backward-stable level; each step costs one
+ * more sweep pair. Counters keep the reference's meaning (one solve per
+ * shifted system). steps in [0, 2]; 0 (default) = the reference's plain solve. */
+int zolo_set_refinement(zolo_ctx* ctx, int steps);
+
+/* Return the device memory cached by the library's allocator on `device`
+ * (blocks of destroyed contexts) to the driver. */
+int zolo_pool_trim(int device);
 
 /* Set the context's (or, with NULL, the global) last-error message. */
 void zolo_set_error(zolo_ctx* ctx, const char* msg);
@@ -250,10 +272,8 @@ int zolo_last_timings(const zolo_ctx* ctx, double* ms);
 
 /* Structure the triangular sweeps run over (per pole, after zolo_factorize):
  * out[0] block rows (32-row tiles), out[1] off-diagonal tiles of L (= of U),
- * out[2] / out[3] forward / backward DAG task records (0 for the band layout),
- * out[4] chunk partial-sum slots, out[5] critical path in block rows,
- * out[6] layout: 0 = block-sparse (ND), 1 = block band (RCM), out[7] block rows of the
- * selectively inverted trailing block (0 = none).
+ * out[2] / out[3] forward / backward DAG task records, out[4] chunk
+ * partial-sum slots, out[5] critical path in block rows, out[6..7] reserved.
  * No equivalent in the reference (development / roofline accounting). */
 int zolo_sweep_profile(const zolo_ctx* ctx, int64_t* out);
 
@@ -290,15 +310,6 @@ int zolo_random_block(int scalar, int64_t n, int64_t k, uint64_t seed, int ortho
  * reference's disorder convention (hamiltonian.hpp:52); used by the
  * synthetic config generators. */
 int zolo_uniform_stream(uint64_t seed, int64_t n, double* out);
-
-/* build_filter_design (filter_design.hpp:133-169) for the window given by its
- * four gap endpoints (window_from_gaps, window.hpp:56-68; a_minus may be
- * -inf, b_plus +inf) at order r; writes ZOLO_DESIGN_LEN(r) doubles. */
-int zolo_build_design(const double* gaps, int r, double* design);
-
-/* eval_g_scalar / eval_filter_scalar (filter_design.hpp:72-82) at npts points;
- * either output may be NULL. */
-int zolo_eval_filter(const double* gaps, int r, int64_t npts, const double* x, double* g_out, double* filter_out);
 
 /* Library version / build tag. */
 const char* zolo_version(void);

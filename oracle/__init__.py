@@ -106,6 +106,18 @@ class Reference(_Lib):
         self._check(self.lib.zr_eval_scalar(_ptr(g), C.c_int(r), _I64(x.size), _ptr(x), _ptr(gv), _ptr(fv)))
         return gv, fv
 
+    def uniform_stream(self, seed, n):
+        out = np.zeros(int(n))
+        self._check(self.lib.zr_uniform_stream(C.c_uint64(seed), _I64(n), _ptr(out)))
+        return out
+
+    def choose_order(self, gaps, eps):
+        g = np.asarray(gaps, dtype=np.float64)
+        r = C.c_int(0)
+        b = np.zeros(1)
+        self._check(self.lib.zr_choose_order(_ptr(g), _D(eps), C.byref(r), _ptr(b)))
+        return int(r.value), float(b[0])
+
     def random_block(self, n, k, seed, cx=False, orthonormalize=False):
         out = np.zeros((n, k), dtype=np.complex128 if cx else np.float64, order="F")
         self._check(self.lib.zr_random_block(C.c_int(int(cx)), _I64(n), _I64(k), C.c_uint64(seed),

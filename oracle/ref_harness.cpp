@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -159,6 +160,25 @@ int zr_eval_scalar(const double* gaps, int r, int64_t npts, const double* x, dou
       if (g_out) g_out[i] = eval_g_scalar(d, x[i]);
       if (filt_out) filt_out[i] = eval_filter_scalar(d, x[i]);
     }
+  });
+}
+
+/// choose_order (filter_design.hpp:219-232): smallest r in [1,8] meeting eps (8 when capped).
+int zr_choose_order(const double* gaps, double eps, int* r_out, double* bound) {
+  return guarded([&] {
+    const OrderChoice c = choose_order(window_of(gaps), eps);
+    *r_out = c.r;
+    if (bound) *bound = c.bound;
+  });
+}
+
+/// n uniforms in [0,1) from raw mt19937_64 bits, (x >> 11) 2^-53 -- the reference's disorder
+/// convention (hamiltonian.hpp:50-53): the seeded inputs of the BASELINE config generators, drawn
+/// here so that a reference-side process needs no product library.
+int zr_uniform_stream(uint64_t seed, int64_t n, double* out) {
+  return guarded([&] {
+    std::mt19937_64 gen(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
   });
 }
 

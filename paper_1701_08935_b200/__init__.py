@@ -144,13 +144,18 @@ def lib():
         L.zolo_rcm.argtypes = [I64, P, P, P, P, P]
         L.zolo_random_block.argtypes = [C.c_int, I64, I64, C.c_uint64, C.c_int, P]
         L.zolo_uniform_stream.argtypes = [C.c_uint64, I64, P]
-        L.zolo_build_design.argtypes = [P, C.c_int, P]
-        L.zolo_eval_filter.argtypes = [P, C.c_int, I64, P, P, P]
+        L.zolo_set_refinement.argtypes = [P, C.c_int]
+        L.zolo_pool_trim.argtypes = [C.c_int]
         _lib = L
     return _lib
 
 
 NCCL_ID_BYTES = 128
+
+
+def pool_trim(device: int = 0) -> None:
+    """Return the device memory the library's allocator keeps cached to the driver."""
+    lib().zolo_pool_trim(int(device))
 
 
 def nccl_unique_id() -> bytes:
@@ -295,11 +300,13 @@ class FilterOperator:
     ``solve="hybrid"`` factors only pole ``hybrid_pole`` and solves the other
     shifted systems by shift-invariant GMRES on K_p^{-1} B (zolo_set_solve_mode;
     BASELINE config 2) to ``inner_tol`` within ``inner_max`` iterations.
+    ``refine=k`` adds k residual-correction steps to every shifted solve
+    (zolo_set_refinement; 0 = the reference's plain solve).
     """
 
     def __init__(self, pencil, design, r: int, is_complex: Optional[bool] = None, device: int = 0, perm=None,
                  ordering: str = "nd", nd_leaf: int = 192, shard=None, solve: str = "direct", hybrid_pole: int = 0,
-                 inner_tol: float = 1e-14, inner_max: int = 256, block_size: int = 1):
+                 inner_tol: float = 1e-14, inner_max: int = 256, block_size: int = 1, refine: int = 0):
         L = lib()
         n, a, b = pencil
         cx = bool(is_complex) if is_complex is not None else np.iscomplexobj(a[2])
@@ -335,6 +342,8 @@ class FilterOperator:
         if solve == "hybrid":
             _check(h, L.zolo_set_solve_mode(h, 1, int(hybrid_pole), float(inner_tol), int(inner_max)))
             self.poles = [int(hybrid_pole)]
+        if refine:
+            _check(h, L.zolo_set_refinement(h, int(refine)))
         self.stats = (FactorStats * self.r)()
         perm_arr = None if perm is None else np.ascontiguousarray(perm, dtype=np.int64)
         st = L.zolo_factorize(h, _ptr(perm_arr), self.stats)
@@ -435,6 +444,10 @@ class FilterOperator:
         _check(self._h, lib().zolo_block_update(self._h, _ptr(y), y.shape[1], _ptr(q), q.shape[1], _ptr(out)))
         return out
 
+    def set_refinement(self, steps: int):
+        """Residual-correction steps per shifted solve from the next application on."""
+        _check(self._h, lib().zolo_set_refinement(self._h, int(steps)))
+
     def last_timings(self):
         ms = np.zeros(8)
         lib().zolo_last_timings(self._h, _ptr(ms))
@@ -453,8 +466,7 @@ class FilterOperator:
         out = np.zeros(8, dtype=np.int64)
         _check(self._h, lib().zolo_sweep_profile(self._h, _ptr(out)))
         return dict(block_rows=int(out[0]), offdiag_tiles=int(out[1]), fwd_tasks=int(out[2]),
-                    bwd_tasks=int(out[3]), chunk_slots=int(out[4]), critical_path=int(out[5]),
-                    layout="band" if out[6] == 1 else "block-sparse", selinv_rows=int(out[7]))
+                    bwd_tasks=int(out[3]), chunk_slots=int(out[4]), critical_path=int(out[5]))
 
     def timer_start(self):
         _check(self._h, lib().zolo_timer(self._h, 0, None))

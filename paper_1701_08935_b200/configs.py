@@ -21,7 +21,21 @@ import scipy.sparse as sp
 from . import _ptr, lib
 
 
+_UNIFORM = None  # alternative source of the stream (a process that must not load the product library)
+
+
+def use_uniform_source(fn) -> None:
+    """Draw the seeded uniforms from fn(seed, n) instead of the product library's
+    zolo_uniform_stream -- bench.py's reference arm passes the reference harness's
+    zr_uniform_stream (oracle/_ref), so its process maps no product code. Both are the
+    raw mt19937_64 stream (pinned equal in tests/test_host_setup.py)."""
+    global _UNIFORM
+    _UNIFORM = fn
+
+
 def uniform(seed: int, n: int) -> np.ndarray:
+    if _UNIFORM is not None:
+        return np.asarray(_UNIFORM(seed, n), dtype=np.float64)
     out = np.zeros(n)
     lib().zolo_uniform_stream(seed, n, _ptr(out))
     return out

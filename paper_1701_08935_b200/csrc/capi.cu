@@ -28,16 +28,16 @@
 #include <vector>
 
 #include "../../include/zolo_b200.h"
-#include "band.cuh"
 #include "host.hpp"
 #include "krylov.cuh"
+#include "tiles.cuh"
 #include "shard.hpp"
 
 namespace zolo {
 void gmres_init(cudaStream_t st, GmresDev g);
 // the caching device allocator below, for the other translation units (driver.cu)
-void* device_alloc(size_t bytes, size_t* got);
-void device_free(void* p, size_t bytes);
+void* device_alloc(size_t bytes, size_t* got, cudaStream_t st);
+void device_free(void* p, size_t bytes, cudaStream_t st);
 }
 
 using namespace zolo;
@@ -59,16 +59,30 @@ struct ZoloError : std::runtime_error {
 // Process-wide caching device allocator: freed blocks stay mapped and are handed to later
 // requests of up to 2x smaller size on the same device, so repeated contexts (every eigensolver
 // call builds one: factors, workspaces, Krylov basis) skip cudaMalloc / cudaFree, driver round
-// trips that cost milliseconds each on a busy host. A release synchronizes the device first, as
-// cudaFree did, so a cached block is never reused while a kernel may still touch it.
+// trips that cost milliseconds each on a busy host. A block is released with an event recorded
+// on the stream that last used it; its next user's stream waits on that event (no device-wide
+// synchronisation). At most ZOLO_POOL_CAP_GB (default 16) stay cached per device: larger frees go
+// back to the driver, and zolo_pool_trim / zolo_ctx_destroy of the last context return the rest.
+struct Cached {
+  void* p;
+  cudaEvent_t done;
+};
 struct DevPool {
   std::mutex mu;
-  std::map<int, std::multimap<size_t, void*>> cache;
+  std::map<int, std::multimap<size_t, Cached>> cache;
   std::map<int, size_t> cached;
+  std::map<int, int> live_ctx;  // contexts per device
 };
 DevPool& dev_pool() {
   static DevPool* pool = new DevPool;  // never destroyed: blocks live until process exit
   return *pool;
+}
+size_t pool_cap() {
+  static const size_t cap = [] {
+    const char* v = std::getenv("ZOLO_POOL_CAP_GB");
+    return static_cast<size_t>((v && *v ? std::atof(v) : 16.0) * double(size_t(1) << 30));
+  }();
+  return cap;
 }
 size_t pool_cached_bytes() {
   int dev = 0;
@@ -80,12 +94,17 @@ size_t pool_cached_bytes() {
 void pool_trim(int dev) {
   DevPool& P = dev_pool();
   std::lock_guard<std::mutex> lock(P.mu);
-  for (auto& kv : P.cache[dev]) cudaFree(kv.second);
+  for (auto& kv : P.cache[dev]) {
+    cudaEventSynchronize(kv.second.done);
+    cudaEventDestroy(kv.second.done);
+    cudaFree(kv.second.p);
+  }
   P.cache[dev].clear();
   P.cached[dev] = 0;
 }
-// returns the block and its size (>= b), or nullptr
-void* pool_alloc(size_t b, size_t* got) {
+// returns the block and its size (>= b), or nullptr; `st` (may be null = legacy stream) is where
+// the block will be used next: it waits for the block's previous user
+void* pool_alloc(size_t b, size_t* got, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   DevPool& P = dev_pool();
@@ -94,11 +113,16 @@ void* pool_alloc(size_t b, size_t* got) {
     auto& m = P.cache[dev];
     auto it = m.lower_bound(b);
     if (it != m.end() && it->first <= 2 * b + (size_t(1) << 20)) {
-      void* p = it->second;
+      Cached c = it->second;
       *got = it->first;
       P.cached[dev] -= it->first;
       m.erase(it);
-      return p;
+      if (st)
+        cudaStreamWaitEvent(st, c.done, 0);
+      else
+        cudaEventSynchronize(c.done);
+      cudaEventDestroy(c.done);
+      return c.p;
     }
   }
   void* p = nullptr;
@@ -110,35 +134,59 @@ void* pool_alloc(size_t b, size_t* got) {
   *got = b;
   return p;
 }
-void pool_free(void* p, size_t b) {
+// `st`: the last stream that used the block (null: synchronise the device, the conservative default)
+void pool_free(void* p, size_t b, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceSynchronize();
   DevPool& P = dev_pool();
-  std::lock_guard<std::mutex> lock(P.mu);
-  P.cache[dev].emplace(b, p);
-  P.cached[dev] += b;
+  cudaEvent_t ev = nullptr;
+  bool keep = false;
+  {
+    std::lock_guard<std::mutex> lock(P.mu);
+    keep = P.cached[dev] + b <= pool_cap();
+    if (keep) P.cached[dev] += b;  // reserve the room
+  }
+  if (keep && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventRecord(ev, st) == cudaSuccess) {
+    if (!st) cudaEventSynchronize(ev);  // legacy stream: unknown users, wait for the device
+    std::lock_guard<std::mutex> lock(P.mu);
+    P.cache[dev].emplace(b, Cached{p, ev});
+    return;
+  }
+  if (ev) cudaEventDestroy(ev);
+  if (keep) {
+    std::lock_guard<std::mutex> lock(P.mu);
+    P.cached[dev] -= b;
+  }
+  cudaFree(p);  // synchronises the device
 }
+
+// the stream of the context whose entry point is running on this thread (guarded): the stream
+// new device blocks are bound to
+thread_local cudaStream_t tls_stream = nullptr;
 
 struct DevMem {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t st = nullptr;  // the stream this block is used on (its context's)
   DevMem() = default;
   DevMem(const DevMem&) = delete;
   DevMem& operator=(const DevMem&) = delete;
   ~DevMem() { release(); }
   void release() {
-    if (p) pool_free(p, bytes);
+    if (p) pool_free(p, bytes, st);
     p = nullptr;
     bytes = 0;
   }
-  // grow-only; returns true when (re)allocated
+  // grow-only; returns true when (re)allocated. Blocks of a context live on its stream
+  // (bind): every kernel that touches them runs there.
   bool ensure(size_t b) {
     if (b <= bytes && p) return false;
     release();
     if (b == 0) b = 16;
+    st = tls_stream;
     size_t got = 0;
-    p = pool_alloc(b, &got);
+    p = pool_alloc(b, &got, st);
     if (!p) {
       cudaError_t e = cudaGetLastError();
       throw ZoloError(ZOLO_ERR_CUDA, "cudaMalloc(" + std::to_string(b) + " B): " + cudaGetErrorString(e));
@@ -211,8 +259,9 @@ void upload(DevMem& m, const std::vector<T>& v, cudaStream_t st) {
 }  // namespace
 
 namespace zolo {
-void* device_alloc(size_t bytes, size_t* got) { return pool_alloc(bytes, got); }
-void device_free(void* p, size_t bytes) { pool_free(p, bytes); }
+cudaStream_t ctx_stream(const zolo_ctx* c);
+void* device_alloc(size_t bytes, size_t* got, cudaStream_t st) { return pool_alloc(bytes, got, st); }
+void device_free(void* p, size_t bytes, cudaStream_t st) { pool_free(p, bytes, st); }
 }  // namespace zolo
 
 struct zolo_ctx {
@@ -240,7 +289,7 @@ struct zolo_ctx {
   // ordering + device pencil in the factor ordering
   std::vector<int64_t> perm;
   bool have_perm = false;
-  BandGeom geom;
+  DevGeom geom;
   DevMem perm_d, arp_d, aci_d, av_d, brp_d, bci_d, bv_d, bvc_d;
   // BSR copies of A and B in the device ordering (zolo_set_block_size): atoms of `bsr` rows
   int64_t bsr = 1, bsr_na = 0;
@@ -258,32 +307,26 @@ struct zolo_ctx {
   int64_t ncap = 0;  // columns the workspace is sized for
   DevMem vin_orig, vin, vout, w, bbuf, chains_fwd, chains_bwd, flags, counter;
   std::vector<std::unique_ptr<DevMem>> xbuf, cbuf;
-  DevMem dl_d, trace_buf;
+  // residual-correction refinement of the shifted solves (zolo_set_refinement): per chain the
+  // residual / correction block, the in-place sweep chains over it and the chain's shift
+  int refine = 0;
+  std::vector<std::unique_ptr<DevMem>> rbuf;
+  DevMem chains_fwd_ref, chains_bwd_ref, chain_sigma;
+  DevMem trace_buf;
   DevMem host_in, host_out;  // staging of the host-buffer entry points
-  int64_t env_tiles = 0;
   bool trace_done = false;
 
-  // block-sparse (nested dissection) factor path
+  // block-sparse factors (nested dissection, or the reference's RCM order)
   int order_mode = ZOLO_ORDER_ND;
   int64_t nd_leaf = 192;
-  bool sparse = false;
   SpGeom sgeom;
-  std::vector<int> sp_col_cnt;
   int64_t critical_path = 0;
-  int sel_s0 = 0, sel_K = 0;  // selectively inverted trailing block [sel_s0, sel_s0 + sel_K) (host.hpp DT_*)
-  int sel_stage = 0;          // its backward input is staged into partial slots [sel_stage, sel_stage + sel_K)
   int iters_seen = 0;         // largest Krylov dimension an apply_filter on this context has needed
   const int* lag_done = nullptr;  // lagged GMRES control: per-column done flags the sweeps may skip on
   int* act_hq[4] = {};   // pinned active lists / done flags, one per lagged-loop slot
   int* done_hq[4] = {};
-  DevMem sp_seltab, sel_mem;
   DevMem sp_row_ptr, sp_row_idx, sp_col_ptr, sp_col_idx, sp_col_tile, sp_tile_row, sp_pad_rows, sp_err;
-  DevMem sp_sched_fwd, sp_sched_bwd, sp_masks, sp_tmap_fwd, sp_tmap_bwd;
-  DevMem sp_tmap_fused;  // claim map of the fused forward + backward launch (dag_fused_launch)
-  DevMem q_fwd[4], q_bwd[4];  // ready-queue structures per direction: cnt0, dptr, didx, init
-  DevMem q_work;              // ready-queue scratch (cnt | q | ctr)
-  int tmap_fused_nch = -1;
-  int tmap_nch = -1;  // chain count the staggered claim maps were built for
+  DevMem sp_sched_fwd, sp_sched_bwd, sp_masks;
   DevMem sp_er, sp_ec, sp_ea, sp_eb;  // scatter lists of the union pattern in the factor ordering
   int64_t sp_nnz = 0;
   int sp_npads = 0;
@@ -341,10 +384,26 @@ namespace {
 
 std::string g_create_err;
 
+// Runs an entry point on the context's device and stream; the caller's current device is
+// restored afterwards (a library call must not move the caller's CUDA state).
+struct DeviceScope {
+  int saved = -1;
+  cudaStream_t saved_stream;
+  DeviceScope(const zolo_ctx* ctx) : saved_stream(tls_stream) {
+    if (ctx && cudaGetDevice(&saved) == cudaSuccess && saved != ctx->device) cudaSetDevice(ctx->device);
+    if (ctx) tls_stream = ctx->st;
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (saved >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != saved) cudaSetDevice(saved);
+    tls_stream = saved_stream;
+  }
+};
+
 template <class F>
 int guarded(zolo_ctx* ctx, F&& f) {
+  DeviceScope scope(ctx);
   try {
-    if (ctx) CK(cudaSetDevice(ctx->device));
     f();
     return ZOLO_OK;
   } catch (const ZoloError& e) {
@@ -533,169 +592,24 @@ void ensure_perm_csr(zolo_ctx& c) {
   upload_device_pencil(c, inv, pos);
 }
 
-// Block-sparse factors under nested dissection (symbolic.cpp) -- or under a
-// caller ordering given as perm -- for every pole.
+// Block-sparse factors for every pole: under nested dissection (symbolic.cpp),
+// under the reference's RCM ordering (ZOLO_ORDER_RCM, band_factor.hpp:203-204:
+// one node, so pivot positions are RCM positions as in the reference's
+// FactorizationError), or under a caller ordering given as perm.
 void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats);
 
 void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats) {
   require(c.have_pencil, "zolo_factorize: no pencil uploaded");
   require(c.have_design, "zolo_factorize: no design installed");
-  if (c.order_mode == ZOLO_ORDER_ND) {
-    do_factorize_sparse(c, perm_in, stats);
+  if (c.order_mode == ZOLO_ORDER_RCM && !perm_in) {
+    Union u = union_pattern(c);
+    std::vector<int64_t> rcm(c.n);
+    rcm_order(c.n, u.rp.data(), u.ci.data(), rcm.data());  // band_factor.hpp:203-204
+    c.sym_ready = false;
+    do_factorize_sparse(c, rcm.data(), stats);
     return;
   }
-  c.sparse = false;
-  c.sym_ready = false;
-  const int64_t n = c.n;
-  Union u = union_pattern(c);
-  c.perm.resize(n);
-  if (perm_in) {
-    std::vector<char> seen(n, 0);
-    for (int64_t i = 0; i < n; ++i) {
-      require(perm_in[i] >= 0 && perm_in[i] < n && !seen[perm_in[i]], "zolo_factorize: invalid permutation");
-      seen[perm_in[i]] = 1;
-      c.perm[i] = perm_in[i];
-    }
-  } else {
-    rcm_order(n, u.rp.data(), u.ci.data(), c.perm.data());  // band_factor.hpp:203-204
-  }
-  std::vector<int> pos(n);
-  for (int64_t k = 0; k < n; ++k) pos[c.perm[k]] = static_cast<int>(k);
-  const int64_t bw = bandwidth_under(n, u.rp.data(), u.ci.data(), c.perm.data());
-
-  BandGeom g;
-  g.n = n;
-  g.nbk = static_cast<int>((n + TILE - 1) / TILE);
-  g.npad = static_cast<int64_t>(g.nbk) * TILE;
-  g.bw = bw;
-  // envelope per block row: dl[i] = i - first nonzero block column (no fill
-  // outside the envelope under unpivoted elimination)
-  {
-    std::vector<int> first(g.npad);
-    for (int64_t t = 0; t < g.npad; ++t) first[t] = static_cast<int>(t);
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t k = u.rp[i]; k < u.rp[i + 1]; ++k) first[pos[i]] = std::min(first[pos[i]], pos[u.ci[k]]);
-    std::vector<int> dl(g.nbk);
-    int jmax = 0;
-    for (int b = 0; b < g.nbk; ++b) {
-      int f = first[static_cast<int64_t>(b) * TILE];
-      for (int q = 1; q < TILE; ++q) f = std::min(f, first[static_cast<int64_t>(b) * TILE + q]);
-      dl[b] = b - f / TILE;
-      jmax = std::max(jmax, dl[b]);
-    }
-    g.J = jmax;
-    upload(c.dl_d, dl, c.st);
-    g.dl = c.dl_d.as<int>();
-    c.env_tiles = 0;
-    for (int b = 0; b < g.nbk; ++b) c.env_tiles += dl[b];
-  }
-  c.geom = g;
-
-  // permuted union entries for the scatter
-  const int64_t nnz = static_cast<int64_t>(u.ci.size());
-  std::vector<int> er(nnz), ec(nnz);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t k = u.rp[i]; k < u.rp[i + 1]; ++k) {
-      er[k] = pos[i];
-      ec[k] = pos[u.ci[k]];
-    }
-  DevMem er_d, ec_d, ea_d, eb_d;
-  upload(er_d, er, c.st);
-  upload(ec_d, ec, c.st);
-  upload(ea_d, u.av, c.st);
-  upload(eb_d, u.bv, c.st);
-
-  // device pencil in the factor ordering (SpMM with A, B)
-  {
-    std::vector<int64_t> inv(g.npad, -1);
-    for (int64_t t = 0; t < n; ++t) inv[t] = c.perm[t];
-    upload_device_pencil(c, inv, pos);
-  }
-
-  // tiles for the context's poles
-  const int r = c.nloc();
-  const size_t per_array = g.tiles_per_array() * TT;
-  const size_t per_diag = static_cast<size_t>(g.nbk) * TT;
-  const size_t per_pole = 2 * per_array + 2 * per_diag;  // complex entries
-  size_t free_b = 0, total_b = 0;
-  CK(cudaMemGetInfo(&free_b, &total_b));
-  const size_t need = per_pole * r * sizeof(cd);
-  c.tiles_mem.release();
-  free_b += pool_cached_bytes();  // cached blocks are reusable
-  if (need + (size_t(1) << 30) > free_b)
-    throw ZoloError(ZOLO_ERR_DOMAIN, "zolo_factorize: band factors need " + std::to_string(need >> 20) +
-                                         " MiB, device has " + std::to_string(free_b >> 20) + " MiB free");
-  c.tiles_mem.ensure(need);
-  c.rownorm_mem.ensure(sizeof(double) * g.npad * r);
-  c.fstate_mem.ensure(sizeof(unsigned long long) * 2 * r);
-  c.tiles.assign(r, FactorTiles());
-  cd* base = c.tiles_mem.as<cd>();
-  for (int j = 0; j < r; ++j) {
-    cd* p = base + per_pole * j;
-    c.tiles[j].Lt = p;
-    c.tiles[j].Ut = p + per_array;
-    c.tiles[j].DinvL = p + 2 * per_array;
-    c.tiles[j].DinvU = p + 2 * per_array + per_diag;
-  }
-  // fail index (int, init -1) and min ratio bits (init +inf)
-  std::vector<unsigned long long> fs(2 * r);
-  const double inf = std::numeric_limits<double>::infinity();
-  unsigned long long infbits;
-  std::memcpy(&infbits, &inf, 8);
-  for (int j = 0; j < r; ++j) {
-    fs[2 * j] = 0xffffffffffffffffull;  // int -1 in the low word
-    fs[2 * j + 1] = infbits;
-  }
-  CK(cudaMemcpyAsync(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice, c.st));
-  CK(cudaStreamSynchronize(c.st));
-
-  while (static_cast<int>(c.pole_streams.size()) < r) {
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    c.pole_streams.push_back(s);
-  }
-  CK(cudaEventRecord(c.ev0, c.st));
-  for (int j = 0; j < r; ++j) CK(cudaStreamWaitEvent(c.pole_streams[j], c.ev0, 0));
-  const double* poles = c.design.data() + ZOLO_DESIGN_HEAD;
-  for (int j = 0; j < r; ++j) {
-    cudaStream_t ps = c.pole_streams[j];
-    double* rn = c.rownorm_mem.as<double>() + g.npad * j;
-    factor_scatter(ps, g, c.tiles[j], nnz, er_d.as<int>(), ec_d.as<int>(), ea_d.as<double>(), eb_d.as<double>(),
-                   c.cx, poles[2 * c.own[j]], poles[2 * c.own[j] + 1], rn);
-    FactorDevState ds;
-    ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
-    ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
-    factor_run(ps, g, c.tiles[j], rn, ds, c.cx);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(c.ev2, ps));
-    CK(cudaStreamWaitEvent(c.st, c.ev2, 0));
-  }
-  CK(cudaEventRecord(c.ev1, c.st));
-  CK(cudaStreamSynchronize(c.st));
-  for (int j = 0; j < r; ++j) CK(cudaStreamSynchronize(c.pole_streams[j]));
-  float ms = 0;
-  CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
-  c.last_ms[1] = ms;
-  CK(cudaMemcpyAsync(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost, c.st));
-  CK(cudaStreamSynchronize(c.st));
-  int fail_any = -1;
-  for (int j = 0; j < r; ++j) {
-    const int fi = static_cast<int>(static_cast<uint32_t>(fs[2 * j] & 0xffffffffull));
-    double mr;
-    std::memcpy(&mr, &fs[2 * j + 1], 8);
-    if (stats) {
-      stats[j].bandwidth = bw;
-      stats[j].stored_entries = static_cast<int64_t>(per_pole);
-      stats[j].min_pivot_ratio = mr;
-      stats[j].pivot_index = fi;
-    }
-    if (fi >= 0 && fail_any < 0) fail_any = fi;
-  }
-  c.factored = fail_any < 0;
-  c.ncap = 0;  // chains must be rebuilt against the new factors
-  if (fail_any >= 0)
-    throw ZoloError(ZOLO_ERR_FACTORIZATION,
-                    "factorize: pivot " + std::to_string(fail_any) + " below threshold");
+  do_factorize_sparse(c, perm_in, stats);
 }
 
 // Ordering + block symbolic analysis + sweep schedules + the device pencil and
@@ -769,13 +683,10 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     if (bs.inv[t] >= 0) c.perm[q++] = bs.inv[t];
   c.critical_path = bs.critical_path;
 
-  // geometry (the band fields that the shared code reads: n, npad, nbk)
-  BandGeom g;
+  DevGeom g;
   g.n = n;
   g.npad = bs.npad;
   g.nbk = nb;
-  g.J = 0;
-  g.bw = -1;
   c.geom = g;
 
   auto to32 = [](const std::vector<int64_t>& v) { return std::vector<int>(v.begin(), v.end()); };
@@ -789,11 +700,9 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   upload(c.sp_col_tile, to32(bs.col_tile), c.st);
   upload(c.sp_tile_row, tile_row, c.st);
   int max_deps = 0;
-  c.sp_col_cnt.assign(nb, 0);
   for (int i = 0; i < nb; ++i) {
-    c.sp_col_cnt[i] = static_cast<int>(bs.col_ptr[i + 1] - bs.col_ptr[i]);
     max_deps = std::max(max_deps, static_cast<int>(bs.row_ptr[i + 1] - bs.row_ptr[i]));
-    max_deps = std::max(max_deps, c.sp_col_cnt[i]);
+    max_deps = std::max(max_deps, static_cast<int>(bs.col_ptr[i + 1] - bs.col_ptr[i]));
   }
   SpGeom s;
   s.n = n;
@@ -812,24 +721,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     static const int near = std::min(std::max(env_int("ZOLO_DAG_NEAR", 4), 0), DAG_REC_DEPS - 1),
                      chunk = std::min(std::max(env_int("ZOLO_DAG_CHUNK", 16), 1), DAG_REC_DEPS - near),
                      order = env_int("ZOLO_DAG_ORDER", 3);
-    static const bool chain = env_int("ZOLO_DAG_CHAIN", 0) != 0;  // chained partials: measured slower
     // self-contained task records: header + the (j, tile id) pairs in processing order
-    // selective inversion of the trailing dense block: only the v2 sweep kernel reads its task kinds
-    static const int sel_kmax = env_int("ZOLO_SELINV", 0);  // off: +1% on cfg2, and the explicit inverse lifts cfg3's residual floor 9e-9 -> 2e-8
-    const bool sel_ok = sel_kmax >= 2 && env_int("ZOLO_DAG_V2", 1) != 0 && (c.cx ? 2 : 1) * std::max(c.r, 1) <= 32;
-    const int s0 = sel_ok ? trailing_dense_start(bs, sel_kmax) : nb;
-    c.sel_s0 = s0;
-    c.sel_K = nb - s0 >= 2 ? nb - s0 : 0;
-    if (c.sel_K) {
-      const int K = c.sel_K;
-      std::vector<int> tab(static_cast<size_t>(K) * K, -1);
-      for (int i = s0; i < nb; ++i)
-        for (int64_t e = bs.row_ptr[i]; e < bs.row_ptr[i + 1]; ++e)
-          if (bs.row_idx[e] >= s0) tab[static_cast<size_t>(i - s0) * K + (bs.row_idx[e] - s0)] = static_cast<int>(e);
-      upload(c.sp_seltab, tab, c.st);
-    }
-    std::vector<int> cslot;
-    int stage_base = 0;  // first slot of the staged backward input of the inverted block
     auto records = [&](const std::vector<DagTask>& ts, bool fwd) {
       std::vector<int> rec(ts.size() * DAG_REC, 0);
       for (size_t t = 0; t < ts.size(); ++t) {
@@ -839,84 +731,23 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
         const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
         const int nd = k.qb - k.qa;
         require(nd <= DAG_REC_DEPS, "zolo_factorize: DAG task record overflow");
-        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out, r[5] = k.flags;
-        if (!fwd && k.out < 0 && ndall == 0 && !(k.flags & (DT_SRCDEP | DT_SLOTDEP))) r[5] |= DT_FWDWAIT;
+        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out;
         for (int q = 0; q < nd; ++q) {
-          int j, tid;
-          if (k.flags & DT_SRCDEP) {  // W(i, kk), kk = nb-1 .. i: input block kk, staged in slot base + kk - s0
-            const int kk = nb - 1 - (k.qa + q);
-            j = stage_base + (kk - s0);
-            tid = (kk - s0) * (kk - s0 + 1) / 2 + (k.i - s0);
-          } else if (k.flags & DT_SLOTDEP) {  // M(i, kk), kk in [s0, i): c_kk from its slot
-            const int kk = static_cast<int>(bs.row_idx[e0 + k.qa + q]);
-            j = cslot[kk];
-            tid = (k.i - s0) * (k.i - s0 - 1) / 2 + (kk - s0);
-          } else {
-            const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
-            j = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
-            tid = static_cast<int>(fwd ? e : bs.col_tile[e]);
-          }
-          r[DAG_REC_HDR + 2 * q] = j;
-          r[DAG_REC_HDR + 2 * q + 1] = tid;
+          const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
+          r[DAG_REC_HDR + 2 * q] = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
+          r[DAG_REC_HDR + 2 * q + 1] = static_cast<int>(fwd ? e : bs.col_tile[e]);
         }
       }
       return rec;
     };
     std::vector<DagTask> tf, tb;
-    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf, chain, s0, &cslot);
-    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb, chain, s0);
-    stage_base = sb;
-    c.sel_stage = sb;
+    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf);
+    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb);
     upload(c.sp_sched_fwd, records(tf, true), c.st);
     upload(c.sp_sched_bwd, records(tb, false), c.st);
     c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), static_cast<int>(tf.size()), sf};
-    c.tmap_nch = -1;
-    c.tmap_fused_nch = -1;
-    c.sp_tmap_fwd.release();
-    c.sp_tmap_bwd.release();
-    c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb + c.sel_K};
-    // ready-queue structures (ZOLO_DAG_QUEUE): a record's dependencies are the row tasks of its
-    // dependency rows and the chunk tasks of its partial slots (exactly what the static schedule
-    // waits on); the selectively inverted block's task kinds are not covered
-    auto build_queue = [&](const std::vector<DagTask>& ts, bool fwd, DevMem* q, DagSched& sc) {
-      if (c.sel_K) return;
-      const int nt = static_cast<int>(ts.size());
-      std::vector<int> row_task(nb, -1), slot_task(std::max(sf, sb) + 1, -1), cnt0(nt, 0), dptr(nt + 1, 0),
-          didx, init;
-      for (int t = 0; t < nt; ++t) (ts[t].out >= 0 ? slot_task[ts[t].out] : row_task[ts[t].i]) = t;
-      std::vector<std::vector<int>> deps(nt);
-      for (int t = 0; t < nt; ++t) {
-        const DagTask& k = ts[t];
-        const int64_t e0 = fwd ? bs.row_ptr[k.i] : bs.col_ptr[k.i];
-        const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
-        for (int qd = k.qa; qd < k.qb; ++qd) {
-          const int64_t e = fwd ? e0 + qd : e0 + ndall - 1 - qd;
-          deps[t].push_back(row_task[fwd ? bs.row_idx[e] : bs.col_idx[e]]);
-        }
-        for (int p = k.pa; p < k.pa + k.pc; ++p) deps[t].push_back(slot_task[p]);
-        cnt0[t] = static_cast<int>(deps[t].size());
-        if (!cnt0[t]) init.push_back(t);
-      }
-      std::vector<std::vector<int>> users(nt);
-      for (int t = 0; t < nt; ++t)
-        for (int d : deps[t]) users[d].push_back(t);
-      for (int t = 0; t < nt; ++t) {
-        didx.insert(didx.end(), users[t].begin(), users[t].end());
-        dptr[t + 1] = static_cast<int>(didx.size());
-      }
-      upload(q[0], cnt0, c.st);
-      upload(q[1], dptr, c.st);
-      upload(q[2], didx, c.st);
-      upload(q[3], init, c.st);
-      sc.q_cnt0 = q[0].as<int>();
-      sc.q_dptr = q[1].as<int>();
-      sc.q_didx = q[2].as<int>();
-      sc.q_init = q[3].as<int>();
-      sc.q_ninit = static_cast<int>(init.size());
-    };
-    build_queue(tf, true, c.q_fwd, c.sched_fwd);
-    build_queue(tb, false, c.q_bwd, c.sched_bwd);
-    c.sp_nslots = std::max(sf, sb + c.sel_K);
+    c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb};
+    c.sp_nslots = std::max(sf, sb);
   }
   clk.mark("sweep schedules");
 
@@ -985,19 +816,6 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     tiles[j].Lt = p + 3 * per_diag;
     tiles[j].Ut = p + 3 * per_diag + per_off;
   }
-  const int K = mstore ? c.sel_K : 0;
-  const size_t sel_strict = static_cast<size_t>(K) * (K > 0 ? K - 1 : 0) / 2, sel_diag = static_cast<size_t>(K) * (K + 1) / 2;
-  const size_t sel_per = (2 * sel_strict + 2 * sel_diag) * TT;
-  if (K) {
-    c.sel_mem.ensure(sizeof(cd) * sel_per * r);
-    for (int j = 0; j < r; ++j) {
-      cd* q = c.sel_mem.as<cd>() + sel_per * j;
-      tiles[j].ML = q;
-      tiles[j].MU = q + sel_strict * TT;
-      tiles[j].WU = q + 2 * sel_strict * TT;
-      tiles[j].WX = c.cx ? q + (2 * sel_strict + sel_diag) * TT : nullptr;
-    }
-  }
   if (mstore) {
     const size_t mper = 2 * static_cast<size_t>(nb) + 2 * static_cast<size_t>(ntiles);
     mstore->ensure(sizeof(uint2) * mper * r);
@@ -1024,7 +842,6 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     c.pole_streams.push_back(st);
   }
-  static const int levels = env_int("ZOLO_FACTOR_LEVELS", 1);
   FactorPlanDev pd;
   pd.lvl_ptr = &c.fplan.lvl_ptr;
   pd.pan_ptr = &c.fplan.pan_ptr;
@@ -1033,7 +850,6 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   pd.pan = c.fp_pan.as<int>();
   pd.tgt = c.fp_tgt.as<int>();
   pd.con = c.fp_con.as<int>();
-  pd.simt = levels == 2;
   CK(cudaStreamSynchronize(c.st));
   CK(cudaEventRecord(c.ev0, c.st));
   for (int j = 0; j < r; ++j) CK(cudaStreamWaitEvent(c.pole_streams[j], c.ev0, 0));
@@ -1047,19 +863,10 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     FactorDevState ds;
     ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
     ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
-    sp_factor(c.pole_streams[j], c.sgeom, c.sp_col_cnt, f, c.sp_nnz, c.sp_er.as<int>(), c.sp_ec.as<int>(),
-              c.sp_ea.as<double>(), c.sp_eb.as<double>(), c.cx, sig[j].real(), sig[j].imag(),
-              c.rownorm_mem.as<double>() + c.sgeom.npad * j, c.sp_pad_rows.as<int>(), c.sp_npads, ds,
-              c.sp_err.as<int>(), levels ? &pd : nullptr);
+    sp_factor(c.pole_streams[j], c.sgeom, f, c.sp_nnz, c.sp_er.as<int>(), c.sp_ec.as<int>(), c.sp_ea.as<double>(),
+              c.sp_eb.as<double>(), c.cx, sig[j].real(), sig[j].imag(), c.rownorm_mem.as<double>() + c.sgeom.npad * j,
+              c.sp_pad_rows.as<int>(), c.sp_npads, ds, c.sp_err.as<int>(), pd);
     if (mstore) {  // sweep factors: occupancy masks, then the swizzled sweep layout
-      if (K) {
-        selinv(c.pole_streams[j], K, c.sel_s0, c.sp_seltab.as<int>(), f, tiles[j].ML, tiles[j].MU, tiles[j].WU,
-               tiles[j].WX);
-        swizzle_tiles(c.pole_streams[j], tiles[j].ML, static_cast<int64_t>(sel_strict));
-        swizzle_tiles(c.pole_streams[j], tiles[j].MU, static_cast<int64_t>(sel_strict));
-        swizzle_tiles(c.pole_streams[j], tiles[j].WU, static_cast<int64_t>(sel_diag));
-        if (tiles[j].WX) swizzle_tiles(c.pole_streams[j], tiles[j].WX, static_cast<int64_t>(sel_diag));
-      }
       tile_masks(c.pole_streams[j], tiles[j].DinvL, nb, tiles[j].mDL);
       tile_masks(c.pole_streams[j], tiles[j].DinvU, nb, tiles[j].mDU);
       tile_masks(c.pole_streams[j], tiles[j].Lt, ntiles, tiles[j].mLt);
@@ -1113,7 +920,6 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
     }
     if (fail[j] >= 0 && fail_any < 0) fail_any = fail[j];
   }
-  c.sparse = true;
   c.factored = fail_any < 0;
   c.ncap = 0;
   if (fail_any >= 0)
@@ -1147,8 +953,8 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   const int nch = c.nchains();
   while (static_cast<int>(c.xbuf.size()) < nch) c.xbuf.emplace_back(new DevMem());
   while (static_cast<int>(c.cbuf.size()) < nch) c.cbuf.emplace_back(new DevMem());
-  // cbuf: band helpers' partial solutions (ld rows), or the DAG chunk partials (32 x nslots rows)
-  const int64_t crows = c.sparse ? static_cast<int64_t>(TILE) * std::max(c.sp_nslots, 1) : ld;
+  // cbuf: the DAG chunk partials (32 x nslots rows)
+  const int64_t crows = static_cast<int64_t>(TILE) * std::max(c.sp_nslots, 1);
   for (int i = 0; i < nch; ++i) {
     c.xbuf[i]->ensure(sizeof(cd) * ld * nc);
     c.cbuf[i]->ensure(sizeof(cd) * crows * nc);
@@ -1165,26 +971,44 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
       // solve:   y = DinvL b - L~ y ;  x = DinvU y - U~ x
       // adjoint: z = b - U~^H z (z_i = U_ii^H y_i) ; w = DinvU^H z - L~^H w (w_i = L_ii^H x_i),
       //          then x_i = DinvL_i^H w_i (blockdiag post-pass)
-      // selectively inverted trailing block: (I + L~)^-1, (I + U~^H)^-1 = MU^H forward; U_SS^-1 and
-      // (DinvU ML)^H backward (host.hpp DT_*)
-      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0, t.ML};
-      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0, t.WU};
-      fwd[2 * p + 1] = Chain{t.Ut, nullptr, t.mUt, nullptr, b, xa, cba, FWD_UH, 0, t.MU};
-      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, t.mLt, t.mDU, xa, xa, cba, BWD_LH, 0, t.WX};
+      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
+      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
+      fwd[2 * p + 1] = Chain{t.Ut, nullptr, t.mUt, nullptr, b, xa, cba, FWD_UH, 0};
+      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, t.mLt, t.mDU, xa, xa, cba, BWD_LH, 0};
     } else {
       cd* x = c.xbuf[p]->as<cd>();
       cd* cb = c.cbuf[p]->as<cd>();
-      fwd[p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0, t.ML};
-      bwd[p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0, t.WU};
+      fwd[p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
+      bwd[p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
     }
   }
   upload(c.chains_fwd, fwd, c.st);
   upload(c.chains_bwd, bwd, c.st);
+  if (c.refine) {  // refinement sweeps: same factors, in place over the residual blocks
+    while (static_cast<int>(c.rbuf.size()) < nch) c.rbuf.emplace_back(new DevMem());
+    std::vector<cd> sig(nch);
+    const double* poles = c.design.data() + ZOLO_DESIGN_HEAD;
+    for (int ch = 0; ch < nch; ++ch) {
+      c.rbuf[ch]->ensure(sizeof(cd) * ld * nc);
+      cd* rb = c.rbuf[ch]->as<cd>();
+      fwd[ch].src = rb;
+      fwd[ch].dst = rb;
+      bwd[ch].src = rb;
+      bwd[ch].dst = rb;
+      // chain 2p solves K_p = A - sigma_p B; chain 2p + 1 (complex pencils) K_p^H = A - conj(sigma_p) B
+      const int p = c.cx ? ch / 2 : ch;
+      const double im = poles[2 * c.own[p] + 1];
+      sig[ch] = mk(poles[2 * c.own[p]], (c.cx && (ch & 1)) ? -im : im);
+    }
+    upload(c.chains_fwd_ref, fwd, c.st);
+    upload(c.chains_bwd_ref, bwd, c.st);
+    upload(c.chain_sigma, sig, c.st);
+  }
   const int64_t ngroups = (nc + CG - 1) / CG;
-  // [owner progress: nch x ngroups uint64 | block flags: nch x ngroups x nbk int |
+  // [(reserved) nch x ngroups uint64 | block flags: nch x ngroups x nbk int |
   //  DAG chunk flags: nch x dag_groups x nslots int]; all epoch-stamped, zeroed with the epoch
   const int64_t nbflags = static_cast<int64_t>(nch) * ngroups * c.geom.nbk;
-  const int64_t nflags = nbflags + (c.sparse ? static_cast<int64_t>(nch) * dag_groups(nc) * c.sp_nslots : 0);
+  const int64_t nflags = nbflags + static_cast<int64_t>(nch) * dag_groups(nc) * c.sp_nslots;
   if (nflags > c.flags_cap || static_cast<int64_t>(nch) * ngroups > c.prog_cap) {
     c.prog_cap = static_cast<int64_t>(nch) * ngroups;
     const size_t bytes = sizeof(unsigned long long) * c.prog_cap + sizeof(int) * nflags;
@@ -1234,110 +1058,48 @@ void combine_g(zolo_ctx& c, const void* vsrc, const int* act, int na, std::vecto
 
 // DAG sweeps (forward, backward, and the adjoint post-pass) of the chains
 // [first, first + nsub) on bbuf's first na (compacted) columns -> their xbuf.
-// Claim order with the chains staggered by `stagger` x (records / chains)
-// positions: each chain keeps its topological order, and at any time only a
-// few chains are in their narrow (top-separator) phase.
-void build_tmap(zolo_ctx& c, int nch) {
-  static const double stagger = [] {
-    const char* v = std::getenv("ZOLO_DAG_STAGGER");
-    return v ? std::atof(v) : 0.0;
-  }();
-  c.tmap_nch = nch;
-  if (stagger <= 0.0 || nch < 2) return;
-  for (int dir = 0; dir < 2; ++dir) {
-    const int nt = dir == 0 ? c.sched_fwd.ntask : c.sched_bwd.ntask;
-    const double delta = stagger * nt / nch;
-    std::vector<std::pair<double, int>> key;
-    key.reserve(static_cast<size_t>(nt) * nch);
-    for (int ci = 0; ci < nch; ++ci)
-      for (int p = 0; p < nt; ++p) key.emplace_back(p + ci * delta, p * nch + ci);
-    std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    std::vector<int> map(key.size());
-    for (size_t k = 0; k < key.size(); ++k) map[k] = key[k].second;
-    upload(dir == 0 ? c.sp_tmap_fwd : c.sp_tmap_bwd, map, c.st);
-  }
-}
-
-// Claim map of the fused launch: every (direction, record, chain) keyed by its sweep progress
-// (forward in [0, 1), backward in [1, 2)) plus a per-chain stagger (ZOLO_FUSE_STAGGER, odd chains
-// shifted), stable-sorted; topological within each chain, chains are independent.
-void build_fused_tmap(zolo_ctx& c, int nch) {
-  static const double stagger = [] {
-    const char* v = std::getenv("ZOLO_FUSE_STAGGER");
-    return v ? std::atof(v) : 0.0;
-  }();
-  const int ntf = c.sched_fwd.ntask, ntb = c.sched_bwd.ntask;
-  std::vector<std::pair<double, int>> key;
-  key.reserve(static_cast<size_t>(ntf + ntb) * nch);
-  for (int dir = 0; dir < 2; ++dir) {
-    const int nt = dir ? ntb : ntf;
-    for (int p = 0; p < nt; ++p)
-      for (int ci = 0; ci < nch; ++ci)
-        key.emplace_back(dir + static_cast<double>(p) / nt + stagger * (ci & 1), (dir << 30) | (p * nch + ci));
-  }
-  std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-  std::vector<int> map(key.size());
-  for (size_t k = 0; k < key.size(); ++k) map[k] = key[k].second;
-  upload(c.sp_tmap_fused, map, c.st);
-  c.tmap_fused_nch = nch;
-}
-
-void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* trace = nullptr) {
+// refinement = true: the in-place sweeps over the chains' residual blocks (rbuf).
+void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* trace = nullptr,
+                  bool refinement = false) {
   const int64_t ld = c.geom.npad;
   unsigned long long* fx = c.flags.as<unsigned long long>();
   int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
   int* cf = fc + c.cflags_off;
-  if (c.tmap_nch != c.nchains()) build_tmap(c, c.nchains());
-  const bool full = first == 0 && nsub == c.nchains() && c.sp_tmap_fwd.p && c.tmap_nch == nsub;
-  const bool presw = c.tiles[0].swz;
-  static const bool fuse = env_int("ZOLO_DAG_FUSED", 0) != 0 && env_int("ZOLO_DAG_V2", 1) != 0;  // measured equal to two launches; staggered chains slower
-  if (fuse && !trace && c.sel_K == 0 && presw && nsub <= 32) {
-    // one launch for both sweep directions (dag_fused_launch)
-    if (c.tmap_fused_nch != nsub) build_fused_tmap(c, nsub);
-    const int g = dag_fused_launch(c.st, c.sgeom, c.sched_fwd, c.sched_bwd, c.chains_fwd.as<Chain>() + first,
-                                   c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf, c.epoch + 1,
-                                   c.counter.as<int>(), c.num_sms, c.sp_tmap_fused.as<int>());
-    c.epoch += 2;
-    if (g < 0) throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: fused sweep launch failed");
-    if (c.cx)
-      for (int ci = first; ci < first + nsub; ++ci)
-        if (ci & 1)
-          blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true, c.xbuf[ci]->as<cd>(), na, ld,
-                          c.tiles[ci / 2].swz);
-    return;
-  }
-  const bool need_v2 = c.sel_K > 0;  // the selectively inverted block's task kinds exist only in dag2_kernel
-  static const bool queue = env_int("ZOLO_DAG_QUEUE", 0) != 0;
-  DagQueueWork qw;
-  const DagQueueWork* qwp = nullptr;
-  if (queue && c.sched_fwd.q_cnt0 && c.sched_bwd.q_cnt0 && !full) {
-    const int64_t nt = static_cast<int64_t>(std::max(c.sched_fwd.ntask, c.sched_bwd.ntask)) * nsub * dag_groups(na);
-    c.q_work.ensure(sizeof(int) * (2 * nt + 2));
-    qw.cnt = c.q_work.as<int>();
-    qw.q = qw.cnt + nt;
-    qw.ctr = qw.q + nt;
-    qwp = &qw;
-  }
-  const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, c.chains_fwd.as<Chain>() + first, nsub, na, ld, fc, cf,
-                                 ++c.epoch, c.counter.as<int>(), 1, c.num_sms, trace,
-                                 full ? c.sp_tmap_fwd.as<int>() : nullptr, presw, need_v2, qwp, c.act_d.as<int>(),
-                                 c.lag_done);
-  if (c.sel_K)  // the backward sweep runs in place: stage the inverted block's input first
-    dag_stage_inputs(c.st, c.chains_bwd.as<Chain>() + first, nsub, static_cast<int64_t>(c.sel_s0) * TILE,
-                     static_cast<int64_t>(c.sel_K) * TILE, na, ld, static_cast<int64_t>(TILE) * c.sched_bwd.nslots,
-                     static_cast<int64_t>(c.sel_stage) * TILE);
-  const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, c.chains_bwd.as<Chain>() + first, nsub, na, ld, fc, cf,
-                                 ++c.epoch, c.counter.as<int>() + 1, 0, c.num_sms, nullptr,
-                                 full ? c.sp_tmap_bwd.as<int>() : nullptr, presw, need_v2, qwp, c.act_d.as<int>(),
-                                 c.lag_done);
-  if (g1 < 0 || g2 < 0)
-    throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: the selectively inverted schedule needs the v2 sweep kernel "
-                                     "(at most 32 chains, ZOLO_DAG_V2 on)");
+  const Chain* cfw = (refinement ? c.chains_fwd_ref : c.chains_fwd).as<Chain>() + first;
+  const Chain* cbw = (refinement ? c.chains_bwd_ref : c.chains_bwd).as<Chain>() + first;
+  const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, cfw, nsub, na, ld, fc, cf, ++c.epoch,
+                                 c.counter.as<int>(), c.num_sms, trace, c.act_d.as<int>(), c.lag_done);
+  const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, cbw, nsub, na, ld, fc, cf, ++c.epoch,
+                                 c.counter.as<int>(), c.num_sms, nullptr, c.act_d.as<int>(), c.lag_done);
+  if (g1 < 0 || g2 < 0) throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: more than 32 chains in one launch");
   if (c.cx)
     for (int ci = first; ci < first + nsub; ++ci)
       if (ci & 1)
-        blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true, c.xbuf[ci]->as<cd>(), na, ld,
-                        c.tiles[ci / 2].swz);
+        blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true,
+                        (refinement ? c.rbuf[ci] : c.xbuf[ci])->as<cd>(), na, ld);
+}
+
+// Residual-correction refinement of every chain's solution (zolo_set_refinement):
+// r = b - K x (K^H for the adjoint chains) from the pencil in FP64, d = K^-1 r by the same
+// sweeps in place over r, x += d.
+void refine_solves(zolo_ctx& c, int na) {
+  const int64_t ld = c.geom.npad, n = ld;
+  const int nch = c.nchains();
+  std::vector<cd*> xs(nch), rs(nch);
+  for (int i = 0; i < nch; ++i) xs[i] = c.xbuf[i]->as<cd>(), rs[i] = c.rbuf[i]->as<cd>();
+  for (int step = 0; step < c.refine; ++step) {
+    if (c.cx)
+      Krylov<cd>::shifted_residual(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<cd>(),
+                                   c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<cd>(),
+                                   c.bbuf.as<cd>(), xs.data(), rs.data(), c.chain_sigma.as<cd>(), nch, na);
+    else
+      Krylov<double>::shifted_residual(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<double>(),
+                                       c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
+                                       c.bv_d.as<double>(), c.bbuf.as<cd>(), xs.data(), rs.data(),
+                                       c.chain_sigma.as<cd>(), nch, na);
+    sweep_sparse(c, 0, nch, na, nullptr, true);
+    add_corrections(c.st, ld, xs.data(), rs.data(), nch, na);
+  }
 }
 
 // out[:, a] = B v[:, act[a]] (complex, the sweeps' input) over the device rows: BSR kernel when
@@ -1353,7 +1115,7 @@ void device_apply_b(zolo_ctx& c, const void* v, const int* act, int na, cd* out)
       Krylov<double>::bsr_spmm(c.st, c.bsr_na, static_cast<int>(c.bsr), c.bbrp_d.as<int>(), c.bbci_d.as<int>(),
                                c.bbv_d.as<double>(), c.brow0_d.as<int>(), reinterpret_cast<const double*>(v), ld, act,
                                na, nullptr, out);
-    zero_rows(c.st, c.sp_pad_rows.as<int>(), c.sparse ? c.sp_npads : 0, out, ld, na);
+    zero_rows(c.st, c.sp_pad_rows.as<int>(), c.sp_npads, out, ld, na);
     return;
   }
   if (c.cx)
@@ -1392,71 +1154,32 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   for (int i = 0; i < nch; ++i) xs[i] = c.xbuf[i]->as<cd>();
   device_apply_b(c, vsrc, act, na, c.bbuf.as<cd>());
   CK(cudaEventRecord(c.ev2_use ? c.ev2_use : c.ev2, c.st));
-  unsigned long long* fx = c.flags.as<unsigned long long>();
-  int* fc = reinterpret_cast<int*>(fx + c.prog_cap);
-  if (c.sparse) {  // block-sparse factors: DAG-scheduled sweeps
-    // ZOLO_TRACE=<file>: per-task timestamps of the first forward sweep (development aid)
-    static const char* dag_trace = std::getenv("ZOLO_TRACE");
-    unsigned long long* dtr = nullptr;
-    const size_t ntask = static_cast<size_t>(c.sched_fwd.ntask) * nch * dag_groups(na);
-    if (dag_trace && !c.trace_done) {
-      c.trace_buf.ensure(sizeof(unsigned long long) * 6 * ntask);
-      CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 6 * ntask, c.st));
-      dtr = c.trace_buf.as<unsigned long long>();
-    }
-    sweep_sparse(c, 0, nch, na, dtr);
-    if (dtr) {
-      std::vector<unsigned long long> h(6 * ntask);
-      CK(cudaMemcpyAsync(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
-      CK(cudaStreamSynchronize(c.st));
-      if (FILE* fh = std::fopen(dag_trace, "w")) {
-        std::fprintf(fh, "# nb %d chains %d groups %d critical_path %lld schedule %d slots %d\n", c.geom.nbk, nch,
-                     dag_groups(na), static_cast<long long>(c.critical_path), c.sched_fwd.ntask,
-                     c.sched_fwd.nslots);
-        for (size_t q = 0; q < ntask; ++q)
-          std::fprintf(fh, "%llu %llu %llu %llu %llu %llu\n", h[6 * q], h[6 * q + 1], h[6 * q + 2], h[6 * q + 3],
-                       h[6 * q + 4], h[6 * q + 5]);
-        std::fclose(fh);
-      }
-      c.trace_done = true;
-    }
-    CK(cudaEventRecord(c.ev3_use ? c.ev3_use : c.ev3, c.st));
-    CK(cudaGetLastError());
-    combine_g(c, vsrc, act, na, xs, wdst);
-    CK(cudaGetLastError());
-    return 0.0f;
+  // ZOLO_TRACE=<file>: per-task timestamps of the first forward sweep (development aid,
+  // tools/dag2_trace_analyze.py)
+  static const char* dag_trace = std::getenv("ZOLO_TRACE");
+  unsigned long long* dtr = nullptr;
+  const size_t ntask = static_cast<size_t>(c.sched_fwd.ntask) * nch * dag_groups(na);
+  if (dag_trace && !c.trace_done) {
+    c.trace_buf.ensure(sizeof(unsigned long long) * 6 * ntask);
+    CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 6 * ntask, c.st));
+    dtr = c.trace_buf.as<unsigned long long>();
   }
-  // ZOLO_TRACE=<file>: dump per-step timestamps of chain 0 / group 0 of the
-  // first forward sweep (development aid for the pipeline's critical path)
-  static const char* trace_path = std::getenv("ZOLO_TRACE");
-  unsigned long long* tr = nullptr;
-  if (trace_path && !c.trace_done) {
-    c.trace_buf.ensure(sizeof(unsigned long long) * 16 * c.geom.nbk);
-    CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 16 * c.geom.nbk, c.st));
-    tr = c.trace_buf.as<unsigned long long>();
-  }
-  const int g1 = trsm_launch(c.st, c.geom, c.chains_fwd.as<Chain>(), nch, na, ld, fx, fc, ++c.epoch,
-                             c.counter.as<int>(), 1, c.num_sms, tr);
-  if (tr) {
-    std::vector<unsigned long long> h(16 * c.geom.nbk);
-    CK(cudaMemcpyAsync(h.data(), tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
+  sweep_sparse(c, 0, nch, na, dtr);
+  if (c.refine) refine_solves(c, na);
+  if (dtr) {
+    std::vector<unsigned long long> h(6 * ntask);
+    CK(cudaMemcpyAsync(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));
-    if (FILE* f = std::fopen(trace_path, "w")) {
-      for (int s = 0; s < c.geom.nbk; ++s) {
-        for (int q = 0; q < 16; ++q) std::fprintf(f, "%llu%c", h[16 * s + q], q == 15 ? '\n' : ' ');
-      }
-      std::fclose(f);
+    if (FILE* fh = std::fopen(dag_trace, "w")) {
+      std::fprintf(fh, "# nb %d chains %d groups %d critical_path %lld schedule %d slots %d\n", c.geom.nbk, nch,
+                   dag_groups(na), static_cast<long long>(c.critical_path), c.sched_fwd.ntask, c.sched_fwd.nslots);
+      for (size_t q = 0; q < ntask; ++q)
+        std::fprintf(fh, "%llu %llu %llu %llu %llu %llu\n", h[6 * q], h[6 * q + 1], h[6 * q + 2], h[6 * q + 3],
+                     h[6 * q + 4], h[6 * q + 5]);
+      std::fclose(fh);
     }
     c.trace_done = true;
   }
-  const int g2 = trsm_launch(c.st, c.geom, c.chains_bwd.as<Chain>(), nch, na, ld, fx, fc, ++c.epoch,
-                             c.counter.as<int>() + 1, 0, c.num_sms);
-  if (c.cx)
-    for (int p = 0; p < c.nloc(); ++p) blockdiag_apply(c.st, c.geom.nbk, c.tiles[p].DinvL, true, xs[2 * p + 1], na, ld);
-  if (g1 < 0 || g2 < 0)
-    throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: " + std::to_string(nch) + " chains x " +
-                                         std::to_string((na + CG - 1) / CG) +
-                                         " column groups exceed the resident CTA budget");
   CK(cudaEventRecord(c.ev3_use ? c.ev3_use : c.ev3, c.st));
   CK(cudaGetLastError());
   combine_g(c, vsrc, act, na, xs, wdst);
@@ -1699,7 +1422,6 @@ void inner_gmres(zolo_ctx& c, int k, int na) {
 float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   const int64_t ld = c.geom.npad, n = ld;
   const int* act = c.act_d.as<int>();
-  require(c.sparse, "hybrid solve: needs the ND (block-sparse) factors");
   ensure_inner(c, c.ncap, std::max(c.r - 1, 1), c.hy_max);
   if (c.cx)
     Krylov<cd>::apply_b(c.st, n, ld, c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
@@ -1737,7 +1459,10 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
                       zolo_report* rep) {
   require(c.factored, "apply_filter: operator not factorized");
   require(c.shard_size == 1 || c.comm, "apply_filter: a pole-sharded context needs its NCCL communicator");
-  require(gmres_max >= 1 && gmres_max <= 64, "apply_filter: gmres_max must be in [1, 64]");
+  // (the reference has no cap, gmres.hpp:98-101; the device Krylov kernels hold up to
+  // KRYLOV_MAX basis vectors per column, krylov.cuh)
+  require(gmres_max >= 1 && gmres_max <= KRYLOV_MAX,
+          "apply_filter: gmres_max must be in [1, " + std::to_string(KRYLOV_MAX) + "]");
   const int64_t n = c.n, ld = c.geom.npad;
   const int maxit = static_cast<int>(gmres_max);
   const int q = 2 * c.r;
@@ -1997,14 +1722,15 @@ void spmm_dev_impl(zolo_ctx& c, int which, const void* x, void* out, int64_t k) 
   const size_t es = sizeof(S);
   if (which == 1 && c.b_identity) {
     CK(cudaMemcpyAsync(out, x, es * n * k, cudaMemcpyDeviceToDevice, c.st));
-    return;
+  } else {
+    c.tmp1.ensure(es * ld * k);
+    c.tmp2.ensure(es * ld * k);
+    Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(x), n, c.tmp1.as<S>(), ld, k, c.perm_d.as<int>());
+    device_spmm<S>(c, which, c.tmp1.as<S>(), k, c.tmp2.as<S>());
+    Krylov<S>::permute_out(c.st, c.tmp2.as<S>(), ld, reinterpret_cast<S*>(out), n, k, c.perm_d.as<int>());
   }
-  c.tmp1.ensure(es * ld * k);
-  c.tmp2.ensure(es * ld * k);
-  Krylov<S>::permute_in(c.st, reinterpret_cast<const S*>(x), n, c.tmp1.as<S>(), ld, k, c.perm_d.as<int>());
-  device_spmm<S>(c, which, c.tmp1.as<S>(), k, c.tmp2.as<S>());
-  Krylov<S>::permute_out(c.st, c.tmp2.as<S>(), ld, reinterpret_cast<S*>(out), n, k, c.perm_d.as<int>());
   CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(c.st));  // like its siblings: d_out is complete when the call returns
 }
 
 template <class S>
@@ -2045,6 +1771,10 @@ void resid_dev_impl(zolo_ctx& c, const void* ax, const void* bx, int64_t k, cons
 }
 
 }  // namespace
+
+namespace zolo {
+cudaStream_t ctx_stream(const zolo_ctx* c) { return c ? c->st : nullptr; }
+}  // namespace zolo
 
 extern "C" {
 
@@ -2132,7 +1862,7 @@ int zolo_ctx_create(int device, zolo_ctx** out) {
 
 int zolo_ctx_destroy(zolo_ctx* c) {
   if (!c) return ZOLO_OK;
-  cudaSetDevice(c->device);
+  DeviceScope scope(c);  // the context's device; the caller's is restored on return
   if (c->st) cudaStreamSynchronize(c->st);
   for (auto s : c->pole_streams) cudaStreamDestroy(s);
   nccl_close(c->comm);
@@ -2297,6 +2027,7 @@ int zolo_set_solve_mode(zolo_ctx* c, int mode, int pole, double inner_tol, int i
   return guarded(c, [&] {
     require(mode == ZOLO_SOLVE_DIRECT || mode == ZOLO_SOLVE_HYBRID, "zolo_set_solve_mode: unknown mode");
     require(c->have_design, "zolo_set_solve_mode: set the design first");
+    require(mode == ZOLO_SOLVE_DIRECT || c->refine == 0, "zolo_set_solve_mode: the hybrid solve has no refinement");
     if (mode == ZOLO_SOLVE_HYBRID) {
       require(pole >= 0 && pole < c->r, "zolo_set_solve_mode: factored pole out of range");
       require(c->order_mode == ZOLO_ORDER_ND, "zolo_set_solve_mode: the hybrid solve needs the ND ordering");
@@ -2310,6 +2041,26 @@ int zolo_set_solve_mode(zolo_ctx* c, int mode, int pole, double inner_tol, int i
     refresh_own(*c);
     if (c->hybrid) hybrid_setup(*c);
   });
+}
+
+int zolo_set_refinement(zolo_ctx* c, int steps) {
+  return guarded(c, [&] {
+    require(steps >= 0 && steps <= 2, "zolo_set_refinement: steps must be in [0, 2]");
+    require(steps == 0 || !c->hybrid, "zolo_set_refinement: not available with the hybrid solve");
+    if (steps != c->refine) {
+      c->refine = steps;
+      c->ncap = 0;  // the workspace (residual blocks, refinement chains) is rebuilt
+    }
+  });
+}
+
+int zolo_pool_trim(int device) {
+  int saved = -1;
+  cudaGetDevice(&saved);
+  if (cudaSetDevice(device) != cudaSuccess) return ZOLO_ERR_CUDA;
+  pool_trim(device);
+  if (saved >= 0) cudaSetDevice(saved);
+  return ZOLO_OK;
 }
 
 int zolo_nccl_unique_id(void* out) {
@@ -2371,11 +2122,12 @@ namespace {
 double bytes_per_column(zolo_ctx& c, int maxit) {
   const double ld = static_cast<double>(c.geom.npad), es = static_cast<double>(c.es());
   const int nch = c.nchains(), q = 2 * c.r;
-  const double crows = c.sparse ? static_cast<double>(TILE) * std::max(c.sp_nslots, 1) : ld;
+  const double crows = static_cast<double>(TILE) * std::max(c.sp_nslots, 1);
   const double nchunk = std::ceil(ld / CHUNK);
   double b = c.n * es + ld * (3 * es + 16 + 16.0 * nch + es * (maxit + 2)) + 16.0 * nch * crows;
   b += es * (maxit + 1) * maxit + 16.0 * q * (maxit * maxit + 4.0 * maxit + 1) + 2 * es * nchunk * (maxit + 1);
   if (c.hybrid) b += 16.0 * ld * (c.hy_max + 4) + 16.0 * (c.r - 1) * c.hy_max * c.hy_max;
+  if (c.refine) b += 16.0 * nch * ld;
   return b;
 }
 
@@ -2386,6 +2138,7 @@ void release_workspace(zolo_ctx& c) {
     m->release();
   for (auto& m : c.xbuf) m->release();
   for (auto& m : c.cbuf) m->release();
+  for (auto& m : c.rbuf) m->release();
   for (auto& m : c.basis) m->release();
   for (auto& m : c.ibasis) m->release();
   for (int k = 0; k < 2; ++k) {
@@ -2576,19 +2329,11 @@ int zolo_sweep_profile(const zolo_ctx* c, int64_t* out) {
   for (int i = 0; i < 8; ++i) out[i] = 0;
   if (!c->factored && !c->sym_ready) return ZOLO_ERR_DOMAIN;
   out[0] = c->geom.nbk;
-  if (c->sparse || (!c->factored && c->sym_ready)) {
-    out[1] = c->sgeom.ntiles;
-    out[2] = c->sched_fwd.ntask;
-    out[3] = c->sched_bwd.ntask;
-    out[4] = c->sp_nslots;
-    out[5] = c->critical_path;
-    out[6] = 0;
-    out[7] = c->sel_K;
-  } else {
-    out[1] = c->env_tiles;
-    out[5] = c->geom.nbk;
-    out[6] = 1;
-  }
+  out[1] = c->sgeom.ntiles;
+  out[2] = c->sched_fwd.ntask;
+  out[3] = c->sched_bwd.ntask;
+  out[4] = c->sp_nslots;
+  out[5] = c->critical_path;
   return ZOLO_OK;
 }
 
@@ -2689,32 +2434,6 @@ int zolo_rcm(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm, int
     if (bw) *bw = bandwidth_under(n, rp, ci, perm);
     if (profile) *profile = profile_under(n, rp, ci, perm);
     return ZOLO_OK;
-  } catch (const std::exception& e) {
-    g_create_err = e.what();
-    return ZOLO_ERR_NUMERICAL;
-  }
-}
-
-int zolo_build_design(const double* gaps, int r, double* design) {
-  try {
-    build_filter_design(gaps, r, design);
-    return ZOLO_OK;
-  } catch (const DesignError& e) {
-    g_create_err = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    g_create_err = e.what();
-    return ZOLO_ERR_NUMERICAL;
-  }
-}
-
-int zolo_eval_filter(const double* gaps, int r, int64_t npts, const double* x, double* g_out, double* f_out) {
-  try {
-    eval_filter_scalar(gaps, r, npts, x, g_out, f_out);
-    return ZOLO_OK;
-  } catch (const DesignError& e) {
-    g_create_err = e.what();
-    return e.code;
   } catch (const std::exception& e) {
     g_create_err = e.what();
     return ZOLO_ERR_NUMERICAL;

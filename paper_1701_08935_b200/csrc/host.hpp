@@ -5,11 +5,6 @@
 #include <vector>
 
 namespace zolo {
-// status-carrying error thrown by the host setup (codes as include/zolo_b200.h)
-struct DesignError : std::runtime_error {
-  int code;
-  DesignError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
 // Block (32x32-tile) structure of the LU factors under a node ordering
 // (symbolic.cpp). Off-diagonal tile ids are row-major slots: row i's tiles
 // (i, row_idx[e]) for e in [row_ptr[i], row_ptr[i+1]), k ascending; column
@@ -40,31 +35,15 @@ struct FactorPlan {
 };
 void factor_plan(const BlockStructure& bs, FactorPlan& plan);
 
-// One claim-ordered task of a DAG triangular sweep (trsm.cu dag_kernel).
+// One claim-ordered task of a DAG triangular sweep (trsm.cu dag2_kernel).
 // Block row i's dependencies, in processing order q (forward: ascending
 // column, backward: descending row), are cut into CHUNK tasks (out >= 0: sum
 // op(T~) u_j over q in [qa, qb) into partial slot `out`) and one ROW task
 // (out = -1: u_i = pre(b_i) - sum over q in [qa, qb) - partial slots
 // [pa, pa + pc)). Every task appears after all tasks it waits on, so
 // persistent CTAs claiming in this order cannot deadlock.
-//
-// Selective inversion of the trailing dense block S = [s0, nb) (the top
-// separator, whose rows otherwise form a serial chain at the end of the
-// forward and the start of the backward sweep): forward rows i in S become a
-// phase-A task (row task over the dependencies outside S plus the b_i entry,
-// written raw into the partial slot cs_i) and phase-B tasks (DT_SLOTDEP:
-// u_i = c_i + sum_{k<i} M(i,k) c_k, the c_k read from their slots);
-// backward rows in S read only the sweep input (DT_SRCDEP: u_i = sum_{k>=i}
-// W(i,k) b_k). M and W are the inverted blocks (factor.cu selinv).
-constexpr int DT_BENTRY = 1;   // chunk-kind task (out >= 0) that also takes the b_i / pre(b_i) entry
-constexpr int DT_SLOTDEP = 2;  // dependencies are (slot of c_k, inverse tile id)
-constexpr int DT_SRCDEP = 4;   // dependencies are (block row k of the sweep input, inverse tile id)
-constexpr int DT_NOB = 8;      // row task without the b_i entry
-constexpr int DT_FWDWAIT = 16; // backward root (no backward dependencies; informational: in a fused
-                               // launch every backward row task waits for its forward u_i)
 struct DagTask {
   int i, qa, qb, pa, pc, out;
-  int flags = 0;
 };
 // first block row of the largest trailing block [s0, nb) of at most kmax block rows whose
 // L pattern is dense (every row holds every earlier row of the block); nb if none
@@ -76,18 +55,11 @@ int trailing_dense_start(const BlockStructure& bs, int kmax);
 // positional order, 1 = by earliest start time (EST), 2 = by longest path to
 // the sweep's end (BL), >= 3: EST - (order - 2)/8 * BL (all weighted by tile
 // products; all topological). Returns the slot count.
-// chain_partials: chunk c adds chunk c-1's partial (pa = its slot, pc = 1) and the row task
-// adds only the last one -- one add-block on the row's critical path instead of one per chunk.
-// s0 < nb: selectively inverted trailing block (see above); cslot (forward) receives cs_i per row.
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
-                 int near, int order, std::vector<DagTask>& tasks, bool chain_partials = false, int64_t s0 = -1,
-                 std::vector<int>* cslot = nullptr);
+                 int near, int order, std::vector<DagTask>& tasks);
 void rcm_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm);
 int64_t bandwidth_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);
 int64_t profile_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);
 void uniform_stream(uint64_t seed, int64_t n, double* out);
 bool random_block(int cx, int64_t n, int64_t k, uint64_t seed, bool orthonormalize, double* out);
-void build_filter_design(const double* gaps, int r, double* out);
-int choose_order(const double* gaps, double eps);
-void eval_filter_scalar(const double* gaps, int r, int64_t npts, const double* x, double* g_out, double* f_out);
 }  // namespace zolo

@@ -24,7 +24,7 @@ namespace {
 
 constexpr int RT = 256;          // threads per reduction block
 constexpr int RPT = CHUNK / RT;  // rows per thread in a chunk
-constexpr int KMAX = 256;        // largest Krylov dimension (outer GMRES <= 64, hybrid inner <= 256)
+constexpr int KMAX = KRYLOV_MAX;  // shared-memory room for the Arnoldi coefficients
 constexpr int SPC = 8;           // SpMM columns per thread (4 and 16 measured the same)
 
 template <class S>
@@ -184,6 +184,66 @@ __global__ void bsr_spmm_kernel(int64_t na, int b, const int* brp, const int* bc
       else
         out[row + (a0 + c) * ld] = acc[c];
     }
+}
+
+// r_z = b - (A - sigma_z B) x_z per chain z (blockIdx.z), one row x SPC columns per thread: the
+// row's A and B entries are read once for the SPC columns (iterative refinement of the shifted
+// solves; K = A - sigma B assembled on the fly, assemble_shifted sparse.hpp:153-186)
+struct ChainPtrs {
+  cd* p[2 * 16];
+};
+template <class S>
+__global__ void shifted_residual_kernel(int64_t n, int64_t ld, const int* arp, const int* aci, const S* av,
+                                        const int* brp, const int* bci, const S* bv, const cd* b, ChainPtrs xs,
+                                        ChainPtrs rs, const cd* sigma, int na) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int a0 = blockIdx.y * SPC, z = blockIdx.z;
+  if (t >= ld) return;
+  const cd* x = xs.p[z];
+  cd* r = rs.p[z];
+  cd ax[SPC], bx[SPC];
+#pragma unroll
+  for (int c = 0; c < SPC; ++c) ax[c] = bx[c] = mk(0.0, 0.0);
+  const int ncl = min(SPC, na - a0);
+  if (t < n) {
+    for (int q = arp[t]; q < arp[t + 1]; ++q) {
+      const cd m = to_cd(av[q]);
+      const int64_t j = aci[q];
+#pragma unroll
+      for (int c = 0; c < SPC; ++c)
+        if (c < ncl) cfma(ax[c], m, x[j + (a0 + c) * ld]);
+    }
+    if (brp) {
+      for (int q = brp[t]; q < brp[t + 1]; ++q) {
+        const cd m = to_cd(bv[q]);
+        const int64_t j = bci[q];
+#pragma unroll
+        for (int c = 0; c < SPC; ++c)
+          if (c < ncl) cfma(bx[c], m, x[j + (a0 + c) * ld]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < SPC; ++c)
+        if (c < ncl) bx[c] = x[t + (a0 + c) * ld];
+    }
+  }
+  const cd sg = sigma[z];
+#pragma unroll
+  for (int c = 0; c < SPC; ++c)
+    if (c < ncl) {
+      const int64_t off = t + (a0 + c) * ld;
+      // padding rows (t >= n) carry zeros in b and x: their residual is zero
+      r[off] = t < n ? cadd(csub(b[off], ax[c]), cmul(sg, bx[c])) : mk(0.0, 0.0);
+    }
+}
+
+__global__ void add_corrections_kernel(int64_t ld, ChainPtrs xs, ChainPtrs ds) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t a = blockIdx.y;
+  const int z = blockIdx.z;
+  if (t >= ld) return;
+  cd* x = xs.p[z];
+  x[t + a * ld] = cadd(x[t + a * ld], ds.p[z][t + a * ld]);
 }
 
 // rows[0..nrows) of columns 0..k-1 set to zero (the identity padding rows of the BSR SpMM output)
@@ -772,6 +832,24 @@ void Krylov<S>::bsr_spmm(cudaStream_t st, int64_t na, int b, const int* brp, con
   if (k > 0 && na > 0)
     bsr_spmm_kernel<S><<<dim3(blocks_for(na * b, 256), static_cast<unsigned>((k + SPC - 1) / SPC)), 256, 0, st>>>(
         na, b, brp, bci, bval, row0, v, ld, act, k, out, outc);
+}
+
+template <class S>
+void Krylov<S>::shifted_residual(cudaStream_t st, int64_t n, int64_t ld, const int* arp, const int* aci, const S* av,
+                                 const int* brp, const int* bci, const S* bv, const cd* b, cd* const* x, cd* const* r,
+                                 const cd* sigma, int nch, int na) {
+  if (na <= 0 || nch <= 0) return;
+  ChainPtrs xp, rp;
+  for (int z = 0; z < nch; ++z) xp.p[z] = x[z], rp.p[z] = r[z];
+  shifted_residual_kernel<S><<<dim3(blocks_for(ld, 256), (na + SPC - 1) / SPC, nch), 256, 0, st>>>(
+      n, ld, arp, aci, av, brp, bci, bv, b, xp, rp, sigma, na);
+}
+
+void add_corrections(cudaStream_t st, int64_t ld, cd* const* x, cd* const* d, int nch, int na) {
+  if (na <= 0 || nch <= 0) return;
+  ChainPtrs xp, dp;
+  for (int z = 0; z < nch; ++z) xp.p[z] = x[z], dp.p[z] = d[z];
+  add_corrections_kernel<<<dim3(blocks_for(ld, 256), na, nch), 256, 0, st>>>(ld, xp, dp);
 }
 
 void zero_rows(cudaStream_t st, const int* rows, int nrows, cd* out, int64_t ld, int64_t k) {

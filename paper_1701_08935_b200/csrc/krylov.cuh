@@ -8,6 +8,7 @@
 namespace zolo {
 
 constexpr int CHUNK = 2048;  // rows per block in the column reductions
+constexpr int KRYLOV_MAX = 256;  // largest Krylov dimension per column (outer GMRES and the hybrid inner solve)
 
 struct GmresDev {
   // per column c (n_v) and shift k (q): see krylov.cu
@@ -71,11 +72,18 @@ struct Krylov {
   static void bsr_spmm(cudaStream_t st, int64_t na, int b, const int* brp, const int* bci, const S* bval,
                        const int* row0, const S* v, int64_t ld, const int* act, int64_t k, S* out, cd* outc);
   // out (ld x k) = M * V (M permuted CSR with S values)
+  // Refinement residuals of the shifted solves (zolo_set_refinement): for every chain z,
+  // r_z[:, a] = b[:, a] - (A - sigma_z B) x_z[:, a], a < na (B = I when brp == nullptr).
+  static void shifted_residual(cudaStream_t st, int64_t n, int64_t ld, const int* arp, const int* aci, const S* av,
+                               const int* brp, const int* bci, const S* bv, const cd* b, cd* const* x, cd* const* r,
+                               const cd* sigma, int nch, int na);
   static void spmm(cudaStream_t st, int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
                    int64_t k, S* out);
 };
 
 // out[rows[q], c] = 0 for q < nrows, c < k (ld rows per column)
+// x_z[:, 0:na] += d_z[:, 0:na] for the chains z < nch (the refinement corrections)
+void add_corrections(cudaStream_t st, int64_t ld, cd* const* x, cd* const* d, int nch, int na);
 void zero_rows(cudaStream_t st, const int* rows, int nrows, cd* out, int64_t ld, int64_t k);
 
 }  // namespace zolo

@@ -490,105 +490,39 @@ int trailing_dense_start(const BlockStructure& bs, int kmax) {
 }
 
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
-                 int near, int order, std::vector<DagTask>& tasks, bool chain_partials, int64_t s0,
-                 std::vector<int>* cslot) {
+                 int near, int order, std::vector<DagTask>& tasks) {
   if (chunk < 1 || near < 0) throw std::invalid_argument("dag_schedule: chunk >= 1, near >= 0");
-  if (s0 < 0 || s0 > nb) s0 = nb;
-  if (nb - s0 < 2) s0 = nb;  // nothing to invert
-  if (cslot) cslot->assign(nb, -1);
   // processing position of block row j in the sweep (forward: j, backward: nb-1-j)
   auto position = [&](int64_t j) { return fwd ? j : nb - 1 - j; };
   std::vector<std::vector<DagTask>> after(nb);  // chunks claimed right after row task at a position
-  std::vector<std::vector<DagTask>> before(nb);  // tasks claimed right before the row task at a position
-  std::vector<DagTask> rows(nb), tail;
+  std::vector<DagTask> rows(nb);
   int slots = 0;
-  // deps [lo, hi) of row i: the `near` latest stay with the row task, the rest go to balanced
-  // chunks of <= chunk deps; returns the first far dependency kept by the row (= lo if none)
-  auto cut = [&](int64_t i, int lo, int hi, int flags, int first_slot, std::vector<DagTask>& out) {
-    const int n = hi - lo;
-    if (n <= near + chunk) return lo;
-    const int far = n - near;
-    const int nchunk = (far + chunk - 1) / chunk;
-    for (int c = 0, q0 = 0; c < nchunk; ++c) {
-      const int q1 = static_cast<int>((static_cast<int64_t>(far) * (c + 1)) / nchunk);
-      out.push_back(DagTask{static_cast<int>(i), lo + q0, lo + q1, 0, 0, first_slot + c, flags});
-      q0 = q1;
-    }
-    return lo + far;
-  };
-  auto nchunks = [&](int n) { return n <= near + chunk ? 0 : (n - near + chunk - 1) / chunk; };
   for (int64_t s = 0; s < nb; ++s) {
     const int64_t i = fwd ? s : nb - 1 - s;
     const int64_t e0 = ptr[i];
     const int nd = static_cast<int>(ptr[i + 1] - e0);
     // dependency at processing index q (ascending completion order)
     auto dep = [&](int q) { return fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q]; };
-    if (i >= s0 && fwd) {
-      // selective inversion, forward: phase A c_i = pre(b_i) - sum_{j < s0} (into slot cs_i), phase B
-      // u_i = c_i + sum_{s0 <= k < i} M(i, k) c_k (appended after every A task)
-      int next = 0;
-      while (next < nd && dep(next) < s0) ++next;
-      const int n_ext = next, n_b = nd - n_ext;
-      if (n_b != i - s0) throw std::logic_error("dag_schedule: trailing block is not dense");
-      const int nch_b = nchunks(n_b);
-      const int cs = slots;  // [cs_i, B chunk partials...] contiguous: the B row adds them in one range
-      slots += 1 + nch_b;
-      if (cslot) (*cslot)[i] = cs;
-      std::vector<DagTask> ch;
-      const int far_a = cut(i, 0, n_ext, 0, slots, ch);
-      const int nch_a = static_cast<int>(ch.size());
-      slots += nch_a;
-      for (const DagTask& t : ch) after[position(dep(t.qb - 1))].push_back(t);
-      rows[s] = DagTask{static_cast<int>(i), far_a, n_ext, cs + 1 + nch_b, nch_a, cs, DT_BENTRY};
-      if (nch_a == 0) rows[s].pa = 0;
-      ch.clear();
-      const int far_b = cut(i, n_ext, nd, DT_SLOTDEP, cs + 1, ch);
-      for (const DagTask& t : ch) tail.push_back(t);
-      tail.push_back(DagTask{static_cast<int>(i), far_b, nd, cs, 1 + nch_b, -1, DT_SLOTDEP | DT_NOB});
-      continue;
-    }
-    if (i >= s0 && !fwd) {
-      // selective inversion, backward: u_i = sum_{k >= i in S} W(i, k) b_k, all from the sweep input
-      const int n_w = static_cast<int>(nb - i);
-      std::vector<DagTask> ch;
-      const int far_w = cut(i, 0, n_w, DT_SRCDEP, slots, ch);
-      const int nch = static_cast<int>(ch.size());
-      for (const DagTask& t : ch) before[s].push_back(t);
-      rows[s] = DagTask{static_cast<int>(i), far_w, n_w, nch ? slots : 0, nch, -1, DT_SRCDEP | DT_NOB};
-      slots += nch;
-      continue;
-    }
-    DagTask row{static_cast<int>(i), 0, nd, slots, 0, -1, 0};
+    DagTask row{static_cast<int>(i), 0, nd, slots, 0, -1};
     if (nd > near + chunk) {
       const int far = nd - near;
       const int nchunk = (far + chunk - 1) / chunk;
-      const int first_slot = slots;
       for (int c = 0, q0 = 0; c < nchunk; ++c) {
         const int q1 = static_cast<int>((static_cast<int64_t>(far) * (c + 1)) / nchunk);  // balanced cut
         const int64_t last = position(dep(q1 - 1));
-        // chained partials: chunk c also adds chunk c-1's partial, so the row task adds one block
-        const int pa = chain_partials && c > 0 ? first_slot + c - 1 : 0;
-        const int pc = chain_partials && c > 0 ? 1 : 0;
-        after[last].push_back(DagTask{static_cast<int>(i), q0, q1, pa, pc, slots++, 0});
+        after[last].push_back(DagTask{static_cast<int>(i), q0, q1, 0, 0, slots++});
         q0 = q1;
       }
       row.qa = far;
-      if (chain_partials) {
-        row.pa = first_slot + nchunk - 1;
-        row.pc = 1;
-      } else {
-        row.pc = nchunk;
-      }
+      row.pc = nchunk;
     }
     rows[s] = row;
   }
   std::vector<DagTask> seq;  // positional topological order
   for (int64_t s = 0; s < nb; ++s) {
-    for (const DagTask& t : before[s]) seq.push_back(t);
     seq.push_back(rows[s]);
     for (const DagTask& t : after[s]) seq.push_back(t);
   }
-  for (const DagTask& t : tail) seq.push_back(t);
   tasks.clear();
   if (order == 0) {
     tasks = std::move(seq);
@@ -605,11 +539,7 @@ int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<
     const DagTask& k = seq[t];
     const int64_t e0 = ptr[k.i];
     const int nd = static_cast<int>(ptr[k.i + 1] - e0);
-    if (!(k.flags & DT_SRCDEP))
-      for (int q = k.qa; q < k.qb; ++q) {
-        const int64_t j = fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q];
-        deps[t].push_back((k.flags & DT_SLOTDEP) ? slot_task[(*cslot)[j]] : row_task[j]);
-      }
+    for (int q = k.qa; q < k.qb; ++q) deps[t].push_back(row_task[fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q]]);
     for (int p = k.pa; p < k.pa + k.pc; ++p) deps[t].push_back(slot_task[p]);
     cost[t] = (k.qb - k.qa) + 0.25 * k.pc + 2.0;
   }
