@@ -267,13 +267,17 @@ void zolo_set_error(zolo_ctx* ctx, const char* msg);
  * ms[4] = kernel launches of the last apply_filter (all kernels),
  * ms[5] = operator applications (sum of active columns) of the last apply_filter,
  * ms[6] = hybrid solve: inner K_p applications (column-steps) of the last apply_filter,
- * ms[7] reserved. ms must hold 8 doubles. */
+ * ms[7] = device time of the GMRES iterations of the last apply_filter.
+ * ms must hold 8 doubles. */
 int zolo_last_timings(const zolo_ctx* ctx, double* ms);
 
 /* Structure the triangular sweeps run over (per pole, after zolo_factorize):
  * out[0] block rows (32-row tiles), out[1] off-diagonal tiles of L (= of U),
  * out[2] / out[3] forward / backward DAG task records, out[4] chunk
- * partial-sum slots, out[5] critical path in block rows, out[6..7] reserved.
+ * partial-sum slots, out[5] critical path in block rows; work accounting of
+ * one pole's sweep tiles (Lt, Ut, DinvL, DinvU: 1024 stored entries each):
+ * out[6] nonzero entries (the scalar fill), out[7] entries inside the
+ * unmasked 8 x 4 blocks the DMMA loops execute (op N).
  * No equivalent in the reference (development / roofline accounting). */
 int zolo_sweep_profile(const zolo_ctx* ctx, int64_t* out);
 

@@ -466,7 +466,8 @@ class FilterOperator:
         out = np.zeros(8, dtype=np.int64)
         _check(self._h, lib().zolo_sweep_profile(self._h, _ptr(out)))
         return dict(block_rows=int(out[0]), offdiag_tiles=int(out[1]), fwd_tasks=int(out[2]),
-                    bwd_tasks=int(out[3]), chunk_slots=int(out[4]), critical_path=int(out[5]))
+                    bwd_tasks=int(out[3]), chunk_slots=int(out[4]), critical_path=int(out[5]),
+                    nonzero_entries=int(out[6]), executed_entries=int(out[7]))
 
     def timer_start(self):
         _check(self._h, lib().zolo_timer(self._h, 0, None))

@@ -220,6 +220,12 @@ WINDOWS = {
     # tools/find_window_gpu.py cfg4s 0.0 32: chemistry_pencil(10, seed=4), 32 eigenvalues around 0
     "cfg4s": {"gaps": [-0.002050713632706902, -0.00195394425863924, 0.0019219309968320887, 0.002050941998095368],
               "count": 32},
+    # eigsh k=72 sigma=0 on tight_binding_pencil(20, seed=3, disorder=1.5): the 32 eigenvalues around 0
+    "cfg3s": {"gaps": [-0.01663101713848762, -0.016183636199440375, 0.014065304252567426, 0.015125174367574061],
+              "count": 32},
+    # eigsh k=72 sigma=0 on multi_gpu_pencil(20, seed=5): the 32 eigenvalues around 0
+    "cfg5s": {"gaps": [-0.01749621111507395, -0.0170219315255981, 0.018059854034975464, 0.01905197161627576],
+              "count": 32},
     # tools/find_window_gpu.py cfg5 0.0 256: multi_gpu_pencil(64, seed=5), 256 eigenvalues around 0
     "cfg5": {"gaps": [-0.004444281498217607, -0.004424367355750291, 0.004403209645170138, 0.004455014820632642],
              "count": 256},
@@ -228,6 +234,12 @@ WINDOWS = {
 
 # BSR block size of a config's pencil (atoms of 13 rows for the chemistry-shaped configs)
 BLOCK_SIZE = {"cfg4": 13, "cfg4s": 13}
+
+# The same generator at a size the reference's CPU path (RCM band LU) finishes in
+# seconds: the configs whose reference factorization is infeasible (cfg3: ~0.5-1 h and 99 GB;
+# cfg5: ~0.4 TB) are compared with the reference on these siblings instead (the cfg4 generator
+# needs ~7 min of reference factorization even at 1000 atoms: no sibling).
+SMALL_SIBLING = {"cfg3": "cfg3s", "cfg5": "cfg5s"}
 
 
 def config(name: str):
@@ -247,6 +259,12 @@ def config(name: str):
     if name == "cfg4s":  # config 4's generator at 10^3 atoms (N = 13000): fits one GPU with all 8 poles
         w = WINDOWS["cfg4s"]
         return chemistry_pencil(10, seed=4), True, w["gaps"], 8, 64, w["count"]
+    if name == "cfg3s":  # config 3's generator at 20^3 (N = 8000)
+        w = WINDOWS["cfg3s"]
+        return tight_binding_pencil(20, seed=3, disorder=1.5), True, w["gaps"], 8, 64, w["count"]
+    if name == "cfg5s":  # config 5's generator at 20^3 (N = 8000)
+        w = WINDOWS["cfg5s"]
+        return multi_gpu_pencil(20, seed=5), True, w["gaps"], 8, 64, w["count"]
     if name == "cfg5":
         w = WINDOWS["cfg5"]
         return multi_gpu_pencil(64, seed=5), True, w["gaps"], 8, 320, w["count"]

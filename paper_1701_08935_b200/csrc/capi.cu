@@ -321,6 +321,7 @@ struct zolo_ctx {
   int64_t nd_leaf = 192;
   SpGeom sgeom;
   int64_t critical_path = 0;
+  int64_t work_nnz = 0, work_exec = 0;  // pole 0's sweep tiles: nonzero entries / entries in unmasked 8x4 blocks
   int iters_seen = 0;         // largest Krylov dimension an apply_filter on this context has needed
   const int* lag_done = nullptr;  // lagged GMRES control: per-column done flags the sweeps may skip on
   int* act_hq[4] = {};   // pinned active lists / done flags, one per lagged-loop slot
@@ -803,7 +804,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   store.ensure(need);
   c.rownorm_mem.ensure(sizeof(double) * c.sgeom.npad * r);
   c.fstate_mem.ensure(sizeof(unsigned long long) * 2 * r);
-  c.sp_err.ensure(sizeof(int) * 4);
+  c.sp_err.ensure(sizeof(int) * 4 + 2 * sizeof(unsigned long long));
   CK(cudaMemsetAsync(c.sp_err.p, 0, sizeof(int) * 4, c.st));
   tiles.assign(r, FactorTiles());
   dt.assign(r, nullptr);
@@ -871,6 +872,15 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
       tile_masks(c.pole_streams[j], tiles[j].DinvU, nb, tiles[j].mDU);
       tile_masks(c.pole_streams[j], tiles[j].Lt, ntiles, tiles[j].mLt);
       tile_masks(c.pole_streams[j], tiles[j].Ut, ntiles, tiles[j].mUt);
+      if (j == 0) {  // work accounting of the sweeps (one pole: all share the structure)
+        c.sp_err.ensure(sizeof(int) * 4 + 2 * sizeof(unsigned long long));
+        unsigned long long* wk = reinterpret_cast<unsigned long long*>(c.sp_err.as<int>() + 4);
+        CK(cudaMemsetAsync(wk, 0, 2 * sizeof(unsigned long long), c.pole_streams[0]));
+        tile_work(c.pole_streams[0], tiles[0].DinvL, tiles[0].mDL, nb, wk);
+        tile_work(c.pole_streams[0], tiles[0].DinvU, tiles[0].mDU, nb, wk);
+        tile_work(c.pole_streams[0], tiles[0].Lt, tiles[0].mLt, ntiles, wk);
+        tile_work(c.pole_streams[0], tiles[0].Ut, tiles[0].mUt, ntiles, wk);
+      }
       swizzle_tiles(c.pole_streams[j], tiles[j].DinvL, nb);
       swizzle_tiles(c.pole_streams[j], tiles[j].DinvU, nb);
       swizzle_tiles(c.pole_streams[j], tiles[j].Lt, ntiles);
@@ -888,8 +898,15 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
   c.last_ms[1] = ms;
   int serr = 0;
+  unsigned long long wk[2] = {0, 0};
   CK(cudaMemcpyAsync(&serr, c.sp_err.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  if (mstore)
+    CK(cudaMemcpyAsync(wk, c.sp_err.as<int>() + 4, sizeof(wk), cudaMemcpyDeviceToHost, c.st));
   CK(cudaStreamSynchronize(c.st));
+  if (mstore) {
+    c.work_nnz = static_cast<int64_t>(wk[0]);
+    c.work_exec = static_cast<int64_t>(wk[1]);
+  }
   if (serr) throw ZoloError(ZOLO_ERR_NUMERICAL, "zolo_factorize: symbolic structure does not cover the fill");
   CK(cudaMemcpyAsync(fs.data(), c.fstate_mem.p, fs.size() * 8, cudaMemcpyDeviceToHost, c.st));
   CK(cudaStreamSynchronize(c.st));
@@ -2334,6 +2351,8 @@ int zolo_sweep_profile(const zolo_ctx* c, int64_t* out) {
   out[3] = c->sched_bwd.ntask;
   out[4] = c->sp_nslots;
   out[5] = c->critical_path;
+  out[6] = c->work_nnz;
+  out[7] = c->work_exec;
   return ZOLO_OK;
 }
 

@@ -362,6 +362,20 @@ __global__ void __launch_bounds__(256) tile_mask_kernel(const cd* tiles, uint2* 
   if (threadIdx.x == 0) masks[t] = make_uint2(mn, mh);
 }
 
+// Work accounting of the sweeps (zolo_sweep_profile): out[0] += nonzero entries of the tiles,
+// out[1] += entries inside their unmasked 8 x 4 blocks (the DMMA k-steps the sweeps execute, op N).
+__global__ void __launch_bounds__(256) tile_work_kernel(const cd* tiles, const uint2* masks, int64_t ntiles,
+                                                        unsigned long long* out) {
+  const int64_t t = blockIdx.x;
+  if (t >= ntiles) return;
+  const cd* T = tiles + t * TT;
+  int nz = 0;
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) nz += (T[e].x != 0.0 || T[e].y != 0.0);
+  nz = __reduce_add_sync(0xffffffffu, nz);
+  if ((threadIdx.x & 31) == 0 && nz) atomicAdd(out, static_cast<unsigned long long>(nz));
+  if (threadIdx.x == 0) atomicAdd(out + 1, static_cast<unsigned long long>(__popc(masks[t].x)) * 32ull);
+}
+
 // Sylvester inertia: negative real parts among the pivots (diagonal of the
 // packed U_ii of every diagonal tile; identity padding rows have pivot 1).
 __global__ void neg_pivots_kernel(const cd* dt, int nb, unsigned long long* out) {
@@ -400,6 +414,10 @@ __global__ void __launch_bounds__(256) swizzle_tile_kernel(cd* tiles) {
     const int col = e / TILE, row = e % TILE;
     T[col * TILE + (row ^ swz(col))] = buf[e];
   }
+}
+
+void tile_work(cudaStream_t st, const cd* tiles, const uint2* masks, int64_t ntiles, unsigned long long* out) {
+  if (ntiles > 0) tile_work_kernel<<<static_cast<unsigned>(ntiles), 256, 0, st>>>(tiles, masks, ntiles, out);
 }
 
 void swizzle_tiles(cudaStream_t st, cd* tiles, int64_t ntiles) {

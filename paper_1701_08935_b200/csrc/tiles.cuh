@@ -113,6 +113,8 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const SpFactor& f, int64_t nnz,
 void tile_masks(cudaStream_t st, const cd* tiles, int64_t ntiles, uint2* masks);
 // tiles permuted in place into the sweep layout: element (row, col) at col*32 + (row ^ swz(col))
 void swizzle_tiles(cudaStream_t st, cd* tiles, int64_t ntiles);
+// out[0] += nonzero entries of the tiles, out[1] += entries in their unmasked 8 x 4 blocks (op N)
+void tile_work(cudaStream_t st, const cd* tiles, const uint2* masks, int64_t ntiles, unsigned long long* out);
 // number of pivots (diagonal of the packed diagonal-tile LUs) with negative real part
 int64_t count_negative_pivots(cudaStream_t st, const cd* dt, int nb);
 
