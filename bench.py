@@ -434,17 +434,22 @@ def main():
     # roofline of the dominant kernel (the DAG-scheduled block-sparse triangular sweeps); per G
     # application, per column, per pole and per solve (P = 2 for complex pencils: solve + adjoint):
     # forward + backward sweep over the off-diagonal tiles plus the diagonal-block inverse products
-    # = 2 (ntiles + nb) complex 32x32 tile-column products of 8 * 1024 flops
+    # = 2 (ntiles + nb) complex 32x32 tile-column products; of their 1024 entries per tile the DMMA
+    # loops execute those in unmasked 8x4 blocks (sweep_profile executed_entries) at 8 flops per
+    # complex MAC -- the executed tensor work, the basis of `achieved`; the scalar fill (nonzero
+    # entries) is the useful share of it
     peaks = load_peaks()
     chains_per_pole = 2 if cx else 1
     tile_products = 2 * (sp["offdiag_tiles"] + sp["block_rows"])
     stored_entries = tile_products * 1024
-    trsm_flops = opapps * len(op.poles) * chains_per_pole * tile_products * 8.0 * 1024  # this rank, K steps
-    achieved = trsm_flops / (trsm_ms * 1e-3) / 1e12 if trsm_ms > 0 else 0.0
-    peak = peaks.get("fp64_tflops")
-    traffic, traffic_src = load_traffic(args.config)
     frac_nz = sp["nonzero_entries"] / stored_entries if stored_entries else None
     frac_exec = sp["executed_entries"] / stored_entries if stored_entries else None
+    units_solved = opapps * len(op.poles) * chains_per_pole  # column solves, this rank, K steps
+    stored_flops = units_solved * stored_entries * 8.0
+    trsm_s = trsm_ms * 1e-3
+    achieved = stored_flops * frac_exec / trsm_s / 1e12 if trsm_ms > 0 else 0.0
+    peak = peaks.get("fp64_tflops")
+    traffic, traffic_src = load_traffic(args.config)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if poles else "weak",
@@ -467,12 +472,13 @@ def main():
                      "traffic_source": traffic_src or "no ncu capture of this config committed (profiles/)",
                      "peak_source": "measured FP64 tensor pipe (tools/fp64_peak.cu mma.sync.m8n8k4.f64, "
                                     "profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no FP64 figure)",
-                     "algorithmic": "8 flops per complex MAC x stored factor entries (off-diagonal L and U "
-                                    "tiles + diagonal-block inverses, 1024 per tile) per column per pole per "
-                                    "solve per G application",
+                     "algorithmic": "8 flops per complex MAC x factor entries inside the unmasked 8x4 blocks "
+                                    "of the sweep tiles (off-diagonal L and U tiles + diagonal-block inverses) "
+                                    "per column per pole per solve per G application: the DMMA work executed",
                      "stored_entries_per_pole_solve": stored_entries,
                      "executed_fraction": frac_exec, "scalar_fill_fraction": frac_nz,
-                     "achieved_scalar_fill": achieved * frac_nz if frac_nz else None,
+                     "achieved_stored_tiles": stored_flops / trsm_s / 1e12 if trsm_ms > 0 else None,
+                     "achieved_scalar_fill": stored_flops * frac_nz / trsm_s / 1e12 if trsm_ms > 0 else None,
                      "trsm_share_of_step": trsm_ms / total_ms if total_ms else None,
                      "trsm_launches": trsm_launches},
         "clocks": clk,

@@ -169,12 +169,33 @@ int zolo_count_below(zolo_ctx* ctx, double sigma, int64_t* count, double* min_pi
  * G v and run an identical (replicated) Krylov iteration; rank 0 adds the
  * constant term. unique_id: ZOLO_NCCL_ID_BYTES bytes from zolo_nccl_unique_id
  * on rank 0, broadcast by the caller; all ranks call collectively, before
- * zolo_factorize. unique_id = NULL with nranks > 1 gives an unreduced context:
+ * zolo_factorize. By default the Arnoldi step is row-sharded: rank g keeps rows
+ * [g rb, (g + 1) rb) of the Krylov vectors (rb = npad / nranks rounded up to
+ * 32), a G application ends with an ncclReduceScatter of the partial sums over
+ * those row blocks, the CGS2 inner products are all-reduced and the next basis
+ * vector all-gathered -- the bytes of one all-reduce per iteration, the
+ * Arnoldi work divided by the ranks (ZOLO_ROW_SHARD=0: the replicated variant,
+ * one ncclAllReduce of G and every rank orthogonalising all rows).
+ * unique_id = NULL with nranks > 1 gives an unreduced context:
  * zolo_apply_g returns the rank's partial sum, zolo_apply_filter refuses.
  * NCCL is loaded with dlopen (libnccl.so.2) only when a communicator is built. */
 #define ZOLO_NCCL_ID_BYTES 128
 int zolo_nccl_unique_id(void* out);
 int zolo_set_pole_shard(zolo_ctx* ctx, int rank, int nranks, const void* unique_id);
+
+/* The same pole shard with the group's collectives staged through the host:
+ * fn(op, buf, count, user) must complete the collective over the nranks
+ * callers (returning 0) on doubles in host memory:
+ *   ZOLO_COLL_ALLREDUCE       buf[0..count) in place, summed over the ranks;
+ *   ZOLO_COLL_REDUCE_SCATTER  in: buf[0 .. nranks count) (rank-major blocks);
+ *                             out: buf[0 .. count) = this rank's block summed;
+ *   ZOLO_COLL_ALLGATHER       in: this rank's block at buf[rank count ..);
+ *                             out: buf[0 .. nranks count) all blocks.
+ * Any transport works (torch.distributed gloo, threads of one process sharing
+ * a GPU -- no kernel of one rank ever waits on another's). */
+enum { ZOLO_COLL_ALLREDUCE = 0, ZOLO_COLL_REDUCE_SCATTER = 1, ZOLO_COLL_ALLGATHER = 2 };
+typedef int (*zolo_collective_fn)(int op, double* buf, int64_t count, void* user);
+int zolo_set_pole_shard_host(zolo_ctx* ctx, int rank, int nranks, zolo_collective_fn fn, void* user);
 
 /* FilterOperator(pencil, design): upload + set_design + factorize. */
 int zolo_filter_create(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,

@@ -100,6 +100,8 @@ class FactorStats(C.Structure):
 
 
 _lib = None
+# zolo_collective_fn (include/zolo_b200.h): op, buffer of doubles, count, user
+COLLECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_void_p)
 
 
 def build() -> None:
@@ -127,6 +129,7 @@ def lib():
         L.zolo_set_design.argtypes = [P, P, C.c_int]
         L.zolo_set_ordering.argtypes = [P, C.c_int, I64]
         L.zolo_set_pole_shard.argtypes = [P, C.c_int, C.c_int, C.c_char_p]
+        L.zolo_set_pole_shard_host.argtypes = [P, C.c_int, C.c_int, COLLECTIVE_FN, P]
         L.zolo_set_block_size.argtypes = [P, I64]
         L.zolo_nccl_unique_id.argtypes = [C.c_char_p]
         L.zolo_count_below.argtypes = [P, D, P, P]
@@ -293,8 +296,11 @@ class FilterOperator:
     ``is_complex`` selects S = complex128 (Hermitian pencil) vs float64.
     ``shard=(rank, nranks, unique_id)`` makes this operator one pole shard of a
     multi-GPU operator (zolo_set_pole_shard): it factors the poles
-    :func:`shard_poles` gives and all-reduces every G application over NCCL;
-    ``unique_id=None`` leaves G unreduced (``apply_g`` returns the partial sum).
+    :func:`shard_poles` gives and reduces every G application over NCCL (row-sharded
+    Arnoldi by default); ``unique_id=None`` leaves G unreduced (``apply_g`` returns the
+    partial sum). ``shard=(rank, nranks, fn)`` with a :data:`COLLECTIVE_FN` callback
+    stages the group's collectives through the host instead (zolo_set_pole_shard_host;
+    sharding.py builds them over torch.distributed or over threads of one process).
     ``block_size=b`` declares a BSR pencil (atoms of b rows, BASELINE config 4;
     zolo_set_block_size): the ordering keeps atoms whole and the SpMMs use BSR.
     ``solve="hybrid"`` factors only pole ``hybrid_pole`` and solves the other
@@ -334,7 +340,11 @@ class FilterOperator:
         self.shard = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
         if shard is not None:
             uid = shard[2] if len(shard) > 2 else None
-            _check(h, L.zolo_set_pole_shard(h, self.shard[0], self.shard[1], uid))
+            if isinstance(uid, COLLECTIVE_FN):
+                self._collective = uid  # keep the callback alive
+                _check(h, L.zolo_set_pole_shard_host(h, self.shard[0], self.shard[1], uid, None))
+            else:
+                _check(h, L.zolo_set_pole_shard(h, self.shard[0], self.shard[1], uid))
         self.poles = shard_poles(self.r, *self.shard)
         if solve not in ("direct", "hybrid"):
             raise DomainError("solve must be 'direct' or 'hybrid'")

@@ -372,8 +372,17 @@ struct zolo_ctx {
   // pole sharding: this context factors the poles own[] of the design
   int shard_rank = 0, shard_size = 1;
   std::vector<int> own;
-  NcclComm* comm = nullptr;
-  DevMem wc;  // compacted partial G (all-reduced over the ranks)
+  Collective* coll = nullptr;  // the group's collectives (NCCL, or host-staged through a callback)
+  // Row-sharded Arnoldi (default with a communicator; ZOLO_ROW_SHARD=0: replicated, G all-reduced):
+  // rank g owns rows [g rb, min(ld, (g + 1) rb)) of every Krylov vector. A G application ends with
+  // a reduce-scatter of the ranks' partial sums over row blocks, the CGS2 inner products are
+  // all-reduced (n_active x (m + 1) scalars), and the next basis vector is all-gathered (every
+  // rank's poles need all of its rows): per iteration the bytes of one all-reduce, and the Arnoldi
+  // work divided by the ranks.
+  bool row_shard = false;
+  bool in_filter = false;  // inside apply_filter (the row-sharded layout applies; zolo_apply_g stays replicated)
+  int64_t rb = 0;
+  DevMem wc, wloc, vpack, vgath;  // blocked partial G | this rank's reduced block | basis block out / in
 
   size_t es() const { return cx ? 16 : 8; }
   int nloc() const { return static_cast<int>(own.size()); }
@@ -1046,14 +1055,40 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   c.maxit_cap = 0;  // GMRES state is sized per (ncap, maxit)
 }
 
-// w[:, act] = (rank 0: constant v) + the context's poles' terms; pole-sharded:
-// computed compacted, all-reduced over the ranks (one ncclAllReduce per G
-// application), then scattered -- every rank ends with the
-// same bits, so the replicated Arnoldi stays identical across ranks. Without a
-// communicator (nranks > 1, no unique id) the rank's partial sum is returned.
+// this rank's Krylov rows [r0, r1) (all rows unless row-sharded)
+inline int64_t row_lo(const zolo_ctx& c) { return c.row_shard ? std::min<int64_t>(c.geom.npad, c.shard_rank * c.rb) : 0; }
+inline int64_t row_hi(const zolo_ctx& c) {
+  return c.row_shard ? std::min<int64_t>(c.geom.npad, (c.shard_rank + 1) * c.rb) : c.geom.npad;
+}
+
+// w[:, act] = (rank 0: constant v) + the context's poles' terms (filter_engine.hpp:60-80).
+// Pole-sharded, row-sharded Arnoldi: written row-blocked, reduce-scattered over the ranks (each
+// rank receives its row block of G v, summed over all poles) and unpacked into w's local rows.
+// Pole-sharded, replicated Arnoldi: computed compacted, all-reduced, scattered -- every rank ends
+// with the same bits. Without a communicator (nranks > 1, no unique id) the rank's partial sum
+// is returned.
 void combine_g(zolo_ctx& c, const void* vsrc, const int* act, int na, std::vector<cd*>& xs, void* wdst) {
   const int64_t ld = c.geom.npad, n = ld;
   const bool sharded = c.shard_size > 1;
+  if (sharded && c.row_shard && c.in_filter) {
+    const int P = c.shard_size;
+    const int64_t rb = c.rb;
+    c.wc.ensure(c.es() * rb * P * std::max(na, 1));
+    c.wloc.ensure(c.es() * rb * std::max(na, 1));
+    if (c.cx)
+      Krylov<cd>::combine_blocked(c.st, ld, rb, P, c.local_constant(), reinterpret_cast<const cd*>(vsrc), act, na,
+                                  xs.data(), c.weights_d.as<cd>(), c.nloc(), c.wc.as<cd>());
+    else
+      Krylov<double>::combine_blocked(c.st, ld, rb, P, c.local_constant(), reinterpret_cast<const double*>(vsrc),
+                                      act, na, xs.data(), c.weights_d.as<cd>(), c.nloc(), c.wc.as<double>());
+    c.coll->reduce_scatter(c.wc.as<double>(), c.wloc.as<double>(), static_cast<size_t>(rb) * na * (c.es() / 8), c.st);
+    const int64_t r0 = row_lo(c), rows = row_hi(c) - r0;
+    if (c.cx)
+      Krylov<cd>::unpack_rows(c.st, c.wloc.as<cd>(), r0, rows, act, na, reinterpret_cast<cd*>(wdst), ld);
+    else
+      Krylov<double>::unpack_rows(c.st, c.wloc.as<double>(), r0, rows, act, na, reinterpret_cast<double*>(wdst), ld);
+    return;
+  }
   void* out = wdst;
   if (sharded) {
     c.wc.ensure(c.es() * ld * std::max(na, 1));
@@ -1066,7 +1101,7 @@ void combine_g(zolo_ctx& c, const void* vsrc, const int* act, int na, std::vecto
     Krylov<double>::combine(c.st, n, ld, c.local_constant(), reinterpret_cast<const double*>(vsrc), act, na,
                             xs.data(), c.weights_d.as<cd>(), c.nloc(), reinterpret_cast<double*>(out), sharded);
   if (!sharded) return;
-  if (c.comm) nccl_allreduce_sum(c.comm, c.wc.as<double>(), static_cast<size_t>(ld) * na * (c.es() / 8), c.st);
+  if (c.coll) c.coll->allreduce(c.wc.as<double>(), static_cast<size_t>(ld) * na * (c.es() / 8), c.st);
   if (c.cx)
     Krylov<cd>::scatter_cols(c.st, ld, c.wc.as<cd>(), act, na, reinterpret_cast<cd*>(wdst));
   else
@@ -1225,7 +1260,7 @@ void ensure_gmres(zolo_ctx& c, int maxit) {
   c.gdone.ensure(sizeof(int) * nv);
   c.gwnorm.ensure(sizeof(double) * nv);
   const int64_t nchunk = (c.geom.npad + CHUNK - 1) / CHUNK;
-  c.partial.ensure(2 * es * nv * nchunk * (maxit + 1) + 64);
+  c.partial.ensure(3 * es * nv * nchunk * (maxit + 1) + 64);
   c.hsave.ensure(es * nv * (maxit + 1));
   c.basis_ptrs.ensure(sizeof(void*) * (maxit + 1));
   c.maxit_cap = maxit;
@@ -1405,7 +1440,7 @@ void inner_gmres(zolo_ctx& c, int k, int na) {
     Krylov<cd>::scatter_cols(c.st, ld, c.xbuf[k]->as<cd>(), act, nai, c.hy_w.as<cd>());
     c.inner_solves += nai;
     c.hy_inner_its += nai;
-    Krylov<cd>::arnoldi(c.st, ld, ld, basis, it, c.hy_w.as<cd>(), act, nai, g, c.ipartial.as<double>(), nchunk,
+    Krylov<cd>::arnoldi(c.st, 0, ld, ld, basis, it, c.hy_w.as<cd>(), act, nai, g, c.ipartial.as<double>(),
                         c.ihsave.as<cd>());
     Krylov<cd>::least_squares(c.st, act, nai, it, g, c.ipartial.as<double>(), nchunk, c.hy_tol);
     if (it + 1 < maxit) Krylov<cd>::next_basis(c.st, n, ld, c.hy_w.as<cd>(), c.ibasis[it + 1]->as<cd>(), act, nai, g);
@@ -1475,7 +1510,7 @@ template <class S>
 int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
                       zolo_report* rep) {
   require(c.factored, "apply_filter: operator not factorized");
-  require(c.shard_size == 1 || c.comm, "apply_filter: a pole-sharded context needs its NCCL communicator");
+  require(c.shard_size == 1 || c.coll, "apply_filter: a pole-sharded context needs its communicator");
   // (the reference has no cap, gmres.hpp:98-101; the device Krylov kernels hold up to
   // KRYLOV_MAX basis vectors per column, krylov.cuh)
   require(gmres_max >= 1 && gmres_max <= KRYLOV_MAX,
@@ -1483,6 +1518,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   const int64_t n = c.n, ld = c.geom.npad;
   const int maxit = static_cast<int>(gmres_max);
   const int q = 2 * c.r;
+  if (c.row_shard) c.rb = ((ld + c.shard_size - 1) / c.shard_size + 31) / 32 * 32;
   ensure_workspace(c, ncols);
   ensure_gmres<S>(c, maxit);
   // basis pointers may predate a reallocation: refresh all
@@ -1511,7 +1547,6 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   for (int64_t k = 0; k < ncols; ++k)
     if (beta[k] != 0.0) active.push_back(static_cast<int>(k));
 
-  const int nchunk = static_cast<int>((ld + CHUNK - 1) / CHUNK);  // device rows incl. padding
   float trsm_ms = 0.0f, busy_ms = 0.0f;
   int trsm_launches = 0;
   int64_t launches = 4;
@@ -1531,8 +1566,10 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     ~LagGuard() {
       c.lag_done = nullptr;
       c.ev2_use = c.ev3_use = nullptr;
+      c.in_filter = false;
     }
   } lag_guard{c};
+  c.in_filter = true;
   c.lag_done = lag ? g.done : nullptr;
   cudaEvent_t ev_done[4], ev_t[4][2], ev_b[4][2];
   for (int p = 0; p < 4; ++p) {
@@ -1572,12 +1609,23 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     apply_g_device(c, vm, na, c.w.p);
     trsm_launches += 2;
     launches += 8 + (it + 1 < maxit ? 1 : 0);
-    Krylov<S>::arnoldi(c.st, ld, ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(), c.act_d.as<int>(), na, g,
-                       c.partial.as<double>(), nchunk, c.hsave.as<S>());
-    Krylov<S>::least_squares(c.st, c.act_d.as<int>(), na, it, g, c.partial.as<double>(), nchunk, tol);
+    const int nls = Krylov<S>::arnoldi(c.st, row_lo(c), row_hi(c), ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(),
+                                       c.act_d.as<int>(), na, g, c.partial.as<double>(), c.hsave.as<S>(),
+                                       c.row_shard ? c.coll : nullptr);
+    Krylov<S>::least_squares(c.st, c.act_d.as<int>(), na, it, g, c.partial.as<double>(), nls, tol);
     if (it + 1 < maxit) {
       S* vn = reinterpret_cast<S*>(basis_block(c, it + 1));
       Krylov<S>::next_basis(c.st, n, ld, c.w.as<S>(), vn, c.act_d.as<int>(), na, g);
+      if (c.row_shard) {  // every rank's poles need all rows of the next basis vector
+        const int64_t r0 = row_lo(c), rows = row_hi(c) - r0, rb = c.rb;
+        c.vpack.ensure(c.es() * rb * std::max(na, 1));
+        c.vgath.ensure(c.es() * rb * c.shard_size * std::max(na, 1));
+        CK(cudaMemsetAsync(c.vpack.p, 0, c.es() * rb * na, c.st));  // the last block's padding rows
+        Krylov<S>::pack_rows(c.st, vn, ld, r0, rows, c.act_d.as<int>(), na, c.vpack.as<S>());
+        c.coll->allgather(c.vpack.as<double>(), c.vgath.as<double>(), static_cast<size_t>(rb) * na * (c.es() / 8),
+                          c.st);
+        Krylov<S>::unpack_blocks(c.st, c.vgath.as<S>(), rb, c.shard_size, c.act_d.as<int>(), na, vn, ld);
+      }
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev_b[p][1], c.st));
@@ -1882,7 +1930,7 @@ int zolo_ctx_destroy(zolo_ctx* c) {
   DeviceScope scope(c);  // the context's device; the caller's is restored on return
   if (c->st) cudaStreamSynchronize(c->st);
   for (auto s : c->pole_streams) cudaStreamDestroy(s);
-  nccl_close(c->comm);
+  delete c->coll;
   if (c->act_h) cudaFreeHost(c->act_h);
   for (int q = 0; q < 4; ++q) {
     if (c->act_hq[q]) cudaFreeHost(c->act_hq[q]);
@@ -2090,24 +2138,41 @@ int zolo_nccl_unique_id(void* out) {
   }
 }
 
+namespace {
+void set_shard(zolo_ctx& c, int rank, int nranks, Collective* coll) {
+  require(nranks >= 1 && rank >= 0 && rank < nranks, "zolo_set_pole_shard: need 0 <= rank < nranks");
+  require(!c.hybrid || nranks == 1, "zolo_set_pole_shard: hybrid solve and pole sharding are exclusive");
+  delete c.coll;
+  c.coll = coll;
+  c.shard_rank = rank;
+  c.shard_size = nranks;
+  static const bool rows = env_int("ZOLO_ROW_SHARD", 1) != 0;
+  c.row_shard = coll && nranks > 1 && rows;
+  c.ncap = 0;
+  if (c.have_design) refresh_own(c);
+}
+}  // namespace
+
 int zolo_set_pole_shard(zolo_ctx* c, int rank, int nranks, const void* unique_id) {
   return guarded(c, [&] {
-    require(nranks >= 1 && rank >= 0 && rank < nranks, "zolo_set_pole_shard: need 0 <= rank < nranks");
-    require(!c->hybrid || nranks == 1, "zolo_set_pole_shard: hybrid solve and pole sharding are exclusive");
-    nccl_close(c->comm);
-    c->comm = nullptr;
-    c->shard_rank = rank;
-    c->shard_size = nranks;
     // a 1-rank communicator is legal: its all-reduce is the identity, which lets one GPU run the
     // in-library NCCL path end to end
+    Collective* coll = nullptr;
     if (unique_id) {
       try {
-        c->comm = nccl_open(unique_id, nranks, rank);
+        coll = nccl_collective(unique_id, nranks, rank);
       } catch (const std::exception& e) {
         throw ZoloError(ZOLO_ERR_CUDA, e.what());
       }
     }
-    if (c->have_design) refresh_own(*c);
+    set_shard(*c, rank, nranks, coll);
+  });
+}
+
+int zolo_set_pole_shard_host(zolo_ctx* c, int rank, int nranks, zolo_collective_fn fn, void* user) {
+  return guarded(c, [&] {
+    require(fn != nullptr, "zolo_set_pole_shard_host: callback missing");
+    set_shard(*c, rank, nranks, host_collective(fn, user, nranks, rank));
   });
 }
 
@@ -2142,7 +2207,8 @@ double bytes_per_column(zolo_ctx& c, int maxit) {
   const double crows = static_cast<double>(TILE) * std::max(c.sp_nslots, 1);
   const double nchunk = std::ceil(ld / CHUNK);
   double b = c.n * es + ld * (3 * es + 16 + 16.0 * nch + es * (maxit + 2)) + 16.0 * nch * crows;
-  b += es * (maxit + 1) * maxit + 16.0 * q * (maxit * maxit + 4.0 * maxit + 1) + 2 * es * nchunk * (maxit + 1);
+  b += es * (maxit + 1) * maxit + 16.0 * q * (maxit * maxit + 4.0 * maxit + 1) + 3 * es * nchunk * (maxit + 1);
+  if (c.row_shard) b += 3.0 * es * ld;  // blocked partial G, the local block, the gathered basis block
   if (c.hybrid) b += 16.0 * ld * (c.hy_max + 4) + 16.0 * (c.r - 1) * c.hy_max * c.hy_max;
   if (c.refine) b += 16.0 * nch * ld;
   return b;
@@ -2150,7 +2216,7 @@ double bytes_per_column(zolo_ctx& c, int maxit) {
 
 void release_workspace(zolo_ctx& c) {
   for (DevMem* m : {&c.vin_orig, &c.vin, &c.vout, &c.w, &c.bbuf, &c.gH, &c.gR, &c.gG, &c.gROT, &c.gY, &c.gZ,
-                    &c.partial, &c.hsave, &c.wc, &c.hy_w, &c.iH, &c.iR, &c.iG, &c.iROT, &c.iY, &c.iZ, &c.ipartial,
+                    &c.partial, &c.hsave, &c.wc, &c.wloc, &c.vpack, &c.vgath, &c.hy_w, &c.iH, &c.iR, &c.iG, &c.iROT, &c.iY, &c.iZ, &c.ipartial,
                     &c.ihsave})
     m->release();
   for (auto& m : c.xbuf) m->release();

@@ -257,12 +257,21 @@ struct XPtrs {
 };
 
 // filter_engine.hpp:60-80
+// rb > 0: the row-blocked reduce-scatter layout over nblk blocks (rows >= ld written as zeros)
 template <class S>
 __global__ void combine_kernel(int64_t ld, double c0, const S* v, const int* act, XPtrs xs, const cd* weights, int r,
-                               S* w, int compact) {
+                               S* w, int compact, int64_t rb, int nblk) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int a = blockIdx.y;
-  if (t >= ld) return;
+  if (rb > 0) {
+    if (t >= rb * nblk) return;
+    if (t >= ld) {
+      w[(t / rb) * rb * gridDim.y + a * rb + t % rb] = szero(S());
+      return;
+    }
+  } else if (t >= ld) {
+    return;
+  }
   const int64_t col = act[a];
   S acc = sscale(v[t + col * ld], c0);
   const int64_t off = t + a * ld;
@@ -279,7 +288,10 @@ __global__ void combine_kernel(int64_t ld, double c0, const S* v, const int* act
       acc = cadd(acc, cadd(cmul(wp, x), cmul(cconj(wp), xa)));
     }
   }
-  w[t + (compact ? a : col) * ld] = acc;
+  if (rb > 0)
+    w[(t / rb) * rb * gridDim.y + a * rb + t % rb] = acc;
+  else
+    w[t + (compact ? a : col) * ld] = acc;
 }
 
 // w[:, act[a]] = wc[:, a] (pole-sharded G: the all-reduced compacted partial sums)
@@ -293,14 +305,14 @@ __global__ void scatter_cols_kernel(int64_t ld, const S* wc, const int* act, S* 
 // ---- CGS2 Arnoldi -------------------------------------------------------
 // K1: partial dots <V_i, w> over a row chunk.
 template <class S>
-__global__ void __launch_bounds__(RT) dots_kernel(int64_t n, int64_t ld, S* const* basis, int m, const S* w,
-                                                  const int* act, S* partial, int nchunk, int hstride,
+__global__ void __launch_bounds__(RT) dots_kernel(int64_t r0, int64_t n, int64_t ld, S* const* basis, int m,
+                                                  const S* w, const int* act, S* partial, int nchunk, int hstride,
                                                   const int* done) {
   __shared__ S red[RT / 32][KMAX];
   const int a = blockIdx.x, chunk = blockIdx.y;
   const int64_t col = act[a];
   if (done[col]) return;  // converged in an earlier iteration (lagged active list)
-  const int64_t base = static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
+  const int64_t base = r0 + static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
   S wr[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
@@ -329,8 +341,8 @@ __global__ void __launch_bounds__(RT) dots_kernel(int64_t n, int64_t ld, S* cons
 // K2/K3: h = sum_chunks partial_in; w -= V h; then either dots with the new w
 // (partial_out as S) or the squared norm (norm_out as double).
 template <class S, bool DOTS>
-__global__ void __launch_bounds__(RT) update_kernel(int64_t n, int64_t ld, S* const* basis, int m, S* w,
-                                                    const int* act, const S* partial_in, S* partial_out,
+__global__ void __launch_bounds__(RT) update_kernel(int64_t r0, int64_t n, int64_t ld, S* const* basis, int m, S* w,
+                                                    const int* act, const S* partial_in, int nin, S* partial_out,
                                                     double* norm_out, int nchunk, int hstride, S* hsave,
                                                     void* Hmat, int maxit, const int* done) {
   __shared__ S hs[KMAX];
@@ -340,7 +352,7 @@ __global__ void __launch_bounds__(RT) update_kernel(int64_t n, int64_t ld, S* co
   if (done[col]) return;
   if (threadIdx.x <= m) {
     S tot = szero(S());
-    for (int c = 0; c < nchunk; ++c) tot = sadd(tot, partial_in[(static_cast<int64_t>(a) * nchunk + c) * hstride + threadIdx.x]);
+    for (int c = 0; c < nin; ++c) tot = sadd(tot, partial_in[(static_cast<int64_t>(a) * nin + c) * hstride + threadIdx.x]);
     hs[threadIdx.x] = tot;
     if (chunk == 0) {
       if (DOTS) {
@@ -354,7 +366,7 @@ __global__ void __launch_bounds__(RT) update_kernel(int64_t n, int64_t ld, S* co
     }
   }
   __syncthreads();
-  const int64_t base = static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
+  const int64_t base = r0 + static_cast<int64_t>(chunk) * CHUNK + threadIdx.x;
   S wr[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
@@ -407,6 +419,43 @@ __global__ void __launch_bounds__(RT) update_kernel(int64_t n, int64_t ld, S* co
       norm_out[static_cast<int64_t>(a) * nchunk + chunk] = tot;
     }
   }
+}
+
+// row-sharded Arnoldi: sum the per-chunk partials of every active column in fixed chunk order
+// (cnt entries each: the m + 1 inner products, or 1 squared norm), one chunk per column out
+template <class T>
+__global__ void reduce_chunks_kernel(const T* partial, int nchunk, int stride, int cnt, const int* act,
+                                     const int* done, T* out) {
+  const int a = blockIdx.x;
+  if (done[act[a]]) return;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    T s = szero(T());
+    for (int c = 0; c < nchunk; ++c) s = sadd(s, partial[(static_cast<int64_t>(a) * nchunk + c) * stride + i]);
+    out[static_cast<int64_t>(a) * stride + i] = s;
+  }
+}
+
+template <class S>
+__global__ void pack_rows_kernel(const S* w, int64_t ld, int64_t r0, int64_t rows, const int* act, S* blk) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int a = blockIdx.y;
+  if (t < rows) blk[t + a * rows] = w[r0 + t + static_cast<int64_t>(act[a]) * ld];
+}
+
+template <class S>
+__global__ void unpack_rows_kernel(const S* blk, int64_t r0, int64_t rows, const int* act, S* w, int64_t ld) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int a = blockIdx.y;
+  if (t < rows) w[r0 + t + static_cast<int64_t>(act[a]) * ld] = blk[t + a * rows];
+}
+
+template <class S>
+__global__ void unpack_blocks_kernel(const S* blocks, int64_t rb, int na, const int* act, S* w, int64_t ld) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // global row
+  const int a = blockIdx.y;
+  if (t >= ld) return;
+  const int64_t p = t / rb;
+  w[t + static_cast<int64_t>(act[a]) * ld] = blocks[(p * na + a) * rb + (t - p * rb)];
 }
 
 __global__ void gmres_init_kernel(GmresDev g) {
@@ -677,26 +726,74 @@ void Krylov<S>::combine(cudaStream_t st, int64_t n, int64_t ld, double c0, const
   const int np = sizeof(S) == sizeof(double) ? r : 2 * r;
   for (int i = 0; i < np; ++i) p.p[i] = xs[i];
   if (na > 0)
-    combine_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, c0, v, act, p, weights, r, w, compact);
+    combine_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, c0, v, act, p, weights, r, w, compact, 0, 1);
+}
+template <class S>
+void Krylov<S>::combine_blocked(cudaStream_t st, int64_t ld, int64_t rb, int nblk, double c0, const S* v,
+                                const int* act, int na, cd* const* xs, const cd* weights, int r, S* out) {
+  XPtrs p;
+  const int np = sizeof(S) == sizeof(double) ? r : 2 * r;
+  for (int i = 0; i < np; ++i) p.p[i] = xs[i];
+  if (na > 0)
+    combine_kernel<S><<<dim3(blocks_for(rb * nblk, 256), na), 256, 0, st>>>(ld, c0, v, act, p, weights, r, out, 0,
+                                                                          rb, nblk);
+}
+template <class S>
+void Krylov<S>::pack_rows(cudaStream_t st, const S* w, int64_t ld, int64_t r0, int64_t rows, const int* act, int na,
+                          S* blk) {
+  if (na > 0 && rows > 0) pack_rows_kernel<S><<<dim3(blocks_for(rows, 256), na), 256, 0, st>>>(w, ld, r0, rows, act, blk);
+}
+template <class S>
+void Krylov<S>::unpack_rows(cudaStream_t st, const S* blk, int64_t r0, int64_t rows, const int* act, int na, S* w,
+                            int64_t ld) {
+  if (na > 0 && rows > 0)
+    unpack_rows_kernel<S><<<dim3(blocks_for(rows, 256), na), 256, 0, st>>>(blk, r0, rows, act, w, ld);
+}
+template <class S>
+void Krylov<S>::unpack_blocks(cudaStream_t st, const S* blocks, int64_t rb, int nblk, const int* act, int na, S* w,
+                              int64_t ld) {
+  if (na > 0) unpack_blocks_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(blocks, rb, na, act, w, ld);
 }
 template <class S>
 void Krylov<S>::scatter_cols(cudaStream_t st, int64_t ld, const S* wc, const int* act, int na, S* w) {
   if (na > 0) scatter_cols_kernel<S><<<dim3(blocks_for(ld, 256), na), 256, 0, st>>>(ld, wc, act, w);
 }
 template <class S>
-void Krylov<S>::arnoldi(cudaStream_t st, int64_t n, int64_t ld, S* const* d_basis, int m, S* w, const int* act,
-                        int na, GmresDev g, double* partial, int nchunk, S* hsave) {
-  if (na <= 0) return;
+int Krylov<S>::arnoldi(cudaStream_t st, int64_t r0, int64_t r1, int64_t ld, S* const* d_basis, int m, S* w,
+                       const int* act, int na, GmresDev g, double* partial, S* hsave, Collective* coll) {
+  const int nchunk = static_cast<int>(std::max<int64_t>(1, (r1 - r0 + CHUNK - 1) / CHUNK));
+  if (na <= 0) return coll ? 1 : nchunk;
   const int hstride = g.maxit + 1;
   S* p1 = reinterpret_cast<S*>(partial);
   S* p2 = p1 + static_cast<int64_t>(na) * nchunk * hstride;
   double* pn = reinterpret_cast<double*>(p1);  // norm partials reuse p1 after K2
   const dim3 grid(na, nchunk);
-  dots_kernel<S><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p1, nchunk, hstride, g.done);
-  update_kernel<S, true><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p1, p2, nullptr, nchunk, hstride, hsave,
-                                              g.H, g.maxit, g.done);
-  update_kernel<S, false><<<grid, RT, 0, st>>>(n, ld, d_basis, m, w, act, p2, nullptr, pn, nchunk, hstride, hsave,
-                                               g.H, g.maxit, g.done);
+  if (!coll) {
+    dots_kernel<S><<<grid, RT, 0, st>>>(r0, r1, ld, d_basis, m, w, act, p1, nchunk, hstride, g.done);
+    update_kernel<S, true><<<grid, RT, 0, st>>>(r0, r1, ld, d_basis, m, w, act, p1, nchunk, p2, nullptr, nchunk,
+                                                hstride, hsave, g.H, g.maxit, g.done);
+    update_kernel<S, false><<<grid, RT, 0, st>>>(r0, r1, ld, d_basis, m, w, act, p2, nchunk, nullptr, pn, nchunk,
+                                                 hstride, hsave, g.H, g.maxit, g.done);
+    return nchunk;
+  }
+  // row-sharded: local chunk partials -> one partial per column -> all-reduced over the ranks (the
+  // done columns' slots carry stale values on every rank alike and are never read)
+  const size_t words = static_cast<size_t>(na) * hstride * (sizeof(S) / sizeof(double));
+  S* red = p2 + static_cast<int64_t>(na) * nchunk * hstride;
+  dots_kernel<S><<<grid, RT, 0, st>>>(r0, r1, ld, d_basis, m, w, act, p1, nchunk, hstride, g.done);
+  reduce_chunks_kernel<S><<<na, 64, 0, st>>>(p1, nchunk, hstride, m + 1, act, g.done, red);
+  coll->allreduce(reinterpret_cast<double*>(red), words, st);
+  update_kernel<S, true><<<grid, RT, 0, st>>>(r0, r1, ld, d_basis, m, w, act, red, 1, p2, nullptr, nchunk, hstride,
+                                              hsave, g.H, g.maxit, g.done);
+  reduce_chunks_kernel<S><<<na, 64, 0, st>>>(p2, nchunk, hstride, m + 1, act, g.done, red);
+  coll->allreduce(reinterpret_cast<double*>(red), words, st);
+  update_kernel<S, false><<<grid, RT, 0, st>>>(r0, r1, ld, d_basis, m, w, act, red, 1, nullptr, pn, nchunk, hstride,
+                                               hsave, g.H, g.maxit, g.done);
+  double* nred = reinterpret_cast<double*>(red);
+  reduce_chunks_kernel<double><<<na, 32, 0, st>>>(pn, nchunk, 1, 1, act, g.done, nred);
+  coll->allreduce(nred, static_cast<size_t>(na), st);
+  cudaMemcpyAsync(pn, nred, sizeof(double) * na, cudaMemcpyDeviceToDevice, st);
+  return 1;
 }
 template <class S>
 void Krylov<S>::least_squares(cudaStream_t st, const int* act, int na, int m, GmresDev g, const double* partial,

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "shard.hpp"
 
 namespace zolo {
 
@@ -45,11 +46,29 @@ struct Krylov {
   // compact: written to w[:, a] instead
   static void combine(cudaStream_t st, int64_t n, int64_t ld, double c0, const S* v, const int* act, int na,
                       cd* const* xs, const cd* weights, int r, S* w, bool compact = false);
+  // the same combine into the row-blocked layout of a reduce-scatter over nblk ranks: row t of
+  // column a at out[(t / rb) rb na + a rb + t % rb]; rows ld .. nblk rb - 1 are zero
+  static void combine_blocked(cudaStream_t st, int64_t ld, int64_t rb, int nblk, double c0, const S* v,
+                              const int* act, int na, cd* const* xs, const cd* weights, int r, S* out);
+  // blk (rows x na, column-major) <-> rows [r0, r0 + rows) of the columns act of w (ld x ncap)
+  static void pack_rows(cudaStream_t st, const S* w, int64_t ld, int64_t r0, int64_t rows, const int* act, int na,
+                        S* blk);
+  static void unpack_rows(cudaStream_t st, const S* blk, int64_t r0, int64_t rows, const int* act, int na, S* w,
+                          int64_t ld);
+  // allgathered blocks (nblk x (rb x na)) -> rows [p rb, min(ld, (p + 1) rb)) of the columns act of w
+  static void unpack_blocks(cudaStream_t st, const S* blocks, int64_t rb, int nblk, const int* act, int na, S* w,
+                            int64_t ld);
   // w[:, act[a]] = wc[:, a]
   static void scatter_cols(cudaStream_t st, int64_t ld, const S* wc, const int* act, int na, S* w);
-  // CGS2 Arnoldi step against basis V_0..V_m (device pointer array)
-  static void arnoldi(cudaStream_t st, int64_t n, int64_t ld, S* const* d_basis, int m, S* w, const int* act,
-                      int na, GmresDev g, double* partial, int nchunk, S* hsave);
+  // CGS2 Arnoldi step against basis V_0..V_m (device pointer array) over the rows [r0, r1) of w
+  // (nchunk = ceil((r1 - r0) / CHUNK) row chunks). coll == nullptr: the rows are all of them, the
+  // chunk partial sums are reduced in fixed order inside the kernels. coll != nullptr (row-sharded
+  // pole groups): [r0, r1) is this rank's row block; every inner product is reduced over the local
+  // chunks and all-reduced over the ranks (n_active x (m + 1) scalars per pass), so all ranks hold
+  // the same H; afterwards partial holds the all-reduced squared norms as ONE chunk per column.
+  // Returns the chunk count least_squares reads.
+  static int arnoldi(cudaStream_t st, int64_t r0, int64_t r1, int64_t ld, S* const* d_basis, int m, S* w,
+                     const int* act, int na, GmresDev g, double* partial, S* hsave, Collective* coll = nullptr);
   // incremental shifted Givens LS + freeze / completion bookkeeping
   static void least_squares(cudaStream_t st, const int* act, int na, int m, GmresDev g, const double* partial,
                             int nchunk, double tol);

@@ -106,3 +106,97 @@ def test_gloo_world2_pole_and_column_sharding(case, tmp_path):
     assert np.abs(gv - full).max() <= 1e-12 * max(1.0, np.abs(full).max())
     y_full = op.apply_filter(v)["y"]
     assert (out["y"] == y_full).all()  # columns are independent: bitwise
+
+
+def _coll_worker(rank, world, port, out_dir):
+    import ctypes as C
+    import sys
+
+    import torch.distributed as dist
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, os.path.dirname(here))
+    from paper_1701_08935_b200 import sharding
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fn = sharding.gloo_collective()
+        cnt = 5
+        res = {}
+        # the three operations exactly as the library calls them (include/zolo_b200.h ZOLO_COLL_*)
+        a = np.arange(cnt, dtype=np.float64) + 10.0 * rank
+        assert fn(0, a.ctypes.data_as(C.POINTER(C.c_double)), cnt, None) == 0
+        res["allreduce"] = a.copy()
+        b = np.arange(world * cnt, dtype=np.float64) * (rank + 1)
+        assert fn(1, b.ctypes.data_as(C.POINTER(C.c_double)), cnt, None) == 0
+        res["reduce_scatter"] = b[:cnt].copy()
+        c = np.zeros(world * cnt)
+        c[rank * cnt:(rank + 1) * cnt] = rank + 0.5
+        assert fn(2, c.ctypes.data_as(C.POINTER(C.c_double)), cnt, None) == 0
+        res["allgather"] = c.copy()
+        np.savez(os.path.join(out_dir, f"coll{rank}.npz"), **res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_collective_callback_world2(tmp_path):
+    """sharding.gloo_collective: the host-staged collective the library calls through
+    zolo_set_pole_shard_host, driven with the library's buffer conventions over gloo."""
+    import torch.multiprocessing as mp
+
+    world, cnt = 2, 5
+    mp.spawn(_coll_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for rank in range(world):
+        d = np.load(tmp_path / f"coll{rank}.npz")
+        assert (d["allreduce"] == sum(np.arange(cnt) + 10.0 * q for q in range(world))).all()
+        full = sum(np.arange(world * cnt, dtype=np.float64) * (q + 1) for q in range(world))
+        assert (d["reduce_scatter"] == full[rank * cnt:(rank + 1) * cnt]).all()
+        assert (d["allgather"] == np.repeat(np.arange(world) + 0.5, cnt)).all()
+
+
+def test_thread_group_collectives():
+    """sharding.ThreadGroup (ranks as threads of one process, the GPU tests' pole groups):
+    every rank gets the same fixed-order sums."""
+    import ctypes as C
+    import threading
+
+    from paper_1701_08935_b200.sharding import ThreadGroup
+
+    world, cnt = 3, 4
+    grp = ThreadGroup(world)
+    out = {}
+
+    def run(rank):
+        fn = grp.callback(rank)
+        a = np.full(cnt, 0.1 * (rank + 1))
+        fn(0, a.ctypes.data_as(C.POINTER(C.c_double)), cnt, None)
+        b = np.arange(world * cnt, dtype=np.float64) + rank
+        fn(1, b.ctypes.data_as(C.POINTER(C.c_double)), cnt, None)
+        c = np.zeros(world * cnt)
+        c[rank * cnt:(rank + 1) * cnt] = rank
+        fn(2, c.ctypes.data_as(C.POINTER(C.c_double)), cnt, None)
+        out[rank] = (a, b[:cnt], c)
+
+    ts = [threading.Thread(target=run, args=(q,)) for q in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for rank in range(world):
+        a, b, c = out[rank]
+        assert (a == out[0][0]).all()  # bitwise identical on every rank
+        assert np.allclose(a, 0.1 + 0.2 + 0.3)
+        full = sum(np.arange(world * cnt, dtype=np.float64) + q for q in range(world))
+        assert (b == full[rank * cnt:(rank + 1) * cnt]).all()
+        assert (c == np.repeat(np.arange(world, dtype=np.float64), cnt)).all()
+
+
+def test_grid_groups():
+    from paper_1701_08935_b200.sharding import grid_groups
+
+    assert grid_groups(8, 2) == [[0, 1], [2, 3], [4, 5], [6, 7]]
+    assert grid_groups(8, 8) == [list(range(8))]
+    with pytest.raises(ValueError):
+        grid_groups(6, 4)
