@@ -434,10 +434,10 @@ def main():
     # roofline of the dominant kernel (the DAG-scheduled block-sparse triangular sweeps); per G
     # application, per column, per pole and per solve (P = 2 for complex pencils: solve + adjoint):
     # forward + backward sweep over the off-diagonal tiles plus the diagonal-block inverse products
-    # = 2 (ntiles + nb) complex 32x32 tile-column products; of their 1024 entries per tile the DMMA
-    # loops execute those in unmasked 8x4 blocks (sweep_profile executed_entries) at 8 flops per
-    # complex MAC -- the executed tensor work, the basis of `achieved`; the scalar fill (nonzero
-    # entries) is the useful share of it
+    # = 2 (ntiles + nb) complex 32x32 tile-column products. ALGORITHMIC flops (SURVEY.md §8(d):
+    # 8 flops per complex MAC x nnz of the factors x n_b) count the nonzero entries of those tiles
+    # (sweep_profile nonzero_entries, the scalar fill); the kernel executes the entries of the
+    # unmasked 8x4 blocks (executed_entries) with 3 real DMMAs per complex MAC (3M, mma.cuh).
     peaks = load_peaks()
     chains_per_pole = 2 if cx else 1
     tile_products = 2 * (sp["offdiag_tiles"] + sp["block_rows"])
@@ -447,7 +447,9 @@ def main():
     units_solved = opapps * len(op.poles) * chains_per_pole  # column solves, this rank, K steps
     stored_flops = units_solved * stored_entries * 8.0
     trsm_s = trsm_ms * 1e-3
-    achieved = stored_flops * frac_exec / trsm_s / 1e12 if trsm_ms > 0 else 0.0
+    achieved = stored_flops * frac_nz / trsm_s / 1e12 if trsm_ms > 0 else 0.0  # algorithmic (scalar fill)
+    # real flops the FP64 pipe executes: 3 DMMAs (6 flops) per complex MAC of the executed entries
+    pipe_flops = units_solved * sp["executed_entries"] * 6.0
     peak = peaks.get("fp64_tflops")
     traffic, traffic_src = load_traffic(args.config)
     line = {
@@ -472,13 +474,13 @@ def main():
                      "traffic_source": traffic_src or "no ncu capture of this config committed (profiles/)",
                      "peak_source": "measured FP64 tensor pipe (tools/fp64_peak.cu mma.sync.m8n8k4.f64, "
                                     "profiles/fp64_peak_r01.json; MEASURED_PEAKS.json has no FP64 figure)",
-                     "algorithmic": "8 flops per complex MAC x factor entries inside the unmasked 8x4 blocks "
-                                    "of the sweep tiles (off-diagonal L and U tiles + diagonal-block inverses) "
-                                    "per column per pole per solve per G application: the DMMA work executed",
+                     "algorithmic": "8 flops per complex MAC x nonzero entries of the sweep tiles (off-diagonal "
+                                    "L and U tiles + diagonal-block inverses: the scalar fill of the factors) per "
+                                    "column per pole per solve per G application (SURVEY.md §8(d) flops_G)",
                      "stored_entries_per_pole_solve": stored_entries,
                      "executed_fraction": frac_exec, "scalar_fill_fraction": frac_nz,
                      "achieved_stored_tiles": stored_flops / trsm_s / 1e12 if trsm_ms > 0 else None,
-                     "achieved_scalar_fill": stored_flops * frac_nz / trsm_s / 1e12 if trsm_ms > 0 else None,
+                     "fp64_pipe_tflops_executed": pipe_flops / trsm_s / 1e12 if trsm_ms > 0 else None,
                      "trsm_share_of_step": trsm_ms / total_ms if total_ms else None,
                      "trsm_launches": trsm_launches},
         "clocks": clk,

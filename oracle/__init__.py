@@ -106,6 +106,35 @@ class Reference(_Lib):
         self._check(self.lib.zr_eval_scalar(_ptr(g), C.c_int(r), _I64(x.size), _ptr(x), _ptr(gv), _ptr(fv)))
         return gv, fv
 
+    def read_mm(self, path):
+        """read_matrix_market through the reference: (n, (rp, ci, vals), is_complex)."""
+        n, nnz = _I64(0), _I64(0)
+        cx = C.c_int(0)
+        p = str(path).encode()
+        self._check(self.lib.zr_read_mm(p, C.byref(n), C.byref(nnz), C.byref(cx), None, None, None))
+        rp = np.zeros(n.value + 1, dtype=np.int64)
+        ci = np.zeros(nnz.value, dtype=np.int64)
+        v = np.zeros(nnz.value, dtype=np.complex128 if cx.value else np.float64)
+        self._check(self.lib.zr_read_mm(p, C.byref(n), C.byref(nnz), C.byref(cx), _ptr(rp), _ptr(ci), _ptr(v)))
+        return int(n.value), (rp, ci, v), bool(cx.value)
+
+    def write_mm(self, path, n, csr, cx):
+        rp = np.ascontiguousarray(csr[0], dtype=np.int64)
+        ci = np.ascontiguousarray(csr[1], dtype=np.int64)
+        v = np.ascontiguousarray(csr[2], dtype=np.complex128 if cx else np.float64)
+        self._check(self.lib.zr_write_mm(str(path).encode(), C.c_int(int(cx)), _I64(n), _ptr(rp), _ptr(ci), _ptr(v)))
+
+    def write_eigvec(self, path, x):
+        cx = np.iscomplexobj(x)
+        x = _as_f(x, cx)
+        self._check(self.lib.zr_write_eigvec(str(path).encode(), C.c_int(int(cx)), _I64(x.shape[0]), _I64(x.shape[1]),
+                                             _ptr(x)))
+
+    def read_eigvec(self, path, n, k, cx):
+        x = np.zeros((n, k), dtype=np.complex128 if cx else np.float64, order="F")
+        self._check(self.lib.zr_read_eigvec(str(path).encode(), C.c_int(int(cx)), _I64(n), _I64(k), _ptr(x)))
+        return x
+
     def uniform_stream(self, seed, n):
         out = np.zeros(int(n))
         self._check(self.lib.zr_uniform_stream(C.c_uint64(seed), _I64(n), _ptr(out)))

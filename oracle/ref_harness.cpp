@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "zoloeig/zoloeig.hpp"
+#include "zoloeig/serialize.hpp"  // needs <json.hpp> (nlohmann 3.11.3, see oracle/Makefile)
 
 using namespace zoloeig;
 
@@ -179,6 +180,72 @@ int zr_uniform_stream(uint64_t seed, int64_t n, double* out) {
   return guarded([&] {
     std::mt19937_64 gen(seed);
     for (int64_t i = 0; i < n; ++i) out[i] = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+  });
+}
+
+/// read_matrix_market (matrix_market.hpp:106-159): pass 1 (rp == nullptr) returns n, nnz and
+/// whether the file is complex; pass 2 fills the full-pattern CSR (values interleaved if complex).
+int zr_read_mm(const char* path, int64_t* n, int64_t* nnz, int* cx, int64_t* rp, int64_t* ci, double* v) {
+  return guarded([&] {
+    const MatrixMarketInfo info = probe_matrix_market(path);
+    *cx = info.complex_field ? 1 : 0;
+    const auto fill = [&](auto tag) {
+      using S = decltype(tag);
+      const SparseHermitian<S> m = read_matrix_market<S>(path);
+      *n = static_cast<int64_t>(m.n);
+      *nnz = static_cast<int64_t>(m.values.size());
+      if (!rp) return;
+      for (std::size_t i = 0; i <= m.n; ++i) rp[i] = static_cast<int64_t>(m.row_offsets[i]);
+      for (std::size_t k = 0; k < m.values.size(); ++k) {
+        ci[k] = static_cast<int64_t>(m.col_indices[k]);
+        if constexpr (is_complex_v<S>) {
+          v[2 * k] = m.values[k].real();
+          v[2 * k + 1] = m.values[k].imag();
+        } else {
+          v[k] = m.values[k];
+        }
+      }
+    };
+    if (*cx)
+      fill(Complex{});
+    else
+      fill(double{});
+  });
+}
+
+/// write_matrix_market (matrix_market.hpp:163-189) of a full-pattern CSR.
+int zr_write_mm(const char* path, int cx, int64_t n, const int64_t* rp, const int64_t* ci, const double* v) {
+  return guarded([&] {
+    if (cx)
+      write_matrix_market<Complex>(path, make_csr<Complex>(n, rp, ci, v));
+    else
+      write_matrix_market<double>(path, make_csr<double>(n, rp, ci, v));
+  });
+}
+
+/// write_eigvec_binary / read_eigvec_binary (serialize.hpp:108-142), n x k column-major.
+int zr_write_eigvec(const char* path, int cx, int64_t n, int64_t k, const double* x) {
+  return guarded([&] {
+    if (cx)
+      write_eigvec_binary(path, load_block<Complex>(n, k, x));
+    else
+      write_eigvec_binary(path, load_block<double>(n, k, x));
+  });
+}
+
+int zr_read_eigvec(const char* path, int cx, int64_t n, int64_t k, double* x) {
+  return guarded([&] {
+    const auto run = [&](auto tag) {
+      using S = decltype(tag);
+      const Matrix<S> m = read_eigvec_binary<S>(path);
+      if (static_cast<int64_t>(m.rows()) != n || static_cast<int64_t>(m.cols()) != k)
+        throw DomainError("eigenvector block shape mismatch");
+      store_block(m, x);
+    };
+    if (cx)
+      run(Complex{});
+    else
+      run(double{});
   });
 }
 

@@ -1084,9 +1084,10 @@ void combine_g(zolo_ctx& c, const void* vsrc, const int* act, int na, std::vecto
     c.coll->reduce_scatter(c.wc.as<double>(), c.wloc.as<double>(), static_cast<size_t>(rb) * na * (c.es() / 8), c.st);
     const int64_t r0 = row_lo(c), rows = row_hi(c) - r0;
     if (c.cx)
-      Krylov<cd>::unpack_rows(c.st, c.wloc.as<cd>(), r0, rows, act, na, reinterpret_cast<cd*>(wdst), ld);
+      Krylov<cd>::unpack_rows(c.st, c.wloc.as<cd>(), r0, rows, rb, act, na, reinterpret_cast<cd*>(wdst), ld);
     else
-      Krylov<double>::unpack_rows(c.st, c.wloc.as<double>(), r0, rows, act, na, reinterpret_cast<double*>(wdst), ld);
+      Krylov<double>::unpack_rows(c.st, c.wloc.as<double>(), r0, rows, rb, act, na, reinterpret_cast<double*>(wdst),
+                                  ld);
     return;
   }
   void* out = wdst;
@@ -1621,7 +1622,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
         c.vpack.ensure(c.es() * rb * std::max(na, 1));
         c.vgath.ensure(c.es() * rb * c.shard_size * std::max(na, 1));
         CK(cudaMemsetAsync(c.vpack.p, 0, c.es() * rb * na, c.st));  // the last block's padding rows
-        Krylov<S>::pack_rows(c.st, vn, ld, r0, rows, c.act_d.as<int>(), na, c.vpack.as<S>());
+        Krylov<S>::pack_rows(c.st, vn, ld, r0, rows, rb, c.act_d.as<int>(), na, c.vpack.as<S>());
         c.coll->allgather(c.vpack.as<double>(), c.vgath.as<double>(), static_cast<size_t>(rb) * na * (c.es() / 8),
                           c.st);
         Krylov<S>::unpack_blocks(c.st, c.vgath.as<S>(), rb, c.shard_size, c.act_d.as<int>(), na, vn, ld);

@@ -435,18 +435,21 @@ __global__ void reduce_chunks_kernel(const T* partial, int nchunk, int stride, i
   }
 }
 
+// blk: column stride `stride` (>= rows; the reduce-scatter / all-gather block height)
 template <class S>
-__global__ void pack_rows_kernel(const S* w, int64_t ld, int64_t r0, int64_t rows, const int* act, S* blk) {
+__global__ void pack_rows_kernel(const S* w, int64_t ld, int64_t r0, int64_t rows, int64_t stride, const int* act,
+                                 S* blk) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int a = blockIdx.y;
-  if (t < rows) blk[t + a * rows] = w[r0 + t + static_cast<int64_t>(act[a]) * ld];
+  if (t < rows) blk[t + a * stride] = w[r0 + t + static_cast<int64_t>(act[a]) * ld];
 }
 
 template <class S>
-__global__ void unpack_rows_kernel(const S* blk, int64_t r0, int64_t rows, const int* act, S* w, int64_t ld) {
+__global__ void unpack_rows_kernel(const S* blk, int64_t r0, int64_t rows, int64_t stride, const int* act, S* w,
+                                   int64_t ld) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int a = blockIdx.y;
-  if (t < rows) w[r0 + t + static_cast<int64_t>(act[a]) * ld] = blk[t + a * rows];
+  if (t < rows) w[r0 + t + static_cast<int64_t>(act[a]) * ld] = blk[t + a * stride];
 }
 
 template <class S>
@@ -739,15 +742,16 @@ void Krylov<S>::combine_blocked(cudaStream_t st, int64_t ld, int64_t rb, int nbl
                                                                           rb, nblk);
 }
 template <class S>
-void Krylov<S>::pack_rows(cudaStream_t st, const S* w, int64_t ld, int64_t r0, int64_t rows, const int* act, int na,
-                          S* blk) {
-  if (na > 0 && rows > 0) pack_rows_kernel<S><<<dim3(blocks_for(rows, 256), na), 256, 0, st>>>(w, ld, r0, rows, act, blk);
+void Krylov<S>::pack_rows(cudaStream_t st, const S* w, int64_t ld, int64_t r0, int64_t rows, int64_t stride,
+                          const int* act, int na, S* blk) {
+  if (na > 0 && rows > 0)
+    pack_rows_kernel<S><<<dim3(blocks_for(rows, 256), na), 256, 0, st>>>(w, ld, r0, rows, stride, act, blk);
 }
 template <class S>
-void Krylov<S>::unpack_rows(cudaStream_t st, const S* blk, int64_t r0, int64_t rows, const int* act, int na, S* w,
-                            int64_t ld) {
+void Krylov<S>::unpack_rows(cudaStream_t st, const S* blk, int64_t r0, int64_t rows, int64_t stride, const int* act,
+                            int na, S* w, int64_t ld) {
   if (na > 0 && rows > 0)
-    unpack_rows_kernel<S><<<dim3(blocks_for(rows, 256), na), 256, 0, st>>>(blk, r0, rows, act, w, ld);
+    unpack_rows_kernel<S><<<dim3(blocks_for(rows, 256), na), 256, 0, st>>>(blk, r0, rows, stride, act, w, ld);
 }
 template <class S>
 void Krylov<S>::unpack_blocks(cudaStream_t st, const S* blocks, int64_t rb, int nblk, const int* act, int na, S* w,

@@ -50,11 +50,11 @@ struct Krylov {
   // column a at out[(t / rb) rb na + a rb + t % rb]; rows ld .. nblk rb - 1 are zero
   static void combine_blocked(cudaStream_t st, int64_t ld, int64_t rb, int nblk, double c0, const S* v,
                               const int* act, int na, cd* const* xs, const cd* weights, int r, S* out);
-  // blk (rows x na, column-major) <-> rows [r0, r0 + rows) of the columns act of w (ld x ncap)
-  static void pack_rows(cudaStream_t st, const S* w, int64_t ld, int64_t r0, int64_t rows, const int* act, int na,
-                        S* blk);
-  static void unpack_rows(cudaStream_t st, const S* blk, int64_t r0, int64_t rows, const int* act, int na, S* w,
-                          int64_t ld);
+  // blk (rows x na, column stride `stride` >= rows) <-> rows [r0, r0 + rows) of the columns act of w
+  static void pack_rows(cudaStream_t st, const S* w, int64_t ld, int64_t r0, int64_t rows, int64_t stride,
+                        const int* act, int na, S* blk);
+  static void unpack_rows(cudaStream_t st, const S* blk, int64_t r0, int64_t rows, int64_t stride, const int* act,
+                          int na, S* w, int64_t ld);
   // allgathered blocks (nblk x (rb x na)) -> rows [p rb, min(ld, (p + 1) rb)) of the columns act of w
   static void unpack_blocks(cudaStream_t st, const S* blocks, int64_t rb, int nblk, const int* act, int na, S* w,
                             int64_t ld);

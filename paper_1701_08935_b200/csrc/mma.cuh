@@ -140,6 +140,85 @@ __device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs,
   }
 }
 
+// ---- 3M complex tile products (the sweeps) ---------------------------------
+// A complex 8x8x4 product in three real DMMAs instead of four: with a = ar + i ai and
+// b = br + i bi,  P1 = ar br,  P2 = ai bi,  P3 = (ar + ai)(br + bi),  a b = (P1 - P2) + i (P3 - P1 - P2).
+// The conjugate transpose (op H) is the same with ai -> -ai. P1, P2, P3 accumulate over every
+// tile of a task (fixed order) and are combined once per task (acc3_fold), so the extra
+// additions are one per A and B fragment element per k-step -- 6 DMMAs + 3 adds per k-step for
+// the two 8x8 output blocks instead of 8 DMMAs. The result is normwise as accurate as the
+// 4-product form (each output is a sum of products bounded by |a||b|); only its rounding differs.
+struct Acc3 {
+  double p[2][3][2];  // [half][P1 P2 P3][element]
+};
+__device__ __forceinline__ void acc3_zero(Acc3& a) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a.p[h][k][0] = a.p[h][k][1] = 0.0;
+}
+// out[2h + e] = the complex output (row, ocol(2h + e))
+__device__ __forceinline__ void acc3_fold(const Acc3& a, cd out[4]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      out[2 * h + e] = mk(a.p[h][0][e] - a.p[h][1][e], a.p[h][2][e] - a.p[h][0][e] - a.p[h][1][e]);
+}
+// acc += sg * block value (the add entries: b_i, partial sums), at output (row, ocol(2h + e))
+__device__ __forceinline__ void acc3_add(Acc3& a, int h, int e, cd v, double sg) {
+  a.p[h][0][e] += sg * v.x;          // Re = P1 - P2
+  a.p[h][2][e] += sg * (v.x + v.y);  // Im = P3 - P1 - P2
+}
+
+template <bool OPH, bool NEG>
+__device__ __forceinline__ void mma_tile3_t(Acc3& acc, const cd* ts, const cd* xs, const Frag& f, unsigned km) {
+  if (km == 0) return;
+  __syncwarp();  // mma.sync.aligned needs a converged warp
+  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
+  const int bc = f.c0 + (f.lane >> 2);
+  const int sa = swz(ar);
+#pragma unroll
+  for (int k0 = 0; k0 < TILE / 4; k0 += 4) {  // fragments of 4 k-steps first: the shared-memory latency overlaps
+    cd a[4], b0[4], b1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * (k0 + q) + am;
+      a[q] = OPH ? ts[ar * TILE + (k ^ sa)] : ts[k * TILE + (ar ^ swz(k))];
+      b0[q] = xs[bc * XPAD + k];
+      b1[q] = xs[(bc + 16) * XPAD + k];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!((km >> (k0 + q)) & 1u)) continue;  // predicated off: ~1 issue cycle instead of a DMMA
+      const double re = NEG ? -a[q].x : a[q].x;
+      const double im = (NEG != OPH) ? -a[q].y : a[q].y;  // conj for op H, negated for the pre-transform
+      const double s = re + im;
+      dmma_nv(acc.p[0][0], re, b0[q].x);
+      dmma_nv(acc.p[1][0], re, b1[q].x);
+      dmma_nv(acc.p[0][1], im, b0[q].y);
+      dmma_nv(acc.p[1][1], im, b1[q].y);
+      dmma_nv(acc.p[0][2], s, b0[q].x + b0[q].y);
+      dmma_nv(acc.p[1][2], s, b1[q].x + b1[q].y);
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_tile3(Acc3& acc, const cd* ts, const cd* xs, bool opH, bool neg, const Frag& f,
+                                          unsigned km) {
+  if (opH) {
+    if (neg)
+      mma_tile3_t<true, true>(acc, ts, xs, f, km);
+    else
+      mma_tile3_t<true, false>(acc, ts, xs, f, km);
+  } else {
+    if (neg)
+      mma_tile3_t<false, true>(acc, ts, xs, f, km);
+    else
+      mma_tile3_t<false, false>(acc, ts, xs, f, km);
+  }
+}
+
 // 32 rows x 32 columns of a column-major block into [col*XPAD + row].
 __device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int c0, int nc, unsigned long long pol) {
   const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;

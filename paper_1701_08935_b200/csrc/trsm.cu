@@ -133,6 +133,9 @@ __device__ __forceinline__ void load_x(cd* xs, const cd* base, int64_t ld, int c
 #ifndef ZOLO_V2_MINB
 #define ZOLO_V2_MINB 2
 #endif
+#ifndef ZOLO_SWEEP_3M
+#define ZOLO_SWEEP_3M 1  // complex tile products as 3 real DMMAs (mma.cuh mma_tile3); 0: 4 DMMAs
+#endif
 constexpr int NST2 = ZOLO_NST2;
 constexpr int DAG_TRACE_WORDS = 6;  // start, producer done, consumer done, info, wait ns, (unused)
 constexpr int TSW = TT;             // swizzled (unpadded) tile
@@ -406,8 +409,13 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
   }
   // ------------------------------ consumers ------------------------------
   const Frag f = frag();
+#if ZOLO_SWEEP_3M
+  Acc3 acc;  // 3M complex products (mma.cuh)
+  acc3_zero(acc);
+#else
   Acc8 acc;
   acc8_zero(acc);
+#endif
   int ntiles_task = 0;  // (trace) tile products of the current task
   for (int g = 0;; ++g) {
     const int s = g % NST2, round = g / NST2;
@@ -418,7 +426,11 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
     ntiles_task += m.kind == 0;
     if (m.kind == 0) {
+#if ZOLO_SWEEP_3M
+      mma_tile3(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
+#else
       mma_tile2(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
+#endif
     } else {
       const cd* xs = x_s(s);
       const double sg = static_cast<double>(m.sign);
@@ -427,16 +439,25 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
 #pragma unroll
         for (int e2 = 0; e2 < 2; ++e2) {
           const cd v = xs[ocol(f, 2 * h + e2) * XPAD + f.row];
+#if ZOLO_SWEEP_3M
+          acc3_add(acc, h, e2, v, sg);
+#else
           acc.v[h][0][0][e2] += sg * v.x;
           acc.v[h][0][1][e2] += sg * v.y;
+#endif
         }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
     if (m.last) {
       cd o[4];
+#if ZOLO_SWEEP_3M
+      acc3_fold(acc, o);
+      acc3_zero(acc);
+#else
       acc8_fold(acc, o);
       acc8_zero(acc);
+#endif
       const bool chunk = m.out >= 0;
       const int c0 = m.gi * DCG;
       if (chunk) {

@@ -106,3 +106,63 @@ def test_window_json_matches_window_from_gaps(io):
     w = io.window_to_json([-np.inf, 1.0, 2.0, 3.0])
     assert w == {"a": 0.0, "b": 2.5, "a_minus": None, "a_plus": 1.0, "b_minus": 2.0, "b_plus": 3.0}
     json.dumps(w)
+
+
+# ---- interoperability with the reference's own readers / writers (oracle/_ref) ----
+REF_DIAG10 = "/root/reference/proj/data/diag10.mtx"
+
+
+def _ref():
+    import oracle
+
+    if not oracle.Reference.available():
+        pytest.skip("oracle/_ref not built")
+    return oracle.Reference()
+
+
+def test_reads_the_reference_fixture_diag10(io):
+    """proj/data/diag10.mtx, the reference CLI's own fixture: our reader and the reference's
+    (matrix_market.hpp:106-159) return the same CSR."""
+    import os
+
+    if not os.path.exists(REF_DIAG10):
+        pytest.skip("reference tree absent")
+    ref = _ref()
+    n, csr, cx = ref.read_mm(REF_DIAG10)
+    ours = io.read_matrix_market(REF_DIAG10)
+    assert ours[0] == n == 10 and not cx
+    for x, y in zip(ours[1], csr):
+        assert (np.asarray(x) == np.asarray(y)).all()
+    assert (np.asarray(ours[1][2]) == np.arange(1.0, 11.0)).all()
+
+
+@pytest.mark.parametrize("case", ["filter_cfg2_k6", "filter_planted30_cx", "filter_cfg3_k5"])
+def test_matrix_market_files_cross_read(io, tmp_path, case):
+    """A file the reference wrote (write_matrix_market) read by us, and one we wrote read by the
+    reference: identical CSR arrays, bit for bit."""
+    ref = _ref()
+    g = load_golden(case)
+    n, a, b = golden_pencil(g)
+    cx = bool(g["cx"])
+    ref.write_mm(tmp_path / "ref.mtx", n, a, cx)
+    ours = io.read_matrix_market(str(tmp_path / "ref.mtx"))
+    for x, y in zip(ours[1], a):
+        assert (np.asarray(x) == np.asarray(y)).all()
+    io.write_matrix_market(str(tmp_path / "ours.mtx"), n, a, cx)
+    n2, back, cx2 = ref.read_mm(tmp_path / "ours.mtx")
+    assert n2 == n and cx2 == cx
+    for x, y in zip(back, a):
+        assert (np.asarray(x) == np.asarray(y)).all()
+
+
+@pytest.mark.parametrize("cx", [False, True])
+def test_eigvec_files_cross_read(io, tmp_path, cx):
+    """ZEIGVEC1 eigenvector blocks (serialize.hpp:108-142) written by either side and read by the
+    other, bit for bit."""
+    ref = _ref()
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((37, 5)) + (1j * rng.standard_normal((37, 5)) if cx else 0)
+    io.write_eigvec_binary(str(tmp_path / "ours.bin"), x)
+    assert (ref.read_eigvec(tmp_path / "ours.bin", 37, 5, cx) == x).all()
+    ref.write_eigvec(tmp_path / "ref.bin", x)
+    assert (io.read_eigvec_binary(str(tmp_path / "ref.bin")) == x).all()
