@@ -223,6 +223,14 @@ int zolo_apply_filter(zolo_ctx* ctx, const double* v, double* y, int64_t ncols, 
 int zolo_apply_filter_device(zolo_ctx* ctx, const void* d_v, void* d_y, int64_t ncols, double gmres_tol,
                              int64_t gmres_max, zolo_report* rep);
 
+/* ShiftedFactor::solve / adjoint_solve (band_factor.hpp:53-117) of one factored
+ * pole: x = (A - sigma_j B)^-1 b (adjoint = 0) or (A - sigma_j B)^-H b
+ * (adjoint = 1) for an n x ncols complex block b (original ordering,
+ * interleaved complex, column-major), through the same device factors and
+ * sweeps as the filter (refined when zolo_set_refinement is on). pole: index
+ * of the design's inner pole, factored by this context. */
+int zolo_shifted_solve(zolo_ctx* ctx, int pole, int adjoint, const double* b, double* x, int64_t ncols);
+
 /* inner_solve_count / g_application_count (filter_engine.hpp:50-51). */
 int zolo_counters(const zolo_ctx* ctx, int64_t* inner_solves, int64_t* g_applications);
 

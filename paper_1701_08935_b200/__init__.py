@@ -136,6 +136,7 @@ def lib():
         L.zolo_set_solve_mode.argtypes = [P, C.c_int, C.c_int, D, C.c_int]
         L.zolo_factorize.argtypes = [P, P, P]
         L.zolo_apply_g.argtypes = [P, P, P, I64]
+        L.zolo_shifted_solve.argtypes = [P, C.c_int, C.c_int, P, P, I64]
         L.zolo_apply_filter.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
         L.zolo_apply_filter_device.argtypes = [P, P, P, I64, D, I64, C.POINTER(_Report)]
         L.zolo_counters.argtypes = [P, P, P]
@@ -260,18 +261,32 @@ class InertiaCounter:
             lib().zolo_ctx_destroy(h)
             self._h = None
 
-    def count_below(self, sigma: float, nudges: int = 3) -> int:
-        """Eigenvalues < sigma. A shift within rounding of an eigenvalue (rejected
-        pivot) is nudged by 1e-12 relative, up to `nudges` times."""
+    def _count_once(self, s: float):
         out = np.zeros(1, dtype=np.int64)
         ratio = np.zeros(1)
+        st = lib().zolo_count_below(self._h, C.c_double(s), _ptr(out), _ptr(ratio))
+        return st, int(out[0]), float(ratio[0])
+
+    def count_below(self, sigma: float, nudges: int = 3, growth_ratio: float = 1e-8) -> int:
+        """Eigenvalues < sigma. A shift within rounding of an eigenvalue (rejected pivot) is
+        nudged by 1e-12 relative, up to `nudges` times. The real-shift LU is unpivoted (the
+        pencil A - sigma B is Hermitian indefinite): when its smallest pivot ratio is below
+        `growth_ratio` -- where element growth could flip a pivot's sign -- the count is
+        confirmed at two shifts 1e-10 (relative) to either side, which must agree (no eigenvalue
+        lies that close); otherwise NumericalError."""
         s = float(sigma)
         for k in range(nudges + 1):
-            st = lib().zolo_count_below(self._h, C.c_double(s), _ptr(out), _ptr(ratio))
+            st, cnt, ratio = self._count_once(s)
             if st != ZOLO_ERR_FACTORIZATION:
                 _check(self._h, st)
-                self.last_min_pivot_ratio = float(ratio[0])
-                return int(out[0])
+                self.last_min_pivot_ratio = ratio
+                if ratio < growth_ratio:
+                    h = 1e-10 * max(1.0, abs(s))
+                    lo, hi = self._count_once(s - h), self._count_once(s + h)
+                    if lo[0] != ZOLO_OK or hi[0] != ZOLO_OK or not (lo[1] == cnt == hi[1]):
+                        raise NumericalError(f"inertia count at {s!r} unstable (min pivot ratio {ratio:.2e}; "
+                                             f"neighbouring counts {lo[1]}, {cnt}, {hi[1]})")
+                return cnt
             s = float(sigma) + (k + 1) * 1e-12 * max(1.0, abs(float(sigma)))
         _check(self._h, st)
 
@@ -398,6 +413,19 @@ class FilterOperator:
         out = np.zeros_like(v)
         _check(self._h, lib().zolo_apply_g(self._h, _ptr(v), _ptr(out), v.shape[1]))
         return out
+
+    def shifted_solve(self, b, pole: int = 0, adjoint: bool = False):
+        """ShiftedFactor::solve / adjoint_solve (band_factor.hpp:53-117) of the factored pole
+        `pole`: (A - sigma_pole B)^-1 b or its adjoint, b an n x k (complex) block."""
+        b = np.asarray(b)
+        if b.ndim == 1:
+            b = b[:, None]
+        if b.shape[0] != self.n:
+            raise DomainError("dimension mismatch")
+        b = np.asfortranarray(b, dtype=np.complex128)
+        x = np.zeros_like(b)
+        _check(self._h, lib().zolo_shifted_solve(self._h, int(pole), int(bool(adjoint)), _ptr(b), _ptr(x), b.shape[1]))
+        return x
 
     def apply_filter(self, v, gmres_tol: float = 1e-12, gmres_max: int = 50):
         """(R_ab(B^-1 A) V, report) (filter_engine.hpp:86-155). Raises GmresError."""

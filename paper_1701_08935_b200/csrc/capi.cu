@@ -11,6 +11,7 @@
 // which columns finish. Everything stays in the factor ordering P v on the
 // device; only the input block is permuted in and the output permuted out.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -204,6 +205,13 @@ struct DevMem {
   T* as() const {
     return reinterpret_cast<T*>(p);
   }
+};
+
+// NVTX range around a phase of the path (factorization, filter application, G application,
+// Arnoldi, Rayleigh-Ritz): visible in Nsight Systems / ncu --nvtx, free without a tool attached
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
 };
 
 // development knobs (schedule tuning); defaults are the shipped configuration
@@ -609,6 +617,7 @@ void ensure_perm_csr(zolo_ctx& c) {
 void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats);
 
 void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats) {
+  Nvtx range("zolo::factorize");
   require(c.have_pencil, "zolo_factorize: no pencil uploaded");
   require(c.have_design, "zolo_factorize: no design installed");
   if (c.order_mode == ZOLO_ORDER_RCM && !perm_in) {
@@ -617,6 +626,10 @@ void do_factorize(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats* stats)
     rcm_order(c.n, u.rp.data(), u.ci.data(), rcm.data());  // band_factor.hpp:203-204
     c.sym_ready = false;
     do_factorize_sparse(c, rcm.data(), stats);
+    if (stats) {  // FactorProfile.bandwidth (band_factor.hpp:31-35): the half-bandwidth under RCM
+      const int64_t bw = bandwidth_under(c.n, u.rp.data(), u.ci.data(), rcm.data());
+      for (int j = 0; j < c.nloc(); ++j) stats[j].bandwidth = bw;
+    }
     return;
   }
   do_factorize_sparse(c, perm_in, stats);
@@ -1135,22 +1148,23 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
 // Residual-correction refinement of every chain's solution (zolo_set_refinement):
 // r = b - K x (K^H for the adjoint chains) from the pencil in FP64, d = K^-1 r by the same
 // sweeps in place over r, x += d.
-void refine_solves(zolo_ctx& c, int na) {
+void refine_solves(zolo_ctx& c, int na, int first = 0, int nsub = -1) {
+  Nvtx range("zolo::refine");
   const int64_t ld = c.geom.npad, n = ld;
-  const int nch = c.nchains();
+  const int nch = nsub < 0 ? c.nchains() : nsub;
   std::vector<cd*> xs(nch), rs(nch);
-  for (int i = 0; i < nch; ++i) xs[i] = c.xbuf[i]->as<cd>(), rs[i] = c.rbuf[i]->as<cd>();
+  for (int i = 0; i < nch; ++i) xs[i] = c.xbuf[first + i]->as<cd>(), rs[i] = c.rbuf[first + i]->as<cd>();
   for (int step = 0; step < c.refine; ++step) {
     if (c.cx)
       Krylov<cd>::shifted_residual(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<cd>(),
                                    c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(), c.bv_d.as<cd>(),
-                                   c.bbuf.as<cd>(), xs.data(), rs.data(), c.chain_sigma.as<cd>(), nch, na);
+                                   c.bbuf.as<cd>(), xs.data(), rs.data(), c.chain_sigma.as<cd>() + first, nch, na);
     else
       Krylov<double>::shifted_residual(c.st, n, ld, c.arp_d.as<int>(), c.aci_d.as<int>(), c.av_d.as<double>(),
                                        c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
                                        c.bv_d.as<double>(), c.bbuf.as<cd>(), xs.data(), rs.data(),
-                                       c.chain_sigma.as<cd>(), nch, na);
-    sweep_sparse(c, 0, nch, na, nullptr, true);
+                                       c.chain_sigma.as<cd>() + first, nch, na);
+    sweep_sparse(c, first, nch, na, nullptr, true);
     add_corrections(c.st, ld, xs.data(), rs.data(), nch, na);
   }
 }
@@ -1199,6 +1213,7 @@ float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst);
 
 // G applied to the columns act[0..na) of vsrc (ld x ncap, S) -> w[:, act].
 float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
+  Nvtx range("zolo::apply_g");
   if (c.hybrid) return apply_g_hybrid(c, vsrc, na, wdst);
   const int64_t ld = c.geom.npad;  // device rows: padding rows (anywhere in ND order) are zero
   const int* act = c.act_d.as<int>();
@@ -1510,6 +1525,7 @@ float apply_g_hybrid(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
 template <class S>
 int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, double tol, int64_t gmres_max,
                       zolo_report* rep) {
+  Nvtx range("zolo::apply_filter");
   require(c.factored, "apply_filter: operator not factorized");
   require(c.shard_size == 1 || c.coll, "apply_filter: a pole-sharded context needs its communicator");
   // (the reference has no cap, gmres.hpp:98-101; the device Krylov kernels hold up to
@@ -1610,10 +1626,12 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
     apply_g_device(c, vm, na, c.w.p);
     trsm_launches += 2;
     launches += 8 + (it + 1 < maxit ? 1 : 0);
+    nvtxRangePushA("zolo::arnoldi");
     const int nls = Krylov<S>::arnoldi(c.st, row_lo(c), row_hi(c), ld, c.basis_ptrs.as<S*>(), it, c.w.as<S>(),
                                        c.act_d.as<int>(), na, g, c.partial.as<double>(), c.hsave.as<S>(),
                                        c.row_shard ? c.coll : nullptr);
     Krylov<S>::least_squares(c.st, c.act_d.as<int>(), na, it, g, c.partial.as<double>(), nls, tol);
+    nvtxRangePop();
     if (it + 1 < maxit) {
       S* vn = reinterpret_cast<S*>(basis_block(c, it + 1));
       Krylov<S>::next_basis(c.st, n, ld, c.w.as<S>(), vn, c.act_d.as<int>(), na, g);
@@ -1737,6 +1755,7 @@ void apply_g_impl(zolo_ctx& c, const double* v, double* gv, int64_t k) {
 
 template <class S>
 void rr_impl(zolo_ctx& c, const double* y, int64_t k, double* at, double* bt) {
+  Nvtx range("zolo::rr_project");
   ensure_perm_csr(c);
   const int64_t n = c.n, ld = c.geom.npad;
   const size_t es = sizeof(S);
@@ -1801,6 +1820,7 @@ void spmm_dev_impl(zolo_ctx& c, int which, const void* x, void* out, int64_t k) 
 
 template <class S>
 void gram_dev_impl(zolo_ctx& c, const void* y, const void* z, int64_t k, int64_t kk, double* out) {
+  Nvtx range("zolo::gram");
   const int64_t n = c.n;
   const int64_t nchunk = (n + CHUNK - 1) / CHUNK;
   c.rr_partial.ensure(sizeof(S) * nchunk * k * kk + 64);
@@ -2185,6 +2205,39 @@ int zolo_filter_create(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, 
   st = zolo_set_design(c, design, r);
   if (st) return st;
   return zolo_factorize(c, nullptr, stats);
+}
+
+int zolo_shifted_solve(zolo_ctx* c, int pole, int adjoint, const double* b, double* x, int64_t ncols) {
+  return guarded(c, [&] {
+    Nvtx range("zolo::shifted_solve");
+    require(c->factored, "shifted_solve: operator not factorized");
+    require(!c->hybrid, "shifted_solve: the hybrid solve factors one pole only");
+    require(ncols >= 1, "shifted_solve: empty block");
+    int p = -1;
+    for (int q = 0; q < c->nloc(); ++q)
+      if (c->own[q] == pole) p = q;
+    require(p >= 0, "shifted_solve: pole not factored by this context");
+    zolo_ctx& C = *c;
+    const int64_t n = C.n, ld = C.geom.npad;
+    ensure_workspace(C, ncols);
+    // ShiftedFactor::solve / adjoint_solve (band_factor.hpp:53-117): complex n x ncols blocks. For a
+    // real pencil K = A - sigma B is complex symmetric, so K^-H b = conj(K^-1 conj(b)).
+    const bool conj_trick = adjoint && !C.cx;
+    const int ch = C.cx ? 2 * p + (adjoint ? 1 : 0) : p;
+    CK(cudaMemcpyAsync(C.vin_orig.p, b, sizeof(cd) * n * ncols, cudaMemcpyHostToDevice, C.st));
+    if (conj_trick) conj_inplace(C.st, C.vin_orig.as<cd>(), n * ncols);
+    Krylov<cd>::permute_in(C.st, C.vin_orig.as<cd>(), n, C.bbuf.as<cd>(), ld, ncols, C.perm_d.as<int>());
+    for (int64_t i = 0; i < ncols; ++i) C.act_h[i] = static_cast<int>(i);
+    CK(cudaMemcpyAsync(C.act_d.p, C.act_h, sizeof(int) * ncols, cudaMemcpyHostToDevice, C.st));
+    sweep_sparse(C, ch, 1, static_cast<int>(ncols));
+    if (C.refine) refine_solves(C, static_cast<int>(ncols), ch, 1);
+    Krylov<cd>::permute_out(C.st, C.xbuf[ch]->as<cd>(), ld, C.vin_orig.as<cd>(), n, ncols, C.perm_d.as<int>());
+    if (conj_trick) conj_inplace(C.st, C.vin_orig.as<cd>(), n * ncols);
+    CK(cudaMemcpyAsync(x, C.vin_orig.p, sizeof(cd) * n * ncols, cudaMemcpyDeviceToHost, C.st));
+    CK(cudaStreamSynchronize(C.st));
+    CK(cudaGetLastError());
+    C.inner_solves += ncols;  // one shifted solve per right-hand side (band_factor.hpp:53-85 per column)
+  });
 }
 
 int zolo_apply_g(zolo_ctx* c, const double* v, double* gv, int64_t ncols) {

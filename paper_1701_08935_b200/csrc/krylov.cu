@@ -246,6 +246,11 @@ __global__ void add_corrections_kernel(int64_t ld, ChainPtrs xs, ChainPtrs ds) {
   x[t + a * ld] = cadd(x[t + a * ld], ds.p[z][t + a * ld]);
 }
 
+__global__ void conj_kernel(cd* x, int64_t count) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t < count) x[t].y = -x[t].y;
+}
+
 // rows[0..nrows) of columns 0..k-1 set to zero (the identity padding rows of the BSR SpMM output)
 __global__ void zero_rows_kernel(const int* rows, int nrows, cd* out, int64_t ld) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -951,6 +956,10 @@ void add_corrections(cudaStream_t st, int64_t ld, cd* const* x, cd* const* d, in
   ChainPtrs xp, dp;
   for (int z = 0; z < nch; ++z) xp.p[z] = x[z], dp.p[z] = d[z];
   add_corrections_kernel<<<dim3(blocks_for(ld, 256), na, nch), 256, 0, st>>>(ld, xp, dp);
+}
+
+void conj_inplace(cudaStream_t st, cd* x, int64_t count) {
+  if (count > 0) conj_kernel<<<blocks_for(count, 256), 256, 0, st>>>(x, count);
 }
 
 void zero_rows(cudaStream_t st, const int* rows, int nrows, cd* out, int64_t ld, int64_t k) {

@@ -101,6 +101,8 @@ struct Krylov {
 };
 
 // out[rows[q], c] = 0 for q < nrows, c < k (ld rows per column)
+// x <- conj(x) (count complex entries)
+void conj_inplace(cudaStream_t st, cd* x, int64_t count);
 // x_z[:, 0:na] += d_z[:, 0:na] for the chains z < nch (the refinement corrections)
 void add_corrections(cudaStream_t st, int64_t ld, cd* const* x, cd* const* d, int nch, int na);
 void zero_rows(cudaStream_t st, const int* rows, int nrows, cd* out, int64_t ld, int64_t k);

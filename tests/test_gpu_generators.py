@@ -131,3 +131,28 @@ def test_cfg5_full_size_eigensolver():
     assert res.converged and res.residual <= 1e-10
     x = res.vectors
     assert np.abs(x.conj().T @ x - np.eye(x.shape[1])).max() <= 1e-8
+
+
+def test_cfg4_full_size_pole_shard():
+    """BASELINE config 4 at full size (N = 104000, 8000 atoms x 13x13 BSR blocks, r = 8): all
+    eight factors need ~283 GB, so it runs pole-sharded over >= 2 GPUs. One rank's share is
+    exercised here on one B200: rank 0 of an 8-rank group (pole 0, ~35 GB of block-sparse factors,
+    atom-aligned ND, BSR SpMM) factors and applies its partial G. Without a communicator the
+    partial sum is returned; its refined and plain solves must agree (an inaccurate factor of this
+    size would not survive the residual correction), and the solve counters count one pole."""
+    import paper_1701_08935_b200 as zb
+    from paper_1701_08935_b200 import configs
+    from paper_1701_08935_b200.design import build_filter_design
+
+    pen, cx, gaps, r, nv, nl = configs.config("cfg4")
+    design = build_filter_design(gaps, r)
+    op = zb.FilterOperator(pen, design, r, is_complex=cx, block_size=13, shard=(0, 8, None))
+    assert op.poles == [0] and op.bsr_info() == (13, 8000)
+    v = zb.random_block(pen[0], 32, 1, cx=cx, orthonormalize=True)
+    g0 = op.apply_g(v)
+    op.set_refinement(1)
+    g1 = op.apply_g(v)
+    assert np.isfinite(g0).all()
+    assert np.linalg.norm(g1 - g0) <= 1e-8 * np.linalg.norm(g1)
+    assert op.inner_solve_count() == 2 * 2 * 1  # two G applications x (solve + adjoint) x one pole
+    assert op.factor_profile()[0]["min_pivot_ratio"] > 0
