@@ -2224,16 +2224,17 @@ int zolo_shifted_solve(zolo_ctx* c, int pole, int adjoint, const double* b, doub
     // real pencil K = A - sigma B is complex symmetric, so K^-H b = conj(K^-1 conj(b)).
     const bool conj_trick = adjoint && !C.cx;
     const int ch = C.cx ? 2 * p + (adjoint ? 1 : 0) : p;
-    CK(cudaMemcpyAsync(C.vin_orig.p, b, sizeof(cd) * n * ncols, cudaMemcpyHostToDevice, C.st));
-    if (conj_trick) conj_inplace(C.st, C.vin_orig.as<cd>(), n * ncols);
-    Krylov<cd>::permute_in(C.st, C.vin_orig.as<cd>(), n, C.bbuf.as<cd>(), ld, ncols, C.perm_d.as<int>());
+    C.tmp1.ensure(sizeof(cd) * n * ncols);  // complex staging (vin_orig holds S = double for real pencils)
+    CK(cudaMemcpyAsync(C.tmp1.p, b, sizeof(cd) * n * ncols, cudaMemcpyHostToDevice, C.st));
+    if (conj_trick) conj_inplace(C.st, C.tmp1.as<cd>(), n * ncols);
+    Krylov<cd>::permute_in(C.st, C.tmp1.as<cd>(), n, C.bbuf.as<cd>(), ld, ncols, C.perm_d.as<int>());
     for (int64_t i = 0; i < ncols; ++i) C.act_h[i] = static_cast<int>(i);
     CK(cudaMemcpyAsync(C.act_d.p, C.act_h, sizeof(int) * ncols, cudaMemcpyHostToDevice, C.st));
     sweep_sparse(C, ch, 1, static_cast<int>(ncols));
     if (C.refine) refine_solves(C, static_cast<int>(ncols), ch, 1);
-    Krylov<cd>::permute_out(C.st, C.xbuf[ch]->as<cd>(), ld, C.vin_orig.as<cd>(), n, ncols, C.perm_d.as<int>());
-    if (conj_trick) conj_inplace(C.st, C.vin_orig.as<cd>(), n * ncols);
-    CK(cudaMemcpyAsync(x, C.vin_orig.p, sizeof(cd) * n * ncols, cudaMemcpyDeviceToHost, C.st));
+    Krylov<cd>::permute_out(C.st, C.xbuf[ch]->as<cd>(), ld, C.tmp1.as<cd>(), n, ncols, C.perm_d.as<int>());
+    if (conj_trick) conj_inplace(C.st, C.tmp1.as<cd>(), n * ncols);
+    CK(cudaMemcpyAsync(x, C.tmp1.p, sizeof(cd) * n * ncols, cudaMemcpyDeviceToHost, C.st));
     CK(cudaStreamSynchronize(C.st));
     CK(cudaGetLastError());
     C.inner_solves += ncols;  // one shifted solve per right-hand side (band_factor.hpp:53-85 per column)

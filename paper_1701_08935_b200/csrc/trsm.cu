@@ -137,7 +137,7 @@ __device__ __forceinline__ void load_x(cd* xs, const cd* base, int64_t ld, int c
 #define ZOLO_SWEEP_3M 1  // complex tile products as 3 real DMMAs (mma.cuh mma_tile3); 0: 4 DMMAs
 #endif
 constexpr int NST2 = ZOLO_NST2;
-constexpr int DAG_TRACE_WORDS = 6;  // start, producer done, consumer done, info, wait ns, (unused)
+constexpr int DAG_TRACE_WORDS = 6;  // claim, -, consumer done, info, wait ns, producer done (tools/dag2_trace_analyze.py)
 constexpr int TSW = TT;             // swizzled (unpadded) tile
 constexpr int P2T = ST + 32;        // threads: 8 consumer warps + the producer warp
 constexpr int DAG2_CHAINS = 32;
@@ -152,12 +152,17 @@ struct DagArgs {
   int* flags;    // per (chain, 32-column group, block): epoch when u_i is final
   int* cflags;   // per (chain, 32-column group, slot): epoch when the partial sum is written
   int* counter;  // [0] task counter, [2] wait-timeout error word
-  unsigned long long* trace;  // optional: per task (start, produced, done, smid<<48|chunk<<47|i<<16|tiles, wait ns)
+  unsigned long long* trace;  // optional: per task (claim, -, done, smid<<48|chunk<<47|i<<16|tiles, wait ns, produced)
   // lagged GMRES control (capi apply_filter_impl): the launch covers a superset of the columns
   // still running; a task whose column group has converged entirely is skipped
   const int* gact = nullptr;
   const int* gdone = nullptr;
+  int policy = 1 | (2 << 2);  // L2 eviction priority: bits 0-1 tiles, bits 2-3 solution blocks (0 first, 1 normal, 2 last)
 };
+
+__device__ __forceinline__ unsigned long long l2_policy(int code) {
+  return code == 0 ? l2_evict_first() : (code == 1 ? l2_evict_normal() : l2_evict_last());
+}
 
 struct Meta2 {
   int kind;  // 0 MMA(tile, x, neg = sign), 1 ADD(x block * sign), 2 END
@@ -244,7 +249,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
   const int ntasks = A.ntask * per_step;
   if (warp == ST / 32) {
     // ------------------------------ producer ------------------------------
-    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    const unsigned long long pol_stream = l2_evict_first(), pol_tile = l2_policy(A.policy & 3),
+                             pol_keep = l2_policy((A.policy >> 2) & 3);
     int g = 0;
     int cur_t = 0;  // claim index of the task being produced (trace)
     // one ring entry: tile (optional) + a 32 x 32 block with column stride `stride`
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
                              static_cast<unsigned>(nc) * TILE * static_cast<unsigned>(sizeof(cd));
       if (lane == 0) mbar_expect_tx(full + s, bytes);
       __syncwarp();
-      if (tile && lane == 0) bulk_copy(tile_s(s), tile, TT * sizeof(cd), full + s, pol_stream);
+      if (tile && lane == 0) bulk_copy(tile_s(s), tile, TT * sizeof(cd), full + s, pol_tile);
       cd* xs = x_s(s);
       if (lane < nc)
         bulk_copy(xs + lane * XPAD, blk + (c0 + lane) * stride, TILE * sizeof(cd), full + s, pol);
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       __syncwarp();
       if (trp && lane == 0) {
         trp[4] = wsum;
-        trp[1] = gtimer();
+        trp[5] = gtimer();
       }
       t = tn;
       rec_lo = nrec_lo;
@@ -549,6 +555,11 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   a.trace = trace;
   a.gact = gact;
   a.gdone = gdone;
+  static const int policy = [] {
+    const char* v = std::getenv("ZOLO_L2_POLICY");  // (development) see DagArgs::policy
+    return v && *v ? std::atoi(v) : (1 | (2 << 2));  // tiles evict_normal (+3% on cfg3), blocks evict_last
+  }();
+  a.policy = policy;
   // the attribute is per device: set it on every launch (a process may drive several GPUs)
   cudaFuncSetAttribute(dag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DAG2_SMEM);
   cudaMemsetAsync(counter, 0, sizeof(int), st);

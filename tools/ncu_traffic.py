@@ -37,8 +37,10 @@ for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
     units["dram_read" if "read" in key else "dram_write"] = scale
 l0 = launches[0]
 rd, wr = l0["dram_read"] * units["dram_read"], l0["dram_write"] * units["dram_write"]
+tu = unit_row[col["gpu__time_duration.sum"]].strip().lower()
+to_ms = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(tu, 1.0)
 res = {"kernel": "dag2_kernel", "config": config, "bytes_per_launch": int(rd + wr), "dram_read": int(rd),
-       "dram_write": int(wr), "duration_ms_cold": l0["duration_ns"] / 1e6 if l0["duration_ns"] else None,
+       "dram_write": int(wr), "duration_ms_cold": l0["duration_ns"] * to_ms if l0["duration_ns"] else None,
        "tensor_pipe_pct": l0["tensor_pipe_pct"], "fp64_pipe_pct": l0["fp64_pipe_pct"],
        "source": f"ncu --set full --clock-control none (cold cache, one launch): {cmd}".strip()}
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
