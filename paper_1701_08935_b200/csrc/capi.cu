@@ -320,6 +320,7 @@ struct zolo_ctx {
   int refine = 0;
   std::vector<std::unique_ptr<DevMem>> rbuf;
   DevMem chains_fwd_ref, chains_bwd_ref, chain_sigma;
+  DevMem tmaps_fwd, tmaps_bwd, tmaps_fwd_ref, tmaps_bwd_ref;  // the chains' x-block tensor maps
   DevMem trace_buf;
   DevMem host_in, host_out;  // staging of the host-buffer entry points
   bool trace_done = false;
@@ -344,6 +345,7 @@ struct zolo_ctx {
   DevMem fp_cols, fp_pan, fp_tgt, fp_con;   // its device arrays
   DagSched sched_fwd, sched_bwd;
   int sp_nslots = 0;
+  int swc = 32;  // sweep task width (columns): 64 for blocks of >= 128 columns (ensure_workspace)
   std::vector<cd*> sp_dt;
   int64_t flags_cap = 0, prog_cap = 0, cflags_off = 0;
   int epoch = 0;
@@ -998,6 +1000,10 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
     c.xbuf[i]->ensure(sizeof(cd) * ld * nc);
     c.cbuf[i]->ensure(sizeof(cd) * crows * nc);
   }
+  // sweep task width: 64 columns halve the tile traffic and the per-task overhead per column, but
+  // pad a block of fewer than 128 columns too much (ZOLO_SWEEP_COLS: development override)
+  static const int swc_env = env_int("ZOLO_SWEEP_COLS", 0);
+  c.swc = (swc_env == 32 || swc_env == 64) ? swc_env : (nc >= 128 ? 64 : 32);
   std::vector<Chain> fwd(nch), bwd(nch);
   for (int p = 0; p < c.nloc(); ++p) {
     const FactorTiles& t = c.tiles[p];
@@ -1010,17 +1016,36 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
       // solve:   y = DinvL b - L~ y ;  x = DinvU y - U~ x
       // adjoint: z = b - U~^H z (z_i = U_ii^H y_i) ; w = DinvU^H z - L~^H w (w_i = L_ii^H x_i),
       //          then x_i = DinvL_i^H w_i (blockdiag post-pass)
-      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
-      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
-      fwd[2 * p + 1] = Chain{t.Ut, nullptr, t.mUt, nullptr, b, xa, cba, FWD_UH, 0};
-      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, t.mLt, t.mDU, xa, xa, cba, BWD_LH, 0};
+      fwd[2 * p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0, nullptr};
+      bwd[2 * p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0, nullptr};
+      fwd[2 * p + 1] = Chain{t.Ut, nullptr, t.mUt, nullptr, b, xa, cba, FWD_UH, 0, nullptr};
+      bwd[2 * p + 1] = Chain{t.Lt, t.DinvU, t.mLt, t.mDU, xa, xa, cba, BWD_LH, 0, nullptr};
     } else {
       cd* x = c.xbuf[p]->as<cd>();
       cd* cb = c.cbuf[p]->as<cd>();
-      fwd[p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0};
-      bwd[p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0};
+      fwd[p] = Chain{t.Lt, t.DinvL, t.mLt, t.mDL, b, x, cb, FWD_L, 0, nullptr};
+      bwd[p] = Chain{t.Ut, t.DinvU, t.mUt, t.mDU, x, x, cb, BWD_U, 0, nullptr};
     }
   }
+  // the sweeps' x-block tensor maps (src, dst, cbuf per chain), sized for the workspace's columns
+  auto with_maps = [&](std::vector<Chain>& chs, DevMem& maps) {
+    struct alignas(64) XMap {
+      unsigned char b[XMAP_BYTES];
+    };
+    std::vector<XMap> hm(3 * chs.size());
+    maps.ensure(sizeof(XMap) * hm.size());
+    for (size_t ch = 0; ch < chs.size(); ++ch) {
+      const cd* bufs[3] = {chs[ch].src, chs[ch].dst, chs[ch].cbuf};
+      const int64_t lds[3] = {ld, ld, crows};
+      for (int k = 0; k < 3; ++k)
+        if (!encode_xblock_map(&hm[3 * ch + k], bufs[k], lds[k], nc, c.swc))
+          throw ZoloError(ZOLO_ERR_CUDA, "cuTensorMapEncodeTiled failed for a sweep block");
+      chs[ch].tmaps = maps.as<unsigned char>() + 3 * ch * sizeof(XMap);
+    }
+    upload(maps, hm, c.st);
+  };
+  with_maps(fwd, c.tmaps_fwd);
+  with_maps(bwd, c.tmaps_bwd);
   upload(c.chains_fwd, fwd, c.st);
   upload(c.chains_bwd, bwd, c.st);
   if (c.refine) {  // refinement sweeps: same factors, in place over the residual blocks
@@ -1039,6 +1064,8 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
       const double im = poles[2 * c.own[p] + 1];
       sig[ch] = mk(poles[2 * c.own[p]], (c.cx && (ch & 1)) ? -im : im);
     }
+    with_maps(fwd, c.tmaps_fwd_ref);
+    with_maps(bwd, c.tmaps_bwd_ref);
     upload(c.chains_fwd_ref, fwd, c.st);
     upload(c.chains_bwd_ref, bwd, c.st);
     upload(c.chain_sigma, sig, c.st);
@@ -1047,7 +1074,7 @@ void ensure_workspace(zolo_ctx& c, int64_t ncols) {
   // [(reserved) nch x ngroups uint64 | block flags: nch x ngroups x nbk int |
   //  DAG chunk flags: nch x dag_groups x nslots int]; all epoch-stamped, zeroed with the epoch
   const int64_t nbflags = static_cast<int64_t>(nch) * ngroups * c.geom.nbk;
-  const int64_t nflags = nbflags + static_cast<int64_t>(nch) * dag_groups(nc) * c.sp_nslots;
+  const int64_t nflags = nbflags + static_cast<int64_t>(nch) * dag_groups(nc, 32) * c.sp_nslots;
   if (nflags > c.flags_cap || static_cast<int64_t>(nch) * ngroups > c.prog_cap) {
     c.prog_cap = static_cast<int64_t>(nch) * ngroups;
     const size_t bytes = sizeof(unsigned long long) * c.prog_cap + sizeof(int) * nflags;
@@ -1133,9 +1160,10 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
   int* cf = fc + c.cflags_off;
   const Chain* cfw = (refinement ? c.chains_fwd_ref : c.chains_fwd).as<Chain>() + first;
   const Chain* cbw = (refinement ? c.chains_bwd_ref : c.chains_bwd).as<Chain>() + first;
-  const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, cfw, nsub, na, ld, fc, cf, ++c.epoch,
+  const int64_t ldp = static_cast<int64_t>(TILE) * std::max(c.sp_nslots, 1);  // cbuf rows (ensure_workspace)
+  const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, cfw, nsub, na, c.swc, ld, ldp, fc, cf, ++c.epoch,
                                  c.counter.as<int>(), c.num_sms, trace, c.act_d.as<int>(), c.lag_done);
-  const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, cbw, nsub, na, ld, fc, cf, ++c.epoch,
+  const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, cbw, nsub, na, c.swc, ld, ldp, fc, cf, ++c.epoch,
                                  c.counter.as<int>(), c.num_sms, nullptr, c.act_d.as<int>(), c.lag_done);
   if (g1 < 0 || g2 < 0) throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: more than 32 chains in one launch");
   if (c.cx)
@@ -1226,7 +1254,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
   // tools/dag2_trace_analyze.py)
   static const char* dag_trace = std::getenv("ZOLO_TRACE");
   unsigned long long* dtr = nullptr;
-  const size_t ntask = static_cast<size_t>(c.sched_fwd.ntask) * nch * dag_groups(na);
+  const size_t ntask = static_cast<size_t>(c.sched_fwd.ntask) * nch * dag_groups(na, c.swc);
   if (dag_trace && !c.trace_done) {
     c.trace_buf.ensure(sizeof(unsigned long long) * 6 * ntask);
     CK(cudaMemsetAsync(c.trace_buf.p, 0, sizeof(unsigned long long) * 6 * ntask, c.st));
@@ -1240,7 +1268,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
     CK(cudaStreamSynchronize(c.st));
     if (FILE* fh = std::fopen(dag_trace, "w")) {
       std::fprintf(fh, "# nb %d chains %d groups %d critical_path %lld schedule %d slots %d\n", c.geom.nbk, nch,
-                   dag_groups(na), static_cast<long long>(c.critical_path), c.sched_fwd.ntask, c.sched_fwd.nslots);
+                   dag_groups(na, c.swc), static_cast<long long>(c.critical_path), c.sched_fwd.ntask, c.sched_fwd.nslots);
       for (size_t q = 0; q < ntask; ++q)
         std::fprintf(fh, "%llu %llu %llu %llu %llu %llu\n", h[6 * q], h[6 * q + 1], h[6 * q + 2], h[6 * q + 3],
                      h[6 * q + 4], h[6 * q + 5]);
@@ -2314,7 +2342,7 @@ int apply_filter_batched_at(zolo_ctx& c, const void* d_v, void* d_y, int64_t nco
     CK(cudaMemGetInfo(&free_b, &total_b));
     free_b += pool_cached_bytes();
     batch = std::max<int64_t>(1, static_cast<int64_t>(0.85 * free_b / per_col));
-    constexpr int64_t G = 32;  // columns per sweep task group (mma.cuh DCG)
+    constexpr int64_t G = 64;  // whole column groups of the widest sweep tasks
     if (batch >= G) {          // whole column groups, spread evenly over the batches
       const int64_t groups = (ncols + G - 1) / G, per = batch / G;
       const int64_t nbat = (groups + per - 1) / per;

@@ -148,74 +148,106 @@ __device__ __forceinline__ void mma_tile2(Acc8& acc, const cd* ts, const cd* xs,
 // additions are one per A and B fragment element per k-step -- 6 DMMAs + 3 adds per k-step for
 // the two 8x8 output blocks instead of 8 DMMAs. The result is normwise as accurate as the
 // 4-product form (each output is a sum of products bounded by |a||b|); only its rounding differs.
+template <int NB>  // 8-column output blocks per warp (16 columns apart)
 struct Acc3 {
-  double p[2][3][2];  // [half][P1 P2 P3][element]
+  double p[NB][3][2];  // [block][P1 P2 P3][element]
 };
-__device__ __forceinline__ void acc3_zero(Acc3& a) {
+template <int NB>
+__device__ __forceinline__ void acc3_zero(Acc3<NB>& a) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < NB; ++h)
 #pragma unroll
     for (int k = 0; k < 3; ++k) a.p[h][k][0] = a.p[h][k][1] = 0.0;
 }
-// out[2h + e] = the complex output (row, ocol(2h + e))
-__device__ __forceinline__ void acc3_fold(const Acc3& a, cd out[4]) {
+// out[2h + e] = the complex output (row, ocol_sw(2h + e))
+template <int NB>
+__device__ __forceinline__ void acc3_fold(const Acc3<NB>& a, cd out[2 * NB]) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < NB; ++h)
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       out[2 * h + e] = mk(a.p[h][0][e] - a.p[h][1][e], a.p[h][2][e] - a.p[h][0][e] - a.p[h][1][e]);
 }
-// acc += sg * block value (the add entries: b_i, partial sums), at output (row, ocol(2h + e))
-__device__ __forceinline__ void acc3_add(Acc3& a, int h, int e, cd v, double sg) {
+// acc += sg * block value (the add entries: b_i, partial sums), at output (row, ocol_sw(2h + e))
+template <int NB>
+__device__ __forceinline__ void acc3_add(Acc3<NB>& a, int h, int e, cd v, double sg) {
   a.p[h][0][e] += sg * v.x;          // Re = P1 - P2
   a.p[h][2][e] += sg * (v.x + v.y);  // Im = P3 - P1 - P2
 }
 
-template <bool OPH, bool NEG>
-__device__ __forceinline__ void mma_tile3_t(Acc3& acc, const cd* ts, const cd* xs, const Frag& f, unsigned km) {
-  if (km == 0) return;
-  __syncwarp();  // mma.sync.aligned needs a converged warp
-  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
-  const int bc = f.c0 + (f.lane >> 2);
-  const int sa = swz(ar);
-#pragma unroll
-  for (int k0 = 0; k0 < TILE / 4; k0 += 4) {  // fragments of 4 k-steps first: the shared-memory latency overlaps
-    cd a[4], b0[4], b1[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = 4 * (k0 + q) + am;
-      a[q] = OPH ? ts[ar * TILE + (k ^ sa)] : ts[k * TILE + (ar ^ swz(k))];
-      b0[q] = xs[bc * XPAD + k];
-      b1[q] = xs[(bc + 16) * XPAD + k];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (!((km >> (k0 + q)) & 1u)) continue;  // predicated off: ~1 issue cycle instead of a DMMA
-      const double re = NEG ? -a[q].x : a[q].x;
-      const double im = (NEG != OPH) ? -a[q].y : a[q].y;  // conj for op H, negated for the pre-transform
-      const double s = re + im;
-      dmma_nv(acc.p[0][0], re, b0[q].x);
-      dmma_nv(acc.p[1][0], re, b1[q].x);
-      dmma_nv(acc.p[0][1], im, b0[q].y);
-      dmma_nv(acc.p[1][1], im, b1[q].y);
-      dmma_nv(acc.p[0][2], s, b0[q].x + b0[q].y);
-      dmma_nv(acc.p[1][2], s, b1[q].x + b1[q].y);
-    }
-  }
+// The sweeps' x block (32 columns x 32 rows) as the tensor copy lands it (trsm.cu tma_xblock,
+// CU_TENSOR_MAP_SWIZZLE_128B): 128-byte lines of 8 complex rows, line = 32 (k / 8) + c, the
+// 16-byte chunk index XORed with line % 8 = c % 8. The sweeps' warps map their DMMA column
+// index n to column pcol(n) = n / 2 + 4 (n % 2) of their 8-column block, so the 8 lanes of a
+// B-fragment quarter warp (n = 2j, 2j + 1 at 4 consecutive rows) read columns j and j + 4:
+// 8 distinct chunks, conflict free without padding, and the address of a fragment is a per-lane
+// base plus a compile-time offset (per k-step parity).
+template <int XC>  // columns of the x block
+__device__ __forceinline__ int xsw(int c, int k) { return 8 * (XC * (k >> 3) + c) + ((k & 7) ^ (c & 7)); }
+__device__ __forceinline__ int pcol(int n) { return (n >> 1) + 4 * (n & 1); }
+// output column of acc3 entry q (= 2h + e) within the 32-column group, sweeps' column map
+__device__ __forceinline__ int ocol_sw(const Frag& f, int q) { return f.c0 + (f.lane & 3) + 4 * (q & 1) + 16 * (q >> 1); }
+
+// Per-lane fragment offsets of the sweeps' tile products, computed once per kernel, so one code
+// path serves all four (op N / op H) x (+ / -) products: tiles are XOR-swizzled (swz), x blocks
+// 128-byte swizzled (xsw). A fragment (row ar, k = 4 kk + am): op N at an + 128 kk; op H
+// (conjugate transpose) at ah[kk & 1] + 4 kk. B fragment (column bc, row k): xb[kk & 1] + 8 XC (kk / 2).
+struct TileOff {
+  int an, ah0, ah1, xb0, xb1;
+};
+template <int XC>
+__device__ __forceinline__ TileOff tile_off(const Frag& f) {
+  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3, sa = swz(ar);
+  const int bc = f.c0 + pcol(f.lane >> 2);
+  TileOff o;
+  o.an = 32 * am + (ar ^ swz(am));
+  const int t = 4 * (sa >> 2), h = 32 * ar + (am ^ (sa & 2));
+  o.ah0 = h + t;
+  o.ah1 = h - t;
+  o.xb0 = 8 * bc + (am ^ (bc & 3)) + (bc & 4);
+  o.xb1 = 8 * bc + (am ^ (bc & 3)) + (4 - (bc & 4));
+  return o;
+}
+__device__ __forceinline__ double flip_sign(double v, int hi_mask) {
+  return __hiloint2double(__double2hiint(v) ^ hi_mask, __double2loint(v));
 }
 
-__device__ __forceinline__ void mma_tile3(Acc3& acc, const cd* ts, const cd* xs, bool opH, bool neg, const Frag& f,
-                                          unsigned km) {
-  if (opH) {
-    if (neg)
-      mma_tile3_t<true, true>(acc, ts, xs, f, km);
-    else
-      mma_tile3_t<true, false>(acc, ts, xs, f, km);
-  } else {
-    if (neg)
-      mma_tile3_t<false, true>(acc, ts, xs, f, km);
-    else
-      mma_tile3_t<false, false>(acc, ts, xs, f, km);
+// acc += op(T) X (3M), or -= with neg (the pre-transform entry); km: the unmasked k-steps of
+// this warp's rows. op and sign are warp-uniform run-time values: the conjugation and the
+// negation are sign flips of the A fragment (integer pipe), the transpose an offset pattern.
+template <int XC, int NB>
+__device__ __forceinline__ void mma_tile3(Acc3<NB>& acc, const cd* ts, const cd* xs, bool opH, bool neg,
+                                          const TileOff& o, unsigned km) {
+  if (km == 0) return;
+  __syncwarp();  // mma.sync.aligned needs a converged warp
+  const int a0 = opH ? o.ah0 : o.an, a1 = opH ? o.ah1 : o.an, ash = opH ? 2 : 7;
+  const int mre = neg ? static_cast<int>(0x80000000u) : 0;
+  const int mim = (neg != opH) ? static_cast<int>(0x80000000u) : 0;  // conj for op H, negated for the pre-transform
+  constexpr int KG = NB > 2 ? 2 : 4;  // k-steps whose fragments are loaded together (register budget)
+#pragma unroll
+  for (int k0 = 0; k0 < TILE / 4; k0 += KG) {  // fragments of KG k-steps first: the shared-memory latency overlaps
+    cd a[KG], b[KG][NB];
+#pragma unroll
+    for (int q = 0; q < KG; ++q) {
+      const int kk = k0 + q;
+      a[q] = ts[((kk & 1) ? a1 : a0) + (kk << ash)];
+      const int xo = ((kk & 1) ? o.xb1 : o.xb0) + 8 * XC * (kk >> 1);
+#pragma unroll
+      for (int h = 0; h < NB; ++h) b[q][h] = xs[xo + 128 * h];  // column bc + 16 h
+    }
+#pragma unroll
+    for (int q = 0; q < KG; ++q) {
+      if (!((km >> (k0 + q)) & 1u)) continue;  // predicated off: ~1 issue cycle instead of a DMMA
+      const double re = flip_sign(a[q].x, mre);
+      const double im = flip_sign(a[q].y, mim);
+      const double s = re + im;
+#pragma unroll
+      for (int h = 0; h < NB; ++h) dmma_nv(acc.p[h][0], re, b[q][h].x);
+#pragma unroll
+      for (int h = 0; h < NB; ++h) dmma_nv(acc.p[h][1], im, b[q][h].y);
+#pragma unroll
+      for (int h = 0; h < NB; ++h) dmma_nv(acc.p[h][2], s, b[q][h].x + b[q][h].y);
+    }
   }
 }
 

@@ -59,7 +59,16 @@ struct Chain {
   cd* cbuf;        // chunk tasks' partial sums (32 * nslots rows x ncols)
   int mode;
   int pad;
+  // three TMA tensor maps in device memory (encode_xblock_map): src, dst, cbuf. The sweeps load a
+  // 32-row x 32-column block of them with one cp.async.bulk.tensor into the 128-byte swizzled
+  // shared-memory layout the DMMA fragments read conflict free (mma.cuh xsw)
+  const unsigned char* tmaps;
 };
+constexpr int XMAP_BYTES = 128;  // sizeof(CUtensorMap)
+// x-block tensor map of a column-major complex block (ld rows, ncols columns; ld a multiple of 32)
+// into `map` (XMAP_BYTES, 64-byte aligned). False when the driver cannot encode it.
+// x blocks of swc (32 or 64) columns
+bool encode_xblock_map(void* map, const cd* base, int64_t ld, int64_t ncols, int swc);
 
 struct FactorDevState {
   int* fail_index;                    // first rejected pivot (device, -1 = none)
@@ -135,9 +144,11 @@ struct DagSched {
 // tasks of a fully converged column group are skipped. trace (optional): per-task timestamps.
 // Returns the grid size, or -1 when the chains exceed the kernel's limit.
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
-                    int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int num_sms,
-                    unsigned long long* trace = nullptr, const int* gact = nullptr, const int* gdone = nullptr);
-int dag_groups(int ncols);
+                    int ncols, int swc, int64_t ld, int64_t ldp, int* flags, int* cflags, int epoch, int* counter,
+                    int num_sms, unsigned long long* trace = nullptr, const int* gact = nullptr,
+                    const int* gdone = nullptr);
+// column groups of swc (32 or 64) columns: the sweep tasks' width
+int dag_groups(int ncols, int swc);
 
 // x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass
 // x_i = DinvL_i^H w_i); x is ld x ncols, D is nbk tiles.

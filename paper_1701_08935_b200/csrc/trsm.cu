@@ -17,6 +17,7 @@
 // mma.sync.m8n8k4.f64 (DMMA, the only FP64 tensor-core path on sm_100a:
 // tcgen05.mma has no f64 kind), fed by a warp-specialised producer through a
 // ring of shared-memory stages filled with cp.async.bulk (the TMA engine).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -125,21 +126,23 @@ __device__ __forceinline__ void load_x(cd* xs, const cd* base, int64_t ld, int c
 // product or add the block into the accumulators, and release the stage on
 // its empty barrier. The ring runs across task boundaries, and no CTA-wide
 // barrier sits on the per-tile path; only the epilogue syncs the consumer
-// warps (named barrier) before the release of u_i.
+// warps: the last one to finish a task (a per-stage shared-memory count) releases u_i.
 // ---------------------------------------------------------------------------
-#ifndef ZOLO_NST2
-#define ZOLO_NST2 3
-#endif
-#ifndef ZOLO_V2_MINB
-#define ZOLO_V2_MINB 2
-#endif
-#ifndef ZOLO_SWEEP_3M
-#define ZOLO_SWEEP_3M 1  // complex tile products as 3 real DMMAs (mma.cuh mma_tile3); 0: 4 DMMAs
-#endif
-constexpr int NST2 = ZOLO_NST2;
+// Sweep task shape (template W): W columns per task (one tile load serves W columns); 8 consumer
+// warps, each 8 rows x W / 2 columns (W / 16 8-column DMMA blocks, 16 apart); a ring of NST
+// stages (tile + x block), MINB CTAs per SM. W = 64 for wide blocks (half the tile traffic and
+// task overhead per column), 32 when the block has fewer than 128 columns (zolo_ctx::swc).
+template <int W>
+struct Shape {
+  static constexpr int NB = W / 16;               // DMMA column blocks per warp
+  static constexpr int NST = W == 64 ? 4 : 3;     // ring stages
+  static constexpr int MINB = W == 64 ? 1 : 2;    // CTAs per SM
+  static constexpr int XS = W * TILE;             // x block: W columns x 32 rows, 128-byte swizzled (mma.cuh xsw)
+};
 constexpr int DAG_TRACE_WORDS = 6;  // claim, -, consumer done, info, wait ns, producer done (tools/dag2_trace_analyze.py)
 constexpr int TSW = TT;             // swizzled (unpadded) tile
-constexpr int P2T = ST + 32;        // threads: 8 consumer warps + the producer warp
+constexpr int CW = ST / 32;         // consumer warps
+constexpr int P2T = ST + 32;        // threads: the consumer warps + the producer warp
 constexpr int DAG2_CHAINS = 32;
 
 struct DagArgs {
@@ -170,8 +173,13 @@ struct Meta2 {
   unsigned mx, my;  // occupancy mask (op N / op H)
   int last, i, ci, gi, out, nc, t, pad;
 };
-constexpr int DAG2_SMEM = NST2 * (TSW + XS2) * static_cast<int>(sizeof(cd)) + NST2 * static_cast<int>(sizeof(Meta2)) +
-                          2 * NST2 * 8 + DAG2_CHAINS * static_cast<int>(sizeof(Chain)) + DAG_REC * 4;
+// stages are 1024-byte aligned (the 128-byte swizzle pattern of the tensor copies repeats every 1 KiB)
+template <int W>
+constexpr int dag2_smem() {
+  return 1024 + Shape<W>::NST * (TSW + Shape<W>::XS) * static_cast<int>(sizeof(cd)) +
+         Shape<W>::NST * static_cast<int>(sizeof(Meta2)) + 2 * Shape<W>::NST * 8 +
+         DAG2_CHAINS * static_cast<int>(sizeof(Chain)) + DAG_REC * 4 + Shape<W>::NST * 4;
+}
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
@@ -203,7 +211,17 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(ST) : "memory"); }
+// 32 rows (row groups 4 rb .. 4 rb + 3 of the map's 8-row groups) x 32 columns (c0 ..) of a
+// block through its tensor map (encode_xblock_map), one TMA instruction, completing on the
+// stage's mbarrier; columns beyond the map's extent are zero-filled
+__device__ __forceinline__ void tma_xblock(void* dst, const unsigned char* tmap, int rb, int c0,
+                                           unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(0), "r"(c0), "r"(4 * rb), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 
 // lane 0 spins on *f >= epoch (bounded: a lost producer is reported through err, never a hung
 // GPU), then the warp reconverges
@@ -226,49 +244,51 @@ __device__ __forceinline__ void warp_wait_flag(const int* f, int epoch, int* err
 //   chunk task: partial_out = sum_q op(T~(i, j_q)) u_(j_q)
 // The pre-transform op(Dinv_i) b_i is ring entry 0 with a negated A operand,
 // so the accumulator holds S = sum - pre(b) and u_i = -S.
-__global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
-  extern __shared__ __align__(16) unsigned char sm2[];
+template <int W>
+__global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
+  constexpr int NST2 = Shape<W>::NST, XSW = Shape<W>::XS, NBW = Shape<W>::NB, SWC = W;
+  extern __shared__ __align__(1024) unsigned char sm2_raw[];
+  unsigned char* sm2 = sm2_raw + ((1024u - (smem_u32(sm2_raw) & 1023u)) & 1023u);
   cd* ring = reinterpret_cast<cd*>(sm2);
-  Meta2* meta = reinterpret_cast<Meta2*>(sm2 + NST2 * (TSW + XS2) * sizeof(cd));
+  Meta2* meta = reinterpret_cast<Meta2*>(sm2 + NST2 * (TSW + XSW) * sizeof(cd));
   unsigned long long* full = reinterpret_cast<unsigned long long*>(meta + NST2);
   unsigned long long* empty = full + NST2;
   Chain* chs = reinterpret_cast<Chain*>(empty + NST2);
   int* recp = reinterpret_cast<int*>(chs + DAG2_CHAINS);
-  auto tile_s = [ring](int s) { return ring + s * (TSW + XS2); };
-  auto x_s = [ring](int s) { return ring + s * (TSW + XS2) + TSW; };
+  unsigned* done = reinterpret_cast<unsigned*>(recp + DAG_REC);  // per stage: consumer warps done with a task
+  auto tile_s = [ring](int s) { return ring + s * (TSW + XSW); };
+  auto x_s = [ring](int s) { return ring + s * (TSW + XSW) + TSW; };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int q = threadIdx.x; q < A.nchains; q += blockDim.x) chs[q] = A.chains[q];
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST2; ++s) {
       mbar_init(full + s, 1);  // the producer's arrive (+ the stage's bulk-copy bytes)
-      mbar_init(empty + s, ST / 32);
+      mbar_init(empty + s, CW);
+      done[s] = 0;
     }
   }
   __syncthreads();
   const int per_step = A.nchains * A.ngroups;
   const int ntasks = A.ntask * per_step;
-  if (warp == ST / 32) {
+  if (warp == CW) {
     // ------------------------------ producer ------------------------------
     const unsigned long long pol_stream = l2_evict_first(), pol_tile = l2_policy(A.policy & 3),
                              pol_keep = l2_policy((A.policy >> 2) & 3);
     int g = 0;
     int cur_t = 0;  // claim index of the task being produced (trace)
-    // one ring entry: tile (optional) + a 32 x 32 block with column stride `stride`
-    auto produce = [&](int kind, int sign, const cd* tile, uint2 mw, const cd* blk, int64_t stride, int c0, int nc,
-                       unsigned long long pol, int last, int i, int ci, int gi, int out) {
+    // one ring entry: tile (optional) + the 32 x 32 block (block row rb, columns c0..) of the
+    // chain's buffer behind tensor map `xmap` (kind 2, the end marker: nothing)
+    auto produce = [&](int kind, int sign, const cd* tile, uint2 mw, const unsigned char* xmap, int rb, int c0,
+                       int nc, unsigned long long pol, int last, int i, int ci, int gi, int out) {
       const int s = g % NST2, round = g / NST2;
       mbar_wait(empty + s, (round & 1) ^ 1);
-      const unsigned bytes = (tile ? static_cast<unsigned>(TT * sizeof(cd)) : 0u) +
-                             static_cast<unsigned>(nc) * TILE * static_cast<unsigned>(sizeof(cd));
-      if (lane == 0) mbar_expect_tx(full + s, bytes);
-      __syncwarp();
-      if (tile && lane == 0) bulk_copy(tile_s(s), tile, TT * sizeof(cd), full + s, pol_tile);
-      cd* xs = x_s(s);
-      if (lane < nc)
-        bulk_copy(xs + lane * XPAD, blk + (c0 + lane) * stride, TILE * sizeof(cd), full + s, pol);
-      else
-        for (int r = 0; r < TILE; ++r) xs[lane * XPAD + r] = mk(0.0, 0.0);
-      __syncwarp();
+      if (lane == 0) {
+        const unsigned bytes = (tile ? static_cast<unsigned>(TT * sizeof(cd)) : 0u) +
+                               (kind != 2 ? static_cast<unsigned>(XSW * sizeof(cd)) : 0u);
+        mbar_expect_tx(full + s, bytes);
+        if (tile) bulk_copy(tile_s(s), tile, TT * sizeof(cd), full + s, pol_tile);
+        if (kind != 2) tma_xblock(x_s(s), xmap, rb, c0, full + s, pol);
+      }
       if (lane == 0) {
         Meta2 m;
         m.kind = kind;
@@ -298,11 +318,14 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     unsigned gmask = 0;
     if (A.gdone && A.ngroups <= 32) {
       for (int gg = 0; gg < A.ngroups; ++gg) {
-        const int cg0 = gg * DCG, ncg = min(DCG, A.ncols - cg0);
-        if (__all_sync(0xffffffffu, lane >= ncg || A.gdone[A.gact[cg0 + lane]] != 0)) gmask |= 1u << gg;
+        const int cg0 = gg * SWC, ncg = min(SWC, A.ncols - cg0);
+        bool all = true;
+        for (int h = 0; h < SWC; h += 32)
+          all = __all_sync(0xffffffffu, h + lane >= ncg || A.gdone[A.gact[cg0 + h + lane]] != 0) && all;
+        if (all) gmask |= 1u << gg;
       }
       if (gmask == (A.ngroups == 32 ? ~0u : (1u << A.ngroups) - 1u)) {  // nothing left: leave at once
-        produce(2, 0, nullptr, make_uint2(0u, 0u), A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
+        produce(2, 0, nullptr, make_uint2(0u, 0u), nullptr, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
         return;
       }
     }
@@ -322,7 +345,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     if (lane == 0) tn_raw = atomicAdd(A.counter, 1);
     for (;;) {
       if (t >= ntasks) {
-        produce(2, 0, nullptr, make_uint2(0u, 0u), A.chains[0].src, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
+        produce(2, 0, nullptr, make_uint2(0u, 0u), nullptr, 0, 0, 0, pol_stream, 1, 0, 0, 0, -1);
         break;
       }
       const int tn = __shfl_sync(0xffffffffu, tn_raw, 0);
@@ -346,7 +369,7 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       const int i = recp[0], nd = recp[1], pa = recp[2], pc = recp[3], out = recp[4];
       const bool chunk = out >= 0;
       const Chain& ch = chs[ci];
-      const int c0 = gi * DCG, nc = min(DCG, A.ncols - c0);
+      const int c0 = gi * SWC, nc = min(SWC, A.ncols - c0);
       const size_t cgi = static_cast<size_t>(ci) * A.ngroups + gi;
       const int* flags = A.flags + cgi * A.s.nb;
       const int* cflags = A.cflags + cgi * A.nslots;
@@ -370,11 +393,10 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
           ++e;
           const uint2 pm = mask_of(31);
           if (ch.pre)
-            produce(0, 1, ch.pre + static_cast<size_t>(i) * TT, pm, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0,
-                    nc, pol_stream, e == nent, i, ci, gi, out);
+            produce(0, 1, ch.pre + static_cast<size_t>(i) * TT, pm, ch.tmaps, i, c0, nc, pol_stream, e == nent, i, ci,
+                    gi, out);
           else
-            produce(1, -1, nullptr, pm, ch.src + static_cast<int64_t>(i) * TILE, A.ld, c0, nc, pol_stream, e == nent, i,
-                    ci, gi, out);
+            produce(1, -1, nullptr, pm, ch.tmaps, i, c0, nc, pol_stream, e == nent, i, ci, gi, out);
         }
         for (int p0 = 0; p0 < pc; p0 += 32) {
           const unsigned prdy =
@@ -386,8 +408,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
               if (trp) wsum += gtimer() - tw;
             }
             ++e;
-            produce(1, 1, nullptr, make_uint2(0xffffffffu, 0xffffffffu), ch.cbuf + static_cast<int64_t>(pa + p) * TILE,
-                    A.ldp, c0, nc, pol_stream, e == nent, i, ci, gi, out);
+            produce(1, 1, nullptr, make_uint2(0xffffffffu, 0xffffffffu), ch.tmaps + 2 * XMAP_BYTES, pa + p, c0, nc,
+                    pol_stream, e == nent, i, ci, gi, out);
           }
         }
         for (int q = 0; q < nd; ++q) {
@@ -398,8 +420,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
             if (trp) wsum += gtimer() - tw;
           }
           ++e;
-          produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, mask_of(q), ch.dst + static_cast<int64_t>(j) * TILE,
-                  A.ld, c0, nc, pol_keep, e == nent, i, ci, gi, out);
+          produce(0, 0, ch.off + static_cast<size_t>(tid) * TT, mask_of(q), ch.tmaps + XMAP_BYTES, j, c0, nc, pol_keep,
+                  e == nent, i, ci, gi, out);
         }
       }
       __syncwarp();
@@ -414,14 +436,11 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     return;
   }
   // ------------------------------ consumers ------------------------------
+  // warp w: rows as frag(), columns 8 ((w / 4) % 2) + 16 h, h < NBW, of the task's SWC
   const Frag f = frag();
-#if ZOLO_SWEEP_3M
-  Acc3 acc;  // 3M complex products (mma.cuh)
+  const TileOff toff = tile_off<SWC>(f);
+  Acc3<NBW> acc;  // 3M complex products (mma.cuh)
   acc3_zero(acc);
-#else
-  Acc8 acc;
-  acc8_zero(acc);
-#endif
   int ntiles_task = 0;  // (trace) tile products of the current task
   for (int g = 0;; ++g) {
     const int s = g % NST2, round = g / NST2;
@@ -432,57 +451,49 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
     const bool opH = ch.mode == FWD_UH || ch.mode == BWD_LH;
     ntiles_task += m.kind == 0;
     if (m.kind == 0) {
-#if ZOLO_SWEEP_3M
-      mma_tile3(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
-#else
-      mma_tile2(acc, tile_s(s), x_s(s), opH, m.sign != 0, f, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
-#endif
+      mma_tile3<SWC, NBW>(acc, tile_s(s), x_s(s), opH, m.sign != 0, toff, ((opH ? m.my : m.mx) >> f.r0) & 0xffu);
     } else {
       const cd* xs = x_s(s);
       const double sg = static_cast<double>(m.sign);
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < NBW; ++h)
 #pragma unroll
         for (int e2 = 0; e2 < 2; ++e2) {
-          const cd v = xs[ocol(f, 2 * h + e2) * XPAD + f.row];
-#if ZOLO_SWEEP_3M
+          const cd v = xs[xsw<SWC>(ocol_sw(f, 2 * h + e2), f.row)];
           acc3_add(acc, h, e2, v, sg);
-#else
-          acc.v[h][0][0][e2] += sg * v.x;
-          acc.v[h][0][1][e2] += sg * v.y;
-#endif
         }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + s);
     if (m.last) {
-      cd o[4];
-#if ZOLO_SWEEP_3M
+      cd o[2 * NBW];
       acc3_fold(acc, o);
       acc3_zero(acc);
-#else
-      acc8_fold(acc, o);
-      acc8_zero(acc);
-#endif
       const bool chunk = m.out >= 0;
-      const int c0 = m.gi * DCG;
+      const int c0 = m.gi * SWC;
       if (chunk) {
         cd* prow = ch.cbuf + static_cast<int64_t>(m.out) * TILE + f.row + c0 * A.ldp;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c = ocol(f, q);
+        for (int q = 0; q < 2 * NBW; ++q) {
+          const int c = ocol_sw(f, q);
           if (c < m.nc) prow[c * A.ldp] = o[q];
         }
       } else {
         cd* urow = ch.dst + static_cast<int64_t>(m.i) * TILE + f.row + c0 * A.ld;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c = ocol(f, q);
+        for (int q = 0; q < 2 * NBW; ++q) {
+          const int c = ocol_sw(f, q);
           if (c < m.nc) urow[c * A.ld] = mk(-o[q].x, -o[q].y);
         }
       }
-      consumers_sync();
-      if (threadIdx.x == 0) {
+      // the last consumer warp to finish the task publishes it: each warp's stores are ordered
+      // before its acq_rel count (syncwarp + cta-scope release), the last warp's gpu-scope release
+      // is cumulative over them. The stage is released only after the count, so the counter of
+      // stage s is reset before the stage can carry another task's last entry.
+      __syncwarp();
+      unsigned prev = 0;
+      if (lane == 0)
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(smem_u32(done + s)) : "memory");
+      if (lane == 0 && prev == CW - 1) {
+        done[s] = 0;
         const size_t cgi = static_cast<size_t>(m.ci) * A.ngroups + m.gi;
         st_release(chunk ? A.cflags + cgi * A.nslots + m.out : A.flags + cgi * A.s.nb + m.i, A.epoch);
         if (A.trace) {
@@ -496,6 +507,8 @@ __global__ void __launch_bounds__(P2T, ZOLO_V2_MINB) dag2_kernel(DagArgs A) {
       }
       ntiles_task = 0;
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
   }
 }
 
@@ -527,24 +540,49 @@ __global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd
 
 }  // namespace
 
+bool encode_xblock_map(void* map, const cd* base, int64_t ld, int64_t ncols, int swc) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static const Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<Encode>(nullptr);
+    return reinterpret_cast<Encode>(fn);
+  }();
+  static_assert(sizeof(CUtensorMap) == XMAP_BYTES, "tensor map size");
+  if (!encode || !base || ld % TILE != 0 || ncols < 1 || (swc != 32 && swc != 64)) return false;
+  // doubles, 3D: (16 doubles = 8 complex rows: one 128-byte swizzle line, ncols, ld / 8 row groups);
+  // the box lands as [row group][column][8 rows] (mma.cuh xsw)
+  const cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(ncols), static_cast<cuuint64_t>(ld / 8)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * sizeof(cd), 128};
+  const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(swc), TILE / 8};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<cd*>(base), dims,
+                strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
   if (ncols > 0) blockdiag_kernel<<<dim3(nb, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld);
 }
 
-int dag_groups(int ncols) { return (ncols + DCG - 1) / DCG; }
+int dag_groups(int ncols, int swc) { return (ncols + swc - 1) / swc; }
 
 int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, const Chain* d_chains, int nchains,
-                    int ncols, int64_t ld, int* flags, int* cflags, int epoch, int* counter, int num_sms,
-                    unsigned long long* trace, const int* gact, const int* gdone) {
+                    int ncols, int swc, int64_t ld, int64_t ldp, int* flags, int* cflags, int epoch, int* counter,
+                    int num_sms, unsigned long long* trace, const int* gact, const int* gdone) {
   if (nchains > DAG2_CHAINS) return -1;
   DagArgs a;
   a.chains = d_chains;
   a.nchains = nchains;
-  a.ngroups = (ncols + DCG - 1) / DCG;
+  a.ngroups = dag_groups(ncols, swc);
   a.ncols = ncols;
   a.epoch = epoch;
   a.ld = ld;
-  a.ldp = static_cast<int64_t>(sched.nslots) * TILE;
+  a.ldp = ldp;  // the chains' cbuf (and their tensor maps) are sized for the larger of the two schedules
   a.recs = sched.recs;
   a.ntask = sched.ntask;
   a.nslots = sched.nslots;
@@ -561,11 +599,18 @@ int dag_trsm_launch(cudaStream_t st, const SpGeom& s, const DagSched& sched, con
   }();
   a.policy = policy;
   // the attribute is per device: set it on every launch (a process may drive several GPUs)
-  cudaFuncSetAttribute(dag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DAG2_SMEM);
+  if (swc != 32 && swc != 64) return -1;
+  cudaFuncSetAttribute(dag2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, dag2_smem<32>());
+  cudaFuncSetAttribute(dag2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, dag2_smem<64>());
   cudaMemsetAsync(counter, 0, sizeof(int), st);
   const int ntasks = sched.ntask * nchains * a.ngroups;
-  const int grid = std::min(ntasks, num_sms * ZOLO_V2_MINB);
-  if (grid > 0) dag2_kernel<<<grid, P2T, DAG2_SMEM, st>>>(a);
+  const int grid = std::min(ntasks, num_sms * (swc == 64 ? Shape<64>::MINB : Shape<32>::MINB));
+  if (grid > 0) {
+    if (swc == 64)
+      dag2_kernel<64><<<grid, P2T, dag2_smem<64>(), st>>>(a);
+    else
+      dag2_kernel<32><<<grid, P2T, dag2_smem<32>(), st>>>(a);
+  }
   return grid;
 }
 
