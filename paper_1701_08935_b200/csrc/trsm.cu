@@ -235,6 +235,7 @@ __device__ __forceinline__ void warp_wait_flag(const int* f, int epoch, int* err
         break;
       }
     }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the block is then read by a tensor copy
   }
   __syncwarp();
 }
@@ -375,6 +376,9 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
       const int* cflags = A.cflags + cgi * A.nslots;
       // every task of a fully converged column group skips (its dependents are in the same group)
       if (!((gmask >> gi) & 1u)) {
+        // the dependencies' blocks were written by generic stores (published by st.release); the
+        // tensor copies read them through the async proxy: order the acquires before them
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         // occupancy masks of all the task's tiles (lane q: dependency q, lane 31: the pre-transform)
         // and readiness of every dependency, each read in parallel (one round trip)
         uint2 my_mask = make_uint2(0xffffffffu, 0xffffffffu);
