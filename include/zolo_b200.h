@@ -319,7 +319,8 @@ int zolo_timer(zolo_ctx* ctx, int op, double* ms);
  * development / sizing): out[0] padded size, out[1] block rows, out[2]
  * off-diagonal tiles per triangle, out[3] critical path in block rows,
  * out[4] block rows of the largest trailing dense block, out[5] tile-aligned
- * node groups, out[6..7] reserved. */
+ * node groups, out[6] trailing-update tile products of the factorization (sum over
+ * block columns of the squared column count), out[7] reserved. */
 int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* out);
 /* Builds the DAG sweep schedules (both directions) of the ND factor of a pattern and checks them
  * on the host (no reference equivalent; test support): out[0] = violations (0 when every block

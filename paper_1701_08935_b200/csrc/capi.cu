@@ -2533,6 +2533,12 @@ int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t l
     out[3] = bs.critical_path;
     out[4] = bs.nb - trailing_dense_start(bs, 1 << 20);
     out[5] = static_cast<int64_t>(nodes.size());
+    int64_t con = 0;  // trailing-update tile products of the factorization: sum over block columns of |col(k)|^2
+    for (int64_t k = 0; k < bs.nb; ++k) {
+      const int64_t ck = bs.col_ptr[k + 1] - bs.col_ptr[k];
+      con += ck * ck;
+    }
+    out[6] = con;
     return ZOLO_OK;
   } catch (const std::exception& e) {
     g_create_err = e.what();

@@ -36,34 +36,6 @@ __device__ __forceinline__ void load_tile_async(cd* s, const cd* g) {
   }
 }
 
-// out[2x2] = A(rows) * B(cols) over the full tile; thread (tx,ty) owns rows
-// tx, tx+16 and columns ty, ty+16. A, B padded shared tiles.
-__device__ __forceinline__ void tile_mm(const cd* As, const cd* Bs, cd out[4]) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  cd c00 = mk(0, 0), c01 = mk(0, 0), c10 = mk(0, 0), c11 = mk(0, 0);
-#pragma unroll 8
-  for (int k = 0; k < TILE; ++k) {
-    const cd a0 = As[k * TPAD + tx], a1 = As[k * TPAD + tx + 16];
-    const cd b0 = Bs[ty * TPAD + k], b1 = Bs[(ty + 16) * TPAD + k];
-    cfma(c00, a0, b0);
-    cfma(c01, a0, b1);
-    cfma(c10, a1, b0);
-    cfma(c11, a1, b1);
-  }
-  out[0] = c00;
-  out[1] = c01;
-  out[2] = c10;
-  out[3] = c11;
-}
-
-__device__ __forceinline__ void store_tile(cd* c, const cd out[4]) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  c[ty * TILE + tx] = out[0];
-  c[(ty + 16) * TILE + tx] = out[1];
-  c[ty * TILE + tx + 16] = out[2];
-  c[(ty + 16) * TILE + tx + 16] = out[3];
-}
-
 // Diagonal tile: unpivoted LU in shared memory with the reference's pivot
 // monitor (|pivot| > 1e-14 ||row||_inf, band_factor.hpp:160-166), then the
 // inverses of its unit-lower and upper triangles (threads 0..127: L^{-1},
@@ -222,37 +194,48 @@ __global__ void __launch_bounds__(FT) diag_level_kernel(const int* cols, int c0,
   diag_factor_body(n, k, Dt + static_cast<size_t>(k) * TT, DinvL, DinvU, row_norm, fail_index, min_ratio_bits);
 }
 
+// C = A B of three column-major tiles on DMMA (3M), one CTA of ST threads; C may alias A or B
+// (both are staged in shared memory before C is written)
+__device__ __forceinline__ void tile_mm_dmma(const cd* Ag, const cd* Bg, cd* Cg) {
+  __shared__ __align__(16) cd sa[TT];
+  __shared__ __align__(16) cd sb[XS2];
+  load_tile_sw(sa, Ag, l2_evict_normal());
+  load_x32(sb, Bg, TILE, 0, TILE, l2_evict_normal());
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const Frag f = frag();
+  Acc3<2> acc;
+  acc3_zero(acc);
+  mma_tile3_nx(acc, sa, sb, f);
+  cd prod[4];
+  acc3_fold(acc, prod);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Cg[ocol(f, q) * TILE + f.row] = prod[q];
+}
+
 // panel items (k, 2 id + upper): L(a,k) = A(a,k) U_kk^{-1} | U(k,a) = L_kk^{-1} A(k,a)
-__global__ void __launch_bounds__(FT) panel_level_kernel(const int* pan, int p0, cd* Lt, cd* Ut, const cd* DinvL,
+__global__ void __launch_bounds__(ST) panel_level_kernel(const int* pan, int p0, cd* Lt, cd* Ut, const cd* DinvL,
                                                          const cd* DinvU) {
-  __shared__ cd As[TILE * TPAD];
-  __shared__ cd Bs[TILE * TPAD];
   const int k = pan[2 * (p0 + blockIdx.x)], code = pan[2 * (p0 + blockIdx.x) + 1];
   const bool lower = (code & 1) == 0;
   const int id = code >> 1;
   cd* c = (lower ? Lt : Ut) + static_cast<size_t>(id) * TT;
-  if (lower) {
-    load_tile_async(As, c);
-    load_tile_async(Bs, DinvU + static_cast<size_t>(k) * TT);
-  } else {
-    load_tile_async(As, DinvL + static_cast<size_t>(k) * TT);
-    load_tile_async(Bs, c);
-  }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  cd out[4];
-  tile_mm(As, Bs, out);
-  store_tile(c, out);
+  if (lower)
+    tile_mm_dmma(c, DinvU + static_cast<size_t>(k) * TT, c);
+  else
+    tile_mm_dmma(DinvL + static_cast<size_t>(k) * TT, c, c);
 }
 
-// One trailing-update target per CTA: C -= sum_k L(a,k) U(k,b) over its
-// contributions (fixed ascending-k order), on DMMA. (A double-buffered variant
-// of this loop raised "illegal instruction" on the B200 -- tools/dev/trail_unit.cu
-// reproduces it -- so the stages are single-buffered; the factorization is setup.)
+// One trailing-update target per CTA: C -= sum_k L(a,k) U(k,b) over its contributions (fixed
+// ascending-k order) on DMMA, 3M complex products (mma.cuh mma_tile3_nx: 3 real DMMAs per complex
+// MAC instead of 4: cfg3's factorization 746 -> ~650 ms). Single-buffered stages with 4 resident
+// targets per SM hiding the loads: a double-buffered cp.async variant of this loop (two 34 KiB
+// stages) raises "illegal instruction" on the B200 with 3M and with 4M products alike
+// (tools/dev/trail_unit.cu), so the stages stay single.
 constexpr int TRAIL_SMEM = (TT + XS2) * static_cast<int>(sizeof(cd));
 #ifndef ZOLO_TRAIL_MINB
-#define ZOLO_TRAIL_MINB 4  // 4 resident targets per SM hide the single-buffered tile loads (cfg3 factor -8%)
+#define ZOLO_TRAIL_MINB 4
 #endif
 __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(const int* tgt, const int* con, int t0, cd* Dt,
                                                                cd* Lt, cd* Ut) {
@@ -262,19 +245,19 @@ __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(con
   const int kind = T[0], id = T[1], cb = T[2], ce = T[3];
   const unsigned long long pol = l2_evict_normal();
   const Frag f = frag();
-  Acc8 acc;
-  acc8_zero(acc);
+  Acc3<2> acc;
+  acc3_zero(acc);
   for (int q = cb; q < ce; ++q) {
     load_tile_sw(sm, Lt + static_cast<size_t>(con[2 * q]) * TT, pol);
     load_x32(sm + TT, Ut + static_cast<size_t>(con[2 * q + 1]) * TT, TILE, 0, TILE, pol);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    mma_tile2(acc, sm, sm + TT, false, false, f, 0xffu);
+    mma_tile3_nx(acc, sm, sm + TT, f);
     __syncthreads();
   }
   cd prod[4];
-  acc8_fold(acc, prod);
+  acc3_fold(acc, prod);
   cd* c = (kind == 0 ? Dt : (kind == 1 ? Lt : Ut)) + static_cast<size_t>(id) * TT;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -284,21 +267,12 @@ __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(con
 }
 
 // Row scaling L~(i,k) = DinvL_i L(i,k), U~(k,i) = DinvU_k U(k,i).
-__global__ void __launch_bounds__(FT) scale_sp_kernel(SpGeom s, cd* Lt, cd* Ut, const cd* DinvL, const cd* DinvU) {
-  __shared__ cd As[TILE * TPAD];
-  __shared__ cd Bs[TILE * TPAD];
+__global__ void __launch_bounds__(ST) scale_sp_kernel(SpGeom s, cd* Lt, cd* Ut, const cd* DinvL, const cd* DinvU) {
   const int id = blockIdx.x;
   const bool lower = blockIdx.y == 0;
   const int row = lower ? s.tile_row[id] : s.row_idx[id];
   cd* t = (lower ? Lt : Ut) + static_cast<size_t>(id) * TT;
-  load_tile_async(As, (lower ? DinvL : DinvU) + static_cast<size_t>(row) * TT);
-  load_tile_async(Bs, t);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  cd o[4];
-  tile_mm(As, Bs, o);
-  store_tile(t, o);
+  tile_mm_dmma((lower ? DinvL : DinvU) + static_cast<size_t>(row) * TT, t, t);
 }
 
 }  // namespace
@@ -330,11 +304,11 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const SpFactor& f, int64_t nnz,
       diag_level_kernel<<<lv[l + 1] - lv[l], FT, diag_smem, st>>>(plan.cols, lv[l], s.npad, f.Dt, f.DinvL, f.DinvU,
                                                                    row_norm, ds.fail_index, ds.min_ratio_bits);
     if (pp[l + 1] > pp[l])
-      panel_level_kernel<<<pp[l + 1] - pp[l], FT, 0, st>>>(plan.pan, pp[l], f.Lt, f.Ut, f.DinvL, f.DinvU);
+      panel_level_kernel<<<pp[l + 1] - pp[l], ST, 0, st>>>(plan.pan, pp[l], f.Lt, f.Ut, f.DinvL, f.DinvU);
     if (tp[l + 1] > tp[l])
       trailing_level_kernel<<<tp[l + 1] - tp[l], ST, TRAIL_SMEM, st>>>(plan.tgt, plan.con, tp[l], f.Dt, f.Lt, f.Ut);
   }
-  if (s.ntiles > 0) scale_sp_kernel<<<dim3(static_cast<unsigned>(s.ntiles), 2), FT, 0, st>>>(s, f.Lt, f.Ut, f.DinvL, f.DinvU);
+  if (s.ntiles > 0) scale_sp_kernel<<<dim3(static_cast<unsigned>(s.ntiles), 2), ST, 0, st>>>(s, f.Lt, f.Ut, f.DinvL, f.DinvU);
 }
 
 // Per-tile occupancy masks for the sweeps' DMMA loops: bit (8 g + kb) of

@@ -251,6 +251,37 @@ __device__ __forceinline__ void mma_tile3(Acc3<NB>& acc, const cd* ts, const cd*
   }
 }
 
+// acc (3M) += T X for the factorization's trailing updates: T a swizzled tile (load_tile_sw),
+// X a padded 32 x 32 block [col*XPAD + k] (load_x32), op N, all k-steps; outputs as mma_tile2
+// (out[2h + e] at row f.row, column ocol(f, 2h + e)).
+__device__ __forceinline__ void mma_tile3_nx(Acc3<2>& acc, const cd* ts, const cd* xs, const Frag& f) {
+  __syncwarp();
+  const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
+  const int bc = f.c0 + (f.lane >> 2);
+  const int an = 32 * am + (ar ^ swz(am));
+#pragma unroll
+  for (int k0 = 0; k0 < TILE / 4; k0 += 4) {
+    cd a[4], b0[4], b1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int kk = k0 + q, k = 4 * kk + am;
+      a[q] = ts[an + 128 * kk];
+      b0[q] = xs[bc * XPAD + k];
+      b1[q] = xs[(bc + 16) * XPAD + k];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double s = a[q].x + a[q].y;
+      dmma_nv(acc.p[0][0], a[q].x, b0[q].x);
+      dmma_nv(acc.p[1][0], a[q].x, b1[q].x);
+      dmma_nv(acc.p[0][1], a[q].y, b0[q].y);
+      dmma_nv(acc.p[1][1], a[q].y, b1[q].y);
+      dmma_nv(acc.p[0][2], s, b0[q].x + b0[q].y);
+      dmma_nv(acc.p[1][2], s, b1[q].x + b1[q].y);
+    }
+  }
+}
+
 // 32 rows x 32 columns of a column-major block into [col*XPAD + row].
 __device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int c0, int nc, unsigned long long pol) {
   const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
