@@ -297,8 +297,12 @@ class InertiaCounter:
         return dict(block_rows=int(out[0]), offdiag_tiles=int(out[1]), critical_path=int(out[5]))
 
     def count_in(self, a: float, b: float) -> int:
-        """Eigenvalues in (a, b) = count_below(b) - count_below(a)."""
-        return self.count_below(b) - self.count_below(a)
+        """Eigenvalues in (a, b) = count_below(b) - count_below(a); an infinite end (the
+        reference's SpectralWindow allows one, window.hpp:28-52) counts all or none."""
+        n = self.n
+        below_b = n if b == np.inf else self.count_below(b)
+        below_a = 0 if a == -np.inf else self.count_below(a)
+        return below_b - below_a
 
 
 class FilterOperator:

@@ -56,6 +56,10 @@ def test_cfg1_full_size_analytic_counts(zb):
         assert ctr.count_below(s) == int(np.sum(lam < s))
     # the configured window: the lowest 32 (gaps[1] = lam[0], gaps[2..3] bracket the cut)
     assert ctr.count_in(0.5 * lam[0], 0.5 * (lam[31] + lam[32])) == 32
+    # the window as configured: a_- = -inf (window.hpp allows one infinite end)
+    assert gaps[0] == -np.inf
+    assert ctr.count_in(0.5 * (gaps[0] + gaps[1]), 0.5 * (gaps[2] + gaps[3])) == 32
+    assert ctr.count_in(-np.inf, np.inf) == pen[0]
 
 
 def test_cfg2_window_count(zb):

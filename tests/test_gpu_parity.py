@@ -292,6 +292,49 @@ def test_lagged_gmres_control_matches_synchronous_loop(zb, case):
     assert (a["counters"] == b["counters"]).all()
 
 
+@pytest.mark.parametrize("case", ["filter_cfg2_k6", "filter_cfg3_k5", "filter_cfg1_k16"])
+def test_sweep_task_width_is_bitwise_transparent(zb, case):
+    """The sweeps' task width (32- or 64-column tasks, ZOLO_SWEEP_COLS; auto picks 64 for blocks of
+    >= 128 columns) changes only which CTA computes which columns: every output column sees the same
+    DMMA sequence, so the filtered block, G, the report and the counters are bitwise identical
+    (including a partially filled last column group)."""
+    a = _subprocess_filter(case, {"ZOLO_SWEEP_COLS": "32"})
+    b = _subprocess_filter(case, {"ZOLO_SWEEP_COLS": "64"})
+    assert (a["y"] == b["y"]).all() and (a["ga"] == b["ga"]).all()
+    assert (a["cols"] == b["cols"]).all() and int(a["it"]) == int(b["it"]) and int(a["ops"]) == int(b["ops"])
+    assert (a["counters"] == b["counters"]).all()
+
+
+def test_sweep_task_width_wide_block(zb):
+    """The same at 160 columns (3 x 64 with a partial group vs 5 x 32) on config 3's generator at
+    12^3 with r = 8, the BASELINE order."""
+    import subprocess
+    import sys
+    import tempfile
+
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_1701_08935_b200 as zb
+from paper_1701_08935_b200 import configs
+from paper_1701_08935_b200.design import build_filter_design
+pen = configs.tight_binding_pencil(12, seed=3, disorder=1.5)
+gaps = configs.window_by_dense_eigs(pen, lo=852, count=24)
+op = zb.FilterOperator(pen, build_filter_design(gaps, 8), 8, is_complex=True, nd_leaf=64)
+v = zb.random_block(pen[0], 160, 1, cx=True, orthonormalize=True)
+y, rep = op.apply_filter(v)
+np.savez(sys.argv[1], y=y, cols=np.array(rep.column_iterations))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for w in ("32", "64"):
+        f = tempfile.mktemp(suffix=".npz")
+        subprocess.run([sys.executable, "-c", code, f], check=True, cwd=root,
+                       env=dict(os.environ, ZOLO_SWEEP_COLS=w), timeout=600)
+        outs.append(np.load(f))
+    assert (outs[0]["y"] == outs[1]["y"]).all() and (outs[0]["cols"] == outs[1]["cols"]).all()
+
+
 @pytest.mark.parametrize("case", ["filter_cfg2_k6", "filter_cfg3_k5", "filter_planted30_cx"])
 def test_refined_solves_match_reference(zb, case):
     """Residual-correction refinement of the shifted solves (zolo_set_refinement) changes only the
