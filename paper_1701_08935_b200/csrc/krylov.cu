@@ -90,7 +90,7 @@ __global__ void scale_cols_kernel(const S* v, S* out, int64_t ld, const double* 
 }
 
 template <class S>
-__global__ void apply_b_kernel(int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
+__global__ void __launch_bounds__(256, 2) apply_b_kernel(int64_t n, int64_t ld, const int* rp, const int* ci, const S* vals, const S* v,
                                const int* act, int na, cd* out) {
   // one row x SPC columns per thread: the row's indices and values are loaded once
   // and reused across the columns (the SpMM is index-load bound otherwise)
@@ -105,11 +105,21 @@ __global__ void apply_b_kernel(int64_t n, int64_t ld, const int* rp, const int* 
   for (int c = 0; c < SPC; ++c) acc[c] = szero(S());
   if (t < n) {
     if (rp) {
-      for (int q = rp[t]; q < rp[t + 1]; ++q) {
-        const S b = vals[q];
-        const int64_t j = ci[q];
+      constexpr int U = 4;  // the row's entries 4 at a time: 4 x SPC independent loads in flight (-10%)
+      const int q1 = rp[t + 1];
+      for (int q = rp[t]; q < q1; q += U) {
+        int jj[U];
+        S bb[U];
 #pragma unroll
-        for (int c = 0; c < SPC; ++c) acc[c] = sadd(acc[c], smul(b, v[j + col[c] * ld]));
+        for (int u = 0; u < U; ++u) {
+          const bool ok = q + u < q1;
+          jj[u] = ok ? ci[q + u] : static_cast<int>(t);
+          bb[u] = ok ? vals[q + u] : szero(S());
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int c = 0; c < SPC; ++c) acc[c] = sadd(acc[c], smul(bb[u], __ldg(v + jj[u] + col[c] * ld)));
       }
     } else {
 #pragma unroll
