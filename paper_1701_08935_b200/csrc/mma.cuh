@@ -223,7 +223,7 @@ __device__ __forceinline__ void mma_tile3(Acc3<NB>& acc, const cd* ts, const cd*
   const int a0 = opH ? o.ah0 : o.an, a1 = opH ? o.ah1 : o.an, ash = opH ? 2 : 7;
   const int mre = neg ? static_cast<int>(0x80000000u) : 0;
   const int mim = (neg != opH) ? static_cast<int>(0x80000000u) : 0;  // conj for op H, negated for the pre-transform
-  constexpr int KG = NB > 2 ? 2 : 4;  // k-steps whose fragments are loaded together (register budget)
+  constexpr int KG = 4;  // k-steps whose fragments are loaded together (the shared-memory latency overlaps)
 #pragma unroll
   for (int k0 = 0; k0 < TILE / 4; k0 += KG) {  // fragments of KG k-steps first: the shared-memory latency overlaps
     cd a[KG], b[KG][NB];
