@@ -756,7 +756,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
         const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
         const int nd = k.qb - k.qa;
         require(nd <= DAG_REC_DEPS, "zolo_factorize: DAG task record overflow");
-        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out;
+        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out, r[5] = k.wait, r[6] = k.gen, r[7] = k.aux;
         for (int q = 0; q < nd; ++q) {
           const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
           r[DAG_REC_HDR + 2 * q] = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
@@ -1161,6 +1161,10 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
   const Chain* cfw = (refinement ? c.chains_fwd_ref : c.chains_fwd).as<Chain>() + first;
   const Chain* cbw = (refinement ? c.chains_bwd_ref : c.chains_bwd).as<Chain>() + first;
   const int64_t ldp = static_cast<int64_t>(TILE) * std::max(c.sp_nslots, 1);  // cbuf rows (ensure_workspace)
+  if ((static_cast<int64_t>(c.epoch) + 3) * DAG_GENS >= (int64_t(1) << 31)) {  // partial-slot stamps near overflow
+    CK(cudaMemsetAsync(c.flags.p, 0, c.flags.bytes, c.st));
+    c.epoch = 0;
+  }
   const int g1 = dag_trsm_launch(c.st, c.sgeom, c.sched_fwd, cfw, nsub, na, c.swc, ld, ldp, fc, cf, ++c.epoch,
                                  c.counter.as<int>(), c.num_sms, trace, c.act_d.as<int>(), c.lag_done);
   const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, cbw, nsub, na, c.swc, ld, ldp, fc, cf, ++c.epoch,
@@ -2561,20 +2565,23 @@ int zolo_dag_schedule_check(int64_t n, const int64_t* rp, const int64_t* ci, int
       const auto& idx = fwd ? bs.row_idx : bs.col_idx;
       std::vector<DagTask> ts;
       const int nslots = dag_schedule(nb, ptr, idx, fwd, chunk, near, order, ts);
-      // every row has one row task; every dependency of every row is summed exactly once; every
-      // slot is written once; a task appears after the tasks it waits on (claim order topological)
-      std::vector<int64_t> row_at(nb, -1), slot_at(nslots, -1), covered(nb, 0);
+      // every row has one row task; every dependency of every row is summed exactly once; a task
+      // appears after the tasks it waits on (claim order topological); the partial slots (see
+      // DagTask): every write stamps more than the slot held, a chunk that continues a chain reads
+      // its own row's previous step, a chunk that takes over a slot waits for the row task that
+      // last read it, a row task reads the last step of each of its chains
+      std::vector<int64_t> row_at(nb, -1), covered(nb, 0);
       for (size_t t = 0; t < ts.size(); ++t) {
         const DagTask& k = ts[t];
-        if (k.out >= 0) {
-          if (slot_at[k.out] >= 0) ++bad;
-          slot_at[k.out] = static_cast<int64_t>(t);
-        } else {
+        if (k.out < 0) {
           if (row_at[k.i] >= 0) ++bad;
           row_at[k.i] = static_cast<int64_t>(t);
         }
         covered[k.i] += k.qb - k.qa;
       }
+      std::vector<int64_t> stamp(nslots, -1);
+      std::vector<int> wrow(nslots, -1), rrow(nslots, -1);  // last writer row / reader row
+      auto st_of = [](int gen, int step) { return static_cast<int64_t>(64) * gen + step; };
       for (size_t t = 0; t < ts.size(); ++t) {
         const DagTask& k = ts[t];
         const int64_t e0 = ptr[k.i];
@@ -2583,8 +2590,30 @@ int zolo_dag_schedule_check(int64_t n, const int64_t* rp, const int64_t* ci, int
           const int64_t j = fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q];
           if (row_at[j] < 0 || row_at[j] >= static_cast<int64_t>(t)) ++bad;
         }
-        for (int pq = k.pa; pq < k.pa + k.pc; ++pq)
-          if (pq >= nslots || slot_at[pq] < 0 || slot_at[pq] >= static_cast<int64_t>(t)) ++bad;
+        if (k.pc > 0 && (k.pa < 0 || k.pa + k.pc > nslots)) {
+          ++bad;
+          continue;
+        }
+        if (k.out >= 0) {
+          const int c = k.aux & 0xffff, ki = k.aux >> 16, step = c / std::max(ki, 1);
+          if (k.out >= nslots || ki < 1 || st_of(k.gen, step) <= stamp[k.out]) ++bad;
+          if (step > 0) {  // continues its chain
+            if (k.pc != 1 || k.pa != k.out || wrow[k.out] != k.i || stamp[k.out] != st_of(k.gen, step - 1) ||
+                k.wait >= 0)
+              ++bad;
+          } else if (wrow[k.out] >= 0) {  // takes over a slot of another row's unit
+            if (k.pc != 0 || k.wait < 0 || k.wait != rrow[k.out] || row_at[k.wait] >= static_cast<int64_t>(t)) ++bad;
+          }
+          stamp[k.out] = st_of(k.gen, step);
+          wrow[k.out] = k.i;
+        } else if (k.pc > 0) {
+          const int nchunk = k.aux;
+          for (int q = 0; q < k.pc; ++q) {
+            const int sl = k.pa + q;
+            if (wrow[sl] != k.i || stamp[sl] != st_of(k.gen, (nchunk - 1 - q) / k.pc)) ++bad;
+            rrow[sl] = k.i;
+          }
+        }
       }
       for (int64_t i = 0; i < nb; ++i)
         if (row_at[i] < 0 || covered[i] != ptr[i + 1] - ptr[i]) ++bad;

@@ -42,8 +42,22 @@ void factor_plan(const BlockStructure& bs, FactorPlan& plan);
 // (out = -1: u_i = pre(b_i) - sum over q in [qa, qb) - partial slots
 // [pa, pa + pc)). Every task appears after all tasks it waits on, so
 // persistent CTAs claiming in this order cannot deadlock.
+// After dag_schedule the chunks of a row ACCUMULATE into K_i = min(DAG_PCHAINS, chunks) partial
+// (at least chunks / 63: a chain has at most 64 steps)
+// slots [pa, pa + K_i) of a unit of DAG_PCHAINS slots: chunk c writes slot pa + c % K_i as step
+// c / K_i of that chain, adding the chain's partial so far (pc = 1) when c >= K_i; the row task adds
+// the K_i partials (pc = K_i). A slot's flag stamp is epoch * DAG_GENS + 64 `gen` + step, `gen`
+// counting the unit's uses; `aux` = c | K_i << 16 (chunks) or the chunk count (rows). Units are
+// reused along the claim order: the first chunk of each chain of a row that takes over a unit waits
+// for the row task that last read it (`wait`: its block row).
+constexpr int DAG_GENS = 4096;
+#ifndef ZOLO_PCHAINS
+#define ZOLO_PCHAINS 2  // measured: 1 / 2 / 4 chains: cfg2 1642 / 1679 / 1711, cfg3 125.8 / 125.6 / 124.9 vec/s; cfg5 fits one batch up to 2
+#endif
+constexpr int DAG_PCHAINS = ZOLO_PCHAINS;
 struct DagTask {
   int i, qa, qb, pa, pc, out;
+  int gen = 0, wait = -1, aux = 0;
 };
 // first block row of the largest trailing block [s0, nb) of at most kmax block rows whose
 // L pattern is dense (every row holds every earlier row of the block); nb if none
@@ -57,6 +71,7 @@ int trailing_dense_start(const BlockStructure& bs, int kmax);
 // products; all topological). Returns the slot count.
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
                  int near, int order, std::vector<DagTask>& tasks);
+int accumulate_slots(std::vector<DagTask>& tasks, int64_t nb);
 void rcm_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* perm);
 int64_t bandwidth_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);
 int64_t profile_under(int64_t n, const int64_t* rp, const int64_t* ci, const int64_t* perm);

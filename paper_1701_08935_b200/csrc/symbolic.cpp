@@ -489,6 +489,82 @@ int trailing_dense_start(const BlockStructure& bs, int kmax) {
   return static_cast<int>(s);
 }
 
+// Partial slots along the claim order (see DagTask). Chunk tasks arrive with distinct slots
+// `out`, consecutive per row in chunk order. A row's chunks are chained into the K_i slots of a
+// unit taken at its first chunk -- a K_i-slot unit freed REUSE_GAP records after the row task that
+// last read it, else a new one -- so the partial sums need one unit per row in flight
+// instead of one 32-row block per chunk task for the whole sweep (config 3: ~1900 slots instead
+// of ~11600), while up to DAG_PCHAINS chunks of a row still run in parallel. Returns the slot
+// count.
+int accumulate_slots(std::vector<DagTask>& tasks, int64_t nb) {
+  constexpr int64_t REUSE_GAP = 64;  // records between a row task and the reuse of its unit
+  constexpr int K = DAG_PCHAINS;
+  struct Free {
+    int base;
+    int64_t free_at;  // claim position from which the unit may be taken
+    int wait;         // the row task that last read it
+    int use;          // uses so far
+  };
+  // freed units by size (a row with K_i chains takes a K_i-slot unit), oldest first
+  std::vector<std::vector<Free>> pool(K + 1);
+  std::vector<size_t> head(K + 1, 0);
+  auto chains = [&](int nchunk) { return std::max(std::min(K, nchunk), (nchunk + 62) / 63); };
+  std::vector<int> base_of(nb, -1), use_of(nb, 0), wait_of(nb, -1), first_out(nb, -1), seen(nb, 0), nch(nb, 0);
+  std::vector<std::vector<int>> next_step(nb);  // per row, per chain
+  for (const DagTask& t : tasks) {
+    if (t.out >= 0 && (first_out[t.i] < 0 || t.out < first_out[t.i])) first_out[t.i] = t.out;
+    if (t.out < 0) nch[t.i] = t.pc;
+  }
+  int nslots = 0;
+  for (int64_t p = 0; p < static_cast<int64_t>(tasks.size()); ++p) {
+    DagTask& t = tasks[p];
+    if (t.out >= 0) {  // chunk c of row t.i
+      const int c = t.out - first_out[t.i];
+      const int ki = chains(nch[t.i]);
+      if (static_cast<int>(pool.size()) <= ki) {
+        pool.resize(ki + 1);
+        head.resize(ki + 1, 0);
+      }
+      std::vector<int>& ns = next_step[t.i];
+      if (ns.empty()) ns.assign(ki, 0);
+      if (c / ki != ns[c % ki]++)
+        throw std::logic_error("dag_schedule: chunks of a partial chain out of order");
+      ++seen[t.i];
+      if (base_of[t.i] < 0) {  // the row's first chunk in claim order takes a unit
+        std::vector<Free>& pl = pool[ki];
+        size_t& hd = head[ki];
+        if (hd < pl.size() && pl[hd].free_at <= p) {
+          base_of[t.i] = pl[hd].base;
+          wait_of[t.i] = pl[hd].wait;
+          use_of[t.i] = pl[hd].use + 1;
+          ++hd;
+        } else {
+          base_of[t.i] = nslots;
+          nslots += ki;
+          wait_of[t.i] = -1;
+          use_of[t.i] = 0;
+        }
+      }
+      const int step = c / ki;
+      if (step >= 64) throw std::runtime_error("dag_schedule: too many chunks per partial chain");
+      t.out = base_of[t.i] + c % ki;
+      t.pa = t.out;
+      t.pc = step > 0 ? 1 : 0;  // the chain's partial so far (step - 1)
+      t.wait = step > 0 ? -1 : wait_of[t.i];
+      t.gen = use_of[t.i];
+      t.aux = c | (ki << 16);
+    } else if (t.pc > 0) {  // row task: adds its K_i partials, then frees the unit
+      if (base_of[t.i] < 0 || seen[t.i] != t.pc) throw std::logic_error("dag_schedule: row task before its chunks");
+      t.aux = t.pc;
+      t.pa = base_of[t.i];
+      t.pc = chains(t.pc);
+      t.gen = use_of[t.i];
+      if (use_of[t.i] + 1 < DAG_GENS / 64) pool[t.pc].push_back(Free{base_of[t.i], p + REUSE_GAP, t.i, use_of[t.i]});
+    }
+  }
+  return std::max(nslots, 1);
+}
+
 int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<int64_t>& idx, bool fwd, int chunk,
                  int near, int order, std::vector<DagTask>& tasks) {
   if (chunk < 1 || near < 0) throw std::invalid_argument("dag_schedule: chunk >= 1, near >= 0");
@@ -526,7 +602,7 @@ int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<
   tasks.clear();
   if (order == 0) {
     tasks = std::move(seq);
-    return slots;
+    return accumulate_slots(tasks, nb);
   }
   // list-scheduling priority over the task graph, with cost = tile products
   // (+1 for the diagonal pre-transform and the store/flag latency)
@@ -541,7 +617,17 @@ int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<
     const int nd = static_cast<int>(ptr[k.i + 1] - e0);
     for (int q = k.qa; q < k.qb; ++q) deps[t].push_back(row_task[fwd ? idx[e0 + q] : idx[e0 + nd - 1 - q]]);
     for (int p = k.pa; p < k.pa + k.pc; ++p) deps[t].push_back(slot_task[p]);
-    cost[t] = (k.qb - k.qa) + 0.25 * k.pc + 2.0;
+    // a row's chunks accumulate in DAG_PCHAINS chains (accumulate_slots): chunk c waits on c - K_i
+    bool later_chunk = false;
+    if (k.out >= 0) {
+      const DagTask& row = seq[row_task[k.i]];
+      const int ki = std::max(std::min(DAG_PCHAINS, row.pc), (row.pc + 62) / 63);  // accumulate_slots chains()
+      if (k.out - row.pa >= ki) {
+        deps[t].push_back(slot_task[k.out - ki]);
+        later_chunk = true;
+      }
+    }
+    cost[t] = (k.qb - k.qa) + 0.25 * k.pc + (later_chunk ? 0.25 : 0.0) + 2.0;
   }
   std::vector<double> key(nt, 0.0);
   // earliest start time (EST) and longest path to the end (bottom level, BL); key = EST - lambda * BL
@@ -558,7 +644,7 @@ int dag_schedule(int64_t nb, const std::vector<int64_t>& ptr, const std::vector<
   for (int64_t t = 0; t < nt; ++t) perm[t] = t;
   std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
   for (int64_t t : perm) tasks.push_back(seq[t]);
-  return slots;
+  return accumulate_slots(tasks, nb);
 }
 
 }  // namespace zolo

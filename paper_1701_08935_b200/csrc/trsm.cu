@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
                              pol_keep = l2_policy((A.policy >> 2) & 3);
     int g = 0;
     int cur_t = 0;  // claim index of the task being produced (trace)
+    int cur_gen = 0;  // the partial-slot generation the task writes (chunk tasks)
     // one ring entry: tile (optional) + the 32 x 32 block (block row rb, columns c0..) of the
     // chain's buffer behind tensor map `xmap` (kind 2, the end marker: nothing)
     auto produce = [&](int kind, int sign, const cd* tile, uint2 mw, const unsigned char* xmap, int rb, int c0,
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
         m.out = out;
         m.nc = nc;
         m.t = cur_t;
-        m.pad = 0;
+        m.pad = cur_gen;
         meta[s] = m;
         mbar_arrive(full + s);
       }
@@ -367,8 +368,13 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
       recp[lane] = rec_lo;
       recp[lane + 32] = rec_hi;
       __syncwarp();
-      const int i = recp[0], nd = recp[1], pa = recp[2], pc = recp[3], out = recp[4];
+      const int i = recp[0], nd = recp[1], pa = recp[2], pc = recp[3], out = recp[4], wait = recp[5], gen = recp[6],
+                aux = recp[7];
       const bool chunk = out >= 0;
+      // partial-slot stamps (DagTask): a chunk writes step c / K_i of its chain and reads the step
+      // before; the row task reads the last step of each of its K_i = pc chains
+      const int cstep = chunk ? (aux & 0xffff) / (aux >> 16) : 0;
+      cur_gen = 64 * gen + cstep;
       const Chain& ch = chs[ci];
       const int c0 = gi * SWC, nc = min(SWC, A.ncols - c0);
       const size_t cgi = static_cast<size_t>(ci) * A.ngroups + gi;
@@ -393,6 +399,11 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
         };
         const int nent = (chunk ? 0 : 1) + pc + nd;
         int e = 0;
+        // a chunk that takes over a partial slot waits until the row task that read it is done
+        if (wait >= 0 && ld_acquire(flags + wait) < A.epoch) warp_wait_flag(flags + wait, A.epoch, A.counter + 2);
+        auto pstamp = [&](int q) {  // the stamp partial q of this task must carry
+          return A.epoch * DAG_GENS + 64 * gen + (chunk ? cstep - 1 : (aux - 1 - q) / pc);
+        };
         if (!chunk) {  // the pre-transform op(Dinv_i) b_i (negated), or b_i itself (negated add)
           ++e;
           const uint2 pm = mask_of(31);
@@ -404,11 +415,11 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
         }
         for (int p0 = 0; p0 < pc; p0 += 32) {
           const unsigned prdy =
-              __ballot_sync(0xffffffffu, p0 + lane >= pc || ld_acquire(cflags + pa + p0 + lane) >= A.epoch);
+              __ballot_sync(0xffffffffu, p0 + lane >= pc || ld_acquire(cflags + pa + p0 + lane) >= pstamp(p0 + lane));
           for (int p = p0; p < pc && p < p0 + 32; ++p) {
             if (!((prdy >> (p - p0)) & 1u)) {
               const unsigned long long tw = trp ? gtimer() : 0;
-              warp_wait_flag(cflags + pa + p, A.epoch, A.counter + 2);
+              warp_wait_flag(cflags + pa + p, pstamp(p), A.counter + 2);
               if (trp) wsum += gtimer() - tw;
             }
             ++e;
@@ -499,7 +510,10 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
       if (lane == 0 && prev == CW - 1) {
         done[s] = 0;
         const size_t cgi = static_cast<size_t>(m.ci) * A.ngroups + m.gi;
-        st_release(chunk ? A.cflags + cgi * A.nslots + m.out : A.flags + cgi * A.s.nb + m.i, A.epoch);
+        if (chunk)
+          st_release(A.cflags + cgi * A.nslots + m.out, A.epoch * DAG_GENS + m.pad);
+        else
+          st_release(A.flags + cgi * A.s.nb + m.i, A.epoch);
         if (A.trace) {
           unsigned long long* trc = A.trace + DAG_TRACE_WORDS * static_cast<size_t>(m.t);
           unsigned smid;

@@ -157,12 +157,17 @@ def test_random_block_is_bit_identical_to_reference():
 
 
 @pytest.mark.parametrize("name,near,chunk,order", [("grid2d", 4, 16, 3), ("grid3d", 4, 16, 3), ("grid3d", 2, 8, 1),
-                                                   ("grid3d", 3, 12, 0), ("random", 4, 16, 2)])
+                                                   ("grid3d", 3, 12, 0), ("random", 4, 16, 2),
+                                                   ("grid3d_wide", 0, 1, 3), ("grid3d_wide", 1, 1, 0)])
 def test_dag_schedules_are_complete_and_topological(name, near, chunk, order):
     """The claim-ordered sweep schedules (symbolic.cpp dag_schedule) of the ND factor: one row task
     per block row, every dependency summed exactly once (near in the row task, the rest in chunk
-    tasks), every partial slot written once, and every task after the tasks it waits on -- the
-    property that lets persistent CTAs claim in order without deadlock (checked in C++ on the host)."""
+    tasks), every task after the tasks it waits on -- the property that lets persistent CTAs claim
+    in order without deadlock -- and the accumulated partial slots: every write a fresh stamp, a
+    chunk continuing its own chain, a slot taken over only after the row task that read it last,
+    each row task reading the last step of each of its chains (checked in C++ on the host).
+    grid3d_wide: one dependency per chunk, so the widest rows need more than 64 chunk steps and
+    take extra chains."""
     import ctypes as C
 
     import scipy.sparse as sp
@@ -173,8 +178,8 @@ def test_dag_schedules_are_complete_and_topological(name, near, chunk, order):
         k = 40
         t = sp.diags([1.0, 1.0, 1.0], [-1, 0, 1], shape=(k, k))
         m = sp.kron(t, sp.identity(k)) + sp.kron(sp.identity(k), t)
-    elif name == "grid3d":
-        k = 14
+    elif name.startswith("grid3d"):
+        k = 14 if name == "grid3d" else 22
         t = sp.diags([1.0, 1.0, 1.0], [-1, 0, 1], shape=(k, k))
         i = sp.identity(k)
         m = sp.kron(sp.kron(t, i), i) + sp.kron(sp.kron(i, t), i) + sp.kron(sp.kron(i, i), t)

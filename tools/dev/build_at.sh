@@ -12,7 +12,7 @@ else (cd $R && git archive $rev paper_1701_08935_b200/csrc include | tar -x -C $
 S=$B/src/paper_1701_08935_b200/csrc
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -I$B/src/include $extra"
 for f in $S/*.cu; do $NV -c $f -o $B/$(basename $f .cu).o & done
-for f in $S/*.cpp; do g++ -std=c++17 -O3 -fPIC -pthread -c $f -o $B/$(basename $f .cpp).o & done
+for f in $S/*.cpp; do g++ -std=c++17 -O3 -fPIC -pthread $(echo "$extra" | grep -o "\-D[A-Z0-9_]*=[0-9]*") -c $f -o $B/$(basename $f .cpp).o & done
 wait
 for f in $S/*.cu $S/*.cpp; do o=$B/$(basename ${f%.*}).o; [ -f $o ] || { echo "missing $o"; exit 1; }; done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/tools/dev/variants/libzolo_$name.so $B/*.o -lcudart -ldl
