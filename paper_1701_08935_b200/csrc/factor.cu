@@ -229,10 +229,10 @@ __global__ void __launch_bounds__(ST) panel_level_kernel(const int* pan, int p0,
 
 // One trailing-update target per CTA: C -= sum_k L(a,k) U(k,b) over its contributions (fixed
 // ascending-k order) on DMMA, 3M complex products (mma.cuh mma_tile3_nx: 3 real DMMAs per complex
-// MAC instead of 4: cfg3's factorization 746 -> ~650 ms). Single-buffered stages with 4 resident
-// targets per SM hiding the loads: a double-buffered cp.async variant of this loop (two 34 KiB
-// stages) raises "illegal instruction" on the B200 with 3M and with 4M products alike
-// (tools/dev/trail_unit.cu), so the stages stay single.
+// MAC instead of 4: cfg3's factorization 746 -> ~595 ms). Single-buffered stages with 4 resident
+// targets per SM hiding the loads. Two 34 KiB stages per target measured slower (3 targets per SM:
+// 630 ms, 2: 746 ms); built from cp.async with the L2::cache_hint operand that two-stage loop
+// raises "illegal instruction" on the B200 (3M and 4M alike; plain cp.async runs).
 constexpr int TRAIL_SMEM = (TT + XS2) * static_cast<int>(sizeof(cd));
 #ifndef ZOLO_TRAIL_MINB
 #define ZOLO_TRAIL_MINB 4
