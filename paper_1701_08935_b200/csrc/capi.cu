@@ -818,6 +818,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   const size_t per_pole = 3 * per_diag + 2 * per_off;
   if (per_pole_out) *per_pole_out = per_pole;
   size_t free_b = 0, total_b = 0;
+  SetupClock clk;
   store.release();
   CK(cudaMemGetInfo(&free_b, &total_b));
   free_b += pool_cached_bytes();  // cached blocks are reusable
@@ -862,6 +863,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   }
   CK(cudaMemcpyAsync(c.fstate_mem.p, fs.data(), fs.size() * 8, cudaMemcpyHostToDevice, c.st));
   CK(cudaStreamSynchronize(c.st));
+  clk.mark("factor storage");
   while (static_cast<int>(c.pole_streams.size()) < r) {
     cudaStream_t st;
     CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -921,6 +923,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, c.ev0, c.ev1));
   c.last_ms[1] = ms;
+  clk.mark("numeric (launch+device)");
   int serr = 0;
   unsigned long long wk[2] = {0, 0};
   CK(cudaMemcpyAsync(&serr, c.sp_err.p, sizeof(int), cudaMemcpyDeviceToHost, c.st));
@@ -2232,11 +2235,15 @@ int zolo_set_pole_shard_host(zolo_ctx* c, int rank, int nranks, zolo_collective_
 int zolo_filter_create(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, const int64_t* a_ci,
                        const double* a_v, const int64_t* b_rp, const int64_t* b_ci, const double* b_v,
                        const double* design, int r, zolo_factor_stats* stats) {
+  SetupClock clk;
   int st = zolo_pencil_upload(c, n, scalar, a_rp, a_ci, a_v, b_rp, b_ci, b_v);
   if (st) return st;
+  clk.mark("pencil_upload");
   st = zolo_set_design(c, design, r);
   if (st) return st;
-  return zolo_factorize(c, nullptr, stats);
+  st = zolo_factorize(c, nullptr, stats);
+  clk.mark("factorize (total)");
+  return st;
 }
 
 int zolo_shifted_solve(zolo_ctx* c, int pole, int adjoint, const double* b, double* x, int64_t ncols) {

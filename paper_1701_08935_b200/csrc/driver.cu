@@ -28,11 +28,13 @@
 #include <algorithm>
 #include <chrono>
 #include <thread>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <complex>
 #include <cstdint>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -62,14 +64,30 @@ struct Fail : std::runtime_error {
   Fail(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
+// complex arithmetic by parts, the same operations as std::complex's operators (no fused
+// multiply-adds in this translation unit), written out so the stride-1 loops below vectorise
+inline double add(double a, double b) { return a + b; }
+inline cplx add(cplx a, cplx b) { return cplx(a.real() + b.real(), a.imag() + b.imag()); }
+inline double sub2(double a, double b) { return a - b; }
+inline cplx sub2(cplx a, cplx b) { return cplx(a.real() - b.real(), a.imag() - b.imag()); }
+inline double mul(double a, double b) { return a * b; }
+inline cplx mul(cplx a, cplx b) {
+  return cplx(a.real() * b.real() - a.imag() * b.imag(), a.real() * b.imag() + a.imag() * b.real());
+}
+inline double mulc(double a, double b) { return a * b; }  // a conj(b)
+inline cplx mulc(cplx a, cplx b) {
+  return cplx(a.real() * b.real() + a.imag() * b.imag(), a.imag() * b.real() - a.real() * b.imag());
+}
+
 // Hermitian eigendecomposition of a dense n x n column-major matrix:
 // A = Z diag(w) Z^H, w ascending. Restated from the reference's
 // dense_hermitian_eig (dense_eig.hpp:42-172: Householder reduction with the
 // reflectors accumulated into Z, unit-modulus rescaling to a real tridiagonal,
 // implicit-shift QL) -- not a new algorithm: the n_v x n_v eigenproblem is
 // host-side setup (north_star), and restating the reference's routine keeps the
-// Ritz bases of iteration >= 2 on the reference's path. The only change is the
-// extra absolute deflation test noted below.
+// Ritz bases of iteration >= 2 on the reference's path. The changes: the extra absolute
+// deflation test noted below, and loop nests running down the columns (stride-1, vectorised)
+// with every sum in the reference's order -- the results are bit-identical to the row-wise form.
 template <class S>
 void herm_eig(int n, std::vector<S> a, std::vector<double>& w, std::vector<S>& z) {
   auto A = [&](int i, int j) -> S& { return a[static_cast<size_t>(j) * n + i]; };
@@ -96,24 +114,35 @@ void herm_eig(int n, std::vector<S> a, std::vector<double>& w, std::vector<S>& z
     sub[k] = alpha;
     if (vn2 == 0.0) continue;
     const double tau = 2.0 / vn2;
-    for (int i = 0; i < m; ++i) {
-      S s(0);
-      for (int j = 0; j < m; ++j) s += A(k + 1 + i, k + 1 + j) * v[j];
-      p[i] = tau * s;
+    // p = tau A v, column by column (stride-1): every p[i] still sums over j in ascending order
+    for (int i = 0; i < m; ++i) p[i] = S(0);
+    for (int j = 0; j < m; ++j) {
+      const S vj = v[j];
+      const S* col = &A(k + 1, k + 1 + j);
+      for (int i = 0; i < m; ++i) p[i] = add(p[i], mul(col[i], vj));
     }
+    for (int i = 0; i < m; ++i) p[i] = tau * p[i];
     S vhp(0);
     for (int i = 0; i < m; ++i) vhp += conj_s(v[i]) * p[i];
     const S kc = 0.5 * tau * vhp;
     for (int i = 0; i < m; ++i) q[i] = p[i] - kc * v[i];
-    for (int i = 0; i < m; ++i)
-      for (int j = 0; j < m; ++j) A(k + 1 + i, k + 1 + j) -= v[i] * conj_s(q[j]) + q[i] * conj_s(v[j]);
-    for (int r = 0; r < n; ++r) {
-      S s(0);
-      for (int j = 0; j < m; ++j) s += Z(r, k + 1 + j) * v[j];
-      tvec[r] = tau * s;
+    for (int j = 0; j < m; ++j) {
+      const S qj = q[j], vj = v[j];
+      S* col = &A(k + 1, k + 1 + j);
+      for (int i = 0; i < m; ++i) col[i] = sub2(col[i], add(mulc(v[i], qj), mulc(q[i], vj)));
     }
-    for (int r = 0; r < n; ++r)
-      for (int j = 0; j < m; ++j) Z(r, k + 1 + j) -= tvec[r] * conj_s(v[j]);
+    for (int r = 0; r < n; ++r) tvec[r] = S(0);
+    for (int j = 0; j < m; ++j) {
+      const S vj = v[j];
+      const S* col = &Z(0, k + 1 + j);
+      for (int r = 0; r < n; ++r) tvec[r] = add(tvec[r], mul(col[r], vj));
+    }
+    for (int r = 0; r < n; ++r) tvec[r] = tau * tvec[r];
+    for (int j = 0; j < m; ++j) {
+      const S vj = v[j];
+      S* col = &Z(0, k + 1 + j);
+      for (int r = 0; r < n; ++r) col[r] = sub2(col[r], mulc(tvec[r], vj));
+    }
   }
   if (n >= 2) sub[n - 2] = A(n - 1, n - 2);
   std::vector<double> d(n), e(std::max(n, 1), 0.0);
@@ -166,10 +195,15 @@ void herm_eig(int n, std::vector<S> a, std::vector<double>& w, std::vector<S>& z
         pp = s * r;
         d[i + 1] = g + pp;
         g = c * r - b;
-        for (int k = 0; k < n; ++k) {
-          const S zf = Z(k, i + 1);
-          Z(k, i + 1) = s * Z(k, i) + c * zf;
-          Z(k, i) = c * Z(k, i) - s * zf;
+        {  // the rotation is real: it acts on the real and imaginary parts alike, as plain doubles
+          double* __restrict__ za = reinterpret_cast<double*>(&Z(0, i));
+          double* __restrict__ zb = reinterpret_cast<double*>(&Z(0, i + 1));
+          const int len = n * static_cast<int>(sizeof(S) / sizeof(double));
+          for (int k = 0; k < len; ++k) {
+            const double zf = zb[k];
+            zb[k] = s * za[k] + c * zf;
+            za[k] = c * za[k] - s * zf;
+          }
         }
       }
       if (r == 0.0 && i >= l) continue;
@@ -285,10 +319,43 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
   if (r < 1 || r > ZOLO_MAX_ORDER) throw Fail(ZOLO_ERR_DOMAIN, "subspace_iteration: order must be in [1,16]");
 
   const auto t0 = clock::now();
+  // (development) ZOLO_SETUP_TIMES=1 prints the driver's phases
+  const bool phases = std::getenv("ZOLO_SETUP_TIMES") != nullptr;
+  auto tp = t0;
+  const auto mark = [&](const char* what) {
+    if (!phases) return;
+    const auto now = clock::now();
+    std::fprintf(stderr, "[solve] %-22s %8.2f ms\n", what, secs(tp, now) * 1e3);
+    tp = now;
+  };
   // the seeded start block (random_gaussian, dense.hpp:193-208) does not depend on the
-  // factorization: generate it on a host thread while the factors are built
-  std::vector<S> h0(static_cast<size_t>(n) * n_ss);
-  std::thread rng([&] { zolo::random_block(scalar, n, n_ss, seed, false, reinterpret_cast<double*>(h0.data())); });
+  // factorization: a host thread generates it and uploads it on its own stream while the factors
+  // are built
+  const size_t es = sizeof(S);
+  const cudaStream_t cst = zolo::ctx_stream(ctx);
+  DevBuf q(es * n * n_ss, cst);
+  cuda_ck(cudaStreamSynchronize(cst));  // the block's previous user (caching allocator) is done
+  int dev = 0;
+  cuda_ck(cudaGetDevice(&dev));
+  cudaError_t up_err = cudaSuccess;
+  std::thread rng([&] {
+    // uninitialised host block: its pages are first touched by the generator's threads
+    struct Free {
+      void operator()(void* p) const { std::free(p); }
+    };
+    std::unique_ptr<void, Free> h0(std::malloc(es * n * n_ss));
+    if (!h0) {
+      up_err = cudaErrorMemoryAllocation;
+      return;
+    }
+    zolo::random_block(scalar, n, n_ss, seed, false, static_cast<double*>(h0.get()));
+    cudaStream_t us = nullptr;
+    if ((up_err = cudaSetDevice(dev)) != cudaSuccess) return;
+    if ((up_err = cudaStreamCreateWithFlags(&us, cudaStreamNonBlocking)) != cudaSuccess) return;
+    up_err = cudaMemcpyAsync(q.p, h0.get(), es * n * n_ss, cudaMemcpyHostToDevice, us);
+    if (up_err == cudaSuccess) up_err = cudaStreamSynchronize(us);
+    cudaStreamDestroy(us);
+  });
   struct Joiner {
     std::thread& t;
     ~Joiner() {
@@ -298,16 +365,15 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
   ck(ctx, zolo_set_refinement(ctx, refine == 1 ? 1 : 0));
   ck(ctx, zolo_filter_create(ctx, n, scalar, a_rp, a_ci, a_v, b_rp, b_ci, b_v, design, r, nullptr));
   const auto t1 = clock::now();
+  mark("filter_create");
   const double wa = design[0], wb = design[1];
   const double scale = std::max(std::abs(wa), std::abs(wb));
 
-  const size_t es = sizeof(S);
-  const cudaStream_t cst = zolo::ctx_stream(ctx);
-  DevBuf q(es * n * n_ss, cst), y(es * n * n_ss, cst), t(es * n * n_ss, cst), u(es * n * n_ss, cst);
+  DevBuf y(es * n * n_ss, cst), t(es * n * n_ss, cst), u(es * n * n_ss, cst);
   {  // Q0: seeded Gaussian block, orthonormalised (CholQR2 == MGS's Q up to rounding)
     rng.join();
-    cuda_ck(cudaMemcpyAsync(q.p, h0.data(), es * n * n_ss, cudaMemcpyHostToDevice, cst));
-    cuda_ck(cudaStreamSynchronize(cst));
+    cuda_ck(up_err);
+    mark("start block upload");
     for (int pass = 0; pass < 2; ++pass) {
       std::vector<S> g(static_cast<size_t>(n_ss) * n_ss), rinv;
       ck(ctx, zolo_gram_device(ctx, q.p, q.p, n_ss, n_ss, reinterpret_cast<double*>(g.data())));
@@ -320,6 +386,7 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
     }
   }
 
+  mark("start block CholQR2");
   int64_t kq = n_ss;  // current subspace width
   int64_t n_iter = 0, n_gmres = 0, n_gmres_min = 0;
   double residual = std::numeric_limits<double>::infinity(), residual_lam = 0.0, filter_ms = 0.0;
@@ -339,6 +406,7 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
     double tm[8];
     zolo_last_timings(ctx, tm);
     filter_ms += tm[0];
+    mark("apply_filter");
     n_gmres = std::max<int64_t>(n_gmres, rep.iterations);
     for (int64_t c = 0; c < kq; ++c) n_gmres_min = n_gmres_min == 0 ? cols[c] : std::min(n_gmres_min, cols[c]);
 
@@ -351,6 +419,7 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
     ck(ctx, zolo_gram_device(ctx, y.p, t.p, kq, kq, reinterpret_cast<double*>(bt.data())));
     hermitianize(k, at);
     hermitianize(k, bt);
+    mark("RR projections");
     std::vector<double> mu;
     std::vector<S> vb;
     herm_eig(k, bt, mu, vb);
@@ -391,8 +460,10 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
         for (int i = 0; i < k; ++i) small[static_cast<size_t>(c) * k + i] += w[static_cast<size_t>(p) * k + i] * v;
       }
     });
+    mark("RR host eigenproblems");
     ck(ctx, zolo_block_gemm_device(ctx, y.p, kq, reinterpret_cast<const double*>(small.data()), kk, q.p));
     kq = kk;
+    mark("RR Q = Y Q~");
 
     // Ritz values inside (a,b) and their residual (eigensolver.hpp:193-207)
     inside.clear();
@@ -421,6 +492,7 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
       residual = std::max(residual, std::sqrt(num[c]) / (scale * std::sqrt(den[c])));
       residual_lam = std::max(residual_lam, std::sqrt(num[c]) / (std::abs(inside_vals[c]) * std::sqrt(den[c])));
     }
+    mark("residuals");
     if (it == 1) first_residual = residual;
     if (residual <= tol) {
       converged = true;
@@ -442,6 +514,7 @@ void run_solve(zolo_ctx* ctx, int64_t n, int scalar, const int64_t* a_rp, const 
   if (vectors && !inside.empty())
     cuda_ck(cudaMemcpyAsync(vectors, u.p, es * n * inside.size(), cudaMemcpyDeviceToHost, cst));
   cuda_ck(cudaStreamSynchronize(cst));
+  mark("vectors to host");
   int64_t inner = 0, gapps = 0;
   zolo_counters(ctx, &inner, &gapps);
   stats[0] = static_cast<double>(n_ss);

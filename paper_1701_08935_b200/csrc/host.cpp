@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <limits>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "host.hpp"
@@ -153,21 +154,53 @@ void uniform_stream(uint64_t seed, int64_t n, double* out) {
   for (int64_t i = 0; i < n; ++i) out[i] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
 }
 
+// The raw mt19937_64 stream is sequential by definition (dense.hpp:193-208 draws in column
+// order from one generator), the Box-Muller transform of each pair of draws is not: the stream is
+// produced block by block on the calling thread and transformed by a few host threads, each
+// Gaussian by the same expression as the serial form (bit-identical output).
+namespace {
+void gaussian_fill(std::mt19937_64& rng, int64_t count, double* out) {
+  constexpr int64_t BLK = int64_t{1} << 20;
+  const int nt = static_cast<int>(std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())));
+  if (count < 4 * BLK || nt < 2) {
+    for (int64_t i = 0; i < count; ++i) out[i] = gaussian(rng);
+    return;
+  }
+  std::vector<uint64_t> raw[2];
+  raw[0].resize(2 * BLK);
+  raw[1].resize(2 * BLK);
+  std::vector<std::thread> pool;
+  const auto join_all = [&] {
+    for (auto& t : pool) t.join();
+    pool.clear();
+  };
+  int buf = 0;
+  for (int64_t i0 = 0; i0 < count; i0 += BLK, buf ^= 1) {
+    const int64_t m = std::min(BLK, count - i0);
+    uint64_t* rw = raw[buf].data();
+    for (int64_t i = 0; i < 2 * m; ++i) rw[i] = rng();  // overlaps the previous block's transform
+    join_all();
+    double* dst = out + i0;
+    for (int q = 0; q < nt; ++q)
+      pool.emplace_back([=] {
+        const int64_t a = m * q / nt, b = m * (q + 1) / nt;
+        for (int64_t i = a; i < b; ++i) {
+          const double u1 = (static_cast<double>(rw[2 * i] >> 11) + 0.5) * 0x1.0p-53;
+          const double u2 = (static_cast<double>(rw[2 * i + 1] >> 11) + 0.5) * 0x1.0p-53;
+          dst[i] = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+        }
+      });
+  }
+  join_all();
+}
+}  // namespace
+
 bool random_block(int cx, int64_t n, int64_t k, uint64_t seed, bool orthonormalize, double* out) {
   std::mt19937_64 rng(seed);
-  if (cx) {
-    auto* z = reinterpret_cast<std::complex<double>*>(out);
-    for (int64_t j = 0; j < k; ++j)
-      for (int64_t i = 0; i < n; ++i) {
-        const double re = gaussian(rng);
-        const double im = gaussian(rng);
-        z[i + j * n] = std::complex<double>(re, im);
-      }
-    return orthonormalize ? mgs(z, n, k) : true;
-  }
-  for (int64_t j = 0; j < k; ++j)
-    for (int64_t i = 0; i < n; ++i) out[i + j * n] = gaussian(rng);
-  return orthonormalize ? mgs(out, n, k) : true;
+  // complex: (re, im) interleaved in column order == the serial draw order
+  gaussian_fill(rng, n * k * (cx ? 2 : 1), out);
+  if (!orthonormalize) return true;
+  return cx ? mgs(reinterpret_cast<std::complex<double>*>(out), n, k) : mgs(out, n, k);
 }
 
 }  // namespace zolo

@@ -156,6 +156,22 @@ def test_random_block_is_bit_identical_to_reference():
     assert np.abs(q0 - g["q0"]).max() == 0.0
 
 
+def test_large_random_block_threaded_transform_is_bit_identical_to_reference():
+    """Blocks of >= 4 Mi Gaussians take host.cpp's threaded Box-Muller path (raw mt19937_64 stream
+    sequential, transform on several threads): same bits as the reference's serial
+    random_gaussian (dense.hpp:193-208), digests in tests/golden/rng_block_large.npz."""
+    import sys
+
+    import paper_1701_08935_b200 as zb
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_golden import array_digest
+
+    g = load_golden("rng_block_large")
+    assert array_digest(zb.random_block(1 << 20, 5, 7, cx=False)) == g["real"]
+    assert array_digest(zb.random_block((1 << 19) + 3, 5, 9, cx=True)) == g["cplx"]
+
+
 @pytest.mark.parametrize("name,near,chunk,order", [("grid2d", 4, 16, 3), ("grid3d", 4, 16, 3), ("grid3d", 2, 8, 1),
                                                    ("grid3d", 3, 12, 0), ("random", 4, 16, 2),
                                                    ("grid3d_wide", 0, 1, 3), ("grid3d_wide", 1, 1, 0)])
