@@ -20,12 +20,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <mutex>
 #include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/zolo_b200.h"
@@ -257,8 +259,8 @@ void h2d_setup(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   }
 }
 
-template <class T>
-void upload(DevMem& m, const std::vector<T>& v, cudaStream_t st) {
+template <class T, class A>
+void upload(DevMem& m, const std::vector<T, A>& v, cudaStream_t st) {
   m.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
   if (!v.empty()) h2d_setup(m.p, v.data(), sizeof(T) * v.size(), st);
   CK(cudaStreamSynchronize(st));
@@ -714,6 +716,57 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   g.nbk = nb;
   c.geom = g;
 
+  // The factor plan and the two sweep schedules depend on the block structure only: host threads
+  // build them while this thread uploads the structure, the scatter lists and the device pencil.
+  std::exception_ptr bg_err[3];
+  std::vector<int> rec_f, rec_b;
+  int ntask_f = 0, ntask_b = 0, sf = 0, sb = 0;
+  // claim-ordered sweep schedules: wide block rows split into chunk tasks
+  static const int near = std::min(std::max(env_int("ZOLO_DAG_NEAR", 4), 0), DAG_REC_DEPS - 1),
+                   chunk = std::min(std::max(env_int("ZOLO_DAG_CHUNK", 16), 1), DAG_REC_DEPS - near),
+                   order = env_int("ZOLO_DAG_ORDER", 3);
+  // self-contained task records: header + the (j, tile id) pairs in processing order
+  auto schedule = [&](bool fwd, std::vector<int>& rec, int& ntask, int& nslots) {
+    std::vector<DagTask> ts;
+    nslots = fwd ? dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, ts)
+                 : dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, ts);
+    ntask = static_cast<int>(ts.size());
+    rec.assign(ts.size() * DAG_REC, 0);
+    for (size_t t = 0; t < ts.size(); ++t) {
+      const DagTask& k = ts[t];
+      int* r = rec.data() + t * DAG_REC;
+      const int64_t e0 = fwd ? bs.row_ptr[k.i] : bs.col_ptr[k.i];
+      const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
+      const int nd = k.qb - k.qa;
+      require(nd <= DAG_REC_DEPS, "zolo_factorize: DAG task record overflow");
+      r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out, r[5] = k.wait, r[6] = k.gen, r[7] = k.aux;
+      for (int q = 0; q < nd; ++q) {
+        const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
+        r[DAG_REC_HDR + 2 * q] = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
+        r[DAG_REC_HDR + 2 * q + 1] = static_cast<int>(fwd ? e : bs.col_tile[e]);
+      }
+    }
+  };
+  auto guard_bg = [&](int slot, auto&& fn) {
+    return std::thread([&bg_err, slot, fn] {
+      try {
+        fn();
+      } catch (...) {
+        bg_err[slot] = std::current_exception();
+      }
+    });
+  };
+  std::thread bg[3] = {guard_bg(0, [&] { factor_plan(bs, c.fplan); }),
+                       guard_bg(1, [&] { schedule(true, rec_f, ntask_f, sf); }),
+                       guard_bg(2, [&] { schedule(false, rec_b, ntask_b, sb); })};
+  struct JoinAll {
+    std::thread* t;
+    ~JoinAll() {
+      for (int k = 0; k < 3; ++k)
+        if (t[k].joinable()) t[k].join();
+    }
+  } join_all{bg};
+
   auto to32 = [](const std::vector<int64_t>& v) { return std::vector<int>(v.begin(), v.end()); };
   std::vector<int> tile_row(bs.ntiles);
   for (int64_t i = 0; i < nb; ++i)
@@ -742,39 +795,6 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   s.col_tile = c.sp_col_tile.as<int>();
   s.tile_row = c.sp_tile_row.as<int>();
   c.sgeom = s;
-  {  // claim-ordered sweep schedules: wide block rows split into chunk tasks
-    static const int near = std::min(std::max(env_int("ZOLO_DAG_NEAR", 4), 0), DAG_REC_DEPS - 1),
-                     chunk = std::min(std::max(env_int("ZOLO_DAG_CHUNK", 16), 1), DAG_REC_DEPS - near),
-                     order = env_int("ZOLO_DAG_ORDER", 3);
-    // self-contained task records: header + the (j, tile id) pairs in processing order
-    auto records = [&](const std::vector<DagTask>& ts, bool fwd) {
-      std::vector<int> rec(ts.size() * DAG_REC, 0);
-      for (size_t t = 0; t < ts.size(); ++t) {
-        const DagTask& k = ts[t];
-        int* r = rec.data() + t * DAG_REC;
-        const int64_t e0 = fwd ? bs.row_ptr[k.i] : bs.col_ptr[k.i];
-        const int ndall = static_cast<int>((fwd ? bs.row_ptr[k.i + 1] : bs.col_ptr[k.i + 1]) - e0);
-        const int nd = k.qb - k.qa;
-        require(nd <= DAG_REC_DEPS, "zolo_factorize: DAG task record overflow");
-        r[0] = k.i, r[1] = nd, r[2] = k.pa, r[3] = k.pc, r[4] = k.out, r[5] = k.wait, r[6] = k.gen, r[7] = k.aux;
-        for (int q = 0; q < nd; ++q) {
-          const int64_t e = fwd ? e0 + k.qa + q : e0 + ndall - 1 - (k.qa + q);
-          r[DAG_REC_HDR + 2 * q] = static_cast<int>(fwd ? bs.row_idx[e] : bs.col_idx[e]);
-          r[DAG_REC_HDR + 2 * q + 1] = static_cast<int>(fwd ? e : bs.col_tile[e]);
-        }
-      }
-      return rec;
-    };
-    std::vector<DagTask> tf, tb;
-    const int sf = dag_schedule(nb, bs.row_ptr, bs.row_idx, true, chunk, near, order, tf);
-    const int sb = dag_schedule(nb, bs.col_ptr, bs.col_idx, false, chunk, near, order, tb);
-    upload(c.sp_sched_fwd, records(tf, true), c.st);
-    upload(c.sp_sched_bwd, records(tb, false), c.st);
-    c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), static_cast<int>(tf.size()), sf};
-    c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), static_cast<int>(tb.size()), sb};
-    c.sp_nslots = std::max(sf, sb);
-  }
-  clk.mark("sweep schedules");
 
   const int64_t nnz = static_cast<int64_t>(u.ci.size());
   std::vector<int> er(nnz), ec(nnz), pads;
@@ -794,8 +814,15 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   c.sp_npads = static_cast<int>(pads.size());
   upload_device_pencil(c, bs.inv, pos);
   clk.mark("device pencil");
-  factor_plan(bs, c.fplan);
-  clk.mark("factor plan");
+  for (int k = 0; k < 3; ++k) bg[k].join();
+  for (int k = 0; k < 3; ++k)
+    if (bg_err[k]) std::rethrow_exception(bg_err[k]);
+  clk.mark("plan + schedules (wait)");
+  upload(c.sp_sched_fwd, rec_f, c.st);
+  upload(c.sp_sched_bwd, rec_b, c.st);
+  c.sched_fwd = DagSched{c.sp_sched_fwd.as<int>(), ntask_f, sf};
+  c.sched_bwd = DagSched{c.sp_sched_bwd.as<int>(), ntask_b, sb};
+  c.sp_nslots = std::max(sf, sb);
   upload(c.fp_cols, c.fplan.cols, c.st);
   upload(c.fp_pan, c.fplan.pan, c.st);
   upload(c.fp_tgt, c.fplan.tgt, c.st);

@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(con
                                                                cd* Lt, cd* Ut) {
   extern __shared__ __align__(16) unsigned char trail_smem[];
   cd* sm = reinterpret_cast<cd*>(trail_smem);
-  const int* T = tgt + 4 * (t0 + blockIdx.x);
-  const int kind = T[0], id = T[1], cb = T[2], ce = T[3];
+  const int* T = tgt + 2 * (t0 + blockIdx.x);  // packed: kind << 30 | tile id, first contribution; end = the next target's first
+  const int kind = static_cast<unsigned>(T[0]) >> 30, id = T[0] & 0x3fffffff, cb = T[1], ce = T[3];
   const unsigned long long pol = l2_evict_normal();
   const Frag f = frag();
   Acc3<2> acc;

@@ -2,6 +2,8 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <memory>
+#include <utility>
 #include <vector>
 
 namespace zolo {
@@ -27,10 +29,30 @@ void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::
 // each target with its contributions (L(a,k), U(k,b)) in ascending k so the
 // accumulation order is fixed (deterministic factors).
 //   pan: 2 ints per item (k, 2 * tile id + upper)
-//   tgt: 4 ints per target (kind 0 = Dt / 1 = Lt / 2 = Ut, tile id, first, end contribution)
+//   tgt: 2 ints per target (kind 0 = Dt / 1 = Lt / 2 = Ut in bits 30-31 | tile id, first
+//        contribution); a target's contributions end where the next target's begin (the lists are
+//        laid out in target order; one sentinel entry closes the last)
 //   con: 2 ints per contribution (L tile id, U tile id)
+// std::vector whose resize leaves new elements uninitialised: the plan's large arrays are sized
+// once and filled by the worker threads (which also take their first-touch page faults)
+template <class T>
+struct NoInit : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInit<U>;
+  };
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    if constexpr (sizeof...(A) == 0)
+      ::new (static_cast<void*>(p)) U;
+    else
+      ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+using RawInts = std::vector<int, NoInit<int>>;
 struct FactorPlan {
-  std::vector<int> lvl_ptr, cols, pan_ptr, pan, tgt_ptr, tgt, con;
+  std::vector<int> lvl_ptr, cols, pan_ptr, pan, tgt_ptr;
+  RawInts tgt, con;
   int64_t contributions = 0;
 };
 void factor_plan(const BlockStructure& bs, FactorPlan& plan);

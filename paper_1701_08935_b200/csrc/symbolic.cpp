@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <exception>
+#include <memory>
 #include <cstdint>
 #include <numeric>
 #include <stdexcept>
@@ -36,7 +38,11 @@ struct Graph {
 };
 
 // BFS over the vertices with mark[v] == tag; returns the visit order and fills level.
-void bfs(const Graph& g, const std::vector<int>& mark, int tag, int64_t root, std::vector<int64_t>& level,
+using Marks = std::unique_ptr<std::atomic<int>[]>;
+inline int mk_get(const Marks& m, int64_t v) { return m[v].load(std::memory_order_relaxed); }
+inline void mk_set(Marks& m, int64_t v, int t) { m[v].store(t, std::memory_order_relaxed); }
+
+void bfs(const Graph& g, const Marks& mark, int tag, int64_t root, std::vector<int64_t>& level,
          std::vector<int64_t>& order) {
   order.clear();
   order.push_back(root);
@@ -45,7 +51,7 @@ void bfs(const Graph& g, const std::vector<int>& mark, int tag, int64_t root, st
     const int64_t u = order[h];
     for (int64_t k = g.rp[u]; k < g.rp[u + 1]; ++k) {
       const int64_t v = g.ci[k];
-      if (mark[v] == tag && level[v] < 0) {
+      if (mk_get(mark, v) == tag && level[v] < 0) {
         level[v] = level[u] + 1;
         order.push_back(v);
       }
@@ -53,26 +59,40 @@ void bfs(const Graph& g, const std::vector<int>& mark, int tag, int64_t root, st
   }
 }
 
+// The two sides of a separator are independent subproblems: down to PAR_DEPTH the first side runs
+// on its own host thread. Pieces are disjoint vertex sets, so `level` entries are touched by one
+// thread only; `mark` entries of neighbours in other pieces are read concurrently (they never
+// equal this piece's tag: tags are unique), hence the relaxed atomics. Every piece's result
+// depends on the graph and the piece alone, so the ordering does not depend on the threading.
+struct NdOut {
+  std::vector<std::vector<int64_t>> nodes;  // elimination order of tree nodes
+  std::vector<int> is_sep;
+  void append(NdOut&& o) {
+    for (auto& nd : o.nodes) nodes.push_back(std::move(nd));
+    is_sep.insert(is_sep.end(), o.is_sep.begin(), o.is_sep.end());
+  }
+};
 struct NdState {
+  static constexpr int PAR_DEPTH = 3;
   const Graph& g;
   int64_t leaf;
-  std::vector<int> mark;
-  int next_tag = 1;
-  std::vector<int64_t> level, order;
-  std::vector<std::vector<int64_t>> nodes;  // elimination order of tree nodes
-  std::vector<int> node_is_sep;
-  explicit NdState(const Graph& gr, int64_t lf) : g(gr), leaf(lf), mark(gr.n, 0), level(gr.n, -1) {}
+  Marks mark;
+  std::atomic<int> next_tag{1};
+  std::vector<int64_t> level;
+  explicit NdState(const Graph& gr, int64_t lf) : g(gr), leaf(lf), mark(new std::atomic<int>[gr.n]), level(gr.n, -1) {
+    for (int64_t v = 0; v < gr.n; ++v) mk_set(mark, v, 0);
+  }
 
-  void emit_leaf(std::vector<int64_t>& idx) {
+  void emit_leaf(std::vector<int64_t>& idx, NdOut& out, std::vector<int64_t>& order) {
     // reverse Cuthill-McKee inside the leaf (degree tie-breaks within the piece)
     const int tag = next_tag++;
-    for (int64_t v : idx) mark[v] = tag;
-    std::vector<int64_t> out;
-    out.reserve(idx.size());
+    for (int64_t v : idx) mk_set(mark, v, tag);
+    std::vector<int64_t> seq;
+    seq.reserve(idx.size());
     std::vector<char> seen_local;
     auto deg = [&](int64_t v) {
       int64_t d = 0;
-      for (int64_t k = g.rp[v]; k < g.rp[v + 1]; ++k) d += mark[g.ci[k]] == tag;
+      for (int64_t k = g.rp[v]; k < g.rp[v + 1]; ++k) d += mk_get(mark, g.ci[k]) == tag;
       return d;
     };
     std::vector<int64_t> q, nb;
@@ -80,28 +100,28 @@ struct NdState {
     while (done < idx.size()) {
       int64_t root = -1, best = INT64_MAX;
       for (int64_t v : idx)
-        if (mark[v] == tag) {
+        if (mk_get(mark, v) == tag) {
           const int64_t d = deg(v);
           if (d < best) best = d, root = v;
         }
       // pseudo-peripheral refinement
       for (int it = 0; it < 2; ++it) {
         for (int64_t v : idx)
-          if (mark[v] == tag) level[v] = -1;
+          if (mk_get(mark, v) == tag) level[v] = -1;
         bfs(g, mark, tag, root, level, order);
         root = order.back();
       }
       q.clear();
       q.push_back(root);
-      mark[root] = -tag;
+      mk_set(mark, root, -tag);
       for (size_t h = 0; h < q.size(); ++h) {
         const int64_t u = q[h];
-        out.push_back(u);
+        seq.push_back(u);
         nb.clear();
         for (int64_t k = g.rp[u]; k < g.rp[u + 1]; ++k) {
           const int64_t v = g.ci[k];
-          if (mark[v] == tag) {
-            mark[v] = -tag;
+          if (mk_get(mark, v) == tag) {
+            mk_set(mark, v, -tag);
             nb.push_back(v);
           }
         }
@@ -111,21 +131,21 @@ struct NdState {
         });
         for (int64_t v : nb) q.push_back(v);
       }
-      done = out.size();
+      done = seq.size();
     }
-    std::reverse(out.begin(), out.end());
+    std::reverse(seq.begin(), seq.end());
     for (int64_t v : idx) level[v] = -1;
-    nodes.push_back(std::move(out));
-    node_is_sep.push_back(0);
+    out.nodes.push_back(std::move(seq));
+    out.is_sep.push_back(0);
   }
 
-  void rec(std::vector<int64_t> idx) {
+  void rec(std::vector<int64_t> idx, int depth, NdOut& out, std::vector<int64_t>& order) {
     if (static_cast<int64_t>(idx.size()) <= leaf) {
-      emit_leaf(idx);
+      emit_leaf(idx, out, order);
       return;
     }
     const int tag = next_tag++;
-    for (int64_t v : idx) mark[v] = tag;
+    for (int64_t v : idx) mk_set(mark, v, tag);
     int64_t root = idx[0];
     for (int it = 0; it < 2; ++it) {
       for (int64_t v : idx) level[v] = -1;
@@ -139,8 +159,8 @@ struct NdState {
       for (int64_t v : idx)
         if (level[v] < 0) b.push_back(v);
       for (int64_t v : idx) level[v] = -1;
-      rec(std::move(a));
-      rec(std::move(b));
+      rec(std::move(a), depth, out, order);
+      rec(std::move(b), depth, out, order);
       return;
     }
     // median level by vertex count
@@ -181,13 +201,37 @@ struct NdState {
     }
     for (int64_t v : idx) level[v] = -1;
     if (a.empty() || b.empty()) {  // no progress (path-like piece): stop dissecting
-      emit_leaf(idx);
+      emit_leaf(idx, out, order);
       return;
     }
-    rec(std::move(a));
-    rec(std::move(b));
-    nodes.push_back(std::move(s));
-    node_is_sep.push_back(1);
+    if (depth < PAR_DEPTH && static_cast<int64_t>(a.size()) > 4 * leaf) {
+      NdOut oa;
+      std::exception_ptr err;
+      std::thread ta([&] {
+        try {
+          std::vector<int64_t> scratch;
+          rec(std::move(a), depth + 1, oa, scratch);
+        } catch (...) {
+          err = std::current_exception();
+        }
+      });
+      NdOut ob;
+      try {
+        rec(std::move(b), depth + 1, ob, order);
+      } catch (...) {
+        ta.join();
+        throw;
+      }
+      ta.join();
+      if (err) std::rethrow_exception(err);
+      out.append(std::move(oa));
+      out.append(std::move(ob));
+    } else {
+      rec(std::move(a), depth + 1, out, order);
+      rec(std::move(b), depth + 1, out, order);
+    }
+    out.nodes.push_back(std::move(s));
+    out.is_sep.push_back(1);
   }
 };
 
@@ -246,13 +290,17 @@ void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std
   NdState st(g, leaf);
   std::vector<int64_t> all(n);
   std::iota(all.begin(), all.end(), 0);
-  st.rec(std::move(all));
-  nodes = std::move(st.nodes);
+  NdOut res;
+  {
+    std::vector<int64_t> scratch;
+    st.rec(std::move(all), 0, res, scratch);
+  }
+  nodes = std::move(res.nodes);
   static const int sep_mode = [] {
     const char* v = std::getenv("ZOLO_SEP_ORDER");
     return v ? std::atoi(v) : 1;
   }();
-  if (sep_mode) order_separators(g, st.node_is_sep, nodes, sep_mode);
+  if (sep_mode) order_separators(g, res.is_sep, nodes, sep_mode);
   // The node just before a separator (in post-order) is the root of its last child subtree,
   // whose factor structure lies inside separator + struct(separator): the two can share a
   // tile without adding fill, so only nodes followed by a non-separator start a new tile.
@@ -265,7 +313,7 @@ void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std
     std::vector<int64_t> cur;
     for (size_t t = 0; t < nodes.size(); ++t) {
       cur.insert(cur.end(), nodes[t].begin(), nodes[t].end());
-      if (t + 1 == nodes.size() || !st.node_is_sep[t + 1]) {
+      if (t + 1 == nodes.size() || !res.is_sep[t + 1]) {
         out.push_back(std::move(cur));
         cur.clear();
       }
@@ -356,8 +404,16 @@ void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::
   bs.critical_path = cp;
 }
 
+// Target-centric build: the contributions of tile (x, y), x > y, are the k in row(x) ∩ row(y)
+// (both sorted: one merge, no searches or hash maps), those of D(x) the k in row(x); each target's
+// contributions are bucketed by the level of k (stable: ascending k within a level = the fixed
+// summation order). Block rows are independent, so the rows are processed by all host threads:
+// pass 1 counts the (level, targets, contributions) of every row, a prefix sum over rows fixes
+// every row's place in every level (the plan does not depend on the thread count), pass 2 writes
+// the packed arrays in place.
 void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
   const int64_t nb = bs.nb;
+  if (bs.ntiles >= (int64_t(1) << 30)) throw std::runtime_error("factor_plan: too many tiles");
   // level = height in the block elimination tree (parent = first structural row below)
   std::vector<int> level(nb, 0);
   int nlev = 0;
@@ -366,111 +422,156 @@ void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
     if (p >= 0) level[p] = std::max(level[p], level[k] + 1);
     nlev = std::max(nlev, level[k] + 1);
   }
-  std::vector<std::vector<int>> by(nlev);
-  for (int64_t k = 0; k < nb; ++k) by[level[k]].push_back(static_cast<int>(k));
-  const int64_t nkey = nb + 2 * bs.ntiles;  // Dt | Lt | Ut
-  // Levels are independent: each thread builds whole levels with its own scratch, then the
-  // per-level lists are concatenated in level order (targets' contribution offsets rebased).
-  struct Level {
-    std::vector<int> pan, tgt, con;
-  };
-  std::vector<Level> lv(nlev);
-  std::atomic<int> next{0};
-  auto worker = [&] {
-    std::vector<int> slot(nkey, -1), cnt, mark(nb, -1), epos(nb, 0);
-    std::vector<int64_t> keys;
-    for (int l = next++; l < nlev; l = next++) {
-      Level& L = lv[l];
-      keys.clear();
-      cnt.clear();
-      // every (a, b) with a, b in col(k): a == b -> Dt(a); a > b -> Lt(a, b); a < b -> Ut(b, a). The
-      // tile id of (x, y), x > y both in col(k), is found by walking col(y), which holds col(k)'s
-      // rows below y (fill): no searches. visit(key, L(a,k) id, U(k,b) id) in a fixed order.
-      auto enumerate = [&](int k, auto&& visit) {
-        const int64_t e0 = bs.col_ptr[k], e1 = bs.col_ptr[k + 1];
-        for (int64_t e = e0; e < e1; ++e) {
-          mark[bs.col_idx[e]] = k;
-          epos[bs.col_idx[e]] = static_cast<int>(e);
-        }
-        for (int64_t ey = e0; ey < e1; ++ey) {
-          const int64_t y = bs.col_idx[ey];
-          const int ty = static_cast<int>(bs.col_tile[ey]);
-          visit(y, ty, ty);
-          for (int64_t e = bs.col_ptr[y]; e < bs.col_ptr[y + 1]; ++e) {
-            const int64_t x = bs.col_idx[e];
-            if (mark[x] != k) continue;
-            const int64_t t = bs.col_tile[e];
-            const int tx = static_cast<int>(bs.col_tile[epos[x]]);
-            visit(nb + t, tx, ty);              // L(x, y) -= L(x, k) U(k, y)
-            visit(nb + bs.ntiles + t, ty, tx);  // U(y, x) -= L(y, k) U(k, x)
-          }
-        }
-      };
-      for (int k : by[l])
+  plan = FactorPlan();
+  {  // columns and panel tiles by level
+    std::vector<std::vector<int>> by(nlev);
+    for (int64_t k = 0; k < nb; ++k) by[level[k]].push_back(static_cast<int>(k));
+    plan.cols.reserve(nb);
+    plan.pan.reserve(4 * bs.ntiles);
+    plan.lvl_ptr.push_back(0);
+    plan.pan_ptr.push_back(0);
+    for (int l = 0; l < nlev; ++l) {
+      for (int k : by[l]) {
+        plan.cols.push_back(k);
         for (int64_t e = bs.col_ptr[k]; e < bs.col_ptr[k + 1]; ++e) {
           const int id = static_cast<int>(bs.col_tile[e]);
-          L.pan.insert(L.pan.end(), {k, 2 * id, k, 2 * id + 1});
+          plan.pan.insert(plan.pan.end(), {k, 2 * id, k, 2 * id + 1});
         }
-      for (int k : by[l])
-        enumerate(k, [&](int64_t key, int, int) {
-          if (slot[key] < 0) {
-            slot[key] = static_cast<int>(keys.size());
-            keys.push_back(key);
-            cnt.push_back(0);
-          }
-          ++cnt[slot[key]];
-        });
-      int64_t c0 = 0;
-      L.tgt.resize(4 * keys.size());
-      for (size_t t = 0; t < keys.size(); ++t) {
-        const int64_t key = keys[t];
-        const int kind = key < nb ? 0 : (key < nb + bs.ntiles ? 1 : 2);
-        L.tgt[4 * t] = kind;
-        L.tgt[4 * t + 1] = static_cast<int>(kind == 0 ? key : (kind == 1 ? key - nb : key - nb - bs.ntiles));
-        L.tgt[4 * t + 2] = static_cast<int>(c0);
-        L.tgt[4 * t + 3] = static_cast<int>(c0);  // fill cursor -> end
-        c0 += cnt[t];
       }
-      L.con.resize(2 * c0);
-      for (int k : by[l])  // contributions of each target in ascending k (fixed summation order)
-        enumerate(k, [&](int64_t key, int la, int ub) {
-          const int at = L.tgt[4 * slot[key] + 3]++;
-          L.con[2 * at] = la;
-          L.con[2 * at + 1] = ub;
-        });
-      for (int64_t key : keys) slot[key] = -1;
+      plan.lvl_ptr.push_back(static_cast<int>(plan.cols.size()));
+      plan.pan_ptr.push_back(static_cast<int>(plan.pan.size() / 2));
+    }
+  }
+  // Every block row's entries re-sorted by (level of k, k): two rows merged in that order yield
+  // their common k grouped by level, ascending k within a level -- a target's contributions per
+  // level in the fixed summation order, with no per-target sort.
+  struct Ent {
+    int lvl, k, id;
+  };
+  std::vector<Ent> ent(bs.ntiles);
+  for (int64_t x = 0; x < nb; ++x) {
+    for (int64_t e = bs.row_ptr[x]; e < bs.row_ptr[x + 1]; ++e)
+      ent[e] = {level[bs.row_idx[e]], static_cast<int>(bs.row_idx[e]), static_cast<int>(e)};
+    std::sort(ent.begin() + bs.row_ptr[x], ent.begin() + bs.row_ptr[x + 1],
+              [](const Ent& p, const Ent& q) { return p.lvl < q.lvl || (p.lvl == q.lvl && p.k < q.k); });
+  }
+  // One contribution: L tile id, U tile id. emit(kind, tile id, level, first, last) per target
+  // and level, contributions [first, last) of `buf`; the U target of a tile follows its L target
+  // with the same contributions, ids swapped.
+  struct Con {
+    int la, ub;
+  };
+  auto row_targets = [&](int64_t x, std::vector<Con>& buf, auto&& emit) {
+    const Ent* rx = ent.data() + bs.row_ptr[x];
+    const int nx = static_cast<int>(bs.row_ptr[x + 1] - bs.row_ptr[x]);
+    buf.resize(std::max<size_t>(buf.size(), nx));
+    for (int q = 0; q < nx;) {  // D(x) -= L(x, k) U(k, x)
+      int e = q;
+      for (; e < nx && rx[e].lvl == rx[q].lvl; ++e) buf[e] = {rx[e].id, rx[e].id};
+      emit(0, static_cast<int>(x), rx[q].lvl, q, e);
+      q = e;
+    }
+    for (int64_t ey = bs.row_ptr[x]; ey < bs.row_ptr[x + 1]; ++ey) {
+      const int64_t y = bs.row_idx[ey];
+      const Ent* ry = ent.data() + bs.row_ptr[y];
+      const int ny = static_cast<int>(bs.row_ptr[y + 1] - bs.row_ptr[y]);
+      // k in row(x) ∩ row(y) (all below y): L(x, y) -= L(x, k) U(k, y), U(y, x) -= L(y, k) U(k, x)
+      int a = 0, b = 0, m = 0, cur = -1;
+      while (a < nx && b < ny) {
+        const Ent &p = rx[a], &q = ry[b];
+        if (p.lvl == q.lvl && p.k == q.k) {
+          if (p.lvl != cur) {
+            if (m) emit(1, static_cast<int>(ey), cur, 0, m);
+            cur = p.lvl;
+            m = 0;
+          }
+          buf[m++] = {p.id, q.id};
+          ++a, ++b;
+        } else if (p.lvl < q.lvl || (p.lvl == q.lvl && p.k < q.k)) {
+          ++a;
+        } else {
+          ++b;
+        }
+      }
+      if (m) emit(1, static_cast<int>(ey), cur, 0, m);
     }
   };
+  // pass 1: per row, its (level, targets, contributions) triples in ascending level
+  struct Cnt {
+    int lvl, nt, nc;
+  };
+  std::vector<std::vector<Cnt>> rows(nb);
   const int nthr = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
-  std::vector<std::thread> pool;
-  for (int q = 1; q < nthr; ++q) pool.emplace_back(worker);
-  worker();
-  for (auto& t : pool) t.join();
-  plan = FactorPlan();
-  int64_t ncon = 0, ntgt = 0, npan = 0;
-  for (const Level& L : lv) ncon += L.con.size() / 2, ntgt += L.tgt.size() / 4, npan += L.pan.size() / 2;
-  if (ncon >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
-  plan.cols.reserve(nb);
-  plan.pan.reserve(2 * npan);
-  plan.tgt.reserve(4 * ntgt);
-  plan.con.reserve(2 * ncon);
-  plan.lvl_ptr.push_back(0);
-  plan.pan_ptr.push_back(0);
-  plan.tgt_ptr.push_back(0);
-  for (int l = 0; l < nlev; ++l) {
-    const int base = static_cast<int>(plan.con.size() / 2);
-    for (int k : by[l]) plan.cols.push_back(k);
-    plan.pan.insert(plan.pan.end(), lv[l].pan.begin(), lv[l].pan.end());
-    for (size_t t = 0; t < lv[l].tgt.size(); t += 4) {
-      plan.tgt.insert(plan.tgt.end(), {lv[l].tgt[t], lv[l].tgt[t + 1], lv[l].tgt[t + 2] + base, lv[l].tgt[t + 3] + base});
+  auto run = [&](auto&& body) {
+    std::atomic<int64_t> next{0};
+    auto worker = [&] {
+      std::vector<Con> buf;
+      std::vector<int> nt(nlev, 0), nc(nlev, 0), touched;
+      // heavy rows (the separators at the end) first
+      for (int64_t i = next++; i < nb; i = next++) body(nb - 1 - i, buf, nt, nc, touched);
+    };
+    std::vector<std::thread> pool;
+    for (int q = 1; q < nthr; ++q) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+  };
+  run([&](int64_t x, std::vector<Con>& buf, std::vector<int>& nt, std::vector<int>& nc, std::vector<int>& touched) {
+    touched.clear();
+    row_targets(x, buf, [&](int kind, int, int l, int q, int e) {
+      const int both = kind ? 2 : 1;  // a tile's L and U targets
+      if (nt[l] == 0) touched.push_back(l);
+      nt[l] += both;
+      nc[l] += both * (e - q);
+    });
+    std::sort(touched.begin(), touched.end());
+    rows[x].reserve(touched.size());
+    for (int l : touched) {
+      rows[x].push_back({l, nt[l], nc[l]});
+      nt[l] = nc[l] = 0;
     }
-    plan.con.insert(plan.con.end(), lv[l].con.begin(), lv[l].con.end());
-    std::vector<int>().swap(lv[l].con);
-    plan.lvl_ptr.push_back(static_cast<int>(plan.cols.size()));
-    plan.pan_ptr.push_back(static_cast<int>(plan.pan.size() / 2));
-    plan.tgt_ptr.push_back(static_cast<int>(plan.tgt.size() / 4));
+  });
+  // offsets: level-major, rows ascending within a level
+  std::vector<int64_t> lt(nlev + 1, 0), lc(nlev + 1, 0);
+  for (int64_t x = 0; x < nb; ++x)
+    for (const Cnt& c : rows[x]) lt[c.lvl + 1] += c.nt, lc[c.lvl + 1] += c.nc;
+  for (int l = 0; l < nlev; ++l) lt[l + 1] += lt[l], lc[l + 1] += lc[l];
+  const int64_t ntgt = lt[nlev], ncon = lc[nlev];
+  if (ncon >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
+  plan.tgt_ptr.assign(lt.begin(), lt.end());
+  {
+    std::vector<int64_t> ct(lt.begin(), lt.end() - 1), cc(lc.begin(), lc.end() - 1);
+    for (int64_t x = 0; x < nb; ++x)
+      for (Cnt& c : rows[x]) {  // counts -> this row's first target / contribution in its level
+        const int nt = c.nt, nc = c.nc;
+        c.nt = static_cast<int>(ct[c.lvl]);
+        c.nc = static_cast<int>(cc[c.lvl]);
+        ct[c.lvl] += nt;
+        cc[c.lvl] += nc;
+      }
   }
-  plan.contributions = static_cast<int64_t>(plan.con.size() / 2);
+  plan.tgt.resize(2 * ntgt + 2);
+  plan.con.resize(2 * ncon);
+  plan.tgt[2 * ntgt] = 0;
+  plan.tgt[2 * ntgt + 1] = static_cast<int>(ncon);  // sentinel: the last target's end
+  // pass 2: the same enumeration, written in place (nt / nc reused as per-level cursors)
+  run([&](int64_t x, std::vector<Con>& buf, std::vector<int>& nt, std::vector<int>& nc, std::vector<int>&) {
+    for (const Cnt& c : rows[x]) nt[c.lvl] = c.nt, nc[c.lvl] = c.nc;
+    row_targets(x, buf, [&](int kind, int id, int l, int q, int e) {
+      int t = nt[l], c = nc[l];
+      plan.tgt[2 * t] = static_cast<int>(static_cast<unsigned>(kind) << 30 | static_cast<unsigned>(id));
+      plan.tgt[2 * t + 1] = c;
+      for (int i = q; i < e; ++i, ++c) plan.con[2 * c] = buf[i].la, plan.con[2 * c + 1] = buf[i].ub;
+      if (kind) {  // the U target: same k, ids swapped
+        ++t;
+        plan.tgt[2 * t] = static_cast<int>(2u << 30 | static_cast<unsigned>(id));
+        plan.tgt[2 * t + 1] = c;
+        for (int i = q; i < e; ++i, ++c) plan.con[2 * c] = buf[i].ub, plan.con[2 * c + 1] = buf[i].la;
+      }
+      nt[l] = t + 1;
+      nc[l] = c;
+    });
+  });
+  plan.contributions = ncon;
 }
 
 int trailing_dense_start(const BlockStructure& bs, int kmax) {

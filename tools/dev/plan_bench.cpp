@@ -32,7 +32,7 @@ int main(int argc, char** argv) {
   int64_t single = 0, multi = 0;
   for (size_t l = 0; l + 1 < plan.lvl_ptr.size(); ++l) {
     int64_t c = 0;
-    for (int t = plan.tgt_ptr[l]; t < plan.tgt_ptr[l + 1]; ++t) c += plan.tgt[4 * t + 3] - plan.tgt[4 * t + 2];
+    for (int t = plan.tgt_ptr[l]; t < plan.tgt_ptr[l + 1]; ++t) c += plan.tgt[2 * t + 3] - plan.tgt[2 * t + 1];
     (plan.lvl_ptr[l + 1] - plan.lvl_ptr[l] == 1 ? single : multi) += c;
   }
   // canonical hash: per level, targets sorted by (kind, id), each with its ordered contributions
@@ -42,12 +42,12 @@ int main(int argc, char** argv) {
     std::vector<int> ts;
     for (int t = plan.tgt_ptr[l]; t < plan.tgt_ptr[l + 1]; ++t) ts.push_back(t);
     std::sort(ts.begin(), ts.end(), [&](int a, int b) {
-      return std::make_pair(plan.tgt[4 * a], plan.tgt[4 * a + 1]) < std::make_pair(plan.tgt[4 * b], plan.tgt[4 * b + 1]);
+      return static_cast<unsigned>(plan.tgt[2 * a]) < static_cast<unsigned>(plan.tgt[2 * b]);  // (kind, id) packed
     });
     for (int t : ts) {
-      mix(plan.tgt[4 * t]);
-      mix(plan.tgt[4 * t + 1]);
-      for (int q = plan.tgt[4 * t + 2]; q < plan.tgt[4 * t + 3]; ++q) mix(plan.con[2 * q]), mix(plan.con[2 * q + 1]);
+      mix(static_cast<unsigned>(plan.tgt[2 * t]) >> 30);
+      mix(plan.tgt[2 * t] & 0x3fffffff);
+      for (int q = plan.tgt[2 * t + 1]; q < plan.tgt[2 * t + 3]; ++q) mix(plan.con[2 * q]), mix(plan.con[2 * q + 1]);
     }
     for (int q = plan.pan_ptr[l]; q < plan.pan_ptr[l + 1]; ++q) mix(plan.pan[2 * q]), mix(plan.pan[2 * q + 1]);
   }
@@ -56,6 +56,6 @@ int main(int argc, char** argv) {
               "contributions %lld (single-column levels %lld, multi %lld), targets %zu\n",
               static_cast<long long>(bs.nb), static_cast<long long>(bs.ntiles), plan.lvl_ptr.size() - 1, ms(t0, t1),
               ms(t1, t2), ms(t2, t3), static_cast<long long>(plan.contributions), static_cast<long long>(single),
-              static_cast<long long>(multi), plan.tgt.size() / 4);
+              static_cast<long long>(multi), plan.tgt.size() / 2 - 1);
   return 0;
 }
