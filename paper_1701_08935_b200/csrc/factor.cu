@@ -227,15 +227,16 @@ __global__ void __launch_bounds__(ST) panel_level_kernel(const int* pan, int p0,
     tile_mm_dmma(DinvL + static_cast<size_t>(k) * TT, c, c);
 }
 
-// One trailing-update target per CTA: C -= sum_k L(a,k) U(k,b) over its contributions (fixed
-// ascending-k order) on DMMA, 3M complex products (mma.cuh mma_tile3_nx: 3 real DMMAs per complex
-// MAC instead of 4: cfg3's factorization 746 -> ~595 ms). Single-buffered stages with 4 resident
-// targets per SM hiding the loads. Two 34 KiB stages per target measured slower (3 targets per SM:
-// 630 ms, 2: 746 ms); built from cp.async with the L2::cache_hint operand that two-stage loop
-// raises "illegal instruction" on the B200 (3M and 4M alike; plain cp.async runs).
-constexpr int TRAIL_SMEM = (TT + XS2) * static_cast<int>(sizeof(cd));
+// One trailing-update target per CTA (left-looking: the tile's whole update, written once):
+// C -= sum_k L(a,k) U(k,b) over ALL its contributions (fixed ascending-k order) on DMMA, 3M complex
+// products (mma.cuh mma_tile3_nx: 3 real DMMAs per complex MAC instead of 4), accumulators in
+// registers across the list. Two 34 KiB stages: the next contribution's tiles stream in (plain
+// cp.async; with the L2::cache_hint operand this loop raised "illegal instruction" on the B200)
+// while the current product runs; 3 targets resident per SM.
+constexpr int TRAIL_STAGE = TT + XS2;
+constexpr int TRAIL_SMEM = 2 * TRAIL_STAGE * static_cast<int>(sizeof(cd));
 #ifndef ZOLO_TRAIL_MINB
-#define ZOLO_TRAIL_MINB 4
+#define ZOLO_TRAIL_MINB 3
 #endif
 __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(const int* tgt, const int* con, int t0, cd* Dt,
                                                                cd* Lt, cd* Ut) {
@@ -243,18 +244,27 @@ __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(con
   cd* sm = reinterpret_cast<cd*>(trail_smem);
   const int* T = tgt + 2 * (t0 + blockIdx.x);  // packed: kind << 30 | tile id, first contribution; end = the next target's first
   const int kind = static_cast<unsigned>(T[0]) >> 30, id = T[0] & 0x3fffffff, cb = T[1], ce = T[3];
-  const unsigned long long pol = l2_evict_normal();
   const Frag f = frag();
   Acc3<2> acc;
   acc3_zero(acc);
-  for (int q = cb; q < ce; ++q) {
-    load_tile_sw(sm, Lt + static_cast<size_t>(con[2 * q]) * TT, pol);
-    load_x32(sm + TT, Ut + static_cast<size_t>(con[2 * q + 1]) * TT, TILE, 0, TILE, pol);
+  auto issue = [&](int q, int stage) {
+    cd* s = sm + stage * TRAIL_STAGE;
+    load_tile_sw(s, Lt + static_cast<size_t>(con[2 * q]) * TT);
+    load_x32(s + TT, Ut + static_cast<size_t>(con[2 * q + 1]) * TT, TILE, 0);
     cp_async_commit();
-    cp_async_wait<0>();
+  };
+  if (cb < ce) issue(cb, 0);
+  for (int q = cb; q < ce; ++q) {
+    const int stage = (q - cb) & 1;
+    if (q + 1 < ce) {
+      issue(q + 1, stage ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    mma_tile3_nx(acc, sm, sm + TT, f);
-    __syncthreads();
+    mma_tile3_nx(acc, sm + stage * TRAIL_STAGE, sm + stage * TRAIL_STAGE + TT, f);
+    __syncthreads();  // the stage is refilled two iterations later
   }
   cd prod[4];
   acc3_fold(acc, prod);
@@ -295,18 +305,19 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const SpFactor& f, int64_t nnz,
   // the attributes are per device (a process may drive several GPUs)
   cudaFuncSetAttribute(diag_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, diag_smem);
   cudaFuncSetAttribute(trailing_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRAIL_SMEM);
-  // level-scheduled: 3 launches per level of the block elimination tree
+  // level-scheduled, left-looking: per level of the block elimination tree the updates of its
+  // block columns (and block rows of U), their diagonal blocks, their panels -- 3 launches
   const std::vector<int>& lv = *plan.lvl_ptr;
   const std::vector<int>& pp = *plan.pan_ptr;
   const std::vector<int>& tp = *plan.tgt_ptr;
   for (size_t l = 0; l + 1 < lv.size(); ++l) {
+    if (tp[l + 1] > tp[l])
+      trailing_level_kernel<<<tp[l + 1] - tp[l], ST, TRAIL_SMEM, st>>>(plan.tgt, plan.con, tp[l], f.Dt, f.Lt, f.Ut);
     if (lv[l + 1] > lv[l])
       diag_level_kernel<<<lv[l + 1] - lv[l], FT, diag_smem, st>>>(plan.cols, lv[l], s.npad, f.Dt, f.DinvL, f.DinvU,
                                                                    row_norm, ds.fail_index, ds.min_ratio_bits);
     if (pp[l + 1] > pp[l])
       panel_level_kernel<<<pp[l + 1] - pp[l], ST, 0, st>>>(plan.pan, pp[l], f.Lt, f.Ut, f.DinvL, f.DinvU);
-    if (tp[l + 1] > tp[l])
-      trailing_level_kernel<<<tp[l + 1] - tp[l], ST, TRAIL_SMEM, st>>>(plan.tgt, plan.con, tp[l], f.Dt, f.Lt, f.Ut);
   }
   if (s.ntiles > 0) scale_sp_kernel<<<dim3(static_cast<unsigned>(s.ntiles), 2), ST, 0, st>>>(s, f.Lt, f.Ut, f.DinvL, f.DinvU);
 }

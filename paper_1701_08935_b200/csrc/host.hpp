@@ -23,11 +23,12 @@ struct BlockStructure {
 void nd_order(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, std::vector<std::vector<int64_t>>& nodes);
 void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::vector<std::vector<int64_t>>& nodes,
                     int tile, BlockStructure& bs);
-// Level-scheduled block LU (factor.cu sp_factor): block columns grouped by
-// their height in the block elimination tree (columns of one level are
-// independent); per level the panel tiles and the trailing-update targets,
-// each target with its contributions (L(a,k), U(k,b)) in ascending k so the
-// accumulation order is fixed (deterministic factors).
+// Level-scheduled left-looking block LU (factor.cu sp_factor): block columns grouped by their
+// height in the block elimination tree (columns of one level are independent). Per level: the
+// trailing-update targets of its columns -- D(y), L(x, y), U(y, x) -- each with ALL its
+// contributions (L(a,k), U(k,b)) in ascending k, so the accumulation order is fixed
+// (deterministic factors) and every tile is written once; then the diagonal blocks; then the
+// panel tiles.
 //   pan: 2 ints per item (k, 2 * tile id + upper)
 //   tgt: 2 ints per target (kind 0 = Dt / 1 = Lt / 2 = Ut in bits 30-31 | tile id, first
 //        contribution); a target's contributions end where the next target's begin (the lists are

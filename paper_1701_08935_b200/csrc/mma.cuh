@@ -53,6 +53,16 @@ __device__ __forceinline__ void load_tile_sw(cd* s, const cd* g, unsigned long l
   }
 }
 
+// the same without an L2 policy (plain cp.async)
+__device__ __forceinline__ void load_tile_sw(cd* s, const cd* g) {
+#pragma unroll
+  for (int q = 0; q < TT / ST; ++q) {
+    const int e = threadIdx.x + q * ST;
+    const int col = e / TILE, row = e % TILE;
+    cp_async16_cg(&s[col * TILE + (row ^ swz(col))], g + e);
+  }
+}
+
 // non-volatile DMMA: lets the scheduler interleave independent accumulators
 __device__ __forceinline__ void dmma_nv(double c[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -292,6 +302,16 @@ __device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int
       cp_async16_cg_hint(&xs[c * XPAD + row], base + row + (c0 + c) * ld, pol);
     else
       xs[c * XPAD + row] = mk(0.0, 0.0);
+  }
+}
+
+// all 32 columns, without an L2 policy (plain cp.async)
+__device__ __forceinline__ void load_x32(cd* xs, const cd* base, int64_t ld, int c0) {
+  const int row = threadIdx.x & 31, cc = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < DCG / 8; ++q) {
+    const int c = cc + 8 * q;
+    cp_async16_cg(&xs[c * XPAD + row], base + row + (c0 + c) * ld);
   }
 }
 

@@ -404,13 +404,13 @@ void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::
   bs.critical_path = cp;
 }
 
-// Target-centric build: the contributions of tile (x, y), x > y, are the k in row(x) ∩ row(y)
-// (both sorted: one merge, no searches or hash maps), those of D(x) the k in row(x); each target's
-// contributions are bucketed by the level of k (stable: ascending k within a level = the fixed
-// summation order). Block rows are independent, so the rows are processed by all host threads:
-// pass 1 counts the (level, targets, contributions) of every row, a prefix sum over rows fixes
-// every row's place in every level (the plan does not depend on the thread count), pass 2 writes
-// the packed arrays in place.
+// Left-looking plan: block column y (and block row y of U) is completed at the level of y. The
+// contributions of tile (x, y), x > y, are the k in row(x) ∩ row(y) (both sorted by k: one merge,
+// no searches), those of D(y) the k in row(y); every such k is a descendant of y in the block
+// elimination tree, so its panels are final at a lower level. A target collects ALL its
+// contributions in ascending k (the fixed summation order) and is written once. Block columns are
+// independent: all host threads count (pass 1), a prefix sum in level / column order fixes every
+// column's place (the plan does not depend on the thread count), pass 2 writes the packed arrays.
 void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
   const int64_t nb = bs.nb;
   if (bs.ntiles >= (int64_t(1) << 30)) throw std::runtime_error("factor_plan: too many tiles");
@@ -423,152 +423,112 @@ void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
     nlev = std::max(nlev, level[k] + 1);
   }
   plan = FactorPlan();
-  {  // columns and panel tiles by level
-    std::vector<std::vector<int>> by(nlev);
-    for (int64_t k = 0; k < nb; ++k) by[level[k]].push_back(static_cast<int>(k));
-    plan.cols.reserve(nb);
-    plan.pan.reserve(4 * bs.ntiles);
-    plan.lvl_ptr.push_back(0);
-    plan.pan_ptr.push_back(0);
-    for (int l = 0; l < nlev; ++l) {
-      for (int k : by[l]) {
-        plan.cols.push_back(k);
-        for (int64_t e = bs.col_ptr[k]; e < bs.col_ptr[k + 1]; ++e) {
-          const int id = static_cast<int>(bs.col_tile[e]);
-          plan.pan.insert(plan.pan.end(), {k, 2 * id, k, 2 * id + 1});
-        }
+  // columns and panel tiles by level
+  std::vector<std::vector<int>> by(nlev);
+  for (int64_t k = 0; k < nb; ++k) by[level[k]].push_back(static_cast<int>(k));
+  plan.cols.reserve(nb);
+  plan.pan.reserve(4 * bs.ntiles);
+  plan.lvl_ptr.push_back(0);
+  plan.pan_ptr.push_back(0);
+  for (int l = 0; l < nlev; ++l) {
+    for (int k : by[l]) {
+      plan.cols.push_back(k);
+      for (int64_t e = bs.col_ptr[k]; e < bs.col_ptr[k + 1]; ++e) {
+        const int id = static_cast<int>(bs.col_tile[e]);
+        plan.pan.insert(plan.pan.end(), {k, 2 * id, k, 2 * id + 1});
       }
-      plan.lvl_ptr.push_back(static_cast<int>(plan.cols.size()));
-      plan.pan_ptr.push_back(static_cast<int>(plan.pan.size() / 2));
     }
+    plan.lvl_ptr.push_back(static_cast<int>(plan.cols.size()));
+    plan.pan_ptr.push_back(static_cast<int>(plan.pan.size() / 2));
   }
-  // Every block row's entries re-sorted by (level of k, k): two rows merged in that order yield
-  // their common k grouped by level, ascending k within a level -- a target's contributions per
-  // level in the fixed summation order, with no per-target sort.
-  struct Ent {
-    int lvl, k, id;
-  };
-  std::vector<Ent> ent(bs.ntiles);
-  for (int64_t x = 0; x < nb; ++x) {
-    for (int64_t e = bs.row_ptr[x]; e < bs.row_ptr[x + 1]; ++e)
-      ent[e] = {level[bs.row_idx[e]], static_cast<int>(bs.row_idx[e]), static_cast<int>(e)};
-    std::sort(ent.begin() + bs.row_ptr[x], ent.begin() + bs.row_ptr[x + 1],
-              [](const Ent& p, const Ent& q) { return p.lvl < q.lvl || (p.lvl == q.lvl && p.k < q.k); });
-  }
-  // One contribution: L tile id, U tile id. emit(kind, tile id, level, first, last) per target
-  // and level, contributions [first, last) of `buf`; the U target of a tile follows its L target
-  // with the same contributions, ids swapped.
+  // targets of block column y: emit(kind, tile id, m) with the m contributions (L tile id, U tile
+  // id) in buf[0, m); the U target of a tile has the same k with the ids swapped
   struct Con {
     int la, ub;
   };
-  auto row_targets = [&](int64_t x, std::vector<Con>& buf, auto&& emit) {
-    const Ent* rx = ent.data() + bs.row_ptr[x];
-    const int nx = static_cast<int>(bs.row_ptr[x + 1] - bs.row_ptr[x]);
-    buf.resize(std::max<size_t>(buf.size(), nx));
-    for (int q = 0; q < nx;) {  // D(x) -= L(x, k) U(k, x)
-      int e = q;
-      for (; e < nx && rx[e].lvl == rx[q].lvl; ++e) buf[e] = {rx[e].id, rx[e].id};
-      emit(0, static_cast<int>(x), rx[q].lvl, q, e);
-      q = e;
+  auto column_targets = [&](int64_t y, std::vector<Con>& buf, auto&& emit) {
+    const int64_t y0 = bs.row_ptr[y], y1 = bs.row_ptr[y + 1];
+    const int ny = static_cast<int>(y1 - y0);
+    buf.resize(std::max<size_t>(buf.size(), ny));
+    if (ny) {  // D(y) -= L(y, k) U(k, y)
+      for (int q = 0; q < ny; ++q) buf[q] = {static_cast<int>(y0 + q), static_cast<int>(y0 + q)};
+      emit(0, static_cast<int>(y), ny);
     }
-    for (int64_t ey = bs.row_ptr[x]; ey < bs.row_ptr[x + 1]; ++ey) {
-      const int64_t y = bs.row_idx[ey];
-      const Ent* ry = ent.data() + bs.row_ptr[y];
-      const int ny = static_cast<int>(bs.row_ptr[y + 1] - bs.row_ptr[y]);
-      // k in row(x) ∩ row(y) (all below y): L(x, y) -= L(x, k) U(k, y), U(y, x) -= L(y, k) U(k, x)
-      int a = 0, b = 0, m = 0, cur = -1;
-      while (a < nx && b < ny) {
-        const Ent &p = rx[a], &q = ry[b];
-        if (p.lvl == q.lvl && p.k == q.k) {
-          if (p.lvl != cur) {
-            if (m) emit(1, static_cast<int>(ey), cur, 0, m);
-            cur = p.lvl;
-            m = 0;
-          }
-          buf[m++] = {p.id, q.id};
-          ++a, ++b;
-        } else if (p.lvl < q.lvl || (p.lvl == q.lvl && p.k < q.k)) {
+    if (!ny) return;
+    for (int64_t e = bs.col_ptr[y]; e < bs.col_ptr[y + 1]; ++e) {
+      const int64_t x = bs.col_idx[e];
+      // k in row(x) ∩ row(y): L(x, y) -= L(x, k) U(k, y), U(y, x) -= L(y, k) U(k, x)
+      int64_t a = bs.row_ptr[x], b = y0;
+      const int64_t a1 = bs.row_ptr[x + 1];
+      int m = 0;
+      while (a < a1 && b < y1) {
+        const int64_t ka = bs.row_idx[a], kb = bs.row_idx[b];
+        if (ka == kb)
+          buf[m++] = {static_cast<int>(a), static_cast<int>(b)}, ++a, ++b;
+        else if (ka < kb)
           ++a;
-        } else {
+        else
           ++b;
-        }
       }
-      if (m) emit(1, static_cast<int>(ey), cur, 0, m);
+      if (m) emit(1, static_cast<int>(bs.col_tile[e]), m);
     }
   };
-  // pass 1: per row, its (level, targets, contributions) triples in ascending level
   struct Cnt {
-    int lvl, nt, nc;
+    int64_t nt = 0, nc = 0;
   };
-  std::vector<std::vector<Cnt>> rows(nb);
+  std::vector<Cnt> cnt(nb);
   const int nthr = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
   auto run = [&](auto&& body) {
     std::atomic<int64_t> next{0};
     auto worker = [&] {
       std::vector<Con> buf;
-      std::vector<int> nt(nlev, 0), nc(nlev, 0), touched;
-      // heavy rows (the separators at the end) first
-      for (int64_t i = next++; i < nb; i = next++) body(nb - 1 - i, buf, nt, nc, touched);
+      // heavy columns (the separators at the end) first
+      for (int64_t i = next++; i < nb; i = next++) body(nb - 1 - i, buf);
     };
     std::vector<std::thread> pool;
     for (int q = 1; q < nthr; ++q) pool.emplace_back(worker);
     worker();
     for (auto& t : pool) t.join();
   };
-  run([&](int64_t x, std::vector<Con>& buf, std::vector<int>& nt, std::vector<int>& nc, std::vector<int>& touched) {
-    touched.clear();
-    row_targets(x, buf, [&](int kind, int, int l, int q, int e) {
-      const int both = kind ? 2 : 1;  // a tile's L and U targets
-      if (nt[l] == 0) touched.push_back(l);
-      nt[l] += both;
-      nc[l] += both * (e - q);
+  run([&](int64_t y, std::vector<Con>& buf) {
+    Cnt c;
+    column_targets(y, buf, [&](int kind, int, int m) {
+      const int both = kind ? 2 : 1;
+      c.nt += both;
+      c.nc += both * m;
     });
-    std::sort(touched.begin(), touched.end());
-    rows[x].reserve(touched.size());
-    for (int l : touched) {
-      rows[x].push_back({l, nt[l], nc[l]});
-      nt[l] = nc[l] = 0;
-    }
+    cnt[y] = c;
   });
-  // offsets: level-major, rows ascending within a level
-  std::vector<int64_t> lt(nlev + 1, 0), lc(nlev + 1, 0);
-  for (int64_t x = 0; x < nb; ++x)
-    for (const Cnt& c : rows[x]) lt[c.lvl + 1] += c.nt, lc[c.lvl + 1] += c.nc;
-  for (int l = 0; l < nlev; ++l) lt[l + 1] += lt[l], lc[l + 1] += lc[l];
-  const int64_t ntgt = lt[nlev], ncon = lc[nlev];
-  if (ncon >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
-  plan.tgt_ptr.assign(lt.begin(), lt.end());
-  {
-    std::vector<int64_t> ct(lt.begin(), lt.end() - 1), cc(lc.begin(), lc.end() - 1);
-    for (int64_t x = 0; x < nb; ++x)
-      for (Cnt& c : rows[x]) {  // counts -> this row's first target / contribution in its level
-        const int nt = c.nt, nc = c.nc;
-        c.nt = static_cast<int>(ct[c.lvl]);
-        c.nc = static_cast<int>(cc[c.lvl]);
-        ct[c.lvl] += nt;
-        cc[c.lvl] += nc;
-      }
+  // offsets in level order, columns in plan.cols order
+  plan.tgt_ptr.assign(1, 0);
+  int64_t ntgt = 0, ncon = 0;
+  for (int l = 0; l < nlev; ++l) {
+    for (int y : by[l]) {
+      const Cnt c = cnt[y];
+      cnt[y] = {ntgt, ncon};
+      ntgt += c.nt;
+      ncon += c.nc;
+    }
+    plan.tgt_ptr.push_back(static_cast<int>(ntgt));
   }
+  if (ncon >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
   plan.tgt.resize(2 * ntgt + 2);
   plan.con.resize(2 * ncon);
   plan.tgt[2 * ntgt] = 0;
   plan.tgt[2 * ntgt + 1] = static_cast<int>(ncon);  // sentinel: the last target's end
-  // pass 2: the same enumeration, written in place (nt / nc reused as per-level cursors)
-  run([&](int64_t x, std::vector<Con>& buf, std::vector<int>& nt, std::vector<int>& nc, std::vector<int>&) {
-    for (const Cnt& c : rows[x]) nt[c.lvl] = c.nt, nc[c.lvl] = c.nc;
-    row_targets(x, buf, [&](int kind, int id, int l, int q, int e) {
-      int t = nt[l], c = nc[l];
+  run([&](int64_t y, std::vector<Con>& buf) {
+    int64_t t = cnt[y].nt, c = cnt[y].nc;
+    column_targets(y, buf, [&](int kind, int id, int m) {
       plan.tgt[2 * t] = static_cast<int>(static_cast<unsigned>(kind) << 30 | static_cast<unsigned>(id));
-      plan.tgt[2 * t + 1] = c;
-      for (int i = q; i < e; ++i, ++c) plan.con[2 * c] = buf[i].la, plan.con[2 * c + 1] = buf[i].ub;
+      plan.tgt[2 * t + 1] = static_cast<int>(c);
+      for (int i = 0; i < m; ++i, ++c) plan.con[2 * c] = buf[i].la, plan.con[2 * c + 1] = buf[i].ub;
+      ++t;
       if (kind) {  // the U target: same k, ids swapped
-        ++t;
         plan.tgt[2 * t] = static_cast<int>(2u << 30 | static_cast<unsigned>(id));
-        plan.tgt[2 * t + 1] = c;
-        for (int i = q; i < e; ++i, ++c) plan.con[2 * c] = buf[i].ub, plan.con[2 * c + 1] = buf[i].la;
+        plan.tgt[2 * t + 1] = static_cast<int>(c);
+        for (int i = 0; i < m; ++i, ++c) plan.con[2 * c] = buf[i].ub, plan.con[2 * c + 1] = buf[i].la;
+        ++t;
       }
-      nt[l] = t + 1;
-      nc[l] = c;
     });
   });
   plan.contributions = ncon;
