@@ -455,7 +455,10 @@ Union union_pattern(const zolo_ctx& c) {
   const int64_t n = c.n;
   const int w = c.cx ? 2 : 1;
   u.rp.assign(n + 1, 0);
-  u.ci.reserve(c.a_ci.size() + (c.b_identity ? n : c.b_ci.size()));
+  const size_t cap = c.a_ci.size() + (c.b_identity ? n : c.b_ci.size());
+  u.ci.reserve(cap);
+  u.av.reserve(cap * w);
+  u.bv.reserve(cap * w);
   for (int64_t i = 0; i < n; ++i) {
     int64_t ka = c.a_rp[i], kb = c.b_identity ? 0 : c.b_rp[i];
     const int64_t ea = c.a_rp[i + 1], eb = c.b_identity ? 1 : c.b_rp[i + 1];
@@ -574,17 +577,38 @@ void upload_device_bsr(zolo_ctx& c, const std::vector<int>& pos) {
 }
 
 void upload_device_pencil(zolo_ctx& c, const std::vector<int64_t>& inv, const std::vector<int>& pos) {
-  upload_device_bsr(c, pos);
   const int w = c.cx ? 2 : 1;
   const int64_t npad = static_cast<int64_t>(inv.size());
-  std::vector<int> prp, pci;
-  std::vector<double> pv;
+  std::vector<int> prp, pci, brp, bci;
+  std::vector<double> pv, bv;
+  // B's permuted copy on a host thread beside A's (plain host work; bad_alloc is the only failure)
+  std::exception_ptr berr;
+  std::thread tb;
+  if (!c.b_identity)
+    tb = std::thread([&] {
+      try {
+        permuted_csr(npad, inv, pos, c.b_rp, c.b_ci, c.b_v, w, brp, bci, bv);
+      } catch (...) {
+        berr = std::current_exception();
+      }
+    });
+  struct Join {
+    std::thread& t;
+    ~Join() {
+      if (t.joinable()) t.join();
+    }
+  } join_b{tb};
+  upload_device_bsr(c, pos);
   permuted_csr(npad, inv, pos, c.a_rp, c.a_ci, c.a_v, w, prp, pci, pv);
   upload(c.arp_d, prp, c.st);
   upload(c.aci_d, pci, c.st);
   upload(c.av_d, pv, c.st);
   if (!c.b_identity) {
-    permuted_csr(npad, inv, pos, c.b_rp, c.b_ci, c.b_v, w, prp, pci, pv);
+    tb.join();
+    if (berr) std::rethrow_exception(berr);
+    prp.swap(brp);
+    pci.swap(bci);
+    pv.swap(bv);
     upload(c.brp_d, prp, c.st);
     upload(c.bci_d, pci, c.st);
     upload(c.bv_d, pv, c.st);
@@ -2063,15 +2087,19 @@ int zolo_pencil_upload(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, 
       c->b_ci.clear();
       c->b_v.clear();
     }
+    // (the message strings are built only on failure: this loop visits every entry)
+    const auto sorted_in_range = [n](const std::vector<int64_t>& rp, const std::vector<int64_t>& ci, int64_t i) {
+      bool ok = true;
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+        ok = ok && ci[k] >= 0 && ci[k] < n && (k == rp[i] || ci[k] > ci[k - 1]);
+      return ok;
+    };
     for (int64_t i = 0; i < n; ++i) {
-      require(c->a_rp[i] <= c->a_rp[i + 1], "zolo_pencil_upload: A offsets not monotone");
-      for (int64_t k = c->a_rp[i]; k < c->a_rp[i + 1]; ++k)
-        require(c->a_ci[k] >= 0 && c->a_ci[k] < n && (k == c->a_rp[i] || c->a_ci[k] > c->a_ci[k - 1]),
-                "zolo_pencil_upload: A column indices must be in range and sorted");
-      if (!c->b_identity)
-        for (int64_t k = c->b_rp[i]; k < c->b_rp[i + 1]; ++k)
-          require(c->b_ci[k] >= 0 && c->b_ci[k] < n && (k == c->b_rp[i] || c->b_ci[k] > c->b_ci[k - 1]),
-                  "zolo_pencil_upload: B column indices must be in range and sorted");
+      if (c->a_rp[i] > c->a_rp[i + 1]) require(false, "zolo_pencil_upload: A offsets not monotone");
+      if (!sorted_in_range(c->a_rp, c->a_ci, i))
+        require(false, "zolo_pencil_upload: A column indices must be in range and sorted");
+      if (!c->b_identity && !sorted_in_range(c->b_rp, c->b_ci, i))
+        require(false, "zolo_pencil_upload: B column indices must be in range and sorted");
     }
     c->have_pencil = true;
     c->have_perm = false;
