@@ -344,7 +344,7 @@ struct zolo_ctx {
   int sp_npads = 0;
   bool sym_ready = false;
   FactorPlan fplan;                         // level-scheduled factorization (host level ranges)
-  DevMem fp_cols, fp_pan, fp_tgt, fp_con;   // its device arrays
+  DevMem fp_cols, fp_pan, fp_tgt, fp_con, fp_cmb, fp_scratch;  // its device arrays; partial products of split targets
   DagSched sched_fwd, sched_bwd;
   int sp_nslots = 0;
   int swc = 32;  // sweep task width (columns): 64 for blocks of >= 128 columns (ensure_workspace)
@@ -851,6 +851,7 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   upload(c.fp_pan, c.fplan.pan, c.st);
   upload(c.fp_tgt, c.fplan.tgt, c.st);
   upload(c.fp_con, c.fplan.con, c.st);
+  upload(c.fp_cmb, c.fplan.cmb, c.st);
   clk.mark("plan upload");
   c.sym_ready = true;
 }
@@ -924,6 +925,10 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   pd.lvl_ptr = &c.fplan.lvl_ptr;
   pd.pan_ptr = &c.fplan.pan_ptr;
   pd.tgt_ptr = &c.fplan.tgt_ptr;
+  pd.cmb_ptr = &c.fplan.cmb_ptr;
+  pd.cmb = c.fp_cmb.as<int>();
+  const size_t scratch_per_pole = static_cast<size_t>(std::max<int64_t>(c.fplan.scratch_slots, 1)) * TT;
+  c.fp_scratch.ensure(sizeof(cd) * scratch_per_pole * r);
   pd.cols = c.fp_cols.as<int>();
   pd.pan = c.fp_pan.as<int>();
   pd.tgt = c.fp_tgt.as<int>();
@@ -941,6 +946,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     FactorDevState ds;
     ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
     ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;
+    pd.scratch = c.fp_scratch.as<cd>() + scratch_per_pole * j;
     sp_factor(c.pole_streams[j], c.sgeom, f, c.sp_nnz, c.sp_er.as<int>(), c.sp_ec.as<int>(), c.sp_ea.as<double>(),
               c.sp_eb.as<double>(), c.cx, sig[j].real(), sig[j].imag(), c.rownorm_mem.as<double>() + c.sgeom.npad * j,
               c.sp_pad_rows.as<int>(), c.sp_npads, ds, c.sp_err.as<int>(), pd);

@@ -239,7 +239,7 @@ constexpr int TRAIL_SMEM = 2 * TRAIL_STAGE * static_cast<int>(sizeof(cd));
 #define ZOLO_TRAIL_MINB 3
 #endif
 __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(const int* tgt, const int* con, int t0, cd* Dt,
-                                                               cd* Lt, cd* Ut) {
+                                                               cd* Lt, cd* Ut, cd* scratch) {
   extern __shared__ __align__(16) unsigned char trail_smem[];
   cd* sm = reinterpret_cast<cd*>(trail_smem);
   const int* T = tgt + 2 * (t0 + blockIdx.x);  // packed: kind << 30 | tile id, first contribution; end = the next target's first
@@ -268,11 +268,35 @@ __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(con
   }
   cd prod[4];
   acc3_fold(acc, prod);
+  if (kind == 3) {  // one part of a split target: its product goes to the level's scratch slot
+    cd* c = scratch + static_cast<size_t>(id) * TT;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[ocol(f, q) * TILE + f.row] = prod[q];
+    return;
+  }
   cd* c = (kind == 0 ? Dt : (kind == 1 ? Lt : Ut)) + static_cast<size_t>(id) * TT;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int e = ocol(f, q) * TILE + f.row;
     c[e] = csub(c[e], prod[q]);
+  }
+}
+
+// Split targets: tile -= part 0 + part 1 + ... (part order: the fixed summation order).
+__global__ void __launch_bounds__(ST) combine_parts_kernel(const int* cmb, int m0, cd* Dt, cd* Lt, cd* Ut,
+                                                           const cd* scratch) {
+  const int* M = cmb + 3 * (m0 + blockIdx.x);
+  const int kind = static_cast<unsigned>(M[0]) >> 30, id = M[0] & 0x3fffffff, s0 = M[1], np = M[2];
+  cd* c = (kind == 0 ? Dt : (kind == 1 ? Lt : Ut)) + static_cast<size_t>(id) * TT;
+#pragma unroll
+  for (int q = 0; q < TT / ST; ++q) {
+    const int e = threadIdx.x + q * ST;
+    cd sum = scratch[static_cast<size_t>(s0) * TT + e];
+    for (int p = 1; p < np; ++p) {
+      const cd v = scratch[static_cast<size_t>(s0 + p) * TT + e];
+      sum = mk(sum.x + v.x, sum.y + v.y);
+    }
+    c[e] = csub(c[e], sum);
   }
 }
 
@@ -310,9 +334,13 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const SpFactor& f, int64_t nnz,
   const std::vector<int>& lv = *plan.lvl_ptr;
   const std::vector<int>& pp = *plan.pan_ptr;
   const std::vector<int>& tp = *plan.tgt_ptr;
+  const std::vector<int>& cp = *plan.cmb_ptr;
   for (size_t l = 0; l + 1 < lv.size(); ++l) {
     if (tp[l + 1] > tp[l])
-      trailing_level_kernel<<<tp[l + 1] - tp[l], ST, TRAIL_SMEM, st>>>(plan.tgt, plan.con, tp[l], f.Dt, f.Lt, f.Ut);
+      trailing_level_kernel<<<tp[l + 1] - tp[l], ST, TRAIL_SMEM, st>>>(plan.tgt, plan.con, tp[l], f.Dt, f.Lt, f.Ut,
+                                                                        plan.scratch);
+    if (cp[l + 1] > cp[l])
+      combine_parts_kernel<<<cp[l + 1] - cp[l], ST, 0, st>>>(plan.cmb, cp[l], f.Dt, f.Lt, f.Ut, plan.scratch);
     if (lv[l + 1] > lv[l])
       diag_level_kernel<<<lv[l + 1] - lv[l], FT, diag_smem, st>>>(plan.cols, lv[l], s.npad, f.Dt, f.DinvL, f.DinvU,
                                                                    row_norm, ds.fail_index, ds.min_ratio_bits);

@@ -33,7 +33,11 @@ void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::
 //   tgt: 2 ints per target (kind 0 = Dt / 1 = Lt / 2 = Ut in bits 30-31 | tile id, first
 //        contribution); a target's contributions end where the next target's begin (the lists are
 //        laid out in target order; one sentinel entry closes the last)
+//        kind 3 = one part of a split target: the id is a scratch slot of the level, the part's
+//        product is stored there
 //   con: 2 ints per contribution (L tile id, U tile id)
+//   cmb: 3 ints per split target (kind | tile id, first scratch slot, parts): tile -= the parts,
+//        in part order
 // std::vector whose resize leaves new elements uninitialised: the plan's large arrays are sized
 // once and filled by the worker threads (which also take their first-touch page faults)
 template <class T>
@@ -52,8 +56,9 @@ struct NoInit : std::allocator<T> {
 };
 using RawInts = std::vector<int, NoInit<int>>;
 struct FactorPlan {
-  std::vector<int> lvl_ptr, cols, pan_ptr, pan, tgt_ptr;
-  RawInts tgt, con;
+  std::vector<int> lvl_ptr, cols, pan_ptr, pan, tgt_ptr, cmb_ptr;
+  RawInts tgt, con, cmb;
+  int64_t scratch_slots = 0;  // partial-product tiles of the widest level (split targets)
   int64_t contributions = 0;
 };
 void factor_plan(const BlockStructure& bs, FactorPlan& plan);

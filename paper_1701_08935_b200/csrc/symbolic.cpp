@@ -473,8 +473,17 @@ void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
       if (m) emit(1, static_cast<int>(bs.col_tile[e]), m);
     }
   };
+  // Long lists are split: a target with more than SPLIT_MIN contributions becomes up to MAXP part
+  // records (kind 3) that each write their partial product into a scratch slot of the level, and
+  // one combine entry subtracts the parts from the tile in part order (fixed summation order). The
+  // top of the tree has few targets with lists of hundreds of products: splitting fills the GPU
+  // there and shortens each level's critical path.
+  auto part_size = [](int m) {
+    constexpr int SPLIT_MIN = 48, PART = 32, MAXP = 16;
+    return m <= SPLIT_MIN ? std::max(m, 1) : std::max(PART, (m + MAXP - 1) / MAXP);
+  };
   struct Cnt {
-    int64_t nt = 0, nc = 0;
+    int64_t nt = 0, nc = 0, ns = 0, nm = 0;  // records, contributions, scratch slots, combine entries
   };
   std::vector<Cnt> cnt(nb);
   const int nthr = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
@@ -494,41 +503,66 @@ void factor_plan(const BlockStructure& bs, FactorPlan& plan) {
     Cnt c;
     column_targets(y, buf, [&](int kind, int, int m) {
       const int both = kind ? 2 : 1;
-      c.nt += both;
+      const int sz = part_size(m);
+      const int np = (m + sz - 1) / sz;
+      c.nt += both * np;
       c.nc += both * m;
+      if (np > 1) c.ns += both * np, c.nm += both;
     });
     cnt[y] = c;
   });
-  // offsets in level order, columns in plan.cols order
+  // offsets in level order, columns in plan.cols order; scratch slots restart at every level
   plan.tgt_ptr.assign(1, 0);
-  int64_t ntgt = 0, ncon = 0;
+  plan.cmb_ptr.assign(1, 0);
+  int64_t ntgt = 0, ncon = 0, ncmb = 0;
+  plan.scratch_slots = 0;
   for (int l = 0; l < nlev; ++l) {
+    int64_t slots = 0;
     for (int y : by[l]) {
       const Cnt c = cnt[y];
-      cnt[y] = {ntgt, ncon};
+      cnt[y] = {ntgt, ncon, slots, ncmb};
       ntgt += c.nt;
       ncon += c.nc;
+      slots += c.ns;
+      ncmb += c.nm;
     }
+    plan.scratch_slots = std::max(plan.scratch_slots, slots);
     plan.tgt_ptr.push_back(static_cast<int>(ntgt));
+    plan.cmb_ptr.push_back(static_cast<int>(ncmb));
   }
   if (ncon >= (int64_t(1) << 31)) throw std::runtime_error("factor_plan: too many updates");
+  if (plan.scratch_slots >= (int64_t(1) << 30)) throw std::runtime_error("factor_plan: too many partial products");
   plan.tgt.resize(2 * ntgt + 2);
   plan.con.resize(2 * ncon);
+  plan.cmb.resize(3 * ncmb);
   plan.tgt[2 * ntgt] = 0;
   plan.tgt[2 * ntgt + 1] = static_cast<int>(ncon);  // sentinel: the last target's end
   run([&](int64_t y, std::vector<Con>& buf) {
-    int64_t t = cnt[y].nt, c = cnt[y].nc;
-    column_targets(y, buf, [&](int kind, int id, int m) {
-      plan.tgt[2 * t] = static_cast<int>(static_cast<unsigned>(kind) << 30 | static_cast<unsigned>(id));
-      plan.tgt[2 * t + 1] = static_cast<int>(c);
-      for (int i = 0; i < m; ++i, ++c) plan.con[2 * c] = buf[i].la, plan.con[2 * c + 1] = buf[i].ub;
-      ++t;
-      if (kind) {  // the U target: same k, ids swapped
-        plan.tgt[2 * t] = static_cast<int>(2u << 30 | static_cast<unsigned>(id));
-        plan.tgt[2 * t + 1] = static_cast<int>(c);
-        for (int i = 0; i < m; ++i, ++c) plan.con[2 * c] = buf[i].ub, plan.con[2 * c + 1] = buf[i].la;
-        ++t;
+    int64_t t = cnt[y].nt, c = cnt[y].nc, sl = cnt[y].ns, cm = cnt[y].nm;
+    // one target (kind, tile id) with the m contributions of buf, ids swapped for the U target
+    auto write = [&](int kind, int id, int m, bool swap) {
+      const int sz = part_size(m);
+      const int np = (m + sz - 1) / sz;
+      if (np > 1) {
+        plan.cmb[3 * cm] = static_cast<int>(static_cast<unsigned>(kind) << 30 | static_cast<unsigned>(id));
+        plan.cmb[3 * cm + 1] = static_cast<int>(sl);
+        plan.cmb[3 * cm + 2] = np;
+        ++cm;
       }
+      for (int p = 0; p < np; ++p) {
+        plan.tgt[2 * t] = np > 1 ? static_cast<int>(3u << 30 | static_cast<unsigned>(sl++))
+                                 : static_cast<int>(static_cast<unsigned>(kind) << 30 | static_cast<unsigned>(id));
+        plan.tgt[2 * t + 1] = static_cast<int>(c);
+        ++t;
+        for (int i = p * sz; i < std::min(m, (p + 1) * sz); ++i, ++c) {
+          plan.con[2 * c] = swap ? buf[i].ub : buf[i].la;
+          plan.con[2 * c + 1] = swap ? buf[i].la : buf[i].ub;
+        }
+      }
+    };
+    column_targets(y, buf, [&](int kind, int id, int m) {
+      write(kind, id, m, false);
+      if (kind) write(2, id, m, true);  // the U target: same k, ids swapped
     });
   });
   plan.contributions = ncon;

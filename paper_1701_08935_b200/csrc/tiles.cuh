@@ -106,10 +106,13 @@ struct FactorPlanDev {
   const std::vector<int>* lvl_ptr = nullptr;
   const std::vector<int>* pan_ptr = nullptr;
   const std::vector<int>* tgt_ptr = nullptr;
+  const std::vector<int>* cmb_ptr = nullptr;
   const int* cols = nullptr;
   const int* pan = nullptr;
   const int* tgt = nullptr;
   const int* con = nullptr;
+  const int* cmb = nullptr;
+  cd* scratch = nullptr;  // this pole's partial products of split targets (plan.scratch_slots tiles)
 };
 // scatter of A - sigma B (assemble_shifted, sparse.hpp:153-186) into the tiles, then the
 // level-scheduled LU (3 launches per level of the block elimination tree) and the row scaling

@@ -57,5 +57,6 @@ int main(int argc, char** argv) {
               static_cast<long long>(bs.nb), static_cast<long long>(bs.ntiles), plan.lvl_ptr.size() - 1, ms(t0, t1),
               ms(t1, t2), ms(t2, t3), static_cast<long long>(plan.contributions), static_cast<long long>(single),
               static_cast<long long>(multi), plan.tgt.size() / 2 - 1);
+  std::printf("split targets %zu, scratch slots %lld\n", plan.cmb.size() / 3, static_cast<long long>(plan.scratch_slots));
   return 0;
 }
