@@ -167,6 +167,11 @@ __device__ __forceinline__ unsigned long long l2_policy(int code) {
   return code == 0 ? l2_evict_first() : (code == 1 ? l2_evict_normal() : l2_evict_last());
 }
 
+// (development) timing probe: the tensor copies fetch 1 / ZOLO_PROBE_XDIV of every x block's rows
+// (results wrong by construction): how much of a sweep is the L2 -> SM traffic of the x blocks
+#ifndef ZOLO_PROBE_XDIV
+#define ZOLO_PROBE_XDIV 1
+#endif
 struct Meta2 {
   int kind;  // 0 MMA(tile, x, neg = sign), 1 ADD(x block * sign), 2 END
   int sign;
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
       mbar_wait(empty + s, (round & 1) ^ 1);
       if (lane == 0) {
         const unsigned bytes = (tile ? static_cast<unsigned>(TT * sizeof(cd)) : 0u) +
-                               (kind != 2 ? static_cast<unsigned>(XSW * sizeof(cd)) : 0u);
+                               (kind != 2 ? static_cast<unsigned>(XSW * sizeof(cd)) / ZOLO_PROBE_XDIV : 0u);
         mbar_expect_tx(full + s, bytes);
         if (tile) bulk_copy(tile_s(s), tile, TT * sizeof(cd), full + s, pol_tile);
         if (kind != 2) tma_xblock(x_s(s), xmap, rb, c0, full + s, pol);
@@ -576,7 +581,7 @@ bool encode_xblock_map(void* map, const cd* base, int64_t ld, int64_t ncols, int
   // the box lands as [row group][column][8 rows] (mma.cuh xsw)
   const cuuint64_t dims[3] = {16, static_cast<cuuint64_t>(ncols), static_cast<cuuint64_t>(ld / 8)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * sizeof(cd), 128};
-  const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(swc), TILE / 8};
+  const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(swc), TILE / 8 / ZOLO_PROBE_XDIV};
   const cuuint32_t estr[3] = {1, 1, 1};
   return encode(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<cd*>(base), dims,
                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
