@@ -1230,11 +1230,16 @@ void sweep_sparse(zolo_ctx& c, int first, int nsub, int na, unsigned long long* 
   const int g2 = dag_trsm_launch(c.st, c.sgeom, c.sched_bwd, cbw, nsub, na, c.swc, ld, ldp, fc, cf, ++c.epoch,
                                  c.counter.as<int>(), c.num_sms, nullptr, c.act_d.as<int>(), c.lag_done);
   if (g1 < 0 || g2 < 0) throw ZoloError(ZOLO_ERR_DOMAIN, "triangular solve: more than 32 chains in one launch");
-  if (c.cx)
+  if (c.cx) {  // the adjoint chains' post-pass x_i = DinvL_i^H w_i, one launch
+    std::vector<const cd*> dv;
+    std::vector<cd*> xv;
     for (int ci = first; ci < first + nsub; ++ci)
-      if (ci & 1)
-        blockdiag_apply(c.st, c.geom.nbk, c.tiles[ci / 2].DinvL, true,
-                        (refinement ? c.rbuf[ci] : c.xbuf[ci])->as<cd>(), na, ld);
+      if (ci & 1) {
+        dv.push_back(c.tiles[ci / 2].DinvL);
+        xv.push_back((refinement ? c.rbuf[ci] : c.xbuf[ci])->as<cd>());
+      }
+    blockdiag_apply(c.st, c.geom.nbk, dv.data(), xv.data(), static_cast<int>(dv.size()), true, na, ld);
+  }
 }
 
 // Residual-correction refinement of every chain's solution (zolo_set_refinement):

@@ -155,6 +155,7 @@ int dag_groups(int ncols, int swc);
 
 // x[:, 0:ncols] <- op(D_i) x for every block row (the adjoint post-pass
 // x_i = DinvL_i^H w_i); x is ld x ncols, D is nbk tiles.
-void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld);
+void blockdiag_apply(cudaStream_t st, int nb, const cd* const* D, cd* const* x, int nchains, bool opH, int ncols,
+                     int64_t ld);
 
 }  // namespace zolo

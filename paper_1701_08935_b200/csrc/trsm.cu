@@ -535,30 +535,49 @@ __global__ void __launch_bounds__(P2T, Shape<W>::MINB) dag2_kernel(DagArgs A) {
   }
 }
 
-// x_i <- op(D_i) x_i per (block row, 16-column group): the adjoint post-pass.
-__global__ void __launch_bounds__(ST) blockdiag_kernel(const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
+// x_i <- op(D_i) x_i, the adjoint post-pass: one CTA per (block row, chain) keeps the diagonal
+// tile in shared memory and walks the block's 16-column groups with a two-stage cp.async ring
+// (one launch for all adjoint chains; per-group CTAs re-read the tile for every group: 307 us per
+// chain at config 3).
+struct BdArgs {
+  const cd* D[DAG2_CHAINS];
+  cd* x[DAG2_CHAINS];
+};
+__global__ void __launch_bounds__(ST) blockdiag_kernel(BdArgs A, bool opH, int ncols, int64_t ld) {
   __shared__ __align__(16) cd ds[TILE_S];
-  __shared__ __align__(16) cd xs[XS];
-  const int i = blockIdx.x, c0 = blockIdx.y * CG, nc = min(CG, ncols - c0);
+  __shared__ __align__(16) cd xs[2][XS];
+  const int i = blockIdx.x;
+  cd* x = A.x[blockIdx.y];
   const Frag f = frag();
   {  // undo the sweep layout (tiles are stored swizzled) into the padded column-major copy
-    const cd* g = D + static_cast<size_t>(i) * TT;
+    const cd* g = A.D[blockIdx.y] + static_cast<size_t>(i) * TT;
 #pragma unroll
     for (int q = 0; q < TT / ST; ++q) {
       const int e = threadIdx.x + q * ST, col = e / TILE, row = e % TILE;
       cp_async16_cg(&ds[col * APAD + row], g + col * TILE + (row ^ swz(col)));
     }
   }
-  load_x(xs, x + static_cast<int64_t>(i) * TILE, ld, c0, nc);
+  const int ngroups = (ncols + CG - 1) / CG;
+  load_x(xs[0], x + static_cast<int64_t>(i) * TILE, ld, 0, min(CG, ncols));
   cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  cd out[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
-  mma_tile(out, ds, xs, opH, f);
-  cd* row = x + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
+  for (int g = 0; g < ngroups; ++g) {
+    const int c0 = g * CG, nc = min(CG, ncols - c0);
+    if (g + 1 < ngroups) {
+      load_x(xs[(g + 1) & 1], x + static_cast<int64_t>(i) * TILE, ld, c0 + CG, min(CG, ncols - c0 - CG));
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    cd out[2] = {mk(0.0, 0.0), mk(0.0, 0.0)};
+    mma_tile(out, ds, xs[g & 1], opH, f);
+    cd* row = x + static_cast<int64_t>(i) * TILE + f.row + c0 * ld;
 #pragma unroll
-  for (int q = 0; q < 2; ++q)
-    if (f.col + q < nc) row[(f.col + q) * ld] = out[q];
+    for (int q = 0; q < 2; ++q)
+      if (f.col + q < nc) row[(f.col + q) * ld] = out[q];
+    __syncthreads();  // the stage is refilled two groups later
+  }
 }
 
 }  // namespace
@@ -588,8 +607,14 @@ bool encode_xblock_map(void* map, const cd* base, int64_t ld, int64_t ncols, int
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void blockdiag_apply(cudaStream_t st, int nb, const cd* D, bool opH, cd* x, int ncols, int64_t ld) {
-  if (ncols > 0) blockdiag_kernel<<<dim3(nb, (ncols + CG - 1) / CG), ST, 0, st>>>(D, opH, x, ncols, ld);
+void blockdiag_apply(cudaStream_t st, int nb, const cd* const* D, cd* const* x, int nchains, bool opH, int ncols,
+                     int64_t ld) {
+  for (int c0 = 0; c0 < nchains && ncols > 0; c0 += DAG2_CHAINS) {
+    BdArgs a;
+    const int nc = std::min(DAG2_CHAINS, nchains - c0);
+    for (int q = 0; q < nc; ++q) a.D[q] = D[c0 + q], a.x[q] = x[c0 + q];
+    blockdiag_kernel<<<dim3(nb, nc), ST, 0, st>>>(a, opH, ncols, ld);
+  }
 }
 
 int dag_groups(int ncols, int swc) { return (ncols + swc - 1) / swc; }
