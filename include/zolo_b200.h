@@ -322,6 +322,14 @@ int zolo_timer(zolo_ctx* ctx, int op, double* ms);
  * node groups, out[6] trailing-update tile products of the factorization (sum over
  * block columns of the squared column count), out[7] reserved. */
 int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* out);
+/* Builds the left-looking factor plan of the ND factor of a pattern (symbolic.cpp factor_plan)
+ * and checks it on the host (no reference equivalent; test support): out[0] = violations (0 when
+ * every tile is completed by exactly one target at the level of its block column, every
+ * contribution is a pair L(a,k), U(k,b) of that target with k below it on a lower level, in
+ * ascending k also across the parts of split targets, every part is read by one combine entry,
+ * and the contributions number sum_k |col(k)|^2), out[1] contributions, out[2] target records,
+ * out[3] split targets, out[4] scratch tiles of the widest level, out[5] levels. */
+int zolo_factor_plan_check(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* out);
 /* Builds the DAG sweep schedules (both directions) of the ND factor of a pattern and checks them
  * on the host (no reference equivalent; test support): out[0] = violations (0 when every block
  * row has one row task, every dependency is summed exactly once, every partial slot is written

@@ -2623,6 +2623,115 @@ int zolo_nd_structure(int64_t n, const int64_t* rp, const int64_t* ci, int64_t l
   }
 }
 
+int zolo_factor_plan_check(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int64_t* out) {
+  try {
+    std::vector<std::vector<int64_t>> nodes;
+    nd_order(n, rp, ci, leaf, nodes);
+    BlockStructure bs;
+    block_symbolic(n, rp, ci, nodes, TILE, bs);
+    FactorPlan plan;
+    factor_plan(bs, plan);
+    const int64_t nb = bs.nb, ntiles = bs.ntiles;
+    std::vector<int> tile_row(ntiles), level(nb, -1);
+    for (int64_t i = 0; i < nb; ++i)
+      for (int64_t e = bs.row_ptr[i]; e < bs.row_ptr[i + 1]; ++e) tile_row[e] = static_cast<int>(i);
+    const int nlev = static_cast<int>(plan.lvl_ptr.size()) - 1;
+    for (int l = 0; l < nlev; ++l)
+      for (int q = plan.lvl_ptr[l]; q < plan.lvl_ptr[l + 1]; ++q) level[plan.cols[q]] = l;
+    int64_t bad = 0, expect = 0, split = 0;
+    for (int64_t k = 0; k < nb; ++k) {
+      const int64_t ck = bs.col_ptr[k + 1] - bs.col_ptr[k];
+      expect += ck * ck;  // D: ck, L and U: ck (ck - 1) / 2 each
+      if (level[k] < 0) ++bad;  // every block column has a level
+    }
+    // a contribution list [c0, c1) of target (kind, tile or diagonal id): every entry is
+    // (L(a, k), U(k, b)) of the target's (a, b) with one k below, a descendant level, ascending
+    // k continuing from `last_k`
+    auto check_list = [&](int kind, int id, int c0, int c1, int lvl, int& last_k) {
+      const int a = kind == 0 ? id : (kind == 1 ? tile_row[id] : static_cast<int>(bs.row_idx[id]));
+      const int b = kind == 0 ? id : (kind == 1 ? static_cast<int>(bs.row_idx[id]) : tile_row[id]);
+      const int y = std::min(a, b);  // the block column (row of U) the target belongs to
+      if (level[y] != lvl) ++bad;
+      for (int q = c0; q < c1; ++q) {
+        const int la = plan.con[2 * q], ub = plan.con[2 * q + 1];
+        if (la < 0 || la >= ntiles || ub < 0 || ub >= ntiles) {
+          ++bad;
+          continue;
+        }
+        const int k = static_cast<int>(bs.row_idx[la]);
+        if (tile_row[la] != a || tile_row[ub] != b || bs.row_idx[ub] != k || k >= y || k <= last_k ||
+            level[k] >= lvl)
+          ++bad;
+        last_k = k;
+      }
+    };
+    std::vector<char> seen(3 * std::max<int64_t>(ntiles, nb) + 3, 0);
+    auto mark_target = [&](int kind, int id) {
+      const int64_t lim = kind == 0 ? nb : ntiles;
+      if (id < 0 || id >= lim) {
+        ++bad;
+        return false;
+      }
+      char& s = seen[3 * static_cast<int64_t>(id) + kind];
+      if (s) ++bad;  // every tile is completed by one target
+      s = 1;
+      return true;
+    };
+    for (int l = 0; l < nlev; ++l) {
+      // part records of the level by scratch slot
+      std::vector<std::pair<int, int>> part(static_cast<size_t>(plan.scratch_slots), {-1, -1});
+      for (int t = plan.tgt_ptr[l]; t < plan.tgt_ptr[l + 1]; ++t) {
+        const int kind = static_cast<unsigned>(plan.tgt[2 * t]) >> 30, id = plan.tgt[2 * t] & 0x3fffffff;
+        const int c0 = plan.tgt[2 * t + 1], c1 = plan.tgt[2 * t + 3];
+        if (c0 > c1 || c1 > plan.contributions) {
+          ++bad;
+          continue;
+        }
+        if (kind == 3) {
+          if (id >= plan.scratch_slots || part[id].first >= 0)
+            ++bad;
+          else
+            part[id] = {c0, c1};
+        } else if (mark_target(kind, id)) {
+          int last_k = -1;
+          check_list(kind, id, c0, c1, l, last_k);
+        }
+      }
+      for (int m = plan.cmb_ptr[l]; m < plan.cmb_ptr[l + 1]; ++m) {
+        const int kind = static_cast<unsigned>(plan.cmb[3 * m]) >> 30, id = plan.cmb[3 * m] & 0x3fffffff;
+        const int s0 = plan.cmb[3 * m + 1], np = plan.cmb[3 * m + 2];
+        ++split;
+        if (kind > 2 || np < 2 || s0 < 0 || s0 + np > plan.scratch_slots || !mark_target(kind, id)) {
+          ++bad;
+          continue;
+        }
+        int last_k = -1;
+        for (int p = 0; p < np; ++p) {  // the parts continue one ascending list
+          if (part[s0 + p].first < 0) {
+            ++bad;
+            continue;
+          }
+          check_list(kind, id, part[s0 + p].first, part[s0 + p].second, l, last_k);
+          part[s0 + p] = {-2, -2};
+        }
+      }
+      for (const auto& pr : part)
+        if (pr.first >= 0) ++bad;  // a part no combine entry reads
+    }
+    if (plan.contributions != expect) ++bad;
+    out[0] = bad;
+    out[1] = plan.contributions;
+    out[2] = plan.tgt_ptr.empty() ? 0 : plan.tgt_ptr.back();
+    out[3] = split;
+    out[4] = plan.scratch_slots;
+    out[5] = nlev;
+    return ZOLO_OK;
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return ZOLO_ERR_DOMAIN;
+  }
+}
+
 int zolo_dag_schedule_check(int64_t n, const int64_t* rp, const int64_t* ci, int64_t leaf, int near, int chunk,
                             int order, int64_t* out) {
   try {

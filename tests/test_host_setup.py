@@ -218,6 +218,53 @@ def test_dag_schedules_are_complete_and_topological(name, near, chunk, order):
     assert out[1] >= 2 * out[3]  # at least one row task per block row and direction
 
 
+@pytest.mark.parametrize("name", ["grid2d", "grid3d", "torus3d", "random"])
+def test_factor_plan_is_complete_and_ordered(name):
+    """The left-looking factor plan (symbolic.cpp factor_plan) of the ND factor: every tile is
+    completed by exactly one target at its block column's level, with all its contributions
+    (L(a,k), U(k,b)), k ascending and on lower levels -- the fixed summation order behind the
+    deterministic factors -- also across the parts of split targets, each part read by one combine
+    entry; the contributions number sum_k |col(k)|^2 (checked in C++ on the host). torus3d is large
+    enough for lists of more than 48 contributions, i.e. split targets."""
+    import ctypes as C
+
+    import scipy.sparse as sp
+
+    import paper_1701_08935_b200 as zb
+
+    if name == "grid2d":
+        k = 60
+        t = sp.diags([1.0, 1.0, 1.0], [-1, 0, 1], shape=(k, k))
+        m = sp.kron(t, sp.identity(k)) + sp.kron(sp.identity(k), t)
+    elif name == "grid3d":
+        k = 14
+        t = sp.diags([1.0, 1.0, 1.0], [-1, 0, 1], shape=(k, k))
+        i = sp.identity(k)
+        m = sp.kron(sp.kron(t, i), i) + sp.kron(sp.kron(i, t), i) + sp.kron(sp.kron(i, i), t)
+    elif name == "torus3d":
+        k = 26
+        t = sp.diags([1.0, 1.0, 1.0], [-1, 0, 1], shape=(k, k)).tolil()
+        t[0, k - 1] = t[k - 1, 0] = 1.0
+        i = sp.identity(k)
+        m = sp.kron(sp.kron(t, i), i) + sp.kron(sp.kron(i, t), i) + sp.kron(sp.kron(i, i), t)
+    else:
+        rng = np.random.default_rng(11)
+        n = 2500
+        r = sp.random(n, n, density=0.003, random_state=rng)
+        m = r + r.T + sp.identity(n)
+    m = sp.csr_matrix(m)
+    m.sort_indices()
+    rp, ci = m.indptr.astype(np.int64), m.indices.astype(np.int64)
+    out = np.zeros(8, dtype=np.int64)
+    L = zb.lib()
+    L.zolo_factor_plan_check.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    assert L.zolo_factor_plan_check(m.shape[0], rp.ctypes.data, ci.ctypes.data, 64, out.ctypes.data) == 0
+    assert out[0] == 0, f"{out[0]} plan violations"
+    assert out[1] > 0 and out[2] > 0
+    if name == "torus3d":
+        assert out[3] > 0 and out[4] > 0, "the torus should split some targets"
+
+
 def test_uniform_stream_matches_reference_mt19937_64():
     """The product's seeded stream (zolo_uniform_stream, host.cpp) equals the reference's
     std::mt19937_64 raw-bit convention (hamiltonian.hpp:50-53) drawn through oracle/_ref
