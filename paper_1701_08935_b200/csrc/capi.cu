@@ -344,6 +344,7 @@ struct zolo_ctx {
   int sp_npads = 0;
   bool sym_ready = false;
   FactorPlan fplan;                         // level-scheduled factorization (host level ranges)
+  DevMem fp_lmask;  // per pole and L tile: occupancy mask written by the panel step (SpFactor::lmask)
   DevMem fp_cols, fp_pan, fp_tgt, fp_con, fp_cmb, fp_scratch;  // its device arrays; partial products of split targets
   DagSched sched_fwd, sched_bwd;
   int sp_nslots = 0;
@@ -929,6 +930,9 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
   pd.cmb = c.fp_cmb.as<int>();
   const size_t scratch_per_pole = static_cast<size_t>(std::max<int64_t>(c.fplan.scratch_slots, 1)) * TT;
   c.fp_scratch.ensure(sizeof(cd) * scratch_per_pole * r);
+  const size_t lmask_per_pole = static_cast<size_t>(std::max<int64_t>(ntiles, 1));
+  c.fp_lmask.ensure(sizeof(unsigned) * lmask_per_pole * r);
+  CK(cudaMemsetAsync(c.fp_lmask.p, 0xff, sizeof(unsigned) * lmask_per_pole * r, c.st));
   pd.cols = c.fp_cols.as<int>();
   pd.pan = c.fp_pan.as<int>();
   pd.tgt = c.fp_tgt.as<int>();
@@ -943,6 +947,7 @@ void sparse_numeric(zolo_ctx& c, const std::vector<std::complex<double>>& sig, D
     f.Ut = tiles[j].Ut;
     f.DinvL = tiles[j].DinvL;
     f.DinvU = tiles[j].DinvU;
+    f.lmask = c.fp_lmask.as<unsigned>() + lmask_per_pole * j;
     FactorDevState ds;
     ds.fail_index = reinterpret_cast<int*>(c.fstate_mem.as<unsigned long long>() + 2 * j);
     ds.min_ratio_bits = c.fstate_mem.as<unsigned long long>() + 2 * j + 1;

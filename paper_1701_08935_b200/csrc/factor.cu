@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(FT) diag_level_kernel(const int* cols, int c0,
 
 // C = A B of three column-major tiles on DMMA (3M), one CTA of ST threads; C may alias A or B
 // (both are staged in shared memory before C is written)
-__device__ __forceinline__ void tile_mm_dmma(const cd* Ag, const cd* Bg, cd* Cg) {
+__device__ __forceinline__ void tile_mm_dmma(const cd* Ag, const cd* Bg, cd* Cg, cd prod[4], const Frag& f) {
   __shared__ __align__(16) cd sa[TT];
   __shared__ __align__(16) cd sb[XS2];
   load_tile_sw(sa, Ag, l2_evict_normal());
@@ -204,27 +204,43 @@ __device__ __forceinline__ void tile_mm_dmma(const cd* Ag, const cd* Bg, cd* Cg)
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  const Frag f = frag();
   Acc3<2> acc;
   acc3_zero(acc);
-  mma_tile3_nx(acc, sa, sb, f);
-  cd prod[4];
+  mma_tile3_nx(acc, sa, sb, f, 0xffu);
   acc3_fold(acc, prod);
 #pragma unroll
   for (int q = 0; q < 4; ++q) Cg[ocol(f, q) * TILE + f.row] = prod[q];
 }
+__device__ __forceinline__ void tile_mm_dmma(const cd* Ag, const cd* Bg, cd* Cg) {
+  cd prod[4];
+  tile_mm_dmma(Ag, Bg, Cg, prod, frag());
+}
 
 // panel items (k, 2 id + upper): L(a,k) = A(a,k) U_kk^{-1} | U(k,a) = L_kk^{-1} A(k,a)
+// The finished L tile's occupancy mask (SpFactor::lmask) is taken from the product's registers.
 __global__ void __launch_bounds__(ST) panel_level_kernel(const int* pan, int p0, cd* Lt, cd* Ut, const cd* DinvL,
-                                                         const cd* DinvU) {
+                                                         const cd* DinvU, unsigned* lmask) {
+  __shared__ unsigned mask;
   const int k = pan[2 * (p0 + blockIdx.x)], code = pan[2 * (p0 + blockIdx.x) + 1];
   const bool lower = (code & 1) == 0;
   const int id = code >> 1;
   cd* c = (lower ? Lt : Ut) + static_cast<size_t>(id) * TT;
-  if (lower)
-    tile_mm_dmma(c, DinvU + static_cast<size_t>(k) * TT, c);
-  else
+  if (!lower) {
     tile_mm_dmma(DinvL + static_cast<size_t>(k) * TT, c, c);
+    return;
+  }
+  if (threadIdx.x == 0) mask = 0u;
+  const Frag f = frag();
+  cd prod[4];
+  tile_mm_dmma(c, DinvU + static_cast<size_t>(k) * TT, c, prod, f);  // (syncs the CTA after `mask = 0`)
+  unsigned bits = 0u;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (prod[q].x != 0.0 || prod[q].y != 0.0) bits |= 1u << ((f.row >> 3) * 8 + (ocol(f, q) >> 2));
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(&mask, bits);
+  __syncthreads();
+  if (threadIdx.x == 0) lmask[id] = mask;
 }
 
 // One trailing-update target per CTA (left-looking: the tile's whole update, written once):
@@ -239,7 +255,8 @@ constexpr int TRAIL_SMEM = 2 * TRAIL_STAGE * static_cast<int>(sizeof(cd));
 #define ZOLO_TRAIL_MINB 3
 #endif
 __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(const int* tgt, const int* con, int t0, cd* Dt,
-                                                               cd* Lt, cd* Ut, cd* scratch) {
+                                                               cd* Lt, cd* Ut, cd* scratch,
+                                                               const unsigned* __restrict__ lmask) {
   extern __shared__ __align__(16) unsigned char trail_smem[];
   cd* sm = reinterpret_cast<cd*>(trail_smem);
   const int* T = tgt + 2 * (t0 + blockIdx.x);  // packed: kind << 30 | tile id, first contribution; end = the next target's first
@@ -247,9 +264,16 @@ __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(con
   const Frag f = frag();
   Acc3<2> acc;
   acc3_zero(acc);
+  unsigned km0 = 0u, km1 = 0u;  // this warp's unmasked k-steps of the L tile in each stage
   auto issue = [&](int q, int stage) {
     cd* s = sm + stage * TRAIL_STAGE;
-    load_tile_sw(s, Lt + static_cast<size_t>(con[2 * q]) * TT);
+    const int la = con[2 * q];
+    const unsigned k8 = (lmask[la] >> f.r0) & 0xffu;
+    if (stage)
+      km1 = k8;
+    else
+      km0 = k8;
+    load_tile_sw(s, Lt + static_cast<size_t>(la) * TT);
     load_x32(s + TT, Ut + static_cast<size_t>(con[2 * q + 1]) * TT, TILE, 0);
     cp_async_commit();
   };
@@ -263,7 +287,7 @@ __global__ void __launch_bounds__(ST, ZOLO_TRAIL_MINB) trailing_level_kernel(con
       cp_async_wait<0>();
     }
     __syncthreads();
-    mma_tile3_nx(acc, sm + stage * TRAIL_STAGE, sm + stage * TRAIL_STAGE + TT, f);
+    mma_tile3_nx(acc, sm + stage * TRAIL_STAGE, sm + stage * TRAIL_STAGE + TT, f, stage ? km1 : km0);
     __syncthreads();  // the stage is refilled two iterations later
   }
   cd prod[4];
@@ -338,14 +362,14 @@ void sp_factor(cudaStream_t st, const SpGeom& s, const SpFactor& f, int64_t nnz,
   for (size_t l = 0; l + 1 < lv.size(); ++l) {
     if (tp[l + 1] > tp[l])
       trailing_level_kernel<<<tp[l + 1] - tp[l], ST, TRAIL_SMEM, st>>>(plan.tgt, plan.con, tp[l], f.Dt, f.Lt, f.Ut,
-                                                                        plan.scratch);
+                                                                        plan.scratch, f.lmask);
     if (cp[l + 1] > cp[l])
       combine_parts_kernel<<<cp[l + 1] - cp[l], ST, 0, st>>>(plan.cmb, cp[l], f.Dt, f.Lt, f.Ut, plan.scratch);
     if (lv[l + 1] > lv[l])
       diag_level_kernel<<<lv[l + 1] - lv[l], FT, diag_smem, st>>>(plan.cols, lv[l], s.npad, f.Dt, f.DinvL, f.DinvU,
                                                                    row_norm, ds.fail_index, ds.min_ratio_bits);
     if (pp[l + 1] > pp[l])
-      panel_level_kernel<<<pp[l + 1] - pp[l], ST, 0, st>>>(plan.pan, pp[l], f.Lt, f.Ut, f.DinvL, f.DinvU);
+      panel_level_kernel<<<pp[l + 1] - pp[l], ST, 0, st>>>(plan.pan, pp[l], f.Lt, f.Ut, f.DinvL, f.DinvU, f.lmask);
   }
   if (s.ntiles > 0) scale_sp_kernel<<<dim3(static_cast<unsigned>(s.ntiles), 2), ST, 0, st>>>(s, f.Lt, f.Ut, f.DinvL, f.DinvU);
 }

@@ -264,7 +264,9 @@ __device__ __forceinline__ void mma_tile3(Acc3<NB>& acc, const cd* ts, const cd*
 // acc (3M) += T X for the factorization's trailing updates: T a swizzled tile (load_tile_sw),
 // X a padded 32 x 32 block [col*XPAD + k] (load_x32), op N, all k-steps; outputs as mma_tile2
 // (out[2h + e] at row f.row, column ocol(f, 2h + e)).
-__device__ __forceinline__ void mma_tile3_nx(Acc3<2>& acc, const cd* ts, const cd* xs, const Frag& f) {
+// km: the k-steps holding nonzeros in this warp's 8 rows of T (the others are predicated off)
+__device__ __forceinline__ void mma_tile3_nx(Acc3<2>& acc, const cd* ts, const cd* xs, const Frag& f, unsigned km) {
+  if (km == 0) return;
   __syncwarp();
   const int ar = f.r0 + (f.lane >> 2), am = f.lane & 3;
   const int bc = f.c0 + (f.lane >> 2);
@@ -281,6 +283,7 @@ __device__ __forceinline__ void mma_tile3_nx(Acc3<2>& acc, const cd* ts, const c
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      if (!((km >> (k0 + q)) & 1u)) continue;
       const double s = a[q].x + a[q].y;
       dmma_nv(acc.p[0][0], a[q].x, b0[q].x);
       dmma_nv(acc.p[1][0], a[q].x, b1[q].x);

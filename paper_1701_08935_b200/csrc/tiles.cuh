@@ -99,6 +99,9 @@ struct SpFactor {
   cd* Ut = nullptr;
   cd* DinvL = nullptr;
   cd* DinvU = nullptr;
+  // per L tile, written by its panel step: bit (8 g + kb) set when rows 8g..8g+7 x columns
+  // 4kb..4kb+3 of L(a,k) hold a nonzero -- the trailing updates skip the empty k-steps
+  unsigned* lmask = nullptr;
 };
 
 // device copy of a FactorPlan (host.hpp): level ranges stay on the host
