@@ -281,6 +281,15 @@ int zolo_subspace_iteration(zolo_ctx* ctx, int64_t n, int scalar, const int64_t*
  * more sweep pair. Counters keep the reference's meaning (one solve per
  * shifted system). steps in [0, 2]; 0 (default) = the reference's plain solve. */
 int zolo_set_refinement(zolo_ctx* ctx, int steps);
+/* Relaxed refinement inside zolo_apply_filter (no reference equivalent): with refinement on, a G
+ * application skips the correction once the GMRES residuals rho of the iteration before satisfy
+ * 10 * rho * (relative residual of the unrefined solves, worst chain, measured once per
+ * factorization) <= gmres_tol -- the later an operator application in a Krylov iteration, the less
+ * exact it must be. out[0] = that measured residual (-1 before the first refined application),
+ * out[1] = G applications of the last zolo_apply_filter that ran unrefined under the rule. */
+int zolo_refinement_stats(const zolo_ctx* ctx, double* out);
+/* on = 0: every G application of a refined zolo_apply_filter is corrected (default: relaxed). */
+int zolo_set_refinement_relaxation(zolo_ctx* ctx, int on);
 
 /* Return the device memory cached by the library's allocator on `device`
  * (blocks of destroyed contexts) to the driver. */

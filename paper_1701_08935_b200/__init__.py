@@ -490,6 +490,19 @@ class FilterOperator:
         """Residual-correction steps per shifted solve from the next application on."""
         _check(self._h, lib().zolo_set_refinement(self._h, int(steps)))
 
+    def set_refinement_relaxation(self, on: bool):
+        """Relaxed refinement (the default): a refined apply_filter skips the correction of the G
+        applications whose GMRES residuals are already small -- zolo_set_refinement_relaxation."""
+        _check(self._h, lib().zolo_set_refinement_relaxation(self._h, int(bool(on))))
+
+    def refinement_stats(self):
+        """(relative residual of the unrefined solves measured at the first refined application or
+        -1, G applications of the last apply_filter that skipped the correction) --
+        zolo_refinement_stats."""
+        out = np.zeros(2)
+        lib().zolo_refinement_stats(self._h, _ptr(out))
+        return float(out[0]), int(out[1])
+
     def last_timings(self):
         ms = np.zeros(8)
         lib().zolo_last_timings(self._h, _ptr(ms))

@@ -320,6 +320,14 @@ struct zolo_ctx {
   // residual-correction refinement of the shifted solves (zolo_set_refinement): per chain the
   // residual / correction block, the in-place sweep chains over it and the chain's shift
   int refine = 0;
+  // relaxed refinement inside apply_filter (inexact Krylov): the measured relative residual of the
+  // unrefined solves (worst chain), and whether the G application being enqueued may skip the
+  // correction because the GMRES residuals are already small enough
+  double unrefined_res = -1.0;
+  bool refine_skip = false;
+  bool refine_relax = true;  // zolo_set_refinement_relaxation
+  int refine_skipped = 0;  // G applications of the last apply_filter that ran unrefined under that rule
+  DevMem norm_buf;
   std::vector<std::unique_ptr<DevMem>> rbuf;
   DevMem chains_fwd_ref, chains_bwd_ref, chain_sigma;
   DevMem tmaps_fwd, tmaps_bwd, tmaps_fwd_ref, tmaps_bwd_ref;  // the chains' x-block tensor maps
@@ -1028,6 +1036,7 @@ void do_factorize_sparse(zolo_ctx& c, const int64_t* perm_in, zolo_factor_stats*
   }
   c.factored = fail_any < 0;
   c.ncap = 0;
+  c.unrefined_res = -1.0;  // measured again with the new factors
   if (fail_any >= 0)
     throw ZoloError(ZOLO_ERR_FACTORIZATION, "factorize: pivot " + std::to_string(fail_any) + " below threshold");
 }
@@ -1266,6 +1275,24 @@ void refine_solves(zolo_ctx& c, int na, int first = 0, int nsub = -1) {
                                        c.b_identity ? nullptr : c.brp_d.as<int>(), c.bci_d.as<int>(),
                                        c.bv_d.as<double>(), c.bbuf.as<cd>(), xs.data(), rs.data(),
                                        c.chain_sigma.as<cd>() + first, nch, na);
+    if (step == 0 && c.in_filter && c.unrefined_res < 0.0 && first == 0 && na > 0) {
+      // ||b - K x||_F / ||b||_F of the unrefined solves, worst chain (once per factorization)
+      c.norm_buf.ensure(sizeof(double) * static_cast<size_t>(nch + 1) * na);
+      double* nb = c.norm_buf.as<double>();
+      for (int ch = 0; ch < nch; ++ch) Krylov<cd>::col_norms(c.st, rs[ch], ld, ld, na, nb + static_cast<size_t>(ch) * na);
+      Krylov<cd>::col_norms(c.st, c.bbuf.as<cd>(), ld, ld, na, nb + static_cast<size_t>(nch) * na);
+      std::vector<double> h(static_cast<size_t>(nch + 1) * na);
+      CK(cudaMemcpyAsync(h.data(), nb, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.st));
+      CK(cudaStreamSynchronize(c.st));
+      double b2 = 0.0, worst = 0.0;
+      for (int a = 0; a < na; ++a) b2 += h[static_cast<size_t>(nch) * na + a] * h[static_cast<size_t>(nch) * na + a];
+      for (int ch = 0; ch < nch; ++ch) {
+        double r2 = 0.0;
+        for (int a = 0; a < na; ++a) r2 += h[static_cast<size_t>(ch) * na + a] * h[static_cast<size_t>(ch) * na + a];
+        worst = std::max(worst, r2);
+      }
+      c.unrefined_res = b2 > 0.0 && std::isfinite(worst) ? std::sqrt(worst / b2) : 1.0;
+    }
     sweep_sparse(c, first, nch, na, nullptr, true);
     add_corrections(c.st, ld, xs.data(), rs.data(), nch, na);
   }
@@ -1335,7 +1362,7 @@ float apply_g_device(zolo_ctx& c, const void* vsrc, int na, void* wdst) {
     dtr = c.trace_buf.as<unsigned long long>();
   }
   sweep_sparse(c, 0, nch, na, dtr);
-  if (c.refine) refine_solves(c, na);
+  if (c.refine && !c.refine_skip) refine_solves(c, na);
   if (dtr) {
     std::vector<unsigned long long> h(6 * ntask);
     CK(cudaMemcpyAsync(h.data(), dtr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, c.st));
@@ -1678,7 +1705,9 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
   // host round trips and a short host stall is absorbed by the queued iterations. The hybrid
   // solve keeps the synchronous loop (its inner GMRES must not see finished columns).
   static const int lag_env = std::min(std::max(env_int("ZOLO_GMRES_LAG", 2), 0), 3);
-  const int lag = c.hybrid ? 0 : lag_env;
+  // refined solves: synchronous control, so that every G application can be judged on the
+  // residuals of the iteration before (a host round trip is nothing beside a refined application)
+  const int lag = (c.hybrid || c.refine) ? 0 : lag_env;
   const int nslot = lag + 1;
   struct LagGuard {
     zolo_ctx& c;
@@ -1686,6 +1715,7 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       c.lag_done = nullptr;
       c.ev2_use = c.ev3_use = nullptr;
       c.in_filter = false;
+      c.refine_skip = false;
     }
   } lag_guard{c};
   c.in_filter = true;
@@ -1714,6 +1744,11 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       if (!dn[col]) next.push_back(col);
     active.swap(next);
   };
+  std::vector<double> res_h;
+  const int q2 = 2 * c.r;
+  int nskipped = 0;  // G applications that ran unrefined under the relaxed-refinement rule
+  c.refine_skip = false;
+  c.refine_skipped = 0;
   int pend[4], npend = 0;  // slots enqueued whose flags are not yet read, oldest first
   for (int it = 0; it < maxit && !active.empty(); ++it) {
     its = it + 1;
@@ -1761,8 +1796,25 @@ int apply_filter_impl(zolo_ctx& c, const void* d_v, void* d_y, int64_t ncols, do
       if (!lag) check_spin();
       collect(q);
       filter_active(c.done_hq[q]);
+      if (c.refine && !active.empty()) {
+        // Relaxed refinement (inexact Krylov: the later a G application, the less exact it must
+        // be): with relative GMRES residuals rho after this iteration, an unrefined application
+        // perturbs the solutions by ~rho x (residual of the unrefined solves) -- skip the
+        // correction once that is a tenth of the GMRES tolerance.
+        res_h.resize(static_cast<size_t>(ncols) * q2);
+        CK(cudaMemcpyAsync(res_h.data(), g.res, sizeof(double) * res_h.size(), cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+        double rho = 0.0;
+        for (int col : active)
+          for (int k = 0; k < q2; ++k) rho = std::max(rho, res_h[static_cast<size_t>(col) * q2 + k]);
+        c.refine_skip = c.refine_relax && c.unrefined_res >= 0.0 && std::isfinite(rho) &&
+                        10.0 * rho * c.unrefined_res <= tol;
+        nskipped += c.refine_skip ? 1 : 0;
+        c.refine_skipped = nskipped;
+      }
     }
   }
+  c.refine_skip = false;
   for (int k = 0; k < npend; ++k) {
     CK(cudaEventSynchronize(ev_done[pend[k]]));
     collect(pend[k]);
@@ -2235,11 +2287,25 @@ int zolo_set_solve_mode(zolo_ctx* c, int mode, int pole, double inner_tol, int i
   });
 }
 
+int zolo_set_refinement_relaxation(zolo_ctx* c, int on) {
+  if (!c) return ZOLO_ERR_DOMAIN;
+  c->refine_relax = on != 0;
+  return ZOLO_OK;
+}
+
+int zolo_refinement_stats(const zolo_ctx* c, double* out) {
+  if (!c || !out) return ZOLO_ERR_DOMAIN;
+  out[0] = c->unrefined_res;
+  out[1] = static_cast<double>(c->refine_skipped);
+  return ZOLO_OK;
+}
+
 int zolo_set_refinement(zolo_ctx* c, int steps) {
   return guarded(c, [&] {
     require(steps >= 0 && steps <= 2, "zolo_set_refinement: steps must be in [0, 2]");
     require(steps == 0 || !c->hybrid, "zolo_set_refinement: not available with the hybrid solve");
     if (steps != c->refine) {
+      c->unrefined_res = -1.0;
       c->refine = steps;
       c->ncap = 0;  // the workspace (residual blocks, refinement chains) is rebuilt
     }

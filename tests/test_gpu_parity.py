@@ -292,6 +292,34 @@ def test_lagged_gmres_control_matches_synchronous_loop(zb, case):
     assert (a["counters"] == b["counters"]).all()
 
 
+def test_relaxed_refinement_matches_full_refinement(zb):
+    """Refined filter applications skip the correction of the G applications whose GMRES residuals
+    are already small (inexact-Krylov relaxation, zolo_refinement_stats): on config 3's generator
+    at 12^3, r = 8, applied to a block of near-eigenvectors (the second subspace iteration's
+    situation) the relaxed filter must agree with the fully refined one to 1e-11 with the same
+    Krylov dimensions, and must have skipped at least one correction."""
+    from paper_1701_08935_b200 import configs
+    from paper_1701_08935_b200.design import build_filter_design
+
+    pen = configs.tight_binding_pencil(12, seed=3, disorder=1.5)
+    gaps = configs.window_by_dense_eigs(pen, lo=852, count=24)
+    op = zb.FilterOperator(pen, build_filter_design(gaps, 8), 8, is_complex=True, nd_leaf=64)
+    v = zb.random_block(pen[0], 40, 1, cx=True, orthonormalize=True)
+    y1, _ = op.apply_filter(v)  # one plain filter application: the block is now close to the invariant subspace
+    q, _ = np.linalg.qr(y1)
+    op.set_refinement(1)
+    op.set_refinement_relaxation(False)
+    yf, repf = op.apply_filter(q)
+    assert op.refinement_stats()[1] == 0
+    op.set_refinement_relaxation(True)
+    yr, repr_ = op.apply_filter(q)
+    res_unrefined, skipped = op.refinement_stats()
+    assert 0.0 < res_unrefined < 1e-6
+    assert skipped >= 1, "no G application was relaxed"
+    assert np.linalg.norm(yr - yf) <= 1e-11 * np.linalg.norm(yf)
+    assert list(repr_.column_iterations) == list(repf.column_iterations)
+
+
 @pytest.mark.parametrize("case", ["filter_cfg2_k6", "filter_cfg3_k5", "filter_cfg1_k16"])
 def test_sweep_task_width_is_bitwise_transparent(zb, case):
     """The sweeps' task width (32- or 64-column tasks, ZOLO_SWEEP_COLS; auto picks 64 for blocks of
