@@ -160,9 +160,11 @@ void uniform_stream(uint64_t seed, int64_t n, double* out) {
 // Gaussian by the same expression as the serial form (bit-identical output).
 namespace {
 void gaussian_fill(std::mt19937_64& rng, int64_t count, double* out) {
-  constexpr int64_t BLK = int64_t{1} << 20;
+  // ~16 blocks per call, between 64 Ki and 1 Mi Gaussians each (a block's raw draws overlap the
+  // transform of the block before)
+  const int64_t BLK = std::min<int64_t>(int64_t{1} << 20, std::max<int64_t>(int64_t{1} << 16, count / 16));
   const int nt = static_cast<int>(std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())));
-  if (count < 4 * BLK || nt < 2) {
+  if (count < (int64_t{1} << 18) || nt < 2) {
     for (int64_t i = 0; i < count; ++i) out[i] = gaussian(rng);
     return;
   }

@@ -157,7 +157,7 @@ def test_random_block_is_bit_identical_to_reference():
 
 
 def test_large_random_block_threaded_transform_is_bit_identical_to_reference():
-    """Blocks of >= 4 Mi Gaussians take host.cpp's threaded Box-Muller path (raw mt19937_64 stream
+    """Blocks of >= 256 Ki Gaussians take host.cpp's threaded Box-Muller path (raw mt19937_64 stream
     sequential, transform on several threads): same bits as the reference's serial
     random_gaussian (dense.hpp:193-208), digests in tests/golden/rng_block_large.npz."""
     import sys
@@ -170,6 +170,8 @@ def test_large_random_block_threaded_transform_is_bit_identical_to_reference():
     g = load_golden("rng_block_large")
     assert array_digest(zb.random_block(1 << 20, 5, 7, cx=False)) == g["real"]
     assert array_digest(zb.random_block((1 << 19) + 3, 5, 9, cx=True)) == g["cplx"]
+    assert array_digest(zb.random_block(32768, 96, 1, cx=False)) == g["mid"]
+    assert array_digest(zb.random_block(40000, 9, 5, cx=True)) == g["mid_cplx"]
 
 
 @pytest.mark.parametrize("name,near,chunk,order", [("grid2d", 4, 16, 3), ("grid3d", 4, 16, 3), ("grid3d", 2, 8, 1),
