@@ -453,10 +453,37 @@ void require(bool ok, const std::string& msg) {
   if (!ok) throw ZoloError(ZOLO_ERR_DOMAIN, msg);
 }
 
+// fn(lo, hi) over [0, n) in contiguous ranges on the host cores (setup loops over the pencil's
+// rows: each range writes its own output rows, so the result does not depend on the threading);
+// the first exception of a range is rethrown on the caller
+template <class F>
+void par_rows(int64_t n, F&& fn) {
+  const int nt = static_cast<int>(std::min<int64_t>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())),
+                                                    std::max<int64_t>(1, n / 2048)));
+  if (nt < 2) {
+    fn(int64_t{0}, n);
+    return;
+  }
+  std::vector<std::exception_ptr> err(nt);
+  std::vector<std::thread> pool;
+  for (int q = 0; q < nt; ++q)
+    pool.emplace_back([&, q] {
+      try {
+        fn(n * q / nt, n * (q + 1) / nt);
+      } catch (...) {
+        err[q] = std::current_exception();
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
 // Union pattern of A and B (B = I when absent): assemble_shifted (sparse.hpp:153-186).
 struct Union {
-  std::vector<int64_t> rp, ci;
-  std::vector<double> av, bv;  // interleaved when complex
+  std::vector<int64_t> rp;
+  std::vector<int64_t, NoInit<int64_t>> ci;
+  std::vector<double, NoInit<double>> av, bv;  // interleaved when complex
 };
 
 Union union_pattern(const zolo_ctx& c) {
@@ -464,27 +491,44 @@ Union union_pattern(const zolo_ctx& c) {
   const int64_t n = c.n;
   const int w = c.cx ? 2 : 1;
   u.rp.assign(n + 1, 0);
-  const size_t cap = c.a_ci.size() + (c.b_identity ? n : c.b_ci.size());
-  u.ci.reserve(cap);
-  u.av.reserve(cap * w);
-  u.bv.reserve(cap * w);
-  for (int64_t i = 0; i < n; ++i) {
+  // the rows' merges are independent: count, prefix sum, fill (all host cores)
+  auto merge_row = [&](int64_t i, auto&& emit) {
     int64_t ka = c.a_rp[i], kb = c.b_identity ? 0 : c.b_rp[i];
     const int64_t ea = c.a_rp[i + 1], eb = c.b_identity ? 1 : c.b_rp[i + 1];
     while (ka < ea || kb < eb) {
       const int64_t ja = ka < ea ? c.a_ci[ka] : n;
       const int64_t jb = kb < eb ? (c.b_identity ? i : c.b_ci[kb]) : n;
       const int64_t j = std::min(ja, jb);
-      u.ci.push_back(j);
-      for (int q = 0; q < w; ++q) {
-        u.av.push_back(ja == j ? c.a_v[ka * w + q] : 0.0);
-        u.bv.push_back(jb == j ? (c.b_identity ? (q == 0 ? 1.0 : 0.0) : c.b_v[kb * w + q]) : 0.0);
-      }
+      emit(j, ja == j ? ka : int64_t{-1}, jb == j ? kb : int64_t{-1});
       if (ja == j) ++ka;
       if (jb == j) ++kb;
     }
-    u.rp[i + 1] = static_cast<int64_t>(u.ci.size());
-  }
+  };
+  par_rows(n, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      int64_t cnt = 0;
+      merge_row(i, [&](int64_t, int64_t, int64_t) { ++cnt; });
+      u.rp[i + 1] = cnt;
+    }
+  });
+  for (int64_t i = 0; i < n; ++i) u.rp[i + 1] += u.rp[i];
+  const size_t nnz = static_cast<size_t>(u.rp[n]);
+  u.ci.resize(nnz);
+  u.av.resize(nnz * w);
+  u.bv.resize(nnz * w);
+  par_rows(n, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      int64_t at = u.rp[i];
+      merge_row(i, [&](int64_t j, int64_t ka, int64_t kb) {
+        u.ci[at] = j;
+        for (int q = 0; q < w; ++q) {
+          u.av[at * w + q] = ka >= 0 ? c.a_v[ka * w + q] : 0.0;
+          u.bv[at * w + q] = kb >= 0 ? (c.b_identity ? (q == 0 ? 1.0 : 0.0) : c.b_v[kb * w + q]) : 0.0;
+        }
+        ++at;
+      });
+    }
+  });
   return u;
 }
 
@@ -492,24 +536,31 @@ Union union_pattern(const zolo_ctx& c) {
 // sorted columns. inv: position -> original row or -1; pos: original -> position.
 void permuted_csr(int64_t npad, const std::vector<int64_t>& inv, const std::vector<int>& pos,
                   const std::vector<int64_t>& rp, const std::vector<int64_t>& ci, const std::vector<double>& v, int w,
-                  std::vector<int>& prp, std::vector<int>& pci, std::vector<double>& pv) {
+                  std::vector<int>& prp, std::vector<int, NoInit<int>>& pci,
+                  std::vector<double, NoInit<double>>& pv) {
   prp.assign(npad + 1, 0);
-  pci.clear();
-  pv.clear();
-  std::vector<std::pair<int, int64_t>> row;
   for (int64_t t = 0; t < npad; ++t) {
     const int64_t i = inv[t];
-    if (i >= 0) {
+    prp[t + 1] = prp[t] + (i >= 0 ? static_cast<int>(rp[i + 1] - rp[i]) : 0);
+  }
+  pci.resize(static_cast<size_t>(prp[npad]));
+  pv.resize(static_cast<size_t>(prp[npad]) * w);
+  par_rows(npad, [&](int64_t lo, int64_t hi) {  // every device row sorts and writes its own range
+    std::vector<std::pair<int, int64_t>> row;
+    for (int64_t t = lo; t < hi; ++t) {
+      const int64_t i = inv[t];
+      if (i < 0) continue;
       row.clear();
       for (int64_t k = rp[i]; k < rp[i + 1]; ++k) row.emplace_back(pos[ci[k]], k);
       std::sort(row.begin(), row.end());
+      int64_t at = prp[t];
       for (auto& e : row) {
-        pci.push_back(e.first);
-        for (int q = 0; q < w; ++q) pv.push_back(v[e.second * w + q]);
+        pci[at] = e.first;
+        for (int q = 0; q < w; ++q) pv[at * w + q] = v[e.second * w + q];
+        ++at;
       }
     }
-    prp[t + 1] = static_cast<int>(pci.size());
-  }
+  });
 }
 
 // Device copies of the pencil in the factor ordering + the position map.
@@ -588,8 +639,9 @@ void upload_device_bsr(zolo_ctx& c, const std::vector<int>& pos) {
 void upload_device_pencil(zolo_ctx& c, const std::vector<int64_t>& inv, const std::vector<int>& pos) {
   const int w = c.cx ? 2 : 1;
   const int64_t npad = static_cast<int64_t>(inv.size());
-  std::vector<int> prp, pci, brp, bci;
-  std::vector<double> pv, bv;
+  std::vector<int> prp, brp;
+  std::vector<int, NoInit<int>> pci, bci;
+  std::vector<double, NoInit<double>> pv, bv;
   // B's permuted copy on a host thread beside A's (plain host work; bad_alloc is the only failure)
   std::exception_ptr berr;
   std::thread tb;
@@ -830,12 +882,15 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
   c.sgeom = s;
 
   const int64_t nnz = static_cast<int64_t>(u.ci.size());
-  std::vector<int> er(nnz), ec(nnz), pads;
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t k = u.rp[i]; k < u.rp[i + 1]; ++k) {
-      er[k] = pos[i];
-      ec[k] = pos[u.ci[k]];
-    }
+  std::vector<int, NoInit<int>> er(nnz), ec(nnz);
+  std::vector<int> pads;
+  par_rows(n, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i)
+      for (int64_t k = u.rp[i]; k < u.rp[i + 1]; ++k) {
+        er[k] = pos[i];
+        ec[k] = pos[u.ci[k]];
+      }
+  });
   for (int64_t t = 0; t < bs.npad; ++t)
     if (bs.inv[t] < 0) pads.push_back(static_cast<int>(t));
   upload(c.sp_er, er, c.st);
@@ -2142,15 +2197,37 @@ int zolo_pencil_upload(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, 
     c->n = n;
     c->cx = scalar;
     const int w = scalar ? 2 : 1;
-    c->a_rp.assign(a_rp, a_rp + n + 1);
-    c->a_ci.assign(a_ci, a_ci + a_rp[n]);
-    c->a_v.assign(a_v, a_v + a_rp[n] * w);
     c->b_identity = b_rp == nullptr;
-    if (!c->b_identity) {
-      c->b_rp.assign(b_rp, b_rp + n + 1);
-      c->b_ci.assign(b_ci, b_ci + b_rp[n]);
-      c->b_v.assign(b_v, b_v + b_rp[n] * w);
-    } else {
+    {  // the host copies of the pencil's arrays, side by side (dense-block pencils: hundreds of MB)
+      std::exception_ptr cerr[4];
+      std::vector<std::thread> cp;
+      auto copy_on_thread = [&](int slot, auto&& fn) {
+        cp.emplace_back([&cerr, slot, fn] {
+          try {
+            fn();
+          } catch (...) {
+            cerr[slot] = std::current_exception();
+          }
+        });
+      };
+      copy_on_thread(0, [&] { c->a_ci.assign(a_ci, a_ci + a_rp[n]); });
+      copy_on_thread(1, [&] { c->a_v.assign(a_v, a_v + a_rp[n] * w); });
+      if (!c->b_identity) {
+        copy_on_thread(2, [&] { c->b_ci.assign(b_ci, b_ci + b_rp[n]); });
+        copy_on_thread(3, [&] { c->b_v.assign(b_v, b_v + b_rp[n] * w); });
+      }
+      try {
+        c->a_rp.assign(a_rp, a_rp + n + 1);
+        if (!c->b_identity) c->b_rp.assign(b_rp, b_rp + n + 1);
+      } catch (...) {
+        for (auto& t : cp) t.join();
+        throw;
+      }
+      for (auto& t : cp) t.join();
+      for (auto& e : cerr)
+        if (e) std::rethrow_exception(e);
+    }
+    if (c->b_identity) {
       c->b_rp.clear();
       c->b_ci.clear();
       c->b_v.clear();
@@ -2162,13 +2239,15 @@ int zolo_pencil_upload(zolo_ctx* c, int64_t n, int scalar, const int64_t* a_rp, 
         ok = ok && ci[k] >= 0 && ci[k] < n && (k == rp[i] || ci[k] > ci[k - 1]);
       return ok;
     };
-    for (int64_t i = 0; i < n; ++i) {
-      if (c->a_rp[i] > c->a_rp[i + 1]) require(false, "zolo_pencil_upload: A offsets not monotone");
-      if (!sorted_in_range(c->a_rp, c->a_ci, i))
-        require(false, "zolo_pencil_upload: A column indices must be in range and sorted");
-      if (!c->b_identity && !sorted_in_range(c->b_rp, c->b_ci, i))
-        require(false, "zolo_pencil_upload: B column indices must be in range and sorted");
-    }
+    par_rows(n, [&](int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i) {
+        if (c->a_rp[i] > c->a_rp[i + 1]) require(false, "zolo_pencil_upload: A offsets not monotone");
+        if (!sorted_in_range(c->a_rp, c->a_ci, i))
+          require(false, "zolo_pencil_upload: A column indices must be in range and sorted");
+        if (!c->b_identity && !sorted_in_range(c->b_rp, c->b_ci, i))
+          require(false, "zolo_pencil_upload: B column indices must be in range and sorted");
+      }
+    });
     c->have_pencil = true;
     c->have_perm = false;
     c->sym_ready = false;
