@@ -457,9 +457,9 @@ void require(bool ok, const std::string& msg) {
 // rows: each range writes its own output rows, so the result does not depend on the threading);
 // the first exception of a range is rethrown on the caller
 template <class F>
-void par_rows(int64_t n, F&& fn) {
+void par_rows(int64_t n, F&& fn, int64_t grain = 2048) {  // grain: rows worth a thread of their own
   const int nt = static_cast<int>(std::min<int64_t>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())),
-                                                    std::max<int64_t>(1, n / 2048)));
+                                                    std::max<int64_t>(1, n / grain)));
   if (nt < 2) {
     fn(int64_t{0}, n);
     return;
@@ -757,17 +757,24 @@ void sparse_symbolic(zolo_ctx& c, const int64_t* perm_in) {
     // atoms of bsr rows (BSR pencils): dissect the block graph, then expand every atom into its
     // rows in order, so atoms stay contiguous in the device ordering (BSR SpMMs)
     const int64_t b = c.bsr, na = n / b;
-    std::vector<int64_t> brp(na + 1, 0), bci, mark(na, -1);
-    for (int64_t I = 0; I < na; ++I) {
-      for (int64_t i = I * b; i < (I + 1) * b; ++i)
-        for (int64_t q = u.rp[i]; q < u.rp[i + 1]; ++q) {
-          const int64_t J = u.ci[q] / b;
-          if (mark[J] != I) {
-            mark[J] = I;
-            bci.push_back(J);
+    std::vector<int64_t> brp(na + 1, 0), bci;
+    std::vector<std::vector<int64_t>> nbr(na);
+    par_rows(na, [&](int64_t lo, int64_t hi) {  // atoms are independent: each range its own marks
+      std::vector<int64_t> mark(na, -1);
+      for (int64_t I = lo; I < hi; ++I) {
+        for (int64_t i = I * b; i < (I + 1) * b; ++i)
+          for (int64_t q = u.rp[i]; q < u.rp[i + 1]; ++q) {
+            const int64_t J = u.ci[q] / b;
+            if (mark[J] != I) {
+              mark[J] = I;
+              nbr[I].push_back(J);
+            }
           }
-        }
-      std::sort(bci.begin() + brp[I], bci.end());
+        std::sort(nbr[I].begin(), nbr[I].end());
+      }
+    }, 16);
+    for (int64_t I = 0; I < na; ++I) {
+      bci.insert(bci.end(), nbr[I].begin(), nbr[I].end());
       brp[I + 1] = static_cast<int64_t>(bci.size());
     }
     std::vector<std::vector<int64_t>> anodes;

@@ -339,17 +339,36 @@ void block_symbolic(int64_t n, const int64_t* rp, const int64_t* ci, const std::
   const int64_t nb = bs.npad / tile;
   bs.nb = nb;
   // block graph (upper part: neighbours with a larger block index)
+  // (block rows are independent: host threads over ranges of blocks, each with its own stamp array,
+  // so a dense-block pencil's millions of entries collapse to the few distinct neighbours at once)
   std::vector<std::vector<int64_t>> up(nb);
-  for (int64_t v = 0; v < n; ++v) {
-    const int64_t bv = bs.pos[v] / tile;
-    for (int64_t k = rp[v]; k < rp[v + 1]; ++k) {
-      const int64_t bw = bs.pos[ci[k]] / tile;
-      if (bw > bv) up[bv].push_back(bw);
+  {
+    const int nt = static_cast<int>(std::min<int64_t>(std::min(16u, std::max(1u, std::thread::hardware_concurrency())),
+                                                      std::max<int64_t>(1, nb / 64)));
+    auto blocks = [&](int64_t lo, int64_t hi) {
+      std::vector<int64_t> stamp(nb, -1);
+      for (int64_t bv = lo; bv < hi; ++bv) {
+        for (int t = 0; t < tile; ++t) {
+          const int64_t v = bs.inv[bv * tile + t];
+          if (v < 0) continue;
+          for (int64_t k = rp[v]; k < rp[v + 1]; ++k) {
+            const int64_t bw = bs.pos[ci[k]] / tile;
+            if (bw > bv && stamp[bw] != bv) {
+              stamp[bw] = bv;
+              up[bv].push_back(bw);
+            }
+          }
+        }
+        std::sort(up[bv].begin(), up[bv].end());
+      }
+    };
+    if (nt < 2) {
+      blocks(0, nb);
+    } else {
+      std::vector<std::thread> pool;
+      for (int q = 0; q < nt; ++q) pool.emplace_back(blocks, nb * q / nt, nb * (q + 1) / nt);
+      for (auto& th : pool) th.join();
     }
-  }
-  for (auto& u : up) {
-    std::sort(u.begin(), u.end());
-    u.erase(std::unique(u.begin(), u.end()), u.end());
   }
   // symbolic elimination through the elimination tree
   std::vector<int64_t> parent(nb, -1);
