@@ -249,7 +249,9 @@ __global__ void __launch_bounds__(ST) panel_level_kernel(const int* pan, int p0,
 // registers across the list. Two 34 KiB stages: the next contribution's tiles stream in (plain
 // cp.async; with the L2::cache_hint operand this loop raised "illegal instruction" on the B200)
 // while the current product runs; 3 targets resident per SM. (Three stages with one barrier per
-// product and 2 targets per SM: 459 ms against 426 for config 3's 8 poles.)
+// product and 2 targets per SM: 459 ms against 426 for config 3's 8 poles; occupancy masks of the
+// U tiles' 8-column groups on top of the L tiles' row masks: 489 ms, the per-block predicates
+// spill at 3 targets per SM.)
 constexpr int TRAIL_STAGE = TT + XS2;
 constexpr int TRAIL_SMEM = 2 * TRAIL_STAGE * static_cast<int>(sizeof(cd));
 #ifndef ZOLO_TRAIL_MINB
