@@ -253,7 +253,16 @@ void h2d_setup(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   for (size_t off = 0, q = 0; off < bytes; off += CH, q ^= 1) {
     const size_t len = std::min(CH, bytes - off);
     CK(cudaEventSynchronize(done[q]));  // the DMA out of this buffer has finished
-    std::memcpy(pin[q], static_cast<const char*>(src) + off, len);
+    {  // the staging copy on four host threads (one thread fills a pinned buffer at ~8 GB/s)
+      constexpr int NT = 4;
+      const char* from = static_cast<const char*>(src) + off;
+      char* to = pin[q];
+      std::thread part[NT - 1];
+      for (int t = 1; t < NT; ++t)
+        part[t - 1] = std::thread([=] { std::memcpy(to + len * t / NT, from + len * t / NT, len * (t + 1) / NT - len * t / NT); });
+      std::memcpy(to, from, len / NT);
+      for (auto& th : part) th.join();
+    }
     CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin[q], len, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(done[q], st));
   }
